@@ -1,0 +1,127 @@
+"""Generate the committed golden fixtures from the REFERENCE itself.
+
+Runs oracle/_ref/ref_harness (the unmodified hegraph headers compiled by
+oracle/Makefile) and records SHA-256 digests (plus metadata) of every array it
+dumps.  Run here, where /root/reference exists:
+
+    python tests/golden/make_golden.py prims      # primitive goldens (seconds)
+    python tests/golden/make_golden.py nets       # network goldens (minutes)
+
+The outputs (tests/golden/*.json) are small and committed; the GPU box never
+needs the reference.
+"""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import subprocess
+import sys
+import tempfile
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+HARNESS = os.path.join(ROOT, "oracle", "_ref", "ref_harness")
+
+PRIM_CASES = {
+    # name: (n, scale_bits, bits, key_seed)
+    "n1024_30x3": (1024, 30, [30, 30, 30], 7),
+    "n1024_36_26x2_36": (1024, 26, [36, 26, 26, 36], 11),
+    "n2048_50_30_50": (2048, 30, [50, 30, 50], 13),
+    "n8192_40_30_40": (8192, 30, [40, 30, 40], 5),
+}
+
+
+def load_dump(d: str) -> dict:
+    with open(os.path.join(d, "index.json")) as f:
+        idx = json.load(f)
+    blob = np.fromfile(os.path.join(d, "blob.bin"), dtype=np.uint8)
+    out = {}
+    for k, v in idx.items():
+        if isinstance(v, dict) and "offset" in v and "dtype" in v:
+            dt = np.uint64 if v["dtype"] == "u64" else np.float64
+            raw = blob[v["offset"]: v["offset"] + 8 * v["count"]]
+            out[k] = raw.view(dt).copy()
+        else:
+            out[k] = v
+    return out
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def make_prims():
+    for name, (n, sb, bits, key_seed) in PRIM_CASES.items():
+        with tempfile.TemporaryDirectory() as d:
+            subprocess.check_call([HARNESS, "prims", d, str(n), str(sb), ",".join(map(str, bits)), str(key_seed)])
+            dump = load_dump(d)
+        g = {"n": n, "scale_bits": sb, "bits": bits, "key_seed": key_seed, "arrays": {}, "meta": {}}
+        for k, v in dump.items():
+            if isinstance(v, np.ndarray):
+                g["arrays"][k] = {"sha256": sha(v), "count": int(v.size),
+                                  "dtype": "u64" if v.dtype == np.uint64 else "f64"}
+                if v.size <= 64:
+                    g["arrays"][k]["values"] = [int(x) for x in v] if v.dtype == np.uint64 else [float(x) for x in v]
+            else:
+                g["meta"][k] = v
+        # a few leading words of the big arrays help debugging without bloating the repo
+        for k in ("ct1", "mul_relin_rescale", "weighted_sum", "ntt_fwd_0"):
+            g["arrays"][k]["head"] = [int(x) for x in dump[k][:8]]
+        for k in ("dec_ct1", "dec_mul_relin_rescale"):
+            g["arrays"][k]["head"] = [float(x) for x in dump[k][:16]]
+        with open(os.path.join(HERE, f"prims_{name}.json"), "w") as f:
+            json.dump(g, f, indent=1)
+        print("wrote", name)
+
+
+def make_nets(which=None):
+    from paper_1810_10121_b200 import graphs  # product-side builders (pure Python, no GPU)
+
+    for name, spec in graphs.GOLDEN_NETS.items():
+        if which and name not in which:
+            continue
+        g, x, ctxp = graphs.build(spec)
+        with tempfile.TemporaryDirectory() as d:
+            gp = os.path.join(d, "graph.json")
+            xp = os.path.join(d, "x.f64")
+            with open(gp, "w") as f:
+                json.dump(g, f)
+            x.astype(np.float64).tofile(xp)
+            pre = os.path.join(d, "out")
+            subprocess.check_call([HARNESS, "net", gp, xp, str(spec["batch"]), str(ctxp["n"]), str(ctxp["scale_bits"]),
+                                   ",".join(map(str, ctxp["bits"])), str(ctxp["security"]), str(spec["key_seed"]),
+                                   str(spec["exec_seed"]), str(spec.get("threads", os.cpu_count())), pre])
+            with open(pre + ".json") as f:
+                res = json.load(f)
+            cts = np.fromfile(pre + ".ct.bin", dtype=np.uint64)
+            outs = {}
+            off = 0
+            for o in res["outputs"]:
+                vals = np.fromfile(pre + "." + o["id"] + ".f64", dtype=np.float64)
+                digs = []
+                for e in o["elements"]:
+                    words = e["size"] * (e["level"] + 1) * ctxp["n"]
+                    digs.append(sha(cts[off: off + words]))
+                    off += words
+                outs[o["id"]] = {"shape": o["shape"], "elements": o["elements"], "ct_sha256": digs,
+                                 "values_sha256": sha(vals), "values_head": [float(v) for v in vals[:64]],
+                                 "values_absmax": float(np.abs(vals).max())}
+                np.save(os.path.join(HERE, f"net_{name}_{o['id']}_values.npy"), vals[: min(vals.size, 64 * 16)])
+            golden = {"spec": spec, "ctx": ctxp, "profile": res["profile"], "outputs": outs,
+                      "ref_execute_ms": res["execute_ms"], "threads": res["threads"]}
+            with open(os.path.join(HERE, f"net_{name}.json"), "w") as f:
+                json.dump(golden, f, indent=1)
+            print("wrote net", name, "execute_ms", res["execute_ms"])
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "prims"
+    if what == "prims":
+        make_prims()
+    elif what == "nets":
+        make_nets(sys.argv[2:] or None)
