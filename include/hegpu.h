@@ -1,0 +1,139 @@
+/*
+ * hegpu.h -- C-ABI of the B200-native CKKS/RNS backend (libhegpu.so).
+ *
+ * This is the drop-in boundary for the reference's HE backend hot path
+ * (arxiv/paper_1810_10121 "hegraph"; paths below are relative to
+ * /root/reference/proj/include/heg/).  Host C++ (graph, planning, keys,
+ * encoders) calls sm_100a CUDA through these entry points; no C++ or torch
+ * types cross it: plain pointers, sizes and status codes.
+ *
+ * Conventions
+ *  - Every function returns 0 on success or an HG_E* code (mirrors heg::errc,
+ *    common.hpp:37-46, plus HG_ECUDA) and never throws; hg_last_error()
+ *    returns the message of the last failure on the calling thread.  The
+ *    messages match the reference's heg::Error texts where one exists.
+ *  - Ciphertext buffers are DEVICE pointers to uint64 words laid out
+ *    [item][poly][limb][N] (the reference's RnsPoly residue order,
+ *    poly.hpp:35-41), NTT form unless stated, `nl` = level + 1 limbs.
+ *  - Work is issued on the context's stream (hg_context_stream); functions
+ *    returning host data synchronise that stream.
+ */
+#ifndef HEGPU_H
+#define HEGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HG_OK 0
+#define HG_E_VALIDATION 1 /* errc::validation */
+#define HG_E_PARSE 2      /* errc::parse */
+#define HG_E_DEPTH 3      /* errc::depth_exceeded */
+#define HG_E_CAPACITY 4   /* errc::capacity */
+#define HG_E_IO 5         /* errc::io */
+#define HG_E_INTERNAL 6   /* errc::internal */
+#define HG_E_CUDA 7       /* CUDA runtime failure */
+
+typedef struct hg_context hg_context;
+typedef struct hg_keys hg_keys;
+typedef struct hg_plan hg_plan;
+
+const char* hg_last_error(void);
+const char* hg_version(void);
+
+/* ---- context (replaces heg::make_context / CryptoContext, context.hpp:90-165) ---- */
+int hg_context_create(int64_t poly_degree, const int* coeff_mod_bits, int nbits, int scale_bits, int security,
+                      int device, hg_context** out);
+void hg_context_destroy(hg_context* ctx);
+/* writes up to `cap` primes; returns the prime count via *count */
+int hg_context_primes(const hg_context* ctx, uint64_t* primes, int cap, int* count);
+/* relin digit counts D_i (ckks_backend.hpp:42-46) and total rows */
+int hg_context_relin_rows(const hg_context* ctx, int* rows);
+/* use an external cudaStream_t (e.g. torch's current stream); NULL restores the private one */
+int hg_context_set_stream(hg_context* ctx, void* cuda_stream);
+void* hg_context_stream(const hg_context* ctx);
+int hg_sync(const hg_context* ctx);
+
+/* ---- keys (replaces heg::ckks::generate_keys, ckks_backend.hpp:74-114) ---- */
+int hg_keys_generate(hg_context* ctx, uint64_t seed, int with_relin, hg_keys** out);
+void hg_keys_destroy(hg_keys* keys);
+/* host copies, NTT form, full chain: secret[(L+1)N], pk[2][(L+1)N], relin[rows][2][(L+1)N] (relin may be NULL) */
+int hg_keys_export(const hg_context* ctx, const hg_keys* keys, uint64_t* secret, uint64_t* pk, uint64_t* relin);
+
+/* ---- ring kernels (NttTables::forward/inverse, ring.hpp:263-301) ---- */
+/* in-place on `rows` limb rows; row r is limb (r % nl) at dev + r*N */
+int hg_ntt_forward(hg_context* ctx, uint64_t* dev, int64_t rows, int nl);
+int hg_ntt_inverse(hg_context* ctx, uint64_t* dev, int64_t rows, int nl);
+
+/* ---- ciphertext primitives (CkksBackend, ckks_backend.hpp:253-377) ---- */
+int hg_add(hg_context* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out, int64_t words, int nl);
+int hg_sub(hg_context* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out, int64_t words, int nl);
+int hg_negate(hg_context* ctx, const uint64_t* a, uint64_t* out, int64_t words, int nl);
+/* poly 0 of each item +/- plaintext (pt_per_item: pt has one [nl][N] block per item, else shared) */
+int hg_add_plain(hg_context* ctx, const uint64_t* ct, const uint64_t* pt, uint64_t* out, int64_t items, int size,
+                 int nl, int pt_per_item, int subtract);
+int hg_multiply_plain(hg_context* ctx, const uint64_t* ct, const uint64_t* pt, uint64_t* out, int64_t items, int size,
+                      int nl, int pt_per_item);
+/* rescale `polys` polys from nl to nl-1 limbs (poly_rescale, poly.hpp:190-228) */
+int hg_rescale(hg_context* ctx, const uint64_t* in, uint64_t* out, int64_t polys, int nl);
+int hg_mod_switch(hg_context* ctx, const uint64_t* in, uint64_t* out, int64_t polys, int nl_in, int nl_out);
+/* size-2 x size-2 -> relinearised size-2 (multiply + relinearize, ckks_backend.hpp:261-281, 508-554) */
+int hg_multiply_relin(hg_context* ctx, const hg_keys* keys, const uint64_t* a, const uint64_t* b, uint64_t* out,
+                      int64_t items, int nl);
+/* size-2 x size-2 -> size-3 tensor only */
+int hg_multiply_tensor(hg_context* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out3, int64_t items, int nl);
+int hg_relinearize(hg_context* ctx, const hg_keys* keys, const uint64_t* in3, uint64_t* out2, int64_t items, int nl);
+/* fused multiply+relin+rescale of x by itself (PolyAct x^2 -> multiply_rescale(x, x)) -> nl-1 limbs */
+int hg_square_relin_rescale(hg_context* ctx, const hg_keys* keys, const uint64_t* in, uint64_t* out, int64_t items,
+                            int nl);
+/* Grouped weighted sum + single rescale (weighted_sum, ckks_backend.hpp:381-411; the Dot/Convolution
+ * contraction, runtime.hpp:1027-1221).  x: size-2 items at nl limbs; groups share an input list:
+ *   out[g*mg+m] = rescale( sum_t  W[(g*mg+m)*kt + t][limb] * x[idx[g*kt+t]] )
+ * w: device residues [(groups*mg)*kt][nl]; idx: device int32 [groups*kt]. out has nl-1 limbs. */
+int hg_weighted_sum(hg_context* ctx, const uint64_t* x, const int32_t* idx, const uint64_t* w, uint64_t* out,
+                    int64_t groups, int mg, int kt, int nl);
+
+/* ---- encoding / encryption (ckks_backend.hpp:182-249) ---- */
+/* host values -> device plaintext (NTT form, nl = level+1 limbs); the fp64 FFT runs on the host */
+int hg_encode(hg_context* ctx, const double* values, int64_t count, int level, double scale, uint64_t* pt_dev);
+/* scalar -> per-limb residues of llround(value*scale) (host array of level+1 words) */
+int hg_encode_constant(hg_context* ctx, double value, int level, double scale, uint64_t* residues_host);
+/* items fresh encryptions at `level`, seeds[item] (host), optional plaintexts pt_dev[item][nl][N] */
+int hg_encrypt(hg_context* ctx, const hg_keys* keys, const uint64_t* pt_dev, const uint64_t* seeds, int64_t items,
+               int level, uint64_t* out);
+/* coefficient-domain m = c0 + c1 s (+ ...) -> host [items][nl][N] */
+int hg_decrypt_coeffs(hg_context* ctx, const hg_keys* keys, const uint64_t* ct, int64_t items, int size, int level,
+                      uint64_t* m_host);
+/* decrypt + CRT + decode to `count` slot values per item (host [items][count]) */
+int hg_decrypt(hg_context* ctx, const hg_keys* keys, const uint64_t* ct, int64_t items, int size, int level,
+               double scale, int64_t count, double* values_host);
+
+/* ---- graph execution (heg::execute, runtime.hpp:1970-1974) ---- */
+/* Load a format_version-1 graph (graph_io.hpp) and plan it for `batch` slots. */
+int hg_plan_create(hg_context* ctx, const hg_keys* keys, const char* graph_json, int64_t batch, uint64_t exec_seed,
+                   hg_plan** out);
+void hg_plan_destroy(hg_plan* plan);
+/* encode + encrypt a Parameter's batch (host row-major values, batch * prod(shape[1:]))  */
+int hg_plan_bind_input(hg_plan* plan, const char* param_id, const double* values, int64_t count);
+/* server-side graph run: ciphertexts stay in HBM, no host round trip between nodes */
+int hg_plan_run(hg_plan* plan);
+/* decrypt + decode an output tensor (host row-major batch * elements) */
+int hg_plan_output(hg_plan* plan, const char* output_id, double* values, int64_t capacity, int64_t* count);
+/* raw output ciphertext access: element count, level, scale; NTT-form words copied to host or device */
+int hg_plan_output_info(hg_plan* plan, const char* output_id, int64_t* elements, int* level, double* scale);
+int hg_plan_output_ciphertexts(hg_plan* plan, const char* output_id, uint64_t* dst, int dst_is_device);
+/* replace a Parameter's bound ciphertexts from host/device NTT-form words (client-encrypted inputs) */
+int hg_plan_input_info(hg_plan* plan, const char* param_id, int64_t* elements, int* level);
+int hg_plan_set_input_ciphertexts(hg_plan* plan, const char* param_id, const uint64_t* src, int src_is_device);
+/* ExecProfile (runtime.hpp:140-156) as JSON */
+int hg_plan_profile_json(hg_plan* plan, char* buf, size_t cap);
+/* kernel launches issued by the last hg_plan_run */
+int64_t hg_plan_launches(const hg_plan* plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,304 @@
+// hg_capi.cpp -- extern "C" boundary (include/hegpu.h).  Converts hg::Error
+// into status codes + a thread-local message; never lets an exception cross.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hegpu.h"
+#include "hg_internal.hpp"
+
+struct hg_context {
+  std::unique_ptr<hg::Context> c;
+  cudaStream_t ext = nullptr;
+  cudaStream_t stream() const { return ext ? ext : c->stream(); }
+};
+struct hg_keys {
+  std::unique_ptr<hg::Keys> k;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return HG_OK;
+  } catch (const hg::Error& e) {
+    g_err = e.what();
+    return e.code();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HG_E_INTERNAL;
+  } catch (...) {
+    g_err = "unknown error";
+    return HG_E_INTERNAL;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) hg::fail(HG_E_VALIDATION, std::string(what) + " must not be null");
+}
+
+void level_ok(const hg::Context& c, int level) {
+  hg::check(level >= 0 && level <= c.max_level(), HG_E_VALIDATION, "level outside the modulus chain");
+}
+}  // namespace
+
+// exported for hg_exec.cpp
+namespace hg {
+cudaStream_t ctx_stream(const hg_context* c) { return c->stream(); }
+Context& ctx_ref(hg_context* c) { return *c->c; }
+const Keys& keys_ref(const hg_keys* k) { return *k->k; }
+void set_last_error(const std::string& s) { g_err = s; }
+}  // namespace hg
+
+extern "C" {
+
+const char* hg_last_error(void) { return g_err.c_str(); }
+const char* hg_version(void) { return "hegpu 0.1 (sm_100a)"; }
+
+int hg_context_create(int64_t n, const int* bits, int nbits, int scale_bits, int security, int device,
+                      hg_context** out) {
+  return guard([&] {
+    need(bits, "coeff_mod_bits");
+    need(out, "out");
+    hg::ContextParamsH p;
+    p.n = n;
+    p.bits.assign(bits, bits + nbits);
+    p.scale_bits = scale_bits;
+    p.security = security;
+    auto* h = new hg_context;
+    try {
+      h->c = std::make_unique<hg::Context>(p, device);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void hg_context_destroy(hg_context* ctx) { delete ctx; }
+
+int hg_context_primes(const hg_context* ctx, uint64_t* primes, int cap, int* count) {
+  return guard([&] {
+    need(ctx, "ctx");
+    const auto& q = ctx->c->primes();
+    if (count) *count = static_cast<int>(q.size());
+    for (int i = 0; primes && i < cap && i < static_cast<int>(q.size()); ++i) primes[i] = q[i];
+  });
+}
+
+int hg_context_relin_rows(const hg_context* ctx, int* rows) {
+  return guard([&] {
+    need(ctx, "ctx");
+    *rows = ctx->c->relin_rows();
+  });
+}
+
+int hg_context_set_stream(hg_context* ctx, void* s) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->ext = static_cast<cudaStream_t>(s);
+  });
+}
+void* hg_context_stream(const hg_context* ctx) { return ctx ? ctx->stream() : nullptr; }
+
+int hg_sync(const hg_context* ctx) {
+  return guard([&] { HG_CUDA(cudaStreamSynchronize(ctx->stream())); });
+}
+
+int hg_keys_generate(hg_context* ctx, uint64_t seed, int with_relin, hg_keys** out) {
+  return guard([&] {
+    need(ctx, "ctx");
+    auto* k = new hg_keys;
+    try {
+      k->k = hg::generate_keys(*ctx->c, seed, with_relin != 0);
+    } catch (...) {
+      delete k;
+      throw;
+    }
+    *out = k;
+  });
+}
+void hg_keys_destroy(hg_keys* keys) { delete keys; }
+
+int hg_keys_export(const hg_context* ctx, const hg_keys* keys, uint64_t* secret, uint64_t* pk, uint64_t* relin) {
+  return guard([&] {
+    need(ctx, "ctx");
+    need(keys, "keys");
+    const hg::Keys& K = *keys->k;
+    if (secret) HG_CUDA(cudaMemcpy(secret, K.secret.p, K.secret.bytes, cudaMemcpyDeviceToHost));
+    if (pk) HG_CUDA(cudaMemcpy(pk, K.pk.p, K.pk.bytes, cudaMemcpyDeviceToHost));
+    if (relin && K.has_relin) HG_CUDA(cudaMemcpy(relin, K.relin.p, K.relin.bytes, cudaMemcpyDeviceToHost));
+  });
+}
+
+int hg_ntt_forward(hg_context* ctx, uint64_t* dev, int64_t rows, int nl) {
+  return guard([&] { hg::k::ntt(*ctx->c, dev, rows, nl, false, ctx->stream()); });
+}
+int hg_ntt_inverse(hg_context* ctx, uint64_t* dev, int64_t rows, int nl) {
+  return guard([&] { hg::k::ntt(*ctx->c, dev, rows, nl, true, ctx->stream()); });
+}
+
+int hg_add(hg_context* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out, int64_t words, int nl) {
+  return guard([&] { hg::k::add(*ctx->c, a, b, out, words, nl, ctx->stream()); });
+}
+int hg_sub(hg_context* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out, int64_t words, int nl) {
+  return guard([&] { hg::k::sub(*ctx->c, a, b, out, words, nl, ctx->stream()); });
+}
+int hg_negate(hg_context* ctx, const uint64_t* a, uint64_t* out, int64_t words, int nl) {
+  return guard([&] { hg::k::negate(*ctx->c, a, out, words, nl, ctx->stream()); });
+}
+int hg_add_plain(hg_context* ctx, const uint64_t* ct, const uint64_t* pt, uint64_t* out, int64_t items, int size,
+                 int nl, int per_item, int subtract) {
+  return guard([&] {
+    hg::k::add_plain(*ctx->c, ct, pt, out, items, size, nl, per_item != 0, subtract != 0, ctx->stream());
+  });
+}
+int hg_multiply_plain(hg_context* ctx, const uint64_t* ct, const uint64_t* pt, uint64_t* out, int64_t items, int size,
+                      int nl, int per_item) {
+  return guard([&] {
+    hg::check(nl >= 2, HG_E_DEPTH, "multiplicative depth exceeded: no level left to rescale");
+    hg::k::mul_plain(*ctx->c, ct, pt, out, items, size, nl, per_item != 0, ctx->stream());
+  });
+}
+int hg_rescale(hg_context* ctx, const uint64_t* in, uint64_t* out, int64_t polys, int nl) {
+  return guard([&] {
+    hg::check(nl >= 2, HG_E_DEPTH, "multiplicative depth exceeded: no level left to rescale");
+    auto* sc = static_cast<int64_t*>(ctx->c->scratch(static_cast<size_t>(polys * ctx->c->n() * 8), 1));
+    hg::k::rescale(*ctx->c, in, out, polys, nl, sc, ctx->stream());
+  });
+}
+int hg_mod_switch(hg_context* ctx, const uint64_t* in, uint64_t* out, int64_t polys, int nl_in, int nl_out) {
+  return guard([&] {
+    hg::check(nl_out >= 1 && nl_out <= nl_in, HG_E_VALIDATION, "modulus switch cannot raise the level");
+    hg::k::mod_switch(*ctx->c, in, out, polys, nl_in, nl_out, ctx->stream());
+  });
+}
+int hg_multiply_relin(hg_context* ctx, const hg_keys* keys, const uint64_t* a, const uint64_t* b, uint64_t* out,
+                      int64_t items, int nl) {
+  return guard([&] {
+    hg::check(nl >= 2, HG_E_DEPTH, "multiplicative depth exceeded: no level left to rescale");
+    auto* c2 = static_cast<uint64_t*>(ctx->c->scratch(static_cast<size_t>(items * nl * ctx->c->n() * 8), 2));
+    hg::k::mul_relin(*ctx->c, *keys->k, a, b, out, items, nl, c2, ctx->stream());
+  });
+}
+int hg_multiply_tensor(hg_context* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out3, int64_t items, int nl) {
+  return guard([&] { hg::k::mul_tensor(*ctx->c, a, b, out3, items, nl, ctx->stream()); });
+}
+int hg_relinearize(hg_context* ctx, const hg_keys* keys, const uint64_t* in3, uint64_t* out2, int64_t items, int nl) {
+  return guard([&] {
+    auto* c2 = static_cast<uint64_t*>(ctx->c->scratch(static_cast<size_t>(items * nl * ctx->c->n() * 8), 2));
+    hg::k::relin3(*ctx->c, *keys->k, in3, out2, items, nl, c2, ctx->stream());
+  });
+}
+int hg_square_relin_rescale(hg_context* ctx, const hg_keys* keys, const uint64_t* in, uint64_t* out, int64_t items,
+                            int nl) {
+  return guard([&] {
+    hg::check(nl >= 2, HG_E_DEPTH, "multiplicative depth exceeded: no level left to rescale");
+    hg::Context& c = *ctx->c;
+    const size_t pw = static_cast<size_t>(nl) * c.n();
+    auto* c2 = static_cast<uint64_t*>(c.scratch(items * pw * 8, 2));
+    auto* prod = static_cast<uint64_t*>(c.scratch(items * 2 * pw * 8, 3));
+    auto* sc = static_cast<int64_t*>(c.scratch(static_cast<size_t>(items * 2 * c.n() * 8), 1));
+    hg::k::square_relin(c, *keys->k, in, prod, items, nl, c2, ctx->stream());
+    hg::k::rescale(c, prod, out, items * 2, nl, sc, ctx->stream());
+  });
+}
+int hg_weighted_sum(hg_context* ctx, const uint64_t* x, const int32_t* idx, const uint64_t* w, uint64_t* out,
+                    int64_t groups, int mg, int kt, int nl) {
+  return guard([&] {
+    hg::check(nl >= 2, HG_E_DEPTH, "multiplicative depth exceeded: no level left to rescale");
+    hg::Context& c = *ctx->c;
+    const int64_t items = groups * mg;
+    auto* acc = static_cast<uint64_t*>(c.scratch(static_cast<size_t>(items * 2 * nl * c.n() * 8), 3));
+    auto* sc = static_cast<int64_t*>(c.scratch(static_cast<size_t>(items * 2 * c.n() * 8), 1));
+    hg::k::gemm_groups(c, x, idx, w, acc, groups, mg, kt, nl, ctx->stream());
+    hg::k::rescale(c, acc, out, items * 2, nl, sc, ctx->stream());
+  });
+}
+
+int hg_encode(hg_context* ctx, const double* values, int64_t count, int level, double scale, uint64_t* pt_dev) {
+  return guard([&] {
+    hg::Context& c = *ctx->c;
+    level_ok(c, level);
+    hg::check(scale > 0.0, HG_E_VALIDATION, "encoding scale must be positive");
+    const int64_t n = c.n();
+    std::vector<double> coeffs(n);
+    c.encoder().values_to_coeffs(values, count, coeffs.data());
+    std::vector<int64_t> ci(n);
+    for (int64_t k = 0; k < n; ++k) {  // ckks_backend.hpp:186-193
+      const double scaled = coeffs[k] * scale;
+      hg::check(std::abs(scaled) < 9.0e18, HG_E_VALIDATION, "encoded coefficient overflows the integer range");
+      ci[k] = std::llround(scaled);
+    }
+    auto* d = static_cast<int64_t*>(c.scratch(n * 8, 4));
+    HG_CUDA(cudaMemcpyAsync(d, ci.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream()));
+    hg::k::lift_ntt(c, d, pt_dev, 1, level + 1, ctx->stream());
+    HG_CUDA(cudaStreamSynchronize(ctx->stream()));
+  });
+}
+
+int hg_encode_constant(hg_context* ctx, double value, int level, double scale, uint64_t* residues) {
+  return guard([&] {
+    hg::Context& c = *ctx->c;
+    level_ok(c, level);
+    hg::check(scale > 0.0, HG_E_VALIDATION, "encoding scale must be positive");
+    const double scaled = value * scale;  // ckks_backend.hpp:203-205
+    hg::check(std::abs(scaled) < 9.0e18, HG_E_VALIDATION, "encoded coefficient overflows the integer range");
+    const int64_t v = std::llround(scaled);
+    for (int i = 0; i <= level; ++i) residues[i] = hg::lift_signed_h(v, c.primes()[i]);
+  });
+}
+
+int hg_encrypt(hg_context* ctx, const hg_keys* keys, const uint64_t* pt_dev, const uint64_t* seeds, int64_t items,
+               int level, uint64_t* out) {
+  return guard([&] {
+    hg::Context& c = *ctx->c;
+    level_ok(c, level);
+    const int64_t n = c.n();
+    std::vector<int64_t> smp(static_cast<size_t>(items * 3 * n));
+    for (int64_t it = 0; it < items; ++it)
+      hg::sample_encryption(seeds[it], n, &smp[it * 3 * n], &smp[it * 3 * n + n], &smp[it * 3 * n + 2 * n]);
+    auto* d = static_cast<int64_t*>(c.scratch(smp.size() * 8, 5));
+    HG_CUDA(cudaMemcpyAsync(d, smp.data(), smp.size() * 8, cudaMemcpyHostToDevice, ctx->stream()));
+    hg::k::encrypt(c, *keys->k, d, pt_dev, out, items, level + 1, ctx->stream());
+    HG_CUDA(cudaStreamSynchronize(ctx->stream()));
+  });
+}
+
+int hg_decrypt_coeffs(hg_context* ctx, const hg_keys* keys, const uint64_t* ct, int64_t items, int size, int level,
+                      uint64_t* m_host) {
+  return guard([&] {
+    hg::Context& c = *ctx->c;
+    level_ok(c, level);
+    const size_t words = static_cast<size_t>(items) * (level + 1) * c.n();
+    auto* m = static_cast<uint64_t*>(c.scratch(words * 8, 6));
+    hg::k::decrypt(c, *keys->k, ct, m, items, size, level + 1, ctx->stream());
+    HG_CUDA(cudaMemcpyAsync(m_host, m, words * 8, cudaMemcpyDeviceToHost, ctx->stream()));
+    HG_CUDA(cudaStreamSynchronize(ctx->stream()));
+  });
+}
+
+namespace hg {
+void decode_coeffs_host(const Context& c, const uint64_t* m, int nl, double scale, int64_t count, double* out);
+}
+
+int hg_decrypt(hg_context* ctx, const hg_keys* keys, const uint64_t* ct, int64_t items, int size, int level,
+               double scale, int64_t count, double* values) {
+  return guard([&] {
+    hg::Context& c = *ctx->c;
+    level_ok(c, level);
+    const int64_t n = c.n();
+    std::vector<uint64_t> m(static_cast<size_t>(items * (level + 1) * n));
+    int rc = hg_decrypt_coeffs(ctx, keys, ct, items, size, level, m.data());
+    if (rc) hg::fail(rc, g_err);
+    for (int64_t it = 0; it < items; ++it)
+      hg::decode_coeffs_host(c, &m[it * (level + 1) * n], level + 1, scale, count, values + it * count);
+  });
+}
+
+}  // extern "C"

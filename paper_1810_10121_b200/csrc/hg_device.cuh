@@ -1,0 +1,121 @@
+// hg_device.cuh -- sm_100a modular arithmetic over RNS limbs.
+//
+// Storage is one uint64 word per residue (the reference's word size,
+// ring.hpp:42) so HEGC-layout buffers move to/from HBM unchanged.  Limbs whose
+// prime is below 2^31 ("small": the 26/30-bit rescale primes of every BASELINE
+// config) run 32-bit Shoup/IMAD arithmetic on the low word; wider primes
+// (36/40/50-bit) use 64-bit Shoup with __umul64hi.  Every value leaving a
+// kernel is canonical in [0, q), so results are
+// bit-identical to the reference regardless of internal lazy ranges.
+#pragma once
+#include <cstdint>
+#include <vector_types.h>
+
+#define HG_MAX_LIMBS 24
+
+namespace hg {
+
+// Per-prime constants (kernel parameter space: uniform, constant-bank access).
+struct LimbInfo {
+  uint64_t q;            // prime
+  uint64_t br_hi, br_lo; // floor(2^128 / q) (ring.hpp:41-47)
+  uint64_t ninv, ninv_s; // N^{-1} mod q and its Shoup constant (ring.hpp:255-256)
+  const ulonglong2* fw;  // {psi^brv, Shoup(psi^brv)}      (ring.hpp:241-254)
+  const ulonglong2* iw;  // {psi^-brv, Shoup(psi^-brv)}
+  const uint2* fw32;     // {psi^brv, floor(w 2^32/q)} for small primes (else null)
+  const uint2* iw32;
+  uint32_t ninv32_s;     // floor(ninv 2^32 / q) for small primes
+  uint32_t small;        // q < 2^31
+};
+
+struct CtxParams {
+  int logn;
+  int nlimbs;
+  int64_t n;
+  LimbInfo limb[HG_MAX_LIMBS];
+};
+
+#ifdef __CUDACC__
+// ---------------------------------------------------------------------------
+// scalar helpers
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint64_t add_mod(uint64_t a, uint64_t b, uint64_t q) {
+  uint64_t s = a + b;
+  return s >= q ? s - q : s;
+}
+__device__ __forceinline__ uint64_t sub_mod(uint64_t a, uint64_t b, uint64_t q) {
+  return a >= b ? a - b : a + q - b;
+}
+__device__ __forceinline__ uint64_t neg_mod(uint64_t a, uint64_t q) { return a == 0 ? 0 : q - a; }
+
+// x * w mod q with Shoup constant ws = floor(w 2^64 / q); x < 2^64, w < q.
+__device__ __forceinline__ uint64_t mul_shoup64(uint64_t x, uint64_t w, uint64_t ws, uint64_t q) {
+  uint64_t hi = __umul64hi(x, ws);
+  uint64_t r = x * w - hi * q;
+  return r >= q ? r - q : r;
+}
+// lazy variant: result in [0, 2q)
+__device__ __forceinline__ uint64_t mul_shoup64_lazy(uint64_t x, uint64_t w, uint64_t ws, uint64_t q) {
+  return x * w - __umul64hi(x, ws) * q;
+}
+
+__device__ __forceinline__ uint32_t mul_shoup32(uint32_t x, uint32_t w, uint32_t ws, uint32_t q) {
+  uint32_t hi = __umulhi(x, ws);
+  uint32_t r = x * w - hi * q;
+  return r >= q ? r - q : r;
+}
+__device__ __forceinline__ uint32_t mul_shoup32_lazy(uint32_t x, uint32_t w, uint32_t ws, uint32_t q) {
+  return x * w - __umulhi(x, ws) * q;
+}
+
+// 128-bit Barrett reduction, z = (z1:z0) < 2^124 (ring.hpp:52-63).
+__device__ __forceinline__ uint64_t reduce128(uint64_t z0, uint64_t z1, const LimbInfo& L) {
+  uint64_t m0hi = __umul64hi(z0, L.br_lo);
+  uint64_t m1lo = z0 * L.br_hi, m1hi = __umul64hi(z0, L.br_hi);
+  uint64_t m2lo = z1 * L.br_lo, m2hi = __umul64hi(z1, L.br_lo);
+  uint64_t m3lo = z1 * L.br_hi;
+  // mid = m0hi + m1lo + m2lo (66 bits); carry = mid >> 64
+  uint64_t s1 = m0hi + m1lo;
+  uint64_t c1 = s1 < m0hi;
+  uint64_t s2 = s1 + m2lo;
+  uint64_t c2 = s2 < s1;
+  uint64_t quot = m3lo + m1hi + m2hi + c1 + c2;
+  uint64_t r = z0 - quot * L.q;
+  return r >= L.q ? r - L.q : r;
+}
+
+__device__ __forceinline__ uint64_t mul_mod(uint64_t a, uint64_t b, const LimbInfo& L) {
+  return reduce128(a * b, __umul64hi(a, b), L);
+}
+
+// 128-bit accumulator
+struct Acc128 {
+  uint64_t lo, hi;
+  __device__ __forceinline__ void zero() { lo = 0; hi = 0; }
+  __device__ __forceinline__ void mac(uint64_t a, uint64_t b) {
+    uint64_t pl = a * b, ph = __umul64hi(a, b);
+    lo += pl;
+    hi += ph + (lo < pl);
+  }
+  __device__ __forceinline__ void mac32(uint32_t a, uint32_t b) {  // a, b < 2^32
+    uint64_t p = (uint64_t)a * b;
+    lo += p;
+    hi += (lo < p);
+  }
+  __device__ __forceinline__ void add(uint64_t v) {
+    lo += v;
+    hi += (lo < v);
+  }
+};
+
+// llround-compatible centred lift of a signed value into [0, q) (poly.hpp:54-58)
+__device__ __forceinline__ uint64_t lift_signed(int64_t v, uint64_t q) {
+  int64_t r = v % (int64_t)q;
+  if (r < 0) r += (int64_t)q;
+  return (uint64_t)r;
+}
+
+#endif  // __CUDACC__
+
+}  // namespace hg

@@ -1,0 +1,529 @@
+// hg_host.cpp -- host-side context, tables, encoder, samplers and key
+// generation for the B200 CKKS backend.
+//
+// Everything here reproduces the reference bit for bit (same primes, same psi,
+// same bit-reversed tables, same Rng streams, same fp64 FFT operation order),
+// because ciphertext parity with the CPU reference depends on it.  Compiled
+// with -ffp-contract=off and no -march flags: the reference's x86-64 build has
+// no FMA, so neither may we.
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <mutex>
+#include <set>
+#include <thread>
+
+#include "hg_internal.hpp"
+
+namespace hg {
+
+using u128 = unsigned __int128;
+
+// ---------------------------------------------------------------------------
+// Rng::gaussian (common.hpp:100-105)
+// ---------------------------------------------------------------------------
+double Rng::gaussian() {
+  double u1 = uniform();
+  double u2 = uniform();
+  while (u1 <= 1e-300) u1 = uniform();
+  return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586476925286766559 * u2);
+}
+
+// ---------------------------------------------------------------------------
+// HMod (ring.hpp:37-111)
+// ---------------------------------------------------------------------------
+HMod::HMod(uint64_t v) : q(v) {
+  check(v >= 3 && v < (uint64_t(1) << 62), HG_EVALIDATION, "modulus must lie in [3, 2^62)");
+  u128 two64 = u128(1) << 64;
+  br_hi = static_cast<uint64_t>(two64 / v);
+  uint64_t rem = static_cast<uint64_t>(two64 % v);
+  br_lo = static_cast<uint64_t>((u128(rem) << 64) / v);
+}
+uint64_t HMod::mul(uint64_t a, uint64_t b) const { return static_cast<uint64_t>(u128(a) * b % q); }
+uint64_t HMod::pow(uint64_t b, uint64_t e) const {
+  uint64_t r = 1, cur = b >= q ? b % q : b;
+  while (e) {
+    if (e & 1) r = mul(r, cur);
+    cur = mul(cur, cur);
+    e >>= 1;
+  }
+  return r;
+}
+uint64_t HMod::shoup(uint64_t w) const { return static_cast<uint64_t>((u128(w) << 64) / q); }
+
+static bool is_prime(uint64_t n) {  // ring.hpp:137-163
+  static const uint64_t bases[] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  if (n < 2) return false;
+  for (uint64_t p : bases) {
+    if (n == p) return true;
+    if (n % p == 0) return false;
+  }
+  uint64_t d = n - 1;
+  int s = 0;
+  while ((d & 1) == 0) { d >>= 1; ++s; }
+  auto mm = [n](uint64_t a, uint64_t b) { return static_cast<uint64_t>(u128(a) * b % n); };
+  for (uint64_t b : bases) {
+    uint64_t x = 1, base = b % n, e = d;
+    while (e) {
+      if (e & 1) x = mm(x, base);
+      base = mm(base, base);
+      e >>= 1;
+    }
+    if (x == 1 || x == n - 1) continue;
+    bool witness = true;
+    for (int i = 1; i < s; ++i) {
+      x = mm(x, x);
+      if (x == n - 1) { witness = false; break; }
+    }
+    if (witness) return false;
+  }
+  return true;
+}
+
+std::vector<uint64_t> generate_ntt_primes(int64_t n, const std::vector<int>& bits) {  // ring.hpp:171-196
+  check(n >= 4 && (n & (n - 1)) == 0, HG_EVALIDATION, "transform size must be a power of two, at least 4");
+  std::vector<uint64_t> primes;
+  std::set<uint64_t> used;
+  const uint64_t step = 2 * static_cast<uint64_t>(n);
+  for (int b : bits) {
+    check(b >= 20 && b <= 60, HG_EVALIDATION, "coefficient modulus bit sizes must lie in [20, 60]");
+    const uint64_t top = uint64_t(1) << b, floor_bound = uint64_t(1) << (b - 1);
+    bool found = false;
+    for (uint64_t k = (top - 2) / step; k >= 1; --k) {
+      const uint64_t cand = k * step + 1;
+      if (cand < floor_bound) break;
+      if (used.count(cand) || !is_prime(cand)) continue;
+      primes.push_back(cand);
+      used.insert(cand);
+      found = true;
+      break;
+    }
+    if (!found)
+      fail(HG_EVALIDATION,
+           "no unused " + std::to_string(b) + "-bit prime supports transform size " + std::to_string(n));
+  }
+  return primes;
+}
+
+// ---------------------------------------------------------------------------
+// SlotEncoder (encoder.hpp:38-115).  Complex products written out as GCC
+// expands std::complex<double> multiplication: (ac - bd, ad + bc).
+// ---------------------------------------------------------------------------
+SlotEncoder::SlotEncoder(int64_t n) : m_n(n) {
+  check(n >= 2 && (n & (n - 1)) == 0, HG_EINTERNAL, "slot encoder needs a power-of-two degree");
+  m_roots.resize(2 * n);
+  m_half.resize(2 * n);
+  const double pi = std::acos(-1.0);
+  for (int64_t j = 0; j < n; ++j) {
+    const double a = -2.0 * pi * static_cast<double>(j) / static_cast<double>(n);
+    m_roots[2 * j] = std::cos(a);
+    m_roots[2 * j + 1] = std::sin(a);
+    const double h = -pi * static_cast<double>(j) / static_cast<double>(n);
+    m_half[2 * j] = std::cos(h);
+    m_half[2 * j + 1] = std::sin(h);
+  }
+  int log_n = 0;
+  while ((int64_t(1) << log_n) < n) ++log_n;
+  m_rev.resize(n);
+  for (int64_t j = 0; j < n; ++j) {
+    uint32_t r = 0;
+    for (int b = 0; b < log_n; ++b) r |= ((static_cast<uint32_t>(j) >> b) & 1u) << (log_n - 1 - b);
+    m_rev[j] = r;
+  }
+}
+
+void SlotEncoder::fft(double* a, bool conj) const {  // encoder.hpp:92-109
+  const int64_t n = m_n;
+  for (int64_t j = 0; j < n; ++j) {
+    const int64_t r = m_rev[j];
+    if (r > j) {
+      std::swap(a[2 * j], a[2 * r]);
+      std::swap(a[2 * j + 1], a[2 * r + 1]);
+    }
+  }
+  for (int64_t len = 2; len <= n; len <<= 1) {
+    const int64_t step = n / len, h = len / 2;
+    for (int64_t start = 0; start < n; start += len) {
+      for (int64_t j = 0; j < h; ++j) {
+        const double wr = m_roots[2 * (j * step)];
+        const double wi = conj ? -m_roots[2 * (j * step) + 1] : m_roots[2 * (j * step) + 1];
+        double* u = a + 2 * (start + j);
+        double* x = a + 2 * (start + j + h);
+        const double vr = x[0] * wr - x[1] * wi;
+        const double vi = x[0] * wi + x[1] * wr;
+        const double ur = u[0], ui = u[1];
+        u[0] = ur + vr;
+        u[1] = ui + vi;
+        x[0] = ur - vr;
+        x[1] = ui - vi;
+      }
+    }
+  }
+}
+
+void SlotEncoder::values_to_coeffs(const double* values, int64_t count, double* coeffs) const {
+  check(count <= m_n / 2, HG_ECAPACITY, "payload exceeds the available slot capacity");
+  std::vector<double> a(2 * m_n, 0.0);
+  for (int64_t m = 0; m < count; ++m) a[2 * m] = values[m];
+  fft(a.data(), false);
+  const double norm = 2.0 / static_cast<double>(m_n);
+  for (int64_t k = 0; k < m_n; ++k) {
+    const double re = m_half[2 * k] * a[2 * k] - m_half[2 * k + 1] * a[2 * k + 1];
+    coeffs[k] = norm * re;
+  }
+}
+
+void SlotEncoder::coeffs_to_values(const double* coeffs, int64_t count, double* values) const {
+  check(count >= 0 && count <= m_n / 2, HG_ECAPACITY, "requested more slots than the ring provides");
+  std::vector<double> b(2 * m_n);
+  for (int64_t k = 0; k < m_n; ++k) {
+    b[2 * k] = coeffs[k] * m_half[2 * k];
+    b[2 * k + 1] = coeffs[k] * -m_half[2 * k + 1];
+  }
+  fft(b.data(), true);
+  for (int64_t m = 0; m < count; ++m) values[m] = b[2 * m];
+}
+
+// ---------------------------------------------------------------------------
+// DevBuf
+// ---------------------------------------------------------------------------
+void DevBuf::alloc(size_t b) {
+  release();
+  if (b == 0) return;
+  HG_CUDA(cudaMalloc(&p, b));
+  bytes = b;
+}
+void DevBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+
+// ---------------------------------------------------------------------------
+// Context (context.hpp:92-109, ring.hpp:223-257)
+// ---------------------------------------------------------------------------
+static int security_bound(int security, int64_t n) {  // context.hpp:52-69
+  struct Row { int64_t n; int b128, b192, b256; };
+  static const Row t[] = {{1024, 27, 19, 14},   {2048, 54, 37, 29},    {4096, 109, 75, 58},
+                          {8192, 218, 152, 118}, {16384, 438, 305, 237}, {32768, 881, 611, 476}};
+  for (const Row& r : t)
+    if (r.n == n) return security == 128 ? r.b128 : security == 192 ? r.b192 : security == 256 ? r.b256 : -1;
+  return -1;
+}
+
+Context::Context(const ContextParamsH& p, int device) : m_p(p), m_device(device) {
+  if (p.n < 1024 || p.n > 32768 || (p.n & (p.n - 1)) != 0)
+    fail(HG_EVALIDATION, "poly_degree must be a power of two in [1024, 32768]");
+  if (p.bits.size() < 2) fail(HG_EVALIDATION, "coefficient modulus needs at least 2 primes (one rescale level)");
+  if (p.scale_bits < 10 || p.scale_bits > 60) fail(HG_EVALIDATION, "scale_bits must lie in [10, 60]");
+  if (p.security != 0 && p.security != 128 && p.security != 192 && p.security != 256)
+    fail(HG_EVALIDATION, "security must be one of 0, 128, 192, 256");
+  check(static_cast<int>(p.bits.size()) <= HG_MAX_LIMBS, HG_EVALIDATION, "too many primes for this build");
+  if (p.security != 0) {
+    int bound = security_bound(p.security, p.n), total = 0;
+    for (int b : p.bits) total += b;
+    if (bound > 0 && total > bound)
+      fprintf(stderr,
+              "warning: coefficient modulus spans %d bits, above the %d-bit estimate for %d-bit security at ring "
+              "dimension %lld; the requested level is not met\n",
+              total, bound, p.security, (long long)p.n);
+  }
+  while ((int64_t(1) << m_logn) < p.n) ++m_logn;
+  m_q = generate_ntt_primes(p.n, p.bits);
+  const int64_t n = p.n;
+  const int nl = static_cast<int>(m_q.size());
+  for (uint64_t q : m_q) m_mod.emplace_back(q);
+
+  HG_CUDA(cudaSetDevice(device));
+  HG_CUDA(cudaStreamCreateWithFlags(&m_stream, cudaStreamNonBlocking));
+
+  // tables: per limb fw (16N) | iw (16N) | fw32 (8N) | iw32 (8N)
+  const size_t per = 48 * static_cast<size_t>(n);
+  m_tables.alloc(per * nl);
+  std::vector<uint8_t> host(per * nl, 0);
+  m_psi.resize(nl);
+  m_invq.assign(nl, std::vector<uint64_t>(nl, 0));
+  m_invq_s.assign(nl, std::vector<uint64_t>(nl, 0));
+  m_kp.logn = m_logn;
+  m_kp.n = n;
+  m_kp.nlimbs = nl;
+  for (int i = 0; i < nl; ++i) {
+    const HMod& M = m_mod[i];
+    const uint64_t q = M.q;
+    const uint64_t exponent = (q - 1) / (2 * static_cast<uint64_t>(n));
+    uint64_t psi = 0;
+    for (uint64_t h = 2;; ++h) {
+      const uint64_t g = M.pow(h, exponent);
+      if (M.pow(g, static_cast<uint64_t>(n)) == q - 1) { psi = g; break; }
+    }
+    const uint64_t psi_inv = M.inv(psi);
+    uint8_t* base = host.data() + per * i;
+    auto* fw = reinterpret_cast<uint64_t*>(base);
+    auto* iw = reinterpret_cast<uint64_t*>(base + 16 * n);
+    auto* fw32 = reinterpret_cast<uint32_t*>(base + 32 * n);
+    auto* iw32 = reinterpret_cast<uint32_t*>(base + 40 * n);
+    const bool small = q < (uint64_t(1) << 31);
+    std::vector<uint64_t>& psi_brv = m_psi[i];
+    psi_brv.resize(n);
+    uint64_t f = 1, b = 1;
+    for (int64_t j = 0; j < n; ++j) {
+      uint64_t r = 0;
+      for (int t = 0; t < m_logn; ++t) r |= ((static_cast<uint64_t>(j) >> t) & 1) << (m_logn - 1 - t);
+      psi_brv[r] = f;
+      fw[2 * r] = f;
+      fw[2 * r + 1] = M.shoup(f);
+      iw[2 * r] = b;
+      iw[2 * r + 1] = M.shoup(b);
+      if (small) {
+        fw32[2 * r] = static_cast<uint32_t>(f);
+        fw32[2 * r + 1] = static_cast<uint32_t>(fw[2 * r + 1] >> 32);
+        iw32[2 * r] = static_cast<uint32_t>(b);
+        iw32[2 * r + 1] = static_cast<uint32_t>(iw[2 * r + 1] >> 32);
+      }
+      f = M.mul(f, psi);
+      b = M.mul(b, psi_inv);
+    }
+    LimbInfo& L = m_kp.limb[i];
+    L.q = q;
+    L.br_hi = M.br_hi;
+    L.br_lo = M.br_lo;
+    L.ninv = M.inv(static_cast<uint64_t>(n) % q);
+    L.ninv_s = M.shoup(L.ninv);
+    L.ninv32_s = static_cast<uint32_t>(L.ninv_s >> 32);
+    L.small = small ? 1u : 0u;
+    uint8_t* dbase = m_tables.as<uint8_t>() + per * i;
+    L.fw = reinterpret_cast<const ulonglong2*>(dbase);
+    L.iw = reinterpret_cast<const ulonglong2*>(dbase + 16 * n);
+    L.fw32 = small ? reinterpret_cast<const uint2*>(dbase + 32 * n) : nullptr;
+    L.iw32 = small ? reinterpret_cast<const uint2*>(dbase + 40 * n) : nullptr;
+  }
+  HG_CUDA(cudaMemcpy(m_tables.p, host.data(), host.size(), cudaMemcpyHostToDevice));
+  for (int t = 0; t < nl; ++t)
+    for (int j = 0; j < nl; ++j) {
+      if (j == t) continue;
+      const HMod& M = m_mod[j];
+      m_invq[t][j] = M.inv(m_q[t] % M.q);
+      m_invq_s[t][j] = M.shoup(m_invq[t][j]);
+    }
+  m_row0.resize(nl);
+  m_digits.resize(nl);
+  for (int i = 0; i < nl; ++i) {  // ckks_backend.hpp:42-46
+    int d = 0;
+    for (uint64_t m = m_q[i] - 1; m != 0; m >>= 15) ++d;
+    m_digits[i] = d == 0 ? 1 : d;
+    m_row0[i] = m_rows;
+    m_rows += m_digits[i];
+  }
+  m_enc = std::make_unique<SlotEncoder>(n);
+}
+
+Context::~Context() {
+  m_scratch.clear();
+  m_tables.release();
+  if (m_stream) cudaStreamDestroy(m_stream);
+}
+
+double Context::default_scale() const { return std::ldexp(1.0, m_p.scale_bits); }
+
+void* Context::scratch(size_t bytes, int slot) {
+  DevBuf& b = m_scratch[slot];
+  if (b.bytes < bytes) {
+    HG_CUDA(cudaStreamSynchronize(m_stream));
+    b.alloc(bytes);
+  }
+  return b.p;
+}
+
+// ---------------------------------------------------------------------------
+// Samplers (poly.hpp:247-276) and keys (ckks_backend.hpp:74-114)
+// ---------------------------------------------------------------------------
+static constexpr double kErrorStdDev = 3.2;  // backend.hpp:29
+
+void sample_ternary(Rng& r, int64_t n, int64_t* out) {
+  for (int64_t k = 0; k < n; ++k) out[k] = static_cast<int64_t>(r.uniform_int(3)) - 1;
+}
+void sample_gaussian(Rng& r, int64_t n, double sigma, int64_t* out) {
+  for (int64_t k = 0; k < n; ++k) out[k] = static_cast<int64_t>(std::llround(r.gaussian() * sigma));
+}
+void sample_encryption(uint64_t seed, int64_t n, int64_t* u, int64_t* e0, int64_t* e1) {
+  Rng rng(seed);
+  Rng u_rng = rng.fork("mask");
+  Rng e_rng = rng.fork("error");
+  sample_ternary(u_rng, n, u);
+  sample_gaussian(e_rng, n, kErrorStdDev, e0);
+  sample_gaussian(e_rng, n, kErrorStdDev, e1);
+}
+
+static void sample_uniform_ntt(const Context& c, Rng& r, uint64_t* out) {
+  const int64_t n = c.n();
+  for (int i = 0; i <= c.max_level(); ++i) {
+    const uint64_t q = c.primes()[i];
+    for (int64_t k = 0; k < n; ++k) out[i * n + k] = r.uniform_int(q);
+  }
+}
+
+std::unique_ptr<Keys> generate_keys(const Context& c, uint64_t seed, bool with_relin) {
+  const int L = c.max_level(), nl = L + 1;
+  const int64_t n = c.n(), pw = nl * n;
+  cudaStream_t s = c.stream();
+  Rng root(seed);
+  Rng secret_rng = root.fork("secret");
+  Rng public_rng = root.fork("public");
+  Rng relin_rng = root.fork("relin");
+  auto keys = std::make_unique<Keys>();
+  keys->secret.alloc(pw * 8);
+  keys->pk.alloc(2 * pw * 8);
+  std::vector<int64_t> coef(n);
+  std::vector<uint64_t> a(pw);
+  DevBuf dcoef(n * 8), de(pw * 8);
+
+  sample_ternary(secret_rng, n, coef.data());
+  HG_CUDA(cudaMemcpyAsync(dcoef.p, coef.data(), n * 8, cudaMemcpyHostToDevice, s));
+  k::lift_ntt(c, dcoef.as<int64_t>(), keys->secret.as<uint64_t>(), 1, nl, s);
+
+  sample_gaussian(public_rng, n, kErrorStdDev, coef.data());
+  HG_CUDA(cudaMemcpyAsync(dcoef.p, coef.data(), n * 8, cudaMemcpyHostToDevice, s));
+  k::lift_ntt(c, dcoef.as<int64_t>(), de.as<uint64_t>(), 1, nl, s);
+  sample_uniform_ntt(c, public_rng, a.data());
+  uint64_t* pk_b = keys->pk.as<uint64_t>();
+  uint64_t* pk_a = pk_b + pw;
+  HG_CUDA(cudaMemcpyAsync(pk_a, a.data(), pw * 8, cudaMemcpyHostToDevice, s));
+  k::keygen_b(c, pk_a, keys->secret.as<uint64_t>(), de.as<uint64_t>(), pk_b, nl, -1, 0, s);
+  HG_CUDA(cudaStreamSynchronize(s));
+
+  if (with_relin) {
+    const int rows = c.relin_rows();
+    keys->relin.alloc(static_cast<size_t>(rows) * 2 * pw * 8);
+    for (int i = 0; i <= L; ++i) {
+      for (int d = 0; d < c.digits(i); ++d) {
+        const int row = c.relin_row(i, d);
+        uint64_t* rb = keys->relin.as<uint64_t>() + static_cast<int64_t>(row) * 2 * pw;
+        uint64_t* ra = rb + pw;
+        sample_gaussian(relin_rng, n, kErrorStdDev, coef.data());
+        sample_uniform_ntt(c, relin_rng, a.data());
+        HG_CUDA(cudaMemcpyAsync(dcoef.p, coef.data(), n * 8, cudaMemcpyHostToDevice, s));
+        k::lift_ntt(c, dcoef.as<int64_t>(), de.as<uint64_t>(), 1, nl, s);
+        HG_CUDA(cudaMemcpyAsync(ra, a.data(), pw * 8, cudaMemcpyHostToDevice, s));
+        const uint64_t f = c.mod(i).pow(2, static_cast<uint64_t>(15) * static_cast<uint64_t>(d));
+        k::keygen_b(c, ra, keys->secret.as<uint64_t>(), de.as<uint64_t>(), rb, nl, i, f, s);
+        HG_CUDA(cudaStreamSynchronize(s));  // host buffers are reused
+      }
+    }
+    keys->has_relin = true;
+  }
+  HG_CUDA(cudaStreamSynchronize(s));
+  return keys;
+}
+
+}  // namespace hg
+
+namespace hg {
+
+// ---------------------------------------------------------------------------
+// CRT reconstruction to a centred double (ring.hpp:350-480, CrtReconstructor)
+// followed by /scale and the slot decode (ckks_backend.hpp:493-505).  The
+// multiword arithmetic and the final to_double() follow the reference's order
+// exactly so decoded values are bit-identical.
+// ---------------------------------------------------------------------------
+namespace {
+struct Crt {
+  int count = 0, width = 0;
+  std::vector<uint64_t> total, half;
+  std::vector<std::vector<uint64_t>> punct;
+  std::vector<uint64_t> punct_inv;
+};
+
+void w_mul(std::vector<uint64_t>& x, uint64_t s) {
+  u128 carry = 0;
+  for (auto& l : x) {
+    u128 cur = u128(l) * s + carry;
+    l = static_cast<uint64_t>(cur);
+    carry = cur >> 64;
+  }
+}
+int w_cmp(const std::vector<uint64_t>& a, const std::vector<uint64_t>& b) {
+  for (size_t i = a.size(); i-- > 0;)
+    if (a[i] != b[i]) return a[i] < b[i] ? -1 : 1;
+  return 0;
+}
+void w_sub(std::vector<uint64_t>& a, const std::vector<uint64_t>& b) {
+  uint64_t borrow = 0;
+  for (size_t i = 0; i < a.size(); ++i) {
+    const uint64_t o = b[i], before = a[i];
+    a[i] = before - o - borrow;
+    borrow = (before < o || (borrow && before == o)) ? 1 : 0;
+  }
+}
+double w_double(const std::vector<uint64_t>& a) {
+  double r = 0.0;
+  for (size_t i = a.size(); i-- > 0;) r = r * 18446744073709551616.0 + static_cast<double>(a[i]);
+  return r;
+}
+
+Crt make_crt(const std::vector<uint64_t>& q, int count) {
+  Crt c;
+  c.count = count;
+  c.width = count + 1;
+  c.total.assign(c.width, 0);
+  c.total[0] = 1;
+  for (int i = 0; i < count; ++i) w_mul(c.total, q[i]);
+  c.half.assign(c.width, 0);
+  for (int i = 0; i < c.width; ++i) {
+    c.half[i] = c.total[i] >> 1;
+    if (i + 1 < c.width) c.half[i] |= c.total[i + 1] << 63;
+  }
+  for (int i = 0; i < count; ++i) {
+    std::vector<uint64_t> p(c.width, 0);
+    p[0] = 1;
+    for (int j = 0; j < count; ++j)
+      if (j != i) w_mul(p, q[j]);
+    uint64_t r = 0;
+    for (int k = c.width; k-- > 0;) r = static_cast<uint64_t>(((u128(r) << 64) | p[k]) % q[i]);
+    HMod M(q[i]);
+    c.punct_inv.push_back(M.inv(r));
+    c.punct.push_back(std::move(p));
+  }
+  return c;
+}
+}  // namespace
+
+void decode_coeffs_host(const Context& ctx, const uint64_t* m, int nl, double scale, int64_t count, double* out) {
+  static std::mutex mu;
+  static std::map<std::pair<const Context*, int>, Crt> cache;
+  const Crt* crt;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto key = std::make_pair(&ctx, nl);
+    auto it = cache.find(key);
+    if (it == cache.end()) it = cache.emplace(key, make_crt(ctx.primes(), nl)).first;
+    crt = &it->second;
+  }
+  const int64_t n = ctx.n();
+  std::vector<double> coeffs(n);
+  std::vector<uint64_t> acc(crt->width);
+  for (int64_t k = 0; k < n; ++k) {
+    std::fill(acc.begin(), acc.end(), 0);
+    for (int i = 0; i < nl; ++i) {
+      const uint64_t s = ctx.mod(i).mul(m[i * n + k], crt->punct_inv[i]);
+      u128 carry = 0;
+      for (int w = 0; w < crt->width; ++w) {
+        u128 cur = u128(crt->punct[i][w]) * s + acc[w] + carry;
+        acc[w] = static_cast<uint64_t>(cur);
+        carry = cur >> 64;
+      }
+    }
+    while (w_cmp(acc, crt->total) >= 0) w_sub(acc, crt->total);
+    double v;
+    if (w_cmp(acc, crt->half) > 0) {
+      std::vector<uint64_t> neg = crt->total;
+      w_sub(neg, acc);
+      v = -w_double(neg);
+    } else {
+      v = w_double(acc);
+    }
+    coeffs[k] = v / scale;
+  }
+  ctx.encoder().coeffs_to_values(coeffs.data(), count, out);
+}
+
+}  // namespace hg

@@ -1,0 +1,276 @@
+// hg_internal.hpp -- host-side C++ of the B200 CKKS backend (not exported).
+//
+// The host owns everything the reference computes once or in double precision
+// (prime generation and twiddle tables, key sampling, the fp64 slot FFT, scale
+// bookkeeping, executor planning); ciphertext arithmetic runs in the CUDA
+// kernels declared at the bottom (hg_kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hg_device.cuh"
+
+namespace hg {
+
+// ---------------------------------------------------------------------------
+// errors: mirror heg::errc (common.hpp:37-61); C-ABI returns these codes.
+// ---------------------------------------------------------------------------
+enum ErrCode : int {
+  HG_OK_ = 0,
+  HG_EVALIDATION = 1,
+  HG_EPARSE = 2,
+  HG_EDEPTH = 3,
+  HG_ECAPACITY = 4,
+  HG_EIO = 5,
+  HG_EINTERNAL = 6,
+  HG_ECUDA = 7,
+};
+
+class Error : public std::runtime_error {
+ public:
+  Error(int code, const std::string& msg) : std::runtime_error(msg), m_code(code) {}
+  int code() const { return m_code; }
+
+ private:
+  int m_code;
+};
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+inline void check(bool c, int code, const std::string& msg) {
+  if (!c) fail(code, msg);
+}
+void cuda_check(cudaError_t e, const char* what);
+#define HG_CUDA(x) ::hg::cuda_check((x), #x)
+
+// ---------------------------------------------------------------------------
+// Rng: the reference's splitmix64 generator (common.hpp:71-122), bit-identical.
+// ---------------------------------------------------------------------------
+inline uint64_t splitmix64(uint64_t& s) {
+  uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+class Rng {
+ public:
+  explicit Rng(uint64_t seed = 0) : m_s(seed ^ 0xd1b54a32d192ed03ULL) {
+    next();
+    next();
+  }
+  uint64_t next() { return splitmix64(m_s); }
+  double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+  uint64_t uniform_int(uint64_t n) { return next() % n; }
+  double gaussian();
+  Rng fork(uint64_t label) const {
+    uint64_t s = m_s;
+    uint64_t mixed = splitmix64(s) ^ (label * 0x9e3779b97f4a7c15ULL + 0x165667b19e3779f9ULL);
+    return Rng(mixed);
+  }
+  Rng fork(const std::string& label) const {
+    uint64_t h = 0xcbf29ce484222325ULL;
+    for (unsigned char c : label) h = (h ^ c) * 0x100000001b3ULL;
+    return fork(h);
+  }
+  uint64_t state() const { return m_s; }
+
+ private:
+  uint64_t m_s;
+};
+
+// ---------------------------------------------------------------------------
+// Host modular helpers (ring.hpp:37-111 semantics)
+// ---------------------------------------------------------------------------
+struct HMod {
+  uint64_t q = 0, br_hi = 0, br_lo = 0;
+  HMod() = default;
+  explicit HMod(uint64_t v);
+  uint64_t mul(uint64_t a, uint64_t b) const;
+  uint64_t pow(uint64_t b, uint64_t e) const;
+  uint64_t inv(uint64_t a) const { return pow(a, q - 2); }
+  uint64_t shoup(uint64_t w) const;
+};
+std::vector<uint64_t> generate_ntt_primes(int64_t n, const std::vector<int>& bits);
+inline uint64_t lift_signed_h(int64_t v, uint64_t q) {
+  int64_t r = v % static_cast<int64_t>(q);
+  if (r < 0) r += static_cast<int64_t>(q);
+  return static_cast<uint64_t>(r);
+}
+
+// ---------------------------------------------------------------------------
+// Slot encoder (encoder.hpp:38-115), fp64 radix-2, bit-identical on x86-64.
+// ---------------------------------------------------------------------------
+class SlotEncoder {
+ public:
+  explicit SlotEncoder(int64_t n);
+  int64_t n() const { return m_n; }
+  void values_to_coeffs(const double* values, int64_t count, double* coeffs) const;
+  void coeffs_to_values(const double* coeffs, int64_t count, double* values) const;
+  const std::vector<double>& roots_interleaved() const { return m_roots; }
+  const std::vector<double>& half_roots_interleaved() const { return m_half; }
+  const std::vector<uint32_t>& rev() const { return m_rev; }
+
+ private:
+  void fft(double* a, bool conj) const;
+  int64_t m_n;
+  std::vector<double> m_roots, m_half;  // interleaved (re, im)
+  std::vector<uint32_t> m_rev;
+};
+
+// ---------------------------------------------------------------------------
+// Device buffer (RAII)
+// ---------------------------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t b) { alloc(b); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t b);
+  void release();
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+// ---------------------------------------------------------------------------
+// Context: primes + twiddle tables resident in HBM (context.hpp:90-157)
+// ---------------------------------------------------------------------------
+struct ContextParamsH {
+  int64_t n = 8192;
+  std::vector<int> bits = {30, 30, 30, 30, 30, 30, 30};
+  int scale_bits = 30;
+  int security = 128;
+};
+
+class Context {
+ public:
+  Context(const ContextParamsH& p, int device);
+  ~Context();
+  const ContextParamsH& params() const { return m_p; }
+  int64_t n() const { return m_p.n; }
+  int logn() const { return m_logn; }
+  int max_level() const { return static_cast<int>(m_q.size()) - 1; }
+  int64_t slot_count() const { return m_p.n / 2; }
+  double default_scale() const;
+  const std::vector<uint64_t>& primes() const { return m_q; }
+  const HMod& mod(int i) const { return m_mod[static_cast<size_t>(i)]; }
+  const CtxParams& kp() const { return m_kp; }
+  int device() const { return m_device; }
+  cudaStream_t stream() const { return m_stream; }
+  const SlotEncoder& encoder() const { return *m_enc; }
+  // host copies of the tables (for tests / host reference use)
+  const std::vector<uint64_t>& psi(int i) const { return m_psi[static_cast<size_t>(i)]; }
+  // rescale constants: inv(q_t mod q_j) and its Shoup constant
+  uint64_t inv_q(int t, int j) const { return m_invq[static_cast<size_t>(t)][static_cast<size_t>(j)]; }
+  uint64_t inv_q_shoup(int t, int j) const { return m_invq_s[static_cast<size_t>(t)][static_cast<size_t>(j)]; }
+  // relin digit counts (ckks_backend.hpp:42-46)
+  int digits(int i) const { return m_digits[static_cast<size_t>(i)]; }
+  int relin_row(int i, int d) const { return m_row0[static_cast<size_t>(i)] + d; }
+  int relin_rows() const { return m_rows; }
+  // scratch arena
+  void* scratch(size_t bytes, int slot = 0);
+
+ private:
+  ContextParamsH m_p;
+  int m_logn = 0;
+  int m_device = 0;
+  cudaStream_t m_stream = nullptr;
+  std::vector<uint64_t> m_q;
+  std::vector<HMod> m_mod;
+  std::vector<std::vector<uint64_t>> m_psi;
+  std::vector<std::vector<uint64_t>> m_invq, m_invq_s;
+  std::vector<int> m_digits, m_row0;
+  int m_rows = 0;
+  DevBuf m_tables;
+  CtxParams m_kp{};
+  std::unique_ptr<SlotEncoder> m_enc;
+  std::map<int, DevBuf> m_scratch;
+};
+
+// ---------------------------------------------------------------------------
+// Keys resident per GPU (ckks_backend.hpp:53-114), NTT form, full chain.
+// ---------------------------------------------------------------------------
+struct Keys {
+  DevBuf secret;  // (L+1) N
+  DevBuf pk;      // [2][(L+1) N]: b then a
+  DevBuf relin;   // [rows][2][(L+1) N]: b then a per (i,d) row
+  bool has_relin = false;
+};
+std::unique_ptr<Keys> generate_keys(const Context& ctx, uint64_t seed, bool with_relin);
+
+// host samplers (poly.hpp:247-276): signed coefficient streams
+void sample_ternary(Rng& r, int64_t n, int64_t* out);
+void sample_gaussian(Rng& r, int64_t n, double sigma, int64_t* out);
+// fresh-encryption samples for one seed: u, e0, e1 (ckks_backend.hpp:470-490)
+void sample_encryption(uint64_t seed, int64_t n, int64_t* u, int64_t* e0, int64_t* e1);
+
+// ---------------------------------------------------------------------------
+// Kernel launchers (hg_kernels.cu).  All buffers are device pointers in the
+// [item][poly][limb][N] layout with `nl` limbs per poly (level = nl - 1).
+// ---------------------------------------------------------------------------
+namespace k {
+// in-place NTT of `rows` limb rows; row r has limb (r % nl) and lives at base + r*N
+void ntt(const Context& c, uint64_t* base, int64_t rows, int nl, bool inverse, cudaStream_t s);
+// lift signed int64 coefficient polys (count of them, N each) to nl limbs and NTT: out [count][nl][N]
+void lift_ntt(const Context& c, const int64_t* src, uint64_t* out, int64_t count, int nl, cudaStream_t s);
+void add(const Context& c, const uint64_t* a, const uint64_t* b, uint64_t* o, int64_t words, int nl, cudaStream_t s);
+void sub(const Context& c, const uint64_t* a, const uint64_t* b, uint64_t* o, int64_t words, int nl, cudaStream_t s);
+void negate(const Context& c, const uint64_t* a, uint64_t* o, int64_t words, int nl, cudaStream_t s);
+// per-item plaintext applied to poly 0: o[item][0] = a[item][0] (+/-) pt[item or 0]; other polys copied
+void add_plain(const Context& c, const uint64_t* ct, const uint64_t* pt, uint64_t* o, int64_t items, int size, int nl,
+               bool pt_per_item, bool subtract, cudaStream_t s);
+// every poly of every item times a plaintext (per-item or shared)
+void mul_plain(const Context& c, const uint64_t* ct, const uint64_t* pt, uint64_t* o, int64_t items, int size, int nl,
+               bool pt_per_item, cudaStream_t s);
+// every poly times a per-limb scalar residue (encode_constant in NTT form)
+void mul_scalar(const Context& c, const uint64_t* ct, const uint64_t* w, uint64_t* o, int64_t items, int size, int nl,
+                cudaStream_t s);
+// rescale `polys` polys from nl to nl-1 limbs (poly.hpp:190-228); scratch int64 [polys][N]
+void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys, int nl, int64_t* scratch,
+             cudaStream_t s);
+// drop limbs: copy first nl_out limbs of each poly
+void mod_switch(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys, int nl_in, int nl_out,
+                cudaStream_t s);
+// weighted sum over groups sharing an input list (Dot: one group; Conv: one per position).
+//  out[g*mg + m][p][j] = sum_t w[((g*mg+m)*kt + t)*nl + j] * x[idx[g*kt + t]][p][j]  (before rescale)
+void gemm_groups(const Context& c, const uint64_t* x, const int32_t* idx, const uint64_t* w, uint64_t* out,
+                 int64_t groups, int mg, int kt, int nl, cudaStream_t s);
+// tensor square + relinearize: in [items][2][nl][N] -> out [items][2][nl][N] (un-rescaled), scratch c2 [items][nl][N]
+void square_relin(const Context& c, const Keys& keys, const uint64_t* in, uint64_t* out, int64_t items, int nl,
+                  uint64_t* c2scratch, cudaStream_t s);
+// general ct x ct (size 2 each) tensor + relin
+void mul_relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, uint64_t* out, int64_t items,
+               int nl, uint64_t* c2scratch, cudaStream_t s);
+// tensor only: out [items][3][nl][N]
+void mul_tensor(const Context& c, const uint64_t* a, const uint64_t* b, uint64_t* out, int64_t items, int nl,
+                cudaStream_t s);
+// relinearize size-3 items -> size-2
+void relin3(const Context& c, const Keys& keys, const uint64_t* in3, uint64_t* out2, int64_t items, int nl,
+            uint64_t* c2scratch, cudaStream_t s);
+// fresh encryption from host samples (int64 [items][3][N]: u, e0, e1) at nl limbs; optional plaintext per item
+void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const uint64_t* pt, uint64_t* out,
+             int64_t items, int nl, cudaStream_t s);
+// decrypt to coefficient-domain m (items x nl x N)
+void decrypt(const Context& c, const Keys& keys, const uint64_t* ct, uint64_t* m, int64_t items, int size, int nl,
+             cudaStream_t s);
+// gather whole items: out[i] = in[idx[i]] (item_words each)
+void gather_items(const uint64_t* in, const int32_t* idx, uint64_t* out, int64_t items, int64_t item_words,
+                  cudaStream_t s);
+// keygen pointwise: out = -(a*s + e) (+ f*s^2 on limb `special` if special >= 0)
+void keygen_b(const Context& c, const uint64_t* a, const uint64_t* sk, const uint64_t* e, uint64_t* out, int nl,
+              int special, uint64_t f, cudaStream_t s);
+}  // namespace k
+
+}  // namespace hg

@@ -1,0 +1,851 @@
+// hg_kernels.cu -- sm_100a kernels for the CKKS/RNS ciphertext hot path.
+//
+// Reference functions restated (paths relative to proj/include/heg/):
+//   NTT forward/inverse            ckks/ring.hpp:263-301
+//   poly add/sub/negate/mul(_acc)  ckks/poly.hpp:87-170
+//   poly_rescale                   ckks/poly.hpp:190-228
+//   relinearize                    ckks/ckks_backend.hpp:508-554
+//   multiply (tensor)              ckks/ckks_backend.hpp:261-281
+//   weighted_sum (fused Dot/Conv)  ckks/ckks_backend.hpp:381-411, runtime.hpp:532-569
+//   fresh_encryption / decrypt     ckks/ckks_backend.hpp:470-490, 238-249
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "hg_device.cuh"
+#include "hg_internal.hpp"
+#include "hg_ntt.cuh"
+
+namespace hg {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(HG_ECUDA, std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+namespace {
+
+constexpr int kNttThreads = 256;
+
+inline int ew_blocks(int64_t work, int threads) {
+  int64_t b = (work + threads - 1) / threads;
+  if (b > (int64_t)148 * 32) b = (int64_t)148 * 32;  // grid-stride beyond 32 CTAs/SM
+  return (int)(b < 1 ? 1 : b);
+}
+
+// --------------------------------------------------------------------------
+// Batched NTT over limb rows
+// --------------------------------------------------------------------------
+template <bool INV>
+__global__ void __launch_bounds__(kNttThreads) k_ntt(uint64_t* __restrict__ base, int nl, const CtxParams P) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  const int64_t row = blockIdx.x;
+  const int limb = (int)(row % nl);
+  uint64_t* g = base + row * P.n;
+  const LimbInfo& L = P.limb[limb];
+  const int n = (int)P.n;
+  if (L.small) {
+    uint32_t* s = reinterpret_cast<uint32_t*>(smem);
+    load_limb(s, g, n);
+    __syncthreads();
+    if (INV) ntt_inverse_smem(s, L, P.logn);
+    else ntt_forward_smem(s, L, P.logn);
+    store_limb(g, s, n);
+  } else {
+    load_limb(smem, g, n);
+    __syncthreads();
+    if (INV) ntt_inverse_smem(smem, L, P.logn);
+    else ntt_forward_smem(smem, L, P.logn);
+    store_limb(g, smem, n);
+  }
+}
+
+// lift signed coefficients (one poly per item) into every limb, then NTT
+__global__ void __launch_bounds__(kNttThreads) k_lift_ntt(const int64_t* __restrict__ src, uint64_t* __restrict__ out,
+                                                          int nl, const CtxParams P) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  const int64_t item = blockIdx.x / nl;
+  const int limb = (int)(blockIdx.x % nl);
+  const LimbInfo& L = P.limb[limb];
+  const int n = (int)P.n;
+  const int64_t* g = src + item * P.n;
+  uint64_t* o = out + (int64_t)blockIdx.x * P.n;
+  if (L.small) {
+    uint32_t* s = reinterpret_cast<uint32_t*>(smem);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s[swz<uint32_t>(i)] = (uint32_t)lift_signed(g[i], L.q);
+    __syncthreads();
+    ntt_forward_smem(s, L, P.logn);
+    store_limb(o, s, n);
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) smem[swz<uint64_t>(i)] = lift_signed(g[i], L.q);
+    __syncthreads();
+    ntt_forward_smem(smem, L, P.logn);
+    store_limb(o, smem, n);
+  }
+}
+
+// --------------------------------------------------------------------------
+// Elementwise (poly.hpp:87-152)
+// --------------------------------------------------------------------------
+template <int OP>  // 0 add, 1 sub, 2 negate
+__global__ void k_elementwise(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, uint64_t* __restrict__ o,
+                              int64_t words, int nl, const CtxParams P) {
+  const int64_t n = P.n;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t q = P.limb[(w / n) % nl].q;
+    const uint64_t x = a[w];
+    if (OP == 0) o[w] = add_mod(x, b[w], q);
+    else if (OP == 1) o[w] = sub_mod(x, b[w], q);
+    else o[w] = neg_mod(x, q);
+  }
+}
+
+// ct (+/-) pt on poly 0 (ckks_backend.hpp:580-589); other polys copied
+__global__ void k_add_plain(const uint64_t* __restrict__ ct, const uint64_t* __restrict__ pt, uint64_t* __restrict__ o,
+                            int64_t items, int size, int nl, int pt_per_item, int subtract, const CtxParams P) {
+  const int64_t n = P.n;
+  const int64_t poly_words = nl * n;
+  const int64_t words = items * size * poly_words;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t item = w / (size * poly_words);
+    const int64_t r = w - item * size * poly_words;
+    const int p = (int)(r / poly_words);
+    const int64_t lw = r - p * poly_words;
+    const uint64_t x = ct[w];
+    if (p == 0) {
+      const uint64_t q = P.limb[lw / n].q;
+      const uint64_t y = pt[(pt_per_item ? item * poly_words : 0) + lw];
+      o[w] = subtract ? sub_mod(x, y, q) : add_mod(x, y, q);
+    } else {
+      o[w] = x;
+    }
+  }
+}
+
+// every poly times plaintext (ckks_backend.hpp:299-310, poly_mul NTT branch poly.hpp:130-136)
+__global__ void k_mul_plain(const uint64_t* __restrict__ ct, const uint64_t* __restrict__ pt, uint64_t* __restrict__ o,
+                            int64_t items, int size, int nl, int pt_per_item, const CtxParams P) {
+  const int64_t n = P.n;
+  const int64_t poly_words = nl * n;
+  const int64_t words = items * size * poly_words;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t item = w / (size * poly_words);
+    const int64_t lw = (w - item * size * poly_words) % poly_words;
+    const LimbInfo& L = P.limb[lw / n];
+    o[w] = mul_mod(ct[w], pt[(pt_per_item ? item * poly_words : 0) + lw], L);
+  }
+}
+
+// every poly times a per-limb scalar (encode_constant in NTT form: ckks_backend.hpp:199-216)
+__global__ void k_mul_scalar(const uint64_t* __restrict__ ct, const uint64_t* __restrict__ wl, uint64_t* __restrict__ o,
+                             int64_t words, int nl, const CtxParams P) {
+  const int64_t n = P.n;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
+    const int limb = (int)((w / n) % nl);
+    o[w] = mul_mod(ct[w], wl[limb], P.limb[limb]);
+  }
+}
+
+// --------------------------------------------------------------------------
+// Rescale (poly.hpp:190-228)
+// --------------------------------------------------------------------------
+struct RescaleK {
+  uint64_t inv[HG_MAX_LIMBS];
+  uint64_t inv_s[HG_MAX_LIMBS];
+};
+
+// step 1: INTT of the top limb, centred lift into int64 scratch
+__global__ void __launch_bounds__(kNttThreads) k_rescale_top(const uint64_t* __restrict__ in, int64_t* __restrict__ cen,
+                                                             int nl, const CtxParams P) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  const int64_t poly = blockIdx.x;
+  const int t = nl - 1;
+  const LimbInfo& L = P.limb[t];
+  const int n = (int)P.n;
+  const uint64_t* g = in + (poly * nl + t) * P.n;
+  int64_t* c = cen + poly * P.n;
+  const uint64_t half = L.q / 2;
+  if (L.small) {
+    uint32_t* s = reinterpret_cast<uint32_t*>(smem);
+    load_limb(s, g, n);
+    __syncthreads();
+    ntt_inverse_smem(s, L, P.logn);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint64_t v = s[swz<uint32_t>(i)];
+      c[i] = v > half ? (int64_t)v - (int64_t)L.q : (int64_t)v;
+    }
+  } else {
+    load_limb(smem, g, n);
+    __syncthreads();
+    ntt_inverse_smem(smem, L, P.logn);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint64_t v = smem[swz<uint64_t>(i)];
+      c[i] = v > half ? (int64_t)v - (int64_t)L.q : (int64_t)v;
+    }
+  }
+}
+
+// step 2: per remaining limb j: corr = NTT_j(lift(c)); out = (x - corr) * q_t^{-1}
+__global__ void __launch_bounds__(kNttThreads) k_rescale_rest(const uint64_t* __restrict__ in,
+                                                              const int64_t* __restrict__ cen,
+                                                              uint64_t* __restrict__ out, int nl, const RescaleK R,
+                                                              const CtxParams P) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  const int t = nl - 1;
+  const int64_t poly = blockIdx.x / t;
+  const int j = (int)(blockIdx.x % t);
+  const LimbInfo& L = P.limb[j];
+  const int n = (int)P.n;
+  const int64_t* c = cen + poly * P.n;
+  const uint64_t* x = in + (poly * nl + j) * P.n;
+  uint64_t* o = out + (poly * t + j) * P.n;
+  const uint64_t inv = R.inv[j], inv_s = R.inv_s[j];
+  if (L.small) {
+    uint32_t* s = reinterpret_cast<uint32_t*>(smem);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s[swz<uint32_t>(i)] = (uint32_t)lift_signed(c[i], L.q);
+    __syncthreads();
+    ntt_forward_smem(s, L, P.logn);
+    const uint32_t q = (uint32_t)L.q, w = (uint32_t)inv, ws = (uint32_t)(inv_s >> 32);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint32_t xv = (uint32_t)x[i], cv = s[swz<uint32_t>(i)];
+      const uint32_t d = xv >= cv ? xv - cv : xv + q - cv;
+      o[i] = mul_shoup32(d, w, ws, q);
+    }
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) smem[swz<uint64_t>(i)] = lift_signed(c[i], L.q);
+    __syncthreads();
+    ntt_forward_smem(smem, L, P.logn);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint64_t d = sub_mod(x[i], smem[swz<uint64_t>(i)], L.q);
+      o[i] = mul_shoup64(d, inv, inv_s, L.q);
+    }
+  }
+}
+
+__global__ void k_mod_switch(const uint64_t* __restrict__ in, uint64_t* __restrict__ out, int64_t polys, int nl_in,
+                             int nl_out, int64_t n) {
+  const int64_t words = polys * nl_out * n;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = w / (nl_out * n);
+    const int64_t r = w - p * nl_out * n;
+    out[w] = in[p * nl_in * n + r];
+  }
+}
+
+// --------------------------------------------------------------------------
+// Grouped modular GEMM for Dot/Conv (weighted_sum before its rescale).
+// Grid: x = column tiles of N, y = (poly, limb) rows, z = (group, m-tile).
+// --------------------------------------------------------------------------
+constexpr int kGemmThreads = 256;
+constexpr int kGemmKC = 32;  // terms staged per chunk
+
+template <int MT>
+__global__ void __launch_bounds__(kGemmThreads) k_gemm_groups(const uint64_t* __restrict__ x,
+                                                              const int32_t* __restrict__ idx,
+                                                              const uint64_t* __restrict__ w,
+                                                              uint64_t* __restrict__ out, int mg, int kt, int nl,
+                                                              const CtxParams P) {
+  __shared__ uint64_t ws[kGemmKC][MT];
+  __shared__ int32_t xs[kGemmKC];
+  const int64_t n = P.n;
+  const int mtiles = (mg + MT - 1) / MT;
+  const int64_t g = blockIdx.z / mtiles;
+  const int m0 = (int)(blockIdx.z % mtiles) * MT;
+  const int pj = blockIdx.y;  // p * nl + j
+  const int j = pj % nl;
+  const int64_t col = (int64_t)blockIdx.x * kGemmThreads + threadIdx.x;
+  const LimbInfo& L = P.limb[j];
+  const int64_t item_words = 2 * nl * n;
+  const uint64_t* xcol = x + (int64_t)pj * n + col;
+
+  Acc128 acc[MT];
+#pragma unroll
+  for (int m = 0; m < MT; ++m) acc[m].zero();
+
+  for (int t0 = 0; t0 < kt; t0 += kGemmKC) {
+    const int tc = min(kGemmKC, kt - t0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kGemmKC * MT; e += kGemmThreads) {
+      const int tt = e / MT, m = e % MT;
+      uint64_t v = 0;
+      if (tt < tc && m0 + m < mg) v = w[(((g * mg + m0 + m) * kt) + t0 + tt) * nl + j];
+      ws[tt][m] = v;
+    }
+    if (threadIdx.x < kGemmKC) xs[threadIdx.x] = threadIdx.x < tc ? idx[g * kt + t0 + threadIdx.x] : 0;
+    __syncthreads();
+    if (col < n) {
+      if (L.small) {
+        for (int tt = 0; tt < tc; ++tt) {
+          const uint32_t xv = (uint32_t)__ldg(xcol + (int64_t)xs[tt] * item_words);
+#pragma unroll
+          for (int m = 0; m < MT; ++m) acc[m].mac32(xv, (uint32_t)ws[tt][m]);
+        }
+      } else {
+        for (int tt = 0; tt < tc; ++tt) {
+          const uint64_t xv = __ldg(xcol + (int64_t)xs[tt] * item_words);
+#pragma unroll
+          for (int m = 0; m < MT; ++m) acc[m].mac(xv, ws[tt][m]);
+        }
+      }
+    }
+  }
+  if (col < n) {
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      if (m0 + m < mg) out[((g * mg + m0 + m) * 2 * nl + pj) * n + col] = reduce128(acc[m].lo, acc[m].hi, L);
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// Tensor product + relinearisation (ckks_backend.hpp:261-281, 508-554)
+// --------------------------------------------------------------------------
+
+// c2 of a product in coefficient form: d2 = a1 * b1 (NTT) -> INTT.  One CTA per (item, limb i).
+__global__ void __launch_bounds__(kNttThreads) k_relin_c2(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
+                                                          int64_t a_stride, int64_t b_stride, int64_t a1_off,
+                                                          int64_t b1_off, uint64_t* __restrict__ c2, int nl,
+                                                          const CtxParams P) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  const int64_t item = blockIdx.x / nl;
+  const int i = (int)(blockIdx.x % nl);
+  const LimbInfo& L = P.limb[i];
+  const int n = (int)P.n;
+  const uint64_t* x1 = a + item * a_stride + a1_off + (int64_t)i * n;
+  const uint64_t* y1 = b + item * b_stride + b1_off + (int64_t)i * n;
+  uint64_t* o = c2 + (item * nl + i) * P.n;
+  if (L.small) {
+    uint32_t* s = reinterpret_cast<uint32_t*>(smem);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) s[swz<uint32_t>(k)] = (uint32_t)mul_mod(x1[k], y1[k], L);
+    __syncthreads();
+    ntt_inverse_smem(s, L, P.logn);
+    store_limb(o, s, n);
+  } else {
+    for (int k = threadIdx.x; k < n; k += blockDim.x) smem[swz<uint64_t>(k)] = mul_mod(x1[k], y1[k], L);
+    __syncthreads();
+    ntt_inverse_smem(smem, L, P.logn);
+    store_limb(o, smem, n);
+  }
+}
+
+// Relinearise one (item, target limb j): acc_{0,1} = d_{0,1} + sum_{i<=l, d<D_i} NTT_j(digit_{i,d}(c2_i)) * key_{i,d}[j].
+// The forward NTT runs its remainder pass first so the last radix-16 pass leaves
+// 16 consecutive evaluations in each thread's registers; the key MAC is fused
+// into that pass and the accumulators never leave registers (N <= 8192) or
+// accumulate in the L2-resident output (N >= 16384).
+struct RelinK {
+  int rows0[HG_MAX_LIMBS];   // first relin row of source limb i
+  int digits[HG_MAX_LIMBS];  // D_i
+  int64_t key_limb_stride;   // words between limbs of one key poly = N
+  int64_t key_poly_words;    // (L+1) N
+};
+
+template <typename W, bool REGACC>
+__device__ void relin_body(W* s, const uint64_t* __restrict__ c2item, const uint64_t* __restrict__ keys,
+                           const RelinK& K, int j, int nl, const LimbInfo& L, int logn, uint64_t* acc_g0,
+                           uint64_t* acc_g1, uint64_t (&acc0)[16], uint64_t (&acc1)[16]) {
+  const int n = 1 << logn;
+  const int rem = logn & 3;
+  const uint64_t q = L.q;
+  const uint64_t qm63 = (uint64_t(1) << 63) / q * q;  // largest multiple of q <= 2^63
+  for (int i = 0; i < nl; ++i) {
+    const uint64_t* src = c2item + (int64_t)i * n;
+    for (int d = 0; d < K.digits[i]; ++d) {
+      const int row = K.rows0[i] + d;
+      const int sh = 15 * d;
+      // stage the digit (coefficient form, < 2^15 < q_j: canonical)
+      for (int k = threadIdx.x; k < n; k += blockDim.x) s[swz<W>(k)] = (W)((src[k] >> sh) & 0x7FFF);
+      __syncthreads();
+      // remainder pass first, then radix-16 passes except the last
+      int s0 = 0;
+      switch (rem) {
+        case 3: fwd_pass<W, 3>(s, L, logn, 0); __syncthreads(); break;
+        case 2: fwd_pass<W, 2>(s, L, logn, 0); __syncthreads(); break;
+        case 1: fwd_pass<W, 1>(s, L, logn, 0); __syncthreads(); break;
+        default: break;
+      }
+      s0 = rem;
+      for (; s0 + 4 < logn; s0 += 4) {
+        fwd_pass<W, 4>(s, L, logn, s0);
+        __syncthreads();
+      }
+      // last pass (s0 = logn - 4): thread vt owns elements 16 vt .. 16 vt + 15
+      const uint64_t* kb = keys + (int64_t)row * 2 * K.key_poly_words + (int64_t)j * n;
+      const uint64_t* ka = kb + K.key_poly_words;
+      for (int vt = threadIdx.x, it = 0; vt < (n >> 4); vt += blockDim.x, ++it) {
+        const int base = vt << 4;
+        W x[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) x[r] = s[swz<W>(base + r)];
+#pragma unroll
+        for (int st = 0; st < 4; ++st) {
+          const int hd = 16 >> (st + 1);
+          const int m = 1 << (s0 + st);
+          const int gshift = logn - s0 - st;
+#pragma unroll
+          for (int r = 0; r < 16; ++r) {
+            if (r & hd) continue;
+            const auto w = Tw<W>::fwd(L, m + ((base + r) >> gshift));
+            ct_bfly(x[r], x[r + hd], w, (W)q);
+          }
+        }
+        const ulonglong2* kb2 = reinterpret_cast<const ulonglong2*>(kb + base);
+        const ulonglong2* ka2 = reinterpret_cast<const ulonglong2*>(ka + base);
+#pragma unroll
+        for (int r2 = 0; r2 < 8; ++r2) {
+          const ulonglong2 vb = __ldg(kb2 + r2), va = __ldg(ka2 + r2);
+          const uint64_t e0 = (uint64_t)x[2 * r2], e1 = (uint64_t)x[2 * r2 + 1];
+          if (REGACC) {
+            if (sizeof(W) == 4) {
+              // products < 2^62; keep accumulators below 2^63 by folding a multiple of q
+              uint64_t t;
+              t = acc0[2 * r2] + e0 * vb.x; acc0[2 * r2] = t >= (1ull << 63) ? t - qm63 : t;
+              t = acc0[2 * r2 + 1] + e1 * vb.y; acc0[2 * r2 + 1] = t >= (1ull << 63) ? t - qm63 : t;
+              t = acc1[2 * r2] + e0 * va.x; acc1[2 * r2] = t >= (1ull << 63) ? t - qm63 : t;
+              t = acc1[2 * r2 + 1] + e1 * va.y; acc1[2 * r2 + 1] = t >= (1ull << 63) ? t - qm63 : t;
+            } else {
+              acc0[2 * r2] = add_mod(acc0[2 * r2], mul_mod(e0, vb.x, L), q);
+              acc0[2 * r2 + 1] = add_mod(acc0[2 * r2 + 1], mul_mod(e1, vb.y, L), q);
+              acc1[2 * r2] = add_mod(acc1[2 * r2], mul_mod(e0, va.x, L), q);
+              acc1[2 * r2 + 1] = add_mod(acc1[2 * r2 + 1], mul_mod(e1, va.y, L), q);
+            }
+          } else {
+            const int k0 = base + 2 * r2;
+            acc_g0[k0] = add_mod(acc_g0[k0], mul_mod(e0, vb.x, L), q);
+            acc_g0[k0 + 1] = add_mod(acc_g0[k0 + 1], mul_mod(e1, vb.y, L), q);
+            acc_g1[k0] = add_mod(acc_g1[k0], mul_mod(e0, va.x, L), q);
+            acc_g1[k0 + 1] = add_mod(acc_g1[k0 + 1], mul_mod(e1, va.y, L), q);
+          }
+        }
+        (void)it;
+      }
+      __syncthreads();  // smem reused by the next digit
+    }
+  }
+}
+
+// One CTA per (item, limb j).  d0/d1 come from the tensor product of (a, b):
+// d0 = a0 b0, d1 = a0 b1 + a1 b0 (ckks_backend.hpp:270-271).
+template <bool REGACC>
+__global__ void __launch_bounds__(512, 1)
+    k_relin(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int64_t a_stride, int64_t b_stride,
+            const uint64_t* __restrict__ c2, const uint64_t* __restrict__ keys, uint64_t* __restrict__ out, int nl,
+            const RelinK K, const CtxParams P) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  const int64_t item = blockIdx.x / nl;
+  const int j = (int)(blockIdx.x % nl);
+  const LimbInfo& L = P.limb[j];
+  const int n = (int)P.n;
+  const int64_t pw = (int64_t)nl * n;
+  const uint64_t* c2item = c2 + item * pw;
+  uint64_t* o0 = out + item * 2 * pw + (int64_t)j * n;
+  uint64_t* o1 = o0 + pw;
+  const uint64_t* a0 = a + item * a_stride + (int64_t)j * n;
+  const uint64_t* a1 = a0 + pw;
+  const uint64_t* b0 = b + item * b_stride + (int64_t)j * n;
+  const uint64_t* b1 = b0 + pw;
+  uint64_t acc0[16], acc1[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) { acc0[r] = 0; acc1[r] = 0; }
+  if (!REGACC) {
+    for (int k = threadIdx.x; k < n; k += blockDim.x) { o0[k] = 0; o1[k] = 0; }
+    __syncthreads();
+  }
+  if (L.small) relin_body<uint32_t, REGACC>(reinterpret_cast<uint32_t*>(smem), c2item, keys, K, j, nl, L, P.logn, o0, o1, acc0, acc1);
+  else relin_body<uint64_t, REGACC>(smem, c2item, keys, K, j, nl, L, P.logn, o0, o1, acc0, acc1);
+  // epilogue: + d0, d1; canonical store
+  const uint64_t q = L.q;
+  if (REGACC) {
+    for (int vt = threadIdx.x; vt < (n >> 4); vt += blockDim.x) {
+      const int base = vt << 4;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const int k = base + r;
+        uint64_t r0 = acc0[r], r1 = acc1[r];
+        if (L.small) { r0 = reduce128(r0, 0, L); r1 = reduce128(r1, 0, L); }
+        const uint64_t x0 = a0[k], x1 = a1[k], y0 = b0[k], y1 = b1[k];
+        const uint64_t d0 = mul_mod(x0, y0, L);
+        const uint64_t d1 = add_mod(mul_mod(x0, y1, L), mul_mod(x1, y0, L), q);
+        o0[k] = add_mod(r0, d0, q);
+        o1[k] = add_mod(r1, d1, q);
+      }
+    }
+  } else {
+    __syncthreads();
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      const uint64_t x0 = a0[k], x1 = a1[k], y0 = b0[k], y1 = b1[k];
+      const uint64_t d0 = mul_mod(x0, y0, L);
+      const uint64_t d1 = add_mod(mul_mod(x0, y1, L), mul_mod(x1, y0, L), q);
+      o0[k] = add_mod(o0[k], d0, q);
+      o1[k] = add_mod(o1[k], d1, q);
+    }
+  }
+}
+
+// relinearise a size-3 input: d0, d1 given directly (no tensor product)
+template <bool REGACC>
+__global__ void __launch_bounds__(512, 1)
+    k_relin3(const uint64_t* __restrict__ in3, const uint64_t* __restrict__ c2, const uint64_t* __restrict__ keys,
+             uint64_t* __restrict__ out, int nl, const RelinK K, const CtxParams P) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  const int64_t item = blockIdx.x / nl;
+  const int j = (int)(blockIdx.x % nl);
+  const LimbInfo& L = P.limb[j];
+  const int n = (int)P.n;
+  const int64_t pw = (int64_t)nl * n;
+  const uint64_t* c2item = c2 + item * pw;
+  uint64_t* o0 = out + item * 2 * pw + (int64_t)j * n;
+  uint64_t* o1 = o0 + pw;
+  const uint64_t* d0p = in3 + item * 3 * pw + (int64_t)j * n;
+  const uint64_t* d1p = d0p + pw;
+  uint64_t acc0[16], acc1[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) { acc0[r] = 0; acc1[r] = 0; }
+  if (!REGACC) {
+    for (int k = threadIdx.x; k < n; k += blockDim.x) { o0[k] = 0; o1[k] = 0; }
+    __syncthreads();
+  }
+  if (L.small) relin_body<uint32_t, REGACC>(reinterpret_cast<uint32_t*>(smem), c2item, keys, K, j, nl, L, P.logn, o0, o1, acc0, acc1);
+  else relin_body<uint64_t, REGACC>(smem, c2item, keys, K, j, nl, L, P.logn, o0, o1, acc0, acc1);
+  const uint64_t q = L.q;
+  if (REGACC) {
+    for (int vt = threadIdx.x; vt < (n >> 4); vt += blockDim.x) {
+      const int base = vt << 4;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const int k = base + r;
+        uint64_t r0 = acc0[r], r1 = acc1[r];
+        if (L.small) { r0 = reduce128(r0, 0, L); r1 = reduce128(r1, 0, L); }
+        o0[k] = add_mod(r0, d0p[k], q);
+        o1[k] = add_mod(r1, d1p[k], q);
+      }
+    }
+  } else {
+    __syncthreads();
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      o0[k] = add_mod(o0[k], d0p[k], q);
+      o1[k] = add_mod(o1[k], d1p[k], q);
+    }
+  }
+}
+
+// tensor only: (d0, d1, d2)
+__global__ void k_tensor(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, uint64_t* __restrict__ out,
+                         int64_t items, int nl, const CtxParams P) {
+  const int64_t n = P.n, pw = nl * n;
+  const int64_t words = items * pw;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t item = w / pw, lw = w - item * pw;
+    const LimbInfo& L = P.limb[lw / n];
+    const uint64_t x0 = a[item * 2 * pw + lw], x1 = a[item * 2 * pw + pw + lw];
+    const uint64_t y0 = b[item * 2 * pw + lw], y1 = b[item * 2 * pw + pw + lw];
+    uint64_t* o = out + item * 3 * pw + lw;
+    o[0] = mul_mod(x0, y0, L);
+    o[pw] = add_mod(mul_mod(x0, y1, L), mul_mod(x1, y0, L), L.q);
+    o[2 * pw] = mul_mod(x1, y1, L);
+  }
+}
+
+// --------------------------------------------------------------------------
+// Encryption / decryption / keygen pointwise kernels
+// --------------------------------------------------------------------------
+// ntt3: [items][3][nl][N] (u, e0, e1 in NTT form) -> out [items][2][nl][N]
+__global__ void k_encrypt_combine(const uint64_t* __restrict__ ntt3, const uint64_t* __restrict__ pk,
+                                  const uint64_t* __restrict__ pt, uint64_t* __restrict__ out, int64_t items, int nl,
+                                  int64_t key_poly_words, const CtxParams P) {
+  const int64_t n = P.n, pw = nl * n;
+  const int64_t words = items * pw;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t item = w / pw, lw = w - item * pw;
+    const LimbInfo& L = P.limb[lw / n];
+    const uint64_t u = ntt3[item * 3 * pw + lw];
+    const uint64_t e0 = ntt3[item * 3 * pw + pw + lw];
+    const uint64_t e1 = ntt3[item * 3 * pw + 2 * pw + lw];
+    uint64_t c0 = add_mod(mul_mod(pk[lw], u, L), e0, L.q);
+    if (pt) c0 = add_mod(c0, pt[item * pw + lw], L.q);
+    const uint64_t c1 = add_mod(mul_mod(pk[key_poly_words + lw], u, L), e1, L.q);
+    out[item * 2 * pw + lw] = c0;
+    out[item * 2 * pw + pw + lw] = c1;
+  }
+}
+
+// m = c0 + c1 s + c2 s^2 (+...) (ckks_backend.hpp:238-247), NTT form
+__global__ void k_decrypt_dot(const uint64_t* __restrict__ ct, const uint64_t* __restrict__ sk, uint64_t* __restrict__ m,
+                              int64_t items, int size, int nl, const CtxParams P) {
+  const int64_t n = P.n, pw = nl * n;
+  const int64_t words = items * pw;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t item = w / pw, lw = w - item * pw;
+    const LimbInfo& L = P.limb[lw / n];
+    const uint64_t s = sk[lw];
+    uint64_t acc = ct[item * size * pw + lw];
+    uint64_t sp = s;
+    for (int j = 1; j < size; ++j) {
+      if (j > 1) sp = mul_mod(sp, s, L);
+      acc = add_mod(acc, mul_mod(ct[item * size * pw + j * pw + lw], sp, L), L.q);
+    }
+    m[w] = acc;
+  }
+}
+
+__global__ void k_keygen_b(const uint64_t* __restrict__ a, const uint64_t* __restrict__ sk,
+                           const uint64_t* __restrict__ e, uint64_t* __restrict__ out, int nl, int special, uint64_t f,
+                           uint64_t fs, const CtxParams P) {
+  const int64_t n = P.n, words = nl * n;
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
+    const int limb = (int)(w / n);
+    const LimbInfo& L = P.limb[limb];
+    const uint64_t s = sk[w];
+    uint64_t v = neg_mod(add_mod(mul_mod(a[w], s, L), e[w], L.q), L.q);
+    if (limb == special) {
+      const uint64_t s2 = mul_mod(s, s, L);
+      v = add_mod(v, mul_shoup64(s2, f, fs, L.q), L.q);
+    }
+    out[w] = v;
+  }
+}
+
+__global__ void k_gather_items(const uint64_t* __restrict__ in, const int32_t* __restrict__ idx,
+                               uint64_t* __restrict__ out, int64_t items, int64_t item_words) {
+  const int64_t vec = item_words / 2;
+  const int64_t total = items * vec;
+  const ulonglong2* in2 = reinterpret_cast<const ulonglong2*>(in);
+  ulonglong2* out2 = reinterpret_cast<ulonglong2*>(out);
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t it = w / vec, r = w - it * vec;
+    out2[w] = in2[(int64_t)idx[it] * vec + r];
+  }
+}
+
+}  // namespace
+
+// ==========================================================================
+// launchers
+// ==========================================================================
+namespace k {
+
+static size_t limb_smem(const Context& c) { return (size_t)c.n() * sizeof(uint64_t); }
+
+static void set_smem(const void* fn, size_t bytes) {
+  static std::map<const void*, size_t> done;
+  auto it = done.find(fn);
+  if (it != done.end() && it->second >= bytes) return;
+  HG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  done[fn] = bytes;
+}
+
+void ntt(const Context& c, uint64_t* base, int64_t rows, int nl, bool inverse, cudaStream_t s) {
+  if (rows <= 0) return;
+  const size_t sm = limb_smem(c);
+  if (inverse) {
+    set_smem((const void*)k_ntt<true>, sm);
+    k_ntt<true><<<(unsigned)rows, kNttThreads, sm, s>>>(base, nl, c.kp());
+  } else {
+    set_smem((const void*)k_ntt<false>, sm);
+    k_ntt<false><<<(unsigned)rows, kNttThreads, sm, s>>>(base, nl, c.kp());
+  }
+  HG_CUDA(cudaGetLastError());
+}
+
+void lift_ntt(const Context& c, const int64_t* src, uint64_t* out, int64_t count, int nl, cudaStream_t s) {
+  if (count <= 0) return;
+  const size_t sm = limb_smem(c);
+  set_smem((const void*)k_lift_ntt, sm);
+  k_lift_ntt<<<(unsigned)(count * nl), kNttThreads, sm, s>>>(src, out, nl, c.kp());
+  HG_CUDA(cudaGetLastError());
+}
+
+void add(const Context& c, const uint64_t* a, const uint64_t* b, uint64_t* o, int64_t words, int nl, cudaStream_t s) {
+  if (words <= 0) return;
+  k_elementwise<0><<<ew_blocks(words, 256), 256, 0, s>>>(a, b, o, words, nl, c.kp());
+  HG_CUDA(cudaGetLastError());
+}
+void sub(const Context& c, const uint64_t* a, const uint64_t* b, uint64_t* o, int64_t words, int nl, cudaStream_t s) {
+  if (words <= 0) return;
+  k_elementwise<1><<<ew_blocks(words, 256), 256, 0, s>>>(a, b, o, words, nl, c.kp());
+  HG_CUDA(cudaGetLastError());
+}
+void negate(const Context& c, const uint64_t* a, uint64_t* o, int64_t words, int nl, cudaStream_t s) {
+  if (words <= 0) return;
+  k_elementwise<2><<<ew_blocks(words, 256), 256, 0, s>>>(a, nullptr, o, words, nl, c.kp());
+  HG_CUDA(cudaGetLastError());
+}
+void add_plain(const Context& c, const uint64_t* ct, const uint64_t* pt, uint64_t* o, int64_t items, int size, int nl,
+               bool per_item, bool subtract, cudaStream_t s) {
+  const int64_t words = items * size * nl * c.n();
+  if (words <= 0) return;
+  k_add_plain<<<ew_blocks(words, 256), 256, 0, s>>>(ct, pt, o, items, size, nl, per_item, subtract, c.kp());
+  HG_CUDA(cudaGetLastError());
+}
+void mul_plain(const Context& c, const uint64_t* ct, const uint64_t* pt, uint64_t* o, int64_t items, int size, int nl,
+               bool per_item, cudaStream_t s) {
+  const int64_t words = items * size * nl * c.n();
+  if (words <= 0) return;
+  k_mul_plain<<<ew_blocks(words, 256), 256, 0, s>>>(ct, pt, o, items, size, nl, per_item, c.kp());
+  HG_CUDA(cudaGetLastError());
+}
+void mul_scalar(const Context& c, const uint64_t* ct, const uint64_t* w, uint64_t* o, int64_t items, int size, int nl,
+                cudaStream_t s) {
+  const int64_t words = items * size * nl * c.n();
+  if (words <= 0) return;
+  k_mul_scalar<<<ew_blocks(words, 256), 256, 0, s>>>(ct, w, o, words, nl, c.kp());
+  HG_CUDA(cudaGetLastError());
+}
+
+void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys, int nl, int64_t* scratch,
+             cudaStream_t s) {
+  check(nl >= 2, HG_EINTERNAL, "rescale needs at least two active moduli");
+  if (polys <= 0) return;
+  const size_t sm = limb_smem(c);
+  set_smem((const void*)k_rescale_top, sm);
+  set_smem((const void*)k_rescale_rest, sm);
+  RescaleK R{};
+  const int t = nl - 1;
+  for (int j = 0; j < t; ++j) {
+    R.inv[j] = c.inv_q(t, j);
+    R.inv_s[j] = c.inv_q_shoup(t, j);
+  }
+  k_rescale_top<<<(unsigned)polys, kNttThreads, sm, s>>>(in, scratch, nl, c.kp());
+  HG_CUDA(cudaGetLastError());
+  k_rescale_rest<<<(unsigned)(polys * t), kNttThreads, sm, s>>>(in, scratch, out, nl, R, c.kp());
+  HG_CUDA(cudaGetLastError());
+}
+
+void mod_switch(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys, int nl_in, int nl_out,
+                cudaStream_t s) {
+  const int64_t words = polys * nl_out * c.n();
+  if (words <= 0) return;
+  k_mod_switch<<<ew_blocks(words, 256), 256, 0, s>>>(in, out, polys, nl_in, nl_out, c.n());
+  HG_CUDA(cudaGetLastError());
+}
+
+void gemm_groups(const Context& c, const uint64_t* x, const int32_t* idx, const uint64_t* w, uint64_t* out,
+                 int64_t groups, int mg, int kt, int nl, cudaStream_t s) {
+  if (groups <= 0 || mg <= 0) return;
+  const int64_t n = c.n();
+  dim3 grid((unsigned)((n + kGemmThreads - 1) / kGemmThreads), (unsigned)(2 * nl), 1);
+  if (mg <= 8) {
+    grid.z = (unsigned)(groups * ((mg + 7) / 8));
+    k_gemm_groups<8><<<grid, kGemmThreads, 0, s>>>(x, idx, w, out, mg, kt, nl, c.kp());
+  } else {
+    grid.z = (unsigned)(groups * ((mg + 15) / 16));
+    k_gemm_groups<16><<<grid, kGemmThreads, 0, s>>>(x, idx, w, out, mg, kt, nl, c.kp());
+  }
+  HG_CUDA(cudaGetLastError());
+}
+
+static RelinK relin_params(const Context& c, int nl) {
+  RelinK K{};
+  for (int i = 0; i < nl; ++i) {
+    K.rows0[i] = c.relin_row(i, 0);
+    K.digits[i] = c.digits(i);
+  }
+  K.key_limb_stride = c.n();
+  K.key_poly_words = (int64_t)(c.max_level() + 1) * c.n();
+  return K;
+}
+
+static void launch_relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, int64_t a_stride,
+                         int64_t b_stride, const uint64_t* c2, uint64_t* out, int64_t items, int nl, cudaStream_t s) {
+  const RelinK K = relin_params(c, nl);
+  const size_t sm = limb_smem(c);
+  const int threads = (int)std::min<int64_t>(512, c.n() / 16);
+  if (c.n() <= 8192) {
+    set_smem((const void*)k_relin<true>, sm);
+    k_relin<true><<<(unsigned)(items * nl), threads, sm, s>>>(a, b, a_stride, b_stride, c2, keys.relin.as<uint64_t>(),
+                                                               out, nl, K, c.kp());
+  } else {
+    set_smem((const void*)k_relin<false>, sm);
+    k_relin<false><<<(unsigned)(items * nl), threads, sm, s>>>(a, b, a_stride, b_stride, c2,
+                                                                keys.relin.as<uint64_t>(), out, nl, K, c.kp());
+  }
+  HG_CUDA(cudaGetLastError());
+}
+
+void square_relin(const Context& c, const Keys& keys, const uint64_t* in, uint64_t* out, int64_t items, int nl,
+                  uint64_t* c2, cudaStream_t s) {
+  mul_relin(c, keys, in, in, out, items, nl, c2, s);
+}
+
+void mul_relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, uint64_t* out, int64_t items,
+               int nl, uint64_t* c2, cudaStream_t s) {
+  if (items <= 0) return;
+  check(keys.has_relin, HG_EINTERNAL, "relinearisation key missing");
+  const int64_t pw = (int64_t)nl * c.n();
+  const size_t sm = limb_smem(c);
+  set_smem((const void*)k_relin_c2, sm);
+  k_relin_c2<<<(unsigned)(items * nl), kNttThreads, sm, s>>>(a, b, 2 * pw, 2 * pw, pw, pw, c2, nl, c.kp());
+  HG_CUDA(cudaGetLastError());
+  launch_relin(c, keys, a, b, 2 * pw, 2 * pw, c2, out, items, nl, s);
+}
+
+void mul_tensor(const Context& c, const uint64_t* a, const uint64_t* b, uint64_t* out, int64_t items, int nl,
+                cudaStream_t s) {
+  const int64_t words = items * nl * c.n();
+  if (words <= 0) return;
+  k_tensor<<<ew_blocks(words, 256), 256, 0, s>>>(a, b, out, items, nl, c.kp());
+  HG_CUDA(cudaGetLastError());
+}
+
+void relin3(const Context& c, const Keys& keys, const uint64_t* in3, uint64_t* out2, int64_t items, int nl,
+            uint64_t* c2, cudaStream_t s) {
+  if (items <= 0) return;
+  check(keys.has_relin, HG_EINTERNAL, "relinearisation key missing");
+  const int64_t pw = (int64_t)nl * c.n();
+  // c2 = INTT(d2): copy d2 rows then inverse NTT
+  for (int64_t it = 0; it < items; ++it)
+    HG_CUDA(cudaMemcpyAsync(c2 + it * pw, in3 + it * 3 * pw + 2 * pw, pw * 8, cudaMemcpyDeviceToDevice, s));
+  ntt(c, c2, items * nl, nl, true, s);
+  const RelinK K = relin_params(c, nl);
+  const size_t sm = limb_smem(c);
+  const int threads = (int)std::min<int64_t>(512, c.n() / 16);
+  if (c.n() <= 8192) {
+    set_smem((const void*)k_relin3<true>, sm);
+    k_relin3<true><<<(unsigned)(items * nl), threads, sm, s>>>(in3, c2, keys.relin.as<uint64_t>(), out2, nl, K,
+                                                                c.kp());
+  } else {
+    set_smem((const void*)k_relin3<false>, sm);
+    k_relin3<false><<<(unsigned)(items * nl), threads, sm, s>>>(in3, c2, keys.relin.as<uint64_t>(), out2, nl, K,
+                                                                 c.kp());
+  }
+  HG_CUDA(cudaGetLastError());
+}
+
+void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const uint64_t* pt, uint64_t* out,
+             int64_t items, int nl, cudaStream_t s) {
+  if (items <= 0) return;
+  const int64_t pw = (int64_t)nl * c.n();
+  uint64_t* tmp = static_cast<uint64_t*>(const_cast<Context&>(c).scratch((size_t)(items * 3 * pw * 8), 7));
+  lift_ntt(c, samples, tmp, items * 3, nl, s);
+  const int64_t words = items * pw;
+  k_encrypt_combine<<<ew_blocks(words, 256), 256, 0, s>>>(tmp, keys.pk.as<uint64_t>(), pt, out, items, nl,
+                                                          (int64_t)(c.max_level() + 1) * c.n(), c.kp());
+  HG_CUDA(cudaGetLastError());
+}
+
+void decrypt(const Context& c, const Keys& keys, const uint64_t* ct, uint64_t* m, int64_t items, int size, int nl,
+             cudaStream_t s) {
+  if (items <= 0) return;
+  const int64_t words = items * nl * c.n();
+  k_decrypt_dot<<<ew_blocks(words, 256), 256, 0, s>>>(ct, keys.secret.as<uint64_t>(), m, items, size, nl, c.kp());
+  HG_CUDA(cudaGetLastError());
+  ntt(c, m, items * nl, nl, true, s);
+}
+
+void gather_items(const uint64_t* in, const int32_t* idx, uint64_t* out, int64_t items, int64_t item_words,
+                  cudaStream_t s) {
+  if (items <= 0) return;
+  k_gather_items<<<ew_blocks(items * item_words / 2, 256), 256, 0, s>>>(in, idx, out, items, item_words);
+  HG_CUDA(cudaGetLastError());
+}
+
+void keygen_b(const Context& c, const uint64_t* a, const uint64_t* sk, const uint64_t* e, uint64_t* out, int nl,
+              int special, uint64_t f, cudaStream_t s) {
+  const int64_t words = (int64_t)nl * c.n();
+  uint64_t fs = 0;
+  if (special >= 0) fs = c.mod(special).shoup(f);
+  k_keygen_b<<<ew_blocks(words, 256), 256, 0, s>>>(a, sk, e, out, nl, special, f, fs, c.kp());
+  HG_CUDA(cudaGetLastError());
+}
+
+}  // namespace k
+}  // namespace hg

@@ -33,6 +33,8 @@ PRIM_CASES = {
     "n1024_36_26x2_36": (1024, 26, [36, 26, 26, 36], 11),
     "n2048_50_30_50": (2048, 30, [50, 30, 50], 13),
     "n8192_40_30_40": (8192, 30, [40, 30, 40], 5),
+    "n4096_30x4": (4096, 30, [30, 30, 30, 30], 17),
+    "n16384_50_30x2_50": (16384, 30, [50, 30, 30, 50], 19),
 }
 
 

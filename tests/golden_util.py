@@ -11,7 +11,8 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 GOLDEN = os.path.join(HERE, "golden")
 
-PRIM_CASES = ["n1024_30x3", "n1024_36_26x2_36", "n2048_50_30_50", "n8192_40_30_40"]
+PRIM_CASES = ["n1024_30x3", "n1024_36_26x2_36", "n2048_50_30_50", "n8192_40_30_40", "n4096_30x4",
+              "n16384_50_30x2_50"]
 
 
 def sha(a: np.ndarray) -> str:
