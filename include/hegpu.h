@@ -52,8 +52,10 @@ void hg_context_destroy(hg_context* ctx);
 int hg_context_primes(const hg_context* ctx, uint64_t* primes, int cap, int* count);
 /* relin digit counts D_i (ckks_backend.hpp:42-46) and total rows */
 int hg_context_relin_rows(const hg_context* ctx, int* rows);
-/* use an external cudaStream_t (e.g. torch's current stream); NULL restores the private one */
+/* issue work on an external cudaStream_t (e.g. torch's current stream; NULL = legacy default stream) */
 int hg_context_set_stream(hg_context* ctx, void* cuda_stream);
+/* back to the context's private non-blocking stream */
+int hg_context_use_private_stream(hg_context* ctx);
 void* hg_context_stream(const hg_context* ctx);
 int hg_sync(const hg_context* ctx);
 

@@ -276,7 +276,7 @@ class TapBackend final : public HEBackend {
 };
 
 int mode_net(int argc, char** argv) {
-  if (argc < 14) return 2;
+  if (argc < 13) return 2;
   const std::string graph_path = argv[2], input_path = argv[3];
   const int64_t batch = std::stoll(argv[4]);
   ContextParams p;

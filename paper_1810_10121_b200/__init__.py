@@ -63,6 +63,7 @@ def lib():
         "hg_context_relin_rows": (C.c_int, [vp, C.POINTER(C.c_int)]),
         "hg_context_set_stream": (C.c_int, [vp, vp]),
         "hg_context_stream": (vp, [vp]),
+        "hg_context_use_private_stream": (C.c_int, [vp]),
         "hg_sync": (C.c_int, [vp]),
         "hg_keys_generate": (C.c_int, [vp, C.c_uint64, C.c_int, C.POINTER(vp)]),
         "hg_keys_destroy": (None, [vp]),
@@ -139,6 +140,15 @@ class Context:
         rows = C.c_int()
         _chk(lib().hg_context_relin_rows(h, C.byref(rows)))
         self.relin_rows = rows.value
+        # share torch's current stream so torch-side reads are ordered after our kernels
+        try:
+            import torch
+
+            if torch.cuda.is_available():
+                torch.cuda.set_device(device)
+                self.set_stream(torch.cuda.current_stream(device).cuda_stream)
+        except ImportError:
+            pass
 
     @property
     def handle(self):

@@ -10,8 +10,7 @@
 
 struct hg_context {
   std::unique_ptr<hg::Context> c;
-  cudaStream_t ext = nullptr;
-  cudaStream_t stream() const { return ext ? ext : c->stream(); }
+  cudaStream_t stream() const { return c->stream(); }
 };
 struct hg_keys {
   std::unique_ptr<hg::Keys> k;
@@ -98,10 +97,17 @@ int hg_context_relin_rows(const hg_context* ctx, int* rows) {
   });
 }
 
+int hg_context_use_private_stream(hg_context* ctx) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->c->set_stream(nullptr, false);
+  });
+}
+
 int hg_context_set_stream(hg_context* ctx, void* s) {
   return guard([&] {
     need(ctx, "ctx");
-    ctx->ext = static_cast<cudaStream_t>(s);
+    ctx->c->set_stream(static_cast<cudaStream_t>(s), true);
   });
 }
 void* hg_context_stream(const hg_context* ctx) { return ctx ? ctx->stream() : nullptr; }
@@ -216,7 +222,8 @@ int hg_weighted_sum(hg_context* ctx, const uint64_t* x, const int32_t* idx, cons
     const int64_t items = groups * mg;
     auto* acc = static_cast<uint64_t*>(c.scratch(static_cast<size_t>(items * 2 * nl * c.n() * 8), 3));
     auto* sc = static_cast<int64_t*>(c.scratch(static_cast<size_t>(items * 2 * c.n() * 8), 1));
-    hg::k::gemm_groups(c, x, idx, w, acc, groups, mg, kt, nl, ctx->stream());
+    hg::k::gemm_groups(c, x, idx, w, static_cast<int64_t>(mg) * kt * nl, nullptr, acc, groups, mg, kt, nl,
+                       ctx->stream());
     hg::k::rescale(c, acc, out, items * 2, nl, sc, ctx->stream());
   });
 }
@@ -281,10 +288,6 @@ int hg_decrypt_coeffs(hg_context* ctx, const hg_keys* keys, const uint64_t* ct, 
     HG_CUDA(cudaMemcpyAsync(m_host, m, words * 8, cudaMemcpyDeviceToHost, ctx->stream()));
     HG_CUDA(cudaStreamSynchronize(ctx->stream()));
   });
-}
-
-namespace hg {
-void decode_coeffs_host(const Context& c, const uint64_t* m, int nl, double scale, int64_t count, double* out);
 }
 
 int hg_decrypt(hg_context* ctx, const hg_keys* keys, const uint64_t* ct, int64_t items, int size, int level,

@@ -328,7 +328,7 @@ double Context::default_scale() const { return std::ldexp(1.0, m_p.scale_bits); 
 void* Context::scratch(size_t bytes, int slot) {
   DevBuf& b = m_scratch[slot];
   if (b.bytes < bytes) {
-    HG_CUDA(cudaStreamSynchronize(m_stream));
+    HG_CUDA(cudaStreamSynchronize(stream()));
     b.alloc(bytes);
   }
   return b.p;
@@ -425,14 +425,14 @@ namespace hg {
 // multiword arithmetic and the final to_double() follow the reference's order
 // exactly so decoded values are bit-identical.
 // ---------------------------------------------------------------------------
-namespace {
-struct Crt {
+struct CrtTables {
   int count = 0, width = 0;
   std::vector<uint64_t> total, half;
   std::vector<std::vector<uint64_t>> punct;
   std::vector<uint64_t> punct_inv;
 };
 
+namespace {
 void w_mul(std::vector<uint64_t>& x, uint64_t s) {
   u128 carry = 0;
   for (auto& l : x) {
@@ -460,8 +460,8 @@ double w_double(const std::vector<uint64_t>& a) {
   return r;
 }
 
-Crt make_crt(const std::vector<uint64_t>& q, int count) {
-  Crt c;
+CrtTables make_crt(const std::vector<uint64_t>& q, int count) {
+  CrtTables c;
   c.count = count;
   c.width = count + 1;
   c.total.assign(c.width, 0);
@@ -487,17 +487,15 @@ Crt make_crt(const std::vector<uint64_t>& q, int count) {
 }
 }  // namespace
 
+std::shared_ptr<const CrtTables> Context::crt(int nl) const {
+  std::lock_guard<std::mutex> lock(m_crt_mu);
+  auto it = m_crt.find(nl);
+  if (it == m_crt.end()) it = m_crt.emplace(nl, std::make_shared<const CrtTables>(make_crt(m_q, nl))).first;
+  return it->second;
+}
+
 void decode_coeffs_host(const Context& ctx, const uint64_t* m, int nl, double scale, int64_t count, double* out) {
-  static std::mutex mu;
-  static std::map<std::pair<const Context*, int>, Crt> cache;
-  const Crt* crt;
-  {
-    std::lock_guard<std::mutex> lock(mu);
-    auto key = std::make_pair(&ctx, nl);
-    auto it = cache.find(key);
-    if (it == cache.end()) it = cache.emplace(key, make_crt(ctx.primes(), nl)).first;
-    crt = &it->second;
-  }
+  const std::shared_ptr<const CrtTables> crt = ctx.crt(nl);
   const int64_t n = ctx.n();
   std::vector<double> coeffs(n);
   std::vector<uint64_t> acc(crt->width);

@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -168,7 +169,8 @@ class Context {
   const HMod& mod(int i) const { return m_mod[static_cast<size_t>(i)]; }
   const CtxParams& kp() const { return m_kp; }
   int device() const { return m_device; }
-  cudaStream_t stream() const { return m_stream; }
+  cudaStream_t stream() const { return m_use_ext ? m_ext : m_stream; }
+  void set_stream(cudaStream_t s, bool use_ext) { m_ext = s; m_use_ext = use_ext; }
   const SlotEncoder& encoder() const { return *m_enc; }
   // host copies of the tables (for tests / host reference use)
   const std::vector<uint64_t>& psi(int i) const { return m_psi[static_cast<size_t>(i)]; }
@@ -181,12 +183,18 @@ class Context {
   int relin_rows() const { return m_rows; }
   // scratch arena
   void* scratch(size_t bytes, int slot = 0);
+  // CRT tables per active-limb count (built lazily by decode_coeffs_host)
+  std::shared_ptr<const struct CrtTables> crt(int nl) const;
 
  private:
+  mutable std::mutex m_crt_mu;
+  mutable std::map<int, std::shared_ptr<const struct CrtTables>> m_crt;
   ContextParamsH m_p;
   int m_logn = 0;
   int m_device = 0;
   cudaStream_t m_stream = nullptr;
+  cudaStream_t m_ext = nullptr;
+  bool m_use_ext = false;
   std::vector<uint64_t> m_q;
   std::vector<HMod> m_mod;
   std::vector<std::vector<uint64_t>> m_psi;
@@ -215,6 +223,9 @@ void sample_ternary(Rng& r, int64_t n, int64_t* out);
 void sample_gaussian(Rng& r, int64_t n, double sigma, int64_t* out);
 // fresh-encryption samples for one seed: u, e0, e1 (ckks_backend.hpp:470-490)
 void sample_encryption(uint64_t seed, int64_t n, int64_t* u, int64_t* e0, int64_t* e1);
+
+// CRT reconstruction + /scale + slot decode of coefficient-domain m (host)
+void decode_coeffs_host(const Context& c, const uint64_t* m, int nl, double scale, int64_t count, double* out);
 
 // ---------------------------------------------------------------------------
 // Kernel launchers (hg_kernels.cu).  All buffers are device pointers in the
@@ -245,8 +256,9 @@ void mod_switch(const Context& c, const uint64_t* in, uint64_t* out, int64_t pol
                 cudaStream_t s);
 // weighted sum over groups sharing an input list (Dot: one group; Conv: one per position).
 //  out[g*mg + m][p][j] = sum_t w[((g*mg+m)*kt + t)*nl + j] * x[idx[g*kt + t]][p][j]  (before rescale)
-void gemm_groups(const Context& c, const uint64_t* x, const int32_t* idx, const uint64_t* w, uint64_t* out,
-                 int64_t groups, int mg, int kt, int nl, cudaStream_t s);
+//  w for group g starts at w + g * w_group_stride (0: shared by all groups); output item = oidx[g*mg+m] (or g*mg+m)
+void gemm_groups(const Context& c, const uint64_t* x, const int32_t* idx, const uint64_t* w, int64_t w_group_stride,
+                 const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt, int nl, cudaStream_t s);
 // tensor square + relinearize: in [items][2][nl][N] -> out [items][2][nl][N] (un-rescaled), scratch c2 [items][nl][N]
 void square_relin(const Context& c, const Keys& keys, const uint64_t* in, uint64_t* out, int64_t items, int nl,
                   uint64_t* c2scratch, cudaStream_t s);

@@ -242,6 +242,8 @@ template <int MT>
 __global__ void __launch_bounds__(kGemmThreads) k_gemm_groups(const uint64_t* __restrict__ x,
                                                               const int32_t* __restrict__ idx,
                                                               const uint64_t* __restrict__ w,
+                                                              int64_t w_group_stride,
+                                                              const int32_t* __restrict__ oidx,
                                                               uint64_t* __restrict__ out, int mg, int kt, int nl,
                                                               const CtxParams P) {
   __shared__ uint64_t ws[kGemmKC][MT];
@@ -267,7 +269,7 @@ __global__ void __launch_bounds__(kGemmThreads) k_gemm_groups(const uint64_t* __
     for (int e = threadIdx.x; e < kGemmKC * MT; e += kGemmThreads) {
       const int tt = e / MT, m = e % MT;
       uint64_t v = 0;
-      if (tt < tc && m0 + m < mg) v = w[(((g * mg + m0 + m) * kt) + t0 + tt) * nl + j];
+      if (tt < tc && m0 + m < mg) v = w[g * w_group_stride + ((int64_t)(m0 + m) * kt + t0 + tt) * nl + j];
       ws[tt][m] = v;
     }
     if (threadIdx.x < kGemmKC) xs[threadIdx.x] = threadIdx.x < tc ? idx[g * kt + t0 + threadIdx.x] : 0;
@@ -291,7 +293,10 @@ __global__ void __launch_bounds__(kGemmThreads) k_gemm_groups(const uint64_t* __
   if (col < n) {
 #pragma unroll
     for (int m = 0; m < MT; ++m) {
-      if (m0 + m < mg) out[((g * mg + m0 + m) * 2 * nl + pj) * n + col] = reduce128(acc[m].lo, acc[m].hi, L);
+      if (m0 + m < mg) {
+        const int64_t oi = oidx ? (int64_t)oidx[g * mg + m0 + m] : g * mg + m0 + m;
+        out[(oi * 2 * nl + pj) * n + col] = reduce128(acc[m].lo, acc[m].hi, L);
+      }
     }
   }
 }
@@ -718,17 +723,17 @@ void mod_switch(const Context& c, const uint64_t* in, uint64_t* out, int64_t pol
   HG_CUDA(cudaGetLastError());
 }
 
-void gemm_groups(const Context& c, const uint64_t* x, const int32_t* idx, const uint64_t* w, uint64_t* out,
-                 int64_t groups, int mg, int kt, int nl, cudaStream_t s) {
+void gemm_groups(const Context& c, const uint64_t* x, const int32_t* idx, const uint64_t* w, int64_t w_group_stride,
+                 const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt, int nl, cudaStream_t s) {
   if (groups <= 0 || mg <= 0) return;
   const int64_t n = c.n();
   dim3 grid((unsigned)((n + kGemmThreads - 1) / kGemmThreads), (unsigned)(2 * nl), 1);
   if (mg <= 8) {
     grid.z = (unsigned)(groups * ((mg + 7) / 8));
-    k_gemm_groups<8><<<grid, kGemmThreads, 0, s>>>(x, idx, w, out, mg, kt, nl, c.kp());
+    k_gemm_groups<8><<<grid, kGemmThreads, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, c.kp());
   } else {
     grid.z = (unsigned)(groups * ((mg + 15) / 16));
-    k_gemm_groups<16><<<grid, kGemmThreads, 0, s>>>(x, idx, w, out, mg, kt, nl, c.kp());
+    k_gemm_groups<16><<<grid, kGemmThreads, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, c.kp());
   }
   HG_CUDA(cudaGetLastError());
 }
