@@ -135,6 +135,16 @@ int hg_plan_profile_json(hg_plan* plan, char* buf, size_t cap);
 /* kernel launches issued by the last hg_plan_run */
 int64_t hg_plan_launches(const hg_plan* plan);
 
+/* ---- measurement hooks (bench.py) ---- */
+/* record CUDA events around every kernel launch of this context (off by default) */
+int hg_kernel_timing(hg_context* ctx, int on);
+/* {"kernel": {"launches": n, "total_ms": t}, ...} for the launches recorded since the last call */
+int hg_kernel_stats_json(hg_context* ctx, char* buf, size_t cap);
+/* kernel launches issued by this context so far (counted at every launch site) */
+int64_t hg_kernel_launches(const hg_context* ctx);
+/* register-only Shoup modmul throughput on all SMs (32-bit words if wide == 0, else 64-bit) */
+int hg_bench_modmul(hg_context* ctx, int wide, double* modmul_per_s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -288,7 +288,14 @@ int mode_net(int argc, char** argv) {
   const uint64_t exec_seed = std::stoull(argv[10]);
   const unsigned threads = static_cast<unsigned>(std::stoul(argv[11]));
   const std::string outprefix = argv[12];
-  const bool dump = !(argc > 13 && std::string(argv[13]) == "--no-dump");
+  bool dump = true;
+  int repeat = 1, warmup = 0;
+  for (int a = 13; a < argc; ++a) {
+    const std::string f = argv[a];
+    if (f == "--no-dump") dump = false;
+    else if (f.rfind("--repeat=", 0) == 0) repeat = std::max(1, std::stoi(f.substr(9)));
+    else if (f.rfind("--warmup=", 0) == 0) warmup = std::max(0, std::stoi(f.substr(9)));
+  }
 
   Graph graph = graph_from_json(load_json_file(graph_path));
   // The single Parameter is bound from a raw little-endian f64 file of batch * prod(shape[1:]) values.
@@ -317,11 +324,25 @@ int mode_net(int argc, char** argv) {
   ExecOptions opts;
   opts.threads = threads;
   opts.seed = exec_seed;
+  // untimed warm-up executes, then `repeat` timed ones (bench.py --impl reference)
+  std::vector<double> runs_ms;
+  for (int w = 0; w < warmup; ++w) {
+    TapBackend quiet(inner, false);
+    (void)execute(graph, inputs, quiet, opts);
+  }
+  for (int r = 0; r + 1 < repeat; ++r) {
+    TapBackend quiet(inner, false);
+    const auto a = std::chrono::steady_clock::now();
+    (void)execute(graph, inputs, quiet, opts);
+    runs_ms.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count());
+  }
   const auto t2 = std::chrono::steady_clock::now();
   ExecResult res = execute(graph, inputs, tap, opts);
   const auto t3 = std::chrono::steady_clock::now();
+  runs_ms.push_back(std::chrono::duration<double, std::milli>(t3 - t2).count());
 
   nlohmann::json out;
+  out["execute_ms_list"] = runs_ms;
   out["keygen_ms"] = std::chrono::duration<double, std::milli>(t1 - t0).count();
   out["execute_ms"] = std::chrono::duration<double, std::milli>(t3 - t2).count();
   out["profile"] = res.profile.to_json();

@@ -99,6 +99,10 @@ def lib():
         "hg_plan_set_input_ciphertexts": (C.c_int, [vp, C.c_char_p, vp, C.c_int]),
         "hg_plan_profile_json": (C.c_int, [vp, C.c_char_p, C.c_size_t]),
         "hg_plan_launches": (C.c_int64, [vp]),
+        "hg_kernel_timing": (C.c_int, [vp, C.c_int]),
+        "hg_kernel_stats_json": (C.c_int, [vp, C.c_char_p, C.c_size_t]),
+        "hg_kernel_launches": (C.c_int64, [vp]),
+        "hg_bench_modmul": (C.c_int, [vp, C.c_int, C.POINTER(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -166,6 +170,22 @@ class Context:
 
     def sync(self):
         _chk(lib().hg_sync(self._h))
+
+    def kernel_timing(self, on: bool):
+        _chk(lib().hg_kernel_timing(self._h, 1 if on else 0))
+
+    def kernel_stats(self) -> dict:
+        buf = C.create_string_buffer(1 << 16)
+        _chk(lib().hg_kernel_stats_json(self._h, buf, len(buf)))
+        return json.loads(buf.value.decode())
+
+    def kernel_launches(self) -> int:
+        return int(lib().hg_kernel_launches(self._h))
+
+    def modmul_peak(self, wide: bool) -> float:
+        v = C.c_double()
+        _chk(lib().hg_bench_modmul(self._h, 1 if wide else 0, C.byref(v)))
+        return v.value
 
     def close(self):
         if getattr(self, "_h", None):

@@ -222,7 +222,7 @@ int hg_weighted_sum(hg_context* ctx, const uint64_t* x, const int32_t* idx, cons
     const int64_t items = groups * mg;
     auto* acc = static_cast<uint64_t*>(c.scratch(static_cast<size_t>(items * 2 * nl * c.n() * 8), 3));
     auto* sc = static_cast<int64_t*>(c.scratch(static_cast<size_t>(items * 2 * c.n() * 8), 1));
-    hg::k::gemm_groups(c, x, idx, w, static_cast<int64_t>(mg) * kt * nl, nullptr, acc, groups, mg, kt, nl,
+    hg::k::gemm_groups(c, x, groups * kt, idx, w, static_cast<int64_t>(mg) * kt * nl, nullptr, acc, groups, mg, kt, nl,
                        ctx->stream());
     hg::k::rescale(c, acc, out, items * 2, nl, sc, ctx->stream());
   });
@@ -303,5 +303,45 @@ int hg_decrypt(hg_context* ctx, const hg_keys* keys, const uint64_t* ct, int64_t
       hg::decode_coeffs_host(c, &m[it * (level + 1) * n], level + 1, scale, count, values + it * count);
   });
 }
+
+}  // extern "C"
+
+extern "C" {
+
+int hg_kernel_timing(hg_context* ctx, int on) {
+  return guard([&] {
+    need(ctx, "ctx");
+    ctx->c->kt_enable(on != 0);
+  });
+}
+
+int hg_kernel_stats_json(hg_context* ctx, char* buf, size_t cap) {
+  return guard([&] {
+    need(ctx, "ctx");
+    auto st = ctx->c->kt_collect();
+    std::string s = "{";
+    bool first = true;
+    for (const auto& [name, v] : st) {
+      if (!first) s += ",";
+      first = false;
+      char tmp[384];
+      snprintf(tmp, sizeof tmp, "\"%s\":{\"launches\":%lld,\"total_ms\":%.6f,\"alg_bytes\":%.0f,\"alg_modmuls\":%.0f}",
+               name.c_str(), static_cast<long long>(v.launches), v.ms, v.bytes, v.modmuls);
+      s += tmp;
+    }
+    s += "}";
+    hg::check(s.size() + 1 <= cap, HG_E_VALIDATION, "stats buffer too small");
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+  });
+}
+
+int hg_bench_modmul(hg_context* ctx, int wide, double* modmul_per_s) {
+  return guard([&] {
+    need(ctx, "ctx");
+    *modmul_per_s = hg::k::modmul_peak(*ctx->c, wide != 0, ctx->stream());
+  });
+}
+
+int64_t hg_kernel_launches(const hg_context* ctx) { return ctx ? ctx->c->kt_launches() : 0; }
 
 }  // extern "C"

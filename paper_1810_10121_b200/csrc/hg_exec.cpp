@@ -807,7 +807,7 @@ Val contraction(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_s
     // weighted_sum scale: x_scale * w_scale / dropped (ckks_backend.hpp:409)
     const double ws = static_cast<double>(c.primes()[level]);
     auto acc = new_ct(P, m_out, level, xt->scale);
-    k::gemm_groups(c, xt->p, C.idx->as<int32_t>(), C.w->as<uint64_t>(), C.w_group_stride, C.oidx->as<int32_t>(),
+    k::gemm_groups(c, xt->p, xt->count, C.idx->as<int32_t>(), C.w->as<uint64_t>(), C.w_group_stride, C.oidx->as<int32_t>(),
                    acc->p, groups, mg, kt, level + 1, S(P));
     P->launches += 1;
     auto r = rescale_t(P, acc);
@@ -815,7 +815,7 @@ Val contraction(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_s
     out.ct = r;
   } else {
     auto acc = new_ct(P, m_out, level, xt->scale);
-    k::gemm_groups(c, xt->p, C.idx->as<int32_t>(), C.w->as<uint64_t>(), C.w_group_stride, C.oidx->as<int32_t>(),
+    k::gemm_groups(c, xt->p, xt->count, C.idx->as<int32_t>(), C.w->as<uint64_t>(), C.w_group_stride, C.oidx->as<int32_t>(),
                    acc->p, groups, mg, kt, level + 1, S(P));
     P->launches += 1;
     out.ct = acc;
@@ -931,7 +931,7 @@ Val kernel_pool(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_s
   out.shape = out_shape;
   out.batched = x.batched;
   auto acc = new_ct(P, m_out, level, xt->scale);
-  k::gemm_groups(c, xt->p, Cn.idx->as<int32_t>(), Cn.w->as<uint64_t>(), 0, Cn.oidx->as<int32_t>(), acc->p, m_out, 1,
+  k::gemm_groups(c, xt->p, xt->count, Cn.idx->as<int32_t>(), Cn.w->as<uint64_t>(), 0, Cn.oidx->as<int32_t>(), acc->p, m_out, 1,
                  kt, level + 1, S(P));
   P->launches += 1;
   if (rescale) {
@@ -1257,7 +1257,7 @@ Val gather(hg_plan* P, const std::vector<int64_t>& out_shape, bool out_batched, 
   auto o = new_ct(P, static_cast<int64_t>(map.size()), src->level, src->scale);
   DevArr d(map.size() * 4, S(P));
   HG_CUDA(cudaMemcpyAsync(d.p, map.data(), map.size() * 4, cudaMemcpyHostToDevice, S(P)));
-  k::gather_items(src->p, d.as<int32_t>(), o->p, o->count, src->item_words(), S(P));
+  k::gather_items(*P->ctx, src->p, d.as<int32_t>(), o->p, o->count, src->item_words(), S(P));
   P->launches += 1;
   HG_CUDA(cudaStreamSynchronize(S(P)));
   out.ct = o;
@@ -1517,6 +1517,7 @@ void run_plan(hg_plan* P) {
   P->launches = 0;
   P->outputs.clear();
   admit_depth(P);
+  const int64_t launches0 = P->ctx->kt_launches();
   std::map<std::string, int64_t> uses;
   for (const auto& [id, n] : P->g.nodes)
     for (const auto& in : n.inputs) ++uses[in];
@@ -1558,6 +1559,7 @@ void run_plan(hg_plan* P) {
     }
   }
   for (const auto& o : P->g.outputs) P->outputs[o] = values.at(o);
+  P->launches = P->ctx->kt_launches() - launches0;  // counted at every launch site
   HG_CUDA(cudaStreamSynchronize(S(P)));
   for (auto& [id, ev] : timing) {
     float ms = 0.f;

@@ -318,6 +318,11 @@ Context::Context(const ContextParamsH& p, int device) : m_p(p), m_device(device)
 }
 
 Context::~Context() {
+  for (const KtRec& r : m_kt) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (cudaEvent_t e : m_kt_pool) cudaEventDestroy(e);
   m_scratch.clear();
   m_tables.release();
   if (m_stream) cudaStreamDestroy(m_stream);
@@ -522,6 +527,54 @@ void decode_coeffs_host(const Context& ctx, const uint64_t* m, int nl, double sc
     coeffs[k] = v / scale;
   }
   ctx.encoder().coeffs_to_values(coeffs.data(), count, out);
+}
+
+}  // namespace hg
+
+namespace hg {
+
+// ---------------------------------------------------------------------------
+// Per-kernel event timing (bench roofline evidence)
+// ---------------------------------------------------------------------------
+void Context::kt_begin(const char* name, cudaStream_t s, double bytes, double modmuls) const {
+  ++m_kt_launches;
+  if (!m_kt_on) return;
+  auto take = [this]() {
+    cudaEvent_t e;
+    if (!m_kt_pool.empty()) {
+      e = m_kt_pool.back();
+      m_kt_pool.pop_back();
+    } else {
+      HG_CUDA(cudaEventCreate(&e));
+    }
+    return e;
+  };
+  KtRec r{name, take(), take(), bytes, modmuls};
+  HG_CUDA(cudaEventRecord(r.a, s));
+  m_kt.push_back(r);
+}
+
+void Context::kt_end(cudaStream_t s) const {
+  if (!m_kt_on || m_kt.empty()) return;
+  HG_CUDA(cudaEventRecord(m_kt.back().b, s));
+}
+
+std::map<std::string, Context::KtStat> Context::kt_collect() const {
+  std::map<std::string, KtStat> out;
+  for (const KtRec& r : m_kt) {
+    HG_CUDA(cudaEventSynchronize(r.b));
+    float ms = 0.f;
+    HG_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    KtStat& slot = out[r.name];
+    slot.launches += 1;
+    slot.ms += ms;
+    slot.bytes += r.bytes;
+    slot.modmuls += r.modmuls;
+    m_kt_pool.push_back(r.a);
+    m_kt_pool.push_back(r.b);
+  }
+  m_kt.clear();
+  return out;
 }
 
 }  // namespace hg

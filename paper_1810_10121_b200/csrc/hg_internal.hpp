@@ -185,8 +185,31 @@ class Context {
   void* scratch(size_t bytes, int slot = 0);
   // CRT tables per active-limb count (built lazily by decode_coeffs_host)
   std::shared_ptr<const struct CrtTables> crt(int nl) const;
+  // per-kernel CUDA-event timing (off by default; bench.py turns it on over the timed region)
+  void kt_enable(bool on) const { m_kt_on = on; }
+  bool kt_enabled() const { return m_kt_on; }
+  // bytes / modmuls: the launch's ALGORITHMIC HBM bytes and modular multiplies
+  void kt_begin(const char* name, cudaStream_t s, double bytes = 0.0, double modmuls = 0.0) const;
+  void kt_end(cudaStream_t s) const;
+  struct KtStat {
+    int64_t launches = 0;
+    double ms = 0.0, bytes = 0.0, modmuls = 0.0;
+  };
+  // per kernel name; synchronises and clears the records
+  std::map<std::string, KtStat> kt_collect() const;
+  int64_t kt_launches() const { return m_kt_launches; }
+  void kt_reset_launches() const { m_kt_launches = 0; }
 
  private:
+  struct KtRec {
+    const char* name;
+    cudaEvent_t a, b;
+    double bytes, modmuls;
+  };
+  mutable bool m_kt_on = false;
+  mutable std::vector<KtRec> m_kt;
+  mutable std::vector<cudaEvent_t> m_kt_pool;
+  mutable int64_t m_kt_launches = 0;
   mutable std::mutex m_crt_mu;
   mutable std::map<int, std::shared_ptr<const struct CrtTables>> m_crt;
   ContextParamsH m_p;
@@ -257,8 +280,10 @@ void mod_switch(const Context& c, const uint64_t* in, uint64_t* out, int64_t pol
 // weighted sum over groups sharing an input list (Dot: one group; Conv: one per position).
 //  out[g*mg + m][p][j] = sum_t w[((g*mg+m)*kt + t)*nl + j] * x[idx[g*kt + t]][p][j]  (before rescale)
 //  w for group g starts at w + g * w_group_stride (0: shared by all groups); output item = oidx[g*mg+m] (or g*mg+m)
-void gemm_groups(const Context& c, const uint64_t* x, const int32_t* idx, const uint64_t* w, int64_t w_group_stride,
-                 const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt, int nl, cudaStream_t s);
+//  x_items: number of items in x (for the algorithmic byte count)
+void gemm_groups(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* idx, const uint64_t* w,
+                 int64_t w_group_stride, const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt, int nl,
+                 cudaStream_t s);
 // tensor square + relinearize: in [items][2][nl][N] -> out [items][2][nl][N] (un-rescaled), scratch c2 [items][nl][N]
 void square_relin(const Context& c, const Keys& keys, const uint64_t* in, uint64_t* out, int64_t items, int nl,
                   uint64_t* c2scratch, cudaStream_t s);
@@ -278,9 +303,11 @@ void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const u
 void decrypt(const Context& c, const Keys& keys, const uint64_t* ct, uint64_t* m, int64_t items, int size, int nl,
              cudaStream_t s);
 // gather whole items: out[i] = in[idx[i]] (item_words each)
-void gather_items(const uint64_t* in, const int32_t* idx, uint64_t* out, int64_t items, int64_t item_words,
+void gather_items(const Context& c, const uint64_t* in, const int32_t* idx, uint64_t* out, int64_t items, int64_t item_words,
                   cudaStream_t s);
 // keygen pointwise: out = -(a*s + e) (+ f*s^2 on limb `special` if special >= 0)
+// register-only Shoup modmul throughput on every SM (modmul/s); wide = 64-bit words
+double modmul_peak(const Context& c, bool wide, cudaStream_t s);
 void keygen_b(const Context& c, const uint64_t* a, const uint64_t* sk, const uint64_t* e, uint64_t* out, int nl,
               int special, uint64_t f, cudaStream_t s);
 }  // namespace k

@@ -638,15 +638,23 @@ static void set_smem(const void* fn, size_t bytes) {
   done[fn] = bytes;
 }
 
+// (N/2) log2 N butterflies per limb transform: the NTT's algorithmic modmul count
+static double bfly(const Context& c) { return 0.5 * (double)c.n() * c.logn(); }
+
 void ntt(const Context& c, uint64_t* base, int64_t rows, int nl, bool inverse, cudaStream_t s) {
   if (rows <= 0) return;
   const size_t sm = limb_smem(c);
+  const double bytes = 2.0 * rows * c.n() * 8, mm = rows * bfly(c);
   if (inverse) {
     set_smem((const void*)k_ntt<true>, sm);
+    c.kt_begin("k_ntt", s, bytes, mm);
     k_ntt<true><<<(unsigned)rows, kNttThreads, sm, s>>>(base, nl, c.kp());
+    c.kt_end(s);
   } else {
     set_smem((const void*)k_ntt<false>, sm);
+    c.kt_begin("k_ntt", s, bytes, mm);
     k_ntt<false><<<(unsigned)rows, kNttThreads, sm, s>>>(base, nl, c.kp());
+    c.kt_end(s);
   }
   HG_CUDA(cudaGetLastError());
 }
@@ -655,44 +663,58 @@ void lift_ntt(const Context& c, const int64_t* src, uint64_t* out, int64_t count
   if (count <= 0) return;
   const size_t sm = limb_smem(c);
   set_smem((const void*)k_lift_ntt, sm);
+  c.kt_begin("k_lift_ntt", s, (double)count * c.n() * 8 * (1 + nl), (double)count * nl * bfly(c));
   k_lift_ntt<<<(unsigned)(count * nl), kNttThreads, sm, s>>>(src, out, nl, c.kp());
+  c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
 
 void add(const Context& c, const uint64_t* a, const uint64_t* b, uint64_t* o, int64_t words, int nl, cudaStream_t s) {
   if (words <= 0) return;
+  c.kt_begin("k_elementwise", s);
   k_elementwise<0><<<ew_blocks(words, 256), 256, 0, s>>>(a, b, o, words, nl, c.kp());
+  c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
 void sub(const Context& c, const uint64_t* a, const uint64_t* b, uint64_t* o, int64_t words, int nl, cudaStream_t s) {
   if (words <= 0) return;
+  c.kt_begin("k_elementwise", s);
   k_elementwise<1><<<ew_blocks(words, 256), 256, 0, s>>>(a, b, o, words, nl, c.kp());
+  c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
 void negate(const Context& c, const uint64_t* a, uint64_t* o, int64_t words, int nl, cudaStream_t s) {
   if (words <= 0) return;
+  c.kt_begin("k_elementwise", s);
   k_elementwise<2><<<ew_blocks(words, 256), 256, 0, s>>>(a, nullptr, o, words, nl, c.kp());
+  c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
 void add_plain(const Context& c, const uint64_t* ct, const uint64_t* pt, uint64_t* o, int64_t items, int size, int nl,
                bool per_item, bool subtract, cudaStream_t s) {
   const int64_t words = items * size * nl * c.n();
   if (words <= 0) return;
+  c.kt_begin("k_add_plain", s);
   k_add_plain<<<ew_blocks(words, 256), 256, 0, s>>>(ct, pt, o, items, size, nl, per_item, subtract, c.kp());
+  c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
 void mul_plain(const Context& c, const uint64_t* ct, const uint64_t* pt, uint64_t* o, int64_t items, int size, int nl,
                bool per_item, cudaStream_t s) {
   const int64_t words = items * size * nl * c.n();
   if (words <= 0) return;
+  c.kt_begin("k_mul_plain", s);
   k_mul_plain<<<ew_blocks(words, 256), 256, 0, s>>>(ct, pt, o, items, size, nl, per_item, c.kp());
+  c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
 void mul_scalar(const Context& c, const uint64_t* ct, const uint64_t* w, uint64_t* o, int64_t items, int size, int nl,
                 cudaStream_t s) {
   const int64_t words = items * size * nl * c.n();
   if (words <= 0) return;
+  c.kt_begin("k_mul_scalar", s);
   k_mul_scalar<<<ew_blocks(words, 256), 256, 0, s>>>(ct, w, o, words, nl, c.kp());
+  c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
 
@@ -709,9 +731,15 @@ void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys,
     R.inv[j] = c.inv_q(t, j);
     R.inv_s[j] = c.inv_q_shoup(t, j);
   }
+  const double nw = (double)c.n() * 8;
+  // top: read the dropped limb, write its centred lift; rest: read x_j and the lift, write out_j
+  c.kt_begin("k_rescale_top", s, 2.0 * polys * nw, polys * bfly(c));
   k_rescale_top<<<(unsigned)polys, kNttThreads, sm, s>>>(in, scratch, nl, c.kp());
+  c.kt_end(s);
   HG_CUDA(cudaGetLastError());
+  c.kt_begin("k_rescale_rest", s, (double)polys * (2.0 * t + 1) * nw, (double)polys * t * (bfly(c) + c.n()));
   k_rescale_rest<<<(unsigned)(polys * t), kNttThreads, sm, s>>>(in, scratch, out, nl, R, c.kp());
+  c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
 
@@ -719,21 +747,32 @@ void mod_switch(const Context& c, const uint64_t* in, uint64_t* out, int64_t pol
                 cudaStream_t s) {
   const int64_t words = polys * nl_out * c.n();
   if (words <= 0) return;
+  c.kt_begin("k_mod_switch", s);
   k_mod_switch<<<ew_blocks(words, 256), 256, 0, s>>>(in, out, polys, nl_in, nl_out, c.n());
+  c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
 
-void gemm_groups(const Context& c, const uint64_t* x, const int32_t* idx, const uint64_t* w, int64_t w_group_stride,
-                 const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt, int nl, cudaStream_t s) {
+void gemm_groups(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* idx, const uint64_t* w,
+                 int64_t w_group_stride, const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt, int nl,
+                 cudaStream_t s) {
   if (groups <= 0 || mg <= 0) return;
   const int64_t n = c.n();
   dim3 grid((unsigned)((n + kGemmThreads - 1) / kGemmThreads), (unsigned)(2 * nl), 1);
+  // algorithmic: every input item once (<= groups*kt distinct), every output once; M*K*2(l+1)N modMACs
+  const double item_bytes = 2.0 * nl * n * 8;
+  const double in_items = std::min<double>((double)groups * kt, (double)x_items);
+  const double gb = (in_items + (double)groups * mg) * item_bytes, gm = (double)groups * mg * kt * 2.0 * nl * n;
   if (mg <= 8) {
     grid.z = (unsigned)(groups * ((mg + 7) / 8));
+    c.kt_begin("k_gemm_groups", s, gb, gm);
     k_gemm_groups<8><<<grid, kGemmThreads, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, c.kp());
+    c.kt_end(s);
   } else {
     grid.z = (unsigned)(groups * ((mg + 15) / 16));
+    c.kt_begin("k_gemm_groups", s, gb, gm);
     k_gemm_groups<16><<<grid, kGemmThreads, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, c.kp());
+    c.kt_end(s);
   }
   HG_CUDA(cudaGetLastError());
 }
@@ -754,14 +793,25 @@ static void launch_relin(const Context& c, const Keys& keys, const uint64_t* a, 
   const RelinK K = relin_params(c, nl);
   const size_t sm = limb_smem(c);
   const int threads = (int)std::min<int64_t>(512, c.n() / 16);
+  // algorithmic: c2 once, the active key rows once, a/b once, out once;
+  // sum_i D_i (l+1) forward NTTs + 2 sum_i D_i (l+1) N key MACs + the 3-product tensor
+  int sd = 0;
+  for (int i = 0; i < nl; ++i) sd += c.digits(i);
+  const double pw8 = (double)nl * c.n() * 8;
+  const double rb = items * pw8 * (1 + 4 + 2) + (double)sd * 2 * pw8;
+  const double rm = (double)items * nl * sd * (bfly(c) + 2.0 * c.n()) + 3.0 * items * nl * c.n();
   if (c.n() <= 8192) {
     set_smem((const void*)k_relin<true>, sm);
+    c.kt_begin("k_relin", s, rb, rm);
     k_relin<true><<<(unsigned)(items * nl), threads, sm, s>>>(a, b, a_stride, b_stride, c2, keys.relin.as<uint64_t>(),
                                                                out, nl, K, c.kp());
+    c.kt_end(s);
   } else {
     set_smem((const void*)k_relin<false>, sm);
+    c.kt_begin("k_relin", s, rb, rm);
     k_relin<false><<<(unsigned)(items * nl), threads, sm, s>>>(a, b, a_stride, b_stride, c2,
                                                                 keys.relin.as<uint64_t>(), out, nl, K, c.kp());
+    c.kt_end(s);
   }
   HG_CUDA(cudaGetLastError());
 }
@@ -778,7 +828,9 @@ void mul_relin(const Context& c, const Keys& keys, const uint64_t* a, const uint
   const int64_t pw = (int64_t)nl * c.n();
   const size_t sm = limb_smem(c);
   set_smem((const void*)k_relin_c2, sm);
+  c.kt_begin("k_relin_c2", s, (double)items * nl * c.n() * 8 * 3, (double)items * nl * (bfly(c) + c.n()));
   k_relin_c2<<<(unsigned)(items * nl), kNttThreads, sm, s>>>(a, b, 2 * pw, 2 * pw, pw, pw, c2, nl, c.kp());
+  c.kt_end(s);
   HG_CUDA(cudaGetLastError());
   launch_relin(c, keys, a, b, 2 * pw, 2 * pw, c2, out, items, nl, s);
 }
@@ -787,7 +839,9 @@ void mul_tensor(const Context& c, const uint64_t* a, const uint64_t* b, uint64_t
                 cudaStream_t s) {
   const int64_t words = items * nl * c.n();
   if (words <= 0) return;
+  c.kt_begin("k_tensor", s);
   k_tensor<<<ew_blocks(words, 256), 256, 0, s>>>(a, b, out, items, nl, c.kp());
+  c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
 
@@ -805,12 +859,16 @@ void relin3(const Context& c, const Keys& keys, const uint64_t* in3, uint64_t* o
   const int threads = (int)std::min<int64_t>(512, c.n() / 16);
   if (c.n() <= 8192) {
     set_smem((const void*)k_relin3<true>, sm);
+    c.kt_begin("k_relin3", s);
     k_relin3<true><<<(unsigned)(items * nl), threads, sm, s>>>(in3, c2, keys.relin.as<uint64_t>(), out2, nl, K,
                                                                 c.kp());
+    c.kt_end(s);
   } else {
     set_smem((const void*)k_relin3<false>, sm);
+    c.kt_begin("k_relin3", s);
     k_relin3<false><<<(unsigned)(items * nl), threads, sm, s>>>(in3, c2, keys.relin.as<uint64_t>(), out2, nl, K,
                                                                  c.kp());
+    c.kt_end(s);
   }
   HG_CUDA(cudaGetLastError());
 }
@@ -822,8 +880,10 @@ void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const u
   uint64_t* tmp = static_cast<uint64_t*>(const_cast<Context&>(c).scratch((size_t)(items * 3 * pw * 8), 7));
   lift_ntt(c, samples, tmp, items * 3, nl, s);
   const int64_t words = items * pw;
+  c.kt_begin("k_encrypt_combine", s);
   k_encrypt_combine<<<ew_blocks(words, 256), 256, 0, s>>>(tmp, keys.pk.as<uint64_t>(), pt, out, items, nl,
                                                           (int64_t)(c.max_level() + 1) * c.n(), c.kp());
+  c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
 
@@ -831,15 +891,19 @@ void decrypt(const Context& c, const Keys& keys, const uint64_t* ct, uint64_t* m
              cudaStream_t s) {
   if (items <= 0) return;
   const int64_t words = items * nl * c.n();
+  c.kt_begin("k_decrypt_dot", s);
   k_decrypt_dot<<<ew_blocks(words, 256), 256, 0, s>>>(ct, keys.secret.as<uint64_t>(), m, items, size, nl, c.kp());
+  c.kt_end(s);
   HG_CUDA(cudaGetLastError());
   ntt(c, m, items * nl, nl, true, s);
 }
 
-void gather_items(const uint64_t* in, const int32_t* idx, uint64_t* out, int64_t items, int64_t item_words,
+void gather_items(const Context& c, const uint64_t* in, const int32_t* idx, uint64_t* out, int64_t items, int64_t item_words,
                   cudaStream_t s) {
   if (items <= 0) return;
+  c.kt_begin("k_gather_items", s);
   k_gather_items<<<ew_blocks(items * item_words / 2, 256), 256, 0, s>>>(in, idx, out, items, item_words);
+  c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
 
@@ -848,9 +912,83 @@ void keygen_b(const Context& c, const uint64_t* a, const uint64_t* sk, const uin
   const int64_t words = (int64_t)nl * c.n();
   uint64_t fs = 0;
   if (special >= 0) fs = c.mod(special).shoup(f);
+  c.kt_begin("k_keygen_b", s);
   k_keygen_b<<<ew_blocks(words, 256), 256, 0, s>>>(a, sk, e, out, nl, special, f, fs, c.kp());
+  c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
 
+}  // namespace k
+}  // namespace hg
+
+// ==========================================================================
+// Register-only modmul microbenchmarks: the measured integer roofline
+// (BASELINE.md §3 asks for a u32 and a u64 Shoup modmul peak from the box).
+// ==========================================================================
+namespace hg {
+namespace {
+__global__ void __launch_bounds__(256) k_modmul_bench32(uint32_t* out, uint32_t q, uint32_t w, uint32_t ws, int iters) {
+  uint32_t x[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) x[r] = (threadIdx.x * 8 + r + blockIdx.x) % q;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) x[r] = mul_shoup32(x[r], w, ws, q);
+  }
+  uint32_t acc = 0;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) acc ^= x[r];
+  if (acc == 0xFFFFFFFFu) out[blockIdx.x] = acc;  // keep the loop alive
+}
+__global__ void __launch_bounds__(256) k_modmul_bench64(uint64_t* out, uint64_t q, uint64_t w, uint64_t ws, int iters) {
+  uint64_t x[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) x[r] = (threadIdx.x * 8 + r + blockIdx.x) % q;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) x[r] = mul_shoup64(x[r], w, ws, q);
+  }
+  uint64_t acc = 0;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) acc ^= x[r];
+  if (acc == ~0ull) out[blockIdx.x] = acc;
+}
+}  // namespace
+
+namespace k {
+double modmul_peak(const Context& c, bool wide, cudaStream_t s) {
+  int sms = 0;
+  HG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device()));
+  const int blocks = sms * 8, threads = 256, iters = 4096;
+  DevBuf out(blocks * 8);
+  cudaEvent_t a, b;
+  HG_CUDA(cudaEventCreate(&a));
+  HG_CUDA(cudaEventCreate(&b));
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    HG_CUDA(cudaEventRecord(a, s));
+    if (wide) {
+      const uint64_t q = c.primes()[0];
+      const HMod& M = c.mod(0);
+      const uint64_t w = q / 3 + 1;
+      k_modmul_bench64<<<blocks, threads, 0, s>>>(out.as<uint64_t>(), q, w, M.shoup(w), iters);
+    } else {
+      const uint32_t q = 1073479681u;  // a 30-bit NTT prime
+      const uint32_t w = q / 3 + 1;
+      const uint32_t ws = (uint32_t)(((unsigned __int128)w << 32) / q);
+      k_modmul_bench32<<<blocks, threads, 0, s>>>(out.as<uint32_t>(), q, w, ws, iters);
+    }
+    HG_CUDA(cudaGetLastError());
+    HG_CUDA(cudaEventRecord(b, s));
+    HG_CUDA(cudaEventSynchronize(b));
+    float ms = 0;
+    HG_CUDA(cudaEventElapsedTime(&ms, a, b));
+    if (rep > 0) best = std::min(best, ms);
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  const double ops = (double)blocks * threads * iters * 8;
+  return ops / (best * 1e-3);
+}
 }  // namespace k
 }  // namespace hg

@@ -50,6 +50,17 @@ class Rng:
     def uniform_int(self, n: int) -> int:
         return self.next() % n
 
+    def next_block(self, k: int) -> np.ndarray:
+        """The next k outputs at once: splitmix64 is a counter (state += golden), so
+        output i is mix(state + (i+1) golden) -- vectorised, bit-identical to k next() calls."""
+        with np.errstate(over="ignore"):
+            st = np.uint64(self.s) + np.arange(1, k + 1, dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15)
+            z = (st ^ (st >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+            z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+            z = z ^ (z >> np.uint64(31))
+        self.s = (self.s + k * 0x9E3779B97F4A7C15) & M64
+        return z
+
     def gaussian(self) -> float:
         u1 = self.uniform()
         u2 = self.uniform()
@@ -107,7 +118,8 @@ def gaussian_tensor(rng: Rng, shape, variance: float) -> np.ndarray:
 
 
 def uniform_tensor(rng: Rng, shape, lo: float, hi: float) -> np.ndarray:
-    return np.array([rng.uniform(lo, hi) for _ in range(int(np.prod(shape)))], dtype=np.float64).reshape(shape)
+    u = (rng.next_block(int(np.prod(shape))) >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+    return (lo + (hi - lo) * u).reshape(shape)
 
 
 def sparse_pm1_tensor(rng: Rng, shape, variance: float) -> np.ndarray:
@@ -126,7 +138,8 @@ def sparse_pm1_tensor(rng: Rng, shape, variance: float) -> np.ndarray:
 
 
 def pixel_tensor(rng: Rng, shape) -> np.ndarray:
-    return np.array([rng.uniform_int(256) / 255.0 for _ in range(int(np.prod(shape)))]).reshape(shape)
+    k = rng.next_block(int(np.prod(shape))) % np.uint64(256)
+    return (k.astype(np.float64) / 255.0).reshape(shape)
 
 
 # ---- BASELINE configurations ----
