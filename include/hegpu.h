@@ -106,6 +106,10 @@ int hg_encode_constant(hg_context* ctx, double value, int level, double scale, u
 /* items fresh encryptions at `level`, seeds[item] (host), optional plaintexts pt_dev[item][nl][N] */
 int hg_encrypt(hg_context* ctx, const hg_keys* keys, const uint64_t* pt_dev, const uint64_t* seeds, int64_t items,
                int level, uint64_t* out);
+/* fresh-encryption samples (u, e0, e1; poly.hpp:257-276 streams of ckks_backend.hpp:470-490) as signed
+ * int64 [items][3][N]: on the GPU (device out) or with the host sampler (host out) */
+int hg_sample_encryption(hg_context* ctx, const uint64_t* seeds, int64_t items, int64_t* out_dev);
+int hg_sample_encryption_host(hg_context* ctx, const uint64_t* seeds, int64_t items, int64_t* out_host);
 /* coefficient-domain m = c0 + c1 s (+ ...) -> host [items][nl][N] */
 int hg_decrypt_coeffs(hg_context* ctx, const hg_keys* keys, const uint64_t* ct, int64_t items, int size, int level,
                       uint64_t* m_host);

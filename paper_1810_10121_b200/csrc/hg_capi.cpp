@@ -267,11 +267,8 @@ int hg_encrypt(hg_context* ctx, const hg_keys* keys, const uint64_t* pt_dev, con
     hg::Context& c = *ctx->c;
     level_ok(c, level);
     const int64_t n = c.n();
-    std::vector<int64_t> smp(static_cast<size_t>(items * 3 * n));
-    for (int64_t it = 0; it < items; ++it)
-      hg::sample_encryption(seeds[it], n, &smp[it * 3 * n], &smp[it * 3 * n + n], &smp[it * 3 * n + 2 * n]);
-    auto* d = static_cast<int64_t*>(c.scratch(smp.size() * 8, 5));
-    HG_CUDA(cudaMemcpyAsync(d, smp.data(), smp.size() * 8, cudaMemcpyHostToDevice, ctx->stream()));
+    auto* d = static_cast<int64_t*>(c.scratch(static_cast<size_t>(items * 3 * n * 8), 5));
+    hg::k::sample_encryption_gpu(c, seeds, items, d, ctx->stream());
     hg::k::encrypt(c, *keys->k, d, pt_dev, out, items, level + 1, ctx->stream());
     HG_CUDA(cudaStreamSynchronize(ctx->stream()));
   });
@@ -344,4 +341,24 @@ int hg_bench_modmul(hg_context* ctx, int wide, double* modmul_per_s) {
 
 int64_t hg_kernel_launches(const hg_context* ctx) { return ctx ? ctx->c->kt_launches() : 0; }
 
+}  // extern "C"
+
+extern "C" {
+// fresh-encryption samples (u, e0, e1) as signed int64 [items][3][N] on the device (GPU sampler)
+int hg_sample_encryption(hg_context* ctx, const uint64_t* seeds, int64_t items, int64_t* out_dev) {
+  return guard([&] {
+    need(ctx, "ctx");
+    hg::k::sample_encryption_gpu(*ctx->c, seeds, items, out_dev, ctx->stream());
+  });
+}
+// the host reference sampler (same streams), for parity tests
+int hg_sample_encryption_host(hg_context* ctx, const uint64_t* seeds, int64_t items, int64_t* out_host) {
+  return guard([&] {
+    need(ctx, "ctx");
+    const int64_t n = ctx->c->n();
+    for (int64_t it = 0; it < items; ++it)
+      hg::sample_encryption(seeds[it], n, out_host + it * 3 * n, out_host + it * 3 * n + n,
+                            out_host + it * 3 * n + 2 * n);
+  });
+}
 }  // extern "C"

@@ -624,15 +624,9 @@ void encrypt_items(hg_plan* P, const std::vector<uint64_t>& seeds, const uint64_
   const Context& c = *P->ctx;
   const int64_t n = c.n(), m = static_cast<int64_t>(seeds.size());
   if (m == 0) return;
-  std::vector<int64_t> smp(static_cast<size_t>(m * 3 * n));
-  host_parallel(m, [&](int64_t it) {
-    sample_encryption(seeds[it], n, &smp[it * 3 * n], &smp[it * 3 * n + n], &smp[it * 3 * n + 2 * n]);
-  });
-  DevArr d(smp.size() * 8, S(P));
-  HG_CUDA(cudaMemcpyAsync(d.p, smp.data(), smp.size() * 8, cudaMemcpyHostToDevice, S(P)));
+  DevArr d(static_cast<size_t>(m) * 3 * n * 8, S(P));
+  k::sample_encryption_gpu(c, seeds.data(), m, d.as<int64_t>(), S(P));
   k::encrypt(c, *P->keys, d.as<int64_t>(), pt, out, m, level + 1, S(P));
-  P->launches += 2;
-  HG_CUDA(cudaStreamSynchronize(S(P)));
 }
 
 std::shared_ptr<CtT> new_ct(hg_plan* P, int64_t count, int level, double scale) {

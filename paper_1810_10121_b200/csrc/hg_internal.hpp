@@ -306,6 +306,8 @@ void decrypt(const Context& c, const Keys& keys, const uint64_t* ct, uint64_t* m
 void gather_items(const Context& c, const uint64_t* in, const int32_t* idx, uint64_t* out, int64_t items, int64_t item_words,
                   cudaStream_t s);
 // keygen pointwise: out = -(a*s + e) (+ f*s^2 on limb `special` if special >= 0)
+// fresh-encryption samples (u, e0, e1) for host seeds, on the GPU, bit-identical to sample_encryption()
+void sample_encryption_gpu(const Context& c, const uint64_t* seeds_host, int64_t items, int64_t* out, cudaStream_t s);
 // register-only Shoup modmul throughput on every SM (modmul/s); wide = 64-bit words
 double modmul_peak(const Context& c, bool wide, cudaStream_t s);
 void keygen_b(const Context& c, const uint64_t* a, const uint64_t* sk, const uint64_t* e, uint64_t* out, int nl,

@@ -10,7 +10,9 @@
 //   fresh_encryption / decrypt     ckks/ckks_backend.hpp:470-490, 238-249
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "hg_device.cuh"
 #include "hg_internal.hpp"
@@ -989,6 +991,147 @@ double modmul_peak(const Context& c, bool wide, cudaStream_t s) {
   cudaEventDestroy(b);
   const double ops = (double)blocks * threads * iters * 8;
   return ops / (best * 1e-3);
+}
+}  // namespace k
+}  // namespace hg
+
+// ==========================================================================
+// Counter-based GPU sampler for fresh encryptions (poly.hpp:257-276,
+// ckks_backend.hpp:470-490, common.hpp:71-122).
+//
+// splitmix64 advances its state by a constant, so the k-th draw of any stream
+// is mix(state0 + (k+1) * golden): every coefficient is sampled independently
+// and bit-identically to the reference's sequential loop.  The Gaussian uses
+// the device log/cos (<= 2 ulp); glibc's are within ~1 ulp, so llround can
+// only disagree when g*sigma lies within ~1e-13 of a half-integer.  Any value
+// within 1e-9 of one is flagged and recomputed on the host with std::log /
+// std::cos (the reference's own functions), which makes the output identical
+// by construction.  A rejected Box-Muller draw (u1 == 0, probability 2^-53)
+// flags the whole item for host resampling.
+// ==========================================================================
+namespace hg {
+namespace {
+constexpr uint64_t kGolden = 0x9e3779b97f4a7c15ULL;
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+// state of Rng(seed).fork(label_hash) after its two warm-up draws
+__device__ __forceinline__ uint64_t fork_state(uint64_t seed, uint64_t label_hash) {
+  const uint64_t s = (seed ^ 0xd1b54a32d192ed03ULL) + 2 * kGolden;         // Rng(seed)
+  const uint64_t mixed = mix64(s + kGolden) ^ (label_hash * kGolden + 0x165667b19e3779f9ULL);
+  return (mixed ^ 0xd1b54a32d192ed03ULL) + 2 * kGolden;                    // Rng(mixed)
+}
+
+struct SampleFlag {
+  int32_t item, which, k, pad;
+};
+
+__global__ void k_sample_encryption(const uint64_t* __restrict__ seeds, int64_t items, int n, uint64_t h_mask,
+                                    uint64_t h_error, int64_t* __restrict__ out, int* __restrict__ nflags,
+                                    SampleFlag* __restrict__ flags, int cap, double guard) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= items * n) return;
+  const int64_t item = gid / n;
+  const int k = (int)(gid % n);
+  const uint64_t seed = seeds[item];
+  int64_t* o = out + item * 3 * n;
+  // ternary mask: uniform_int(3) - 1, one draw per coefficient
+  const uint64_t su = fork_state(seed, h_mask);
+  o[k] = (int64_t)(mix64(su + (uint64_t)(k + 1) * kGolden) % 3) - 1;
+  // error stream: e0 uses draws 2k+1, 2k+2; e1 uses 2n+2k+1, 2n+2k+2
+  const uint64_t se = fork_state(seed, h_error);
+#pragma unroll
+  for (int which = 0; which < 2; ++which) {
+    const uint64_t base = (uint64_t)which * 2 * n + 2 * (uint64_t)k;
+    const uint64_t d1 = mix64(se + (base + 1) * kGolden);
+    const uint64_t d2 = mix64(se + (base + 2) * kGolden);
+    const double u1 = (double)(d1 >> 11) * 0x1.0p-53;
+    const double u2 = (double)(d2 >> 11) * 0x1.0p-53;
+    int64_t r = 0;
+    bool flag = false;
+    if (u1 <= 1e-300) {
+      flag = true;  // rejection would shift the stream: host resamples the item
+    } else {
+      const double g = sqrt(-2.0 * log(u1)) * cos(6.283185307179586476925286766559 * u2);
+      const double v = g * 3.2;
+      const double a = fabs(v);
+      const double frac = a - floor(a);
+      if (fabs(frac - 0.5) < guard) flag = true;
+      r = llround(v);
+    }
+    o[(1 + which) * n + k] = r;
+    if (flag) {
+      const int slot = atomicAdd(nflags, 1);
+      if (slot < cap) flags[slot] = SampleFlag{(int32_t)item, which, k, u1 <= 1e-300 ? 1 : 0};
+    }
+  }
+}
+}  // namespace
+
+namespace k {
+void sample_encryption_gpu(const Context& c, const uint64_t* seeds_host, int64_t items, int64_t* out,
+                           cudaStream_t s) {
+  if (items <= 0) return;
+  const int n = (int)c.n();
+  const int cap = 1024;
+  // HG_SAMPLER_GUARD widens the host-fix-up band (tests use it to exercise that path)
+  static const double guard = [] {
+    const char* e = std::getenv("HG_SAMPLER_GUARD");
+    return e ? std::atof(e) : 1e-9;
+  }();
+  auto fnv = [](const char* str) {
+    uint64_t h = 0xcbf29ce484222325ULL;
+    for (const unsigned char* p = (const unsigned char*)str; *p; ++p) h = (h ^ *p) * 0x100000001b3ULL;
+    return h;
+  };
+  // one small device block: [seeds | counter | flags]
+  const size_t seed_bytes = (size_t)items * 8, flag_bytes = 16 + (size_t)cap * sizeof(SampleFlag);
+  uint8_t* buf = static_cast<uint8_t*>(const_cast<Context&>(c).scratch(seed_bytes + flag_bytes, 8));
+  uint64_t* d_seeds = reinterpret_cast<uint64_t*>(buf);
+  int* d_n = reinterpret_cast<int*>(buf + seed_bytes);
+  SampleFlag* d_flags = reinterpret_cast<SampleFlag*>(buf + seed_bytes + 16);
+  HG_CUDA(cudaMemcpyAsync(d_seeds, seeds_host, seed_bytes, cudaMemcpyHostToDevice, s));
+  HG_CUDA(cudaMemsetAsync(d_n, 0, 4, s));
+  const int64_t total = items * n;
+  c.kt_begin("k_sample_encryption", s, (double)items * 3 * n * 8, 0.0);
+  k_sample_encryption<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(d_seeds, items, n, fnv("mask"), fnv("error"),
+                                                                       out, d_n, d_flags, cap, guard);
+  c.kt_end(s);
+  HG_CUDA(cudaGetLastError());
+  int nflags = 0;
+  HG_CUDA(cudaMemcpyAsync(&nflags, d_n, 4, cudaMemcpyDeviceToHost, s));
+  HG_CUDA(cudaStreamSynchronize(s));
+  if (nflags == 0) return;
+  // host fix-up with the reference's own libm (bit-exact by construction)
+  std::vector<SampleFlag> fl(std::min(nflags, cap));
+  HG_CUDA(cudaMemcpy(fl.data(), d_flags, fl.size() * sizeof(SampleFlag), cudaMemcpyDeviceToHost));
+  std::vector<int64_t> whole;
+  auto resample_item = [&](int64_t it) {
+    whole.resize(3 * (size_t)n);
+    sample_encryption(seeds_host[it], n, whole.data(), whole.data() + n, whole.data() + 2 * n);
+    HG_CUDA(cudaMemcpy(out + it * 3 * n, whole.data(), whole.size() * 8, cudaMemcpyHostToDevice));
+  };
+  if (nflags > cap) {
+    for (int64_t it = 0; it < items; ++it) resample_item(it);
+    return;
+  }
+  // Box-Muller rejections shift the whole stream: resample those items sequentially first
+  std::vector<int32_t> rejected;
+  for (const SampleFlag& f : fl)
+    if (f.pad && std::find(rejected.begin(), rejected.end(), f.item) == rejected.end()) rejected.push_back(f.item);
+  for (int32_t it : rejected) resample_item(it);
+  for (const SampleFlag& f : fl) {
+    if (std::find(rejected.begin(), rejected.end(), f.item) != rejected.end()) continue;
+    Rng e = Rng(seeds_host[f.item]).fork("error");
+    // advance to draw index base (two draws per Gaussian): state += base * golden
+    const uint64_t base = (uint64_t)f.which * 2 * n + 2 * (uint64_t)f.k;
+    for (uint64_t i = 0; i < base; ++i) e.next();
+    const int64_t v = static_cast<int64_t>(std::llround(e.gaussian() * 3.2));
+    HG_CUDA(cudaMemcpy(out + (int64_t)f.item * 3 * n + (1 + f.which) * n + f.k, &v, 8, cudaMemcpyHostToDevice));
+  }
 }
 }  // namespace k
 }  // namespace hg
