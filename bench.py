@@ -59,29 +59,34 @@ class ClockSampler:
     def __init__(self, device: int):
         self.device = device
         self.rows = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([c.strip() for c in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self._p = None
+        self._f = None
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        # one long-running sampler process (-lms 200); no per-sample fork inside the timed region
+        try:
+            self._f = tempfile.TemporaryFile(mode="w+")
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
+                                        "--format=csv,noheader,nounits", "-lms", "200"], stdout=self._f,
+                                       stderr=subprocess.DEVNULL)
+        except Exception:
+            self._p = None
         return self
 
     def __exit__(self, *exc):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self._p is None:
+            return
+        time.sleep(0.25)  # make sure at least one sample lands inside short regions
+        self._p.terminate()
+        try:
+            self._p.wait(timeout=5)
+        except Exception:
+            self._p.kill()
+        self._f.seek(0)
+        for line in self._f.read().splitlines():
+            if line.strip():
+                self.rows.append([c.strip() for c in line.split(",")])
+        self._f.close()
 
     def summary(self) -> dict:
         if not self.rows:

@@ -451,6 +451,7 @@ enum class Action { Proceed, ReturnUnchanged, FreshZero, Negate };  // runtime.h
 
 struct Profile {  // ExecProfile (runtime.hpp:140-156)
   std::map<std::string, double> wall_ms;
+  std::map<std::string, double> host_ms;  // host time spent issuing each node (diagnostic)
   int64_t bypass_mult = 0, bypass_add = 0;
   int64_t add = 0, mul_ct = 0, mul_pt = 0, negate = 0;
   int64_t peak_elements = 0;
@@ -1525,6 +1526,7 @@ void run_plan(hg_plan* P) {
     HG_CUDA(cudaEventCreate(&e0));
     HG_CUDA(cudaEventCreate(&e1));
     HG_CUDA(cudaEventRecord(e0, S(P)));
+    const auto h0 = std::chrono::steady_clock::now();
     Val v;
     if (node.op == Op::Parameter) {
       auto it = P->bound.find(id);
@@ -1536,6 +1538,7 @@ void run_plan(hg_plan* P) {
       v = exec_node(P, node, in);
     }
     HG_CUDA(cudaEventRecord(e1, S(P)));
+    P->prof.host_ms[id] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
     timing.push_back({id, {e0, e1}});
     live += v.handles();
     P->prof.peak_elements = std::max(P->prof.peak_elements, live);
@@ -1750,8 +1753,9 @@ int hg_plan_output(hg_plan* P, const char* id, double* values, int64_t capacity,
 
 int hg_plan_profile_json(hg_plan* P, char* buf, size_t cap) {
   return guard_x([&] {
-    nlohmann::json wall = nlohmann::json::object();
+    nlohmann::json wall = nlohmann::json::object(), host = nlohmann::json::object();
     for (const auto& [id, ms] : P->prof.wall_ms) wall[id] = ms;
+    for (const auto& [id, ms] : P->prof.host_ms) host[id] = ms;
     nlohmann::json j = {{"wall_ms", wall},
                         {"bypass", {{"mult", P->prof.bypass_mult}, {"add", P->prof.bypass_add}}},
                         {"ct_ops",
@@ -1759,6 +1763,7 @@ int hg_plan_profile_json(hg_plan* P, char* buf, size_t cap) {
                           {"negate", P->prof.negate}}},
                         {"peak_elements", P->prof.peak_elements},
                         {"total_wall_ms", P->prof.total_wall_ms},
+                        {"host_issue_ms", host},
                         {"gpu_launches", P->launches}};
     const std::string s = j.dump();
     hg::check(s.size() + 1 <= cap, HG_E_VALIDATION, "profile buffer too small");

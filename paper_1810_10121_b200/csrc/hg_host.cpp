@@ -262,7 +262,8 @@ Context::Context(const ContextParamsH& p, int device) : m_p(p), m_device(device)
     auto* iw = reinterpret_cast<uint64_t*>(base + 16 * n);
     auto* fw32 = reinterpret_cast<uint32_t*>(base + 32 * n);
     auto* iw32 = reinterpret_cast<uint32_t*>(base + 40 * n);
-    const bool small = q < (uint64_t(1) << 31);
+    // 32-bit word path: lazy butterflies keep values in [0, 4q), so 4q must fit in 32 bits
+    const bool small = q < (uint64_t(1) << 30);
     std::vector<uint64_t>& psi_brv = m_psi[i];
     psi_brv.resize(n);
     uint64_t f = 1, b = 1;
@@ -414,6 +415,23 @@ std::unique_ptr<Keys> generate_keys(const Context& c, uint64_t seed, bool with_r
         HG_CUDA(cudaStreamSynchronize(s));  // host buffers are reused
       }
     }
+    // Shoup companions for the key-switch MAC (one-time, host)
+    std::vector<uint64_t> kv(static_cast<size_t>(rows) * 2 * pw), kp(kv.size());
+    HG_CUDA(cudaMemcpy(kv.data(), keys->relin.p, kv.size() * 8, cudaMemcpyDeviceToHost));
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < hw; ++t)
+      pool.emplace_back([&, t] {
+        for (size_t w = t; w < kv.size(); w += hw) {
+          const int limb = static_cast<int>((w / n) % nl);
+          const uint64_t q = c.primes()[limb], v = kv[w];
+          if (q < (uint64_t(1) << 30)) kp[w] = (static_cast<uint64_t>((u128(v) << 32) / q) << 32) | v;
+          else kp[w] = static_cast<uint64_t>((u128(v) << 64) / q);
+        }
+      });
+    for (auto& th : pool) th.join();
+    keys->relin_pack.alloc(kp.size() * 8);
+    HG_CUDA(cudaMemcpy(keys->relin_pack.p, kp.data(), kp.size() * 8, cudaMemcpyHostToDevice));
     keys->has_relin = true;
   }
   HG_CUDA(cudaStreamSynchronize(s));

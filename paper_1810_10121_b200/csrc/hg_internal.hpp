@@ -237,6 +237,9 @@ struct Keys {
   DevBuf secret;  // (L+1) N
   DevBuf pk;      // [2][(L+1) N]: b then a
   DevBuf relin;   // [rows][2][(L+1) N]: b then a per (i,d) row
+  // same shape, Shoup companions for the key-switch MAC: limbs < 2^30 hold
+  // (floor(w 2^32/q) << 32 | w), wider limbs hold floor(w 2^64/q)
+  DevBuf relin_pack;
   bool has_relin = false;
 };
 std::unique_ptr<Keys> generate_keys(const Context& ctx, uint64_t seed, bool with_relin);
@@ -313,5 +316,19 @@ double modmul_peak(const Context& c, bool wide, cudaStream_t s);
 void keygen_b(const Context& c, const uint64_t* a, const uint64_t* sk, const uint64_t* e, uint64_t* out, int nl,
               int special, uint64_t f, cudaStream_t s);
 }  // namespace k
+
+// limb-stationary lazy-transform kernels (hg_kernels2.cu)
+namespace k2 {
+// rows of limb j live at base + (k * nl + j) N for k < rows_per_limb; limbs [limb_begin, limb_end)
+void ntt(const Context& c, uint64_t* base, int64_t rows_per_limb, int nl, int limb_begin, int limb_end, bool inverse,
+         cudaStream_t s);
+void lift_ntt(const Context& c, const int64_t* src, uint64_t* out, int64_t items, int nl, cudaStream_t s);
+void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys, int nl, int64_t* cen, cudaStream_t s);
+void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_stride, int64_t b_stride,
+              int64_t a1_off, int64_t b1_off, uint64_t* c2, int64_t items, int nl, cudaStream_t s);
+// given_d: a = size-3 input (d0, d1 taken from it); else d0/d1 from the tensor of a and b
+void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, int64_t a_stride,
+           int64_t b_stride, bool given_d, const uint64_t* c2, uint64_t* out, int64_t items, int nl, cudaStream_t s);
+}  // namespace k2
 
 }  // namespace hg

@@ -645,6 +645,10 @@ static double bfly(const Context& c) { return 0.5 * (double)c.n() * c.logn(); }
 
 void ntt(const Context& c, uint64_t* base, int64_t rows, int nl, bool inverse, cudaStream_t s) {
   if (rows <= 0) return;
+  if (rows % nl == 0 && c.n() >= 1024) {  // limb-stationary lazy kernels (hg_kernels2.cu)
+    k2::ntt(c, base, rows / nl, nl, 0, nl, inverse, s);
+    return;
+  }
   const size_t sm = limb_smem(c);
   const double bytes = 2.0 * rows * c.n() * 8, mm = rows * bfly(c);
   if (inverse) {
@@ -663,6 +667,8 @@ void ntt(const Context& c, uint64_t* base, int64_t rows, int nl, bool inverse, c
 
 void lift_ntt(const Context& c, const int64_t* src, uint64_t* out, int64_t count, int nl, cudaStream_t s) {
   if (count <= 0) return;
+  k2::lift_ntt(c, src, out, count, nl, s);
+  return;
   const size_t sm = limb_smem(c);
   set_smem((const void*)k_lift_ntt, sm);
   c.kt_begin("k_lift_ntt", s, (double)count * c.n() * 8 * (1 + nl), (double)count * nl * bfly(c));
@@ -724,6 +730,8 @@ void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys,
              cudaStream_t s) {
   check(nl >= 2, HG_EINTERNAL, "rescale needs at least two active moduli");
   if (polys <= 0) return;
+  k2::rescale(c, in, out, polys, nl, scratch, s);
+  return;
   const size_t sm = limb_smem(c);
   set_smem((const void*)k_rescale_top, sm);
   set_smem((const void*)k_rescale_rest, sm);
@@ -828,6 +836,11 @@ void mul_relin(const Context& c, const Keys& keys, const uint64_t* a, const uint
   if (items <= 0) return;
   check(keys.has_relin, HG_EINTERNAL, "relinearisation key missing");
   const int64_t pw = (int64_t)nl * c.n();
+  if (c.n() <= 8192) {
+    k2::relin_c2(c, a, b, 2 * pw, 2 * pw, pw, pw, c2, items, nl, s);
+    k2::relin(c, keys, a, b, 2 * pw, 2 * pw, false, c2, out, items, nl, s);
+    return;
+  }
   const size_t sm = limb_smem(c);
   set_smem((const void*)k_relin_c2, sm);
   c.kt_begin("k_relin_c2", s, (double)items * nl * c.n() * 8 * 3, (double)items * nl * (bfly(c) + c.n()));
@@ -856,6 +869,10 @@ void relin3(const Context& c, const Keys& keys, const uint64_t* in3, uint64_t* o
   for (int64_t it = 0; it < items; ++it)
     HG_CUDA(cudaMemcpyAsync(c2 + it * pw, in3 + it * 3 * pw + 2 * pw, pw * 8, cudaMemcpyDeviceToDevice, s));
   ntt(c, c2, items * nl, nl, true, s);
+  if (c.n() <= 8192) {
+    k2::relin(c, keys, in3, nullptr, 3 * pw, 0, true, c2, out2, items, nl, s);
+    return;
+  }
   const RelinK K = relin_params(c, nl);
   const size_t sm = limb_smem(c);
   const int threads = (int)std::min<int64_t>(512, c.n() / 16);

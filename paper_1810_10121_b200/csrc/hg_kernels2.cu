@@ -1,0 +1,528 @@
+// hg_kernels2.cu -- limb-stationary transform kernels (sm_100a).
+//
+// Every CTA owns ONE RNS limb and a group of rows (polys/items) of that limb:
+// the limb's twiddle table is staged into shared memory once and reused for
+// all rows of the group (the table is as large as the data, so re-reading it
+// per transform from L2 dominated the first version).  Limbs are launched in
+// two classes: primes < 2^30 run on 32-bit words (Harvey lazy butterflies in
+// [0, 4q)), wider primes on 64-bit words.  Outputs are canonical, hence
+// identical to the reference (ring.hpp:263-301, poly.hpp:190-228,
+// ckks_backend.hpp:508-554).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "hg_device.cuh"
+#include "hg_internal.hpp"
+#include "hg_ntt.cuh"
+
+namespace hg {
+namespace {
+
+struct LimbList {
+  int count;
+  int limb[HG_MAX_LIMBS];
+};
+
+template <typename W>
+__device__ __forceinline__ W lift_w(int64_t v, uint64_t q) {
+  return (W)lift_signed(v, q);
+}
+
+// Common CTA prologue: figure out the limb and the row range, stage twiddles.
+template <typename W, bool TWS>
+struct Cta {
+  int limb, r0, r1;
+  const LimbInfo* L;
+  W* s;
+  const typename Lz<W>::TW* tw;
+  __device__ __forceinline__ Cta(uint64_t* smem, const LimbList& LL, int64_t rows, int G, const CtxParams& P,
+                                 bool inverse) {
+    limb = LL.limb[blockIdx.x % LL.count];
+    const int g = blockIdx.x / LL.count;
+    r0 = g * G;
+    r1 = (int)min((int64_t)(g + 1) * G, rows);
+    L = &P.limb[limb];
+    s = reinterpret_cast<W*>(smem);
+    const typename Lz<W>::TW* src = inverse ? Lz<W>::inv_table(*L) : Lz<W>::fwd_table(*L);
+    if (TWS) {
+      auto* t = reinterpret_cast<typename Lz<W>::TW*>(reinterpret_cast<uint8_t*>(smem) + P.n * sizeof(W));
+      stage_tw(t, src, (int)P.n);
+      tw = t;
+    } else {
+      tw = src;
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// batched NTT of rows: row k of limb j at base + (k*nl + j) N
+// ---------------------------------------------------------------------------
+template <typename W, bool INV, bool TWS>
+__global__ void __launch_bounds__(512) k_ntt_lz(uint64_t* __restrict__ base, int nl, int64_t rows, int G,
+                                                const LimbList LL, const CtxParams P) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  Cta<W, TWS> c(smem, LL, rows, G, P, INV);
+  const int n = (int)P.n;
+  const W q = (W)c.L->q, q2 = q + q;
+  for (int r = c.r0; r < c.r1; ++r) {
+    uint64_t* g = base + ((int64_t)r * nl + c.limb) * n;
+    load_limb(c.s, g, n);
+    __syncthreads();
+    if (INV) inv_lz<W>(c.s, P.logn, c.tw, Lz<W>::ninv(*c.L), q, q2);
+    else fwd_lz<W>(c.s, P.logn, c.tw, q, q2);
+    store_limb(g, c.s, n);
+    __syncthreads();
+  }
+}
+
+// lift signed int64 polys (one per item) into limb j, forward NTT: out[item][nl][N]
+template <typename W, bool TWS>
+__global__ void __launch_bounds__(512) k_lift_ntt_lz(const int64_t* __restrict__ src, uint64_t* __restrict__ out, int nl,
+                                                     int64_t items, int G, const LimbList LL, const CtxParams P) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  Cta<W, TWS> c(smem, LL, items, G, P, false);
+  const int n = (int)P.n;
+  const W q = (W)c.L->q, q2 = q + q;
+  for (int r = c.r0; r < c.r1; ++r) {
+    const int64_t* g = src + (int64_t)r * n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) c.s[swz<W>(i)] = lift_w<W>(g[i], c.L->q);
+    __syncthreads();
+    fwd_lz<W>(c.s, P.logn, c.tw, q, q2);
+    store_limb(out + ((int64_t)r * nl + c.limb) * n, c.s, n);
+    __syncthreads();
+  }
+}
+
+// rescale step 1 (poly.hpp:196-205): INTT of the top limb t, centred lift -> int64 [poly][N]
+template <typename W, bool TWS>
+__global__ void __launch_bounds__(512) k_rescale_top_lz(const uint64_t* __restrict__ in, int64_t* __restrict__ cen,
+                                                        int nl, int64_t polys, int G, const LimbList LL,
+                                                        const CtxParams P) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  Cta<W, TWS> c(smem, LL, polys, G, P, true);
+  const int n = (int)P.n;
+  const W q = (W)c.L->q, q2 = q + q;
+  const uint64_t half = c.L->q / 2;
+  for (int r = c.r0; r < c.r1; ++r) {
+    load_limb(c.s, in + ((int64_t)r * nl + c.limb) * n, n);
+    __syncthreads();
+    inv_lz<W>(c.s, P.logn, c.tw, Lz<W>::ninv(*c.L), q, q2);
+    int64_t* o = cen + (int64_t)r * n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint64_t v = c.s[swz<W>(i)];
+      o[i] = v > half ? (int64_t)v - (int64_t)c.L->q : (int64_t)v;
+    }
+    __syncthreads();
+  }
+}
+
+struct RescaleC {
+  uint64_t inv[HG_MAX_LIMBS];
+  uint64_t inv_s[HG_MAX_LIMBS];
+};
+
+// rescale step 2 (poly.hpp:207-225): out_j = (x_j - NTT_j(lift(c))) * q_t^{-1}
+template <typename W, bool TWS>
+__global__ void __launch_bounds__(512) k_rescale_rest_lz(const uint64_t* __restrict__ in,
+                                                         const int64_t* __restrict__ cen, uint64_t* __restrict__ out,
+                                                         int nl, int64_t polys, int G, const LimbList LL,
+                                                         const RescaleC R, const CtxParams P) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  Cta<W, TWS> c(smem, LL, polys, G, P, false);
+  const int n = (int)P.n, t = nl - 1, j = c.limb;
+  const W q = (W)c.L->q, q2 = q + q;
+  for (int r = c.r0; r < c.r1; ++r) {
+    const int64_t* cv = cen + (int64_t)r * n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) c.s[swz<W>(i)] = lift_w<W>(cv[i], c.L->q);
+    __syncthreads();
+    fwd_lz_but_last(c.s, P.logn, c.tw, q, q2);
+    const uint64_t* x = in + ((int64_t)r * nl + j) * n;
+    uint64_t* o = out + ((int64_t)r * t + j) * n;
+    for (int vt = threadIdx.x; vt < (n >> 4); vt += blockDim.x) {
+      W y[16];
+      fwd_last_group(c.s, vt, P.logn, c.tw, q, q2, y);
+      const ulonglong2* x2 = reinterpret_cast<const ulonglong2*>(x + (vt << 4));
+      ulonglong2* o2 = reinterpret_cast<ulonglong2*>(o + (vt << 4));
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        const ulonglong2 xv = x2[h];
+        ulonglong2 ov;
+        const uint64_t c0 = canon4<W>(y[2 * h], q, q2), c1 = canon4<W>(y[2 * h + 1], q, q2);
+        ov.x = mul_shoup64(sub_mod(xv.x, c0, c.L->q), R.inv[j], R.inv_s[j], c.L->q);
+        ov.y = mul_shoup64(sub_mod(xv.y, c1, c.L->q), R.inv[j], R.inv_s[j], c.L->q);
+        o2[h] = ov;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// relinearisation prologue: c2 = INTT(a1 * b1) per (item, limb i)  (ckks_backend.hpp:509)
+template <typename W, bool TWS>
+__global__ void __launch_bounds__(512) k_relin_c2_lz(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
+                                                     int64_t a_stride, int64_t b_stride, int64_t a1_off, int64_t b1_off,
+                                                     uint64_t* __restrict__ c2, int nl, int64_t items, int G,
+                                                     const LimbList LL, const CtxParams P) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  Cta<W, TWS> c(smem, LL, items, G, P, true);
+  const int n = (int)P.n;
+  const W q = (W)c.L->q, q2 = q + q;
+  for (int r = c.r0; r < c.r1; ++r) {
+    const uint64_t* x1 = a + r * a_stride + a1_off + (int64_t)c.limb * n;
+    const uint64_t* y1 = b + r * b_stride + b1_off + (int64_t)c.limb * n;
+    for (int k = threadIdx.x; k < n; k += blockDim.x) c.s[swz<W>(k)] = (W)mul_mod(x1[k], y1[k], *c.L);
+    __syncthreads();
+    inv_lz<W>(c.s, P.logn, c.tw, Lz<W>::ninv(*c.L), q, q2);
+    store_limb(c2 + ((int64_t)r * nl + c.limb) * n, c.s, n);
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Relinearisation key switch (ckks_backend.hpp:508-554), one CTA per (limb j,
+// group of items): for every source residue i <= l and digit d < D_i the
+// digit (c2_i >> 15d) & 0x7FFF is staged, forward-transformed mod q_j with the
+// staged twiddles, and its last radix-16 pass feeds the key MAC directly from
+// registers: thread vt owns evaluations 16 vt .. 16 vt + 15 for the whole
+// item, so the two accumulators never leave registers.
+//   small limbs: packed key words (ws32 << 32 | w); acc += lazy Shoup, kept in [0, 2q)
+//   wide limbs : key value + its 64-bit Shoup constant; acc canonical
+// Epilogue adds d0 = a0 b0 and d1 = a0 b1 + a1 b0 (or given d0, d1 for size-3 inputs).
+// ---------------------------------------------------------------------------
+struct RelinC {
+  int rows0[HG_MAX_LIMBS];
+  int digits[HG_MAX_LIMBS];
+  int64_t key_poly_words;  // (L+1) N
+};
+
+template <typename W, bool TWS, bool GIVEN_D>
+__global__ void __launch_bounds__(512) k_relin_lz(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
+                                                  int64_t a_stride, int64_t b_stride, const uint64_t* __restrict__ c2,
+                                                  const uint64_t* __restrict__ kval,
+                                                  const uint64_t* __restrict__ kpack, uint64_t* __restrict__ out,
+                                                  int nl, int64_t items, int G, const RelinC K, const LimbList LL,
+                                                  const CtxParams P) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  Cta<W, TWS> c(smem, LL, items, G, P, false);
+  const int n = (int)P.n, logn = P.logn, j = c.limb;
+  const W q = (W)c.L->q, q2 = q + q;
+  const uint64_t Q = c.L->q;
+  const int64_t pw = (int64_t)nl * n;
+  const int vt = threadIdx.x;  // blockDim.x == n / 16: one 16-element group per thread
+  for (int item = c.r0; item < c.r1; ++item) {
+    W acc0[16], acc1[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) { acc0[r] = 0; acc1[r] = 0; }
+    const uint64_t* c2item = c2 + (int64_t)item * pw;
+    for (int i = 0; i < nl; ++i) {
+      const uint64_t* src = c2item + (int64_t)i * n;
+      for (int d = 0; d < K.digits[i]; ++d) {
+        const int row = K.rows0[i] + d;
+        const int sh = 15 * d;
+        for (int k = threadIdx.x; k < n; k += blockDim.x) c.s[swz<W>(k)] = (W)((src[k] >> sh) & 0x7FFF);
+        __syncthreads();
+        fwd_lz_but_last(c.s, logn, c.tw, q, q2);
+        W x[16];
+        fwd_last_group(c.s, vt, logn, c.tw, q, q2, x);
+        const int64_t koff = (int64_t)row * 2 * K.key_poly_words + (int64_t)j * n + (vt << 4);
+        if (sizeof(W) == 4) {
+          const ulonglong2* kb2 = reinterpret_cast<const ulonglong2*>(kpack + koff);
+          const ulonglong2* ka2 = reinterpret_cast<const ulonglong2*>(kpack + koff + K.key_poly_words);
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            const ulonglong2 vb = __ldg(kb2 + h), va = __ldg(ka2 + h);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const uint64_t pb = e ? vb.y : vb.x, pa = e ? va.y : va.x;
+              const uint32_t xv = (uint32_t)x[2 * h + e];
+              const uint32_t q32 = (uint32_t)Q, q232 = q32 + q32;
+              uint32_t t0 = xv * (uint32_t)pb - __umulhi(xv, (uint32_t)(pb >> 32)) * q32;
+              uint32_t t1 = xv * (uint32_t)pa - __umulhi(xv, (uint32_t)(pa >> 32)) * q32;
+              uint32_t s0 = (uint32_t)acc0[2 * h + e] + t0, s1 = (uint32_t)acc1[2 * h + e] + t1;
+              acc0[2 * h + e] = (W)(s0 >= q232 ? s0 - q232 : s0);
+              acc1[2 * h + e] = (W)(s1 >= q232 ? s1 - q232 : s1);
+            }
+          }
+        } else {
+          const ulonglong2* kb2 = reinterpret_cast<const ulonglong2*>(kval + koff);
+          const ulonglong2* ka2 = reinterpret_cast<const ulonglong2*>(kval + koff + K.key_poly_words);
+          const ulonglong2* sb2 = reinterpret_cast<const ulonglong2*>(kpack + koff);
+          const ulonglong2* sa2 = reinterpret_cast<const ulonglong2*>(kpack + koff + K.key_poly_words);
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            const ulonglong2 vb = __ldg(kb2 + h), va = __ldg(ka2 + h), wb = __ldg(sb2 + h), wa = __ldg(sa2 + h);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const uint64_t xv = canon4<uint64_t>((uint64_t)x[2 * h + e], Q, Q + Q);
+              const uint64_t t0 = mul_shoup64(xv, e ? vb.y : vb.x, e ? wb.y : wb.x, Q);
+              const uint64_t t1 = mul_shoup64(xv, e ? va.y : va.x, e ? wa.y : wa.x, Q);
+              acc0[2 * h + e] = (W)add_mod((uint64_t)acc0[2 * h + e], t0, Q);
+              acc1[2 * h + e] = (W)add_mod((uint64_t)acc1[2 * h + e], t1, Q);
+            }
+          }
+        }
+        __syncthreads();  // smem reused by the next digit
+      }
+    }
+    // epilogue: + d0, d1; canonical store
+    const int k0 = vt << 4;
+    uint64_t* o0 = out + (int64_t)item * 2 * pw + (int64_t)j * n + k0;
+    uint64_t* o1 = o0 + pw;
+    const uint64_t* p0;
+    const uint64_t* p1;
+    const uint64_t* q0 = nullptr;
+    const uint64_t* q1 = nullptr;
+    if (GIVEN_D) {  // a = (d0, d1, d2) size-3 input
+      p0 = a + (int64_t)item * a_stride + (int64_t)j * n + k0;
+      p1 = p0 + pw;
+    } else {
+      p0 = a + (int64_t)item * a_stride + (int64_t)j * n + k0;
+      p1 = p0 + pw;
+      q0 = b + (int64_t)item * b_stride + (int64_t)j * n + k0;
+      q1 = q0 + pw;
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      uint64_t r0 = (uint64_t)acc0[r], r1 = (uint64_t)acc1[r];
+      if (sizeof(W) == 4) {
+        r0 = r0 >= Q ? r0 - Q : r0;
+        r1 = r1 >= Q ? r1 - Q : r1;
+      }
+      uint64_t d0, d1;
+      if (GIVEN_D) {
+        d0 = p0[r];
+        d1 = p1[r];
+      } else {
+        const uint64_t x0 = p0[r], x1 = p1[r], y0 = q0[r], y1 = q1[r];
+        d0 = mul_mod(x0, y0, *c.L);
+        d1 = add_mod(mul_mod(x0, y1, *c.L), mul_mod(x1, y0, *c.L), Q);
+      }
+      o0[r] = add_mod(r0, d0, Q);
+      o1[r] = add_mod(r1, d1, Q);
+    }
+  }
+}
+
+}  // namespace
+
+// ===========================================================================
+// launchers
+// ===========================================================================
+namespace k2 {
+
+struct Classes {
+  LimbList small{}, wide{};
+};
+
+static Classes classify(const Context& c, int limb_begin, int limb_end) {
+  Classes cl;
+  for (int j = limb_begin; j < limb_end; ++j) {
+    if (c.kp().limb[j].small) cl.small.limb[cl.small.count++] = j;
+    else cl.wide.limb[cl.wide.count++] = j;
+  }
+  return cl;
+}
+
+static void set_smem_attr(const void* fn, size_t bytes) {
+  static std::map<const void*, size_t> done;
+  auto it = done.find(fn);
+  if (it != done.end() && it->second >= bytes) return;
+  HG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  done[fn] = bytes;
+}
+
+constexpr size_t kSmemCap = 227 * 1024;
+
+template <typename W>
+static size_t data_bytes(const Context& c) { return (size_t)c.n() * sizeof(W); }
+template <typename W>
+static size_t tw_bytes(const Context& c) { return (size_t)c.n() * sizeof(typename Lz<W>::TW); }
+template <typename W>
+static bool stage_ok(const Context& c) { return data_bytes<W>(c) + tw_bytes<W>(c) <= kSmemCap; }
+
+static int threads_for(const Context& c) { return (int)std::min<int64_t>(512, c.n() / 16); }
+
+// rows per CTA so that the grid still covers every SM a few times over
+static int group_size(int64_t rows, int limbs, int ctas_per_sm) {
+  const int64_t target = 148LL * ctas_per_sm * 3;
+  int64_t g = (rows * limbs + target - 1) / target;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(g, 16));
+}
+
+static double bfly(const Context& c) { return 0.5 * (double)c.n() * c.logn(); }
+
+// Launch `Kern<W,TWS>` over one limb class.  F(fn_ptr, grid, smem, G) does the launch.
+template <typename W, typename Launch>
+static void for_class(const Context& c, const LimbList& LL, int64_t rows, bool allow_tws, Launch&& launch) {
+  if (LL.count == 0 || rows <= 0) return;
+  const bool tws = allow_tws && stage_ok<W>(c);
+  const size_t sm = data_bytes<W>(c) + (tws ? tw_bytes<W>(c) : 0);
+  const int per_sm = std::max<int>(1, (int)(kSmemCap / sm));
+  const int G = group_size(rows, LL.count, std::min(per_sm, 2));
+  const unsigned grid = (unsigned)(LL.count * ((rows + G - 1) / G));
+  launch(tws, grid, sm, G);
+}
+
+void ntt(const Context& c, uint64_t* base, int64_t rows_per_limb, int nl, int limb_begin, int limb_end, bool inverse,
+         cudaStream_t s) {
+  const Classes cl = classify(c, limb_begin, limb_end);
+  const int th = threads_for(c);
+  const double nw = (double)c.n() * 8;
+#define HG_NTT_LAUNCH(W, LL)                                                                                      \
+  for_class<W>(c, LL, rows_per_limb, true, [&](bool tws, unsigned grid, size_t sm, int G) {                       \
+    const void* fn = inverse ? (tws ? (const void*)k_ntt_lz<W, true, true> : (const void*)k_ntt_lz<W, true, false>) \
+                             : (tws ? (const void*)k_ntt_lz<W, false, true> : (const void*)k_ntt_lz<W, false, false>); \
+    set_smem_attr(fn, sm);                                                                                        \
+    c.kt_begin("k_ntt_lz", s, 2.0 * rows_per_limb * LL.count * nw, (double)rows_per_limb * LL.count * bfly(c));   \
+    if (inverse) {                                                                                                \
+      if (tws) k_ntt_lz<W, true, true><<<grid, th, sm, s>>>(base, nl, rows_per_limb, G, LL, c.kp());            \
+      else k_ntt_lz<W, true, false><<<grid, th, sm, s>>>(base, nl, rows_per_limb, G, LL, c.kp());               \
+    } else {                                                                                                      \
+      if (tws) k_ntt_lz<W, false, true><<<grid, th, sm, s>>>(base, nl, rows_per_limb, G, LL, c.kp());           \
+      else k_ntt_lz<W, false, false><<<grid, th, sm, s>>>(base, nl, rows_per_limb, G, LL, c.kp());              \
+    }                                                                                                             \
+    c.kt_end(s);                                                                                                  \
+    HG_CUDA(cudaGetLastError());                                                                                  \
+  });
+  HG_NTT_LAUNCH(uint32_t, cl.small)
+  HG_NTT_LAUNCH(uint64_t, cl.wide)
+#undef HG_NTT_LAUNCH
+}
+
+void lift_ntt(const Context& c, const int64_t* src, uint64_t* out, int64_t items, int nl, cudaStream_t s) {
+  const Classes cl = classify(c, 0, nl);
+  const int th = threads_for(c);
+  const double nw = (double)c.n() * 8;
+#define HG_LIFT_LAUNCH(W, LL)                                                                                     \
+  for_class<W>(c, LL, items, true, [&](bool tws, unsigned grid, size_t sm, int G) {                               \
+    const void* fn = tws ? (const void*)k_lift_ntt_lz<W, true> : (const void*)k_lift_ntt_lz<W, false>;             \
+    set_smem_attr(fn, sm);                                                                                        \
+    c.kt_begin("k_lift_ntt_lz", s, (double)items * LL.count * 2 * nw, (double)items * LL.count * bfly(c));        \
+    if (tws) k_lift_ntt_lz<W, true><<<grid, th, sm, s>>>(src, out, nl, items, G, LL, c.kp());                      \
+    else k_lift_ntt_lz<W, false><<<grid, th, sm, s>>>(src, out, nl, items, G, LL, c.kp());                         \
+    c.kt_end(s);                                                                                                  \
+    HG_CUDA(cudaGetLastError());                                                                                  \
+  });
+  HG_LIFT_LAUNCH(uint32_t, cl.small)
+  HG_LIFT_LAUNCH(uint64_t, cl.wide)
+#undef HG_LIFT_LAUNCH
+}
+
+void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys, int nl, int64_t* cen,
+             cudaStream_t s) {
+  check(nl >= 2, HG_EINTERNAL, "rescale needs at least two active moduli");
+  if (polys <= 0) return;
+  const int t = nl - 1;
+  const int th = threads_for(c);
+  const double nw = (double)c.n() * 8;
+  RescaleC R{};
+  for (int j = 0; j < t; ++j) {
+    R.inv[j] = c.inv_q(t, j);
+    R.inv_s[j] = c.inv_q_shoup(t, j);
+  }
+  const Classes top = classify(c, t, t + 1);
+#define HG_TOP_LAUNCH(W, LL)                                                                                      \
+  for_class<W>(c, LL, polys, true, [&](bool tws, unsigned grid, size_t sm, int G) {                               \
+    const void* fn = tws ? (const void*)k_rescale_top_lz<W, true> : (const void*)k_rescale_top_lz<W, false>;       \
+    set_smem_attr(fn, sm);                                                                                        \
+    c.kt_begin("k_rescale_top_lz", s, 2.0 * polys * nw, (double)polys * bfly(c));                                 \
+    if (tws) k_rescale_top_lz<W, true><<<grid, th, sm, s>>>(in, cen, nl, polys, G, LL, c.kp());                    \
+    else k_rescale_top_lz<W, false><<<grid, th, sm, s>>>(in, cen, nl, polys, G, LL, c.kp());                       \
+    c.kt_end(s);                                                                                                  \
+    HG_CUDA(cudaGetLastError());                                                                                  \
+  });
+  HG_TOP_LAUNCH(uint32_t, top.small)
+  HG_TOP_LAUNCH(uint64_t, top.wide)
+#undef HG_TOP_LAUNCH
+  const Classes rest = classify(c, 0, t);
+#define HG_REST_LAUNCH(W, LL)                                                                                     \
+  for_class<W>(c, LL, polys, true, [&](bool tws, unsigned grid, size_t sm, int G) {                               \
+    const void* fn = tws ? (const void*)k_rescale_rest_lz<W, true> : (const void*)k_rescale_rest_lz<W, false>;     \
+    set_smem_attr(fn, sm);                                                                                        \
+    c.kt_begin("k_rescale_rest_lz", s, (double)polys * LL.count * 3 * nw,                                         \
+               (double)polys * LL.count * (bfly(c) + c.n()));                                                     \
+    if (tws) k_rescale_rest_lz<W, true><<<grid, th, sm, s>>>(in, cen, out, nl, polys, G, LL, R, c.kp());           \
+    else k_rescale_rest_lz<W, false><<<grid, th, sm, s>>>(in, cen, out, nl, polys, G, LL, R, c.kp());              \
+    c.kt_end(s);                                                                                                  \
+    HG_CUDA(cudaGetLastError());                                                                                  \
+  });
+  HG_REST_LAUNCH(uint32_t, rest.small)
+  HG_REST_LAUNCH(uint64_t, rest.wide)
+#undef HG_REST_LAUNCH
+}
+
+static RelinC relin_consts(const Context& c, int nl) {
+  RelinC K{};
+  for (int i = 0; i < nl; ++i) {
+    K.rows0[i] = c.relin_row(i, 0);
+    K.digits[i] = c.digits(i);
+  }
+  K.key_poly_words = (int64_t)(c.max_level() + 1) * c.n();
+  return K;
+}
+
+void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, int64_t a_stride,
+           int64_t b_stride, bool given_d, const uint64_t* c2, uint64_t* out, int64_t items, int nl, cudaStream_t s) {
+  check(c.n() / 16 <= 512, HG_EINTERNAL, "relin_lz: ring degree above 8192");
+  const RelinC K = relin_consts(c, nl);
+  const Classes cl = classify(c, 0, nl);
+  const int th = (int)(c.n() / 16);
+  int sd = 0;
+  for (int i = 0; i < nl; ++i) sd += c.digits(i);
+  const double pw8 = (double)nl * c.n() * 8;
+#define HG_RELIN_LAUNCH(W, LL, GD)                                                                                \
+  for_class<W>(c, LL, items, true, [&](bool tws, unsigned grid, size_t sm, int G) {                               \
+    const void* fn = tws ? (const void*)k_relin_lz<W, true, GD> : (const void*)k_relin_lz<W, false, GD>;           \
+    set_smem_attr(fn, sm);                                                                                        \
+    const double frac = (double)LL.count / nl;                                                                    \
+    c.kt_begin("k_relin_lz", s, frac * (items * pw8 * 7 + (double)sd * 2 * pw8),                                   \
+               (double)items * LL.count * (sd * (bfly(c) + 2.0 * c.n()) + 3.0 * c.n()));                          \
+    if (tws)                                                                                                      \
+      k_relin_lz<W, true, GD><<<grid, th, sm, s>>>(a, b, a_stride, b_stride, c2, keys.relin.as<uint64_t>(),       \
+                                                   keys.relin_pack.as<uint64_t>(), out, nl, items, G, K, LL,      \
+                                                   c.kp());                                                       \
+    else                                                                                                          \
+      k_relin_lz<W, false, GD><<<grid, th, sm, s>>>(a, b, a_stride, b_stride, c2, keys.relin.as<uint64_t>(),      \
+                                                    keys.relin_pack.as<uint64_t>(), out, nl, items, G, K, LL,     \
+                                                    c.kp());                                                      \
+    c.kt_end(s);                                                                                                  \
+    HG_CUDA(cudaGetLastError());                                                                                  \
+  });
+  if (given_d) {
+    HG_RELIN_LAUNCH(uint32_t, cl.small, true)
+    HG_RELIN_LAUNCH(uint64_t, cl.wide, true)
+  } else {
+    HG_RELIN_LAUNCH(uint32_t, cl.small, false)
+    HG_RELIN_LAUNCH(uint64_t, cl.wide, false)
+  }
+#undef HG_RELIN_LAUNCH
+}
+
+void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_stride, int64_t b_stride,
+              int64_t a1_off, int64_t b1_off, uint64_t* c2, int64_t items, int nl, cudaStream_t s) {
+  const Classes cl = classify(c, 0, nl);
+  const int th = threads_for(c);
+  const double nw = (double)c.n() * 8;
+#define HG_C2_LAUNCH(W, LL)                                                                                       \
+  for_class<W>(c, LL, items, true, [&](bool tws, unsigned grid, size_t sm, int G) {                               \
+    const void* fn = tws ? (const void*)k_relin_c2_lz<W, true> : (const void*)k_relin_c2_lz<W, false>;             \
+    set_smem_attr(fn, sm);                                                                                        \
+    c.kt_begin("k_relin_c2_lz", s, (double)items * LL.count * 3 * nw, (double)items * LL.count * (bfly(c) + c.n())); \
+    if (tws)                                                                                                      \
+      k_relin_c2_lz<W, true><<<grid, th, sm, s>>>(a, b, a_stride, b_stride, a1_off, b1_off, c2, nl, items, G, LL, \
+                                                  c.kp());                                                        \
+    else                                                                                                          \
+      k_relin_c2_lz<W, false><<<grid, th, sm, s>>>(a, b, a_stride, b_stride, a1_off, b1_off, c2, nl, items, G,     \
+                                                   LL, c.kp());                                                   \
+    c.kt_end(s);                                                                                                  \
+    HG_CUDA(cudaGetLastError());                                                                                  \
+  });
+  HG_C2_LAUNCH(uint32_t, cl.small)
+  HG_C2_LAUNCH(uint64_t, cl.wide)
+#undef HG_C2_LAUNCH
+}
+
+}  // namespace k2
+}  // namespace hg

@@ -203,4 +203,201 @@ __device__ __forceinline__ void store_limb(uint64_t* __restrict__ g, const W* s,
   }
 }
 
+// ===========================================================================
+// Lazy (Harvey) transform core with twiddles in shared memory.
+//
+// Values stay in [0, 4q) through the forward transform and [0, 2q) through
+// the inverse, so each butterfly is one lazy Shoup product plus three
+// add/sub/compare ops; a single canonicalisation at the end returns residues
+// in [0, q), which makes every output word identical to the reference's
+// eagerly-reduced transform.  32-bit words need 4q < 2^32 (small primes are
+// < 2^30); 64-bit words need 4q < 2^64 (all primes are < 2^62).
+// ===========================================================================
+template <typename W>
+struct Lz;
+template <>
+struct Lz<uint32_t> {
+  using TW = uint2;
+  static __device__ __forceinline__ uint32_t mulw(uint32_t x, TW w, uint32_t q) { return x * w.x - __umulhi(x, w.y) * q; }
+  static __device__ __forceinline__ const TW* fwd_table(const LimbInfo& L) { return L.fw32; }
+  static __device__ __forceinline__ const TW* inv_table(const LimbInfo& L) { return L.iw32; }
+  static __device__ __forceinline__ TW ninv(const LimbInfo& L) { return make_uint2((uint32_t)L.ninv, L.ninv32_s); }
+};
+template <>
+struct Lz<uint64_t> {
+  using TW = ulonglong2;
+  static __device__ __forceinline__ uint64_t mulw(uint64_t x, TW w, uint64_t q) { return x * w.x - __umul64hi(x, w.y) * q; }
+  static __device__ __forceinline__ const TW* fwd_table(const LimbInfo& L) { return L.fw; }
+  static __device__ __forceinline__ const TW* inv_table(const LimbInfo& L) { return L.iw; }
+  static __device__ __forceinline__ TW ninv(const LimbInfo& L) { return make_ulonglong2(L.ninv, L.ninv_s); }
+};
+
+template <typename W>
+__device__ __forceinline__ void ct_lz(W& a, W& b, typename Lz<W>::TW w, W q, W q2) {
+  const W x = a >= q2 ? a - q2 : a;
+  const W t = Lz<W>::mulw(b, w, q);
+  a = x + t;
+  b = x - t + q2;
+}
+template <typename W>
+__device__ __forceinline__ void gs_lz(W& a, W& b, typename Lz<W>::TW w, W q, W q2) {
+  W s = a + b;
+  s = s >= q2 ? s - q2 : s;
+  const W d = a - b + q2;
+  a = s;
+  b = Lz<W>::mulw(d, w, q);
+}
+// [0, 4q) -> [0, q)
+template <typename W>
+__device__ __forceinline__ W canon4(W x, W q, W q2) {
+  x = x >= q2 ? x - q2 : x;
+  return x >= q ? x - q : x;
+}
+
+// K forward stages (s0 .. s0+K-1) on one register group whose element j_r = base + r * 2^tl
+template <typename W, int K>
+__device__ __forceinline__ void fwd_group_lz(W (&x)[1 << K], int base, int tl, int s0, int logn,
+                                             const typename Lz<W>::TW* tw, W q, W q2) {
+  constexpr int R = 1 << K;
+#pragma unroll
+  for (int st = 0; st < K; ++st) {
+    const int hd = R >> (st + 1);
+    const int m = 1 << (s0 + st);
+    const int gshift = logn - s0 - st;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (r & hd) continue;
+      ct_lz(x[r], x[r + hd], tw[m + ((base + (r << tl)) >> gshift)], q, q2);
+    }
+  }
+}
+
+// K inverse stages with t = 2^s0 .. 2^(s0+K-1) on a group j_r = base + r * 2^s0
+template <typename W, int K>
+__device__ __forceinline__ void inv_group_lz(W (&x)[1 << K], int base, int s0, int logn,
+                                             const typename Lz<W>::TW* tw, W q, W q2) {
+  constexpr int R = 1 << K;
+#pragma unroll
+  for (int st = 0; st < K; ++st) {
+    const int hd = 1 << st;
+    const int u = s0 + st;
+    const int h = 1 << (logn - u - 1);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (r & hd) continue;
+      gs_lz(x[r], x[r + hd], tw[h + ((base + (r << s0)) >> (u + 1))], q, q2);
+    }
+  }
+}
+
+template <typename W, int K>
+__device__ __forceinline__ void fwd_pass_lz(W* s, int logn, int s0, const typename Lz<W>::TW* tw, W q, W q2) {
+  constexpr int R = 1 << K;
+  const int tl = logn - s0 - K;
+  for (int vt = threadIdx.x; vt < (1 << (logn - K)); vt += blockDim.x) {
+    const int base = ((vt >> tl) << (logn - s0)) + (vt & ((1 << tl) - 1));
+    W x[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r] = s[swz<W>(base + (r << tl))];
+    fwd_group_lz<W, K>(x, base, tl, s0, logn, tw, q, q2);
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[swz<W>(base + (r << tl))] = x[r];
+  }
+}
+
+template <typename W, int K>
+__device__ __forceinline__ void inv_pass_lz(W* s, int logn, int s0, const typename Lz<W>::TW* tw, W q, W q2) {
+  constexpr int R = 1 << K;
+  for (int vt = threadIdx.x; vt < (1 << (logn - K)); vt += blockDim.x) {
+    const int base = ((vt >> s0) << (s0 + K)) + (vt & ((1 << s0) - 1));
+    W x[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r] = s[swz<W>(base + (r << s0))];
+    inv_group_lz<W, K>(x, base, s0, logn, tw, q, q2);
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[swz<W>(base + (r << s0))] = x[r];
+  }
+}
+
+// Forward transform of s[] except the final radix-16 pass, which the caller
+// runs itself (fwd_last_group) so it can fuse its epilogue.  Remainder pass
+// first: the last pass then leaves 16 consecutive outputs per group.
+template <typename W>
+__device__ __forceinline__ void fwd_lz_but_last(W* s, int logn, const typename Lz<W>::TW* tw, W q, W q2) {
+  const int rem = logn & 3;
+  switch (rem) {
+    case 3: fwd_pass_lz<W, 3>(s, logn, 0, tw, q, q2); __syncthreads(); break;
+    case 2: fwd_pass_lz<W, 2>(s, logn, 0, tw, q, q2); __syncthreads(); break;
+    case 1: fwd_pass_lz<W, 1>(s, logn, 0, tw, q, q2); __syncthreads(); break;
+    default: break;
+  }
+  for (int s0 = rem; s0 + 4 < logn; s0 += 4) {
+    fwd_pass_lz<W, 4>(s, logn, s0, tw, q, q2);
+    __syncthreads();
+  }
+}
+// the last pass for group vt: loads x[16] = outputs 16 vt .. 16 vt + 15 in [0, 4q)
+template <typename W>
+__device__ __forceinline__ void fwd_last_group(const W* s, int vt, int logn, const typename Lz<W>::TW* tw, W q, W q2,
+                                               W (&x)[16]) {
+  const int base = vt << 4;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) x[r] = s[swz<W>(base + r)];
+  fwd_group_lz<W, 4>(x, base, 0, logn - 4, logn, tw, q, q2);
+}
+
+// Full forward transform in place, canonical output.
+template <typename W>
+__device__ __forceinline__ void fwd_lz(W* s, int logn, const typename Lz<W>::TW* tw, W q, W q2) {
+  fwd_lz_but_last(s, logn, tw, q, q2);
+  for (int vt = threadIdx.x; vt < (1 << (logn - 4)); vt += blockDim.x) {
+    W x[16];
+    fwd_last_group(s, vt, logn, tw, q, q2, x);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) s[swz<W>((vt << 4) + r)] = canon4(x[r], q, q2);
+  }
+  __syncthreads();
+}
+
+// Full inverse transform in place (input canonical), times N^{-1}, canonical output.
+// Remainder pass first so the last pass is radix-16 and carries the N^{-1} scaling.
+template <typename W>
+__device__ __forceinline__ void inv_lz(W* s, int logn, const typename Lz<W>::TW* tw, typename Lz<W>::TW ninv, W q,
+                                       W q2) {
+  const int rem = logn & 3;
+  switch (rem) {
+    case 3: inv_pass_lz<W, 3>(s, logn, 0, tw, q, q2); __syncthreads(); break;
+    case 2: inv_pass_lz<W, 2>(s, logn, 0, tw, q, q2); __syncthreads(); break;
+    case 1: inv_pass_lz<W, 1>(s, logn, 0, tw, q, q2); __syncthreads(); break;
+    default: break;
+  }
+  int s0 = rem;
+  for (; s0 + 4 < logn; s0 += 4) {
+    inv_pass_lz<W, 4>(s, logn, s0, tw, q, q2);
+    __syncthreads();
+  }
+  for (int vt = threadIdx.x; vt < (1 << (logn - 4)); vt += blockDim.x) {
+    const int base = ((vt >> s0) << (s0 + 4)) + (vt & ((1 << s0) - 1));
+    W x[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) x[r] = s[swz<W>(base + (r << s0))];
+    inv_group_lz<W, 4>(x, base, s0, logn, tw, q, q2);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      W y = Lz<W>::mulw(x[r], ninv, q);  // [0, 2q)
+      s[swz<W>(base + (r << s0))] = y >= q ? y - q : y;
+    }
+  }
+  __syncthreads();
+}
+
+// stage a limb's twiddle table (N entries) into shared memory
+template <typename TW>
+__device__ __forceinline__ void stage_tw(TW* dst, const TW* __restrict__ src, int n) {
+  const uint4* s4 = reinterpret_cast<const uint4*>(src);
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+  const int words = n * (int)sizeof(TW) / 16;
+  for (int i = threadIdx.x; i < words; i += blockDim.x) d4[i] = __ldg(s4 + i);
+}
+
 }  // namespace hg
