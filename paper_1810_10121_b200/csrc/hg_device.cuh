@@ -24,8 +24,12 @@ struct LimbInfo {
   const ulonglong2* iw;  // {psi^-brv, Shoup(psi^-brv)}
   const uint2* fw32;     // {psi^brv, floor(w 2^32/q)} for small primes (else null)
   const uint2* iw32;
+  const ulonglong2* fwp; // pass-ordered copies for the lazy kernels (conflict-free smem loads)
+  const ulonglong2* iwp;
+  const uint2* fwp32;
+  const uint2* iwp32;
   uint32_t ninv32_s;     // floor(ninv 2^32 / q) for small primes
-  uint32_t small;        // q < 2^31
+  uint32_t small;        // q < 2^30 (32-bit lazy word path)
 };
 
 struct CtxParams {

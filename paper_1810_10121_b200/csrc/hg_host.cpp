@@ -238,7 +238,8 @@ Context::Context(const ContextParamsH& p, int device) : m_p(p), m_device(device)
   HG_CUDA(cudaStreamCreateWithFlags(&m_stream, cudaStreamNonBlocking));
 
   // tables: per limb fw (16N) | iw (16N) | fw32 (8N) | iw32 (8N)
-  const size_t per = 48 * static_cast<size_t>(n);
+  // per limb: fw (16N) | iw (16N) | fw32 (8N) | iw32 (8N) | fwp (16N) | iwp (16N) | fwp32 (8N) | iwp32 (8N)
+  const size_t per = 96 * static_cast<size_t>(n);
   m_tables.alloc(per * nl);
   std::vector<uint8_t> host(per * nl, 0);
   m_psi.resize(nl);
@@ -284,6 +285,52 @@ Context::Context(const ContextParamsH& p, int device) : m_p(p), m_device(device)
       f = M.mul(f, psi);
       b = M.mul(b, psi_inv);
     }
+    // Pass-ordered ("transposed") copies for the lazy kernels (hg_ntt.cuh): within each
+    // stage the entries are regrouped so that lane-consecutive thread groups read
+    // consecutive words (conflict-free shared-memory twiddle loads).  Passes run
+    // remainder-first in both directions.
+    {
+      auto* fwp = reinterpret_cast<uint64_t*>(base + 48 * n);
+      auto* iwp = reinterpret_cast<uint64_t*>(base + 64 * n);
+      auto* fwp32 = reinterpret_cast<uint32_t*>(base + 80 * n);
+      auto* iwp32 = reinterpret_cast<uint32_t*>(base + 88 * n);
+      auto put = [&](uint64_t* d64, uint32_t* d32, const uint64_t* s64, const uint32_t* s32, int64_t dst, int64_t src) {
+        d64[2 * dst] = s64[2 * src];
+        d64[2 * dst + 1] = s64[2 * src + 1];
+        if (small) {
+          d32[2 * dst] = s32[2 * src];
+          d32[2 * dst + 1] = s32[2 * src + 1];
+        }
+      };
+      const int logn = m_logn, rem = logn & 3;
+      std::vector<std::pair<int, int>> passes;  // (s0, K)
+      if (rem) passes.push_back({0, rem});
+      for (int s0 = rem; s0 < logn; s0 += 4) passes.push_back({s0, 4});
+      fwp[0] = fw[0];
+      fwp[1] = fw[1];
+      iwp[0] = iw[0];
+      iwp[1] = iw[1];
+      if (small) {
+        fwp32[0] = fw32[0];
+        fwp32[1] = fw32[1];
+        iwp32[0] = iw32[0];
+        iwp32[1] = iw32[1];
+      }
+      for (auto [s0, K] : passes)
+        for (int st = 0; st < K; ++st) {
+          // forward stage S = s0 + st: old[2^S + g 2^st + i] -> new[2^S + i 2^s0 + g]
+          const int64_t S = s0 + st, nb = int64_t(1) << s0, per_g = int64_t(1) << st;
+          for (int64_t g = 0; g < nb; ++g)
+            for (int64_t ii = 0; ii < per_g; ++ii)
+              put(fwp, fwp32, fw, fw32, (int64_t(1) << S) + ii * nb + g, (int64_t(1) << S) + g * per_g + ii);
+          // inverse stage u = s0 + st, h = 2^(logn-u-1):
+          //   old[h + gi 2^(K-st-1) + ii] -> new[h + ii nbi + gi], nbi = 2^(logn - s0 - K)
+          const int64_t h = int64_t(1) << (logn - S - 1), nbi = int64_t(1) << (logn - s0 - K),
+                        per_i = int64_t(1) << (K - st - 1);
+          for (int64_t gi = 0; gi < nbi; ++gi)
+            for (int64_t ii = 0; ii < per_i; ++ii) put(iwp, iwp32, iw, iw32, h + ii * nbi + gi, h + gi * per_i + ii);
+        }
+    }
     LimbInfo& L = m_kp.limb[i];
     L.q = q;
     L.br_hi = M.br_hi;
@@ -297,6 +344,10 @@ Context::Context(const ContextParamsH& p, int device) : m_p(p), m_device(device)
     L.iw = reinterpret_cast<const ulonglong2*>(dbase + 16 * n);
     L.fw32 = small ? reinterpret_cast<const uint2*>(dbase + 32 * n) : nullptr;
     L.iw32 = small ? reinterpret_cast<const uint2*>(dbase + 40 * n) : nullptr;
+    L.fwp = reinterpret_cast<const ulonglong2*>(dbase + 48 * n);
+    L.iwp = reinterpret_cast<const ulonglong2*>(dbase + 64 * n);
+    L.fwp32 = small ? reinterpret_cast<const uint2*>(dbase + 80 * n) : nullptr;
+    L.iwp32 = small ? reinterpret_cast<const uint2*>(dbase + 88 * n) : nullptr;
   }
   HG_CUDA(cudaMemcpy(m_tables.p, host.data(), host.size(), cudaMemcpyHostToDevice));
   for (int t = 0; t < nl; ++t)

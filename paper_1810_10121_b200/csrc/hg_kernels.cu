@@ -767,6 +767,10 @@ void gemm_groups(const Context& c, const uint64_t* x, int64_t x_items, const int
                  int64_t w_group_stride, const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt, int nl,
                  cudaStream_t s) {
   if (groups <= 0 || mg <= 0) return;
+  if (c.n() % 2048 == 0) {  // IMAD.WIDE kernel (hg_kernels2.cu)
+    k2::gemm(c, x, x_items, idx, w, w_group_stride, oidx, out, groups, mg, kt, nl, s);
+    return;
+  }
   const int64_t n = c.n();
   dim3 grid((unsigned)((n + kGemmThreads - 1) / kGemmThreads), (unsigned)(2 * nl), 1);
   // algorithmic: every input item once (<= groups*kt distinct), every output once; M*K*2(l+1)N modMACs

@@ -60,7 +60,7 @@ struct Cta {
 // batched NTT of rows: row k of limb j at base + (k*nl + j) N
 // ---------------------------------------------------------------------------
 template <typename W, bool INV, bool TWS>
-__global__ void __launch_bounds__(512) k_ntt_lz(uint64_t* __restrict__ base, int nl, int64_t rows, int G,
+__global__ void __launch_bounds__(512, sizeof(W) == 4 ? 2 : 1) k_ntt_lz(uint64_t* __restrict__ base, int nl, int64_t rows, int G,
                                                 const LimbList LL, const CtxParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
   Cta<W, TWS> c(smem, LL, rows, G, P, INV);
@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(512) k_ntt_lz(uint64_t* __restrict__ base, int
 
 // lift signed int64 polys (one per item) into limb j, forward NTT: out[item][nl][N]
 template <typename W, bool TWS>
-__global__ void __launch_bounds__(512) k_lift_ntt_lz(const int64_t* __restrict__ src, uint64_t* __restrict__ out, int nl,
+__global__ void __launch_bounds__(512, sizeof(W) == 4 ? 2 : 1) k_lift_ntt_lz(const int64_t* __restrict__ src, uint64_t* __restrict__ out, int nl,
                                                      int64_t items, int G, const LimbList LL, const CtxParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
   Cta<W, TWS> c(smem, LL, items, G, P, false);
@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(512) k_lift_ntt_lz(const int64_t* __restrict__
 
 // rescale step 1 (poly.hpp:196-205): INTT of the top limb t, centred lift -> int64 [poly][N]
 template <typename W, bool TWS>
-__global__ void __launch_bounds__(512) k_rescale_top_lz(const uint64_t* __restrict__ in, int64_t* __restrict__ cen,
+__global__ void __launch_bounds__(512, sizeof(W) == 4 ? 2 : 1) k_rescale_top_lz(const uint64_t* __restrict__ in, int64_t* __restrict__ cen,
                                                         int nl, int64_t polys, int G, const LimbList LL,
                                                         const CtxParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
@@ -125,7 +125,7 @@ struct RescaleC {
 
 // rescale step 2 (poly.hpp:207-225): out_j = (x_j - NTT_j(lift(c))) * q_t^{-1}
 template <typename W, bool TWS>
-__global__ void __launch_bounds__(512) k_rescale_rest_lz(const uint64_t* __restrict__ in,
+__global__ void __launch_bounds__(512, sizeof(W) == 4 ? 2 : 1) k_rescale_rest_lz(const uint64_t* __restrict__ in,
                                                          const int64_t* __restrict__ cen, uint64_t* __restrict__ out,
                                                          int nl, int64_t polys, int G, const LimbList LL,
                                                          const RescaleC R, const CtxParams P) {
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(512) k_rescale_rest_lz(const uint64_t* __restr
 
 // relinearisation prologue: c2 = INTT(a1 * b1) per (item, limb i)  (ckks_backend.hpp:509)
 template <typename W, bool TWS>
-__global__ void __launch_bounds__(512) k_relin_c2_lz(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
+__global__ void __launch_bounds__(512, sizeof(W) == 4 ? 2 : 1) k_relin_c2_lz(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
                                                      int64_t a_stride, int64_t b_stride, int64_t a1_off, int64_t b1_off,
                                                      uint64_t* __restrict__ c2, int nl, int64_t items, int G,
                                                      const LimbList LL, const CtxParams P) {
@@ -198,7 +198,7 @@ struct RelinC {
 };
 
 template <typename W, bool TWS, bool GIVEN_D>
-__global__ void __launch_bounds__(512) k_relin_lz(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
+__global__ void __launch_bounds__(512, 1) k_relin_lz(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
                                                   int64_t a_stride, int64_t b_stride, const uint64_t* __restrict__ c2,
                                                   const uint64_t* __restrict__ kval,
                                                   const uint64_t* __restrict__ kpack, uint64_t* __restrict__ out,
@@ -301,6 +301,163 @@ __global__ void __launch_bounds__(512) k_relin_lz(const uint64_t* __restrict__ a
       }
       o0[r] = add_mod(r0, d0, Q);
       o1[r] = add_mod(r1, d1, Q);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Grouped modular GEMM for the fused weighted sum (Dot/Conv/Pool before the
+// single rescale; ckks_backend.hpp:381-411, runtime.hpp:1027-1221):
+//   out[oidx[g*mg+m]][p][j][col] = sum_t W[g][m][t][j] * x[idx[g*kt+t]][p][j][col]  (mod q_j)
+// Small limbs (q < 2^30): one IMAD.WIDE.U32 per MAC into a 64-bit accumulator,
+// folded (acc_hi * (2^32 mod q) + acc_lo) every floor(2^63/q^2) terms.
+// Wide limbs: x and w split into b = ceil(bits(q)/2)-bit halves, three 64-bit
+// accumulators (hh, cross, ll), recombined with 2^b, 2^2b mod q at the end.
+// Grid: x = (m-tile fastest, group), y = column tile, z = (poly, limb of class).
+// ---------------------------------------------------------------------------
+constexpr int kGT = 256;  // threads per CTA
+constexpr int kKC = 32;   // terms staged per chunk
+
+template <bool WIDE, int MT, int C>
+__global__ void __launch_bounds__(kGT) k_gemm_lz(const uint64_t* __restrict__ x, const int32_t* __restrict__ idx,
+                                                 const uint64_t* __restrict__ w, int64_t w_group_stride,
+                                                 const int32_t* __restrict__ oidx, uint64_t* __restrict__ out, int mg,
+                                                 int kt, int nl, const LimbList LL, const CtxParams P) {
+  constexpr int WW = WIDE ? 2 : 1;
+  constexpr int NA = WIDE ? 3 : 1;
+  __shared__ __align__(16) uint32_t ws[kKC][MT * WW];
+  __shared__ int32_t xs[kKC];
+  const int mtiles = (mg + MT - 1) / MT;
+  const int mt = blockIdx.x % mtiles;
+  const int64_t g = blockIdx.x / mtiles;
+  const int m0 = mt * MT;
+  const int p = blockIdx.z / LL.count;
+  const int j = LL.limb[blockIdx.z % LL.count];
+  const LimbInfo& L = P.limb[j];
+  const int64_t n = P.n;
+  const int64_t col0 = ((int64_t)blockIdx.y * kGT + threadIdx.x) * C;
+  const int64_t item_words = 2 * (int64_t)nl * n;
+  const uint64_t* xrow = x + ((int64_t)p * nl + j) * n + col0;
+  const uint64_t q = L.q;
+  const int qbits = 64 - __clzll((long long)q);
+  const int b = (qbits + 1) / 2;
+  const uint64_t bmask = (1ull << b) - 1;
+  // terms between folds: keeps every accumulator below 2^64
+  uint64_t Fq;
+  if (WIDE) Fq = (1ull << 62) >> (2 * b);
+  else Fq = (1ull << 63) / (q * q);
+  const int F = (int)max((uint64_t)1, min((uint64_t)1 << 30, Fq));
+  const uint64_t r32 = (1ull << 32) % q;
+  int since = 0;
+
+  uint64_t acc[MT][C][NA];
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int c = 0; c < C; ++c)
+#pragma unroll
+      for (int a = 0; a < NA; ++a) acc[m][c][a] = 0;
+
+  const bool live = col0 < n;
+  for (int t0 = 0; t0 < kt; t0 += kKC) {
+    const int tc = min(kKC, kt - t0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kKC * MT; e += kGT) {
+      const int tt = e / MT, m = e % MT;
+      uint64_t v = 0;
+      if (tt < tc && m0 + m < mg) v = w[g * w_group_stride + ((int64_t)(m0 + m) * kt + t0 + tt) * nl + j];
+      if (WIDE) {
+        ws[tt][2 * m] = (uint32_t)(v & bmask);
+        ws[tt][2 * m + 1] = (uint32_t)(v >> b);
+      } else {
+        ws[tt][m] = (uint32_t)v;
+      }
+    }
+    if (threadIdx.x < kKC) xs[threadIdx.x] = threadIdx.x < tc ? idx[g * kt + t0 + threadIdx.x] : 0;
+    __syncthreads();
+    if (!live) continue;
+    for (int f0 = 0; f0 < tc;) {
+      const int f1 = min(tc, f0 + F);
+      if (since + (f1 - f0) > F) {
+        // fold: small limbs acc_hi * (2^32 mod q) + acc_lo (< 2^63); wide limbs a full reduction
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+#pragma unroll
+            for (int a = 0; a < NA; ++a) {
+              if (WIDE) acc[m][c][a] = reduce128(acc[m][c][a], 0, L);
+              else acc[m][c][a] = (acc[m][c][a] >> 32) * r32 + (acc[m][c][a] & 0xffffffffull);
+            }
+        since = 0;
+      }
+      since += f1 - f0;
+      for (int tt = f0; tt < f1; ++tt) {
+        const uint64_t* xp = xrow + (int64_t)xs[tt] * item_words;
+        uint64_t xv[C];
+        if (C == 1) {
+          xv[0] = __ldg(xp);
+        } else {
+#pragma unroll
+          for (int c = 0; c < C; c += 2) {
+            const ulonglong2 v2 = __ldg(reinterpret_cast<const ulonglong2*>(xp + c));
+            xv[c] = v2.x;
+            xv[c + 1] = v2.y;
+          }
+        }
+        if (WIDE) {
+          uint32_t xl[C], xh[C];
+#pragma unroll
+          for (int c = 0; c < C; ++c) {
+            xl[c] = (uint32_t)(xv[c] & bmask);
+            xh[c] = (uint32_t)(xv[c] >> b);
+          }
+#pragma unroll
+          for (int m = 0; m < MT; ++m) {
+            const uint32_t wl = ws[tt][2 * m], wh = ws[tt][2 * m + 1];
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+              acc[m][c][0] += (uint64_t)xh[c] * wh;
+              acc[m][c][1] += (uint64_t)xh[c] * wl;
+              acc[m][c][1] += (uint64_t)xl[c] * wh;
+              acc[m][c][2] += (uint64_t)xl[c] * wl;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int m = 0; m < MT; ++m) {
+            const uint32_t wv = ws[tt][m];
+#pragma unroll
+            for (int c = 0; c < C; ++c) acc[m][c][0] += (uint64_t)(uint32_t)xv[c] * wv;
+          }
+        }
+      }
+      f0 = f1;
+    }
+  }
+  if (!live) return;
+  const uint64_t c2b = WIDE ? mul_mod((1ull << b) % q, (1ull << b) % q, L) : 0, cb = WIDE ? (1ull << b) % q : 0;
+#pragma unroll
+  for (int m = 0; m < MT; ++m) {
+    if (m0 + m >= mg) break;
+    const int64_t oi = oidx ? (int64_t)oidx[g * mg + m0 + m] : g * mg + m0 + m;
+    uint64_t* o = out + (oi * 2 * nl + (int64_t)p * nl + j) * n + col0;
+    uint64_t r[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      if (WIDE) {
+        const uint64_t hh = reduce128(acc[m][c][0], 0, L), md = reduce128(acc[m][c][1], 0, L),
+                       ll = reduce128(acc[m][c][2], 0, L);
+        r[c] = add_mod(add_mod(mul_mod(hh, c2b, L), mul_mod(md, cb, L), q), ll, q);
+      } else {
+        r[c] = reduce128(acc[m][c][0], 0, L);
+      }
+    }
+    if (C == 1) {
+      o[0] = r[0];
+    } else {
+#pragma unroll
+      for (int c = 0; c < C; c += 2) *reinterpret_cast<ulonglong2*>(o + c) = make_ulonglong2(r[c], r[c + 1]);
     }
   }
 }
@@ -498,6 +655,41 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
     HG_RELIN_LAUNCH(uint64_t, cl.wide, false)
   }
 #undef HG_RELIN_LAUNCH
+}
+
+void gemm(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* idx, const uint64_t* w,
+          int64_t w_group_stride, const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt, int nl,
+          cudaStream_t s) {
+  if (groups <= 0 || mg <= 0) return;
+  const Classes cl = classify(c, 0, nl);
+  const int64_t n = c.n();
+  const double item_bytes = 2.0 * nl * n * 8;
+  const double in_items = std::min<double>((double)groups * kt, (double)x_items);
+  auto launch = [&](const LimbList& LL, bool wide) {
+    if (LL.count == 0) return;
+    const double frac = (double)LL.count / nl;
+    const double gb = frac * (in_items + (double)groups * mg) * item_bytes;
+    const double gm = frac * (double)groups * mg * kt * 2.0 * nl * n;
+    int MT, C;
+    if (wide) { MT = mg <= 4 ? 4 : 8; C = mg <= 4 ? 2 : 1; }
+    else { MT = mg <= 4 ? 4 : mg <= 8 ? 8 : 16; C = mg <= 8 ? 4 : 2; }
+    const int mtiles = (mg + MT - 1) / MT;
+    dim3 grid((unsigned)(mtiles * groups), (unsigned)((n + (int64_t)kGT * C - 1) / ((int64_t)kGT * C)),
+              (unsigned)(2 * LL.count));
+    c.kt_begin("k_gemm_lz", s, gb, gm);
+    if (wide) {
+      if (MT == 4) k_gemm_lz<true, 4, 2><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
+      else k_gemm_lz<true, 8, 1><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
+    } else {
+      if (MT == 4) k_gemm_lz<false, 4, 4><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
+      else if (MT == 8) k_gemm_lz<false, 8, 4><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
+      else k_gemm_lz<false, 16, 2><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
+    }
+    c.kt_end(s);
+    HG_CUDA(cudaGetLastError());
+  };
+  launch(cl.small, false);
+  launch(cl.wide, true);
 }
 
 void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_stride, int64_t b_stride,

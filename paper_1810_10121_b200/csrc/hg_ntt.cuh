@@ -219,16 +219,16 @@ template <>
 struct Lz<uint32_t> {
   using TW = uint2;
   static __device__ __forceinline__ uint32_t mulw(uint32_t x, TW w, uint32_t q) { return x * w.x - __umulhi(x, w.y) * q; }
-  static __device__ __forceinline__ const TW* fwd_table(const LimbInfo& L) { return L.fw32; }
-  static __device__ __forceinline__ const TW* inv_table(const LimbInfo& L) { return L.iw32; }
+  static __device__ __forceinline__ const TW* fwd_table(const LimbInfo& L) { return L.fwp32; }
+  static __device__ __forceinline__ const TW* inv_table(const LimbInfo& L) { return L.iwp32; }
   static __device__ __forceinline__ TW ninv(const LimbInfo& L) { return make_uint2((uint32_t)L.ninv, L.ninv32_s); }
 };
 template <>
 struct Lz<uint64_t> {
   using TW = ulonglong2;
   static __device__ __forceinline__ uint64_t mulw(uint64_t x, TW w, uint64_t q) { return x * w.x - __umul64hi(x, w.y) * q; }
-  static __device__ __forceinline__ const TW* fwd_table(const LimbInfo& L) { return L.fw; }
-  static __device__ __forceinline__ const TW* inv_table(const LimbInfo& L) { return L.iw; }
+  static __device__ __forceinline__ const TW* fwd_table(const LimbInfo& L) { return L.fwp; }
+  static __device__ __forceinline__ const TW* inv_table(const LimbInfo& L) { return L.iwp; }
   static __device__ __forceinline__ TW ninv(const LimbInfo& L) { return make_ulonglong2(L.ninv, L.ninv_s); }
 };
 
@@ -254,38 +254,39 @@ __device__ __forceinline__ W canon4(W x, W q, W q2) {
   return x >= q ? x - q : x;
 }
 
-// K forward stages (s0 .. s0+K-1) on one register group whose element j_r = base + r * 2^tl
+// K forward stages (s0 .. s0+K-1) on one register group of block g (elements
+// j_r = g 2^(logn-s0) + off + r 2^tl).  Twiddles come from the pass-ordered
+// table: stage S = s0+st, slot i = r >> (K-st) lives at 2^S + i 2^s0 + g.
 template <typename W, int K>
-__device__ __forceinline__ void fwd_group_lz(W (&x)[1 << K], int base, int tl, int s0, int logn,
-                                             const typename Lz<W>::TW* tw, W q, W q2) {
+__device__ __forceinline__ void fwd_group_lz(W (&x)[1 << K], int g, int s0, const typename Lz<W>::TW* tw, W q, W q2) {
   constexpr int R = 1 << K;
 #pragma unroll
   for (int st = 0; st < K; ++st) {
     const int hd = R >> (st + 1);
     const int m = 1 << (s0 + st);
-    const int gshift = logn - s0 - st;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       if (r & hd) continue;
-      ct_lz(x[r], x[r + hd], tw[m + ((base + (r << tl)) >> gshift)], q, q2);
+      ct_lz(x[r], x[r + hd], tw[m + ((r >> (K - st)) << s0) + g], q, q2);
     }
   }
 }
 
-// K inverse stages with t = 2^s0 .. 2^(s0+K-1) on a group j_r = base + r * 2^s0
+// K inverse stages with t = 2^s0 .. 2^(s0+K-1) on the group of block gi = vt >> s0.
+// Pass-ordered table: stage u = s0+st, h = 2^(logn-u-1), slot i = r >> (st+1) at h + i 2^(logn-s0-K) + gi.
 template <typename W, int K>
-__device__ __forceinline__ void inv_group_lz(W (&x)[1 << K], int base, int s0, int logn,
+__device__ __forceinline__ void inv_group_lz(W (&x)[1 << K], int gi, int s0, int logn,
                                              const typename Lz<W>::TW* tw, W q, W q2) {
   constexpr int R = 1 << K;
+  const int nbs = logn - s0 - K;
 #pragma unroll
   for (int st = 0; st < K; ++st) {
     const int hd = 1 << st;
-    const int u = s0 + st;
-    const int h = 1 << (logn - u - 1);
+    const int h = 1 << (logn - s0 - st - 1);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       if (r & hd) continue;
-      gs_lz(x[r], x[r + hd], tw[h + ((base + (r << s0)) >> (u + 1))], q, q2);
+      gs_lz(x[r], x[r + hd], tw[h + ((r >> (st + 1)) << nbs) + gi], q, q2);
     }
   }
 }
@@ -295,11 +296,12 @@ __device__ __forceinline__ void fwd_pass_lz(W* s, int logn, int s0, const typena
   constexpr int R = 1 << K;
   const int tl = logn - s0 - K;
   for (int vt = threadIdx.x; vt < (1 << (logn - K)); vt += blockDim.x) {
-    const int base = ((vt >> tl) << (logn - s0)) + (vt & ((1 << tl) - 1));
+    const int g = vt >> tl;
+    const int base = (g << (logn - s0)) + (vt & ((1 << tl) - 1));
     W x[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) x[r] = s[swz<W>(base + (r << tl))];
-    fwd_group_lz<W, K>(x, base, tl, s0, logn, tw, q, q2);
+    fwd_group_lz<W, K>(x, g, s0, tw, q, q2);
 #pragma unroll
     for (int r = 0; r < R; ++r) s[swz<W>(base + (r << tl))] = x[r];
   }
@@ -309,11 +311,12 @@ template <typename W, int K>
 __device__ __forceinline__ void inv_pass_lz(W* s, int logn, int s0, const typename Lz<W>::TW* tw, W q, W q2) {
   constexpr int R = 1 << K;
   for (int vt = threadIdx.x; vt < (1 << (logn - K)); vt += blockDim.x) {
-    const int base = ((vt >> s0) << (s0 + K)) + (vt & ((1 << s0) - 1));
+    const int gi = vt >> s0;
+    const int base = (gi << (s0 + K)) + (vt & ((1 << s0) - 1));
     W x[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) x[r] = s[swz<W>(base + (r << s0))];
-    inv_group_lz<W, K>(x, base, s0, logn, tw, q, q2);
+    inv_group_lz<W, K>(x, gi, s0, logn, tw, q, q2);
 #pragma unroll
     for (int r = 0; r < R; ++r) s[swz<W>(base + (r << s0))] = x[r];
   }
@@ -343,7 +346,7 @@ __device__ __forceinline__ void fwd_last_group(const W* s, int vt, int logn, con
   const int base = vt << 4;
 #pragma unroll
   for (int r = 0; r < 16; ++r) x[r] = s[swz<W>(base + r)];
-  fwd_group_lz<W, 4>(x, base, 0, logn - 4, logn, tw, q, q2);
+  fwd_group_lz<W, 4>(x, vt, logn - 4, tw, q, q2);
 }
 
 // Full forward transform in place, canonical output.
@@ -377,11 +380,12 @@ __device__ __forceinline__ void inv_lz(W* s, int logn, const typename Lz<W>::TW*
     __syncthreads();
   }
   for (int vt = threadIdx.x; vt < (1 << (logn - 4)); vt += blockDim.x) {
-    const int base = ((vt >> s0) << (s0 + 4)) + (vt & ((1 << s0) - 1));
+    const int gi = vt >> s0;
+    const int base = (gi << (s0 + 4)) + (vt & ((1 << s0) - 1));
     W x[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) x[r] = s[swz<W>(base + (r << s0))];
-    inv_group_lz<W, 4>(x, base, s0, logn, tw, q, q2);
+    inv_group_lz<W, 4>(x, gi, s0, logn, tw, q, q2);
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       W y = Lz<W>::mulw(x[r], ninv, q);  // [0, 2q)
