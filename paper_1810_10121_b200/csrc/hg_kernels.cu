@@ -840,7 +840,7 @@ void mul_relin(const Context& c, const Keys& keys, const uint64_t* a, const uint
   if (items <= 0) return;
   check(keys.has_relin, HG_EINTERNAL, "relinearisation key missing");
   const int64_t pw = (int64_t)nl * c.n();
-  if (c.n() <= 8192) {
+  if (c.logn() <= 14) {
     k2::relin_c2(c, a, b, 2 * pw, 2 * pw, pw, pw, c2, items, nl, s);
     k2::relin(c, keys, a, b, 2 * pw, 2 * pw, false, c2, out, items, nl, s);
     return;
@@ -873,7 +873,7 @@ void relin3(const Context& c, const Keys& keys, const uint64_t* in3, uint64_t* o
   for (int64_t it = 0; it < items; ++it)
     HG_CUDA(cudaMemcpyAsync(c2 + it * pw, in3 + it * 3 * pw + 2 * pw, pw * 8, cudaMemcpyDeviceToDevice, s));
   ntt(c, c2, items * nl, nl, true, s);
-  if (c.n() <= 8192) {
+  if (c.logn() <= 14) {
     k2::relin(c, keys, in3, nullptr, 3 * pw, 0, true, c2, out2, items, nl, s);
     return;
   }

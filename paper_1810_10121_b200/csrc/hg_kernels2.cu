@@ -1,13 +1,12 @@
-// hg_kernels2.cu -- limb-stationary transform kernels (sm_100a).
+// hg_kernels2.cu -- limb-stationary transform kernels and the fused GEMM (sm_100a).
 //
-// Every CTA owns ONE RNS limb and a group of rows (polys/items) of that limb:
-// the limb's twiddle table is staged into shared memory once and reused for
-// all rows of the group (the table is as large as the data, so re-reading it
-// per transform from L2 dominated the first version).  Limbs are launched in
-// two classes: primes < 2^30 run on 32-bit words (Harvey lazy butterflies in
-// [0, 4q)), wider primes on 64-bit words.  Outputs are canonical, hence
-// identical to the reference (ring.hpp:263-301, poly.hpp:190-228,
-// ckks_backend.hpp:508-554).
+// Every transform CTA owns ONE RNS limb and a group of rows (polys/items) of
+// that limb: the limb's (pass-ordered) twiddle table is staged into shared
+// memory once and reused for all rows of the group.  Limbs are launched in two
+// classes: primes < 2^30 run on 32-bit words, wider primes on 64-bit words.
+// The ring degree is a template parameter (hg_ntt_lz.cuh).  Outputs are
+// canonical, hence identical to the reference (ring.hpp:263-301,
+// poly.hpp:190-228, ckks_backend.hpp:381-411, 508-554).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -15,7 +14,7 @@
 
 #include "hg_device.cuh"
 #include "hg_internal.hpp"
-#include "hg_ntt.cuh"
+#include "hg_ntt_lz.cuh"
 
 namespace hg {
 namespace {
@@ -25,18 +24,26 @@ struct LimbList {
   int limb[HG_MAX_LIMBS];
 };
 
-template <typename W>
-__device__ __forceinline__ W lift_w(int64_t v, uint64_t q) {
-  return (W)lift_signed(v, q);
-}
+constexpr size_t kSmemCap = 227 * 1024;
 
-// Common CTA prologue: figure out the limb and the row range, stage twiddles.
-template <typename W, bool TWS>
+template <typename W, int LOGN>
+struct Cfg {
+  static constexpr int N = 1 << LOGN;
+  static constexpr size_t data_bytes = ((size_t)lz::smem_words<LOGN>() * sizeof(W) + 15) / 16 * 16;
+  static constexpr size_t tw_bytes = (size_t)N * sizeof(lz::TWT<W>);
+  static constexpr bool TWS = data_bytes + tw_bytes <= kSmemCap;
+  static constexpr size_t smem = data_bytes + (TWS ? tw_bytes : 0);
+  static constexpr int threads = N / 16 < 512 ? N / 16 : 512;
+  static constexpr int min_blocks = (sizeof(W) == 4 && 2 * smem <= kSmemCap && threads <= 512) ? 2 : 1;
+};
+
+// CTA prologue: limb, row range, twiddles (staged in shared memory when they fit)
+template <typename W, int LOGN>
 struct Cta {
   int limb, r0, r1;
   const LimbInfo* L;
   W* s;
-  const typename Lz<W>::TW* tw;
+  const lz::TWT<W>* tw;
   __device__ __forceinline__ Cta(uint64_t* smem, const LimbList& LL, int64_t rows, int G, const CtxParams& P,
                                  bool inverse) {
     limb = LL.limb[blockIdx.x % LL.count];
@@ -45,10 +52,10 @@ struct Cta {
     r1 = (int)min((int64_t)(g + 1) * G, rows);
     L = &P.limb[limb];
     s = reinterpret_cast<W*>(smem);
-    const typename Lz<W>::TW* src = inverse ? Lz<W>::inv_table(*L) : Lz<W>::fwd_table(*L);
-    if (TWS) {
-      auto* t = reinterpret_cast<typename Lz<W>::TW*>(reinterpret_cast<uint8_t*>(smem) + P.n * sizeof(W));
-      stage_tw(t, src, (int)P.n);
+    const lz::TWT<W>* src = inverse ? Lz<W>::inv_table(*L) : Lz<W>::fwd_table(*L);
+    if constexpr (Cfg<W, LOGN>::TWS) {
+      auto* t = reinterpret_cast<lz::TWT<W>*>(reinterpret_cast<uint8_t*>(smem) + Cfg<W, LOGN>::data_bytes);
+      stage_tw(t, src, Cfg<W, LOGN>::N);
       tw = t;
     } else {
       tw = src;
@@ -56,62 +63,61 @@ struct Cta {
   }
 };
 
+#define HG_KERNEL template <typename W, int LOGN> __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_blocks)
+
 // ---------------------------------------------------------------------------
 // batched NTT of rows: row k of limb j at base + (k*nl + j) N
 // ---------------------------------------------------------------------------
-template <typename W, bool INV, bool TWS>
-__global__ void __launch_bounds__(512, sizeof(W) == 4 ? 2 : 1) k_ntt_lz(uint64_t* __restrict__ base, int nl, int64_t rows, int G,
-                                                const LimbList LL, const CtxParams P) {
+template <typename W, int LOGN, bool INV>
+__global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_blocks)
+    k_ntt_t(uint64_t* __restrict__ base, int nl, int64_t rows, int G, const LimbList LL, const CtxParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
-  Cta<W, TWS> c(smem, LL, rows, G, P, INV);
-  const int n = (int)P.n;
+  Cta<W, LOGN> c(smem, LL, rows, G, P, INV);
+  constexpr int n = 1 << LOGN;
   const W q = (W)c.L->q, q2 = q + q;
   for (int r = c.r0; r < c.r1; ++r) {
     uint64_t* g = base + ((int64_t)r * nl + c.limb) * n;
-    load_limb(c.s, g, n);
+    lz::load<W, LOGN>(c.s, g);
     __syncthreads();
-    if (INV) inv_lz<W>(c.s, P.logn, c.tw, Lz<W>::ninv(*c.L), q, q2);
-    else fwd_lz<W>(c.s, P.logn, c.tw, q, q2);
-    store_limb(g, c.s, n);
+    if (INV) lz::inv<W, LOGN>(c.s, c.tw, Lz<W>::ninv(*c.L), q, q2);
+    else lz::fwd<W, LOGN>(c.s, c.tw, q, q2);
+    lz::store<W, LOGN>(g, c.s);
     __syncthreads();
   }
 }
 
 // lift signed int64 polys (one per item) into limb j, forward NTT: out[item][nl][N]
-template <typename W, bool TWS>
-__global__ void __launch_bounds__(512, sizeof(W) == 4 ? 2 : 1) k_lift_ntt_lz(const int64_t* __restrict__ src, uint64_t* __restrict__ out, int nl,
-                                                     int64_t items, int G, const LimbList LL, const CtxParams P) {
+HG_KERNEL k_lift_ntt_t(const int64_t* __restrict__ src, uint64_t* __restrict__ out, int nl, int64_t items, int G,
+                       const LimbList LL, const CtxParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
-  Cta<W, TWS> c(smem, LL, items, G, P, false);
-  const int n = (int)P.n;
+  Cta<W, LOGN> c(smem, LL, items, G, P, false);
+  constexpr int n = 1 << LOGN;
   const W q = (W)c.L->q, q2 = q + q;
   for (int r = c.r0; r < c.r1; ++r) {
     const int64_t* g = src + (int64_t)r * n;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) c.s[swz<W>(i)] = lift_w<W>(g[i], c.L->q);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) c.s[lz::padj(i)] = (W)lift_signed(g[i], c.L->q);
     __syncthreads();
-    fwd_lz<W>(c.s, P.logn, c.tw, q, q2);
-    store_limb(out + ((int64_t)r * nl + c.limb) * n, c.s, n);
+    lz::fwd<W, LOGN>(c.s, c.tw, q, q2);
+    lz::store<W, LOGN>(out + ((int64_t)r * nl + c.limb) * n, c.s);
     __syncthreads();
   }
 }
 
 // rescale step 1 (poly.hpp:196-205): INTT of the top limb t, centred lift -> int64 [poly][N]
-template <typename W, bool TWS>
-__global__ void __launch_bounds__(512, sizeof(W) == 4 ? 2 : 1) k_rescale_top_lz(const uint64_t* __restrict__ in, int64_t* __restrict__ cen,
-                                                        int nl, int64_t polys, int G, const LimbList LL,
-                                                        const CtxParams P) {
+HG_KERNEL k_rescale_top_t(const uint64_t* __restrict__ in, int64_t* __restrict__ cen, int nl, int64_t polys, int G,
+                          const LimbList LL, const CtxParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
-  Cta<W, TWS> c(smem, LL, polys, G, P, true);
-  const int n = (int)P.n;
+  Cta<W, LOGN> c(smem, LL, polys, G, P, true);
+  constexpr int n = 1 << LOGN;
   const W q = (W)c.L->q, q2 = q + q;
   const uint64_t half = c.L->q / 2;
   for (int r = c.r0; r < c.r1; ++r) {
-    load_limb(c.s, in + ((int64_t)r * nl + c.limb) * n, n);
+    lz::load<W, LOGN>(c.s, in + ((int64_t)r * nl + c.limb) * n);
     __syncthreads();
-    inv_lz<W>(c.s, P.logn, c.tw, Lz<W>::ninv(*c.L), q, q2);
+    lz::inv<W, LOGN>(c.s, c.tw, Lz<W>::ninv(*c.L), q, q2);
     int64_t* o = cen + (int64_t)r * n;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const uint64_t v = c.s[swz<W>(i)];
+      const uint64_t v = c.s[lz::padj(i)];
       o[i] = v > half ? (int64_t)v - (int64_t)c.L->q : (int64_t)v;
     }
     __syncthreads();
@@ -124,35 +130,33 @@ struct RescaleC {
 };
 
 // rescale step 2 (poly.hpp:207-225): out_j = (x_j - NTT_j(lift(c))) * q_t^{-1}
-template <typename W, bool TWS>
-__global__ void __launch_bounds__(512, sizeof(W) == 4 ? 2 : 1) k_rescale_rest_lz(const uint64_t* __restrict__ in,
-                                                         const int64_t* __restrict__ cen, uint64_t* __restrict__ out,
-                                                         int nl, int64_t polys, int G, const LimbList LL,
-                                                         const RescaleC R, const CtxParams P) {
+HG_KERNEL k_rescale_rest_t(const uint64_t* __restrict__ in, const int64_t* __restrict__ cen,
+                           uint64_t* __restrict__ out, int nl, int64_t polys, int G, const LimbList LL,
+                           const RescaleC R, const CtxParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
-  Cta<W, TWS> c(smem, LL, polys, G, P, false);
-  const int n = (int)P.n, t = nl - 1, j = c.limb;
+  Cta<W, LOGN> c(smem, LL, polys, G, P, false);
+  constexpr int n = 1 << LOGN;
+  const int t = nl - 1, j = c.limb;
   const W q = (W)c.L->q, q2 = q + q;
+  const uint64_t Q = c.L->q, inv = R.inv[j], inv_s = R.inv_s[j];
   for (int r = c.r0; r < c.r1; ++r) {
     const int64_t* cv = cen + (int64_t)r * n;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) c.s[swz<W>(i)] = lift_w<W>(cv[i], c.L->q);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) c.s[lz::padj(i)] = (W)lift_signed(cv[i], Q);
     __syncthreads();
-    fwd_lz_but_last(c.s, P.logn, c.tw, q, q2);
+    lz::fwd_but_last<W, LOGN>(c.s, c.tw, q, q2);
     const uint64_t* x = in + ((int64_t)r * nl + j) * n;
     uint64_t* o = out + ((int64_t)r * t + j) * n;
     for (int vt = threadIdx.x; vt < (n >> 4); vt += blockDim.x) {
       W y[16];
-      fwd_last_group(c.s, vt, P.logn, c.tw, q, q2, y);
+      lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, y);
       const ulonglong2* x2 = reinterpret_cast<const ulonglong2*>(x + (vt << 4));
       ulonglong2* o2 = reinterpret_cast<ulonglong2*>(o + (vt << 4));
 #pragma unroll
       for (int h = 0; h < 8; ++h) {
         const ulonglong2 xv = x2[h];
-        ulonglong2 ov;
         const uint64_t c0 = canon4<W>(y[2 * h], q, q2), c1 = canon4<W>(y[2 * h + 1], q, q2);
-        ov.x = mul_shoup64(sub_mod(xv.x, c0, c.L->q), R.inv[j], R.inv_s[j], c.L->q);
-        ov.y = mul_shoup64(sub_mod(xv.y, c1, c.L->q), R.inv[j], R.inv_s[j], c.L->q);
-        o2[h] = ov;
+        o2[h] = make_ulonglong2(mul_shoup64(sub_mod(xv.x, c0, Q), inv, inv_s, Q),
+                                mul_shoup64(sub_mod(xv.y, c1, Q), inv, inv_s, Q));
       }
     }
     __syncthreads();
@@ -160,36 +164,35 @@ __global__ void __launch_bounds__(512, sizeof(W) == 4 ? 2 : 1) k_rescale_rest_lz
 }
 
 // relinearisation prologue: c2 = INTT(a1 * b1) per (item, limb i)  (ckks_backend.hpp:509)
-template <typename W, bool TWS>
-__global__ void __launch_bounds__(512, sizeof(W) == 4 ? 2 : 1) k_relin_c2_lz(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
-                                                     int64_t a_stride, int64_t b_stride, int64_t a1_off, int64_t b1_off,
-                                                     uint64_t* __restrict__ c2, int nl, int64_t items, int G,
-                                                     const LimbList LL, const CtxParams P) {
+HG_KERNEL k_relin_c2_t(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int64_t a_stride,
+                       int64_t b_stride, int64_t a1_off, int64_t b1_off, uint64_t* __restrict__ c2, int nl,
+                       int64_t items, int G, const LimbList LL, const CtxParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
-  Cta<W, TWS> c(smem, LL, items, G, P, true);
-  const int n = (int)P.n;
+  Cta<W, LOGN> c(smem, LL, items, G, P, true);
+  constexpr int n = 1 << LOGN;
   const W q = (W)c.L->q, q2 = q + q;
   for (int r = c.r0; r < c.r1; ++r) {
     const uint64_t* x1 = a + r * a_stride + a1_off + (int64_t)c.limb * n;
     const uint64_t* y1 = b + r * b_stride + b1_off + (int64_t)c.limb * n;
-    for (int k = threadIdx.x; k < n; k += blockDim.x) c.s[swz<W>(k)] = (W)mul_mod(x1[k], y1[k], *c.L);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) c.s[lz::padj(k)] = (W)mul_mod(x1[k], y1[k], *c.L);
     __syncthreads();
-    inv_lz<W>(c.s, P.logn, c.tw, Lz<W>::ninv(*c.L), q, q2);
-    store_limb(c2 + ((int64_t)r * nl + c.limb) * n, c.s, n);
+    lz::inv<W, LOGN>(c.s, c.tw, Lz<W>::ninv(*c.L), q, q2);
+    lz::store<W, LOGN>(c2 + ((int64_t)r * nl + c.limb) * n, c.s);
     __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------------------
 // Relinearisation key switch (ckks_backend.hpp:508-554), one CTA per (limb j,
-// group of items): for every source residue i <= l and digit d < D_i the
-// digit (c2_i >> 15d) & 0x7FFF is staged, forward-transformed mod q_j with the
-// staged twiddles, and its last radix-16 pass feeds the key MAC directly from
-// registers: thread vt owns evaluations 16 vt .. 16 vt + 15 for the whole
-// item, so the two accumulators never leave registers.
-//   small limbs: packed key words (ws32 << 32 | w); acc += lazy Shoup, kept in [0, 2q)
-//   wide limbs : key value + its 64-bit Shoup constant; acc canonical
-// Epilogue adds d0 = a0 b0 and d1 = a0 b1 + a1 b0 (or given d0, d1 for size-3 inputs).
+// group of items), blockDim = N/16: thread vt owns evaluations 16 vt .. 16 vt+15.
+// For every source residue i <= l and digit d < D_i the digit (c2_i >> 15d) &
+// 0x7FFF is staged, transformed mod q_j, and its last radix-16 pass feeds the
+// key MAC straight from registers.  The accumulators stay in registers across
+// all rows (ACC_GLOBAL: 64-bit limbs at N >= 16384 accumulate in the output,
+// which is L2-resident while the CTA works on it).
+//   32-bit limbs: packed key words (ws32 << 32 | w); acc += lazy Shoup in [0, 2q)
+//   64-bit limbs: key value + 64-bit Shoup constant; acc canonical
+// Epilogue adds d0 = a0 b0, d1 = a0 b1 + a1 b0 (or given d0, d1).
 // ---------------------------------------------------------------------------
 struct RelinC {
   int rows0[HG_MAX_LIMBS];
@@ -197,39 +200,54 @@ struct RelinC {
   int64_t key_poly_words;  // (L+1) N
 };
 
-template <typename W, bool TWS, bool GIVEN_D>
-__global__ void __launch_bounds__(512, 1) k_relin_lz(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b,
-                                                  int64_t a_stride, int64_t b_stride, const uint64_t* __restrict__ c2,
-                                                  const uint64_t* __restrict__ kval,
-                                                  const uint64_t* __restrict__ kpack, uint64_t* __restrict__ out,
-                                                  int nl, int64_t items, int G, const RelinC K, const LimbList LL,
-                                                  const CtxParams P) {
+template <typename W, int LOGN>
+struct RelinCfg {
+  static constexpr int threads = (1 << LOGN) / 16;
+  static constexpr bool ACC_GLOBAL = sizeof(W) == 8 && LOGN >= 14;
+};
+
+template <typename W, int LOGN, bool GIVEN_D>
+__global__ void __launch_bounds__(RelinCfg<W, LOGN>::threads, 1)
+    k_relin_t(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int64_t a_stride, int64_t b_stride,
+              const uint64_t* __restrict__ c2, const uint64_t* __restrict__ kval,
+              const uint64_t* __restrict__ kpack, uint64_t* __restrict__ out, int nl, int64_t items, int G,
+              const RelinC K, const LimbList LL, const CtxParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
-  Cta<W, TWS> c(smem, LL, items, G, P, false);
-  const int n = (int)P.n, logn = P.logn, j = c.limb;
+  Cta<W, LOGN> c(smem, LL, items, G, P, false);
+  constexpr int n = 1 << LOGN;
+  constexpr bool AG = RelinCfg<W, LOGN>::ACC_GLOBAL;
+  const int j = c.limb;
   const W q = (W)c.L->q, q2 = q + q;
   const uint64_t Q = c.L->q;
   const int64_t pw = (int64_t)nl * n;
-  const int vt = threadIdx.x;  // blockDim.x == n / 16: one 16-element group per thread
+  const int vt = threadIdx.x;
+  const int k0 = vt << 4;
   for (int item = c.r0; item < c.r1; ++item) {
     W acc0[16], acc1[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) { acc0[r] = 0; acc1[r] = 0; }
+    uint64_t* o0 = out + (int64_t)item * 2 * pw + (int64_t)j * n + k0;
+    uint64_t* o1 = o0 + pw;
+    if constexpr (AG) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) { o0[r] = 0; o1[r] = 0; }
+    }
     const uint64_t* c2item = c2 + (int64_t)item * pw;
     for (int i = 0; i < nl; ++i) {
       const uint64_t* src = c2item + (int64_t)i * n;
       for (int d = 0; d < K.digits[i]; ++d) {
         const int row = K.rows0[i] + d;
         const int sh = 15 * d;
-        for (int k = threadIdx.x; k < n; k += blockDim.x) c.s[swz<W>(k)] = (W)((src[k] >> sh) & 0x7FFF);
+        for (int k = threadIdx.x; k < n; k += blockDim.x) c.s[lz::padj(k)] = (W)((src[k] >> sh) & 0x7FFF);
         __syncthreads();
-        fwd_lz_but_last(c.s, logn, c.tw, q, q2);
+        lz::fwd_but_last<W, LOGN>(c.s, c.tw, q, q2);
         W x[16];
-        fwd_last_group(c.s, vt, logn, c.tw, q, q2, x);
-        const int64_t koff = (int64_t)row * 2 * K.key_poly_words + (int64_t)j * n + (vt << 4);
-        if (sizeof(W) == 4) {
+        lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, x);
+        const int64_t koff = (int64_t)row * 2 * K.key_poly_words + (int64_t)j * n + k0;
+        if constexpr (sizeof(W) == 4) {
           const ulonglong2* kb2 = reinterpret_cast<const ulonglong2*>(kpack + koff);
           const ulonglong2* ka2 = reinterpret_cast<const ulonglong2*>(kpack + koff + K.key_poly_words);
+          const uint32_t q32 = (uint32_t)Q, q232 = q32 + q32;
 #pragma unroll
           for (int h = 0; h < 8; ++h) {
             const ulonglong2 vb = __ldg(kb2 + h), va = __ldg(ka2 + h);
@@ -237,12 +255,11 @@ __global__ void __launch_bounds__(512, 1) k_relin_lz(const uint64_t* __restrict_
             for (int e = 0; e < 2; ++e) {
               const uint64_t pb = e ? vb.y : vb.x, pa = e ? va.y : va.x;
               const uint32_t xv = (uint32_t)x[2 * h + e];
-              const uint32_t q32 = (uint32_t)Q, q232 = q32 + q32;
-              uint32_t t0 = xv * (uint32_t)pb - __umulhi(xv, (uint32_t)(pb >> 32)) * q32;
-              uint32_t t1 = xv * (uint32_t)pa - __umulhi(xv, (uint32_t)(pa >> 32)) * q32;
-              uint32_t s0 = (uint32_t)acc0[2 * h + e] + t0, s1 = (uint32_t)acc1[2 * h + e] + t1;
-              acc0[2 * h + e] = (W)(s0 >= q232 ? s0 - q232 : s0);
-              acc1[2 * h + e] = (W)(s1 >= q232 ? s1 - q232 : s1);
+              const uint32_t t0 = xv * (uint32_t)pb - __umulhi(xv, (uint32_t)(pb >> 32)) * q32;
+              const uint32_t t1 = xv * (uint32_t)pa - __umulhi(xv, (uint32_t)(pa >> 32)) * q32;
+              const uint32_t s0 = (uint32_t)acc0[2 * h + e] + t0, s1 = (uint32_t)acc1[2 * h + e] + t1;
+              acc0[2 * h + e] = (W)min(s0, s0 - q232);
+              acc1[2 * h + e] = (W)min(s1, s1 - q232);
             }
           }
         } else {
@@ -258,8 +275,13 @@ __global__ void __launch_bounds__(512, 1) k_relin_lz(const uint64_t* __restrict_
               const uint64_t xv = canon4<uint64_t>((uint64_t)x[2 * h + e], Q, Q + Q);
               const uint64_t t0 = mul_shoup64(xv, e ? vb.y : vb.x, e ? wb.y : wb.x, Q);
               const uint64_t t1 = mul_shoup64(xv, e ? va.y : va.x, e ? wa.y : wa.x, Q);
-              acc0[2 * h + e] = (W)add_mod((uint64_t)acc0[2 * h + e], t0, Q);
-              acc1[2 * h + e] = (W)add_mod((uint64_t)acc1[2 * h + e], t1, Q);
+              if constexpr (AG) {
+                o0[2 * h + e] = add_mod(o0[2 * h + e], t0, Q);
+                o1[2 * h + e] = add_mod(o1[2 * h + e], t1, Q);
+              } else {
+                acc0[2 * h + e] = (W)add_mod((uint64_t)acc0[2 * h + e], t0, Q);
+                acc1[2 * h + e] = (W)add_mod((uint64_t)acc1[2 * h + e], t1, Q);
+              }
             }
           }
         }
@@ -267,35 +289,29 @@ __global__ void __launch_bounds__(512, 1) k_relin_lz(const uint64_t* __restrict_
       }
     }
     // epilogue: + d0, d1; canonical store
-    const int k0 = vt << 4;
-    uint64_t* o0 = out + (int64_t)item * 2 * pw + (int64_t)j * n + k0;
-    uint64_t* o1 = o0 + pw;
-    const uint64_t* p0;
-    const uint64_t* p1;
-    const uint64_t* q0 = nullptr;
-    const uint64_t* q1 = nullptr;
-    if (GIVEN_D) {  // a = (d0, d1, d2) size-3 input
-      p0 = a + (int64_t)item * a_stride + (int64_t)j * n + k0;
-      p1 = p0 + pw;
-    } else {
-      p0 = a + (int64_t)item * a_stride + (int64_t)j * n + k0;
-      p1 = p0 + pw;
-      q0 = b + (int64_t)item * b_stride + (int64_t)j * n + k0;
-      q1 = q0 + pw;
-    }
+    const uint64_t* p0 = a + (int64_t)item * a_stride + (int64_t)j * n + k0;
+    const uint64_t* p1 = p0 + pw;
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
-      uint64_t r0 = (uint64_t)acc0[r], r1 = (uint64_t)acc1[r];
-      if (sizeof(W) == 4) {
-        r0 = r0 >= Q ? r0 - Q : r0;
-        r1 = r1 >= Q ? r1 - Q : r1;
+      uint64_t r0, r1;
+      if constexpr (AG) {
+        r0 = o0[r];
+        r1 = o1[r];
+      } else {
+        r0 = (uint64_t)acc0[r];
+        r1 = (uint64_t)acc1[r];
+        if constexpr (sizeof(W) == 4) {
+          r0 = r0 >= Q ? r0 - Q : r0;
+          r1 = r1 >= Q ? r1 - Q : r1;
+        }
       }
       uint64_t d0, d1;
-      if (GIVEN_D) {
+      if constexpr (GIVEN_D) {
         d0 = p0[r];
         d1 = p1[r];
       } else {
-        const uint64_t x0 = p0[r], x1 = p1[r], y0 = q0[r], y1 = q1[r];
+        const uint64_t* q0 = b + (int64_t)item * b_stride + (int64_t)j * n + k0;
+        const uint64_t x0 = p0[r], x1 = p1[r], y0 = q0[r], y1 = q0[pw + r];
         d0 = mul_mod(x0, y0, *c.L);
         d1 = add_mod(mul_mod(x0, y1, *c.L), mul_mod(x1, y0, *c.L), Q);
       }
@@ -317,6 +333,7 @@ __global__ void __launch_bounds__(512, 1) k_relin_lz(const uint64_t* __restrict_
 // ---------------------------------------------------------------------------
 constexpr int kGT = 256;  // threads per CTA
 constexpr int kKC = 32;   // terms staged per chunk
+constexpr int kTU = 4;    // terms unrolled per inner step (loads issued together)
 
 template <bool WIDE, int MT, int C>
 __global__ void __launch_bounds__(kGT) k_gemm_lz(const uint64_t* __restrict__ x, const int32_t* __restrict__ idx,
@@ -343,10 +360,8 @@ __global__ void __launch_bounds__(kGT) k_gemm_lz(const uint64_t* __restrict__ x,
   const int b = (qbits + 1) / 2;
   const uint64_t bmask = (1ull << b) - 1;
   // terms between folds: keeps every accumulator below 2^64
-  uint64_t Fq;
-  if (WIDE) Fq = (1ull << 62) >> (2 * b);
-  else Fq = (1ull << 63) / (q * q);
-  const int F = (int)max((uint64_t)1, min((uint64_t)1 << 30, Fq));
+  const uint64_t Fq = WIDE ? ((1ull << 62) >> (2 * b)) : ((1ull << 63) / (q * q));
+  const int F = (int)max((uint64_t)kTU, min((uint64_t)1 << 30, Fq / kTU * kTU));
   const uint64_t r32 = (1ull << 32) % q;
   int since = 0;
 
@@ -373,13 +388,13 @@ __global__ void __launch_bounds__(kGT) k_gemm_lz(const uint64_t* __restrict__ x,
         ws[tt][m] = (uint32_t)v;
       }
     }
-    if (threadIdx.x < kKC) xs[threadIdx.x] = threadIdx.x < tc ? idx[g * kt + t0 + threadIdx.x] : 0;
+    // padded terms (tt >= tc) read item 0 with weight 0
+    if (threadIdx.x < kKC) xs[threadIdx.x] = threadIdx.x < tc ? idx[g * kt + t0 + threadIdx.x] : idx[g * kt];
     __syncthreads();
     if (!live) continue;
-    for (int f0 = 0; f0 < tc;) {
-      const int f1 = min(tc, f0 + F);
-      if (since + (f1 - f0) > F) {
-        // fold: small limbs acc_hi * (2^32 mod q) + acc_lo (< 2^63); wide limbs a full reduction
+    const int tcu = (tc + kTU - 1) / kTU * kTU;
+    for (int f0 = 0; f0 < tcu; f0 += kTU) {
+      if (since + kTU > F) {
 #pragma unroll
         for (int m = 0; m < MT; ++m)
 #pragma unroll
@@ -391,26 +406,32 @@ __global__ void __launch_bounds__(kGT) k_gemm_lz(const uint64_t* __restrict__ x,
             }
         since = 0;
       }
-      since += f1 - f0;
-      for (int tt = f0; tt < f1; ++tt) {
-        const uint64_t* xp = xrow + (int64_t)xs[tt] * item_words;
-        uint64_t xv[C];
+      since += kTU;
+      // issue the kTU term loads together, then the MACs
+      uint64_t xv[kTU][C];
+#pragma unroll
+      for (int u = 0; u < kTU; ++u) {
+        const uint64_t* xp = xrow + (int64_t)xs[f0 + u] * item_words;
         if (C == 1) {
-          xv[0] = __ldg(xp);
+          xv[u][0] = __ldg(xp);
         } else {
 #pragma unroll
           for (int c = 0; c < C; c += 2) {
             const ulonglong2 v2 = __ldg(reinterpret_cast<const ulonglong2*>(xp + c));
-            xv[c] = v2.x;
-            xv[c + 1] = v2.y;
+            xv[u][c] = v2.x;
+            xv[u][c + 1] = v2.y;
           }
         }
+      }
+#pragma unroll
+      for (int u = 0; u < kTU; ++u) {
+        const int tt = f0 + u;
         if (WIDE) {
           uint32_t xl[C], xh[C];
 #pragma unroll
           for (int c = 0; c < C; ++c) {
-            xl[c] = (uint32_t)(xv[c] & bmask);
-            xh[c] = (uint32_t)(xv[c] >> b);
+            xl[c] = (uint32_t)(xv[u][c] & bmask);
+            xh[c] = (uint32_t)(xv[u][c] >> b);
           }
 #pragma unroll
           for (int m = 0; m < MT; ++m) {
@@ -428,15 +449,15 @@ __global__ void __launch_bounds__(kGT) k_gemm_lz(const uint64_t* __restrict__ x,
           for (int m = 0; m < MT; ++m) {
             const uint32_t wv = ws[tt][m];
 #pragma unroll
-            for (int c = 0; c < C; ++c) acc[m][c][0] += (uint64_t)(uint32_t)xv[c] * wv;
+            for (int c = 0; c < C; ++c) acc[m][c][0] += (uint64_t)(uint32_t)xv[u][c] * wv;
           }
         }
       }
-      f0 = f1;
     }
   }
   if (!live) return;
-  const uint64_t c2b = WIDE ? mul_mod((1ull << b) % q, (1ull << b) % q, L) : 0, cb = WIDE ? (1ull << b) % q : 0;
+  const uint64_t cb = WIDE ? (1ull << b) % q : 0;
+  const uint64_t c2b = WIDE ? mul_mod(cb, cb, L) : 0;
 #pragma unroll
   for (int m = 0; m < MT; ++m) {
     if (m0 + m >= mg) break;
@@ -490,17 +511,6 @@ static void set_smem_attr(const void* fn, size_t bytes) {
   done[fn] = bytes;
 }
 
-constexpr size_t kSmemCap = 227 * 1024;
-
-template <typename W>
-static size_t data_bytes(const Context& c) { return (size_t)c.n() * sizeof(W); }
-template <typename W>
-static size_t tw_bytes(const Context& c) { return (size_t)c.n() * sizeof(typename Lz<W>::TW); }
-template <typename W>
-static bool stage_ok(const Context& c) { return data_bytes<W>(c) + tw_bytes<W>(c) <= kSmemCap; }
-
-static int threads_for(const Context& c) { return (int)std::min<int64_t>(512, c.n() / 16); }
-
 // rows per CTA so that the grid still covers every SM a few times over
 static int group_size(int64_t rows, int limbs, int ctas_per_sm) {
   const int64_t target = 148LL * ctas_per_sm * 3;
@@ -510,61 +520,75 @@ static int group_size(int64_t rows, int limbs, int ctas_per_sm) {
 
 static double bfly(const Context& c) { return 0.5 * (double)c.n() * c.logn(); }
 
-// Launch `Kern<W,TWS>` over one limb class.  F(fn_ptr, grid, smem, G) does the launch.
-template <typename W, typename Launch>
-static void for_class(const Context& c, const LimbList& LL, int64_t rows, bool allow_tws, Launch&& launch) {
-  if (LL.count == 0 || rows <= 0) return;
-  const bool tws = allow_tws && stage_ok<W>(c);
-  const size_t sm = data_bytes<W>(c) + (tws ? tw_bytes<W>(c) : 0);
-  const int per_sm = std::max<int>(1, (int)(kSmemCap / sm));
-  const int G = group_size(rows, LL.count, std::min(per_sm, 2));
-  const unsigned grid = (unsigned)(LL.count * ((rows + G - 1) / G));
-  launch(tws, grid, sm, G);
+// dispatch a functor templated on (W, LOGN) for the context's ring degree
+template <typename W, typename F>
+static void by_logn(const Context& c, F&& f) {
+  switch (c.logn()) {
+    case 10: f.template operator()<W, 10>(); break;
+    case 11: f.template operator()<W, 11>(); break;
+    case 12: f.template operator()<W, 12>(); break;
+    case 13: f.template operator()<W, 13>(); break;
+    case 14: f.template operator()<W, 14>(); break;
+    case 15: f.template operator()<W, 15>(); break;
+    default: fail(HG_EVALIDATION, "ring degree outside 2^10..2^15");
+  }
+}
+
+template <typename W, int LOGN>
+static void grid_for(const LimbList& LL, int64_t rows, unsigned& grid, int& G) {
+  using Cf = Cfg<W, LOGN>;
+  const int per_sm = std::max<int>(1, (int)(kSmemCap / Cf::smem));
+  G = group_size(rows, LL.count, std::min(per_sm, 2));
+  grid = (unsigned)(LL.count * ((rows + G - 1) / G));
 }
 
 void ntt(const Context& c, uint64_t* base, int64_t rows_per_limb, int nl, int limb_begin, int limb_end, bool inverse,
          cudaStream_t s) {
+  if (rows_per_limb <= 0) return;
   const Classes cl = classify(c, limb_begin, limb_end);
-  const int th = threads_for(c);
   const double nw = (double)c.n() * 8;
-#define HG_NTT_LAUNCH(W, LL)                                                                                      \
-  for_class<W>(c, LL, rows_per_limb, true, [&](bool tws, unsigned grid, size_t sm, int G) {                       \
-    const void* fn = inverse ? (tws ? (const void*)k_ntt_lz<W, true, true> : (const void*)k_ntt_lz<W, true, false>) \
-                             : (tws ? (const void*)k_ntt_lz<W, false, true> : (const void*)k_ntt_lz<W, false, false>); \
-    set_smem_attr(fn, sm);                                                                                        \
-    c.kt_begin("k_ntt_lz", s, 2.0 * rows_per_limb * LL.count * nw, (double)rows_per_limb * LL.count * bfly(c));   \
-    if (inverse) {                                                                                                \
-      if (tws) k_ntt_lz<W, true, true><<<grid, th, sm, s>>>(base, nl, rows_per_limb, G, LL, c.kp());            \
-      else k_ntt_lz<W, true, false><<<grid, th, sm, s>>>(base, nl, rows_per_limb, G, LL, c.kp());               \
-    } else {                                                                                                      \
-      if (tws) k_ntt_lz<W, false, true><<<grid, th, sm, s>>>(base, nl, rows_per_limb, G, LL, c.kp());           \
-      else k_ntt_lz<W, false, false><<<grid, th, sm, s>>>(base, nl, rows_per_limb, G, LL, c.kp());              \
-    }                                                                                                             \
-    c.kt_end(s);                                                                                                  \
-    HG_CUDA(cudaGetLastError());                                                                                  \
-  });
-  HG_NTT_LAUNCH(uint32_t, cl.small)
-  HG_NTT_LAUNCH(uint64_t, cl.wide)
-#undef HG_NTT_LAUNCH
+  auto run = [&](const LimbList& LL, auto wtag) {
+    using W = decltype(wtag);
+    if (LL.count == 0) return;
+    by_logn<W>(c, [&]<typename W_, int LOGN>() {
+      using Cf = Cfg<W_, LOGN>;
+      unsigned grid;
+      int G;
+      grid_for<W_, LOGN>(LL, rows_per_limb, grid, G);
+      const void* fn = inverse ? (const void*)k_ntt_t<W_, LOGN, true> : (const void*)k_ntt_t<W_, LOGN, false>;
+      set_smem_attr(fn, Cf::smem);
+      c.kt_begin("k_ntt_t", s, 2.0 * rows_per_limb * LL.count * nw, (double)rows_per_limb * LL.count * bfly(c));
+      if (inverse) k_ntt_t<W_, LOGN, true><<<grid, Cf::threads, Cf::smem, s>>>(base, nl, rows_per_limb, G, LL, c.kp());
+      else k_ntt_t<W_, LOGN, false><<<grid, Cf::threads, Cf::smem, s>>>(base, nl, rows_per_limb, G, LL, c.kp());
+      c.kt_end(s);
+      HG_CUDA(cudaGetLastError());
+    });
+  };
+  run(cl.small, uint32_t{});
+  run(cl.wide, uint64_t{});
 }
 
 void lift_ntt(const Context& c, const int64_t* src, uint64_t* out, int64_t items, int nl, cudaStream_t s) {
+  if (items <= 0) return;
   const Classes cl = classify(c, 0, nl);
-  const int th = threads_for(c);
   const double nw = (double)c.n() * 8;
-#define HG_LIFT_LAUNCH(W, LL)                                                                                     \
-  for_class<W>(c, LL, items, true, [&](bool tws, unsigned grid, size_t sm, int G) {                               \
-    const void* fn = tws ? (const void*)k_lift_ntt_lz<W, true> : (const void*)k_lift_ntt_lz<W, false>;             \
-    set_smem_attr(fn, sm);                                                                                        \
-    c.kt_begin("k_lift_ntt_lz", s, (double)items * LL.count * 2 * nw, (double)items * LL.count * bfly(c));        \
-    if (tws) k_lift_ntt_lz<W, true><<<grid, th, sm, s>>>(src, out, nl, items, G, LL, c.kp());                      \
-    else k_lift_ntt_lz<W, false><<<grid, th, sm, s>>>(src, out, nl, items, G, LL, c.kp());                         \
-    c.kt_end(s);                                                                                                  \
-    HG_CUDA(cudaGetLastError());                                                                                  \
-  });
-  HG_LIFT_LAUNCH(uint32_t, cl.small)
-  HG_LIFT_LAUNCH(uint64_t, cl.wide)
-#undef HG_LIFT_LAUNCH
+  auto run = [&](const LimbList& LL, auto wtag) {
+    using W = decltype(wtag);
+    if (LL.count == 0) return;
+    by_logn<W>(c, [&]<typename W_, int LOGN>() {
+      using Cf = Cfg<W_, LOGN>;
+      unsigned grid;
+      int G;
+      grid_for<W_, LOGN>(LL, items, grid, G);
+      set_smem_attr((const void*)k_lift_ntt_t<W_, LOGN>, Cf::smem);
+      c.kt_begin("k_lift_ntt_t", s, (double)items * LL.count * 2 * nw, (double)items * LL.count * bfly(c));
+      k_lift_ntt_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(src, out, nl, items, G, LL, c.kp());
+      c.kt_end(s);
+      HG_CUDA(cudaGetLastError());
+    });
+  };
+  run(cl.small, uint32_t{});
+  run(cl.wide, uint64_t{});
 }
 
 void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys, int nl, int64_t* cen,
@@ -572,42 +596,48 @@ void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys,
   check(nl >= 2, HG_EINTERNAL, "rescale needs at least two active moduli");
   if (polys <= 0) return;
   const int t = nl - 1;
-  const int th = threads_for(c);
   const double nw = (double)c.n() * 8;
   RescaleC R{};
   for (int j = 0; j < t; ++j) {
     R.inv[j] = c.inv_q(t, j);
     R.inv_s[j] = c.inv_q_shoup(t, j);
   }
-  const Classes top = classify(c, t, t + 1);
-#define HG_TOP_LAUNCH(W, LL)                                                                                      \
-  for_class<W>(c, LL, polys, true, [&](bool tws, unsigned grid, size_t sm, int G) {                               \
-    const void* fn = tws ? (const void*)k_rescale_top_lz<W, true> : (const void*)k_rescale_top_lz<W, false>;       \
-    set_smem_attr(fn, sm);                                                                                        \
-    c.kt_begin("k_rescale_top_lz", s, 2.0 * polys * nw, (double)polys * bfly(c));                                 \
-    if (tws) k_rescale_top_lz<W, true><<<grid, th, sm, s>>>(in, cen, nl, polys, G, LL, c.kp());                    \
-    else k_rescale_top_lz<W, false><<<grid, th, sm, s>>>(in, cen, nl, polys, G, LL, c.kp());                       \
-    c.kt_end(s);                                                                                                  \
-    HG_CUDA(cudaGetLastError());                                                                                  \
-  });
-  HG_TOP_LAUNCH(uint32_t, top.small)
-  HG_TOP_LAUNCH(uint64_t, top.wide)
-#undef HG_TOP_LAUNCH
-  const Classes rest = classify(c, 0, t);
-#define HG_REST_LAUNCH(W, LL)                                                                                     \
-  for_class<W>(c, LL, polys, true, [&](bool tws, unsigned grid, size_t sm, int G) {                               \
-    const void* fn = tws ? (const void*)k_rescale_rest_lz<W, true> : (const void*)k_rescale_rest_lz<W, false>;     \
-    set_smem_attr(fn, sm);                                                                                        \
-    c.kt_begin("k_rescale_rest_lz", s, (double)polys * LL.count * 3 * nw,                                         \
-               (double)polys * LL.count * (bfly(c) + c.n()));                                                     \
-    if (tws) k_rescale_rest_lz<W, true><<<grid, th, sm, s>>>(in, cen, out, nl, polys, G, LL, R, c.kp());           \
-    else k_rescale_rest_lz<W, false><<<grid, th, sm, s>>>(in, cen, out, nl, polys, G, LL, R, c.kp());              \
-    c.kt_end(s);                                                                                                  \
-    HG_CUDA(cudaGetLastError());                                                                                  \
-  });
-  HG_REST_LAUNCH(uint32_t, rest.small)
-  HG_REST_LAUNCH(uint64_t, rest.wide)
-#undef HG_REST_LAUNCH
+  const Classes top = classify(c, t, t + 1), rest = classify(c, 0, t);
+  auto run_top = [&](const LimbList& LL, auto wtag) {
+    using W = decltype(wtag);
+    if (LL.count == 0) return;
+    by_logn<W>(c, [&]<typename W_, int LOGN>() {
+      using Cf = Cfg<W_, LOGN>;
+      unsigned grid;
+      int G;
+      grid_for<W_, LOGN>(LL, polys, grid, G);
+      set_smem_attr((const void*)k_rescale_top_t<W_, LOGN>, Cf::smem);
+      c.kt_begin("k_rescale_top_t", s, 2.0 * polys * nw, (double)polys * bfly(c));
+      k_rescale_top_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(in, cen, nl, polys, G, LL, c.kp());
+      c.kt_end(s);
+      HG_CUDA(cudaGetLastError());
+    });
+  };
+  auto run_rest = [&](const LimbList& LL, auto wtag) {
+    using W = decltype(wtag);
+    if (LL.count == 0) return;
+    by_logn<W>(c, [&]<typename W_, int LOGN>() {
+      using Cf = Cfg<W_, LOGN>;
+      unsigned grid;
+      int G;
+      grid_for<W_, LOGN>(LL, polys, grid, G);
+      set_smem_attr((const void*)k_rescale_rest_t<W_, LOGN>, Cf::smem);
+      c.kt_begin("k_rescale_rest_t", s, (double)polys * LL.count * 3 * nw,
+                 (double)polys * LL.count * (bfly(c) + c.n()));
+      k_rescale_rest_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(in, cen, out, nl, polys, G, LL, R, c.kp());
+      c.kt_end(s);
+      HG_CUDA(cudaGetLastError());
+    });
+  };
+  run_top(top.small, uint32_t{});
+  run_top(top.wide, uint64_t{});
+  run_rest(rest.small, uint32_t{});
+  run_rest(rest.wide, uint64_t{});
 }
 
 static RelinC relin_consts(const Context& c, int nl) {
@@ -620,41 +650,74 @@ static RelinC relin_consts(const Context& c, int nl) {
   return K;
 }
 
+bool relin_supported(const Context& c) { return c.logn() >= 10 && c.logn() <= 14; }
+
 void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, int64_t a_stride,
            int64_t b_stride, bool given_d, const uint64_t* c2, uint64_t* out, int64_t items, int nl, cudaStream_t s) {
-  check(c.n() / 16 <= 512, HG_EINTERNAL, "relin_lz: ring degree above 8192");
+  check(relin_supported(c), HG_EINTERNAL, "key switch: ring degree outside 2^10..2^14");
+  if (items <= 0) return;
   const RelinC K = relin_consts(c, nl);
   const Classes cl = classify(c, 0, nl);
-  const int th = (int)(c.n() / 16);
   int sd = 0;
   for (int i = 0; i < nl; ++i) sd += c.digits(i);
   const double pw8 = (double)nl * c.n() * 8;
-#define HG_RELIN_LAUNCH(W, LL, GD)                                                                                \
-  for_class<W>(c, LL, items, true, [&](bool tws, unsigned grid, size_t sm, int G) {                               \
-    const void* fn = tws ? (const void*)k_relin_lz<W, true, GD> : (const void*)k_relin_lz<W, false, GD>;           \
-    set_smem_attr(fn, sm);                                                                                        \
-    const double frac = (double)LL.count / nl;                                                                    \
-    c.kt_begin("k_relin_lz", s, frac * (items * pw8 * 7 + (double)sd * 2 * pw8),                                   \
-               (double)items * LL.count * (sd * (bfly(c) + 2.0 * c.n()) + 3.0 * c.n()));                          \
-    if (tws)                                                                                                      \
-      k_relin_lz<W, true, GD><<<grid, th, sm, s>>>(a, b, a_stride, b_stride, c2, keys.relin.as<uint64_t>(),       \
-                                                   keys.relin_pack.as<uint64_t>(), out, nl, items, G, K, LL,      \
-                                                   c.kp());                                                       \
-    else                                                                                                          \
-      k_relin_lz<W, false, GD><<<grid, th, sm, s>>>(a, b, a_stride, b_stride, c2, keys.relin.as<uint64_t>(),      \
-                                                    keys.relin_pack.as<uint64_t>(), out, nl, items, G, K, LL,     \
-                                                    c.kp());                                                      \
-    c.kt_end(s);                                                                                                  \
-    HG_CUDA(cudaGetLastError());                                                                                  \
-  });
-  if (given_d) {
-    HG_RELIN_LAUNCH(uint32_t, cl.small, true)
-    HG_RELIN_LAUNCH(uint64_t, cl.wide, true)
-  } else {
-    HG_RELIN_LAUNCH(uint32_t, cl.small, false)
-    HG_RELIN_LAUNCH(uint64_t, cl.wide, false)
-  }
-#undef HG_RELIN_LAUNCH
+  auto run = [&](const LimbList& LL, auto wtag) {
+    using W = decltype(wtag);
+    if (LL.count == 0) return;
+    by_logn<W>(c, [&]<typename W_, int LOGN>() {
+      if constexpr (LOGN <= 14) {
+        using Cf = Cfg<W_, LOGN>;
+        const int threads = RelinCfg<W_, LOGN>::threads;
+        const int64_t target = 148LL * 3;
+        const int G = (int)std::max<int64_t>(1, std::min<int64_t>(16, (items * LL.count + target - 1) / target));
+        const unsigned grid = (unsigned)(LL.count * ((items + G - 1) / G));
+        const void* fn = given_d ? (const void*)k_relin_t<W_, LOGN, true> : (const void*)k_relin_t<W_, LOGN, false>;
+        set_smem_attr(fn, Cf::smem);
+        const double frac = (double)LL.count / nl;
+        c.kt_begin("k_relin_t", s, frac * (items * pw8 * 7 + (double)sd * 2 * pw8),
+                   (double)items * LL.count * (sd * (bfly(c) + 2.0 * c.n()) + 3.0 * c.n()));
+        if (given_d)
+          k_relin_t<W_, LOGN, true><<<grid, threads, Cf::smem, s>>>(a, b, a_stride, b_stride, c2,
+                                                                    keys.relin.as<uint64_t>(),
+                                                                    keys.relin_pack.as<uint64_t>(), out, nl, items, G,
+                                                                    K, LL, c.kp());
+        else
+          k_relin_t<W_, LOGN, false><<<grid, threads, Cf::smem, s>>>(a, b, a_stride, b_stride, c2,
+                                                                     keys.relin.as<uint64_t>(),
+                                                                     keys.relin_pack.as<uint64_t>(), out, nl, items,
+                                                                     G, K, LL, c.kp());
+        c.kt_end(s);
+        HG_CUDA(cudaGetLastError());
+      }
+    });
+  };
+  run(cl.small, uint32_t{});
+  run(cl.wide, uint64_t{});
+}
+
+void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_stride, int64_t b_stride,
+              int64_t a1_off, int64_t b1_off, uint64_t* c2, int64_t items, int nl, cudaStream_t s) {
+  if (items <= 0) return;
+  const Classes cl = classify(c, 0, nl);
+  const double nw = (double)c.n() * 8;
+  auto run = [&](const LimbList& LL, auto wtag) {
+    using W = decltype(wtag);
+    if (LL.count == 0) return;
+    by_logn<W>(c, [&]<typename W_, int LOGN>() {
+      using Cf = Cfg<W_, LOGN>;
+      unsigned grid;
+      int G;
+      grid_for<W_, LOGN>(LL, items, grid, G);
+      set_smem_attr((const void*)k_relin_c2_t<W_, LOGN>, Cf::smem);
+      c.kt_begin("k_relin_c2_t", s, (double)items * LL.count * 3 * nw, (double)items * LL.count * (bfly(c) + c.n()));
+      k_relin_c2_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(a, b, a_stride, b_stride, a1_off, b1_off, c2, nl,
+                                                                 items, G, LL, c.kp());
+      c.kt_end(s);
+      HG_CUDA(cudaGetLastError());
+    });
+  };
+  run(cl.small, uint32_t{});
+  run(cl.wide, uint64_t{});
 }
 
 void gemm(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* idx, const uint64_t* w,
@@ -690,30 +753,6 @@ void gemm(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* i
   };
   launch(cl.small, false);
   launch(cl.wide, true);
-}
-
-void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_stride, int64_t b_stride,
-              int64_t a1_off, int64_t b1_off, uint64_t* c2, int64_t items, int nl, cudaStream_t s) {
-  const Classes cl = classify(c, 0, nl);
-  const int th = threads_for(c);
-  const double nw = (double)c.n() * 8;
-#define HG_C2_LAUNCH(W, LL)                                                                                       \
-  for_class<W>(c, LL, items, true, [&](bool tws, unsigned grid, size_t sm, int G) {                               \
-    const void* fn = tws ? (const void*)k_relin_c2_lz<W, true> : (const void*)k_relin_c2_lz<W, false>;             \
-    set_smem_attr(fn, sm);                                                                                        \
-    c.kt_begin("k_relin_c2_lz", s, (double)items * LL.count * 3 * nw, (double)items * LL.count * (bfly(c) + c.n())); \
-    if (tws)                                                                                                      \
-      k_relin_c2_lz<W, true><<<grid, th, sm, s>>>(a, b, a_stride, b_stride, a1_off, b1_off, c2, nl, items, G, LL, \
-                                                  c.kp());                                                        \
-    else                                                                                                          \
-      k_relin_c2_lz<W, false><<<grid, th, sm, s>>>(a, b, a_stride, b_stride, a1_off, b1_off, c2, nl, items, G,     \
-                                                   LL, c.kp());                                                   \
-    c.kt_end(s);                                                                                                  \
-    HG_CUDA(cudaGetLastError());                                                                                  \
-  });
-  HG_C2_LAUNCH(uint32_t, cl.small)
-  HG_C2_LAUNCH(uint64_t, cl.wide)
-#undef HG_C2_LAUNCH
 }
 
 }  // namespace k2

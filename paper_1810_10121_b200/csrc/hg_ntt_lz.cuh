@@ -1,0 +1,186 @@
+// hg_ntt_lz.cuh -- compile-time-degree lazy NTT core (the transforms of
+// NttTables::forward / inverse, ring.hpp:263-301).
+//
+// LOGN is a template parameter, so every pass offset, stride and twiddle
+// index below is a compile-time constant plus one per-thread base.  Shared
+// memory is padded (word j lives at j + j/16) instead of XOR-swizzled: with
+// the radix-16, remainder-first pass structure the strides are 2^{0,4,8,12}
+// and the padded addresses of a thread's 16 elements are base + constant, so
+// shared-memory access costs no address arithmetic and stays (nearly)
+// bank-conflict free.  Values are kept lazily in [0, 4q) (forward) / [0, 2q)
+// (inverse) and canonicalised once at the end: every output word equals the
+// reference's eagerly reduced transform.
+#pragma once
+#include "hg_ntt.cuh"
+
+namespace hg {
+namespace lz {
+
+__host__ __device__ constexpr int padj(int j) { return j + (j >> 4); }
+__host__ __device__ constexpr int po(int r, int t) { return (r << t) + ((r << t) >> 4); }
+template <int LOGN>
+__host__ __device__ constexpr int smem_words() { return (1 << LOGN) + (1 << (LOGN - 4)); }
+
+template <typename W>
+using TWT = typename Lz<W>::TW;
+
+// ---- forward (Cooley-Tukey), remainder-first passes ------------------------
+// stages S0 .. S0+K-1 of block g; pass-ordered twiddle at 2^S + (r >> (K-st)) 2^S0 + g
+template <typename W, int K, int S0>
+__device__ __forceinline__ void fwd_group(W (&x)[1 << K], int g, const TWT<W>* tw, W q, W q2) {
+  constexpr int R = 1 << K;
+#pragma unroll
+  for (int st = 0; st < K; ++st) {
+    const int hd = R >> (st + 1);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (r & hd) continue;
+      ct_lz(x[r], x[r + hd], tw[(1 << (S0 + st)) + ((r >> (K - st)) << S0) + g], q, q2);
+    }
+  }
+}
+
+template <typename W, int LOGN, int K, int S0>
+__device__ __forceinline__ void fwd_pass(W* s, const TWT<W>* tw, W q, W q2) {
+  constexpr int R = 1 << K, TL = LOGN - S0 - K;
+  for (int vt = threadIdx.x; vt < (1 << (LOGN - K)); vt += blockDim.x) {
+    const int g = vt >> TL;
+    const int pb = padj((g << (LOGN - S0)) + (vt & ((1 << TL) - 1)));
+    W x[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r] = s[pb + po(r, TL)];
+    fwd_group<W, K, S0>(x, g, tw, q, q2);
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[pb + po(r, TL)] = x[r];
+  }
+}
+
+// all passes but the last radix-16 one; ends with a barrier
+template <typename W, int LOGN>
+__device__ __forceinline__ void fwd_but_last(W* s, const TWT<W>* tw, W q, W q2) {
+  constexpr int REM = LOGN & 3;
+  if constexpr (REM != 0) {
+    fwd_pass<W, LOGN, REM, 0>(s, tw, q, q2);
+    __syncthreads();
+  }
+  if constexpr (REM + 4 < LOGN) {
+    fwd_pass<W, LOGN, 4, REM>(s, tw, q, q2);
+    __syncthreads();
+  }
+  if constexpr (REM + 8 < LOGN) {
+    fwd_pass<W, LOGN, 4, REM + 4>(s, tw, q, q2);
+    __syncthreads();
+  }
+  if constexpr (REM + 12 < LOGN) {
+    fwd_pass<W, LOGN, 4, REM + 8>(s, tw, q, q2);
+    __syncthreads();
+  }
+  static_assert(LOGN <= 16, "transform size");
+}
+
+// the last pass of group vt: x[r] = evaluation 16 vt + r, in [0, 4q)
+template <typename W, int LOGN>
+__device__ __forceinline__ void fwd_last(const W* s, int vt, const TWT<W>* tw, W q, W q2, W (&x)[16]) {
+  const int pb = padj(vt << 4);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) x[r] = s[pb + r];
+  fwd_group<W, 4, LOGN - 4>(x, vt, tw, q, q2);
+}
+
+template <typename W, int LOGN>
+__device__ __forceinline__ void fwd(W* s, const TWT<W>* tw, W q, W q2) {
+  fwd_but_last<W, LOGN>(s, tw, q, q2);
+  for (int vt = threadIdx.x; vt < (1 << (LOGN - 4)); vt += blockDim.x) {
+    W x[16];
+    fwd_last<W, LOGN>(s, vt, tw, q, q2, x);
+    const int pb = padj(vt << 4);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) s[pb + r] = canon4(x[r], q, q2);
+  }
+  __syncthreads();
+}
+
+// ---- inverse (Gentleman-Sande), remainder-first passes -----------------------
+// stages t = 2^S0 .. of block gi; pass-ordered twiddle at h + (r >> (st+1)) 2^(LOGN-S0-K) + gi
+template <typename W, int LOGN, int K, int S0>
+__device__ __forceinline__ void inv_group(W (&x)[1 << K], int gi, const TWT<W>* tw, W q, W q2) {
+  constexpr int R = 1 << K, NBS = LOGN - S0 - K;
+#pragma unroll
+  for (int st = 0; st < K; ++st) {
+    const int hd = 1 << st;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (r & hd) continue;
+      gs_lz(x[r], x[r + hd], tw[(1 << (LOGN - S0 - st - 1)) + ((r >> (st + 1)) << NBS) + gi], q, q2);
+    }
+  }
+}
+
+template <typename W, int LOGN, int K, int S0, bool LAST>
+__device__ __forceinline__ void inv_pass(W* s, const TWT<W>* tw, TWT<W> ninv, W q, W q2) {
+  constexpr int R = 1 << K;
+  for (int vt = threadIdx.x; vt < (1 << (LOGN - K)); vt += blockDim.x) {
+    const int gi = vt >> S0;
+    const int pb = padj((gi << (S0 + K)) + (vt & ((1 << S0) - 1)));
+    W x[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r] = s[pb + po(r, S0)];
+    inv_group<W, LOGN, K, S0>(x, gi, tw, q, q2);
+    if constexpr (LAST) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const W y = Lz<W>::mulw(x[r], ninv, q);  // x N^{-1} in [0, 2q)
+        x[r] = y >= q ? y - q : y;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[pb + po(r, S0)] = x[r];
+  }
+}
+
+// full inverse, input canonical, output canonical and scaled by N^{-1}; ends with a barrier
+template <typename W, int LOGN>
+__device__ __forceinline__ void inv(W* s, const TWT<W>* tw, TWT<W> ninv, W q, W q2) {
+  constexpr int REM = LOGN & 3;
+  if constexpr (REM != 0) {
+    inv_pass<W, LOGN, REM, 0, false>(s, tw, ninv, q, q2);
+    __syncthreads();
+  }
+  if constexpr (REM + 4 < LOGN) {
+    inv_pass<W, LOGN, 4, REM, false>(s, tw, ninv, q, q2);
+    __syncthreads();
+  }
+  if constexpr (REM + 8 < LOGN) {
+    inv_pass<W, LOGN, 4, REM + 4, false>(s, tw, ninv, q, q2);
+    __syncthreads();
+  }
+  if constexpr (REM + 12 < LOGN) {
+    inv_pass<W, LOGN, 4, REM + 8, false>(s, tw, ninv, q, q2);
+    __syncthreads();
+  }
+  inv_pass<W, LOGN, 4, LOGN - 4, true>(s, tw, ninv, q, q2);
+  __syncthreads();
+}
+
+// ---- global <-> padded shared staging ---------------------------------------
+template <typename W, int LOGN>
+__device__ __forceinline__ void load(W* s, const uint64_t* __restrict__ g) {
+  const ulonglong2* g2 = reinterpret_cast<const ulonglong2*>(g);
+  for (int i = threadIdx.x; i < (1 << (LOGN - 1)); i += blockDim.x) {
+    const ulonglong2 v = g2[i];
+    const int p = padj(2 * i);
+    s[p] = (W)v.x;
+    s[p + 1] = (W)v.y;
+  }
+}
+template <typename W, int LOGN>
+__device__ __forceinline__ void store(uint64_t* __restrict__ g, const W* s) {
+  ulonglong2* g2 = reinterpret_cast<ulonglong2*>(g);
+  for (int i = threadIdx.x; i < (1 << (LOGN - 1)); i += blockDim.x) {
+    const int p = padj(2 * i);
+    g2[i] = make_ulonglong2((uint64_t)s[p], (uint64_t)s[p + 1]);
+  }
+}
+
+}  // namespace lz
+}  // namespace hg
