@@ -473,6 +473,11 @@ struct NodeCache {
   std::shared_ptr<DevArr> res;    // per-item constant residues
   bool pt_is_const = false;
   int64_t counts_add = 0;
+  // contraction plan (deterministic per node): term classes and the per-run profile increments
+  bool planned = false;
+  std::vector<uint8_t> cls;
+  int64_t d_bmult = 0, d_badd = 0, d_mulpt = 0, d_neg = 0, d_add = 0;
+  int64_t n_general = 0, n_pass_only = 0, n_empty = 0, n_fresh = 0;
 };
 
 }  // namespace
@@ -691,51 +696,60 @@ Val contraction(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_s
   const int level = xt->level;  // uniform-level tensor: min over any term subset is this level
   NodeCache& C = P->cache[node.id];
 
-  // planning + counts (sequential, like runtime.hpp:1104-1112)
-  int64_t n_general_outputs = 0, n_pass_only = 0, n_empty = 0;
-  std::vector<uint8_t> cls(static_cast<size_t>(w_space));
-  for (int64_t i = 0; i < w_space; ++i) {
-    if (!can_bypass) { cls[i] = 0; continue; }
-    switch (apply_bypass(P, Op::Multiply, classify_scalar(P, rv.t->v[i]))) {
-      case Action::Proceed: cls[i] = 0; break;
-      case Action::ReturnUnchanged: cls[i] = 1; break;
-      case Action::Negate: cls[i] = 2; break;
-      case Action::FreshZero: cls[i] = 3; break;
-    }
-  }
-  for (int64_t g = 0; g < groups; ++g)
-    for (int m = 0; m < mg; ++m) {
-      int64_t gcount = 0, o = 0, ng = 0, z = 0, skipped = 0;
-      for (int t = 0; t < kt; ++t) {
-        int64_t we;
-        w_index(g, m, t, we);
-        switch (cls[we]) {
-          case 0: ++gcount; break;
-          case 1: ++o; break;
-          case 2: ++ng; break;
-          case 3:
-            if (P->opt_add) ++skipped;
-            else ++z;
-            break;
-        }
+  // planning + counts (sequential, like runtime.hpp:1104-1112); the plan is a pure
+  // function of the weights and the bypass config, so it is built once per node
+  if (!C.planned) {
+    C.cls.assign(static_cast<size_t>(w_space), 0);
+    for (int64_t i = 0; i < w_space && can_bypass; ++i) {
+      switch (apply_bypass(P, Op::Multiply, classify_scalar(P, rv.t->v[i]))) {
+        case Action::Proceed: C.cls[i] = 0; break;
+        case Action::ReturnUnchanged: C.cls[i] = 1; break;
+        case Action::Negate: C.cls[i] = 2; break;
+        case Action::FreshZero: C.cls[i] = 3; break;
       }
-      // add_plan_counts (runtime.hpp:512-525)
-      P->prof.bypass_mult += o + ng + z + skipped;
-      P->prof.bypass_add += skipped;
-      P->prof.mul_pt += gcount;
-      P->prof.negate += ng;
-      const int64_t pass = o + ng + z;
-      P->prof.add += gcount > 0 ? gcount - 1 + pass : std::max<int64_t>(0, pass - 1);
-      check(z == 0, HG_EVALIDATION,
-            "node '" + node.id + "': fresh-zero terms (optimized_addition off) are not supported on the GPU path");
-      if (gcount > 0) ++n_general_outputs;
-      else if (pass > 0) ++n_pass_only;
-      else ++n_empty;
     }
-  check(n_empty == 0, HG_EVALIDATION, "node '" + node.id + "': outputs whose every term is skipped are not supported");
-  check(n_general_outputs == 0 || n_pass_only == 0, HG_EVALIDATION,
+    for (int64_t g = 0; g < groups; ++g)
+      for (int m = 0; m < mg; ++m) {
+        int64_t gcount = 0, o = 0, ng = 0, z = 0, skipped = 0;
+        for (int t = 0; t < kt; ++t) {
+          int64_t we;
+          w_index(g, m, t, we);
+          switch (C.cls[we]) {
+            case 0: ++gcount; break;
+            case 1: ++o; break;
+            case 2: ++ng; break;
+            case 3:
+              if (P->opt_add) ++skipped;
+              else ++z;
+              break;
+          }
+        }
+        // add_plan_counts (runtime.hpp:512-525)
+        C.d_bmult += o + ng + z + skipped;
+        C.d_badd += skipped;
+        C.d_mulpt += gcount;
+        C.d_neg += ng;
+        const int64_t pass = o + ng + z;
+        C.d_add += gcount > 0 ? gcount - 1 + pass : std::max<int64_t>(0, pass - 1);
+        C.n_fresh += z;
+        if (gcount > 0) ++C.n_general;
+        else if (pass > 0) ++C.n_pass_only;
+        else ++C.n_empty;
+      }
+    C.planned = true;
+  }
+  const std::vector<uint8_t>& cls = C.cls;
+  P->prof.bypass_mult += C.d_bmult;
+  P->prof.bypass_add += C.d_badd;
+  P->prof.mul_pt += C.d_mulpt;
+  P->prof.negate += C.d_neg;
+  P->prof.add += C.d_add;
+  check(C.n_fresh == 0, HG_EVALIDATION,
+        "node '" + node.id + "': fresh-zero terms (optimized_addition off) are not supported on the GPU path");
+  check(C.n_empty == 0, HG_EVALIDATION, "node '" + node.id + "': outputs whose every term is skipped are not supported");
+  check(C.n_general == 0 || C.n_pass_only == 0, HG_EVALIDATION,
         "node '" + node.id + "': mixing rescaled and pass-through-only outputs yields mixed levels (unsupported)");
-  const bool rescale = n_general_outputs > 0;
+  const bool rescale = C.n_general > 0;
   if (rescale) require_mul_headroom(level);
 
   // device constants for this node (built once per level: model load)

@@ -29,7 +29,7 @@ constexpr size_t kSmemCap = 227 * 1024;
 template <typename W, int LOGN>
 struct Cfg {
   static constexpr int N = 1 << LOGN;
-  static constexpr size_t data_bytes = ((size_t)lz::smem_words<LOGN>() * sizeof(W) + 15) / 16 * 16;
+  static constexpr size_t data_bytes = ((size_t)lz::smem_words<W, LOGN>() * sizeof(W) + 15) / 16 * 16;
   static constexpr size_t tw_bytes = (size_t)N * sizeof(lz::TWT<W>);
   static constexpr bool TWS = data_bytes + tw_bytes <= kSmemCap;
   static constexpr size_t smem = data_bytes + (TWS ? tw_bytes : 0);
@@ -95,7 +95,7 @@ HG_KERNEL k_lift_ntt_t(const int64_t* __restrict__ src, uint64_t* __restrict__ o
   const W q = (W)c.L->q, q2 = q + q;
   for (int r = c.r0; r < c.r1; ++r) {
     const int64_t* g = src + (int64_t)r * n;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) c.s[lz::padj(i)] = (W)lift_signed(g[i], c.L->q);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) c.s[lz::padw<W>(i)] = (W)lift_signed(g[i], c.L->q);
     __syncthreads();
     lz::fwd<W, LOGN>(c.s, c.tw, q, q2);
     lz::store<W, LOGN>(out + ((int64_t)r * nl + c.limb) * n, c.s);
@@ -117,7 +117,7 @@ HG_KERNEL k_rescale_top_t(const uint64_t* __restrict__ in, int64_t* __restrict__
     lz::inv<W, LOGN>(c.s, c.tw, Lz<W>::ninv(*c.L), q, q2);
     int64_t* o = cen + (int64_t)r * n;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const uint64_t v = c.s[lz::padj(i)];
+      const uint64_t v = c.s[lz::padw<W>(i)];
       o[i] = v > half ? (int64_t)v - (int64_t)c.L->q : (int64_t)v;
     }
     __syncthreads();
@@ -141,7 +141,7 @@ HG_KERNEL k_rescale_rest_t(const uint64_t* __restrict__ in, const int64_t* __res
   const uint64_t Q = c.L->q, inv = R.inv[j], inv_s = R.inv_s[j];
   for (int r = c.r0; r < c.r1; ++r) {
     const int64_t* cv = cen + (int64_t)r * n;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) c.s[lz::padj(i)] = (W)lift_signed(cv[i], Q);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) c.s[lz::padw<W>(i)] = (W)lift_signed(cv[i], Q);
     __syncthreads();
     lz::fwd_but_last<W, LOGN>(c.s, c.tw, q, q2);
     const uint64_t* x = in + ((int64_t)r * nl + j) * n;
@@ -174,7 +174,7 @@ HG_KERNEL k_relin_c2_t(const uint64_t* __restrict__ a, const uint64_t* __restric
   for (int r = c.r0; r < c.r1; ++r) {
     const uint64_t* x1 = a + r * a_stride + a1_off + (int64_t)c.limb * n;
     const uint64_t* y1 = b + r * b_stride + b1_off + (int64_t)c.limb * n;
-    for (int k = threadIdx.x; k < n; k += blockDim.x) c.s[lz::padj(k)] = (W)mul_mod(x1[k], y1[k], *c.L);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) c.s[lz::padw<W>(k)] = (W)mul_mod(x1[k], y1[k], *c.L);
     __syncthreads();
     lz::inv<W, LOGN>(c.s, c.tw, Lz<W>::ninv(*c.L), q, q2);
     lz::store<W, LOGN>(c2 + ((int64_t)r * nl + c.limb) * n, c.s);
@@ -204,7 +204,19 @@ template <typename W, int LOGN>
 struct RelinCfg {
   static constexpr int threads = (1 << LOGN) / 16;
   static constexpr bool ACC_GLOBAL = sizeof(W) == 8 && LOGN >= 14;
+  // stage each source residue of c2 once in shared memory (cp.async, prefetched
+  // one residue ahead) instead of re-reading it from L2 for every digit
+  static constexpr bool C2S = Cfg<W, LOGN>::smem + ((size_t)8 << LOGN) <= kSmemCap;
+  static constexpr size_t smem = Cfg<W, LOGN>::smem + (C2S ? ((size_t)8 << LOGN) : 0);
 };
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];\n" ::"l"(p)); }
 
 template <typename W, int LOGN, bool GIVEN_D>
 __global__ void __launch_bounds__(RelinCfg<W, LOGN>::threads, 1)
@@ -216,6 +228,14 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN>::threads, 1)
   Cta<W, LOGN> c(smem, LL, items, G, P, false);
   constexpr int n = 1 << LOGN;
   constexpr bool AG = RelinCfg<W, LOGN>::ACC_GLOBAL;
+  constexpr bool C2S = RelinCfg<W, LOGN>::C2S;
+  uint64_t* c2s = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(smem) + Cfg<W, LOGN>::smem);
+  auto stage_c2 = [&](const uint64_t* gsrc) {
+    for (int k = threadIdx.x * 2; k < n; k += blockDim.x * 2) cp_async16(c2s + k, gsrc + k);
+    cp_async_commit();
+  };
+  (void)c2s;
+  (void)stage_c2;
   const int j = c.limb;
   const W q = (W)c.L->q, q2 = q + q;
   const uint64_t Q = c.L->q;
@@ -235,11 +255,33 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN>::threads, 1)
     const uint64_t* c2item = c2 + (int64_t)item * pw;
     for (int i = 0; i < nl; ++i) {
       const uint64_t* src = c2item + (int64_t)i * n;
+      if constexpr (C2S) {
+        if (item == c.r0 && i == 0) stage_c2(src);  // first residue of the group: nothing prefetched yet
+        cp_async_wait_all();
+        __syncthreads();  // c2s holds residue i of this item
+      }
       for (int d = 0; d < K.digits[i]; ++d) {
         const int row = K.rows0[i] + d;
         const int sh = 15 * d;
-        for (int k = threadIdx.x; k < n; k += blockDim.x) c.s[lz::padj(k)] = (W)((src[k] >> sh) & 0x7FFF);
+        const int64_t kof = (int64_t)row * 2 * K.key_poly_words + (int64_t)j * n + k0;
+        prefetch_l1(kpack + kof);  // this thread's key lines for the MAC below
+        prefetch_l1(kpack + kof + K.key_poly_words);
+        if constexpr (sizeof(W) == 8) {
+          prefetch_l1(kval + kof);
+          prefetch_l1(kval + kof + K.key_poly_words);
+        }
+        if constexpr (C2S) {
+          for (int k = threadIdx.x; k < n; k += blockDim.x) c.s[lz::padw<W>(k)] = (W)((c2s[k] >> sh) & 0x7FFF);
+        } else {
+          for (int k = threadIdx.x; k < n; k += blockDim.x) c.s[lz::padw<W>(k)] = (W)((src[k] >> sh) & 0x7FFF);
+        }
         __syncthreads();
+        if constexpr (C2S) {
+          if (d == K.digits[i] - 1) {  // residue consumed: prefetch the next one behind this digit's NTT
+            if (i + 1 < nl) stage_c2(src + n);
+            else if (item + 1 < c.r1) stage_c2(c2 + (int64_t)(item + 1) * pw);
+          }
+        }
         lz::fwd_but_last<W, LOGN>(c.s, c.tw, q, q2);
         W x[16];
         lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, x);
@@ -666,7 +708,7 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
     if (LL.count == 0) return;
     by_logn<W>(c, [&]<typename W_, int LOGN>() {
       if constexpr (LOGN <= 14) {
-        using Cf = Cfg<W_, LOGN>;
+        using Cf = RelinCfg<W_, LOGN>;
         const int threads = RelinCfg<W_, LOGN>::threads;
         const int64_t target = 148LL * 3;
         const int G = (int)std::max<int64_t>(1, std::min<int64_t>(16, (items * LL.count + target - 1) / target));

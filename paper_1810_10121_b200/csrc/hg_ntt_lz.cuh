@@ -16,10 +16,17 @@
 namespace hg {
 namespace lz {
 
-__host__ __device__ constexpr int padj(int j) { return j + (j >> 4); }
-__host__ __device__ constexpr int po(int r, int t) { return (r << t) + ((r << t) >> 4); }
-template <int LOGN>
-__host__ __device__ constexpr int smem_words() { return (1 << LOGN) + (1 << (LOGN - 4)); }
+// one pad word per 32 (32-bit words) or per 16 (64-bit words): a row of 128 bytes
+template <typename W>
+__host__ __device__ constexpr int pshift() { return sizeof(W) == 4 ? 5 : 4; }
+template <typename W>
+__host__ __device__ constexpr int padw(int j) { return j + (j >> pshift<W>()); }
+// padded offset of element r << t relative to the padded group base (no carry into
+// the pad bits for every pass of the remainder-first radix-16 structure)
+template <typename W>
+__host__ __device__ constexpr int pow_(int r, int t) { return (r << t) + ((r << t) >> pshift<W>()); }
+template <typename W, int LOGN>
+__host__ __device__ constexpr int smem_words() { return (1 << LOGN) + (1 << (LOGN - pshift<W>())); }
 
 template <typename W>
 using TWT = typename Lz<W>::TW;
@@ -45,13 +52,13 @@ __device__ __forceinline__ void fwd_pass(W* s, const TWT<W>* tw, W q, W q2) {
   constexpr int R = 1 << K, TL = LOGN - S0 - K;
   for (int vt = threadIdx.x; vt < (1 << (LOGN - K)); vt += blockDim.x) {
     const int g = vt >> TL;
-    const int pb = padj((g << (LOGN - S0)) + (vt & ((1 << TL) - 1)));
+    const int pb = padw<W>((g << (LOGN - S0)) + (vt & ((1 << TL) - 1)));
     W x[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) x[r] = s[pb + po(r, TL)];
+    for (int r = 0; r < R; ++r) x[r] = s[pb + pow_<W>(r,TL)];
     fwd_group<W, K, S0>(x, g, tw, q, q2);
 #pragma unroll
-    for (int r = 0; r < R; ++r) s[pb + po(r, TL)] = x[r];
+    for (int r = 0; r < R; ++r) s[pb + pow_<W>(r,TL)] = x[r];
   }
 }
 
@@ -81,7 +88,7 @@ __device__ __forceinline__ void fwd_but_last(W* s, const TWT<W>* tw, W q, W q2) 
 // the last pass of group vt: x[r] = evaluation 16 vt + r, in [0, 4q)
 template <typename W, int LOGN>
 __device__ __forceinline__ void fwd_last(const W* s, int vt, const TWT<W>* tw, W q, W q2, W (&x)[16]) {
-  const int pb = padj(vt << 4);
+  const int pb = padw<W>(vt << 4);
 #pragma unroll
   for (int r = 0; r < 16; ++r) x[r] = s[pb + r];
   fwd_group<W, 4, LOGN - 4>(x, vt, tw, q, q2);
@@ -93,7 +100,7 @@ __device__ __forceinline__ void fwd(W* s, const TWT<W>* tw, W q, W q2) {
   for (int vt = threadIdx.x; vt < (1 << (LOGN - 4)); vt += blockDim.x) {
     W x[16];
     fwd_last<W, LOGN>(s, vt, tw, q, q2, x);
-    const int pb = padj(vt << 4);
+    const int pb = padw<W>(vt << 4);
 #pragma unroll
     for (int r = 0; r < 16; ++r) s[pb + r] = canon4(x[r], q, q2);
   }
@@ -121,10 +128,10 @@ __device__ __forceinline__ void inv_pass(W* s, const TWT<W>* tw, TWT<W> ninv, W 
   constexpr int R = 1 << K;
   for (int vt = threadIdx.x; vt < (1 << (LOGN - K)); vt += blockDim.x) {
     const int gi = vt >> S0;
-    const int pb = padj((gi << (S0 + K)) + (vt & ((1 << S0) - 1)));
+    const int pb = padw<W>((gi << (S0 + K)) + (vt & ((1 << S0) - 1)));
     W x[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) x[r] = s[pb + po(r, S0)];
+    for (int r = 0; r < R; ++r) x[r] = s[pb + pow_<W>(r,S0)];
     inv_group<W, LOGN, K, S0>(x, gi, tw, q, q2);
     if constexpr (LAST) {
 #pragma unroll
@@ -134,7 +141,7 @@ __device__ __forceinline__ void inv_pass(W* s, const TWT<W>* tw, TWT<W> ninv, W 
       }
     }
 #pragma unroll
-    for (int r = 0; r < R; ++r) s[pb + po(r, S0)] = x[r];
+    for (int r = 0; r < R; ++r) s[pb + pow_<W>(r,S0)] = x[r];
   }
 }
 
@@ -168,7 +175,7 @@ __device__ __forceinline__ void load(W* s, const uint64_t* __restrict__ g) {
   const ulonglong2* g2 = reinterpret_cast<const ulonglong2*>(g);
   for (int i = threadIdx.x; i < (1 << (LOGN - 1)); i += blockDim.x) {
     const ulonglong2 v = g2[i];
-    const int p = padj(2 * i);
+    const int p = padw<W>(2 * i);
     s[p] = (W)v.x;
     s[p + 1] = (W)v.y;
   }
@@ -177,7 +184,7 @@ template <typename W, int LOGN>
 __device__ __forceinline__ void store(uint64_t* __restrict__ g, const W* s) {
   ulonglong2* g2 = reinterpret_cast<ulonglong2*>(g);
   for (int i = threadIdx.x; i < (1 << (LOGN - 1)); i += blockDim.x) {
-    const int p = padj(2 * i);
+    const int p = padw<W>(2 * i);
     g2[i] = make_ulonglong2((uint64_t)s[p], (uint64_t)s[p + 1]);
   }
 }

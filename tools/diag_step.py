@@ -29,3 +29,10 @@ for it in range(6):
           f"nodes {sum(pr['wall_ms'].values()):.2f} ms launches {plan.launches()}")
 print("wall", {k: round(v, 3) for k, v in pr["wall_ms"].items()})
 print("host", {k: round(v, 3) for k, v in pr["host_issue_ms"].items()})
+ctx.kernel_timing(True)
+ctx.kernel_stats()
+plan.run()
+torch.cuda.synchronize()
+st = ctx.kernel_stats()
+for k, v in sorted(st.items(), key=lambda kv: -kv[1]["total_ms"]):
+    print(f"  {k:24s} {v['launches']:4d} {v['total_ms']:9.3f} ms")
