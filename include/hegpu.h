@@ -103,6 +103,10 @@ int hg_weighted_sum(hg_context* ctx, const uint64_t* x, const int32_t* idx, cons
 int hg_encode(hg_context* ctx, const double* values, int64_t count, int level, double scale, uint64_t* pt_dev);
 /* scalar -> per-limb residues of llround(value*scale) (host array of level+1 words) */
 int hg_encode_constant(hg_context* ctx, double value, int level, double scale, uint64_t* residues_host);
+/* write those residues into every slot of a device plaintext (the NTT form of a constant) */
+int hg_fill_constant(hg_context* ctx, const uint64_t* residues_host, int level, uint64_t* pt_dev);
+/* decode a device plaintext (NTT form) to `count` slot values (CkksBackend::decode) */
+int hg_decode(hg_context* ctx, const uint64_t* pt_dev, int level, double scale, int64_t count, double* values_host);
 /* items fresh encryptions at `level`, seeds[item] (host), optional plaintexts pt_dev[item][nl][N] */
 int hg_encrypt(hg_context* ctx, const hg_keys* keys, const uint64_t* pt_dev, const uint64_t* seeds, int64_t items,
                int level, uint64_t* out);

@@ -103,6 +103,8 @@ def lib():
         "hg_kernel_stats_json": (C.c_int, [vp, C.c_char_p, C.c_size_t]),
         "hg_kernel_launches": (C.c_int64, [vp]),
         "hg_bench_modmul": (C.c_int, [vp, C.c_int, C.POINTER(C.c_double)]),
+        "hg_decode": (C.c_int, [vp, vp, C.c_int, C.c_double, C.c_int64, f64p]),
+        "hg_fill_constant": (C.c_int, [vp, u64p, C.c_int, vp]),
         "hg_sample_encryption": (C.c_int, [vp, u64p, C.c_int64, vp]),
         "hg_sample_encryption_host": (C.c_int, [vp, u64p, C.c_int64, vp]),
     }

@@ -361,4 +361,33 @@ int hg_sample_encryption_host(hg_context* ctx, const uint64_t* seeds, int64_t it
                             out_host + it * 3 * n + 2 * n);
   });
 }
+
+// decode one NTT-form plaintext (CkksBackend::decode, ckks_backend.hpp:218-221)
+int hg_decode(hg_context* ctx, const uint64_t* pt_dev, int level, double scale, int64_t count, double* values) {
+  return guard([&] {
+    hg::Context& c = *ctx->c;
+    level_ok(c, level);
+    const int64_t n = c.n(), words = (int64_t)(level + 1) * n;
+    auto* m = static_cast<uint64_t*>(c.scratch(static_cast<size_t>(words * 8), 6));
+    HG_CUDA(cudaMemcpyAsync(m, pt_dev, words * 8, cudaMemcpyDeviceToDevice, ctx->stream()));
+    hg::k::ntt(c, m, level + 1, level + 1, true, ctx->stream());
+    std::vector<uint64_t> mh(static_cast<size_t>(words));
+    HG_CUDA(cudaMemcpyAsync(mh.data(), m, words * 8, cudaMemcpyDeviceToHost, ctx->stream()));
+    HG_CUDA(cudaStreamSynchronize(ctx->stream()));
+    hg::decode_coeffs_host(c, mh.data(), level + 1, scale, count, values);
+  });
+}
+
+// fill a device plaintext with encode_constant residues (the same word in every slot, NTT form)
+int hg_fill_constant(hg_context* ctx, const uint64_t* residues, int level, uint64_t* pt_dev) {
+  return guard([&] {
+    hg::Context& c = *ctx->c;
+    level_ok(c, level);
+    const int64_t n = c.n();
+    std::vector<uint64_t> h(static_cast<size_t>((level + 1) * n));
+    for (int i = 0; i <= level; ++i) std::fill(h.begin() + i * n, h.begin() + (i + 1) * n, residues[i]);
+    HG_CUDA(cudaMemcpyAsync(pt_dev, h.data(), h.size() * 8, cudaMemcpyHostToDevice, ctx->stream()));
+    HG_CUDA(cudaStreamSynchronize(ctx->stream()));
+  });
+}
 }  // extern "C"
