@@ -19,6 +19,7 @@
 #include <chrono>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -478,7 +479,24 @@ struct NodeCache {
   std::vector<uint8_t> cls;
   int64_t d_bmult = 0, d_badd = 0, d_mulpt = 0, d_neg = 0, d_add = 0;
   int64_t n_general = 0, n_pass_only = 0, n_empty = 0, n_fresh = 0;
+  // tensor-core GEMM: byte-split weights packed per residue width class
+  struct TcClass {
+    int bytes = 0;
+    std::vector<int> limbs;
+    std::shared_ptr<DevArr> w;
+    int64_t group_stride = 0;
+  };
+  std::vector<TcClass> tc;
 };
+
+// HG_GEMM_TC=0 disables the tcgen05 path (falls back to the IMAD GEMM, same results)
+bool tc_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HG_GEMM_TC");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 }  // namespace
 }  // namespace hg
@@ -804,10 +822,39 @@ Val contraction(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_s
     HG_CUDA(cudaMemcpyAsync(C.w->p, wres.data(), wres.size() * 8, cudaMemcpyHostToDevice, S(P)));
     HG_CUDA(cudaMemcpyAsync(C.idx->p, xi.data(), xi.size() * 4, cudaMemcpyHostToDevice, S(P)));
     HG_CUDA(cudaMemcpyAsync(C.oidx->p, oi.data(), oi.size() * 4, cudaMemcpyHostToDevice, S(P)));
+    C.tc.clear();
+    if (tc_enabled() && mg >= 8 && k2::gemm_tc_supported(c, mg, kt)) {
+      std::map<int, std::vector<int>> by_bytes;
+      for (int j = 0; j < nl; ++j) by_bytes[k2::tc_bytes(c, j)].push_back(j);
+      for (auto& [bytes, limbs] : by_bytes) {
+        NodeCache::TcClass tcc;
+        tcc.bytes = bytes;
+        tcc.limbs = limbs;
+        std::vector<uint8_t> packed;
+        k2::pack_weights_tc(wres, wgroups, mg, kt, nl, limbs, bytes, k2::tc_ntile(bytes), packed, tcc.group_stride);
+        if (w_shared) tcc.group_stride = 0;
+        tcc.w = std::make_shared<DevArr>(packed.size(), S(P));
+        HG_CUDA(cudaMemcpyAsync(tcc.w->p, packed.data(), packed.size(), cudaMemcpyHostToDevice, S(P)));
+        HG_CUDA(cudaStreamSynchronize(S(P)));  // `packed` is pageable and goes out of scope
+        C.tc.push_back(std::move(tcc));
+      }
+    }
     HG_CUDA(cudaStreamSynchronize(S(P)));
     C.level = level;
     C.w_group_stride = w_shared ? 0 : static_cast<int64_t>(mg) * kt * nl;
   }
+  auto run_gemm = [&](uint64_t* accp) {
+    if (!C.tc.empty()) {
+      for (const auto& tcc : C.tc)
+        k2::gemm_tc(c, xt->p, xt->count, C.idx->as<int32_t>(), tcc.w->as<uint8_t>(), tcc.group_stride,
+                    C.oidx->as<int32_t>(), accp, groups, mg, kt, level + 1, tcc.limbs, tcc.bytes, S(P));
+      P->launches += static_cast<int64_t>(C.tc.size());
+    } else {
+      k::gemm_groups(c, xt->p, xt->count, C.idx->as<int32_t>(), C.w->as<uint64_t>(), C.w_group_stride,
+                     C.oidx->as<int32_t>(), accp, groups, mg, kt, level + 1, S(P));
+      P->launches += 1;
+    }
+  };
 
   Val out;
   out.shape = out_shape;
@@ -816,17 +863,13 @@ Val contraction(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_s
     // weighted_sum scale: x_scale * w_scale / dropped (ckks_backend.hpp:409)
     const double ws = static_cast<double>(c.primes()[level]);
     auto acc = new_ct(P, m_out, level, xt->scale);
-    k::gemm_groups(c, xt->p, xt->count, C.idx->as<int32_t>(), C.w->as<uint64_t>(), C.w_group_stride, C.oidx->as<int32_t>(),
-                   acc->p, groups, mg, kt, level + 1, S(P));
-    P->launches += 1;
+    run_gemm(acc->p);
     auto r = rescale_t(P, acc);
     r->scale = xt->scale * ws / ws;
     out.ct = r;
   } else {
     auto acc = new_ct(P, m_out, level, xt->scale);
-    k::gemm_groups(c, xt->p, xt->count, C.idx->as<int32_t>(), C.w->as<uint64_t>(), C.w_group_stride, C.oidx->as<int32_t>(),
-                   acc->p, groups, mg, kt, level + 1, S(P));
-    P->launches += 1;
+    run_gemm(acc->p);
     out.ct = acc;
   }
   return out;

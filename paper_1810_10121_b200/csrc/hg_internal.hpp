@@ -333,6 +333,18 @@ void gemm(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* i
 // given_d: a = size-3 input (d0, d1 taken from it); else d0/d1 from the tensor of a and b
 void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, int64_t a_stride,
            int64_t b_stride, bool given_d, const uint64_t* c2, uint64_t* out, int64_t items, int nl, cudaStream_t s);
+
+// tcgen05 byte-split GEMM (hg_gemm_tc.cu).  Limbs are processed per residue
+// width (bytes = ceil(bits(q)/8)); weights pre-packed by pack_weights_tc for
+// exactly `limbs` (wres = [wgroups][mg][kt][nl] residues).
+bool gemm_tc_supported(const Context& c, int mg, int kt);
+int tc_bytes(const Context& c, int limb);
+int tc_ntile(int bytes);
+void pack_weights_tc(const std::vector<uint64_t>& wres, int64_t wgroups, int mg, int kt, int nl,
+                     const std::vector<int>& limbs, int WB, int NT, std::vector<uint8_t>& out, int64_t& group_stride);
+void gemm_tc(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* idx, const uint8_t* wpk,
+             int64_t w_group_stride, const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt, int nl,
+             const std::vector<int>& limbs, int bytes, cudaStream_t s);
 }  // namespace k2
 
 }  // namespace hg
