@@ -99,8 +99,15 @@ int hg_weighted_sum(hg_context* ctx, const uint64_t* x, const int32_t* idx, cons
                     int64_t groups, int mg, int kt, int nl);
 
 /* ---- encoding / encryption (ckks_backend.hpp:182-249) ---- */
-/* host values -> device plaintext (NTT form, nl = level+1 limbs); the fp64 FFT runs on the host */
+/* values (host or device) -> device plaintext (NTT form, nl = level+1 limbs).  Replaces
+ * CkksBackend::encode (ckks_backend.hpp:182-197); the fp64 FFT + llround run on the GPU,
+ * bit-identical to the reference's SlotEncoder (encoder.hpp:58-77). */
 int hg_encode(hg_context* ctx, const double* values, int64_t count, int level, double scale, uint64_t* pt_dev);
+/* `cols` plaintexts at once: slot m of column e is values[e*col_stride + m*elem_stride]
+ * (pack_cipher's batch columns, packing.hpp:57-63, read straight from a [batch][elements]
+ * array with col_stride = 1, elem_stride = elements).  pt_dev: [cols][level+1][N]. */
+int hg_encode_batch(hg_context* ctx, const double* values, int64_t cols, int64_t count, int64_t col_stride,
+                    int64_t elem_stride, int level, double scale, uint64_t* pt_dev);
 /* scalar -> per-limb residues of llround(value*scale) (host array of level+1 words) */
 int hg_encode_constant(hg_context* ctx, double value, int level, double scale, uint64_t* residues_host);
 /* write those residues into every slot of a device plaintext (the NTT form of a constant) */
@@ -142,6 +149,24 @@ int hg_plan_set_input_ciphertexts(hg_plan* plan, const char* param_id, const uin
 int hg_plan_profile_json(hg_plan* plan, char* buf, size_t cap);
 /* kernel launches issued by the last hg_plan_run */
 int64_t hg_plan_launches(const hg_plan* plan);
+
+/* ---- output-sharded multi-GPU execution (one process per GPU, NCCL over NVLink) ----
+ * The reference runs each layer's outputs as independent parallel_for bodies
+ * (common.hpp:134-140, runtime.hpp:1104-1221); here every Dot/Conv computes only
+ * this rank's block of outputs (conv windows / Dot rows, else Dot columns), x^2
+ * runs on the shard, and a tensor is all-gathered (grouped in-place NCCL
+ * broadcasts) where a consumer needs every element.  Results are bit-identical
+ * to the unsharded run on every rank. */
+/* 128-byte NCCL unique id (rank 0 creates it; the caller broadcasts it, e.g. via torch.distributed) */
+int hg_comm_unique_id(void* id_out);
+/* join a `world`-rank group as `rank` on the plan's device; world == 1 turns sharding off */
+int hg_plan_set_comm(hg_plan* plan, int rank, int world, const void* id);
+/* in-process group on ONE device (checks the sharded path without NCCL): the plans, which
+ * share one context, run in lockstep, each computing its shard; gathers are device copies */
+int hg_group_run(hg_plan** plans, int world);
+/* the partition rule (host only): rank's block [g0,g1) x [m0,m1) of a contraction with
+ * `groups` input windows x `mg` outputs per window -> out4 = {g0, g1, m0, m1} */
+int hg_shard_partition(int64_t groups, int64_t mg, int world, int rank, int64_t* out4);
 
 /* ---- measurement hooks (bench.py) ---- */
 /* record CUDA events around every kernel launch of this context (off by default) */

@@ -83,13 +83,18 @@ def lib():
         "hg_square_relin_rescale": (C.c_int, [vp, vp, vp, vp, C.c_int64, C.c_int]),
         "hg_weighted_sum": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, C.c_int, C.c_int, C.c_int]),
         "hg_encode": (C.c_int, [vp, f64p, C.c_int64, C.c_int, C.c_double, vp]),
+        "hg_comm_unique_id": (C.c_int, [vp]),
+        "hg_plan_set_comm": (C.c_int, [vp, C.c_int, C.c_int, vp]),
+        "hg_group_run": (C.c_int, [C.POINTER(vp), C.c_int]),
+        "hg_shard_partition": (C.c_int, [C.c_int64, C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64)]),
+        "hg_encode_batch": (C.c_int, [vp, vp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_double, vp]),
         "hg_encode_constant": (C.c_int, [vp, C.c_double, C.c_int, C.c_double, u64p]),
         "hg_encrypt": (C.c_int, [vp, vp, vp, u64p, C.c_int64, C.c_int, vp]),
         "hg_decrypt_coeffs": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int, C.c_int, u64p]),
         "hg_decrypt": (C.c_int, [vp, vp, vp, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_int64, f64p]),
         "hg_plan_create": (C.c_int, [vp, vp, C.c_char_p, C.c_int64, C.c_uint64, C.POINTER(vp)]),
         "hg_plan_destroy": (None, [vp]),
-        "hg_plan_bind_input": (C.c_int, [vp, C.c_char_p, f64p, C.c_int64]),
+        "hg_plan_bind_input": (C.c_int, [vp, C.c_char_p, vp, C.c_int64]),
         "hg_plan_run": (C.c_int, [vp]),
         "hg_plan_output": (C.c_int, [vp, C.c_char_p, f64p, C.c_int64, C.POINTER(C.c_int64)]),
         "hg_plan_output_info": (C.c_int, [vp, C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int),
@@ -251,12 +256,24 @@ class Plan:
         self.keys = keys
         self.batch = batch
 
-    def bind_input(self, param_id: str, values: np.ndarray):
+    def bind_input(self, param_id: str, values):
+        """values: [batch, *shape] float64 -- numpy, or a contiguous torch tensor (pinned host or cuda)."""
+        if hasattr(values, "data_ptr"):
+            if not values.is_contiguous() or str(values.dtype) != "torch.float64":
+                raise HEError(1, "bind_input: tensor values must be contiguous float64")
+            _chk(lib().hg_plan_bind_input(self._h, param_id.encode(), values.data_ptr(), values.numel()))
+            return
         v = np.ascontiguousarray(values, dtype=np.float64)
-        _chk(lib().hg_plan_bind_input(self._h, param_id.encode(), v.ctypes.data_as(f64p), v.size))
+        _chk(lib().hg_plan_bind_input(self._h, param_id.encode(), v.ctypes.data, v.size))
 
     def run(self):
         _chk(lib().hg_plan_run(self._h))
+
+    def set_comm(self, rank: int, world: int, comm_id: bytes = None):
+        """Shard every Dot/Conv over `world` ranks (one process per GPU, NCCL);
+        comm_id: the 128 bytes from comm_unique_id() on rank 0, shared by the caller."""
+        buf = None if comm_id is None else C.create_string_buffer(bytes(comm_id), 128)
+        _chk(lib().hg_plan_set_comm(self._h, rank, world, buf))
 
     def output(self, out_id: str, shape=None) -> np.ndarray:
         n = C.c_int64()
@@ -327,3 +344,24 @@ def call(name: str, *args):
         else:
             conv.append(a)
     _chk(fn(*conv))
+
+
+# ---- output-sharded execution ----
+
+def comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _chk(lib().hg_comm_unique_id(buf))
+    return buf.raw
+
+
+def group_run(plans):
+    """Run plans of one graph (sharing one Context) as an in-process shard group on one GPU."""
+    arr = (vp * len(plans))(*[p._h for p in plans])
+    _chk(lib().hg_group_run(arr, len(plans)))
+
+
+def shard_partition(groups: int, mg: int, world: int, rank: int):
+    """The executor's contraction partition: (g0, g1, m0, m1) of rank (host only)."""
+    out = (C.c_int64 * 4)()
+    _chk(lib().hg_shard_partition(groups, mg, world, rank, out))
+    return tuple(out)

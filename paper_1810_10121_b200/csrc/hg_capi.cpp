@@ -228,25 +228,43 @@ int hg_weighted_sum(hg_context* ctx, const uint64_t* x, const int32_t* idx, cons
   });
 }
 
+static void encode_batch_impl(hg_context* ctx, const double* values, int64_t cols, int64_t count, int64_t col_stride,
+                              int64_t elem_stride, int level, double scale, uint64_t* pt_dev) {
+  hg::Context& c = *ctx->c;
+  level_ok(c, level);
+  hg::check(scale > 0.0, HG_E_VALIDATION, "encoding scale must be positive");
+  hg::check(cols >= 0 && count >= 0, HG_E_VALIDATION, "negative size");
+  if (cols == 0) return;
+  const int64_t n = c.n();
+  cudaPointerAttributes pa{};
+  const bool on_device = cudaPointerGetAttributes(&pa, values) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
+  (void)cudaGetLastError();
+  const double* dv = values;
+  if (!on_device) {  // stage the host span the columns cover
+    const int64_t span = (cols - 1) * col_stride + (count > 0 ? (count - 1) * elem_stride + 1 : 1);
+    auto* d = static_cast<double*>(c.scratch(static_cast<size_t>(span) * 8, 10));
+    HG_CUDA(cudaMemcpyAsync(d, values, static_cast<size_t>(span) * 8, cudaMemcpyHostToDevice, ctx->stream()));
+    dv = d;
+  }
+  auto* ci = static_cast<int64_t*>(c.scratch(static_cast<size_t>(cols * n) * 8 + 16, 4));
+  int* flag = reinterpret_cast<int*>(ci + cols * n);
+  HG_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), ctx->stream()));
+  hg::k::encode_fft(c, dv, cols, count, col_stride, elem_stride, scale, ci, flag, ctx->stream());
+  hg::k::lift_ntt(c, ci, pt_dev, cols, level + 1, ctx->stream());
+  int overflow = 0;
+  HG_CUDA(cudaMemcpyAsync(&overflow, flag, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream()));
+  HG_CUDA(cudaStreamSynchronize(ctx->stream()));
+  hg::check(overflow == 0, HG_E_VALIDATION, "encoded coefficient overflows the integer range");
+}
+
 int hg_encode(hg_context* ctx, const double* values, int64_t count, int level, double scale, uint64_t* pt_dev) {
-  return guard([&] {
-    hg::Context& c = *ctx->c;
-    level_ok(c, level);
-    hg::check(scale > 0.0, HG_E_VALIDATION, "encoding scale must be positive");
-    const int64_t n = c.n();
-    std::vector<double> coeffs(n);
-    c.encoder().values_to_coeffs(values, count, coeffs.data());
-    std::vector<int64_t> ci(n);
-    for (int64_t k = 0; k < n; ++k) {  // ckks_backend.hpp:186-193
-      const double scaled = coeffs[k] * scale;
-      hg::check(std::abs(scaled) < 9.0e18, HG_E_VALIDATION, "encoded coefficient overflows the integer range");
-      ci[k] = std::llround(scaled);
-    }
-    auto* d = static_cast<int64_t*>(c.scratch(n * 8, 4));
-    HG_CUDA(cudaMemcpyAsync(d, ci.data(), n * 8, cudaMemcpyHostToDevice, ctx->stream()));
-    hg::k::lift_ntt(c, d, pt_dev, 1, level + 1, ctx->stream());
-    HG_CUDA(cudaStreamSynchronize(ctx->stream()));
-  });
+  // CkksBackend::encode (ckks_backend.hpp:182-197), encoded on the GPU
+  return guard([&] { encode_batch_impl(ctx, values, 1, count, count, 1, level, scale, pt_dev); });
+}
+
+int hg_encode_batch(hg_context* ctx, const double* values, int64_t cols, int64_t count, int64_t col_stride,
+                    int64_t elem_stride, int level, double scale, uint64_t* pt_dev) {
+  return guard([&] { encode_batch_impl(ctx, values, cols, count, col_stride, elem_stride, level, scale, pt_dev); });
 }
 
 int hg_encode_constant(hg_context* ctx, double value, int level, double scale, uint64_t* residues) {

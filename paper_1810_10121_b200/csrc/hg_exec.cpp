@@ -31,6 +31,9 @@
 #include <thread>
 #include <vector>
 
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl is dlopen'ed (the process's own, e.g. torch's)
+
 #include <nlohmann/json.hpp>
 
 #include "../../include/hegpu.h"
@@ -428,12 +431,33 @@ struct DevArr {  // stream-ordered scratch array
   T* as() const { return static_cast<T*>(p); }
 };
 
+// Element ownership of a sharded ciphertext tensor: ranges[r] are the
+// sorted, disjoint element ranges [b, e) rank r computed.  The tensor's buffer is
+// full-size on every rank; only the caller's own ranges are valid until gathered.
+struct ShardMap {
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> ranges;
+  int64_t count(int r) const {
+    int64_t c = 0;
+    for (const auto& [b, e] : ranges[static_cast<size_t>(r)]) c += e - b;
+    return c;
+  }
+};
+
+// Moves the other ranks' ranges of a sharded tensor into this rank's buffer.
+// Every rank calls it for the same tensors in the same order (the gather points
+// are a pure function of the graph and the world size).
+struct Transport {
+  virtual ~Transport() = default;
+  virtual void allgatherv(hg_plan* P, const std::string& id, CtT& ct, const ShardMap& m) = 0;
+};
+
 struct Val {
   std::vector<int64_t> shape;
   bool batched = false;
   bool from_constants = false;
   std::shared_ptr<const HTensor> raw;
   std::shared_ptr<CtT> ct;
+  std::shared_ptr<const ShardMap> shard;  // null: every element valid here
   bool is_raw() const { return raw != nullptr; }
   bool is_cipher() const { return ct != nullptr; }
   int64_t handles() const { return ct ? ct->count : 0; }
@@ -474,6 +498,9 @@ struct NodeCache {
   std::shared_ptr<DevArr> res;    // per-item constant residues
   bool pt_is_const = false;
   int64_t counts_add = 0;
+  // sharded contraction: every rank's output ranges; this rank's output count
+  std::shared_ptr<const ShardMap> shard;
+  int64_t local_count = 0;
   // contraction plan (deterministic per node): term classes and the per-run profile increments
   bool planned = false;
   std::vector<uint8_t> cls;
@@ -496,6 +523,21 @@ bool tc_enabled() {
     return !(e && e[0] == '0');
   }();
   return on;
+}
+// contractions with fewer outputs per group (HG_TC_MIN_OUTPUTS) or fewer terms per output
+// (HG_TC_MIN_TERMS) than these stay on the IMAD GEMM: a tensor-core CTA needs a few K steps to
+// amortise its TMEM/barrier setup (measured: conv 5x25 is 2x slower on tcgen05, dense 100x845 3x faster)
+int tc_env(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+int tc_min_outputs() {
+  static const int v = tc_env("HG_TC_MIN_OUTPUTS", 1);
+  return v;
+}
+int tc_min_terms() {
+  static const int v = tc_env("HG_TC_MIN_TERMS", 64);
+  return v;
 }
 
 }  // namespace
@@ -521,12 +563,65 @@ struct hg_plan {
   // bypass config (runtime.hpp:84-88 defaults)
   bool opt_mul = true, opt_add = true;
   double eps = 0.0;
+  // output-sharded execution over `world` ranks (one GPU each); the transport
+  // all-gathers a sharded tensor where a consumer needs every element
+  int rank = 0, world = 1;
+  std::shared_ptr<hg::Transport> transport;
+  std::map<std::string, hg::Val>* live = nullptr;  // the running step's values (in-process group transport)
 };
 
 namespace hg {
 namespace {
 
 cudaStream_t S(const hg_plan* P) { return P->ctx->stream(); }
+
+// ---------------------------------------------------------------------------
+// Output sharding: each Dot/Conv computes only this rank's block
+// of outputs; tensors are all-gathered where a consumer needs every element.
+// ---------------------------------------------------------------------------
+struct Part {
+  int64_t g0, g1, m0, m1;
+};
+// balanced contiguous split of [0, n): the first n % world ranks get one extra
+void split_range(int64_t n, int world, int rank, int64_t& b, int64_t& e) {
+  const int64_t base = n / world, extra = n % world;
+  b = rank * base + std::min<int64_t>(rank, extra);
+  e = b + base + (rank < extra ? 1 : 0);
+}
+// a contraction of `groups` input windows x `mg` outputs per window: split the
+// windows (conv positions, Dot rows) when there is more than one, else the outputs
+Part shard_part(int64_t groups, int64_t mg, int world, int rank) {
+  Part p{0, groups, 0, mg};
+  if (world <= 1) return p;
+  if (groups > 1) split_range(groups, world, rank, p.g0, p.g1);
+  else split_range(mg, world, rank, p.m0, p.m1);
+  return p;
+}
+std::vector<std::pair<int64_t, int64_t>> coalesce(std::vector<int64_t> v) {
+  std::sort(v.begin(), v.end());
+  std::vector<std::pair<int64_t, int64_t>> r;
+  for (int64_t x : v) {
+    if (!r.empty() && r.back().second == x) ++r.back().second;
+    else r.push_back({x, x + 1});
+  }
+  return r;
+}
+
+void ensure_full(hg_plan* P, const std::string& id, Val& v) {
+  if (!v.shard) return;
+  if (P->world > 1) {
+    check(P->transport != nullptr, HG_EINTERNAL, "sharded plan without a transport");
+    P->transport->allgatherv(P, id, *v.ct, *v.shard);
+  }
+  v.shard = nullptr;
+}
+
+// consumers that work element-by-element on their own shard (no gather needed)
+bool keeps_shard(const GNode& node) {
+  if (node.op == Op::Reshape) return true;
+  if (node.op == Op::PolyAct) return attr_f64(node, "a") == 1.0 && attr_f64(node, "b") == 0.0 && attr_f64(node, "c") == 0.0;
+  return false;
+}
 
 Special classify_scalar(const hg_plan* P, double v) {  // runtime.hpp:395-401
   if (std::abs(v) <= P->eps) return Special::Zero;
@@ -620,25 +715,42 @@ void host_parallel(int64_t n, const std::function<void(int64_t)>& body) {
   if (err) std::rethrow_exception(err);
 }
 
-// Encode batch columns (full FFT encode at level/scale) for a set of elements
-// into a device plaintext array [count][nl][N] (ckks_backend.hpp:182-197).
+// Slot-encode `cols` columns already in device memory (column e, slot m at
+// dvals[e*col_stride + m*elem_stride]) at level/scale into a device plaintext
+// array [cols][nl][N] (ckks_backend.hpp:182-197): bit-exact fp64 FFT + llround
+// on the GPU (hg_encode.cu), then lift + forward NTT per limb.
+std::shared_ptr<DevArr> encode_device(hg_plan* P, const double* dvals, int64_t cols, int64_t count, int64_t col_stride,
+                                      int64_t elem_stride, int level, double scale) {
+  const Context& c = *P->ctx;
+  const int64_t n = c.n();
+  check(level >= 0 && level <= c.max_level(), HG_EVALIDATION, "level outside the modulus chain");
+  check(scale > 0.0, HG_EVALIDATION, "encoding scale must be positive");
+  auto pt = std::make_shared<DevArr>(static_cast<size_t>(cols) * (level + 1) * n * 8, S(P));
+  if (cols == 0) return pt;
+  DevArr ci(static_cast<size_t>(cols * n) * 8, S(P));
+  DevArr flag(sizeof(int), S(P));
+  HG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), S(P)));
+  k::encode_fft(c, dvals, cols, count, col_stride, elem_stride, scale, ci.as<int64_t>(), flag.as<int>(), S(P));
+  k::lift_ntt(c, ci.as<int64_t>(), pt->as<uint64_t>(), cols, level + 1, S(P));
+  P->launches += 2;
+  int overflow = 0;
+  HG_CUDA(cudaMemcpyAsync(&overflow, flag.p, sizeof(int), cudaMemcpyDeviceToHost, S(P)));
+  HG_CUDA(cudaStreamSynchronize(S(P)));
+  check(overflow == 0, HG_EVALIDATION, "encoded coefficient overflows the integer range");
+  return pt;
+}
+
+// Encode host batch columns (bias columns, runtime.hpp:386-409): staged to the device, encoded there.
 std::shared_ptr<DevArr> encode_columns(hg_plan* P, const std::vector<std::vector<double>>& cols, int level,
                                        double scale) {
-  const Context& c = *P->ctx;
-  const int64_t n = c.n(), m = static_cast<int64_t>(cols.size());
-  check(level >= 0 && level <= c.max_level(), HG_EVALIDATION, "level outside the modulus chain");
-  std::vector<int64_t> ci(static_cast<size_t>(m * n));
-  host_parallel(m, [&](int64_t e) {
-    std::vector<double> coeffs(n);
-    c.encoder().values_to_coeffs(cols[e].data(), static_cast<int64_t>(cols[e].size()), coeffs.data());
-    for (int64_t k = 0; k < n; ++k) ci[e * n + k] = llround_checked(coeffs[k], scale);
-  });
-  DevArr src(ci.size() * 8, S(P));
-  HG_CUDA(cudaMemcpyAsync(src.p, ci.data(), ci.size() * 8, cudaMemcpyHostToDevice, S(P)));
-  auto pt = std::make_shared<DevArr>(static_cast<size_t>(m) * (level + 1) * n * 8, S(P));
-  k::lift_ntt(c, src.as<int64_t>(), pt->as<uint64_t>(), m, level + 1, S(P));
-  P->launches += 1;
-  HG_CUDA(cudaStreamSynchronize(S(P)));  // host staging buffer goes out of scope
+  const int64_t m = static_cast<int64_t>(cols.size());
+  int64_t count = 0;
+  for (const auto& col : cols) count = std::max<int64_t>(count, static_cast<int64_t>(col.size()));
+  std::vector<double> flat(static_cast<size_t>(m * count), 0.0);  // shorter columns: zero slots, as the encoder pads
+  for (int64_t e = 0; e < m; ++e) std::copy(cols[e].begin(), cols[e].end(), flat.begin() + e * count);
+  DevArr d(flat.size() * 8, S(P));
+  HG_CUDA(cudaMemcpyAsync(d.p, flat.data(), flat.size() * 8, cudaMemcpyHostToDevice, S(P)));
+  auto pt = encode_device(P, d.as<double>(), m, count, count, 1, level, scale);  // synchronises
   return pt;
 }
 
@@ -770,19 +882,25 @@ Val contraction(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_s
   const bool rescale = C.n_general > 0;
   if (rescale) require_mul_headroom(level);
 
+  // this rank's block of the contraction (everything when world == 1)
+  const bool sharded = P->world > 1;
+  const Part part = shard_part(groups, mg, P->world, P->rank);
+  const int64_t lg = part.g1 - part.g0;
+  const int lmg = static_cast<int>(part.m1 - part.m0);
+
   // device constants for this node (built once per level: model load)
   if (C.level != level) {
     const int nl = level + 1;
     const uint64_t ql = c.primes()[level];
     const double w_scale = static_cast<double>(ql);  // operand_scale(level), backend.hpp:167-170
-    const int64_t wgroups = w_shared ? 1 : groups;
-    std::vector<uint64_t> wres(static_cast<size_t>(wgroups * mg * kt * nl));
-    for (int64_t g = 0; g < wgroups; ++g)
-      for (int m = 0; m < mg; ++m)
+    const int64_t wgroups = w_shared ? 1 : lg;
+    std::vector<uint64_t> wres(static_cast<size_t>(wgroups * lmg * kt * nl));
+    for (int64_t gl = 0; gl < wgroups; ++gl)
+      for (int ml = 0; ml < lmg; ++ml)
         for (int t = 0; t < kt; ++t) {
           int64_t we;
-          w_index(g, m, t, we);
-          uint64_t* dst = &wres[((g * mg + m) * kt + t) * nl];
+          w_index(w_shared ? 0 : part.g0 + gl, static_cast<int>(part.m0) + ml, t, we);
+          uint64_t* dst = &wres[((gl * lmg + ml) * kt + t) * nl];
           switch (cls[we]) {
             case 0: {
               const int64_t v = llround_checked(rv.t->v[we], w_scale);
@@ -803,18 +921,40 @@ Val contraction(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_s
               for (int j = 0; j < nl; ++j) dst[j] = 0;
           }
         }
-    std::vector<int32_t> xi(static_cast<size_t>(groups * kt)), oi(static_cast<size_t>(m_out));
-    for (int64_t g = 0; g < groups; ++g) {
+    // output element of every local (g, m); sharded plans accumulate into a compact
+    // buffer (sorted local elements) and record every rank's ownership for the gathers
+    std::vector<int32_t> xi(static_cast<size_t>(lg * kt)), oi(static_cast<size_t>(lg * lmg));
+    for (int64_t gl = 0; gl < lg; ++gl) {
       for (int t = 0; t < kt; ++t) {
         int64_t xe;
-        x_index(g, t, xe);
-        xi[g * kt + t] = static_cast<int32_t>(xe);
+        x_index(part.g0 + gl, t, xe);
+        xi[gl * kt + t] = static_cast<int32_t>(xe);
       }
-      for (int m = 0; m < mg; ++m) {
+      for (int ml = 0; ml < lmg; ++ml) {
         int64_t oe;
-        out_index(g, m, oe);
-        oi[g * mg + m] = static_cast<int32_t>(oe);
+        out_index(part.g0 + gl, static_cast<int>(part.m0) + ml, oe);
+        oi[gl * lmg + ml] = static_cast<int32_t>(oe);
       }
+    }
+    C.shard.reset();
+    C.local_count = lg * lmg;
+    if (sharded) {
+      auto map = std::make_shared<ShardMap>();
+      for (int r = 0; r < P->world; ++r) {
+        const Part pr = shard_part(groups, mg, P->world, r);
+        std::vector<int64_t> els;
+        for (int64_t g = pr.g0; g < pr.g1; ++g)
+          for (int64_t m = pr.m0; m < pr.m1; ++m) {
+            int64_t oe;
+            out_index(g, static_cast<int>(m), oe);
+            els.push_back(oe);
+          }
+        map->ranges.push_back(coalesce(std::move(els)));
+      }
+      std::vector<int64_t> mine(oi.begin(), oi.end());
+      std::sort(mine.begin(), mine.end());
+      for (auto& o : oi) o = static_cast<int32_t>(std::lower_bound(mine.begin(), mine.end(), o) - mine.begin());
+      C.shard = map;
     }
     C.w = std::make_shared<DevArr>(wres.size() * 8, S(P));
     C.idx = std::make_shared<DevArr>(xi.size() * 4, S(P));
@@ -823,7 +963,7 @@ Val contraction(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_s
     HG_CUDA(cudaMemcpyAsync(C.idx->p, xi.data(), xi.size() * 4, cudaMemcpyHostToDevice, S(P)));
     HG_CUDA(cudaMemcpyAsync(C.oidx->p, oi.data(), oi.size() * 4, cudaMemcpyHostToDevice, S(P)));
     C.tc.clear();
-    if (tc_enabled() && mg >= 8 && k2::gemm_tc_supported(c, mg, kt)) {
+    if (tc_enabled() && lmg >= tc_min_outputs() && kt >= tc_min_terms() && k2::gemm_tc_supported(c, lmg, kt)) {
       std::map<int, std::vector<int>> by_bytes;
       for (int j = 0; j < nl; ++j) by_bytes[k2::tc_bytes(c, j)].push_back(j);
       for (auto& [bytes, limbs] : by_bytes) {
@@ -831,7 +971,8 @@ Val contraction(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_s
         tcc.bytes = bytes;
         tcc.limbs = limbs;
         std::vector<uint8_t> packed;
-        k2::pack_weights_tc(wres, wgroups, mg, kt, nl, limbs, bytes, k2::tc_ntile(bytes), packed, tcc.group_stride);
+        k2::pack_weights_tc(wres, wgroups, lmg, kt, nl, limbs, bytes, k2::tc_ntile(bytes, lmg), packed,
+                            tcc.group_stride);
         if (w_shared) tcc.group_stride = 0;
         tcc.w = std::make_shared<DevArr>(packed.size(), S(P));
         HG_CUDA(cudaMemcpyAsync(tcc.w->p, packed.data(), packed.size(), cudaMemcpyHostToDevice, S(P)));
@@ -841,17 +982,18 @@ Val contraction(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_s
     }
     HG_CUDA(cudaStreamSynchronize(S(P)));
     C.level = level;
-    C.w_group_stride = w_shared ? 0 : static_cast<int64_t>(mg) * kt * nl;
+    C.w_group_stride = w_shared ? 0 : static_cast<int64_t>(lmg) * kt * nl;
   }
   auto run_gemm = [&](uint64_t* accp) {
+    if (C.local_count == 0) return;  // nothing assigned to this rank
     if (!C.tc.empty()) {
       for (const auto& tcc : C.tc)
         k2::gemm_tc(c, xt->p, xt->count, C.idx->as<int32_t>(), tcc.w->as<uint8_t>(), tcc.group_stride,
-                    C.oidx->as<int32_t>(), accp, groups, mg, kt, level + 1, tcc.limbs, tcc.bytes, S(P));
+                    C.oidx->as<int32_t>(), accp, lg, lmg, kt, level + 1, tcc.limbs, tcc.bytes, S(P));
       P->launches += static_cast<int64_t>(C.tc.size());
     } else {
       k::gemm_groups(c, xt->p, xt->count, C.idx->as<int32_t>(), C.w->as<uint64_t>(), C.w_group_stride,
-                     C.oidx->as<int32_t>(), accp, groups, mg, kt, level + 1, S(P));
+                     C.oidx->as<int32_t>(), accp, lg, lmg, kt, level + 1, S(P));
       P->launches += 1;
     }
   };
@@ -859,18 +1001,28 @@ Val contraction(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_s
   Val out;
   out.shape = out_shape;
   out.batched = out_batched;
+  auto acc = new_ct(P, sharded ? C.local_count : m_out, level, xt->scale);
+  run_gemm(acc->p);
+  std::shared_ptr<CtT> res = acc;
   if (rescale) {
     // weighted_sum scale: x_scale * w_scale / dropped (ckks_backend.hpp:409)
     const double ws = static_cast<double>(c.primes()[level]);
-    auto acc = new_ct(P, m_out, level, xt->scale);
-    run_gemm(acc->p);
-    auto r = rescale_t(P, acc);
-    r->scale = xt->scale * ws / ws;
-    out.ct = r;
+    res = C.local_count > 0 ? rescale_t(P, acc) : new_ct(P, 0, level - 1, xt->scale);
+    res->scale = xt->scale * ws / ws;
+  }
+  if (sharded) {
+    // place this rank's (sorted, compact) outputs at their element positions
+    auto full = new_ct(P, m_out, res->level, res->scale);
+    int64_t off = 0;
+    for (const auto& [b, e] : C.shard->ranges[static_cast<size_t>(P->rank)]) {
+      HG_CUDA(cudaMemcpyAsync(full->item(b), res->item(off), static_cast<size_t>((e - b) * res->item_words()) * 8,
+                              cudaMemcpyDeviceToDevice, S(P)));
+      off += e - b;
+    }
+    out.ct = full;
+    out.shard = C.shard;
   } else {
-    auto acc = new_ct(P, m_out, level, xt->scale);
-    run_gemm(acc->p);
-    out.ct = acc;
+    out.ct = res;
   }
   return out;
 }
@@ -1038,6 +1190,28 @@ Val kernel_poly_act(hg_plan* P, const GNode& node, const std::vector<int64_t>& o
     return o;
   };
   std::shared_ptr<CtT> acc;
+  if (x.shard && P->world > 1) {
+    // sharded x^2 (keeps_shard): multiply_rescale on this rank's element ranges only
+    check(a == 1.0 && b == 0.0 && cc == 0.0, HG_EINTERNAL, "sharded polynomial activation must be x^2");
+    require_mul_headroom(level);
+    const int nl = level + 1;
+    const double dropped = static_cast<double>(c.primes()[level]);
+    auto o = new_ct(P, m, level - 1, xe->scale * xe->scale / dropped);
+    for (const auto& [b0, e0] : x.shard->ranges[static_cast<size_t>(P->rank)]) {
+      const int64_t cnt = e0 - b0;
+      DevArr prod(static_cast<size_t>(cnt) * 2 * nl * c.n() * 8, S(P));
+      DevArr c2(static_cast<size_t>(cnt) * nl * c.n() * 8, S(P));
+      DevArr sc(static_cast<size_t>(cnt) * 2 * c.n() * 8, S(P));
+      k::square_relin(c, *P->keys, xe->item(b0), prod.as<uint64_t>(), cnt, nl, c2.as<uint64_t>(), S(P));
+      k::rescale(c, prod.as<uint64_t>(), o->item(b0), cnt * 2, nl, sc.as<int64_t>(), S(P));
+    }
+    Val out;
+    out.shape = out_shape;
+    out.batched = x.batched;
+    out.ct = o;
+    out.shard = x.shard;
+    return out;
+  }
   if (a != 0.0) {
     require_mul_headroom(level);
     const int nl = level + 1;
@@ -1385,6 +1559,7 @@ Val kernel_rearrange(hg_plan* P, const GNode& node, const std::vector<int64_t>& 
     out.shape = out_shape;
     out.batched = out_batched;
     out.ct = x.ct;  // handle copy: zero-copy view
+    out.shard = x.shard;  // same element order: ownership carries over
     return out;
   }
   const auto es = element_space(out_shape, out_batched);
@@ -1564,58 +1739,80 @@ Val exec_node(hg_plan* P, const GNode& node, const std::vector<const Val*>& in) 
   }
 }
 
-void run_plan(hg_plan* P) {
+struct RunState {
+  std::map<std::string, int64_t> uses;
+  std::map<std::string, Val> values;
+  int64_t live = 0, launches0 = 0;
+  std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> timing;
+};
+
+void run_begin(hg_plan* P, RunState& st) {
   P->prof = Profile{};
   P->launches = 0;
   P->outputs.clear();
   admit_depth(P);
-  const int64_t launches0 = P->ctx->kt_launches();
-  std::map<std::string, int64_t> uses;
+  st.launches0 = P->ctx->kt_launches();
   for (const auto& [id, n] : P->g.nodes)
-    for (const auto& in : n.inputs) ++uses[in];
-  for (const auto& o : P->g.outputs) ++uses[o];
-  std::map<std::string, Val> values;
-  int64_t live = 0;
-  std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> timing;
-  for (const auto& id : P->order) {
-    const GNode& node = P->g.nodes.at(id);
-    cudaEvent_t e0, e1;
-    HG_CUDA(cudaEventCreate(&e0));
-    HG_CUDA(cudaEventCreate(&e1));
-    HG_CUDA(cudaEventRecord(e0, S(P)));
-    const auto h0 = std::chrono::steady_clock::now();
-    Val v;
-    if (node.op == Op::Parameter) {
-      auto it = P->bound.find(id);
-      if (it == P->bound.end()) fail(HG_EVALIDATION, "no input bound for parameter '" + id + "'");
-      v = it->second;
-    } else {
-      std::vector<const Val*> in;
-      for (const auto& i : node.inputs) in.push_back(&values.at(i));
-      v = exec_node(P, node, in);
-    }
-    HG_CUDA(cudaEventRecord(e1, S(P)));
-    P->prof.host_ms[id] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
-    timing.push_back({id, {e0, e1}});
-    live += v.handles();
-    P->prof.peak_elements = std::max(P->prof.peak_elements, live);
-    values[id] = std::move(v);
+    for (const auto& in : n.inputs) ++st.uses[in];
+  for (const auto& o : P->g.outputs) ++st.uses[o];
+  P->live = &st.values;
+}
+
+void run_node(hg_plan* P, RunState& st, const std::string& id) {
+  const GNode& node = P->g.nodes.at(id);
+  cudaEvent_t e0, e1;
+  HG_CUDA(cudaEventCreate(&e0));
+  HG_CUDA(cudaEventCreate(&e1));
+  HG_CUDA(cudaEventRecord(e0, S(P)));
+  const auto h0 = std::chrono::steady_clock::now();
+  Val v;
+  if (node.op == Op::Parameter) {
+    auto it = P->bound.find(id);
+    if (it == P->bound.end()) fail(HG_EVALIDATION, "no input bound for parameter '" + id + "'");
+    v = it->second;
+  } else {
+    std::vector<const Val*> in;
     for (const auto& i : node.inputs) {
-      auto u = uses.find(i);
-      if (u == uses.end()) continue;
-      if (--(u->second) > 0) continue;
-      auto vt = values.find(i);
-      if (vt != values.end()) {
-        live -= vt->second.handles();
-        values.erase(vt);
-      }
-      uses.erase(u);
+      Val& iv = st.values.at(i);
+      if (iv.shard && !keeps_shard(node)) ensure_full(P, i, iv);
+      in.push_back(&iv);
     }
+    v = exec_node(P, node, in);
   }
-  for (const auto& o : P->g.outputs) P->outputs[o] = values.at(o);
-  P->launches = P->ctx->kt_launches() - launches0;  // counted at every launch site
+  HG_CUDA(cudaEventRecord(e1, S(P)));
+  P->prof.host_ms[id] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+  st.timing.push_back({id, {e0, e1}});
+  st.live += v.handles();
+  P->prof.peak_elements = std::max(P->prof.peak_elements, st.live);
+  st.values[id] = std::move(v);
+}
+
+// drop the inputs of `id` whose last consumer it was
+void run_release(hg_plan* P, RunState& st, const std::string& id) {
+  for (const auto& i : P->g.nodes.at(id).inputs) {
+    auto u = st.uses.find(i);
+    if (u == st.uses.end()) continue;
+    if (--(u->second) > 0) continue;
+    auto vt = st.values.find(i);
+    if (vt != st.values.end()) {
+      st.live -= vt->second.handles();
+      st.values.erase(vt);
+    }
+    st.uses.erase(u);
+  }
+}
+
+void run_outputs(hg_plan* P, RunState& st) {
+  for (const auto& o : P->g.outputs) {
+    ensure_full(P, o, st.values.at(o));
+    P->outputs[o] = st.values.at(o);
+  }
+}
+
+void run_end(hg_plan* P, RunState& st) {
+  P->launches = P->ctx->kt_launches() - st.launches0;  // counted at every launch site
   HG_CUDA(cudaStreamSynchronize(S(P)));
-  for (auto& [id, ev] : timing) {
+  for (auto& [id, ev] : st.timing) {
     float ms = 0.f;
     HG_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second));
     P->prof.wall_ms[id] += ms;
@@ -1623,6 +1820,113 @@ void run_plan(hg_plan* P) {
     cudaEventDestroy(ev.first);
     cudaEventDestroy(ev.second);
   }
+  st.timing.clear();
+  P->live = nullptr;
+}
+
+void run_plan(hg_plan* P) {
+  RunState st;
+  run_begin(P, st);
+  try {
+    for (const auto& id : P->order) {
+      run_node(P, st, id);
+      run_release(P, st, id);
+    }
+    run_outputs(P, st);
+  } catch (...) {
+    P->live = nullptr;
+    throw;
+  }
+  run_end(P, st);
+}
+
+// In-process group: all ranks' plans on one device and stream, stepped node by
+// node in lockstep so a gather always finds every rank's shard computed.  Used
+// to check the sharded path on one GPU; the NCCL transport runs one plan per process.
+struct LocalGroupTransport final : Transport {
+  std::vector<hg_plan*> plans;
+  void allgatherv(hg_plan* P, const std::string& id, CtT& ct, const ShardMap& m) override {
+    const int64_t ew = ct.item_words();
+    for (int r = 0; r < static_cast<int>(plans.size()); ++r) {
+      if (r == P->rank) continue;
+      check(plans[r]->live != nullptr, HG_EINTERNAL, "group peer is not running");
+      const Val& pv = plans[r]->live->at(id);
+      check(pv.ct && pv.ct->level == ct.level && pv.ct->count == ct.count, HG_EINTERNAL, "group peer tensor mismatch");
+      for (const auto& [b, e] : m.ranges[static_cast<size_t>(r)])
+        HG_CUDA(cudaMemcpyAsync(ct.p + b * ew, pv.ct->p + b * ew, static_cast<size_t>((e - b) * ew) * 8,
+                                cudaMemcpyDeviceToDevice, S(P)));
+    }
+  }
+};
+
+// NCCL over NVLink/NVSwitch, one process per GPU: a gather is one grouped set of
+// in-place broadcasts, each rank broadcasting its own ranges (an all-gather-v).
+struct NcclApi {
+  decltype(&ncclGetUniqueId) get_id = nullptr;
+  decltype(&ncclCommInitRank) init = nullptr;
+  decltype(&ncclCommDestroy) destroy = nullptr;
+  decltype(&ncclBroadcast) bcast = nullptr;
+  decltype(&ncclGroupStart) gstart = nullptr;
+  decltype(&ncclGroupEnd) gend = nullptr;
+  decltype(&ncclGetErrorString) errstr = nullptr;
+};
+const NcclApi& nccl() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) fail(HG_EINTERNAL, std::string("NCCL is not loadable: ") + dlerror());
+    auto sym = [&](const char* name) {
+      void* f = dlsym(h, name);
+      if (!f) fail(HG_EINTERNAL, std::string("NCCL symbol missing: ") + name);
+      return f;
+    };
+    a.get_id = reinterpret_cast<decltype(a.get_id)>(sym("ncclGetUniqueId"));
+    a.init = reinterpret_cast<decltype(a.init)>(sym("ncclCommInitRank"));
+    a.destroy = reinterpret_cast<decltype(a.destroy)>(sym("ncclCommDestroy"));
+    a.bcast = reinterpret_cast<decltype(a.bcast)>(sym("ncclBroadcast"));
+    a.gstart = reinterpret_cast<decltype(a.gstart)>(sym("ncclGroupStart"));
+    a.gend = reinterpret_cast<decltype(a.gend)>(sym("ncclGroupEnd"));
+    a.errstr = reinterpret_cast<decltype(a.errstr)>(sym("ncclGetErrorString"));
+    return a;
+  }();
+  return api;
+}
+void nccl_ok(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) fail(HG_ECUDA, std::string(what) + ": " + nccl().errstr(r));
+}
+
+struct NcclTransport final : Transport {
+  ncclComm_t comm = nullptr;
+  ~NcclTransport() override {
+    if (comm) nccl().destroy(comm);
+  }
+  void allgatherv(hg_plan* P, const std::string&, CtT& ct, const ShardMap& m) override {
+    const int64_t ew = ct.item_words();
+    nccl_ok(nccl().gstart(), "ncclGroupStart");
+    for (int r = 0; r < static_cast<int>(m.ranges.size()); ++r)
+      for (const auto& [b, e] : m.ranges[static_cast<size_t>(r)])
+        nccl_ok(nccl().bcast(ct.p + b * ew, ct.p + b * ew, static_cast<size_t>((e - b) * ew), ncclUint64, r, comm,
+                             S(P)),
+                "ncclBroadcast");
+    nccl_ok(nccl().gend(), "ncclGroupEnd");
+  }
+};
+
+void run_group(const std::vector<hg_plan*>& ps) {
+  std::vector<RunState> st(ps.size());
+  for (size_t r = 0; r < ps.size(); ++r) run_begin(ps[r], st[r]);
+  try {
+    for (const auto& id : ps[0]->order) {
+      for (size_t r = 0; r < ps.size(); ++r) run_node(ps[r], st[r], id);
+      for (size_t r = 0; r < ps.size(); ++r) run_release(ps[r], st[r], id);
+    }
+    for (size_t r = 0; r < ps.size(); ++r) run_outputs(ps[r], st[r]);
+  } catch (...) {
+    for (auto* p : ps) p->live = nullptr;
+    throw;
+  }
+  for (size_t r = 0; r < ps.size(); ++r) run_end(ps[r], st[r]);
 }
 
 }  // namespace
@@ -1700,12 +2004,19 @@ int hg_plan_bind_input(hg_plan* P, const char* param_id, const double* values, i
     hg::Rng seed_rng = P->rng.fork("inputs").fork(std::string(param_id));
     std::vector<uint64_t> seeds(static_cast<size_t>(nb));
     for (auto& s : seeds) s = seed_rng.next();
-    std::vector<std::vector<double>> cols(static_cast<size_t>(nb));
-    for (int64_t e = 0; e < nb; ++e) {
-      cols[e].resize(P->batch);
-      for (int64_t b = 0; b < P->batch; ++b) cols[e][b] = values[b * nb + e];
+    // values: [batch][nb] row-major (packing.hpp:57-63: column e = element e across the batch),
+    // host (pinned or pageable) or device memory; encoded on the GPU
+    cudaPointerAttributes pa{};
+    const bool on_device = cudaPointerGetAttributes(&pa, values) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
+    (void)cudaGetLastError();
+    std::unique_ptr<hg::DevArr> staged;
+    const double* dvals = values;
+    if (!on_device) {
+      staged = std::make_unique<hg::DevArr>(static_cast<size_t>(count) * 8, hg::S(P));
+      HG_CUDA(cudaMemcpyAsync(staged->p, values, static_cast<size_t>(count) * 8, cudaMemcpyHostToDevice, hg::S(P)));
+      dvals = staged->as<double>();
     }
-    auto pt = hg::encode_columns(P, cols, L, c.default_scale());
+    auto pt = hg::encode_device(P, dvals, nb, P->batch, 1, nb, L, c.default_scale());
     auto ct = hg::new_ct(P, nb, L, c.default_scale());
     hg::encrypt_items(P, seeds, pt->as<uint64_t>(), L, ct->p);
     hg::Val v;
@@ -1752,6 +2063,69 @@ int hg_plan_run(hg_plan* P) {
   return guard_x([&] { hg::run_plan(P); });
 }
 
+int hg_comm_unique_id(void* id_out) {
+  return guard_x([&] {
+    hg::check(id_out != nullptr, HG_E_VALIDATION, "null argument");
+    ncclUniqueId id;
+    hg::nccl_ok(hg::nccl().get_id(&id), "ncclGetUniqueId");
+    std::memcpy(id_out, &id, sizeof(id));
+  });
+}
+
+int hg_plan_set_comm(hg_plan* P, int rank, int world, const void* id) {
+  return guard_x([&] {
+    hg::check(P && world >= 1 && rank >= 0 && rank < world, HG_E_VALIDATION, "invalid rank/world");
+    P->cache.clear();  // contraction blocks depend on the partition
+    P->rank = rank;
+    P->world = world;
+    P->transport.reset();
+    if (world == 1) return;
+    hg::check(id != nullptr, HG_E_VALIDATION, "a communicator id is required for world > 1");
+    auto t = std::make_shared<hg::NcclTransport>();
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    HG_CUDA(cudaSetDevice(P->ctx->device()));
+    hg::nccl_ok(hg::nccl().init(&t->comm, world, uid, rank), "ncclCommInitRank");
+    P->transport = t;
+  });
+}
+
+int hg_group_run(hg_plan** plans, int world) {
+  return guard_x([&] {
+    hg::check(plans && world >= 1, HG_E_VALIDATION, "invalid group");
+    std::vector<hg_plan*> ps(plans, plans + world);
+    for (auto* p : ps) {
+      hg::check(p && p->ctx == ps[0]->ctx, HG_E_VALIDATION, "group plans must share one context (device and stream)");
+      hg::check(p->g.nodes.size() == ps[0]->g.nodes.size() && p->order == ps[0]->order, HG_E_VALIDATION,
+                "group plans must run the same graph");
+    }
+    auto t = std::dynamic_pointer_cast<hg::LocalGroupTransport>(ps[0]->transport);
+    if (!t || t->plans != ps || ps[0]->world != world) {
+      t = std::make_shared<hg::LocalGroupTransport>();
+      t->plans = ps;
+      for (int r = 0; r < world; ++r) {
+        ps[r]->cache.clear();
+        ps[r]->rank = r;
+        ps[r]->world = world;
+        ps[r]->transport = t;
+      }
+    }
+    hg::run_group(ps);
+  });
+}
+
+int hg_shard_partition(int64_t groups, int64_t mg, int world, int rank, int64_t* out4) {
+  return guard_x([&] {
+    hg::check(out4 && world >= 1 && rank >= 0 && rank < world && groups >= 0 && mg >= 0, HG_E_VALIDATION,
+              "invalid partition query");
+    const hg::Part p = hg::shard_part(groups, mg, world, rank);
+    out4[0] = p.g0;
+    out4[1] = p.g1;
+    out4[2] = p.m0;
+    out4[3] = p.m1;
+  });
+}
+
 int hg_plan_output_info(hg_plan* P, const char* id, int64_t* elements, int* level, double* scale) {
   return guard_x([&] {
     auto it = P->outputs.find(id);
@@ -1794,7 +2168,7 @@ int hg_plan_output(hg_plan* P, const char* id, double* values, int64_t capacity,
     const hg::Context& c = *P->ctx;
     const int nl = v.ct->nl();
     const int64_t n = c.n();
-    hg::DevBuf md(static_cast<size_t>(m) * nl * n * 8);
+    hg::DevArr md(static_cast<size_t>(m) * nl * n * 8, hg::S(P));
     hg::k::decrypt(c, *P->keys, v.ct->p, md.as<uint64_t>(), m, 2, nl, hg::S(P));
     std::vector<uint64_t> mh(static_cast<size_t>(m) * nl * n);
     HG_CUDA(cudaMemcpyAsync(mh.data(), md.p, mh.size() * 8, cudaMemcpyDeviceToHost, hg::S(P)));

@@ -317,7 +317,8 @@ bool gemm_tc_supported(const Context& c, int mg, int kt) {
 }
 
 int tc_bytes(const Context& c, int limb) { return limb_bytes(c.primes()[limb]); }
-int tc_ntile(int bytes) { return bytes <= 4 ? 64 : 32; }
+// output tile: the smallest MMA N covering the outputs (fewer TMEM columns -> more CTAs per SM)
+int tc_ntile(int bytes, int mg) { return mg <= 16 ? 16 : (mg <= 32 || bytes > 4) ? 32 : 64; }
 
 void gemm_tc(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* idx, const uint8_t* wpk,
              int64_t w_group_stride, const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt, int nl,
@@ -327,14 +328,13 @@ void gemm_tc(const Context& c, const uint64_t* x, int64_t x_items, const int32_t
   const double in_items = std::min<double>((double)groups * kt, (double)x_items);
   c.kt_begin("k_gemm_tc", s, frac * (in_items + (double)groups * mg) * item_bytes,
              frac * (double)groups * mg * kt * 2.0 * nl * c.n());
-  switch (bytes) {
-    case 4: launch_tc<4, 64>(c, x, idx, wpk, w_group_stride, oidx, out, groups, mg, kt, nl, limbs, s); break;
-    case 5: launch_tc<5, 32>(c, x, idx, wpk, w_group_stride, oidx, out, groups, mg, kt, nl, limbs, s); break;
-    case 6: launch_tc<6, 32>(c, x, idx, wpk, w_group_stride, oidx, out, groups, mg, kt, nl, limbs, s); break;
-    case 7: launch_tc<7, 32>(c, x, idx, wpk, w_group_stride, oidx, out, groups, mg, kt, nl, limbs, s); break;
-    default: fail(HG_EINTERNAL, "tensor-core GEMM: unsupported residue width");
-  }
-  c.kt_end(s);
+  const int nt = tc_ntile(bytes, mg);
+#define HG_TC(B, NT) \
+  if (bytes == B && nt == NT) { launch_tc<B, NT>(c, x, idx, wpk, w_group_stride, oidx, out, groups, mg, kt, nl, limbs, s); c.kt_end(s); return; }
+  HG_TC(4, 16) HG_TC(4, 32) HG_TC(4, 64)
+  HG_TC(5, 16) HG_TC(5, 32) HG_TC(6, 16) HG_TC(6, 32) HG_TC(7, 16) HG_TC(7, 32)
+#undef HG_TC
+  fail(HG_EINTERNAL, "tensor-core GEMM: unsupported residue width");
 }
 
 }  // namespace k2

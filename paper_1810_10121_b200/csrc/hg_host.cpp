@@ -367,6 +367,10 @@ Context::Context(const ContextParamsH& p, int device) : m_p(p), m_device(device)
     m_rows += m_digits[i];
   }
   m_enc = std::make_unique<SlotEncoder>(n);
+  m_enc_dev.alloc(static_cast<size_t>(4 * n) * sizeof(double));
+  HG_CUDA(cudaMemcpy(m_enc_dev.p, m_enc->roots_interleaved().data(), 2 * n * sizeof(double), cudaMemcpyHostToDevice));
+  HG_CUDA(cudaMemcpy(m_enc_dev.as<double>() + 2 * n, m_enc->half_roots_interleaved().data(), 2 * n * sizeof(double),
+                     cudaMemcpyHostToDevice));
 }
 
 Context::~Context() {

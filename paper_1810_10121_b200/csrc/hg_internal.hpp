@@ -172,6 +172,9 @@ class Context {
   cudaStream_t stream() const { return m_use_ext ? m_ext : m_stream; }
   void set_stream(cudaStream_t s, bool use_ext) { m_ext = s; m_use_ext = use_ext; }
   const SlotEncoder& encoder() const { return *m_enc; }
+  // device copies of the encoder tables: roots (2N doubles), half roots (2N doubles)
+  const double* enc_roots_dev() const { return m_enc_dev.as<double>(); }
+  const double* enc_half_dev() const { return m_enc_dev.as<double>() + 2 * m_p.n; }
   // host copies of the tables (for tests / host reference use)
   const std::vector<uint64_t>& psi(int i) const { return m_psi[static_cast<size_t>(i)]; }
   // rescale constants: inv(q_t mod q_j) and its Shoup constant
@@ -227,6 +230,7 @@ class Context {
   DevBuf m_tables;
   CtxParams m_kp{};
   std::unique_ptr<SlotEncoder> m_enc;
+  DevBuf m_enc_dev;
   std::map<int, DevBuf> m_scratch;
 };
 
@@ -311,6 +315,11 @@ void gather_items(const Context& c, const uint64_t* in, const int32_t* idx, uint
 // keygen pointwise: out = -(a*s + e) (+ f*s^2 on limb `special` if special >= 0)
 // fresh-encryption samples (u, e0, e1) for host seeds, on the GPU, bit-identical to sample_encryption()
 void sample_encryption_gpu(const Context& c, const uint64_t* seeds_host, int64_t items, int64_t* out, cudaStream_t s);
+// bit-exact slot encode on the GPU (encoder.hpp:58-77 + ckks_backend.hpp:186-192):
+// column e holds values[e*col_stride + m*elem_stride], m < count; out int64 [cols][N]
+// = llround(coeff * scale).  Sets *flag (device int) when a coefficient overflows.
+void encode_fft(const Context& c, const double* values, int64_t cols, int64_t count, int64_t col_stride,
+                int64_t elem_stride, double scale, int64_t* out, int* flag, cudaStream_t s);
 // register-only Shoup modmul throughput on every SM (modmul/s); wide = 64-bit words
 double modmul_peak(const Context& c, bool wide, cudaStream_t s);
 void keygen_b(const Context& c, const uint64_t* a, const uint64_t* sk, const uint64_t* e, uint64_t* out, int nl,
@@ -339,7 +348,7 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
 // exactly `limbs` (wres = [wgroups][mg][kt][nl] residues).
 bool gemm_tc_supported(const Context& c, int mg, int kt);
 int tc_bytes(const Context& c, int limb);
-int tc_ntile(int bytes);
+int tc_ntile(int bytes, int mg);
 void pack_weights_tc(const std::vector<uint64_t>& wres, int64_t wgroups, int mg, int kt, int nl,
                      const std::vector<int>& limbs, int WB, int NT, std::vector<uint8_t>& out, int64_t& group_stride);
 void gemm_tc(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* idx, const uint8_t* wpk,

@@ -270,19 +270,17 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN>::threads, 1)
           prefetch_l1(kval + kof);
           prefetch_l1(kval + kof + K.key_poly_words);
         }
+        // digit (c2_i >> 15d) & 0x7FFF (ckks_backend.hpp:520-521), extracted inside the first NTT pass
         if constexpr (C2S) {
-          for (int k = threadIdx.x; k < n; k += blockDim.x) c.s[lz::padw<W>(k)] = (W)((c2s[k] >> sh) & 0x7FFF);
-        } else {
-          for (int k = threadIdx.x; k < n; k += blockDim.x) c.s[lz::padw<W>(k)] = (W)((src[k] >> sh) & 0x7FFF);
-        }
-        __syncthreads();
-        if constexpr (C2S) {
+          lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return (W)((c2s[k] >> sh) & 0x7FFF); }, c.tw, q, q2);
           if (d == K.digits[i] - 1) {  // residue consumed: prefetch the next one behind this digit's NTT
             if (i + 1 < nl) stage_c2(src + n);
             else if (item + 1 < c.r1) stage_c2(c2 + (int64_t)(item + 1) * pw);
           }
+        } else {
+          lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return (W)((__ldg(src + k) >> sh) & 0x7FFF); }, c.tw, q, q2);
         }
-        lz::fwd_but_last<W, LOGN>(c.s, c.tw, q, q2);
+        lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2);
         W x[16];
         lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, x);
         const int64_t koff = (int64_t)row * 2 * K.key_poly_words + (int64_t)j * n + k0;

@@ -232,17 +232,23 @@ struct Lz<uint64_t> {
   static __device__ __forceinline__ TW ninv(const LimbInfo& L) { return make_ulonglong2(L.ninv, L.ninv_s); }
 };
 
+// a >= m ? a - m : a  (a < 2m).  32-bit: one fused add+min (VIADDMNMX): a - m wraps above a when a < m
+template <typename W>
+__device__ __forceinline__ W csub(W a, W m) {
+  if constexpr (sizeof(W) == 4) return min(a, a - m);
+  else return a >= m ? a - m : a;
+}
+
 template <typename W>
 __device__ __forceinline__ void ct_lz(W& a, W& b, typename Lz<W>::TW w, W q, W q2) {
-  const W x = a >= q2 ? a - q2 : a;
+  const W x = csub(a, q2);
   const W t = Lz<W>::mulw(b, w, q);
   a = x + t;
   b = x - t + q2;
 }
 template <typename W>
 __device__ __forceinline__ void gs_lz(W& a, W& b, typename Lz<W>::TW w, W q, W q2) {
-  W s = a + b;
-  s = s >= q2 ? s - q2 : s;
+  const W s = csub<W>(a + b, q2);
   const W d = a - b + q2;
   a = s;
   b = Lz<W>::mulw(d, w, q);
@@ -250,8 +256,7 @@ __device__ __forceinline__ void gs_lz(W& a, W& b, typename Lz<W>::TW w, W q, W q
 // [0, 4q) -> [0, q)
 template <typename W>
 __device__ __forceinline__ W canon4(W x, W q, W q2) {
-  x = x >= q2 ? x - q2 : x;
-  return x >= q ? x - q : x;
+  return csub(csub(x, q2), q);
 }
 
 // K forward stages (s0 .. s0+K-1) on one register group of block g (elements

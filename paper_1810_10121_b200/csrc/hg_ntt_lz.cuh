@@ -85,6 +85,37 @@ __device__ __forceinline__ void fwd_but_last(W* s, const TWT<W>* tw, W q, W q2) 
   static_assert(LOGN <= 16, "transform size");
 }
 
+// First pass with its input produced on the fly: element k (natural order) = get(k).
+// Fuses the staging of a freshly computed row (e.g. a relinearisation digit) into
+// the pass, saving one shared-memory store + load per element.  Ends with a barrier.
+template <typename W, int LOGN, typename Get>
+__device__ __forceinline__ void fwd_first_from(W* s, Get get, const TWT<W>* tw, W q, W q2) {
+  constexpr int K = (LOGN & 3) ? (LOGN & 3) : 4, R = 1 << K, TL = LOGN - K;
+  for (int vt = threadIdx.x; vt < (1 << TL); vt += blockDim.x) {
+    const int pb = padw<W>(vt);
+    W x[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r] = get(vt + (r << TL));
+    fwd_group<W, K, 0>(x, 0, tw, q, q2);
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[pb + pow_<W>(r, TL)] = x[r];
+  }
+  __syncthreads();
+}
+// the passes between fwd_first_from and fwd_last; ends with a barrier when it runs any
+template <typename W, int LOGN>
+__device__ __forceinline__ void fwd_middle(W* s, const TWT<W>* tw, W q, W q2) {
+  constexpr int K0 = (LOGN & 3) ? (LOGN & 3) : 4;
+  if constexpr (K0 + 4 < LOGN) {
+    fwd_pass<W, LOGN, 4, K0>(s, tw, q, q2);
+    __syncthreads();
+  }
+  if constexpr (K0 + 8 < LOGN) {
+    fwd_pass<W, LOGN, 4, K0 + 4>(s, tw, q, q2);
+    __syncthreads();
+  }
+}
+
 // the last pass of group vt: x[r] = evaluation 16 vt + r, in [0, 4q)
 template <typename W, int LOGN>
 __device__ __forceinline__ void fwd_last(const W* s, int vt, const TWT<W>* tw, W q, W q2, W (&x)[16]) {
@@ -136,8 +167,7 @@ __device__ __forceinline__ void inv_pass(W* s, const TWT<W>* tw, TWT<W> ninv, W 
     if constexpr (LAST) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        const W y = Lz<W>::mulw(x[r], ninv, q);  // x N^{-1} in [0, 2q)
-        x[r] = y >= q ? y - q : y;
+        x[r] = csub(Lz<W>::mulw(x[r], ninv, q), q);  // x N^{-1} in [0, 2q) -> canonical
       }
     }
 #pragma unroll
