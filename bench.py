@@ -150,7 +150,8 @@ def reference_arm(args):
     prof = res["profile"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": args.gpus,
-        "steps": len(runs), "warmup": 1, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "steps": len(runs), "warmup": 1, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if args.mode == "shard" and args.gpus > 1 else "weak",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": workload_config(args, ctxp),
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": threads, "kind": "reference",
@@ -168,11 +169,14 @@ def workload_config(args, ctxp) -> dict:
     return {"workload": f"BASELINE configs[2] CryptoNets-shaped (Pad, Conv 5x5/2 x5, x^2, Dense 845->100, x^2, "
                         f"Dense 100->10), batch {args.batch} images per ciphertext",
             "config": args.config, "poly_degree": ctxp["n"], "coeff_mod_bits": ctxp["bits"],
-            "scale_bits": ctxp["scale_bits"], "global_batch": args.batch * args.gpus,
+            "scale_bits": ctxp["scale_bits"],
+            "global_batch": args.batch * (args.gpus if args.mode == "replicas" else 1),
             "special_prime_reading": "coeff_mod_bits=[base, rescale..., special]; special = q_L",
             "l2": "inputs (784 ciphertexts, 720 MB) exceed the 126 MB L2 every step",
             "paradigm": "encrypted-data, bypass {mult: on, add: on, eps: 0}",
-            "parallelism": f"replicas x{args.gpus}"}
+            "parallelism": (f"replicas x{args.gpus}" if args.mode == "replicas" or args.gpus == 1 else
+                            f"output-sharded Dot/Conv over {args.gpus} GPUs, x^2 on the shard, "
+                            f"NCCL all-gather-v of activations between layers")}
 
 
 def roofline_from_stats(stats: dict, peaks: dict, int_peak32: float):
@@ -219,6 +223,12 @@ def ours_arm(args):
     ctx = P.Context(ctxp["n"], ctxp["bits"], ctxp["scale_bits"], security=ctxp["security"], device=dev)
     keys = P.Keys(ctx, spec["key_seed"])
     plan = P.Plan(ctx, keys, g, spec["batch"], spec["exec_seed"])
+    shard = ws > 1 and args.mode == "shard"
+    if shard:
+        # every Dot/Conv split by outputs over the ranks; activations all-gathered over NVLink (NCCL)
+        obj = [P.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        plan.set_comm(rank, ws, obj[0])
     plan.bind_input("x", x)
     log(f"[rank {rank}] setup {time.time() - t0:.1f}s")
     stream = torch.cuda.current_stream(dev)
@@ -249,7 +259,8 @@ def ours_arm(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
-    value = ws * spec["batch"] / (ms_step / 1e3)
+    images = spec["batch"] * (1 if shard else ws)  # shard: one batch split over the ranks; replicas: one per rank
+    value = images / (ms_step / 1e3)
 
     # ---- e2e: pinned host pixels -> H2D -> GPU encode+encrypt -> graph -> decrypt -> D2H -> host decode ----
     x_host = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).pin_memory()
@@ -298,13 +309,14 @@ def ours_arm(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if shard else "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded pixels k/255, weights N(0,1/fan_in))",
             "config": workload_config(args, ctxp),
             "roofline": rl, "roofline_modmul": rl_int,
             "int_peaks": {"modmul32_per_s": int_peak32, "modmul64_per_s": int_peak64},
             "cpu_baseline": cpu,
-            "e2e": {"value": ws * spec["batch"] / e2e_s, "unit": "images/s", "h2d_bytes_per_step": h2d,
+            "e2e": {"value": images / e2e_s, "unit": "images/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
                     "step_ms": [round(v, 3) for v in e2e_steps_ms]},
             "gpu_launches": launches,
@@ -327,6 +339,8 @@ def main():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--batch", type=int, default=4096)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--mode", default="shard", choices=["shard", "replicas"],
+                    help="N>1: shard each Dot/Conv by outputs (NCCL gathers) or run independent replicas")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)
