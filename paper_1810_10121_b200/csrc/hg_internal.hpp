@@ -244,6 +244,7 @@ struct Keys {
   // same shape, Shoup companions for the key-switch MAC: limbs < 2^30 hold
   // (floor(w 2^32/q) << 32 | w), wider limbs hold floor(w 2^64/q)
   DevBuf relin_pack;
+  DevBuf relin_mont;  // u32 [rows][2][(L+1) N]: w 2^32 mod q for limbs q < 2^30 (key-switch MAC from shared memory)
   bool has_relin = false;
 };
 std::unique_ptr<Keys> generate_keys(const Context& ctx, uint64_t seed, bool with_relin);

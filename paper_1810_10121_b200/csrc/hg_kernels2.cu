@@ -194,6 +194,8 @@ HG_KERNEL k_relin_c2_t(const uint64_t* __restrict__ a, const uint64_t* __restric
 //   64-bit limbs: key value + 64-bit Shoup constant; acc canonical
 // Epilogue adds d0 = a0 b0, d1 = a0 b1 + a1 b0 (or given d0, d1).
 // ---------------------------------------------------------------------------
+constexpr bool kPrefetchKeys = false;
+
 struct RelinC {
   int rows0[HG_MAX_LIMBS];
   int digits[HG_MAX_LIMBS];
@@ -207,8 +209,22 @@ struct RelinCfg {
   // stage each source residue of c2 once in shared memory (cp.async, prefetched
   // one residue ahead) instead of re-reading it from L2 for every digit
   static constexpr bool C2S = Cfg<W, LOGN>::smem + ((size_t)8 << LOGN) <= kSmemCap;
-  static constexpr size_t smem = Cfg<W, LOGN>::smem + (C2S ? ((size_t)8 << LOGN) : 0);
+  // 32-bit limbs: the digit's key row (b and a, Montgomery form, 4 bytes each) is
+  // copied into shared memory with cp.async while the digit's NTT runs
+  static constexpr size_t key_bytes = (size_t)8 << LOGN;
+  static constexpr bool KS = sizeof(W) == 4 && C2S &&
+                             Cfg<W, LOGN>::smem + ((size_t)8 << LOGN) + key_bytes <= kSmemCap;
+  static constexpr size_t smem = Cfg<W, LOGN>::smem + (C2S ? ((size_t)8 << LOGN) : 0) + (KS ? key_bytes : 0);
 };
+// conflict-free slot of 16-byte key chunk c (thread t reads chunks 4t .. 4t+3 with LDS.128)
+__device__ __forceinline__ int key_slot(int c) { return c ^ ((c >> 2) & 7); }
+// -q^{-1} mod 2^32 (Newton), for the Montgomery key MAC
+__device__ __forceinline__ uint32_t neg_qinv32(uint32_t q) {
+  uint32_t inv = q;  // correct to 3 bits for odd q
+#pragma unroll
+  for (int i = 0; i < 4; ++i) inv *= 2u - q * inv;
+  return 0u - inv;
+}
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
@@ -222,14 +238,18 @@ template <typename W, int LOGN, bool GIVEN_D>
 __global__ void __launch_bounds__(RelinCfg<W, LOGN>::threads, 1)
     k_relin_t(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int64_t a_stride, int64_t b_stride,
               const uint64_t* __restrict__ c2, const uint64_t* __restrict__ kval,
-              const uint64_t* __restrict__ kpack, uint64_t* __restrict__ out, int nl, int64_t items, int G,
-              const RelinC K, const LimbList LL, const CtxParams P) {
+              const uint64_t* __restrict__ kpack, const uint32_t* __restrict__ kmont, uint64_t* __restrict__ out,
+              int nl, int64_t items, int G, const RelinC K, const LimbList LL, const CtxParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
   Cta<W, LOGN> c(smem, LL, items, G, P, false);
   constexpr int n = 1 << LOGN;
   constexpr bool AG = RelinCfg<W, LOGN>::ACC_GLOBAL;
   constexpr bool C2S = RelinCfg<W, LOGN>::C2S;
+  constexpr bool KS = RelinCfg<W, LOGN>::KS;
   uint64_t* c2s = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(smem) + Cfg<W, LOGN>::smem);
+  uint4* ks = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(smem) + Cfg<W, LOGN>::smem + ((size_t)8 << LOGN));
+  (void)ks;
+  (void)kmont;
   auto stage_c2 = [&](const uint64_t* gsrc) {
     for (int k = threadIdx.x * 2; k < n; k += blockDim.x * 2) cp_async16(c2s + k, gsrc + k);
     cp_async_commit();
@@ -242,6 +262,8 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN>::threads, 1)
   const int64_t pw = (int64_t)nl * n;
   const int vt = threadIdx.x;
   const int k0 = vt << 4;
+  const uint32_t qneg = neg_qinv32((uint32_t)Q);
+  (void)qneg;
   for (int item = c.r0; item < c.r1; ++item) {
     W acc0[16], acc1[16];
 #pragma unroll
@@ -263,28 +285,69 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN>::threads, 1)
       for (int d = 0; d < K.digits[i]; ++d) {
         const int row = K.rows0[i] + d;
         const int sh = 15 * d;
+        bool c2_staged = false;
+        if constexpr (KS) {
+          // this digit's key row (b then a) -> shared memory, behind the NTT below
+          const uint4* kb = reinterpret_cast<const uint4*>(kmont + (int64_t)row * 2 * K.key_poly_words + (int64_t)j * n);
+          const uint4* ka = reinterpret_cast<const uint4*>(kmont + ((int64_t)row * 2 + 1) * K.key_poly_words + (int64_t)j * n);
+          for (int ch = threadIdx.x; ch < n / 4; ch += blockDim.x) {
+            cp_async16(ks + key_slot(ch), kb + ch);
+            cp_async16(ks + n / 4 + key_slot(ch), ka + ch);
+          }
+          cp_async_commit();
+        }
         const int64_t kof = (int64_t)row * 2 * K.key_poly_words + (int64_t)j * n + k0;
-        prefetch_l1(kpack + kof);  // this thread's key lines for the MAC below
-        prefetch_l1(kpack + kof + K.key_poly_words);
-        if constexpr (sizeof(W) == 8) {
-          prefetch_l1(kval + kof);
-          prefetch_l1(kval + kof + K.key_poly_words);
+        if (kPrefetchKeys) {
+          prefetch_l1(kpack + kof);  // this thread's key lines for the MAC below
+          prefetch_l1(kpack + kof + K.key_poly_words);
+          if constexpr (sizeof(W) == 8) {
+            prefetch_l1(kval + kof);
+            prefetch_l1(kval + kof + K.key_poly_words);
+          }
         }
         // digit (c2_i >> 15d) & 0x7FFF (ckks_backend.hpp:520-521), extracted inside the first NTT pass
         if constexpr (C2S) {
           lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return (W)((c2s[k] >> sh) & 0x7FFF); }, c.tw, q, q2);
           if (d == K.digits[i] - 1) {  // residue consumed: prefetch the next one behind this digit's NTT
-            if (i + 1 < nl) stage_c2(src + n);
-            else if (item + 1 < c.r1) stage_c2(c2 + (int64_t)(item + 1) * pw);
+            if (i + 1 < nl) { stage_c2(src + n); c2_staged = true; }
+            else if (item + 1 < c.r1) { stage_c2(c2 + (int64_t)(item + 1) * pw); c2_staged = true; }
           }
         } else {
           lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return (W)((__ldg(src + k) >> sh) & 0x7FFF); }, c.tw, q, q2);
         }
-        lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2);
+        if constexpr (KS) {
+          // key row landed (the c2 prefetch committed after it may still be in flight)
+          lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2, [&] {
+            if (c2_staged) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+            else cp_async_wait_all();
+          });
+        } else {
+          lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2);
+        }
+        (void)c2_staged;
         W x[16];
         lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, x);
         const int64_t koff = (int64_t)row * 2 * K.key_poly_words + (int64_t)j * n + k0;
-        if constexpr (sizeof(W) == 4) {
+        if constexpr (KS) {
+          // Montgomery MAC: U = (x km + m q) / 2^32 with m = -(x km) q^{-1} mod 2^32; x < 4q < 2^32,
+          // km < q, so U < 2q and U = x w mod q
+          const uint32_t q32 = (uint32_t)Q, q232 = q32 + q32;
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const uint4 vb = ks[key_slot(4 * vt + h)], va = ks[n / 4 + key_slot(4 * vt + h)];
+            const uint32_t kb_[4] = {vb.x, vb.y, vb.z, vb.w}, ka_[4] = {va.x, va.y, va.z, va.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const uint32_t xv = (uint32_t)x[4 * h + e];
+              const uint64_t tb = (uint64_t)xv * kb_[e], ta = (uint64_t)xv * ka_[e];
+              const uint32_t ub = (uint32_t)((tb + (uint64_t)((uint32_t)tb * qneg) * q32) >> 32);
+              const uint32_t ua = (uint32_t)((ta + (uint64_t)((uint32_t)ta * qneg) * q32) >> 32);
+              const uint32_t s0 = (uint32_t)acc0[4 * h + e] + ub, s1 = (uint32_t)acc1[4 * h + e] + ua;
+              acc0[4 * h + e] = (W)min(s0, s0 - q232);
+              acc1[4 * h + e] = (W)min(s1, s1 - q232);
+            }
+          }
+        } else if constexpr (sizeof(W) == 4) {
           const ulonglong2* kb2 = reinterpret_cast<const ulonglong2*>(kpack + koff);
           const ulonglong2* ka2 = reinterpret_cast<const ulonglong2*>(kpack + koff + K.key_poly_words);
           const uint32_t q32 = (uint32_t)Q, q232 = q32 + q32;
@@ -597,7 +660,7 @@ void ntt(const Context& c, uint64_t* base, int64_t rows_per_limb, int nl, int li
       grid_for<W_, LOGN>(LL, rows_per_limb, grid, G);
       const void* fn = inverse ? (const void*)k_ntt_t<W_, LOGN, true> : (const void*)k_ntt_t<W_, LOGN, false>;
       set_smem_attr(fn, Cf::smem);
-      c.kt_begin("k_ntt_t", s, 2.0 * rows_per_limb * LL.count * nw, (double)rows_per_limb * LL.count * bfly(c));
+      c.kt_begin(sizeof(W_) == 4 ? "k_ntt_t/u32" : "k_ntt_t/u64", s, 2.0 * rows_per_limb * LL.count * nw, (double)rows_per_limb * LL.count * bfly(c));
       if (inverse) k_ntt_t<W_, LOGN, true><<<grid, Cf::threads, Cf::smem, s>>>(base, nl, rows_per_limb, G, LL, c.kp());
       else k_ntt_t<W_, LOGN, false><<<grid, Cf::threads, Cf::smem, s>>>(base, nl, rows_per_limb, G, LL, c.kp());
       c.kt_end(s);
@@ -621,7 +684,7 @@ void lift_ntt(const Context& c, const int64_t* src, uint64_t* out, int64_t items
       int G;
       grid_for<W_, LOGN>(LL, items, grid, G);
       set_smem_attr((const void*)k_lift_ntt_t<W_, LOGN>, Cf::smem);
-      c.kt_begin("k_lift_ntt_t", s, (double)items * LL.count * 2 * nw, (double)items * LL.count * bfly(c));
+      c.kt_begin(sizeof(W_) == 4 ? "k_lift_ntt_t/u32" : "k_lift_ntt_t/u64", s, (double)items * LL.count * 2 * nw, (double)items * LL.count * bfly(c));
       k_lift_ntt_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(src, out, nl, items, G, LL, c.kp());
       c.kt_end(s);
       HG_CUDA(cudaGetLastError());
@@ -652,7 +715,7 @@ void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys,
       int G;
       grid_for<W_, LOGN>(LL, polys, grid, G);
       set_smem_attr((const void*)k_rescale_top_t<W_, LOGN>, Cf::smem);
-      c.kt_begin("k_rescale_top_t", s, 2.0 * polys * nw, (double)polys * bfly(c));
+      c.kt_begin(sizeof(W_) == 4 ? "k_rescale_top_t/u32" : "k_rescale_top_t/u64", s, 2.0 * polys * nw, (double)polys * bfly(c));
       k_rescale_top_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(in, cen, nl, polys, G, LL, c.kp());
       c.kt_end(s);
       HG_CUDA(cudaGetLastError());
@@ -667,7 +730,7 @@ void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys,
       int G;
       grid_for<W_, LOGN>(LL, polys, grid, G);
       set_smem_attr((const void*)k_rescale_rest_t<W_, LOGN>, Cf::smem);
-      c.kt_begin("k_rescale_rest_t", s, (double)polys * LL.count * 3 * nw,
+      c.kt_begin(sizeof(W_) == 4 ? "k_rescale_rest_t/u32" : "k_rescale_rest_t/u64", s, (double)polys * LL.count * 3 * nw,
                  (double)polys * LL.count * (bfly(c) + c.n()));
       k_rescale_rest_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(in, cen, out, nl, polys, G, LL, R, c.kp());
       c.kt_end(s);
@@ -714,17 +777,19 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
         const void* fn = given_d ? (const void*)k_relin_t<W_, LOGN, true> : (const void*)k_relin_t<W_, LOGN, false>;
         set_smem_attr(fn, Cf::smem);
         const double frac = (double)LL.count / nl;
-        c.kt_begin("k_relin_t", s, frac * (items * pw8 * 7 + (double)sd * 2 * pw8),
+        c.kt_begin(sizeof(W_) == 4 ? "k_relin_t/u32" : "k_relin_t/u64", s, frac * (items * pw8 * 7 + (double)sd * 2 * pw8),
                    (double)items * LL.count * (sd * (bfly(c) + 2.0 * c.n()) + 3.0 * c.n()));
         if (given_d)
           k_relin_t<W_, LOGN, true><<<grid, threads, Cf::smem, s>>>(a, b, a_stride, b_stride, c2,
                                                                     keys.relin.as<uint64_t>(),
-                                                                    keys.relin_pack.as<uint64_t>(), out, nl, items, G,
+                                                                    keys.relin_pack.as<uint64_t>(),
+                                                                    keys.relin_mont.as<uint32_t>(), out, nl, items, G,
                                                                     K, LL, c.kp());
         else
           k_relin_t<W_, LOGN, false><<<grid, threads, Cf::smem, s>>>(a, b, a_stride, b_stride, c2,
                                                                      keys.relin.as<uint64_t>(),
-                                                                     keys.relin_pack.as<uint64_t>(), out, nl, items,
+                                                                     keys.relin_pack.as<uint64_t>(),
+                                                                     keys.relin_mont.as<uint32_t>(), out, nl, items,
                                                                      G, K, LL, c.kp());
         c.kt_end(s);
         HG_CUDA(cudaGetLastError());
@@ -749,7 +814,7 @@ void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_
       int G;
       grid_for<W_, LOGN>(LL, items, grid, G);
       set_smem_attr((const void*)k_relin_c2_t<W_, LOGN>, Cf::smem);
-      c.kt_begin("k_relin_c2_t", s, (double)items * LL.count * 3 * nw, (double)items * LL.count * (bfly(c) + c.n()));
+      c.kt_begin(sizeof(W_) == 4 ? "k_relin_c2_t/u32" : "k_relin_c2_t/u64", s, (double)items * LL.count * 3 * nw, (double)items * LL.count * (bfly(c) + c.n()));
       k_relin_c2_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(a, b, a_stride, b_stride, a1_off, b1_off, c2, nl,
                                                                  items, G, LL, c.kp());
       c.kt_end(s);

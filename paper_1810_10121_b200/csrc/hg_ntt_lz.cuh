@@ -102,16 +102,25 @@ __device__ __forceinline__ void fwd_first_from(W* s, Get get, const TWT<W>* tw, 
   }
   __syncthreads();
 }
-// the passes between fwd_first_from and fwd_last; ends with a barrier when it runs any
-template <typename W, int LOGN>
-__device__ __forceinline__ void fwd_middle(W* s, const TWT<W>* tw, W q, W q2) {
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+// the passes between fwd_first_from and fwd_last; ends with a barrier, and runs
+// `pre()` (e.g. a cp.async wait) right before that last barrier
+template <typename W, int LOGN, typename Pre = NoHook>
+__device__ __forceinline__ void fwd_middle(W* s, const TWT<W>* tw, W q, W q2, Pre pre = Pre{}) {
   constexpr int K0 = (LOGN & 3) ? (LOGN & 3) : 4;
   if constexpr (K0 + 4 < LOGN) {
     fwd_pass<W, LOGN, 4, K0>(s, tw, q, q2);
+    if constexpr (!(K0 + 8 < LOGN)) pre();
+    __syncthreads();
+  } else {
+    pre();
     __syncthreads();
   }
   if constexpr (K0 + 8 < LOGN) {
     fwd_pass<W, LOGN, 4, K0 + 4>(s, tw, q, q2);
+    pre();
     __syncthreads();
   }
 }
