@@ -175,7 +175,7 @@ int hg_kernel_timing(hg_context* ctx, int on);
 int hg_kernel_stats_json(hg_context* ctx, char* buf, size_t cap);
 /* kernel launches issued by this context so far (counted at every launch site) */
 int64_t hg_kernel_launches(const hg_context* ctx);
-/* register-only Shoup modmul throughput on all SMs (32-bit words if wide == 0, else 64-bit) */
+/* register-only modmul throughput on all SMs: wide 0 = 32-bit Shoup, 1 = 64-bit Shoup, 2 = fp64 (q < 2^50) */
 int hg_bench_modmul(hg_context* ctx, int wide, double* modmul_per_s);
 
 #ifdef __cplusplus

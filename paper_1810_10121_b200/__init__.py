@@ -191,9 +191,10 @@ class Context:
     def kernel_launches(self) -> int:
         return int(lib().hg_kernel_launches(self._h))
 
-    def modmul_peak(self, wide: bool) -> float:
+    def modmul_peak(self, wide) -> float:
+        """modmul/s of a register-only microkernel: False/0 u32 Shoup, True/1 u64 Shoup, 2 fp64."""
         v = C.c_double()
-        _chk(lib().hg_bench_modmul(self._h, 1 if wide else 0, C.byref(v)))
+        _chk(lib().hg_bench_modmul(self._h, int(wide), C.byref(v)))
         return v.value
 
     def close(self):

@@ -353,7 +353,7 @@ int hg_kernel_stats_json(hg_context* ctx, char* buf, size_t cap) {
 int hg_bench_modmul(hg_context* ctx, int wide, double* modmul_per_s) {
   return guard([&] {
     need(ctx, "ctx");
-    *modmul_per_s = hg::k::modmul_peak(*ctx->c, wide != 0, ctx->stream());
+    *modmul_per_s = hg::k::modmul_peak(*ctx->c, wide, ctx->stream());
   });
 }
 

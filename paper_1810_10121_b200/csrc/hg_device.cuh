@@ -30,6 +30,11 @@ struct LimbInfo {
   const uint2* iwp32;
   uint32_t ninv32_s;     // floor(ninv 2^32 / q) for small primes
   uint32_t small;        // q < 2^30 (32-bit lazy word path)
+  uint32_t fp;           // 2^30 <= q < 2^50: fp64 lane (exact FMA-based modmul, hg_ntt.cuh Lz<double>)
+  double qd, qinvd;      // q and fl(1/q)
+  double ninvd;          // N^{-1} mod q
+  const double* fwpd;    // pass-ordered psi^brv / psi^-brv as doubles (fp64 lane)
+  const double* iwpd;
 };
 
 struct CtxParams {
@@ -91,6 +96,30 @@ __device__ __forceinline__ uint64_t reduce128(uint64_t z0, uint64_t z1, const Li
 
 __device__ __forceinline__ uint64_t mul_mod(uint64_t a, uint64_t b, const LimbInfo& L) {
   return reduce128(a * b, __umul64hi(a, b), L);
+}
+
+// Exact a*b mod q on the fp64 pipe, for q < 2^50 and integers |a| < 2^51, |b| < q
+// held in doubles.  a*b = h + l exactly (FMA residual); e ~ round(h/q) by the
+// 1.5*2^52 rounding constant; h - e q is an integer below 2^51 in magnitude, so the
+// FMA computes it exactly.  Result congruent to a*b, in (-2q, 2q).
+__device__ __forceinline__ double mulmod_f64(double a, double b, double q, double qinv) {
+  const double h = __dmul_rn(a, b);
+  const double l = __fma_rn(a, b, -h);
+  const double M = 6755399441055744.0;
+  const double e = __dadd_rn(__fma_rn(h, qinv, M), -M);
+  return __dadd_rn(__fma_rn(-e, q, h), l);
+}
+
+// fp64 lane: |a| < 2^51 -> a - q round(a/q), in [-q/2, q/2] (up to rounding of 1/q)
+__device__ __forceinline__ double reduce_f64(double a, double q, double qinv) {
+  const double M = 6755399441055744.0;
+  const double e = __dadd_rn(__fma_rn(a, qinv, M), -M);
+  return __fma_rn(-e, q, a);
+}
+// |a| < 2^51 -> canonical [0, q)
+__device__ __forceinline__ double canon_f64(double a, double q, double qinv) {
+  const double r = reduce_f64(a, q, qinv);
+  return r < 0.0 ? __dadd_rn(r, q) : r;
 }
 
 // 128-bit accumulator

@@ -239,7 +239,8 @@ Context::Context(const ContextParamsH& p, int device) : m_p(p), m_device(device)
 
   // tables: per limb fw (16N) | iw (16N) | fw32 (8N) | iw32 (8N)
   // per limb: fw (16N) | iw (16N) | fw32 (8N) | iw32 (8N) | fwp (16N) | iwp (16N) | fwp32 (8N) | iwp32 (8N)
-  const size_t per = 96 * static_cast<size_t>(n);
+  //           | fwpd (8N) | iwpd (8N)   (fp64 lane: pass-ordered twiddles as doubles)
+  const size_t per = 112 * static_cast<size_t>(n);
   m_tables.alloc(per * nl);
   std::vector<uint8_t> host(per * nl, 0);
   m_psi.resize(nl);
@@ -330,6 +331,12 @@ Context::Context(const ContextParamsH& p, int device) : m_p(p), m_device(device)
           for (int64_t gi = 0; gi < nbi; ++gi)
             for (int64_t ii = 0; ii < per_i; ++ii) put(iwp, iwp32, iw, iw32, h + ii * nbi + gi, h + gi * per_i + ii);
         }
+      auto* fwpd = reinterpret_cast<double*>(base + 96 * n);
+      auto* iwpd = reinterpret_cast<double*>(base + 104 * n);
+      for (int64_t e = 0; e < n; ++e) {
+        fwpd[e] = static_cast<double>(fwp[2 * e]);
+        iwpd[e] = static_cast<double>(iwp[2 * e]);
+      }
     }
     LimbInfo& L = m_kp.limb[i];
     L.q = q;
@@ -339,6 +346,10 @@ Context::Context(const ContextParamsH& p, int device) : m_p(p), m_device(device)
     L.ninv_s = M.shoup(L.ninv);
     L.ninv32_s = static_cast<uint32_t>(L.ninv_s >> 32);
     L.small = small ? 1u : 0u;
+    L.fp = (!small && q < (uint64_t(1) << 50)) ? 1u : 0u;
+    L.qd = static_cast<double>(q);
+    L.qinvd = 1.0 / static_cast<double>(q);
+    L.ninvd = static_cast<double>(L.ninv);
     uint8_t* dbase = m_tables.as<uint8_t>() + per * i;
     L.fw = reinterpret_cast<const ulonglong2*>(dbase);
     L.iw = reinterpret_cast<const ulonglong2*>(dbase + 16 * n);
@@ -348,6 +359,8 @@ Context::Context(const ContextParamsH& p, int device) : m_p(p), m_device(device)
     L.iwp = reinterpret_cast<const ulonglong2*>(dbase + 64 * n);
     L.fwp32 = small ? reinterpret_cast<const uint2*>(dbase + 80 * n) : nullptr;
     L.iwp32 = small ? reinterpret_cast<const uint2*>(dbase + 88 * n) : nullptr;
+    L.fwpd = reinterpret_cast<const double*>(dbase + 96 * n);
+    L.iwpd = reinterpret_cast<const double*>(dbase + 104 * n);
   }
   HG_CUDA(cudaMemcpy(m_tables.p, host.data(), host.size(), cudaMemcpyHostToDevice));
   for (int t = 0; t < nl; ++t)

@@ -322,7 +322,7 @@ void sample_encryption_gpu(const Context& c, const uint64_t* seeds_host, int64_t
 void encode_fft(const Context& c, const double* values, int64_t cols, int64_t count, int64_t col_stride,
                 int64_t elem_stride, double scale, int64_t* out, int* flag, cudaStream_t s);
 // register-only Shoup modmul throughput on every SM (modmul/s); wide = 64-bit words
-double modmul_peak(const Context& c, bool wide, cudaStream_t s);
+double modmul_peak(const Context& c, int mode, cudaStream_t s);  // 0: u32 Shoup, 1: u64 Shoup, 2: fp64
 void keygen_b(const Context& c, const uint64_t* a, const uint64_t* sk, const uint64_t* e, uint64_t* out, int nl,
               int special, uint64_t f, cudaStream_t s);
 }  // namespace k

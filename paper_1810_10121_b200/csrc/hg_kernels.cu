@@ -9,6 +9,7 @@
 //   weighted_sum (fused Dot/Conv)  ckks/ckks_backend.hpp:381-411, runtime.hpp:532-569
 //   fresh_encryption / decrypt     ckks/ckks_backend.hpp:470-490, 238-249
 #include <cuda_runtime.h>
+#include <cmath>
 
 #include <algorithm>
 #include <cstdio>
@@ -976,10 +977,24 @@ __global__ void __launch_bounds__(256) k_modmul_bench64(uint64_t* out, uint64_t 
   for (int r = 0; r < 8; ++r) acc ^= x[r];
   if (acc == ~0ull) out[blockIdx.x] = acc;
 }
+__global__ void __launch_bounds__(256) k_modmul_bench_f64(double* out, double q, double qinv, double w, int iters) {
+  double x[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) x[r] = (double)((threadIdx.x * 8 + r + blockIdx.x) % 1000003);
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) x[r] = mulmod_f64(x[r], w, q, qinv);
+  }
+  double acc = 0;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) acc += x[r];
+  if (acc == 12345.0) out[blockIdx.x] = acc;
+}
 }  // namespace
 
 namespace k {
-double modmul_peak(const Context& c, bool wide, cudaStream_t s) {
+double modmul_peak(const Context& c, int mode, cudaStream_t s) {
+  const bool wide = mode == 1;
   int sms = 0;
   HG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device()));
   const int blocks = sms * 8, threads = 256, iters = 4096;
@@ -990,7 +1005,10 @@ double modmul_peak(const Context& c, bool wide, cudaStream_t s) {
   float best = 1e30f;
   for (int rep = 0; rep < 4; ++rep) {
     HG_CUDA(cudaEventRecord(a, s));
-    if (wide) {
+    if (mode == 2) {
+      const double q = 1125899904679937.0;  // a 50-bit NTT prime
+      k_modmul_bench_f64<<<blocks, threads, 0, s>>>(out.as<double>(), q, 1.0 / q, std::floor(q / 3), iters);
+    } else if (wide) {
       const uint64_t q = c.primes()[0];
       const HMod& M = c.mod(0);
       const uint64_t w = q / 3 + 1;

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "hg_device.cuh"
@@ -74,7 +75,7 @@ __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_block
   extern __shared__ __align__(16) uint64_t smem[];
   Cta<W, LOGN> c(smem, LL, rows, G, P, INV);
   constexpr int n = 1 << LOGN;
-  const W q = (W)c.L->q, q2 = q + q;
+  const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
   for (int r = c.r0; r < c.r1; ++r) {
     uint64_t* g = base + ((int64_t)r * nl + c.limb) * n;
     lz::load<W, LOGN>(c.s, g);
@@ -92,7 +93,7 @@ HG_KERNEL k_lift_ntt_t(const int64_t* __restrict__ src, uint64_t* __restrict__ o
   extern __shared__ __align__(16) uint64_t smem[];
   Cta<W, LOGN> c(smem, LL, items, G, P, false);
   constexpr int n = 1 << LOGN;
-  const W q = (W)c.L->q, q2 = q + q;
+  const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
   for (int r = c.r0; r < c.r1; ++r) {
     const int64_t* g = src + (int64_t)r * n;
     for (int i = threadIdx.x; i < n; i += blockDim.x) c.s[lz::padw<W>(i)] = (W)lift_signed(g[i], c.L->q);
@@ -109,7 +110,7 @@ HG_KERNEL k_rescale_top_t(const uint64_t* __restrict__ in, int64_t* __restrict__
   extern __shared__ __align__(16) uint64_t smem[];
   Cta<W, LOGN> c(smem, LL, polys, G, P, true);
   constexpr int n = 1 << LOGN;
-  const W q = (W)c.L->q, q2 = q + q;
+  const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
   const uint64_t half = c.L->q / 2;
   for (int r = c.r0; r < c.r1; ++r) {
     lz::load<W, LOGN>(c.s, in + ((int64_t)r * nl + c.limb) * n);
@@ -137,7 +138,7 @@ HG_KERNEL k_rescale_rest_t(const uint64_t* __restrict__ in, const int64_t* __res
   Cta<W, LOGN> c(smem, LL, polys, G, P, false);
   constexpr int n = 1 << LOGN;
   const int t = nl - 1, j = c.limb;
-  const W q = (W)c.L->q, q2 = q + q;
+  const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
   const uint64_t Q = c.L->q, inv = R.inv[j], inv_s = R.inv_s[j];
   for (int r = c.r0; r < c.r1; ++r) {
     const int64_t* cv = cen + (int64_t)r * n;
@@ -170,7 +171,7 @@ HG_KERNEL k_relin_c2_t(const uint64_t* __restrict__ a, const uint64_t* __restric
   extern __shared__ __align__(16) uint64_t smem[];
   Cta<W, LOGN> c(smem, LL, items, G, P, true);
   constexpr int n = 1 << LOGN;
-  const W q = (W)c.L->q, q2 = q + q;
+  const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
   for (int r = c.r0; r < c.r1; ++r) {
     const uint64_t* x1 = a + r * a_stride + a1_off + (int64_t)c.limb * n;
     const uint64_t* y1 = b + r * b_stride + b1_off + (int64_t)c.limb * n;
@@ -257,7 +258,7 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN>::threads, 1)
   (void)c2s;
   (void)stage_c2;
   const int j = c.limb;
-  const W q = (W)c.L->q, q2 = q + q;
+  const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
   const uint64_t Q = c.L->q;
   const int64_t pw = (int64_t)nl * n;
   const int vt = threadIdx.x;
@@ -307,13 +308,13 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN>::threads, 1)
         }
         // digit (c2_i >> 15d) & 0x7FFF (ckks_backend.hpp:520-521), extracted inside the first NTT pass
         if constexpr (C2S) {
-          lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return (W)((c2s[k] >> sh) & 0x7FFF); }, c.tw, q, q2);
+          lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return (W)(uint32_t)((c2s[k] >> sh) & 0x7FFF); }, c.tw, q, q2);
           if (d == K.digits[i] - 1) {  // residue consumed: prefetch the next one behind this digit's NTT
             if (i + 1 < nl) { stage_c2(src + n); c2_staged = true; }
             else if (item + 1 < c.r1) { stage_c2(c2 + (int64_t)(item + 1) * pw); c2_staged = true; }
           }
         } else {
-          lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return (W)((__ldg(src + k) >> sh) & 0x7FFF); }, c.tw, q, q2);
+          lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return (W)(uint32_t)((__ldg(src + k) >> sh) & 0x7FFF); }, c.tw, q, q2);
         }
         if constexpr (KS) {
           // key row landed (the c2 prefetch committed after it may still be in flight)
@@ -345,6 +346,28 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN>::threads, 1)
               const uint32_t s0 = (uint32_t)acc0[4 * h + e] + ub, s1 = (uint32_t)acc1[4 * h + e] + ua;
               acc0[4 * h + e] = (W)min(s0, s0 - q232);
               acc1[4 * h + e] = (W)min(s1, s1 - q232);
+            }
+          }
+        } else if constexpr (std::is_floating_point_v<W>) {
+          // fp64 lane: exact FMA modmul of the lazy evaluation by the key word, reduced sum
+          const ulonglong2* kb2 = reinterpret_cast<const ulonglong2*>(kval + koff);
+          const ulonglong2* ka2 = reinterpret_cast<const ulonglong2*>(kval + koff + K.key_poly_words);
+          double* od0 = reinterpret_cast<double*>(o0);
+          double* od1 = reinterpret_cast<double*>(o1);
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            const ulonglong2 vb = __ldg(kb2 + h), va = __ldg(ka2 + h);
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const double t0 = mulmod_f64(x[2 * h + e], (double)(e ? vb.y : vb.x), q, q2);
+              const double t1 = mulmod_f64(x[2 * h + e], (double)(e ? va.y : va.x), q, q2);
+              if constexpr (AG) {
+                od0[2 * h + e] = reduce_f64(__dadd_rn(od0[2 * h + e], t0), q, q2);
+                od1[2 * h + e] = reduce_f64(__dadd_rn(od1[2 * h + e], t1), q, q2);
+              } else {
+                acc0[2 * h + e] = reduce_f64(__dadd_rn(acc0[2 * h + e], t0), q, q2);
+                acc1[2 * h + e] = reduce_f64(__dadd_rn(acc1[2 * h + e], t1), q, q2);
+              }
             }
           }
         } else if constexpr (sizeof(W) == 4) {
@@ -397,7 +420,12 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN>::threads, 1)
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       uint64_t r0, r1;
-      if constexpr (AG) {
+      if constexpr (std::is_floating_point_v<W>) {
+        const double a0 = AG ? reinterpret_cast<const double*>(o0)[r] : (double)acc0[r];
+        const double a1 = AG ? reinterpret_cast<const double*>(o1)[r] : (double)acc1[r];
+        r0 = (uint64_t)canon_f64(a0, q, q2);
+        r1 = (uint64_t)canon_f64(a1, q, q2);
+      } else if constexpr (AG) {
         r0 = o0[r];
         r1 = o1[r];
       } else {
@@ -594,16 +622,28 @@ __global__ void __launch_bounds__(kGT) k_gemm_lz(const uint64_t* __restrict__ x,
 namespace k2 {
 
 struct Classes {
-  LimbList small{}, wide{};
+  LimbList small{}, wide{}, fp{};
 };
 
-static Classes classify(const Context& c, int limb_begin, int limb_end) {
+// small: 32-bit lanes; wide: 64-bit integer lanes.  With fp64 = true, limbs with
+// 2^30 <= q < 2^50 go to the fp64 lane (`fp`) instead of `wide`.
+static Classes classify(const Context& c, int limb_begin, int limb_end, bool fp64 = false) {
   Classes cl;
   for (int j = limb_begin; j < limb_end; ++j) {
     if (c.kp().limb[j].small) cl.small.limb[cl.small.count++] = j;
+    else if (fp64 && c.kp().limb[j].fp) cl.fp.limb[cl.fp.count++] = j;
     else cl.wide.limb[cl.wide.count++] = j;
   }
   return cl;
+}
+
+// HG_FP64_LANE=0 keeps every wide limb on 64-bit integer arithmetic (same results)
+static bool fp64_lane() {
+  static const bool on = [] {
+    const char* e = std::getenv("HG_FP64_LANE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 static void set_smem_attr(const void* fn, size_t bytes) {
@@ -648,7 +688,7 @@ static void grid_for(const LimbList& LL, int64_t rows, unsigned& grid, int& G) {
 void ntt(const Context& c, uint64_t* base, int64_t rows_per_limb, int nl, int limb_begin, int limb_end, bool inverse,
          cudaStream_t s) {
   if (rows_per_limb <= 0) return;
-  const Classes cl = classify(c, limb_begin, limb_end);
+  const Classes cl = classify(c, limb_begin, limb_end, fp64_lane());
   const double nw = (double)c.n() * 8;
   auto run = [&](const LimbList& LL, auto wtag) {
     using W = decltype(wtag);
@@ -660,7 +700,7 @@ void ntt(const Context& c, uint64_t* base, int64_t rows_per_limb, int nl, int li
       grid_for<W_, LOGN>(LL, rows_per_limb, grid, G);
       const void* fn = inverse ? (const void*)k_ntt_t<W_, LOGN, true> : (const void*)k_ntt_t<W_, LOGN, false>;
       set_smem_attr(fn, Cf::smem);
-      c.kt_begin(sizeof(W_) == 4 ? "k_ntt_t/u32" : "k_ntt_t/u64", s, 2.0 * rows_per_limb * LL.count * nw, (double)rows_per_limb * LL.count * bfly(c));
+      c.kt_begin(std::is_floating_point_v<W_> ? "k_ntt_t/f64" : sizeof(W_) == 4 ? "k_ntt_t/u32" : "k_ntt_t/u64", s, 2.0 * rows_per_limb * LL.count * nw, (double)rows_per_limb * LL.count * bfly(c));
       if (inverse) k_ntt_t<W_, LOGN, true><<<grid, Cf::threads, Cf::smem, s>>>(base, nl, rows_per_limb, G, LL, c.kp());
       else k_ntt_t<W_, LOGN, false><<<grid, Cf::threads, Cf::smem, s>>>(base, nl, rows_per_limb, G, LL, c.kp());
       c.kt_end(s);
@@ -668,12 +708,13 @@ void ntt(const Context& c, uint64_t* base, int64_t rows_per_limb, int nl, int li
     });
   };
   run(cl.small, uint32_t{});
+  run(cl.fp, double{});
   run(cl.wide, uint64_t{});
 }
 
 void lift_ntt(const Context& c, const int64_t* src, uint64_t* out, int64_t items, int nl, cudaStream_t s) {
   if (items <= 0) return;
-  const Classes cl = classify(c, 0, nl);
+  const Classes cl = classify(c, 0, nl, fp64_lane());
   const double nw = (double)c.n() * 8;
   auto run = [&](const LimbList& LL, auto wtag) {
     using W = decltype(wtag);
@@ -684,13 +725,14 @@ void lift_ntt(const Context& c, const int64_t* src, uint64_t* out, int64_t items
       int G;
       grid_for<W_, LOGN>(LL, items, grid, G);
       set_smem_attr((const void*)k_lift_ntt_t<W_, LOGN>, Cf::smem);
-      c.kt_begin(sizeof(W_) == 4 ? "k_lift_ntt_t/u32" : "k_lift_ntt_t/u64", s, (double)items * LL.count * 2 * nw, (double)items * LL.count * bfly(c));
+      c.kt_begin(std::is_floating_point_v<W_> ? "k_lift_ntt_t/f64" : sizeof(W_) == 4 ? "k_lift_ntt_t/u32" : "k_lift_ntt_t/u64", s, (double)items * LL.count * 2 * nw, (double)items * LL.count * bfly(c));
       k_lift_ntt_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(src, out, nl, items, G, LL, c.kp());
       c.kt_end(s);
       HG_CUDA(cudaGetLastError());
     });
   };
   run(cl.small, uint32_t{});
+  run(cl.fp, double{});
   run(cl.wide, uint64_t{});
 }
 
@@ -705,7 +747,7 @@ void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys,
     R.inv[j] = c.inv_q(t, j);
     R.inv_s[j] = c.inv_q_shoup(t, j);
   }
-  const Classes top = classify(c, t, t + 1), rest = classify(c, 0, t);
+  const Classes top = classify(c, t, t + 1, fp64_lane()), rest = classify(c, 0, t, fp64_lane());
   auto run_top = [&](const LimbList& LL, auto wtag) {
     using W = decltype(wtag);
     if (LL.count == 0) return;
@@ -715,7 +757,7 @@ void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys,
       int G;
       grid_for<W_, LOGN>(LL, polys, grid, G);
       set_smem_attr((const void*)k_rescale_top_t<W_, LOGN>, Cf::smem);
-      c.kt_begin(sizeof(W_) == 4 ? "k_rescale_top_t/u32" : "k_rescale_top_t/u64", s, 2.0 * polys * nw, (double)polys * bfly(c));
+      c.kt_begin(std::is_floating_point_v<W_> ? "k_rescale_top_t/f64" : sizeof(W_) == 4 ? "k_rescale_top_t/u32" : "k_rescale_top_t/u64", s, 2.0 * polys * nw, (double)polys * bfly(c));
       k_rescale_top_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(in, cen, nl, polys, G, LL, c.kp());
       c.kt_end(s);
       HG_CUDA(cudaGetLastError());
@@ -730,7 +772,7 @@ void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys,
       int G;
       grid_for<W_, LOGN>(LL, polys, grid, G);
       set_smem_attr((const void*)k_rescale_rest_t<W_, LOGN>, Cf::smem);
-      c.kt_begin(sizeof(W_) == 4 ? "k_rescale_rest_t/u32" : "k_rescale_rest_t/u64", s, (double)polys * LL.count * 3 * nw,
+      c.kt_begin(std::is_floating_point_v<W_> ? "k_rescale_rest_t/f64" : sizeof(W_) == 4 ? "k_rescale_rest_t/u32" : "k_rescale_rest_t/u64", s, (double)polys * LL.count * 3 * nw,
                  (double)polys * LL.count * (bfly(c) + c.n()));
       k_rescale_rest_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(in, cen, out, nl, polys, G, LL, R, c.kp());
       c.kt_end(s);
@@ -738,8 +780,10 @@ void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys,
     });
   };
   run_top(top.small, uint32_t{});
+  run_top(top.fp, double{});
   run_top(top.wide, uint64_t{});
   run_rest(rest.small, uint32_t{});
+  run_rest(rest.fp, double{});
   run_rest(rest.wide, uint64_t{});
 }
 
@@ -760,7 +804,7 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
   check(relin_supported(c), HG_EINTERNAL, "key switch: ring degree outside 2^10..2^14");
   if (items <= 0) return;
   const RelinC K = relin_consts(c, nl);
-  const Classes cl = classify(c, 0, nl);
+  const Classes cl = classify(c, 0, nl, fp64_lane());
   int sd = 0;
   for (int i = 0; i < nl; ++i) sd += c.digits(i);
   const double pw8 = (double)nl * c.n() * 8;
@@ -777,7 +821,7 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
         const void* fn = given_d ? (const void*)k_relin_t<W_, LOGN, true> : (const void*)k_relin_t<W_, LOGN, false>;
         set_smem_attr(fn, Cf::smem);
         const double frac = (double)LL.count / nl;
-        c.kt_begin(sizeof(W_) == 4 ? "k_relin_t/u32" : "k_relin_t/u64", s, frac * (items * pw8 * 7 + (double)sd * 2 * pw8),
+        c.kt_begin(std::is_floating_point_v<W_> ? "k_relin_t/f64" : sizeof(W_) == 4 ? "k_relin_t/u32" : "k_relin_t/u64", s, frac * (items * pw8 * 7 + (double)sd * 2 * pw8),
                    (double)items * LL.count * (sd * (bfly(c) + 2.0 * c.n()) + 3.0 * c.n()));
         if (given_d)
           k_relin_t<W_, LOGN, true><<<grid, threads, Cf::smem, s>>>(a, b, a_stride, b_stride, c2,
@@ -797,13 +841,14 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
     });
   };
   run(cl.small, uint32_t{});
+  run(cl.fp, double{});
   run(cl.wide, uint64_t{});
 }
 
 void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_stride, int64_t b_stride,
               int64_t a1_off, int64_t b1_off, uint64_t* c2, int64_t items, int nl, cudaStream_t s) {
   if (items <= 0) return;
-  const Classes cl = classify(c, 0, nl);
+  const Classes cl = classify(c, 0, nl, fp64_lane());
   const double nw = (double)c.n() * 8;
   auto run = [&](const LimbList& LL, auto wtag) {
     using W = decltype(wtag);
@@ -814,7 +859,7 @@ void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_
       int G;
       grid_for<W_, LOGN>(LL, items, grid, G);
       set_smem_attr((const void*)k_relin_c2_t<W_, LOGN>, Cf::smem);
-      c.kt_begin(sizeof(W_) == 4 ? "k_relin_c2_t/u32" : "k_relin_c2_t/u64", s, (double)items * LL.count * 3 * nw, (double)items * LL.count * (bfly(c) + c.n()));
+      c.kt_begin(std::is_floating_point_v<W_> ? "k_relin_c2_t/f64" : sizeof(W_) == 4 ? "k_relin_c2_t/u32" : "k_relin_c2_t/u64", s, (double)items * LL.count * 3 * nw, (double)items * LL.count * (bfly(c) + c.n()));
       k_relin_c2_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(a, b, a_stride, b_stride, a1_off, b1_off, c2, nl,
                                                                  items, G, LL, c.kp());
       c.kt_end(s);
@@ -822,6 +867,7 @@ void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_
     });
   };
   run(cl.small, uint32_t{});
+  run(cl.fp, double{});
   run(cl.wide, uint64_t{});
 }
 

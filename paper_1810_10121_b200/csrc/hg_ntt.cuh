@@ -13,6 +13,7 @@
 // swizzled within 32-word chunks so the small-stride passes stay free of bank
 // conflicts.
 #pragma once
+#include <type_traits>
 #include "hg_device.cuh"
 
 namespace hg {
@@ -232,6 +233,18 @@ struct Lz<uint64_t> {
   static __device__ __forceinline__ TW ninv(const LimbInfo& L) { return make_ulonglong2(L.ninv, L.ninv_s); }
 };
 
+// fp64 lane (2^30 <= q < 2^50): residues are integers held in doubles, signed and
+// lazily bounded (|x| < 1.7q < 2^51, see mulmod_f64); the slot that carries 2q in
+// the integer lanes carries fl(1/q) here.  Each butterfly reduces its additive
+// input and multiplies exactly with an FMA residual; outputs are canonicalised once.
+template <>
+struct Lz<double> {
+  using TW = double;
+  static __device__ __forceinline__ const TW* fwd_table(const LimbInfo& L) { return L.fwpd; }
+  static __device__ __forceinline__ const TW* inv_table(const LimbInfo& L) { return L.iwpd; }
+  static __device__ __forceinline__ TW ninv(const LimbInfo& L) { return L.ninvd; }
+};
+
 // a >= m ? a - m : a  (a < 2m).  32-bit: one fused add+min (VIADDMNMX): a - m wraps above a when a < m
 template <typename W>
 __device__ __forceinline__ W csub(W a, W m) {
@@ -241,22 +254,36 @@ __device__ __forceinline__ W csub(W a, W m) {
 
 template <typename W>
 __device__ __forceinline__ void ct_lz(W& a, W& b, typename Lz<W>::TW w, W q, W q2) {
-  const W x = csub(a, q2);
-  const W t = Lz<W>::mulw(b, w, q);
-  a = x + t;
-  b = x - t + q2;
+  if constexpr (std::is_floating_point_v<W>) {  // fp64 lane: q2 = 1/q
+    const double x = reduce_f64(a, q, q2);
+    const double t = mulmod_f64(b, w, q, q2);
+    a = __dadd_rn(x, t);
+    b = __dsub_rn(x, t);
+  } else {
+    const W x = csub(a, q2);
+    const W t = Lz<W>::mulw(b, w, q);
+    a = x + t;
+    b = x - t + q2;
+  }
 }
 template <typename W>
 __device__ __forceinline__ void gs_lz(W& a, W& b, typename Lz<W>::TW w, W q, W q2) {
-  const W s = csub<W>(a + b, q2);
-  const W d = a - b + q2;
-  a = s;
-  b = Lz<W>::mulw(d, w, q);
+  if constexpr (std::is_floating_point_v<W>) {
+    const double s = __dadd_rn(a, b), d = __dsub_rn(a, b);
+    a = reduce_f64(s, q, q2);
+    b = mulmod_f64(d, w, q, q2);
+  } else {
+    const W s = csub<W>(a + b, q2);
+    const W d = a - b + q2;
+    a = s;
+    b = Lz<W>::mulw(d, w, q);
+  }
 }
-// [0, 4q) -> [0, q)
+// [0, 4q) -> [0, q)   (fp64 lane: any |x| < 2^51 -> [0, q))
 template <typename W>
 __device__ __forceinline__ W canon4(W x, W q, W q2) {
-  return csub(csub(x, q2), q);
+  if constexpr (std::is_floating_point_v<W>) return canon_f64(x, q, q2);
+  else return csub(csub(x, q2), q);
 }
 
 // K forward stages (s0 .. s0+K-1) on one register group of block g (elements

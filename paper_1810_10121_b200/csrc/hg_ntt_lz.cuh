@@ -11,6 +11,8 @@
 // (inverse) and canonicalised once at the end: every output word equals the
 // reference's eagerly reduced transform.
 #pragma once
+#include <type_traits>
+
 #include "hg_ntt.cuh"
 
 namespace hg {
@@ -30,6 +32,13 @@ __host__ __device__ constexpr int smem_words() { return (1 << LOGN) + (1 << (LOG
 
 template <typename W>
 using TWT = typename Lz<W>::TW;
+
+// the second modulus constant the lazy passes take: 2q (integer lanes) or 1/q (fp64 lane)
+template <typename W>
+__device__ __forceinline__ W q2_of(const LimbInfo& L) {
+  if constexpr (std::is_integral_v<W>) return (W)(L.q + L.q);
+  else return L.qinvd;
+}
 
 // ---- forward (Cooley-Tukey), remainder-first passes ------------------------
 // stages S0 .. S0+K-1 of block g; pass-ordered twiddle at 2^S + (r >> (K-st)) 2^S0 + g
@@ -176,7 +185,10 @@ __device__ __forceinline__ void inv_pass(W* s, const TWT<W>* tw, TWT<W> ninv, W 
     if constexpr (LAST) {
 #pragma unroll
       for (int r = 0; r < R; ++r) {
-        x[r] = csub(Lz<W>::mulw(x[r], ninv, q), q);  // x N^{-1} in [0, 2q) -> canonical
+        if constexpr (sizeof(W) == 8 && !std::is_integral_v<W>)
+          x[r] = canon_f64(mulmod_f64(x[r], ninv, q, q2), q, q2);  // fp64 lane: q2 carries 1/q
+        else
+          x[r] = csub(Lz<W>::mulw(x[r], ninv, q), q);  // x N^{-1} in [0, 2q) -> canonical
       }
     }
 #pragma unroll
