@@ -567,6 +567,12 @@ struct hg_plan {
   // all-gathers a sharded tensor where a consumer needs every element
   int rank = 0, world = 1;
   std::shared_ptr<hg::Transport> transport;
+  // fresh encryptions inside a run skip the sampler's synchronous fix-up check; the
+  // flag counts land in pinned memory and are checked once the run has synchronised
+  // (a non-zero count re-runs the step with synchronous sampling)
+  int* sample_flags = nullptr;  // pinned host ints
+  int sample_flag_cap = 0, sample_flag_used = 0;
+  bool in_run = false, sync_sampling = false;
   std::map<std::string, hg::Val>* live = nullptr;  // the running step's values (in-process group transport)
 };
 
@@ -756,12 +762,16 @@ std::shared_ptr<DevArr> encode_columns(hg_plan* P, const std::vector<std::vector
 
 // Fresh encryptions of zero (or of per-item plaintexts) from per-item seeds
 // (ckks_backend.hpp:223-236, 470-490).
-void encrypt_items(hg_plan* P, const std::vector<uint64_t>& seeds, const uint64_t* pt, int level, uint64_t* out) {
+void encrypt_items(hg_plan* P, const std::vector<uint64_t>& seeds, const uint64_t* pt, int level, uint64_t* out,
+                   const uint64_t* seeds_dev = nullptr) {
   const Context& c = *P->ctx;
   const int64_t n = c.n(), m = static_cast<int64_t>(seeds.size());
   if (m == 0) return;
   DevArr d(static_cast<size_t>(m) * 3 * n * 8, S(P));
-  k::sample_encryption_gpu(c, seeds.data(), m, d.as<int64_t>(), S(P));
+  int* deferred = nullptr;
+  if (P->in_run && !P->sync_sampling && P->sample_flag_used < P->sample_flag_cap)
+    deferred = &P->sample_flags[P->sample_flag_used++];
+  k::sample_encryption_gpu(c, seeds.data(), m, d.as<int64_t>(), S(P), deferred, seeds_dev);
   k::encrypt(c, *P->keys, d.as<int64_t>(), pt, out, m, level + 1, S(P));
 }
 
@@ -1517,35 +1527,59 @@ Val kernel_pad(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_sh
   });
   // fill elements: encrypt_zero_at(ref_level, ref_scale, node_rng.fork(e).next()) (runtime.hpp:1834-1838)
   const auto& xt = x.ct;
-  Rng node_rng = P->rng.fork("node").fork(node.id);
-  std::vector<uint64_t> seeds;
-  std::vector<int32_t> gmap(static_cast<size_t>(m_out));
-  for (int64_t e = 0; e < m_out; ++e) {
-    if (map[e] >= 0) {
-      gmap[e] = static_cast<int32_t>(map[e]);
-    } else {
-      gmap[e] = static_cast<int32_t>(xt->count + static_cast<int64_t>(seeds.size()));
-      seeds.push_back(node_rng.fork(static_cast<uint64_t>(e)).next());
-    }
-  }
-  // concatenate [x ; fresh fills] then gather
-  auto cat = new_ct(P, xt->count + static_cast<int64_t>(seeds.size()), xt->level, xt->scale);
-  HG_CUDA(cudaMemcpyAsync(cat->p, xt->p, xt->words() * 8, cudaMemcpyDeviceToDevice, S(P)));
-  if (!seeds.empty()) {
-    std::shared_ptr<DevArr> pt;
-    if (fill != 0.0) {
+  const Context& c = *P->ctx;
+  NodeCache& C = P->cache[node.id];
+  if (C.level != xt->level || C.local_count != xt->count) {
+    // the copy map, fill positions, fill seeds (deterministic per plan) and fill plaintexts, once
+    Rng node_rng = P->rng.fork("node").fork(node.id);
+    std::vector<int32_t> both, fdst;
+    std::vector<uint64_t> seeds;
+    for (int64_t e = 0; e < m_out; ++e)
+      if (map[e] >= 0) both.push_back(static_cast<int32_t>(map[e]));
+    const size_t ncopy = both.size();
+    for (int64_t e = 0; e < m_out; ++e)
+      if (map[e] >= 0) both.push_back(static_cast<int32_t>(e));
+      else {
+        fdst.push_back(static_cast<int32_t>(e));
+        seeds.push_back(node_rng.fork(static_cast<uint64_t>(e)).next());
+      }
+    C.idx = std::make_shared<DevArr>(both.size() * 4 + 4, S(P));
+    C.oidx = std::make_shared<DevArr>(fdst.size() * 4 + 4, S(P));
+    C.w = std::make_shared<DevArr>(seeds.size() * 8 + 8, S(P));
+    HG_CUDA(cudaMemcpyAsync(C.idx->p, both.data(), both.size() * 4, cudaMemcpyHostToDevice, S(P)));
+    HG_CUDA(cudaMemcpyAsync(C.oidx->p, fdst.data(), fdst.size() * 4, cudaMemcpyHostToDevice, S(P)));
+    HG_CUDA(cudaMemcpyAsync(C.w->p, seeds.data(), seeds.size() * 8, cudaMemcpyHostToDevice, S(P)));
+    C.fill_pos.assign(seeds.begin(), seeds.end());  // host copy of the seeds (fix-up path)
+    C.groups = static_cast<int64_t>(ncopy);
+    C.pt.reset();
+    if (fill != 0.0 && !seeds.empty()) {
       const int nl = xt->nl();
-      const Context& c = *P->ctx;
       const int64_t q = llround_checked(fill, xt->scale);
       std::vector<uint64_t> ptv;
       for (size_t i = 0; i < seeds.size(); ++i)
         for (int j = 0; j < nl; ++j) ptv.insert(ptv.end(), static_cast<size_t>(c.n()), lift_signed_h(q, c.primes()[j]));
-      pt = std::make_shared<DevArr>(ptv.size() * 8, S(P));
-      HG_CUDA(cudaMemcpyAsync(pt->p, ptv.data(), ptv.size() * 8, cudaMemcpyHostToDevice, S(P)));
+      C.pt = std::make_shared<DevArr>(ptv.size() * 8, S(P));
+      HG_CUDA(cudaMemcpyAsync(C.pt->p, ptv.data(), ptv.size() * 8, cudaMemcpyHostToDevice, S(P)));
     }
-    encrypt_items(P, seeds, pt ? pt->as<uint64_t>() : nullptr, xt->level, cat->item(xt->count));
+    HG_CUDA(cudaStreamSynchronize(S(P)));
+    C.level = xt->level;
+    C.local_count = xt->count;
   }
-  return gather(P, out_shape, out_batched, cat, gmap);
+  // output = x's elements copied into place + the fresh fills (encrypted compactly, then placed)
+  auto out = new_ct(P, m_out, xt->level, xt->scale);
+  const int64_t ncopy = C.groups, nfill = static_cast<int64_t>(C.fill_pos.size());
+  k::scatter_items(c, xt->p, C.idx->as<int32_t>(), C.idx->as<int32_t>() + ncopy, out->p, ncopy, xt->item_words(), S(P));
+  if (nfill > 0) {
+    std::vector<uint64_t> seeds(C.fill_pos.begin(), C.fill_pos.end());
+    auto fills = new_ct(P, nfill, xt->level, xt->scale);
+    encrypt_items(P, seeds, C.pt ? C.pt->as<uint64_t>() : nullptr, xt->level, fills->p, C.w->as<uint64_t>());
+    k::scatter_items(c, fills->p, nullptr, C.oidx->as<int32_t>(), out->p, nfill, xt->item_words(), S(P));
+  }
+  Val v;
+  v.shape = out_shape;
+  v.batched = out_batched;
+  v.ct = out;
+  return v;
 }
 
 Val kernel_rearrange(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_shape, const Val& x) {
@@ -1824,7 +1858,23 @@ void run_end(hg_plan* P, RunState& st) {
   P->live = nullptr;
 }
 
-void run_plan(hg_plan* P) {
+void arm_sample_flags(hg_plan* P) {
+  if (!P->sample_flags) {
+    P->sample_flag_cap = 256;
+    HG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&P->sample_flags), sizeof(int) * P->sample_flag_cap));
+  }
+  P->sample_flag_used = 0;
+  P->in_run = true;
+}
+// after the run's synchronisation: did any deferred fresh encryption need the host fix-up?
+bool sample_flags_hit(hg_plan* P) {
+  P->in_run = false;
+  for (int i = 0; i < P->sample_flag_used; ++i)
+    if (P->sample_flags[i] != 0) return true;
+  return false;
+}
+
+void run_plan_once(hg_plan* P) {
   RunState st;
   run_begin(P, st);
   try {
@@ -1835,9 +1885,25 @@ void run_plan(hg_plan* P) {
     run_outputs(P, st);
   } catch (...) {
     P->live = nullptr;
+    P->in_run = false;
     throw;
   }
   run_end(P, st);
+}
+
+void run_plan(hg_plan* P) {
+  arm_sample_flags(P);
+  run_plan_once(P);
+  if (sample_flags_hit(P)) {  // rare (values within 1e-9 of a rounding boundary): redo with host fix-ups
+    P->sync_sampling = true;
+    try {
+      run_plan_once(P);
+    } catch (...) {
+      P->sync_sampling = false;
+      throw;
+    }
+    P->sync_sampling = false;
+  }
 }
 
 // In-process group: all ranks' plans on one device and stream, stepped node by
@@ -1985,6 +2051,7 @@ int hg_plan_create(hg_context* ctx, const hg_keys* keys, const char* graph_json,
 void hg_plan_destroy(hg_plan* plan) {
   if (!plan) return;
   cudaStreamSynchronize(plan->ctx->stream());
+  if (plan->sample_flags) cudaFreeHost(plan->sample_flags);
   delete plan;
 }
 
@@ -2110,7 +2177,20 @@ int hg_group_run(hg_plan** plans, int world) {
         ps[r]->transport = t;
       }
     }
+    for (auto* p : ps) hg::arm_sample_flags(p);
     hg::run_group(ps);
+    bool hit = false;
+    for (auto* p : ps) hit = hg::sample_flags_hit(p) || hit;
+    if (hit) {
+      for (auto* p : ps) p->sync_sampling = true;
+      try {
+        hg::run_group(ps);
+      } catch (...) {
+        for (auto* p : ps) p->sync_sampling = false;
+        throw;
+      }
+      for (auto* p : ps) p->sync_sampling = false;
+    }
   });
 }
 

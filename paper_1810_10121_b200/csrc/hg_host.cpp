@@ -236,6 +236,15 @@ Context::Context(const ContextParamsH& p, int device) : m_p(p), m_device(device)
 
   HG_CUDA(cudaSetDevice(device));
   HG_CUDA(cudaStreamCreateWithFlags(&m_stream, cudaStreamNonBlocking));
+  {
+    // keep freed ciphertext buffers in the stream-ordered pool across synchronisations
+    // (the default threshold 0 returns them to the driver at every sync, and the next
+    // step's cudaMallocAsync pays for fresh physical allocations)
+    cudaMemPool_t pool;
+    HG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;
+    HG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
 
   // tables: per limb fw (16N) | iw (16N) | fw32 (8N) | iw32 (8N)
   // per limb: fw (16N) | iw (16N) | fw32 (8N) | iw32 (8N) | fwp (16N) | iwp (16N) | fwp32 (8N) | iwp32 (8N)

@@ -315,7 +315,14 @@ void gather_items(const Context& c, const uint64_t* in, const int32_t* idx, uint
                   cudaStream_t s);
 // keygen pointwise: out = -(a*s + e) (+ f*s^2 on limb `special` if special >= 0)
 // fresh-encryption samples (u, e0, e1) for host seeds, on the GPU, bit-identical to sample_encryption()
-void sample_encryption_gpu(const Context& c, const uint64_t* seeds_host, int64_t items, int64_t* out, cudaStream_t s);
+// deferred_flag_count (pinned host int): skip the synchronous fix-up check; the count of
+// values needing the host fix-up lands there once the stream reaches it (0 = output final)
+// seeds_dev: the same seeds already on the device (skips the host->device copy)
+void sample_encryption_gpu(const Context& c, const uint64_t* seeds_host, int64_t items, int64_t* out, cudaStream_t s,
+                           int* deferred_flag_count = nullptr, const uint64_t* seeds_dev = nullptr);
+// out[dst[i]] = in[src ? src[i] : i] for whole items
+void scatter_items(const Context& c, const uint64_t* in, const int32_t* src, const int32_t* dst, uint64_t* out,
+                   int64_t items, int64_t item_words, cudaStream_t s);
 // bit-exact slot encode on the GPU (encoder.hpp:58-77 + ckks_backend.hpp:186-192):
 // column e holds values[e*col_stride + m*elem_stride], m < count; out int64 [cols][N]
 // = llround(coeff * scale).  Sets *flag (device int) when a coefficient overflows.

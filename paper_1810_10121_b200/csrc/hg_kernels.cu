@@ -624,6 +624,21 @@ __global__ void k_gather_items(const uint64_t* __restrict__ in, const int32_t* _
   }
 }
 
+// out[dst[i]] = in[src ? src[i] : i], whole items (item_words u64 each)
+__global__ void k_scatter_items(const uint64_t* __restrict__ in, const int32_t* __restrict__ src,
+                                const int32_t* __restrict__ dst, uint64_t* __restrict__ out, int64_t items,
+                                int64_t item_words) {
+  const int64_t vec = item_words / 2;
+  const int64_t total = items * vec;
+  const ulonglong2* in2 = reinterpret_cast<const ulonglong2*>(in);
+  ulonglong2* out2 = reinterpret_cast<ulonglong2*>(out);
+  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < total; w += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t it = w / vec, r = w - it * vec;
+    const int64_t si = src ? (int64_t)src[it] : it;
+    out2[(int64_t)dst[it] * vec + r] = in2[si * vec + r];
+  }
+}
+
 }  // namespace
 
 // ==========================================================================
@@ -931,6 +946,15 @@ void gather_items(const Context& c, const uint64_t* in, const int32_t* idx, uint
   HG_CUDA(cudaGetLastError());
 }
 
+void scatter_items(const Context& c, const uint64_t* in, const int32_t* src, const int32_t* dst, uint64_t* out,
+                   int64_t items, int64_t item_words, cudaStream_t s) {
+  if (items <= 0) return;
+  c.kt_begin("k_scatter_items", s, 2.0 * items * item_words * 8, 0.0);
+  k_scatter_items<<<ew_blocks(items * item_words / 2, 256), 256, 0, s>>>(in, src, dst, out, items, item_words);
+  c.kt_end(s);
+  HG_CUDA(cudaGetLastError());
+}
+
 void keygen_b(const Context& c, const uint64_t* a, const uint64_t* sk, const uint64_t* e, uint64_t* out, int nl,
               int special, uint64_t f, cudaStream_t s) {
   const int64_t words = (int64_t)nl * c.n();
@@ -1112,7 +1136,7 @@ __global__ void k_sample_encryption(const uint64_t* __restrict__ seeds, int64_t 
 
 namespace k {
 void sample_encryption_gpu(const Context& c, const uint64_t* seeds_host, int64_t items, int64_t* out,
-                           cudaStream_t s) {
+                           cudaStream_t s, int* deferred_flag_count, const uint64_t* seeds_dev) {
   if (items <= 0) return;
   const int n = (int)c.n();
   const int cap = 1024;
@@ -1132,7 +1156,8 @@ void sample_encryption_gpu(const Context& c, const uint64_t* seeds_host, int64_t
   uint64_t* d_seeds = reinterpret_cast<uint64_t*>(buf);
   int* d_n = reinterpret_cast<int*>(buf + seed_bytes);
   SampleFlag* d_flags = reinterpret_cast<SampleFlag*>(buf + seed_bytes + 16);
-  HG_CUDA(cudaMemcpyAsync(d_seeds, seeds_host, seed_bytes, cudaMemcpyHostToDevice, s));
+  if (seeds_dev) d_seeds = const_cast<uint64_t*>(seeds_dev);  // cached on the device by the caller
+  else HG_CUDA(cudaMemcpyAsync(d_seeds, seeds_host, seed_bytes, cudaMemcpyHostToDevice, s));
   HG_CUDA(cudaMemsetAsync(d_n, 0, 4, s));
   const int64_t total = items * n;
   c.kt_begin("k_sample_encryption", s, (double)items * 3 * n * 8, 0.0);
@@ -1140,6 +1165,11 @@ void sample_encryption_gpu(const Context& c, const uint64_t* seeds_host, int64_t
                                                                        out, d_n, d_flags, cap, guard);
   c.kt_end(s);
   HG_CUDA(cudaGetLastError());
+  if (deferred_flag_count) {
+    // caller checks the count after its own synchronisation and redoes the work if it is non-zero
+    HG_CUDA(cudaMemcpyAsync(deferred_flag_count, d_n, 4, cudaMemcpyDeviceToHost, s));
+    return;
+  }
   int nflags = 0;
   HG_CUDA(cudaMemcpyAsync(&nflags, d_n, 4, cudaMemcpyDeviceToHost, s));
   HG_CUDA(cudaStreamSynchronize(s));
