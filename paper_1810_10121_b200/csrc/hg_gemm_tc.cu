@@ -27,10 +27,14 @@
 namespace hg {
 namespace {
 
+struct LimbListTc {
+  int count;
+  int limb[HG_MAX_LIMBS];
+};
+
 constexpr int kTcM = 128;      // coefficients per CTA tile (MMA M)
 constexpr int kTcK = 32;       // terms per MMA step (i8: 32 bytes of K)
 constexpr int kTcThreads = 256;
-constexpr int kTcStages = 2;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -97,37 +101,132 @@ constexpr int kBTileBytes = NT * kTcK;
 
 template <int XB, int WB, int NT>
 struct TcCfg {
-  static constexpr int S = XB + WB - 1;                                 // shift groups
+  static constexpr int S = XB + WB - 1;  // shift groups
   static constexpr int COLS = S * NT <= 32 ? 32 : S * NT <= 64 ? 64 : S * NT <= 128 ? 128 : S * NT <= 256 ? 256 : 512;
-  static constexpr int stage_bytes = XB * kATileBytes + WB * kBTileBytes<NT>;
-  static constexpr int smem = kTcStages * stage_bytes + 64;
+  static constexpr int a_bytes = XB * kATileBytes;
+  static constexpr int w_bytes = WB * kBTileBytes<NT>;
+  // A/W ring as deep as shared memory allows; loads run LOOK K steps ahead of the MMA
+  // (L2 latency ~1-2 us vs ~0.3 us of MMA per step), a slot is refilled 2 steps after its MMA
+  static constexpr int RING = (220 * 1024) / (a_bytes + w_bytes) < 12 ? (220 * 1024) / (a_bytes + w_bytes) : 12;
+  static constexpr int LOOK = RING - 2;
+  static_assert(RING >= 4, "shared memory ring");
+  static constexpr int off_w = RING * a_bytes;
+  static constexpr int off_bar = off_w + RING * w_bytes;
+  static constexpr int smem = off_bar + (2 * RING + 2) * 8 + 16;
   static_assert(S * NT <= 512, "TMEM columns");
 };
 
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// Byte planes of the distinct input items, once per contraction:
+//   planes[((item * 2 + poly) * nlc + lp) * N * XB + (col / 128) * XB * 128 + b * 128 + col % 128]
+//     = byte b of x[item][poly][limb lp][col]
+// so one (term, plane) row of a 128-coefficient tile is 128 contiguous bytes.
+template <int XB>
+__global__ void k_split_planes(const uint64_t* __restrict__ x, uint8_t* __restrict__ planes, int64_t items, int nl,
+                               const LimbListTc LL, int64_t n) {
+  const int64_t quads = n / 4;
+  const int64_t total = items * 2 * LL.count * quads;
+  for (int64_t gq = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gq < total; gq += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c4 = gq % quads, row = gq / quads;  // row = (item * 2 + poly) * nlc + lp
+    const int lp = (int)(row % LL.count);
+    const int64_t ip = row / LL.count;                 // item * 2 + poly
+    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(x + (ip * nl + LL.limb[lp]) * n + 4 * c4);
+    const ulonglong2 v0 = __ldg(src), v1 = __ldg(src + 1);
+    const int64_t col = 4 * c4;
+    uint8_t* dst = planes + row * n * XB + (col >> 7) * XB * 128 + (col & 127);
+    // 4x4 byte transpose of the low words (planes 0..3), then of the high words (planes 4..)
+    {
+      const uint32_t w0 = (uint32_t)v0.x, w1 = (uint32_t)v0.y, w2 = (uint32_t)v1.x, w3 = (uint32_t)v1.y;
+      const uint32_t t0 = __byte_perm(w0, w1, 0x5140), t1 = __byte_perm(w0, w1, 0x7362);
+      const uint32_t u0 = __byte_perm(w2, w3, 0x5140), u1 = __byte_perm(w2, w3, 0x7362);
+      const uint32_t pl[4] = {__byte_perm(t0, u0, 0x5410), __byte_perm(t0, u0, 0x7632), __byte_perm(t1, u1, 0x5410),
+                              __byte_perm(t1, u1, 0x7632)};
+#pragma unroll
+      for (int b = 0; b < (XB < 4 ? XB : 4); ++b) *reinterpret_cast<uint32_t*>(dst + b * 128) = pl[b];
+    }
+    if constexpr (XB > 4) {
+      const uint32_t w0 = (uint32_t)(v0.x >> 32), w1 = (uint32_t)(v0.y >> 32), w2 = (uint32_t)(v1.x >> 32),
+                     w3 = (uint32_t)(v1.y >> 32);
+      const uint32_t t0 = __byte_perm(w0, w1, 0x5140), t1 = __byte_perm(w0, w1, 0x7362);
+      const uint32_t u0 = __byte_perm(w2, w3, 0x5140), u1 = __byte_perm(w2, w3, 0x7362);
+      const uint32_t pl[4] = {__byte_perm(t0, u0, 0x5410), __byte_perm(t0, u0, 0x7632), __byte_perm(t1, u1, 0x5410),
+                              __byte_perm(t1, u1, 0x7632)};
+#pragma unroll
+      for (int b = 4; b < XB; ++b) *reinterpret_cast<uint32_t*>(dst + b * 128) = pl[b - 4];
+    }
+  }
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// tile decomposition (n-tile fastest, then coefficient tile, poly, group, limb of the class):
+// CTAs running together share their A rows in L2
+struct TcTile {
+  int nt, p, lp;
+  int64_t ct, g;
+};
+__device__ __forceinline__ TcTile tc_tile(int64_t t, int ntiles, int64_t ncol, int64_t groups) {
+  TcTile r;
+  r.nt = (int)(t % ntiles);
+  t /= ntiles;
+  r.ct = t % ncol;
+  t /= ncol;
+  r.p = (int)(t & 1);
+  t >>= 1;
+  r.g = t % groups;
+  r.lp = (int)(t / groups);
+  return r;
+}
+
+// Warp-specialised persistent kernel (384 threads):
+//   warp 0      MMA issuer: waits a ring slot's `full` barrier, issues the XB x WB
+//               tcgen05.mma.kind::i8 into the TMEM shift groups, commits to `empty`
+//               (and to `tmem_full` after a tile's last K step);
+//   warps 1-7   producers: gather the 32 terms' byte-plane rows (by idx) and the packed
+//               W tile of each K step into the ring with cp.async, LOOK steps ahead;
+//               after their own copies of a step land: fence.proxy.async + arrive `full`;
+//   warps 8-15  epilogue (two per TMEM lane quadrant, each half of the tile's outputs):
+//               TMEM -> registers, shift groups recombined and reduced mod q,
+//               then arrive `tmem_empty` so the next tile's MMAs may overwrite TMEM.
+constexpr int kTcProducers = 224;
+constexpr int kTcThreadsWS = 512;  // + 8 epilogue warps: two per TMEM lane quadrant
+
 template <int XB, int WB, int NT>
-__global__ void __launch_bounds__(kTcThreads, 1)
-    k_gemm_tc(const uint64_t* __restrict__ x, const int32_t* __restrict__ idx, const uint8_t* __restrict__ wpk,
-              const int32_t* __restrict__ oidx, uint64_t* __restrict__ out, int mg, int kt, int nl, int limb_pos,
-              int limb, int64_t w_group_stride, const CtxParams P) {
+__global__ void __launch_bounds__(kTcThreadsWS, 1)
+    k_gemm_tc(const uint8_t* __restrict__ planes, const int32_t* __restrict__ idx, const uint8_t* __restrict__ wpk,
+              const int32_t* __restrict__ oidx, uint64_t* __restrict__ out, int mg, int kt, int nl,
+              const LimbListTc LL, int64_t groups, int64_t w_group_stride, const CtxParams P) {
   using Cf = TcCfg<XB, WB, NT>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kTcStages * Cf::stage_bytes);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kTcStages);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cf::off_bar);
+  uint64_t* empty = full + Cf::RING;
+  uint64_t* tmem_full = empty + Cf::RING;
+  uint64_t* tmem_empty = tmem_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t n = P.n;
-  const int64_t col0 = (int64_t)blockIdx.x * kTcM;
-  const int nt = blockIdx.y;
-  const int64_t g = blockIdx.z >> 1;
-  const int p = blockIdx.z & 1;
   const int ksteps = (kt + kTcK - 1) / kTcK;
   const int ntiles = (mg + NT - 1) / NT;
-  const int64_t item_words = 2 * (int64_t)nl * n;
-  const uint64_t* xrow = x + ((int64_t)p * nl + limb) * n + col0;
-  // packed weights of (group, limb_pos, n-tile): [kstep][WB planes][NT x 32 bytes]
-  const uint8_t* wt = wpk + g * w_group_stride + ((int64_t)limb_pos * ntiles + nt) * ksteps * WB * kBTileBytes<NT>;
+  const int64_t ncol = n / kTcM;
+  const int64_t row_bytes = n * XB;
+  const int64_t tiles = (int64_t)ntiles * ncol * 2 * groups * LL.count;
+  const uint32_t sbase = smem_u32(smem);
 
   if (tid == 0) {
-    for (int s = 0; s < kTcStages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < Cf::RING; ++s) {
+      mbar_init(&full[s], kTcProducers);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    mbar_init(tmem_empty, 256);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -140,119 +239,135 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tmem_slot;
 
-  // producer mapping: 32 coefficient quads x 8 term lanes; each thread converts 4 terms x 4 coefficients
-  const int cq = tid & 31;        // coefficients 4cq .. 4cq+3
-  const int tl = tid >> 5;        // terms tl, tl+8, tl+16, tl+24
-  for (int ks = 0; ks < ksteps; ++ks) {
-    const int st = ks % kTcStages;
-    uint8_t* sa = smem + st * Cf::stage_bytes;
-    uint8_t* sb = sa + XB * kATileBytes;
-    // load X (4 terms x 4 coefficients per thread) before waiting for the stage to drain
-    ulonglong2 v[4][2];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int t = ks * kTcK + tl + 8 * u;
-      if (t < kt) {
-        const ulonglong2* src = reinterpret_cast<const ulonglong2*>(xrow + (int64_t)idx[g * kt + t] * item_words + 4 * cq);
-        v[u][0] = __ldg(src);
-        v[u][1] = __ldg(src + 1);
-      } else {
-        v[u][0] = make_ulonglong2(0, 0);
-        v[u][1] = make_ulonglong2(0, 0);
-      }
-    }
-    if (ks >= kTcStages) mbar_wait(&bars[st], ((ks - kTcStages) / kTcStages) & 1);
-    // X bytes -> A planes (4 coefficients packed per 32-bit store)
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int k = tl + 8 * u;
-      const uint64_t e0 = v[u][0].x, e1 = v[u][0].y, e2 = v[u][1].x, e3 = v[u][1].y;
-#pragma unroll
-      for (int b = 0; b < XB; ++b) {
-        const uint32_t word = (uint32_t)((e0 >> (8 * b)) & 0xFF) | ((uint32_t)((e1 >> (8 * b)) & 0xFF) << 8) |
-                              ((uint32_t)((e2 >> (8 * b)) & 0xFF) << 16) | ((uint32_t)((e3 >> (8 * b)) & 0xFF) << 24);
-        *reinterpret_cast<uint32_t*>(sa + b * kATileBytes + a_off(4 * cq, k)) = word;
-      }
-    }
-    // W bytes: a contiguous pre-packed block
-    const uint4* wsrc = reinterpret_cast<const uint4*>(wt + (int64_t)ks * WB * kBTileBytes<NT>);
-    uint4* wdst = reinterpret_cast<uint4*>(sb);
-    for (int i = tid; i < WB * kBTileBytes<NT> / 16; i += kTcThreads) wdst[i] = __ldg(wsrc + i);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0) {
+    // ---------------- MMA issuer ----------------
+    if (lane == 0) {
       constexpr uint32_t idesc = idesc_i8<NT>();
+      int64_t k = 0, tcount = 0;
+      for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tcount) {
+        if (tcount > 0) mbar_wait(tmem_empty, (uint32_t)((tcount - 1) & 1));  // epilogue has read TMEM
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        for (int s = 0; s < ksteps; ++s, ++k) {
+          const int slot = (int)(k % Cf::RING);
+          mbar_wait(&full[slot], (uint32_t)((k / Cf::RING) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t sa = sbase + slot * Cf::a_bytes;
+          const uint32_t sb = sbase + Cf::off_w + slot * Cf::w_bytes;
 #pragma unroll
-      for (int a = 0; a < WB; ++a) {
+          for (int a = 0; a < WB; ++a) {
 #pragma unroll
-        for (int b = 0; b < XB; ++b) {
-          const int s = a + b;
-          const int a_first = s - (XB - 1) > 0 ? s - (XB - 1) : 0;  // first (a, b) pair reaching group s
-          const uint32_t acc = (ks > 0 || a != a_first) ? 1u : 0u;
-          const uint64_t ad = umma_desc(smem_u32(sa + b * kATileBytes), 1024, 128);
-          const uint64_t bd = umma_desc(smem_u32(sb + a * kBTileBytes<NT>), (NT / 8) * 128, 128);
-          umma_i8(tmem + (uint32_t)(s * NT), ad, bd, idesc, acc);
+            for (int b = 0; b < XB; ++b) {
+              const int sg = a + b;
+              const int a_first = sg - (XB - 1) > 0 ? sg - (XB - 1) : 0;  // first (a, b) pair reaching group sg
+              const uint32_t acc = (s > 0 || a != a_first) ? 1u : 0u;
+              umma_i8(tmem + (uint32_t)(sg * NT), umma_desc(sa + b * kATileBytes, 1024, 128),
+                      umma_desc(sb + a * kBTileBytes<NT>, (NT / 8) * 128, 128), idesc, acc);
+            }
+          }
+          umma_commit(&empty[slot]);
+        }
+        umma_commit(tmem_full);
+      }
+    }
+  } else if (warp < 8) {
+    // ---------------- producers ----------------
+    const int pt = tid - 32;
+    int64_t k = 0;
+    auto land = [&](int64_t kk) {  // own copies of step kk complete -> visible to the async proxy
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&full[kk % Cf::RING]);
+    };
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      const TcTile T = tc_tile(tile, ntiles, ncol, groups);
+      const uint8_t* prow = planes + ((int64_t)T.p * LL.count + T.lp) * row_bytes + T.ct * XB * 128;
+      const int64_t item_stride = 2 * (int64_t)LL.count * row_bytes;
+      const uint8_t* wt = wpk + T.g * w_group_stride + ((int64_t)T.lp * ntiles + T.nt) * ksteps * Cf::w_bytes;
+      const int32_t* gidx = idx + T.g * kt;
+      for (int s = 0; s < ksteps; ++s, ++k) {
+        const int slot = (int)(k % Cf::RING);
+        if (k >= Cf::RING) mbar_wait(&empty[slot], (uint32_t)(((k / Cf::RING) - 1) & 1));  // MMA(k - RING) done
+        const uint32_t adst = sbase + slot * Cf::a_bytes;
+        // 16-byte chunk c: j = c & 7 (coefficients 16 j ..), plane b, term kk
+        for (int c = pt; c < kTcK * XB * 8; c += kTcProducers) {
+          const int j = c & 7, rest = c >> 3, b = rest % XB, kk = rest / XB;
+          const int t = s * kTcK + kk;
+          if (t < kt)
+            cp_async16(adst + b * kATileBytes + ((kk >> 3) * 8 + j) * 128 + (kk & 7) * 16,
+                       prow + (int64_t)__ldg(gidx + t) * item_stride + b * 128 + j * 16);
+        }
+        const uint32_t wdst = sbase + Cf::off_w + slot * Cf::w_bytes;
+        const uint8_t* wsrc = wt + (int64_t)s * Cf::w_bytes;
+        for (int c = pt; c < Cf::w_bytes / 16; c += kTcProducers) cp_async16(wdst + c * 16, wsrc + c * 16);
+        cp_async_commit();
+        if (k >= Cf::LOOK) {
+          cp_async_wait<Cf::LOOK>();
+          land(k - Cf::LOOK);
         }
       }
-      umma_commit(&bars[st]);
     }
-  }
-  // wait for the final commit (commits complete in order)
-  mbar_wait(&bars[(ksteps - 1) % kTcStages], ((ksteps - 1) / kTcStages) & 1);
-  asm volatile("tcgen05.fence::after_thread_sync;");
-
-  // epilogue: warp w reads lanes 32 (w % 4) .. +31 (= coefficients), columns split by w / 4
-  const LimbInfo& L = P.limb[limb];
-  const uint64_t q = L.q;
-  const int lane_base = 32 * (warp & 3);
-  const int64_t col = col0 + lane_base + lane;
-  uint64_t pw[Cf::S];  // 2^8s mod q
-  {
-    uint64_t v = 1 % q;
+    // drain: the last LOOK steps
+    cp_async_wait<0>();
+    for (int64_t kk = k - Cf::LOOK < 0 ? 0 : k - Cf::LOOK; kk < k; ++kk) land(kk);
+  } else {
+    // ---------------- epilogue ----------------
+    const int quad = warp & 3;  // TMEM lanes 32 quad .. +31 = coefficients
+    const int half = (warp - 8) >> 2;
+    int64_t tcount = 0;
+    for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++tcount) {
+      const TcTile T = tc_tile(tile, ntiles, ncol, groups);
+      const int limb = LL.limb[T.lp];
+      const LimbInfo& L = P.limb[limb];
+      const uint64_t q = L.q;
+      const int64_t col = T.ct * kTcM + 32 * quad + lane;
+      mbar_wait(tmem_full, (uint32_t)(tcount & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      // 2^8s mod q for the small-limb recombination (sum_s D_s (2^8s mod q) < 7 2^31 2^30 < 2^64)
+      uint32_t pw32[Cf::S];
+      {
+        uint64_t v = 1 % q;
 #pragma unroll
-    for (int s = 0; s < Cf::S; ++s) {
-      pw[s] = v;
-      v = mul_mod(v, 256 % q, L);
-    }
-  }
-  const int nhalf = NT / 2;
-  const int nbeg = (warp >> 2) * nhalf;
-  for (int n0 = nbeg; n0 < nbeg + nhalf; n0 += 8) {
-    uint32_t d[Cf::S][8];
-#pragma unroll
-    for (int s = 0; s < Cf::S; ++s)
-      tmem_ld8(tmem + ((uint32_t)lane_base << 16) + (uint32_t)(s * NT + n0), d[s]);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int m = nt * NT + n0 + e;
-      if (m >= mg) break;
-      uint64_t r;
-      if (q < (1ull << 30)) {
-        // sum_s D_s 2^8s < 2^(8(S-1)+31) < 2^124: one 128-bit reduction
-        uint64_t lo = 0, hi = 0;
-#pragma unroll
-        for (int s = 0; s < Cf::S; ++s) {
-          const uint64_t dv = d[s][e];
-          const int sh = 8 * s;
-          const uint64_t plo = sh < 64 ? dv << sh : 0;
-          const uint64_t phi = sh == 0 ? 0 : (sh < 64 ? dv >> (64 - sh) : dv << (sh - 64));
-          lo += plo;
-          hi += phi + (lo < plo);
+        for (int sg = 0; sg < Cf::S; ++sg) {
+          pw32[sg] = (uint32_t)v;
+          v = (v << 8) % q;
         }
-        r = reduce128(lo, hi, L);
-      } else {
-        uint64_t accq = 0;
-#pragma unroll
-        for (int s = 0; s < Cf::S; ++s) accq = add_mod(accq, mul_mod(d[s][e], pw[s], L), q);
-        r = accq;
       }
-      const int64_t oi = oidx ? (int64_t)oidx[g * mg + m] : g * mg + m;
-      out[(oi * 2 * nl + (int64_t)p * nl + limb) * n + col] = r;
+      const int nlo = half * (NT / 2), nhi = nlo + NT / 2;
+      for (int n0 = nlo; n0 < nhi; n0 += 8) {
+        uint32_t d[Cf::S][8];
+#pragma unroll
+        for (int sg = 0; sg < Cf::S; ++sg)
+          tmem_ld8(tmem + ((uint32_t)(32 * quad) << 16) + (uint32_t)(sg * NT + n0), d[sg]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (n0 + 8 >= nhi) {  // this thread's TMEM reads done: the MMA warp may start the next tile
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          mbar_arrive(tmem_empty);
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int m = T.nt * NT + n0 + e;
+          if (m >= mg) break;
+          uint64_t res;
+          if (q < (1ull << 30)) {
+            uint64_t acc64 = 0;
+#pragma unroll
+            for (int sg = 0; sg < Cf::S; ++sg) acc64 += (uint64_t)d[sg][e] * pw32[sg];
+            res = reduce128(acc64, 0, L);
+          } else {
+            uint64_t accq = 0, pw = 1;
+            const uint64_t b256 = 256 % q;
+#pragma unroll
+            for (int sg = 0; sg < Cf::S; ++sg) {
+              accq = add_mod(accq, mul_mod(d[sg][e], pw, L), q);
+              pw = mul_mod(pw, b256, L);
+            }
+            res = accq;
+          }
+          const int64_t oi = oidx ? (int64_t)oidx[T.g * mg + m] : T.g * mg + m;
+          out[(oi * 2 * nl + (int64_t)T.p * nl + limb) * n + col] = res;
+        }
+      }
     }
   }
-  asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(Cf::COLS));
 }
@@ -291,11 +406,11 @@ void pack_weights_tc(const std::vector<uint64_t>& wres, int64_t wgroups, int mg,
     }
 }
 
-// one launch per limb class width; wpk packed by pack_weights_tc for `limbs`
+// byte planes of the input items, then one persistent GEMM launch per residue width
 template <int XB, int NT>
-static void launch_tc(const Context& c, const uint64_t* x, const int32_t* idx, const uint8_t* wpk,
+static void launch_tc(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* idx, const uint8_t* wpk,
                       int64_t w_group_stride, const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt,
-                      int nl, const std::vector<int>& limbs, cudaStream_t s) {
+                      int nl, const std::vector<int>& limbs, cudaStream_t s, double alg_bytes, double alg_macs) {
   using Cf = TcCfg<XB, XB, NT>;
   static bool attr = false;
   if (!attr) {
@@ -303,13 +418,30 @@ static void launch_tc(const Context& c, const uint64_t* x, const int32_t* idx, c
                                  Cf::smem));
     attr = true;
   }
-  const int ntiles = (mg + NT - 1) / NT;
-  for (size_t lp = 0; lp < limbs.size(); ++lp) {
-    dim3 grid((unsigned)(c.n() / kTcM), (unsigned)ntiles, (unsigned)(groups * 2));
-    k_gemm_tc<XB, XB, NT><<<grid, kTcThreads, Cf::smem, s>>>(x, idx, wpk, oidx, out, mg, kt, nl, (int)lp, limbs[lp],
-                                                             w_group_stride, c.kp());
+  LimbListTc LL{};
+  LL.count = (int)limbs.size();
+  for (size_t i = 0; i < limbs.size(); ++i) LL.limb[i] = limbs[i];
+  const int64_t n = c.n();
+  const size_t plane_bytes = (size_t)x_items * 2 * LL.count * n * XB;
+  uint8_t* planes = static_cast<uint8_t*>(const_cast<Context&>(c).scratch(plane_bytes, 11));
+  int sms = 148;
+  HG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device()));
+  {
+    const int64_t work = x_items * 2 * LL.count * (n / 4);
+    const unsigned blocks = (unsigned)std::min<int64_t>((work + 255) / 256, (int64_t)sms * 16);
+    c.kt_begin("k_split_planes", s, (double)x_items * 2 * LL.count * n * (8 + XB), 0.0);
+    k_split_planes<XB><<<blocks, 256, 0, s>>>(x, planes, x_items, nl, LL, n);
+    c.kt_end(s);
     HG_CUDA(cudaGetLastError());
   }
+  const int ntiles = (mg + NT - 1) / NT;
+  const int64_t tiles = (int64_t)ntiles * (n / kTcM) * 2 * groups * LL.count;
+  const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+  c.kt_begin("k_gemm_tc", s, alg_bytes, alg_macs);
+  k_gemm_tc<XB, XB, NT><<<grid, kTcThreadsWS, Cf::smem, s>>>(planes, idx, wpk, oidx, out, mg, kt, nl, LL, groups,
+                                                         w_group_stride, c.kp());
+  c.kt_end(s);
+  HG_CUDA(cudaGetLastError());
 }
 
 bool gemm_tc_supported(const Context& c, int mg, int kt) {
@@ -326,11 +458,14 @@ void gemm_tc(const Context& c, const uint64_t* x, int64_t x_items, const int32_t
   const double item_bytes = 2.0 * nl * c.n() * 8;
   const double frac = (double)limbs.size() / nl;
   const double in_items = std::min<double>((double)groups * kt, (double)x_items);
-  c.kt_begin("k_gemm_tc", s, frac * (in_items + (double)groups * mg) * item_bytes,
-             frac * (double)groups * mg * kt * 2.0 * nl * c.n());
   const int nt = tc_ntile(bytes, mg);
-#define HG_TC(B, NT) \
-  if (bytes == B && nt == NT) { launch_tc<B, NT>(c, x, idx, wpk, w_group_stride, oidx, out, groups, mg, kt, nl, limbs, s); c.kt_end(s); return; }
+#define HG_TC(B, NT)                                                                                  \
+  if (bytes == B && nt == NT) {                                                                       \
+    launch_tc<B, NT>(c, x, x_items, idx, wpk, w_group_stride, oidx, out, groups, mg, kt, nl, limbs, s, \
+                     frac * (in_items + (double)groups * mg) * item_bytes,                            \
+                     frac * (double)groups * mg * kt * 2.0 * nl * c.n());                             \
+    return;                                                                                           \
+  }
   HG_TC(4, 16) HG_TC(4, 32) HG_TC(4, 64)
   HG_TC(5, 16) HG_TC(5, 32) HG_TC(6, 16) HG_TC(6, 32) HG_TC(7, 16) HG_TC(7, 32)
 #undef HG_TC

@@ -614,6 +614,94 @@ __global__ void __launch_bounds__(kGT) k_gemm_lz(const uint64_t* __restrict__ x,
   }
 }
 
+// fp64-lane GEMM for 2^30 <= q < 2^50 (the same contract as k_gemm_lz): one exact
+// FMA-residual modmul (mulmod_f64) per MAC into a double accumulator, reduced every
+// F terms so |acc| stays below 2^52; canonicalised at the end.
+template <int MT, int C>
+__global__ void __launch_bounds__(kGT) k_gemm_f64(const uint64_t* __restrict__ x, const int32_t* __restrict__ idx,
+                                                  const uint64_t* __restrict__ w, int64_t w_group_stride,
+                                                  const int32_t* __restrict__ oidx, uint64_t* __restrict__ out,
+                                                  int mg, int kt, int nl, const LimbList LL, const CtxParams P) {
+  __shared__ __align__(16) double ws[kKC][MT];
+  __shared__ int32_t xs[kKC];
+  const int mtiles = (mg + MT - 1) / MT;
+  const int mt = blockIdx.x % mtiles;
+  const int64_t g = blockIdx.x / mtiles;
+  const int m0 = mt * MT;
+  const int p = blockIdx.z / LL.count;
+  const int j = LL.limb[blockIdx.z % LL.count];
+  const LimbInfo& L = P.limb[j];
+  const int64_t n = P.n;
+  const int64_t col0 = ((int64_t)blockIdx.y * kGT + threadIdx.x) * C;
+  const int64_t item_words = 2 * (int64_t)nl * n;
+  const uint64_t* xrow = x + ((int64_t)p * nl + j) * n + col0;
+  const double q = L.qd, qinv = L.qinvd;
+  // |mulmod_f64| < 1.2 q: F terms keep |acc| < 0.6 q + 1.2 q F < 2^52
+  const int F = (int)max(1.0, min(1.0e9, 4.0e15 / (1.2 * q)));
+  int since = 0;
+  double acc[MT][C];
+#pragma unroll
+  for (int m = 0; m < MT; ++m)
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[m][c] = 0.0;
+  const bool live = col0 < n;
+  for (int t0 = 0; t0 < kt; t0 += kKC) {
+    const int tc = min(kKC, kt - t0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kKC * MT; e += kGT) {
+      const int tt = e / MT, m = e % MT;
+      uint64_t v = 0;
+      if (tt < tc && m0 + m < mg) v = w[g * w_group_stride + ((int64_t)(m0 + m) * kt + t0 + tt) * nl + j];
+      ws[tt][m] = (double)v;
+    }
+    if (threadIdx.x < kKC) xs[threadIdx.x] = threadIdx.x < tc ? idx[g * kt + t0 + threadIdx.x] : idx[g * kt];
+    __syncthreads();
+    if (!live) continue;
+    const int tcu = (tc + kTU - 1) / kTU * kTU;
+    for (int f0 = 0; f0 < tcu; f0 += kTU) {
+      if (since + kTU > F) {
+#pragma unroll
+        for (int m = 0; m < MT; ++m)
+#pragma unroll
+          for (int c = 0; c < C; ++c) acc[m][c] = reduce_f64(acc[m][c], q, qinv);
+        since = 0;
+      }
+      since += kTU;
+      double xv[kTU][C];
+#pragma unroll
+      for (int u = 0; u < kTU; ++u) {
+        const uint64_t* xp = xrow + (int64_t)xs[f0 + u] * item_words;
+#pragma unroll
+        for (int c = 0; c < C; c += 2) {
+          const ulonglong2 v2 = __ldg(reinterpret_cast<const ulonglong2*>(xp + c));
+          xv[u][c] = (double)v2.x;
+          xv[u][c + 1] = (double)v2.y;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kTU; ++u) {
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          const double wv = ws[f0 + u][m];
+#pragma unroll
+          for (int c = 0; c < C; ++c) acc[m][c] = __dadd_rn(acc[m][c], mulmod_f64(xv[u][c], wv, q, qinv));
+        }
+      }
+    }
+  }
+  if (!live) return;
+#pragma unroll
+  for (int m = 0; m < MT; ++m) {
+    if (m0 + m >= mg) break;
+    const int64_t oi = oidx ? (int64_t)oidx[g * mg + m0 + m] : g * mg + m0 + m;
+    uint64_t* o = out + (oi * 2 * nl + (int64_t)p * nl + j) * n + col0;
+#pragma unroll
+    for (int c = 0; c < C; c += 2)
+      *reinterpret_cast<ulonglong2*>(o + c) =
+          make_ulonglong2((uint64_t)canon_f64(acc[m][c], q, qinv), (uint64_t)canon_f64(acc[m][c + 1], q, qinv));
+  }
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -875,7 +963,7 @@ void gemm(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* i
           int64_t w_group_stride, const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt, int nl,
           cudaStream_t s) {
   if (groups <= 0 || mg <= 0) return;
-  const Classes cl = classify(c, 0, nl);
+  const Classes cl = classify(c, 0, nl, fp64_lane());
   const int64_t n = c.n();
   const double item_bytes = 2.0 * nl * n * 8;
   const double in_items = std::min<double>((double)groups * kt, (double)x_items);
@@ -885,17 +973,20 @@ void gemm(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* i
     const double gb = frac * (in_items + (double)groups * mg) * item_bytes;
     const double gm = frac * (double)groups * mg * kt * 2.0 * nl * n;
     int MT, C;
-    if (wide) { MT = mg <= 4 ? 4 : 8; C = mg <= 4 ? 2 : 1; }
-    else { MT = mg <= 4 ? 4 : mg <= 8 ? 8 : 16; C = mg <= 8 ? 4 : 2; }
+    // output rows per thread: exact for 5 (CryptoNets conv), else the next power of two
+    if (wide) { MT = mg <= 4 ? 4 : mg == 5 ? 5 : 8; C = mg <= 5 ? 2 : 1; }
+    else { MT = mg <= 4 ? 4 : mg == 5 ? 5 : mg <= 8 ? 8 : 16; C = mg <= 8 ? 4 : 2; }
     const int mtiles = (mg + MT - 1) / MT;
     dim3 grid((unsigned)(mtiles * groups), (unsigned)((n + (int64_t)kGT * C - 1) / ((int64_t)kGT * C)),
               (unsigned)(2 * LL.count));
     c.kt_begin("k_gemm_lz", s, gb, gm);
     if (wide) {
       if (MT == 4) k_gemm_lz<true, 4, 2><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
+      else if (MT == 5) k_gemm_lz<true, 5, 2><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
       else k_gemm_lz<true, 8, 1><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
     } else {
       if (MT == 4) k_gemm_lz<false, 4, 4><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
+      else if (MT == 5) k_gemm_lz<false, 5, 4><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
       else if (MT == 8) k_gemm_lz<false, 8, 4><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
       else k_gemm_lz<false, 16, 2><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
     }
@@ -904,6 +995,21 @@ void gemm(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* i
   };
   launch(cl.small, false);
   launch(cl.wide, true);
+  if (cl.fp.count > 0) {
+    const LimbList& LL = cl.fp;
+    const double frac = (double)LL.count / nl;
+    const int MT = mg <= 4 ? 4 : mg == 5 ? 5 : 8, C = 2;
+    const int mtiles = (mg + MT - 1) / MT;
+    dim3 grid((unsigned)(mtiles * groups), (unsigned)((n + (int64_t)kGT * C - 1) / ((int64_t)kGT * C)),
+              (unsigned)(2 * LL.count));
+    c.kt_begin("k_gemm_f64", s, frac * (in_items + (double)groups * mg) * item_bytes,
+               frac * (double)groups * mg * kt * 2.0 * nl * n);
+    if (MT == 4) k_gemm_f64<4, 2><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
+    else if (MT == 5) k_gemm_f64<5, 2><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
+    else k_gemm_f64<8, 2><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
+    c.kt_end(s);
+    HG_CUDA(cudaGetLastError());
+  }
 }
 
 }  // namespace k2
