@@ -35,6 +35,11 @@ struct LimbInfo {
   double ninvd;          // N^{-1} mod q
   const double* fwpd;    // pass-ordered psi^brv / psi^-brv as doubles (fp64 lane)
   const double* iwpd;
+  // N >= 2^14: pass-ordered tables of the two (N/2)-point half transforms that follow the
+  // first forward stage, [2][N/2] (hg_host.cpp); u64 pairs, u32 pairs (small), doubles
+  const ulonglong2* fwh;
+  const uint2* fwh32;
+  const double* fwhd;
 };
 
 struct CtxParams {

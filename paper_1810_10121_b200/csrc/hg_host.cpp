@@ -249,7 +249,8 @@ Context::Context(const ContextParamsH& p, int device) : m_p(p), m_device(device)
   // tables: per limb fw (16N) | iw (16N) | fw32 (8N) | iw32 (8N)
   // per limb: fw (16N) | iw (16N) | fw32 (8N) | iw32 (8N) | fwp (16N) | iwp (16N) | fwp32 (8N) | iwp32 (8N)
   //           | fwpd (8N) | iwpd (8N)   (fp64 lane: pass-ordered twiddles as doubles)
-  const size_t per = 112 * static_cast<size_t>(n);
+  //           | fwh (16N) | fwh32 (8N) | fwhd (8N)  (half-transform tables, [2][N/2] each, see below)
+  const size_t per = 144 * static_cast<size_t>(n);
   m_tables.alloc(per * nl);
   std::vector<uint8_t> host(per * nl, 0);
   m_psi.resize(nl);
@@ -340,6 +341,45 @@ Context::Context(const ContextParamsH& p, int device) : m_p(p), m_device(device)
           for (int64_t gi = 0; gi < nbi; ++gi)
             for (int64_t ii = 0; ii < per_i; ++ii) put(iwp, iwp32, iw, iw32, h + ii * nbi + gi, h + gi * per_i + ii);
         }
+      // Half transforms (N >= 2^14): after the first forward stage (distance N/2, twiddle
+      // psi_1), the halves h = 0, 1 are independent (N/2)-point transforms whose stage-s
+      // twiddles are tw[2^s + h 2^(s-1) + j'] -> as a table of their own, T_h[2^(s-1) + j'],
+      // pass-ordered for logn - 1 like the tables above.
+      if (logn >= 14) {
+        const int lh = logn - 1, remh = lh & 3;
+        const int64_t nh = n / 2;
+        std::vector<std::pair<int, int>> ph;
+        if (remh) ph.push_back({0, remh});
+        for (int s0 = remh; s0 < lh; s0 += 4) ph.push_back({s0, 4});
+        auto* fwh = reinterpret_cast<uint64_t*>(base + 112 * n);
+        auto* fwh32 = reinterpret_cast<uint32_t*>(base + 128 * n);
+        auto* fwhd = reinterpret_cast<double*>(base + 136 * n);
+        for (int hh = 0; hh < 2; ++hh) {
+          std::vector<int64_t> th(static_cast<size_t>(nh), 0);  // T_h as indices into fw
+          for (int S = 1; S < logn; ++S)
+            for (int64_t jj = 0; jj < (int64_t(1) << (S - 1)); ++jj)
+              th[static_cast<size_t>((int64_t(1) << (S - 1)) + jj)] = (int64_t(1) << S) + hh * (int64_t(1) << (S - 1)) + jj;
+          std::vector<int64_t> perm(static_cast<size_t>(nh), 0);  // pass-ordered slot -> T_h slot
+          for (auto [s0, K] : ph)
+            for (int st = 0; st < K; ++st) {
+              const int64_t S = s0 + st, nb = int64_t(1) << s0, per_g = int64_t(1) << st;
+              for (int64_t g = 0; g < nb; ++g)
+                for (int64_t ii = 0; ii < per_g; ++ii)
+                  perm[static_cast<size_t>((int64_t(1) << S) + ii * nb + g)] = (int64_t(1) << S) + g * per_g + ii;
+            }
+          for (int64_t e = 1; e < nh; ++e) {
+            const int64_t src = th[static_cast<size_t>(perm[static_cast<size_t>(e)])];
+            const int64_t dst = hh * nh + e;
+            fwh[2 * dst] = fw[2 * src];
+            fwh[2 * dst + 1] = fw[2 * src + 1];
+            if (small) {
+              fwh32[2 * dst] = fw32[2 * src];
+              fwh32[2 * dst + 1] = fw32[2 * src + 1];
+            }
+            fwhd[dst] = static_cast<double>(fw[2 * src]);
+          }
+        }
+      }
       auto* fwpd = reinterpret_cast<double*>(base + 96 * n);
       auto* iwpd = reinterpret_cast<double*>(base + 104 * n);
       for (int64_t e = 0; e < n; ++e) {
@@ -370,6 +410,9 @@ Context::Context(const ContextParamsH& p, int device) : m_p(p), m_device(device)
     L.iwp32 = small ? reinterpret_cast<const uint2*>(dbase + 88 * n) : nullptr;
     L.fwpd = reinterpret_cast<const double*>(dbase + 96 * n);
     L.iwpd = reinterpret_cast<const double*>(dbase + 104 * n);
+    L.fwh = reinterpret_cast<const ulonglong2*>(dbase + 112 * n);
+    L.fwh32 = small ? reinterpret_cast<const uint2*>(dbase + 128 * n) : nullptr;
+    L.fwhd = reinterpret_cast<const double*>(dbase + 136 * n);
   }
   HG_CUDA(cudaMemcpy(m_tables.p, host.data(), host.size(), cudaMemcpyHostToDevice));
   for (int t = 0; t < nl; ++t)

@@ -45,15 +45,22 @@ struct Cta {
   const LimbInfo* L;
   W* s;
   const lz::TWT<W>* tw;
+  // half >= 0: a half transform of a 2^(LOGN+1)-point forward NTT (its own twiddle table)
   __device__ __forceinline__ Cta(uint64_t* smem, const LimbList& LL, int64_t rows, int G, const CtxParams& P,
-                                 bool inverse) {
-    limb = LL.limb[blockIdx.x % LL.count];
-    const int g = blockIdx.x / LL.count;
+                                 bool inverse, int bid = -1, int half = -1) {
+    if (bid < 0) bid = blockIdx.x;
+    limb = LL.limb[bid % LL.count];
+    const int g = bid / LL.count;
     r0 = g * G;
     r1 = (int)min((int64_t)(g + 1) * G, rows);
     L = &P.limb[limb];
     s = reinterpret_cast<W*>(smem);
     const lz::TWT<W>* src = inverse ? Lz<W>::inv_table(*L) : Lz<W>::fwd_table(*L);
+    if (half >= 0) {
+      if constexpr (std::is_floating_point_v<W>) src = L->fwhd + half * Cfg<W, LOGN>::N;
+      else if constexpr (sizeof(W) == 4) src = L->fwh32 + half * Cfg<W, LOGN>::N;
+      else src = L->fwh + half * Cfg<W, LOGN>::N;
+    }
     if constexpr (Cfg<W, LOGN>::TWS) {
       auto* t = reinterpret_cast<lz::TWT<W>*>(reinterpret_cast<uint8_t*>(smem) + Cfg<W, LOGN>::data_bytes);
       stage_tw(t, src, Cfg<W, LOGN>::N);
@@ -195,27 +202,30 @@ HG_KERNEL k_relin_c2_t(const uint64_t* __restrict__ a, const uint64_t* __restric
 //   64-bit limbs: key value + 64-bit Shoup constant; acc canonical
 // Epilogue adds d0 = a0 b0, d1 = a0 b1 + a1 b0 (or given d0, d1).
 // ---------------------------------------------------------------------------
-constexpr bool kPrefetchKeys = false;
-
 struct RelinC {
   int rows0[HG_MAX_LIMBS];
   int digits[HG_MAX_LIMBS];
   int64_t key_poly_words;  // (L+1) N
 };
 
-template <typename W, int LOGN>
+// SPLIT: LOGN is the half transform of a 2^(LOGN+1)-point ring (two CTAs per row, one per
+// half of the evaluations; the first forward stage is applied while reading the digits)
+template <typename W, int LOGN, bool SPLIT = false>
 struct RelinCfg {
-  static constexpr int threads = (1 << LOGN) / 16;
+  // thread vt owns evaluation groups vt + g threads (16 evaluations each), g < GPT
+  static constexpr int threads = (1 << LOGN) / 16 < 512 ? (1 << LOGN) / 16 : 512;
+  static constexpr int GPT = (1 << LOGN) / 16 / threads;
   static constexpr bool ACC_GLOBAL = sizeof(W) == 8 && LOGN >= 14;
   // stage each source residue of c2 once in shared memory (cp.async, prefetched
   // one residue ahead) instead of re-reading it from L2 for every digit
-  static constexpr bool C2S = Cfg<W, LOGN>::smem + ((size_t)8 << LOGN) <= kSmemCap;
+  static constexpr bool C2S = !SPLIT && Cfg<W, LOGN>::smem + ((size_t)8 << LOGN) <= kSmemCap;
   // 32-bit limbs: the digit's key row (b and a, Montgomery form, 4 bytes each) is
   // copied into shared memory with cp.async while the digit's NTT runs
   static constexpr size_t key_bytes = (size_t)8 << LOGN;
-  static constexpr bool KS = sizeof(W) == 4 && C2S &&
-                             Cfg<W, LOGN>::smem + ((size_t)8 << LOGN) + key_bytes <= kSmemCap;
+  static constexpr bool KS = sizeof(W) == 4 && (C2S || SPLIT) &&
+                             Cfg<W, LOGN>::smem + (C2S ? ((size_t)8 << LOGN) : 0) + key_bytes <= kSmemCap;
   static constexpr size_t smem = Cfg<W, LOGN>::smem + (C2S ? ((size_t)8 << LOGN) : 0) + (KS ? key_bytes : 0);
+  static constexpr size_t ks_off = Cfg<W, LOGN>::smem + (C2S ? ((size_t)8 << LOGN) : 0);
 };
 // conflict-free slot of 16-byte key chunk c (thread t reads chunks 4t .. 4t+3 with LDS.128)
 __device__ __forceinline__ int key_slot(int c) { return c ^ ((c >> 2) & 7); }
@@ -233,22 +243,24 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
-__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];\n" ::"l"(p)); }
 
-template <typename W, int LOGN, bool GIVEN_D>
-__global__ void __launch_bounds__(RelinCfg<W, LOGN>::threads, 1)
+template <typename W, int LOGN, bool GIVEN_D, bool SPLIT = false>
+__global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT>::threads, 1)
     k_relin_t(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int64_t a_stride, int64_t b_stride,
               const uint64_t* __restrict__ c2, const uint64_t* __restrict__ kval,
               const uint64_t* __restrict__ kpack, const uint32_t* __restrict__ kmont, uint64_t* __restrict__ out,
               int nl, int64_t items, int G, const RelinC K, const LimbList LL, const CtxParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
-  Cta<W, LOGN> c(smem, LL, items, G, P, false);
-  constexpr int n = 1 << LOGN;
-  constexpr bool AG = RelinCfg<W, LOGN>::ACC_GLOBAL;
-  constexpr bool C2S = RelinCfg<W, LOGN>::C2S;
-  constexpr bool KS = RelinCfg<W, LOGN>::KS;
+  const int half = SPLIT ? (int)(blockIdx.x & 1) : 0;
+  Cta<W, LOGN> c(smem, LL, items, G, P, false, SPLIT ? (int)(blockIdx.x >> 1) : -1, SPLIT ? half : -1);
+  constexpr int n = 1 << LOGN;                     // evaluations handled by this CTA
+  constexpr int nfull = SPLIT ? 2 * n : n;          // ring degree
+  constexpr bool AG = RelinCfg<W, LOGN, SPLIT>::ACC_GLOBAL;
+  constexpr bool C2S = RelinCfg<W, LOGN, SPLIT>::C2S;
+  constexpr bool KS = RelinCfg<W, LOGN, SPLIT>::KS;
   uint64_t* c2s = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(smem) + Cfg<W, LOGN>::smem);
-  uint4* ks = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(smem) + Cfg<W, LOGN>::smem + ((size_t)8 << LOGN));
+  uint4* ks = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(smem) + RelinCfg<W, LOGN, SPLIT>::ks_off);
+  const int64_t hoff = (int64_t)half * n;           // this CTA's evaluation offset
   (void)ks;
   (void)kmont;
   auto stage_c2 = [&](const uint64_t* gsrc) {
@@ -260,24 +272,37 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN>::threads, 1)
   const int j = c.limb;
   const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
   const uint64_t Q = c.L->q;
-  const int64_t pw = (int64_t)nl * n;
-  const int vt = threadIdx.x;
-  const int k0 = vt << 4;
+  const int64_t pw = (int64_t)nl * nfull;
+  constexpr int GPT = RelinCfg<W, LOGN, SPLIT>::GPT;
+  // SPLIT: the first forward stage, x_k +/- psi_1 x_{k+N/2}, fused into the digit read
+  using TWW = lz::TWT<W>;
+  TWW psi1{};
+  if constexpr (SPLIT) {
+    if constexpr (std::is_floating_point_v<W>) psi1 = (double)c.L->fw[1].x;
+    else if constexpr (sizeof(W) == 4) psi1 = c.L->fw32[1];
+    else psi1 = c.L->fw[1];
+  }
+  (void)psi1;
   const uint32_t qneg = neg_qinv32((uint32_t)Q);
   (void)qneg;
   for (int item = c.r0; item < c.r1; ++item) {
-    W acc0[16], acc1[16];
+    W acc0[GPT][16], acc1[GPT][16];
 #pragma unroll
-    for (int r = 0; r < 16; ++r) { acc0[r] = 0; acc1[r] = 0; }
-    uint64_t* o0 = out + (int64_t)item * 2 * pw + (int64_t)j * n + k0;
-    uint64_t* o1 = o0 + pw;
+    for (int gi = 0; gi < GPT; ++gi)
+#pragma unroll
+      for (int r = 0; r < 16; ++r) { acc0[gi][r] = 0; acc1[gi][r] = 0; }
+    uint64_t* const obase = out + (int64_t)item * 2 * pw + (int64_t)j * nfull + hoff;
     if constexpr (AG) {
 #pragma unroll
-      for (int r = 0; r < 16; ++r) { o0[r] = 0; o1[r] = 0; }
+      for (int gi = 0; gi < GPT; ++gi) {
+        uint64_t* o0 = obase + ((threadIdx.x + gi * blockDim.x) << 4);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) { o0[r] = 0; o0[pw + r] = 0; }
+      }
     }
     const uint64_t* c2item = c2 + (int64_t)item * pw;
     for (int i = 0; i < nl; ++i) {
-      const uint64_t* src = c2item + (int64_t)i * n;
+      const uint64_t* src = c2item + (int64_t)i * nfull;
       if constexpr (C2S) {
         if (item == c.r0 && i == 0) stage_c2(src);  // first residue of the group: nothing prefetched yet
         cp_async_wait_all();
@@ -289,23 +314,15 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN>::threads, 1)
         bool c2_staged = false;
         if constexpr (KS) {
           // this digit's key row (b then a) -> shared memory, behind the NTT below
-          const uint4* kb = reinterpret_cast<const uint4*>(kmont + (int64_t)row * 2 * K.key_poly_words + (int64_t)j * n);
-          const uint4* ka = reinterpret_cast<const uint4*>(kmont + ((int64_t)row * 2 + 1) * K.key_poly_words + (int64_t)j * n);
+          const uint4* kb = reinterpret_cast<const uint4*>(kmont + (int64_t)row * 2 * K.key_poly_words + (int64_t)j * nfull + hoff);
+          const uint4* ka = reinterpret_cast<const uint4*>(kmont + ((int64_t)row * 2 + 1) * K.key_poly_words + (int64_t)j * nfull + hoff);
           for (int ch = threadIdx.x; ch < n / 4; ch += blockDim.x) {
             cp_async16(ks + key_slot(ch), kb + ch);
             cp_async16(ks + n / 4 + key_slot(ch), ka + ch);
           }
           cp_async_commit();
         }
-        const int64_t kof = (int64_t)row * 2 * K.key_poly_words + (int64_t)j * n + k0;
-        if (kPrefetchKeys) {
-          prefetch_l1(kpack + kof);  // this thread's key lines for the MAC below
-          prefetch_l1(kpack + kof + K.key_poly_words);
-          if constexpr (sizeof(W) == 8) {
-            prefetch_l1(kval + kof);
-            prefetch_l1(kval + kof + K.key_poly_words);
-          }
-        }
+
         // digit (c2_i >> 15d) & 0x7FFF (ckks_backend.hpp:520-521), extracted inside the first NTT pass
         if constexpr (C2S) {
           lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return (W)(uint32_t)((c2s[k] >> sh) & 0x7FFF); }, c.tw, q, q2);
@@ -313,6 +330,14 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN>::threads, 1)
             if (i + 1 < nl) { stage_c2(src + n); c2_staged = true; }
             else if (item + 1 < c.r1) { stage_c2(c2 + (int64_t)(item + 1) * pw); c2_staged = true; }
           }
+        } else if constexpr (SPLIT) {
+          lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
+            const W x0 = (W)(uint32_t)((__ldg(src + k) >> sh) & 0x7FFF);
+            W x1 = (W)(uint32_t)((__ldg(src + k + n) >> sh) & 0x7FFF);
+            W x0b = x0;
+            ct_lz<W>(x0b, x1, psi1, q, q2);  // (x0 + psi x1, x0 - psi x1), lazy
+            return half ? x1 : x0b;
+          }, c.tw, q, q2);
         } else {
           lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return (W)(uint32_t)((__ldg(src + k) >> sh) & 0x7FFF); }, c.tw, q, q2);
         }
@@ -326,87 +351,95 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN>::threads, 1)
           lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2);
         }
         (void)c2_staged;
-        W x[16];
-        lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, x);
-        const int64_t koff = (int64_t)row * 2 * K.key_poly_words + (int64_t)j * n + k0;
-        if constexpr (KS) {
-          // Montgomery MAC: U = (x km + m q) / 2^32 with m = -(x km) q^{-1} mod 2^32; x < 4q < 2^32,
-          // km < q, so U < 2q and U = x w mod q
-          const uint32_t q32 = (uint32_t)Q, q232 = q32 + q32;
 #pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            const uint4 vb = ks[key_slot(4 * vt + h)], va = ks[n / 4 + key_slot(4 * vt + h)];
-            const uint32_t kb_[4] = {vb.x, vb.y, vb.z, vb.w}, ka_[4] = {va.x, va.y, va.z, va.w};
+        for (int gi = 0; gi < GPT; ++gi) {
+          const int vt = threadIdx.x + gi * blockDim.x, k0 = vt << 4;
+          uint64_t* o0 = obase + k0;
+          uint64_t* o1 = o0 + pw;
+          (void)o0;
+          (void)o1;
+          W x[16];
+          lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, x);
+          const int64_t koff = (int64_t)row * 2 * K.key_poly_words + (int64_t)j * nfull + hoff + k0;
+          if constexpr (KS) {
+            // Montgomery MAC: U = (x km + m q) / 2^32 with m = -(x km) q^{-1} mod 2^32; x < 4q < 2^32,
+            // km < q, so U < 2q and U = x w mod q
+            const uint32_t q32 = (uint32_t)Q, q232 = q32 + q32;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const uint32_t xv = (uint32_t)x[4 * h + e];
-              const uint64_t tb = (uint64_t)xv * kb_[e], ta = (uint64_t)xv * ka_[e];
-              const uint32_t ub = (uint32_t)((tb + (uint64_t)((uint32_t)tb * qneg) * q32) >> 32);
-              const uint32_t ua = (uint32_t)((ta + (uint64_t)((uint32_t)ta * qneg) * q32) >> 32);
-              const uint32_t s0 = (uint32_t)acc0[4 * h + e] + ub, s1 = (uint32_t)acc1[4 * h + e] + ua;
-              acc0[4 * h + e] = (W)min(s0, s0 - q232);
-              acc1[4 * h + e] = (W)min(s1, s1 - q232);
-            }
-          }
-        } else if constexpr (std::is_floating_point_v<W>) {
-          // fp64 lane: exact FMA modmul of the lazy evaluation by the key word, reduced sum
-          const ulonglong2* kb2 = reinterpret_cast<const ulonglong2*>(kval + koff);
-          const ulonglong2* ka2 = reinterpret_cast<const ulonglong2*>(kval + koff + K.key_poly_words);
-          double* od0 = reinterpret_cast<double*>(o0);
-          double* od1 = reinterpret_cast<double*>(o1);
+            for (int h = 0; h < 4; ++h) {
+              const uint4 vb = ks[key_slot(4 * vt + h)], va = ks[n / 4 + key_slot(4 * vt + h)];
+              const uint32_t kb_[4] = {vb.x, vb.y, vb.z, vb.w}, ka_[4] = {va.x, va.y, va.z, va.w};
 #pragma unroll
-          for (int h = 0; h < 8; ++h) {
-            const ulonglong2 vb = __ldg(kb2 + h), va = __ldg(ka2 + h);
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const double t0 = mulmod_f64(x[2 * h + e], (double)(e ? vb.y : vb.x), q, q2);
-              const double t1 = mulmod_f64(x[2 * h + e], (double)(e ? va.y : va.x), q, q2);
-              if constexpr (AG) {
-                od0[2 * h + e] = reduce_f64(__dadd_rn(od0[2 * h + e], t0), q, q2);
-                od1[2 * h + e] = reduce_f64(__dadd_rn(od1[2 * h + e], t1), q, q2);
-              } else {
-                acc0[2 * h + e] = reduce_f64(__dadd_rn(acc0[2 * h + e], t0), q, q2);
-                acc1[2 * h + e] = reduce_f64(__dadd_rn(acc1[2 * h + e], t1), q, q2);
+              for (int e = 0; e < 4; ++e) {
+                const uint32_t xv = (uint32_t)x[4 * h + e];
+                const uint64_t tb = (uint64_t)xv * kb_[e], ta = (uint64_t)xv * ka_[e];
+                const uint32_t ub = (uint32_t)((tb + (uint64_t)((uint32_t)tb * qneg) * q32) >> 32);
+                const uint32_t ua = (uint32_t)((ta + (uint64_t)((uint32_t)ta * qneg) * q32) >> 32);
+                const uint32_t s0 = (uint32_t)acc0[gi][4 * h + e] + ub, s1 = (uint32_t)acc1[gi][4 * h + e] + ua;
+                acc0[gi][4 * h + e] = (W)min(s0, s0 - q232);
+                acc1[gi][4 * h + e] = (W)min(s1, s1 - q232);
               }
             }
-          }
-        } else if constexpr (sizeof(W) == 4) {
-          const ulonglong2* kb2 = reinterpret_cast<const ulonglong2*>(kpack + koff);
-          const ulonglong2* ka2 = reinterpret_cast<const ulonglong2*>(kpack + koff + K.key_poly_words);
-          const uint32_t q32 = (uint32_t)Q, q232 = q32 + q32;
+          } else if constexpr (std::is_floating_point_v<W>) {
+            // fp64 lane: exact FMA modmul of the lazy evaluation by the key word, reduced sum
+            const ulonglong2* kb2 = reinterpret_cast<const ulonglong2*>(kval + koff);
+            const ulonglong2* ka2 = reinterpret_cast<const ulonglong2*>(kval + koff + K.key_poly_words);
+            double* od0 = reinterpret_cast<double*>(o0);
+            double* od1 = reinterpret_cast<double*>(o1);
 #pragma unroll
-          for (int h = 0; h < 8; ++h) {
-            const ulonglong2 vb = __ldg(kb2 + h), va = __ldg(ka2 + h);
+            for (int h = 0; h < 8; ++h) {
+              const ulonglong2 vb = __ldg(kb2 + h), va = __ldg(ka2 + h);
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const uint64_t pb = e ? vb.y : vb.x, pa = e ? va.y : va.x;
-              const uint32_t xv = (uint32_t)x[2 * h + e];
-              const uint32_t t0 = xv * (uint32_t)pb - __umulhi(xv, (uint32_t)(pb >> 32)) * q32;
-              const uint32_t t1 = xv * (uint32_t)pa - __umulhi(xv, (uint32_t)(pa >> 32)) * q32;
-              const uint32_t s0 = (uint32_t)acc0[2 * h + e] + t0, s1 = (uint32_t)acc1[2 * h + e] + t1;
-              acc0[2 * h + e] = (W)min(s0, s0 - q232);
-              acc1[2 * h + e] = (W)min(s1, s1 - q232);
+              for (int e = 0; e < 2; ++e) {
+                const double t0 = mulmod_f64(x[2 * h + e], (double)(e ? vb.y : vb.x), q, q2);
+                const double t1 = mulmod_f64(x[2 * h + e], (double)(e ? va.y : va.x), q, q2);
+                if constexpr (AG) {
+                  od0[2 * h + e] = reduce_f64(__dadd_rn(od0[2 * h + e], t0), q, q2);
+                  od1[2 * h + e] = reduce_f64(__dadd_rn(od1[2 * h + e], t1), q, q2);
+                } else {
+                  acc0[gi][2 * h + e] = reduce_f64(__dadd_rn(acc0[gi][2 * h + e], t0), q, q2);
+                  acc1[gi][2 * h + e] = reduce_f64(__dadd_rn(acc1[gi][2 * h + e], t1), q, q2);
+                }
+              }
             }
-          }
-        } else {
-          const ulonglong2* kb2 = reinterpret_cast<const ulonglong2*>(kval + koff);
-          const ulonglong2* ka2 = reinterpret_cast<const ulonglong2*>(kval + koff + K.key_poly_words);
-          const ulonglong2* sb2 = reinterpret_cast<const ulonglong2*>(kpack + koff);
-          const ulonglong2* sa2 = reinterpret_cast<const ulonglong2*>(kpack + koff + K.key_poly_words);
+          } else if constexpr (sizeof(W) == 4) {
+            const ulonglong2* kb2 = reinterpret_cast<const ulonglong2*>(kpack + koff);
+            const ulonglong2* ka2 = reinterpret_cast<const ulonglong2*>(kpack + koff + K.key_poly_words);
+            const uint32_t q32 = (uint32_t)Q, q232 = q32 + q32;
 #pragma unroll
-          for (int h = 0; h < 8; ++h) {
-            const ulonglong2 vb = __ldg(kb2 + h), va = __ldg(ka2 + h), wb = __ldg(sb2 + h), wa = __ldg(sa2 + h);
+            for (int h = 0; h < 8; ++h) {
+              const ulonglong2 vb = __ldg(kb2 + h), va = __ldg(ka2 + h);
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const uint64_t xv = canon4<uint64_t>((uint64_t)x[2 * h + e], Q, Q + Q);
-              const uint64_t t0 = mul_shoup64(xv, e ? vb.y : vb.x, e ? wb.y : wb.x, Q);
-              const uint64_t t1 = mul_shoup64(xv, e ? va.y : va.x, e ? wa.y : wa.x, Q);
-              if constexpr (AG) {
-                o0[2 * h + e] = add_mod(o0[2 * h + e], t0, Q);
-                o1[2 * h + e] = add_mod(o1[2 * h + e], t1, Q);
-              } else {
-                acc0[2 * h + e] = (W)add_mod((uint64_t)acc0[2 * h + e], t0, Q);
-                acc1[2 * h + e] = (W)add_mod((uint64_t)acc1[2 * h + e], t1, Q);
+              for (int e = 0; e < 2; ++e) {
+                const uint64_t pb = e ? vb.y : vb.x, pa = e ? va.y : va.x;
+                const uint32_t xv = (uint32_t)x[2 * h + e];
+                const uint32_t t0 = xv * (uint32_t)pb - __umulhi(xv, (uint32_t)(pb >> 32)) * q32;
+                const uint32_t t1 = xv * (uint32_t)pa - __umulhi(xv, (uint32_t)(pa >> 32)) * q32;
+                const uint32_t s0 = (uint32_t)acc0[gi][2 * h + e] + t0, s1 = (uint32_t)acc1[gi][2 * h + e] + t1;
+                acc0[gi][2 * h + e] = (W)min(s0, s0 - q232);
+                acc1[gi][2 * h + e] = (W)min(s1, s1 - q232);
+              }
+            }
+          } else {
+            const ulonglong2* kb2 = reinterpret_cast<const ulonglong2*>(kval + koff);
+            const ulonglong2* ka2 = reinterpret_cast<const ulonglong2*>(kval + koff + K.key_poly_words);
+            const ulonglong2* sb2 = reinterpret_cast<const ulonglong2*>(kpack + koff);
+            const ulonglong2* sa2 = reinterpret_cast<const ulonglong2*>(kpack + koff + K.key_poly_words);
+#pragma unroll
+            for (int h = 0; h < 8; ++h) {
+              const ulonglong2 vb = __ldg(kb2 + h), va = __ldg(ka2 + h), wb = __ldg(sb2 + h), wa = __ldg(sa2 + h);
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const uint64_t xv = canon4<uint64_t>((uint64_t)x[2 * h + e], Q, Q + Q);
+                const uint64_t t0 = mul_shoup64(xv, e ? vb.y : vb.x, e ? wb.y : wb.x, Q);
+                const uint64_t t1 = mul_shoup64(xv, e ? va.y : va.x, e ? wa.y : wa.x, Q);
+                if constexpr (AG) {
+                  o0[2 * h + e] = add_mod(o0[2 * h + e], t0, Q);
+                  o1[2 * h + e] = add_mod(o1[2 * h + e], t1, Q);
+                } else {
+                  acc0[gi][2 * h + e] = (W)add_mod((uint64_t)acc0[gi][2 * h + e], t0, Q);
+                  acc1[gi][2 * h + e] = (W)add_mod((uint64_t)acc1[gi][2 * h + e], t1, Q);
+                }
               }
             }
           }
@@ -415,39 +448,45 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN>::threads, 1)
       }
     }
     // epilogue: + d0, d1; canonical store
-    const uint64_t* p0 = a + (int64_t)item * a_stride + (int64_t)j * n + k0;
-    const uint64_t* p1 = p0 + pw;
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      uint64_t r0, r1;
-      if constexpr (std::is_floating_point_v<W>) {
-        const double a0 = AG ? reinterpret_cast<const double*>(o0)[r] : (double)acc0[r];
-        const double a1 = AG ? reinterpret_cast<const double*>(o1)[r] : (double)acc1[r];
-        r0 = (uint64_t)canon_f64(a0, q, q2);
-        r1 = (uint64_t)canon_f64(a1, q, q2);
-      } else if constexpr (AG) {
-        r0 = o0[r];
-        r1 = o1[r];
-      } else {
-        r0 = (uint64_t)acc0[r];
-        r1 = (uint64_t)acc1[r];
-        if constexpr (sizeof(W) == 4) {
-          r0 = r0 >= Q ? r0 - Q : r0;
-          r1 = r1 >= Q ? r1 - Q : r1;
+    for (int gi = 0; gi < GPT; ++gi) {
+      const int k0 = (threadIdx.x + gi * blockDim.x) << 4;
+      uint64_t* o0 = obase + k0;
+      uint64_t* o1 = o0 + pw;
+      const uint64_t* p0 = a + (int64_t)item * a_stride + (int64_t)j * nfull + hoff + k0;
+      const uint64_t* p1 = p0 + pw;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        uint64_t r0, r1;
+        if constexpr (std::is_floating_point_v<W>) {
+          const double a0 = AG ? reinterpret_cast<const double*>(o0)[r] : (double)acc0[gi][r];
+          const double a1 = AG ? reinterpret_cast<const double*>(o1)[r] : (double)acc1[gi][r];
+          r0 = (uint64_t)canon_f64(a0, q, q2);
+          r1 = (uint64_t)canon_f64(a1, q, q2);
+        } else if constexpr (AG) {
+          r0 = o0[r];
+          r1 = o1[r];
+        } else {
+          r0 = (uint64_t)acc0[gi][r];
+          r1 = (uint64_t)acc1[gi][r];
+          if constexpr (sizeof(W) == 4) {
+            r0 = r0 >= Q ? r0 - Q : r0;
+            r1 = r1 >= Q ? r1 - Q : r1;
+          }
         }
+        uint64_t d0, d1;
+        if constexpr (GIVEN_D) {
+          d0 = p0[r];
+          d1 = p1[r];
+        } else {
+          const uint64_t* q0 = b + (int64_t)item * b_stride + (int64_t)j * nfull + hoff + k0;
+          const uint64_t x0 = p0[r], x1 = p1[r], y0 = q0[r], y1 = q0[pw + r];
+          d0 = mul_mod(x0, y0, *c.L);
+          d1 = add_mod(mul_mod(x0, y1, *c.L), mul_mod(x1, y0, *c.L), Q);
+        }
+        o0[r] = add_mod(r0, d0, Q);
+        o1[r] = add_mod(r1, d1, Q);
       }
-      uint64_t d0, d1;
-      if constexpr (GIVEN_D) {
-        d0 = p0[r];
-        d1 = p1[r];
-      } else {
-        const uint64_t* q0 = b + (int64_t)item * b_stride + (int64_t)j * n + k0;
-        const uint64_t x0 = p0[r], x1 = p1[r], y0 = q0[r], y1 = q0[pw + r];
-        d0 = mul_mod(x0, y0, *c.L);
-        d1 = add_mod(mul_mod(x0, y1, *c.L), mul_mod(x1, y0, *c.L), Q);
-      }
-      o0[r] = add_mod(r0, d0, Q);
-      o1[r] = add_mod(r1, d1, Q);
     }
   }
 }
@@ -901,28 +940,30 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
     if (LL.count == 0) return;
     by_logn<W>(c, [&]<typename W_, int LOGN>() {
       if constexpr (LOGN <= 14) {
-        using Cf = RelinCfg<W_, LOGN>;
-        const int threads = RelinCfg<W_, LOGN>::threads;
+        // 2^14: two CTAs per row, one per half of the evaluations (2^13-point half transforms)
+        constexpr bool SPLIT = LOGN == 14 && !std::is_same_v<W_, uint64_t>;
+        constexpr int LT = SPLIT ? LOGN - 1 : LOGN;
+        using Cf = RelinCfg<W_, LT, SPLIT>;
+        const int threads = Cf::threads;
         const int64_t target = 148LL * 3;
-        const int G = (int)std::max<int64_t>(1, std::min<int64_t>(16, (items * LL.count + target - 1) / target));
-        const unsigned grid = (unsigned)(LL.count * ((items + G - 1) / G));
-        const void* fn = given_d ? (const void*)k_relin_t<W_, LOGN, true> : (const void*)k_relin_t<W_, LOGN, false>;
+        const int halves = SPLIT ? 2 : 1;
+        const int G = (int)std::max<int64_t>(
+            1, std::min<int64_t>(16, (items * LL.count * halves + target - 1) / target));
+        const unsigned grid = (unsigned)(LL.count * ((items + G - 1) / G) * halves);
+        const void* fn =
+            given_d ? (const void*)k_relin_t<W_, LT, true, SPLIT> : (const void*)k_relin_t<W_, LT, false, SPLIT>;
         set_smem_attr(fn, Cf::smem);
         const double frac = (double)LL.count / nl;
         c.kt_begin(std::is_floating_point_v<W_> ? "k_relin_t/f64" : sizeof(W_) == 4 ? "k_relin_t/u32" : "k_relin_t/u64", s, frac * (items * pw8 * 7 + (double)sd * 2 * pw8),
                    (double)items * LL.count * (sd * (bfly(c) + 2.0 * c.n()) + 3.0 * c.n()));
         if (given_d)
-          k_relin_t<W_, LOGN, true><<<grid, threads, Cf::smem, s>>>(a, b, a_stride, b_stride, c2,
-                                                                    keys.relin.as<uint64_t>(),
-                                                                    keys.relin_pack.as<uint64_t>(),
-                                                                    keys.relin_mont.as<uint32_t>(), out, nl, items, G,
-                                                                    K, LL, c.kp());
+          k_relin_t<W_, LT, true, SPLIT><<<grid, threads, Cf::smem, s>>>(
+              a, b, a_stride, b_stride, c2, keys.relin.as<uint64_t>(), keys.relin_pack.as<uint64_t>(),
+              keys.relin_mont.as<uint32_t>(), out, nl, items, G, K, LL, c.kp());
         else
-          k_relin_t<W_, LOGN, false><<<grid, threads, Cf::smem, s>>>(a, b, a_stride, b_stride, c2,
-                                                                     keys.relin.as<uint64_t>(),
-                                                                     keys.relin_pack.as<uint64_t>(),
-                                                                     keys.relin_mont.as<uint32_t>(), out, nl, items,
-                                                                     G, K, LL, c.kp());
+          k_relin_t<W_, LT, false, SPLIT><<<grid, threads, Cf::smem, s>>>(
+              a, b, a_stride, b_stride, c2, keys.relin.as<uint64_t>(), keys.relin_pack.as<uint64_t>(),
+              keys.relin_mont.as<uint32_t>(), out, nl, items, G, K, LL, c.kp());
         c.kt_end(s);
         HG_CUDA(cudaGetLastError());
       }
