@@ -171,6 +171,55 @@ HG_KERNEL k_rescale_rest_t(const uint64_t* __restrict__ in, const int64_t* __res
   }
 }
 
+// the first forward stage's twiddle psi_1 (pass-ordered index 1) in the lane's format
+template <typename W>
+__device__ __forceinline__ lz::TWT<W> first_twiddle(const LimbInfo& L) {
+  if constexpr (std::is_floating_point_v<W>) return (double)L.fw[1].x;
+  else if constexpr (sizeof(W) == 4) return L.fw32[1];
+  else return L.fw[1];
+}
+
+// rescale step 2 for N = 2^(LOGN+1): two CTAs per row, one per half of the evaluations;
+// the first forward stage is applied while lifting c (as in the split key switch)
+template <typename W, int LOGN>
+__global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_blocks)
+    k_rescale_rest_s(const uint64_t* __restrict__ in, const int64_t* __restrict__ cen, uint64_t* __restrict__ out,
+                     int nl, int64_t polys, int G, const LimbList LL, const RescaleC R, const CtxParams P) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  const int half = (int)(blockIdx.x & 1);
+  Cta<W, LOGN> c(smem, LL, polys, G, P, false, (int)(blockIdx.x >> 1), half);
+  constexpr int n = 1 << LOGN, nfull = 2 * n;
+  const int t = nl - 1, j = c.limb;
+  const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
+  const uint64_t Q = c.L->q, inv = R.inv[j], inv_s = R.inv_s[j];
+  const lz::TWT<W> psi1 = first_twiddle<W>(*c.L);
+  for (int r = c.r0; r < c.r1; ++r) {
+    const int64_t* cv = cen + (int64_t)r * nfull;
+    lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
+      W x0 = (W)lift_signed(__ldg(cv + k), Q), x1 = (W)lift_signed(__ldg(cv + k + n), Q);
+      ct_lz<W>(x0, x1, psi1, q, q2);
+      return half ? x1 : x0;
+    }, c.tw, q, q2);
+    lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2);
+    const uint64_t* x = in + ((int64_t)r * nl + j) * nfull + (int64_t)half * n;
+    uint64_t* o = out + ((int64_t)r * t + j) * nfull + (int64_t)half * n;
+    for (int vt = threadIdx.x; vt < (n >> 4); vt += blockDim.x) {
+      W y[16];
+      lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, y);
+      const ulonglong2* x2 = reinterpret_cast<const ulonglong2*>(x + (vt << 4));
+      ulonglong2* o2 = reinterpret_cast<ulonglong2*>(o + (vt << 4));
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        const ulonglong2 xv = x2[h];
+        const uint64_t c0 = canon4<W>(y[2 * h], q, q2), c1 = canon4<W>(y[2 * h + 1], q, q2);
+        o2[h] = make_ulonglong2(mul_shoup64(sub_mod(xv.x, c0, Q), inv, inv_s, Q),
+                                mul_shoup64(sub_mod(xv.y, c1, Q), inv, inv_s, Q));
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // relinearisation prologue: c2 = INTT(a1 * b1) per (item, limb i)  (ckks_backend.hpp:509)
 HG_KERNEL k_relin_c2_t(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int64_t a_stride,
                        int64_t b_stride, int64_t a1_off, int64_t b1_off, uint64_t* __restrict__ c2, int nl,
@@ -894,6 +943,22 @@ void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys,
     using W = decltype(wtag);
     if (LL.count == 0) return;
     by_logn<W>(c, [&]<typename W_, int LOGN>() {
+      if constexpr (LOGN == 14 && std::is_same_v<W_, uint32_t>) {
+        // two CTAs per row, one per half of the evaluations (measured: helps the 32-bit
+        // lane, whose 2^14 tables crowd shared memory; the fp64 lane is faster unsplit)
+        using Cf = Cfg<W_, LOGN - 1>;
+        unsigned grid;
+        int G;
+        grid_for<W_, LOGN - 1>(LL, polys, grid, G);
+        set_smem_attr((const void*)k_rescale_rest_s<W_, LOGN - 1>, Cf::smem);
+        c.kt_begin("k_rescale_rest_t/u32", s, (double)polys * LL.count * 3 * nw,
+                   (double)polys * LL.count * (bfly(c) + c.n()));
+        k_rescale_rest_s<W_, LOGN - 1><<<grid * 2, Cf::threads, Cf::smem, s>>>(in, cen, out, nl, polys, G, LL, R,
+                                                                             c.kp());
+        c.kt_end(s);
+        HG_CUDA(cudaGetLastError());
+        return;
+      }
       using Cf = Cfg<W_, LOGN>;
       unsigned grid;
       int G;
