@@ -285,6 +285,7 @@ GOLDEN_NETS = {
     "c1": _spec("c1", 4096),
     "c3_n2048": _spec("c3", 64, n=2048),
     "c5_n2048": _spec("c5", 64, n=2048),
+    "c4_n2048": _spec("c4", 32, n=2048),
     "c3": _spec("c3", 4096),
     "c5": _spec("c5", 8192),
 }
