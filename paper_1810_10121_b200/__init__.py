@@ -15,7 +15,7 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhegpu.so")
+LIB_PATH = os.environ.get("HG_LIBHEGPU") or os.path.join(_HERE, "libhegpu.so")
 
 HG_ERRORS = {1: "validation", 2: "parse", 3: "depth_exceeded", 4: "capacity", 5: "io", 6: "internal", 7: "cuda"}
 

@@ -153,6 +153,15 @@ __device__ __forceinline__ uint64_t lift_signed(int64_t v, uint64_t q) {
   if (r < 0) r += (int64_t)q;
   return (uint64_t)r;
 }
+// lift_signed (poly.hpp:63-67) by Barrett reduction instead of a 64-bit division.  For an
+// arbitrary 64-bit input (not a product < q^2) the Barrett quotient can be 2 short, so
+// reduce128's single correction is followed by a second one.
+__device__ __forceinline__ uint64_t lift_signed(int64_t v, const LimbInfo& L) {
+  const uint64_t a = v < 0 ? (uint64_t)(-v) : (uint64_t)v;
+  uint64_t r = reduce128(a, 0, L);
+  r = r >= L.q ? r - L.q : r;
+  return (v < 0 && r != 0) ? L.q - r : r;
+}
 
 #endif  // __CUDACC__
 

@@ -74,12 +74,12 @@ __global__ void __launch_bounds__(kNttThreads) k_lift_ntt(const int64_t* __restr
   uint64_t* o = out + (int64_t)blockIdx.x * P.n;
   if (L.small) {
     uint32_t* s = reinterpret_cast<uint32_t*>(smem);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) s[swz<uint32_t>(i)] = (uint32_t)lift_signed(g[i], L.q);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s[swz<uint32_t>(i)] = (uint32_t)lift_signed(g[i], L);
     __syncthreads();
     ntt_forward_smem(s, L, P.logn);
     store_limb(o, s, n);
   } else {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) smem[swz<uint64_t>(i)] = lift_signed(g[i], L.q);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) smem[swz<uint64_t>(i)] = lift_signed(g[i], L);
     __syncthreads();
     ntt_forward_smem(smem, L, P.logn);
     store_limb(o, smem, n);
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kNttThreads) k_rescale_rest(const uint64_t* __
   const uint64_t inv = R.inv[j], inv_s = R.inv_s[j];
   if (L.small) {
     uint32_t* s = reinterpret_cast<uint32_t*>(smem);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) s[swz<uint32_t>(i)] = (uint32_t)lift_signed(c[i], L.q);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s[swz<uint32_t>(i)] = (uint32_t)lift_signed(c[i], L);
     __syncthreads();
     ntt_forward_smem(s, L, P.logn);
     const uint32_t q = (uint32_t)L.q, w = (uint32_t)inv, ws = (uint32_t)(inv_s >> 32);
@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kNttThreads) k_rescale_rest(const uint64_t* __
       o[i] = mul_shoup32(d, w, ws, q);
     }
   } else {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) smem[swz<uint64_t>(i)] = lift_signed(c[i], L.q);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) smem[swz<uint64_t>(i)] = lift_signed(c[i], L);
     __syncthreads();
     ntt_forward_smem(smem, L, P.logn);
     for (int i = threadIdx.x; i < n; i += blockDim.x) {

@@ -65,6 +65,7 @@ struct Cta {
       auto* t = reinterpret_cast<lz::TWT<W>*>(reinterpret_cast<uint8_t*>(smem) + Cfg<W, LOGN>::data_bytes);
       stage_tw(t, src, Cfg<W, LOGN>::N);
       tw = t;
+      __syncthreads();  // kernels may start with a fused first pass that reads twiddles at once
     } else {
       tw = src;
     }
@@ -103,7 +104,7 @@ HG_KERNEL k_lift_ntt_t(const int64_t* __restrict__ src, uint64_t* __restrict__ o
   const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
   for (int r = c.r0; r < c.r1; ++r) {
     const int64_t* g = src + (int64_t)r * n;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) c.s[lz::padw<W>(i)] = (W)lift_signed(g[i], c.L->q);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) c.s[lz::padw<W>(i)] = (W)lift_signed(g[i], *c.L);
     __syncthreads();
     lz::fwd<W, LOGN>(c.s, c.tw, q, q2);
     lz::store<W, LOGN>(out + ((int64_t)r * nl + c.limb) * n, c.s);
@@ -149,9 +150,8 @@ HG_KERNEL k_rescale_rest_t(const uint64_t* __restrict__ in, const int64_t* __res
   const uint64_t Q = c.L->q, inv = R.inv[j], inv_s = R.inv_s[j];
   for (int r = c.r0; r < c.r1; ++r) {
     const int64_t* cv = cen + (int64_t)r * n;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) c.s[lz::padw<W>(i)] = (W)lift_signed(cv[i], Q);
-    __syncthreads();
-    lz::fwd_but_last<W, LOGN>(c.s, c.tw, q, q2);
+    lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return (W)lift_signed(__ldg(cv + k), *c.L); }, c.tw, q, q2);
+    lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2);
     const uint64_t* x = in + ((int64_t)r * nl + j) * n;
     uint64_t* o = out + ((int64_t)r * t + j) * n;
     for (int vt = threadIdx.x; vt < (n >> 4); vt += blockDim.x) {
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_block
   for (int r = c.r0; r < c.r1; ++r) {
     const int64_t* cv = cen + (int64_t)r * nfull;
     lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
-      W x0 = (W)lift_signed(__ldg(cv + k), Q), x1 = (W)lift_signed(__ldg(cv + k + n), Q);
+      W x0 = (W)lift_signed(__ldg(cv + k), *c.L), x1 = (W)lift_signed(__ldg(cv + k + n), *c.L);
       ct_lz<W>(x0, x1, psi1, q, q2);
       return half ? x1 : x0;
     }, c.tw, q, q2);
