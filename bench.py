@@ -270,13 +270,21 @@ def ours_arm(args):
         logits = plan.output("logits")
     barrier()
     torch.cuda.synchronize()
+    # pipelined: the host decode of step i (hg_plan_output_async) overlaps step i+1's GPU work;
+    # every step still does its own H2D, encode, encrypt, graph, decrypt, D2H and decode
     t1 = time.perf_counter()
     e2e_marks = []
+    pending = None
     for _ in range(args.steps):
         plan.bind_input("x", x_host)
         plan.run()
-        logits = plan.output("logits")
+        ticket = plan.output_async("logits")
+        if pending is not None:
+            logits = pending.wait()
+        pending = ticket
         e2e_marks.append(time.perf_counter())
+    logits = pending.wait()
+    e2e_marks[-1] = time.perf_counter()
     torch.cuda.synchronize()
     e2e_s = (time.perf_counter() - t1) / args.steps
     e2e_steps_ms = [1e3 * (b - a) for a, b in zip([t1] + e2e_marks[:-1], e2e_marks)]

@@ -40,6 +40,7 @@ extern "C" {
 typedef struct hg_context hg_context;
 typedef struct hg_keys hg_keys;
 typedef struct hg_plan hg_plan;
+typedef struct hg_output hg_output;
 
 const char* hg_last_error(void);
 const char* hg_version(void);
@@ -145,6 +146,13 @@ int hg_plan_output_ciphertexts(hg_plan* plan, const char* output_id, uint64_t* d
 /* replace a Parameter's bound ciphertexts from host/device NTT-form words (client-encrypted inputs) */
 int hg_plan_input_info(hg_plan* plan, const char* param_id, int64_t* elements, int* level);
 int hg_plan_set_input_ciphertexts(hg_plan* plan, const char* param_id, const uint64_t* src, int src_is_device);
+/* Pipelined output: enqueue the GPU decrypt + device->host copy of an output now and
+ * decode it on a host thread (overlapping the next step's GPU work); the ticket is
+ * consumed by hg_output_wait, which returns the same values as hg_plan_output.  The
+ * output tensor may be replaced by the next hg_plan_run once this call returns. */
+int hg_plan_output_async(hg_plan* plan, const char* output_id, hg_output** ticket);
+int hg_output_count(const hg_output* ticket, int64_t* count);
+int hg_output_wait(hg_output* ticket, double* values, int64_t capacity, int64_t* count);
 /* ExecProfile (runtime.hpp:140-156) as JSON */
 int hg_plan_profile_json(hg_plan* plan, char* buf, size_t cap);
 /* kernel launches issued by the last hg_plan_run */

@@ -87,6 +87,9 @@ def lib():
         "hg_plan_set_comm": (C.c_int, [vp, C.c_int, C.c_int, vp]),
         "hg_group_run": (C.c_int, [C.POINTER(vp), C.c_int]),
         "hg_shard_partition": (C.c_int, [C.c_int64, C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64)]),
+        "hg_plan_output_async": (C.c_int, [vp, C.c_char_p, C.POINTER(vp)]),
+        "hg_output_wait": (C.c_int, [vp, f64p, C.c_int64, C.POINTER(C.c_int64)]),
+        "hg_output_count": (C.c_int, [vp, C.POINTER(C.c_int64)]),
         "hg_encode_batch": (C.c_int, [vp, vp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_double, vp]),
         "hg_encode_constant": (C.c_int, [vp, C.c_double, C.c_int, C.c_double, u64p]),
         "hg_encrypt": (C.c_int, [vp, vp, vp, u64p, C.c_int64, C.c_int, vp]),
@@ -283,6 +286,12 @@ class Plan:
         _chk(lib().hg_plan_output(self._h, out_id.encode(), buf.ctypes.data_as(f64p), n.value, C.byref(n)))
         return buf if shape is None else buf.reshape(shape)
 
+    def output_async(self, out_id: str) -> "PendingOutput":
+        """Enqueue decrypt + copy of an output; decode runs on a host thread (see hg_plan_output_async)."""
+        h = vp()
+        _chk(lib().hg_plan_output_async(self._h, out_id.encode(), C.byref(h)))
+        return PendingOutput(h)
+
     def output_info(self, out_id: str):
         e, lv, sc = C.c_int64(), C.c_int(), C.c_double()
         _chk(lib().hg_plan_output_info(self._h, out_id.encode(), C.byref(e), C.byref(lv), C.byref(sc)))
@@ -366,3 +375,20 @@ def shard_partition(groups: int, mg: int, world: int, rank: int):
     out = (C.c_int64 * 4)()
     _chk(lib().hg_shard_partition(groups, mg, world, rank, out))
     return tuple(out)
+
+
+class PendingOutput:
+    """Ticket of hg_plan_output_async; wait() returns the decoded values (row-major batch x elements)."""
+
+    def __init__(self, h):
+        self._h = h
+
+    def wait(self) -> np.ndarray:
+        if self._h is None:
+            raise HEError(1, "output already collected")
+        h, self._h = self._h, None
+        n = C.c_int64()
+        _chk(lib().hg_output_count(h, C.byref(n)))
+        buf = np.zeros(n.value, dtype=np.float64)
+        _chk(lib().hg_output_wait(h, buf.ctypes.data_as(f64p), n.value, C.byref(n)))
+        return buf

@@ -2262,6 +2262,133 @@ int hg_plan_output(hg_plan* P, const char* id, double* values, int64_t capacity,
   });
 }
 
+// Asynchronous output: the GPU decrypt and the device->host copy are enqueued now; a
+// host thread waits for them and decodes, so the host decode of one step overlaps the
+// next step's GPU work (a pipelined end-to-end loop).  hg_output_wait joins it.
+// pinned staging buffers, recycled (cudaMallocHost / cudaFreeHost synchronise the device)
+struct PinnedPool {
+  std::mutex mu;
+  std::vector<std::pair<size_t, void*>> free;
+  void* get(size_t bytes) {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      for (size_t i = 0; i < free.size(); ++i)
+        if (free[i].first >= bytes) {
+          void* p = free[i].second;
+          free.erase(free.begin() + static_cast<long>(i));
+          return p;
+        }
+    }
+    void* p = nullptr;
+    HG_CUDA(cudaMallocHost(&p, bytes));
+    return p;
+  }
+  void put(void* p, size_t bytes) {
+    std::lock_guard<std::mutex> g(mu);
+    free.push_back({bytes, p});
+  }
+  ~PinnedPool() {
+    for (auto& [b, p] : free) cudaFreeHost(p);
+  }
+};
+std::shared_ptr<PinnedPool> pinned_pool() {
+  static std::shared_ptr<PinnedPool> pool = std::make_shared<PinnedPool>();
+  return pool;
+}
+
+struct hg_output {
+  std::thread th;
+  std::shared_ptr<PinnedPool> pool;
+  uint64_t* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  cudaEvent_t done = nullptr;
+  std::vector<double> values;
+  int64_t count = 0;
+  std::string err;
+  int err_code = 0;
+  ~hg_output() {
+    if (th.joinable()) th.join();
+    if (done) cudaEventDestroy(done);
+    if (pinned) pool->put(pinned, pinned_bytes);
+  }
+};
+
+int hg_plan_output_async(hg_plan* P, const char* id, hg_output** out) {
+  return guard_x([&] {
+    hg::check(out != nullptr, HG_E_VALIDATION, "null argument");
+    *out = nullptr;
+    auto it = P->outputs.find(id);
+    hg::check(it != P->outputs.end(), HG_E_VALIDATION, std::string("no output '") + id + "' (run the plan first)");
+    const hg::Val& v = it->second;
+    auto t = std::make_unique<hg_output>();
+    if (v.is_raw()) {
+      t->values = v.raw->v;
+      t->count = v.raw->count();
+      *out = t.release();
+      return;
+    }
+    const int64_t m = v.ct->count;
+    const int64_t batch = v.batched && !v.shape.empty() ? v.shape[0] : 1;
+    const hg::Context& c = *P->ctx;
+    const int nl = v.ct->nl();
+    const int64_t n = c.n();
+    const double scale = v.ct->scale;
+    const size_t words = static_cast<size_t>(m) * nl * n;
+    t->pool = pinned_pool();
+    t->pinned = static_cast<uint64_t*>(t->pool->get(words * 8));
+    t->pinned_bytes = words * 8;
+    HG_CUDA(cudaEventCreateWithFlags(&t->done, cudaEventDisableTiming));
+    {
+      hg::DevArr md(words * 8, hg::S(P));
+      hg::k::decrypt(c, *P->keys, v.ct->p, md.as<uint64_t>(), m, 2, nl, hg::S(P));
+      HG_CUDA(cudaMemcpyAsync(t->pinned, md.p, words * 8, cudaMemcpyDeviceToHost, hg::S(P)));
+    }
+    HG_CUDA(cudaEventRecord(t->done, hg::S(P)));
+    t->count = m * batch;
+    t->values.assign(static_cast<size_t>(m * batch), 0.0);
+    hg_output* raw = t.get();
+    raw->th = std::thread([raw, &c, m, batch, nl, n, scale] {
+      try {
+        HG_CUDA(cudaEventSynchronize(raw->done));
+        std::vector<double> cols(static_cast<size_t>(m * batch));
+        hg::host_parallel(m, [&](int64_t e) {
+          hg::decode_coeffs_host(c, raw->pinned + e * nl * n, nl, scale, batch, &cols[e * batch]);
+        });
+        for (int64_t e = 0; e < m; ++e)
+          for (int64_t b = 0; b < batch; ++b) raw->values[b * m + e] = cols[e * batch + b];
+      } catch (const hg::Error& e) {
+        raw->err = e.what();
+        raw->err_code = e.code();
+      } catch (const std::exception& e) {
+        raw->err = e.what();
+        raw->err_code = HG_E_INTERNAL;
+      }
+    });
+    *out = t.release();
+  });
+}
+
+int hg_output_count(const hg_output* t, int64_t* count) {
+  return guard_x([&] {
+    hg::check(t != nullptr && count != nullptr, HG_E_VALIDATION, "null argument");
+    *count = t->count;
+  });
+}
+
+int hg_output_wait(hg_output* t, double* values, int64_t capacity, int64_t* count) {
+  return guard_x([&] {
+    hg::check(t != nullptr, HG_E_VALIDATION, "null output ticket");
+    std::unique_ptr<hg_output> own(t);
+    if (own->th.joinable()) own->th.join();
+    if (own->err_code) hg::fail(own->err_code, own->err);
+    if (count) *count = own->count;
+    if (values) {
+      hg::check(capacity >= own->count, HG_E_VALIDATION, "output buffer too small");
+      std::copy(own->values.begin(), own->values.end(), values);
+    }
+  });
+}
+
 int hg_plan_profile_json(hg_plan* P, char* buf, size_t cap) {
   return guard_x([&] {
     nlohmann::json wall = nlohmann::json::object(), host = nlohmann::json::object();

@@ -53,4 +53,6 @@ def test_net_bit_exact(name, cuda_ok):
         assert not bad, f"{name}/{oid}: ciphertexts {bad[:8]} differ from the reference"
         vals = plan.output(oid)
         assert G.sha(vals) == want["values_sha256"], f"{name}/{oid}: decoded values differ"
+        # the pipelined output path (decode on a host thread) returns the same doubles
+        assert G.sha(plan.output_async(oid).wait()) == want["values_sha256"]
     plan.close()
