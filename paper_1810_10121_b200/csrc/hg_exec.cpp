@@ -1582,6 +1582,249 @@ Val kernel_pad(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_sh
   return v;
 }
 
+// per-item plaintexts of raw operand elements at (level, scale): encode_raw (runtime.hpp:408-411)
+std::shared_ptr<DevArr> encode_raw_items(hg_plan* P, const RawView& rv, int64_t m, int level, double scale) {
+  const Context& c = *P->ctx;
+  if (rv.column) {
+    std::vector<std::vector<double>> cols(static_cast<size_t>(m));
+    for (int64_t e = 0; e < m; ++e) cols[static_cast<size_t>(e)] = batch_column(*rv.t, e);
+    return encode_columns(P, cols, level, scale);
+  }
+  const int nl = level + 1;
+  std::vector<uint64_t> ptv(static_cast<size_t>(m) * nl * c.n());
+  for (int64_t e = 0; e < m; ++e) {
+    const int64_t q = llround_checked(rv.t->v[static_cast<size_t>(e)], scale);
+    for (int j = 0; j < nl; ++j)
+      std::fill(ptv.begin() + (e * nl + j) * c.n(), ptv.begin() + (e * nl + j + 1) * c.n(), lift_signed_h(q, c.primes()[j]));
+  }
+  auto pt = std::make_shared<DevArr>(ptv.size() * 8, S(P));
+  HG_CUDA(cudaMemcpyAsync(pt->p, ptv.data(), ptv.size() * 8, cudaMemcpyHostToDevice, S(P)));
+  return pt;
+}
+
+// Concat (runtime.hpp:1770-1802): handles of the parts, in output order.  Raw parts join
+// the ciphertext tensor as fresh encryptions (promote_raw_cipher, runtime.hpp:1909-1925).
+Val kernel_concat(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_shape,
+                  const std::vector<const Val*>& in) {
+  const Context& c = *P->ctx;
+  bool out_batched = false;
+  int level = INT_MAX;
+  double scale = 0.0;
+  bool have = false;
+  for (const Val* v : in) {
+    out_batched = out_batched || v->batched;
+    if (v->is_cipher()) {
+      level = std::min(level, v->ct->level);
+      if (!have) scale = v->ct->scale;
+      have = true;
+    }
+  }
+  check(have, HG_EINTERNAL, "concat without a bound operand");
+  for (const Val* v : in)
+    check(!v->is_cipher() || v->ct->level == level, HG_EVALIDATION,
+          "node '" + node.id + "': concatenating ciphertexts of different levels is not supported on the GPU path");
+  const int64_t axis = attr_i64(node, "axis");
+  if (out_batched) check(axis != 0, HG_EVALIDATION, "concatenating along the batch dimension is not supported");
+  const int64_t m_out = space_count(out_shape, out_batched);
+  auto out = new_ct(P, m_out, level, scale);
+  int64_t offset = 0;
+  for (size_t i = 0; i < in.size(); ++i) {
+    const Val& v = *in[i];
+    std::vector<int32_t> src, dst;
+    for_each_index(element_space(v.shape, out_batched), [&](const std::vector<int64_t>& idx, int64_t flat) {
+      std::vector<int64_t> full;
+      if (out_batched) full.push_back(0);
+      full.insert(full.end(), idx.begin(), idx.end());
+      full[static_cast<size_t>(axis)] += offset;
+      int64_t f = 0;
+      for (size_t a = out_batched ? 1 : 0; a < out_shape.size(); ++a) f = f * out_shape[a] + full[a];
+      src.push_back(static_cast<int32_t>(flat));
+      dst.push_back(static_cast<int32_t>(f));
+    });
+    offset += v.shape[static_cast<size_t>(axis)];
+    std::shared_ptr<CtT> part = v.ct;
+    if (!v.is_cipher()) {  // promote_raw_cipher: encrypt(encode_raw(rv, e, level, scale), rng.next())
+      const int64_t mi = space_count(v.shape, v.batched);
+      const RawView rv = raw_view(P, v, mi);
+      Rng rng = P->rng.fork("promote").fork(node.id + "/" + node.inputs[i]);
+      std::vector<uint64_t> seeds(static_cast<size_t>(mi));
+      for (auto& sd : seeds) sd = rng.next();
+      auto pts = encode_raw_items(P, rv, mi, level, scale);
+      part = new_ct(P, mi, level, scale);
+      encrypt_items(P, seeds, pts->as<uint64_t>(), level, part->p);
+    }
+    DevArr d(src.size() * 8, S(P));
+    HG_CUDA(cudaMemcpyAsync(d.p, src.data(), src.size() * 4, cudaMemcpyHostToDevice, S(P)));
+    HG_CUDA(cudaMemcpyAsync(d.as<int32_t>() + src.size(), dst.data(), dst.size() * 4, cudaMemcpyHostToDevice, S(P)));
+    k::scatter_items(c, part->p, d.as<int32_t>(), d.as<int32_t>() + src.size(), out->p, static_cast<int64_t>(src.size()),
+                     out->item_words(), S(P));
+    HG_CUDA(cudaStreamSynchronize(S(P)));  // src/dst are pageable host vectors
+  }
+  Val o;
+  o.shape = out_shape;
+  o.batched = out_batched;
+  o.ct = out;
+  return o;
+}
+
+// Sum over axes (runtime.hpp:1851-1900): each output is the add-chain of its group,
+// evaluated as one grouped GEMM with unit weights (exact modular sums).
+Val kernel_sum(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_shape, const Val& x) {
+  check(x.is_cipher(), HG_EVALIDATION, "node '" + node.id + "': Sum of this operand is not supported");
+  std::set<int64_t> axes;
+  for (int64_t ax : attr_ints(node, "axes")) axes.insert(ax);
+  if (x.batched)
+    check(!axes.count(0), HG_EVALIDATION,
+          "summing across the batch dimension requires rotations, which this build does not provide");
+  const bool out_batched = x.batched;
+  const int64_t m_out = space_count(out_shape, out_batched);
+  std::vector<std::vector<int32_t>> groups(static_cast<size_t>(m_out));
+  for_each_index(element_space(x.shape, x.batched), [&](const std::vector<int64_t>& idx, int64_t flat) {
+    std::vector<int64_t> full;
+    if (x.batched) full.push_back(0);
+    full.insert(full.end(), idx.begin(), idx.end());
+    std::vector<int64_t> dst;
+    for (size_t a = 0; a < full.size(); ++a)
+      if (!axes.count(static_cast<int64_t>(a))) dst.push_back(full[a]);
+    int64_t f = 0;
+    for (size_t a = out_batched ? 1 : 0; a < out_shape.size(); ++a) f = f * out_shape[a] + dst[a];
+    groups[static_cast<size_t>(f)].push_back(static_cast<int32_t>(flat));
+  });
+  const int kt = static_cast<int>(groups.empty() ? 0 : groups[0].size());
+  for (const auto& g : groups) {
+    check(static_cast<int>(g.size()) == kt, HG_EINTERNAL, "uneven sum groups");
+    P->prof.add += static_cast<int64_t>(g.size()) - 1;
+  }
+  const Context& c = *P->ctx;
+  const auto& xt = x.ct;
+  const int nl = xt->nl();
+  NodeCache& C = P->cache[node.id];
+  if (C.level != xt->level) {
+    std::vector<int32_t> xi;
+    for (const auto& g : groups) xi.insert(xi.end(), g.begin(), g.end());
+    std::vector<uint64_t> ones(static_cast<size_t>(kt) * nl, 1);
+    C.idx = std::make_shared<DevArr>(xi.size() * 4 + 4, S(P));
+    C.w = std::make_shared<DevArr>(ones.size() * 8, S(P));
+    HG_CUDA(cudaMemcpyAsync(C.idx->p, xi.data(), xi.size() * 4, cudaMemcpyHostToDevice, S(P)));
+    HG_CUDA(cudaMemcpyAsync(C.w->p, ones.data(), ones.size() * 8, cudaMemcpyHostToDevice, S(P)));
+    HG_CUDA(cudaStreamSynchronize(S(P)));
+    C.level = xt->level;
+  }
+  auto out = new_ct(P, m_out, xt->level, xt->scale);
+  k::gemm_groups(c, xt->p, xt->count, C.idx->as<int32_t>(), C.w->as<uint64_t>(), 0, nullptr, out->p, m_out, 1, kt, nl,
+                 S(P));
+  Val o;
+  o.shape = out_shape;
+  o.batched = out_batched;
+  o.ct = out;
+  return o;
+}
+
+// BatchNormInference with plaintext statistics (runtime.hpp:1326-1420, EncryptedData):
+// the per-channel affine map g x + b, g = gamma / sqrt(var + eps), b = beta - g mean.
+Val kernel_batchnorm(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_shape,
+                     const std::vector<const Val*>& in) {
+  const Val& x = *in[0];
+  check(x.is_cipher(), HG_EVALIDATION, "batch normalization expects a bound operand");
+  for (size_t i = 1; i < in.size(); ++i)
+    check(in[i]->is_raw() && in[i]->from_constants, HG_EVALIDATION,
+          "batch normalization statistics must be plaintext constants");
+  const double eps = attr_f64(node, "epsilon");
+  const HTensor &gamma = *in[1]->raw, &beta = *in[2]->raw, &mean = *in[3]->raw, &var = *in[4]->raw;
+  const int64_t channels = x.shape[1];
+  int64_t inner = 1;
+  for (size_t a = 2; a < x.shape.size(); ++a) inner *= x.shape[a];
+  std::vector<double> g(static_cast<size_t>(channels)), b(static_cast<size_t>(channels));
+  for (int64_t ch = 0; ch < channels; ++ch) {
+    g[ch] = gamma.v[ch] / std::sqrt(var.v[ch] + eps);
+    b[ch] = beta.v[ch] - g[ch] * mean.v[ch];
+  }
+  const Context& c = *P->ctx;
+  const auto& xt = x.ct;
+  const int64_t m = xt->count;
+  auto channel_of = [&](int64_t e) { return (e / inner) % channels; };
+  std::vector<Action> act(static_cast<size_t>(m));
+  std::vector<char> add_skip(static_cast<size_t>(m), 0);
+  for (int64_t e = 0; e < m; ++e) {
+    const int64_t ch = channel_of(e);
+    act[e] = apply_bypass(P, Op::Multiply, classify_scalar(P, g[ch]));
+    if (act[e] == Action::Proceed) ++P->prof.mul_pt;
+    else {
+      ++P->prof.bypass_mult;
+      if (act[e] == Action::Negate) ++P->prof.negate;
+    }
+    if (apply_bypass(P, Op::Add, classify_scalar(P, b[ch])) == Action::ReturnUnchanged) {
+      add_skip[e] = 1;
+      ++P->prof.bypass_add;
+    } else {
+      ++P->prof.add;
+    }
+  }
+  for (int64_t e = 1; e < m; ++e)
+    check(act[e] == act[0], HG_EVALIDATION,
+          "node '" + node.id + "': batch-norm channels with different bypass actions give mixed levels (unsupported)");
+  std::shared_ptr<CtT> t = xt;
+  const int level = xt->level;
+  switch (m > 0 ? act[0] : Action::ReturnUnchanged) {
+    case Action::ReturnUnchanged: break;
+    case Action::Negate: {
+      auto o = new_ct(P, m, level, xt->scale);
+      k::negate(c, xt->p, o->p, xt->words(), xt->nl(), S(P));
+      t = o;
+      break;
+    }
+    case Action::FreshZero: {  // encrypt_zero_at(level, scale, node_rng.fork(e).next())
+      Rng node_rng = P->rng.fork("node").fork(node.id);
+      std::vector<uint64_t> seeds(static_cast<size_t>(m));
+      for (int64_t e = 0; e < m; ++e) seeds[e] = node_rng.fork(static_cast<uint64_t>(e)).next();
+      auto o = new_ct(P, m, level, xt->scale);
+      encrypt_items(P, seeds, nullptr, level, o->p);
+      t = o;
+      break;
+    }
+    case Action::Proceed: {  // multiply_plain_rescale(x, encode_constant(g, level, operand_scale(level)))
+      require_mul_headroom(level);
+      const int nl = level + 1;
+      const double ws = static_cast<double>(c.primes()[level]);
+      std::vector<uint64_t> w(static_cast<size_t>(m) * nl);
+      for (int64_t e = 0; e < m; ++e) {
+        const int64_t q = llround_checked(g[channel_of(e)], ws);
+        for (int j = 0; j < nl; ++j) w[e * nl + j] = lift_signed_h(q, c.primes()[j]);
+      }
+      DevArr dw(w.size() * 8, S(P));
+      HG_CUDA(cudaMemcpyAsync(dw.p, w.data(), w.size() * 8, cudaMemcpyHostToDevice, S(P)));
+      auto prod = new_ct(P, m, level, xt->scale * ws);
+      k::scalar_items(c, xt->p, dw.as<uint64_t>(), prod->p, m, 2, nl, false, S(P));
+      t = rescale_t(P, prod);
+      HG_CUDA(cudaStreamSynchronize(S(P)));  // w is a pageable host vector
+      break;
+    }
+  }
+  // add_plain(t, encode_constant(b, t.level, t.scale)) unless skipped (a zero add leaves the words unchanged)
+  const int nl = t->nl();
+  std::vector<uint64_t> bw(static_cast<size_t>(m) * nl, 0);
+  bool any_add = false;
+  for (int64_t e = 0; e < m; ++e) {
+    if (add_skip[e]) continue;
+    any_add = true;
+    const int64_t q = llround_checked(b[channel_of(e)], t->scale);
+    for (int j = 0; j < nl; ++j) bw[e * nl + j] = lift_signed_h(q, c.primes()[j]);
+  }
+  if (any_add) {
+    DevArr db(bw.size() * 8, S(P));
+    HG_CUDA(cudaMemcpyAsync(db.p, bw.data(), bw.size() * 8, cudaMemcpyHostToDevice, S(P)));
+    auto o = new_ct(P, m, t->level, t->scale);
+    k::scalar_items(c, t->p, db.as<uint64_t>(), o->p, m, 2, nl, true, S(P));
+    HG_CUDA(cudaStreamSynchronize(S(P)));
+    t = o;
+  }
+  Val out;
+  out.shape = out_shape;
+  out.batched = x.batched;
+  out.ct = t;
+  return out;
+}
+
 Val kernel_rearrange(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_shape, const Val& x) {
   check(x.is_cipher(), HG_EVALIDATION, "node '" + node.id + "': rearrangement of this operand is not supported");
   bool out_batched = x.batched;
@@ -1768,6 +2011,9 @@ Val exec_node(hg_plan* P, const GNode& node, const std::vector<const Val*>& in) 
     case Op::Slice:
     case Op::Reverse:
     case Op::Broadcast: return kernel_rearrange(P, node, out_shape, *in[0]);
+    case Op::Concat: return kernel_concat(P, node, out_shape, in);
+    case Op::Sum: return kernel_sum(P, node, out_shape, *in[0]);
+    case Op::BatchNormInference: return kernel_batchnorm(P, node, out_shape, in);
     default:
       fail(HG_EVALIDATION, "node '" + node.id + "': op not supported on the GPU path");
   }

@@ -279,6 +279,9 @@ void mul_plain(const Context& c, const uint64_t* ct, const uint64_t* pt, uint64_
 // every poly times a per-limb scalar residue (encode_constant in NTT form)
 void mul_scalar(const Context& c, const uint64_t* ct, const uint64_t* w, uint64_t* o, int64_t items, int size, int nl,
                 cudaStream_t s);
+// per-item scalar residues w [items][nl]: add ? poly 0 + w : every poly * w
+void scalar_items(const Context& c, const uint64_t* ct, const uint64_t* w, uint64_t* o, int64_t items, int size,
+                  int nl, bool add, cudaStream_t s);
 // rescale `polys` polys from nl to nl-1 limbs (poly.hpp:190-228); scratch int64 [polys][N]
 void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys, int nl, int64_t* scratch,
              cudaStream_t s);

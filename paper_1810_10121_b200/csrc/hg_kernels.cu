@@ -148,6 +148,24 @@ __global__ void k_mul_scalar(const uint64_t* __restrict__ ct, const uint64_t* __
   }
 }
 
+// per-item scalars (encode_constant residues of one value per element): every poly of
+// item i times w[i][limb], or poly 0 of item i plus w[i][limb]
+__global__ void k_scalar_items(const uint64_t* __restrict__ ct, const uint64_t* __restrict__ w,
+                               uint64_t* __restrict__ o, int64_t items, int size, int nl, int add, const CtxParams P) {
+  const int64_t n = P.n;
+  const int64_t words = items * size * nl * n;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < words; x += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = x / n;
+    const int limb = (int)(row % nl);
+    const int poly = (int)((row / nl) % size);
+    const int64_t item = row / ((int64_t)nl * size);
+    const uint64_t wv = w[item * nl + limb];
+    const LimbInfo& L = P.limb[limb];
+    if (add) o[x] = poly == 0 ? add_mod(ct[x], wv, L.q) : ct[x];
+    else o[x] = mul_mod(ct[x], wv, L);
+  }
+}
+
 // --------------------------------------------------------------------------
 // Rescale (poly.hpp:190-228)
 // --------------------------------------------------------------------------
@@ -738,6 +756,16 @@ void mul_scalar(const Context& c, const uint64_t* ct, const uint64_t* w, uint64_
   if (words <= 0) return;
   c.kt_begin("k_mul_scalar", s);
   k_mul_scalar<<<ew_blocks(words, 256), 256, 0, s>>>(ct, w, o, words, nl, c.kp());
+  c.kt_end(s);
+  HG_CUDA(cudaGetLastError());
+}
+
+void scalar_items(const Context& c, const uint64_t* ct, const uint64_t* w, uint64_t* o, int64_t items, int size,
+                  int nl, bool add, cudaStream_t s) {
+  const int64_t words = items * size * nl * c.n();
+  if (words <= 0) return;
+  c.kt_begin(add ? "k_add_scalar_items" : "k_mul_scalar_items", s, 2.0 * words * 8, add ? 0.0 : (double)words);
+  k_scalar_items<<<ew_blocks(words, 256), 256, 0, s>>>(ct, w, o, items, size, nl, add ? 1 : 0, c.kp());
   c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }

@@ -251,6 +251,30 @@ def mini(seed: int, batch: int):
     return g.json(["mul", "fc"]), x
 
 
+def ops2(seed: int, batch: int):
+    """Second coverage graph (test-only; N=2048): BatchNormInference, Sum, Negate and a
+    Concat that promotes a batch-column constant to fresh encryptions."""
+    wr = Rng(seed).fork("ops2")
+    g = G("ops2_bn_sum_concat")
+    g.param("x", [1, 2, 4, 4])
+    g.const("gamma", np.array([1.5, 0.75]))
+    g.const("beta", np.array([0.25, 0.0]))
+    g.const("mean", np.array([0.1, 0.0]))
+    g.const("var", np.array([2.0, 0.5]))
+    g.op("bn", "BatchNormInference", ["x", "gamma", "beta", "mean", "var"], epsilon=1e-5)
+    g.op("sq", "PolyAct", ["bn"], a=1.0, b=0.0, c=0.0)
+    g.op("s", "Sum", ["sq"], axes=[3])
+    g.op("ns", "Negate", ["s"])
+    g.const("k", gaussian_tensor(wr.fork("k"), (2, 3), 0.5))
+    g.op("kb", "Broadcast", ["k"], shape=[-1, 2, 3], axes=[0])
+    g.op("cat", "Concat", ["s", "ns", "kb"], axis=2)
+    g.op("flat", "Reshape", ["cat"], shape=[-1, 22])
+    g.const("w", gaussian_tensor(wr.fork("w"), (22, 3), 1.0 / 22))
+    g.op("fc", "Dot", ["flat", "w"])
+    x = uniform_tensor(Rng(seed).fork("inputs").fork("x"), (batch, 2, 4, 4), -1.0, 1.0)
+    return g.json(["fc", "cat"]), x
+
+
 CONFIGS = {"c1": config1, "c3": config3, "c4": config4, "c5": config5}
 MINI_CONTEXT = {"n": 2048, "bits": [45, 30, 30, 30, 30, 45], "scale_bits": 30, "security": 0}
 
@@ -262,8 +286,8 @@ def key_seed(seed: int) -> int:
 def build(spec: dict):
     """spec: {"config": "c1"|"c3"|"c4"|"c5"|"mini", "batch": B, "seed": s} -> (graph, x, ctx params)."""
     cfg = spec["config"]
-    if cfg == "mini":
-        g, x = mini(spec["seed"], spec["batch"])
+    if cfg in ("mini", "ops2"):
+        g, x = (mini if cfg == "mini" else ops2)(spec["seed"], spec["batch"])
         ctxp = dict(MINI_CONTEXT)
     else:
         g, x = CONFIGS[cfg](spec["seed"], spec["batch"])
@@ -282,6 +306,7 @@ def _spec(config, batch, seed=1, **kw):
 
 GOLDEN_NETS = {
     "mini": _spec("mini", 16, seed=3),
+    "ops2": _spec("ops2", 16, seed=4),
     "c1": _spec("c1", 4096),
     "c3_n2048": _spec("c3", 64, n=2048),
     "c5_n2048": _spec("c5", 64, n=2048),

@@ -13,7 +13,7 @@ from tests import golden_util as G
 
 pytestmark = pytest.mark.gpu
 
-NETS = ["mini", "c1", "c3_n2048", "c5_n2048", "c4_n2048", "c3", "c5"]
+NETS = ["mini", "ops2", "c1", "c3_n2048", "c5_n2048", "c4_n2048", "c3", "c5"]
 
 
 def _available(name):

@@ -13,7 +13,7 @@ from tests import golden_util as G
 
 pytestmark = pytest.mark.gpu
 
-CASES = [("mini", 2), ("c1", 2), ("c1", 3), ("c3_n2048", 2), ("c3_n2048", 4), ("c5_n2048", 3), ("c4_n2048", 4), ("c3", 8)]
+CASES = [("mini", 2), ("ops2", 2), ("c1", 2), ("c1", 3), ("c3_n2048", 2), ("c3_n2048", 4), ("c5_n2048", 3), ("c4_n2048", 4), ("c3", 8)]
 
 
 def _available(name):
