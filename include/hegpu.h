@@ -49,6 +49,9 @@ const char* hg_version(void);
 int hg_context_create(int64_t poly_degree, const int* coeff_mod_bits, int nbits, int scale_bits, int security,
                       int device, hg_context** out);
 void hg_context_destroy(hg_context* ctx);
+/* the ContextParams a context was built from (ring degree, coeff_mod_bits, scale_bits, security) */
+int hg_context_params(const hg_context* ctx, int64_t* n, int* bits, int cap, int* nbits, int* scale_bits,
+                      int* security);
 /* writes up to `cap` primes; returns the prime count via *count */
 int hg_context_primes(const hg_context* ctx, uint64_t* primes, int cap, int* count);
 /* relin digit counts D_i (ckks_backend.hpp:42-46) and total rows */
@@ -65,6 +68,18 @@ int hg_keys_generate(hg_context* ctx, uint64_t seed, int with_relin, hg_keys** o
 void hg_keys_destroy(hg_keys* keys);
 /* host copies, NTT form, full chain: secret[(L+1)N], pk[2][(L+1)N], relin[rows][2][(L+1)N] (relin may be NULL) */
 int hg_keys_export(const hg_context* ctx, const hg_keys* keys, uint64_t* secret, uint64_t* pk, uint64_t* relin);
+
+/* ---- key and ciphertext files (keyio.hpp:36-302: HEGK / HEGC, coefficient-domain u64 LE) ----
+ * Byte-identical to the reference's save_keys / save_ciphertext; loading re-homes the
+ * payload into the GPU's NTT-form residency. */
+int hg_keys_save(const hg_context* ctx, const hg_keys* keys, const char* path);
+/* load_keys (keyio.hpp:171-238): builds the context from the file's header on `device` */
+int hg_keys_load(const char* path, int device, hg_context** ctx_out, hg_keys** keys_out);
+/* save_ciphertext (keyio.hpp:244-259) of a device ciphertext [size][level+1][N] (NTT form) */
+int hg_ciphertext_save(hg_context* ctx, const uint64_t* ct_dev, int size, int level, double scale, const char* path);
+/* load_ciphertext (keyio.hpp:267-293); ct_dev NULL = header only (size, level, scale) */
+int hg_ciphertext_load(hg_context* ctx, const char* path, uint64_t* ct_dev, int64_t capacity_words, int* size,
+                       int* level, double* scale);
 
 /* ---- ring kernels (NttTables::forward/inverse, ring.hpp:263-301) ---- */
 /* in-place on `rows` limb rows; row r is limb (r % nl) at dev + r*N */

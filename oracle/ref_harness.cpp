@@ -31,6 +31,7 @@
 #include "heg/backend.hpp"
 #include "heg/ckks/ckks_backend.hpp"
 #include "heg/graph_io.hpp"
+#include "heg/keyio.hpp"
 #include "heg/runtime.hpp"
 
 using namespace heg;
@@ -386,6 +387,34 @@ int mode_net(int argc, char** argv) {
   return 0;
 }
 
+// io <outdir> <n> <scale_bits> <bits> <key_seed> <enc_seed>: the reference's own HEGK / HEGC files
+// (keyio.hpp) for generate_keys(key_seed) and one encryption of seeded slot values, plus the
+// values its decrypt returns.
+int mode_io(int argc, char** argv) {
+  if (argc < 8) return 2;
+  const std::string outdir = argv[2];
+  ContextParams p;
+  p.poly_degree = std::stoll(argv[3]);
+  p.scale_bits = std::stoi(argv[4]);
+  p.coeff_mod_bits = parse_bits(argv[5]);
+  p.security = 0;
+  const uint64_t key_seed = std::stoull(argv[6]), enc_seed = std::stoull(argv[7]);
+  ContextPtr ctx = make_context(p);
+  KeySet keys = generate_keys(*ctx, key_seed);
+  CkksBackend be(ctx, keys);
+  save_keys(outdir + "/keys.hegk", *ctx, &be.keys());
+  Rng r(enc_seed);
+  std::vector<double> v(static_cast<size_t>(ctx->poly_degree() / 2));
+  for (auto& x : v) x = r.uniform(-1.0, 1.0);
+  CiphertextPtr ct = be.encrypt(*be.encode(v, ctx->max_level(), ctx->default_scale()), enc_seed);
+  save_ciphertext(outdir + "/ct.hegc", *ctx, *ct);
+  const std::vector<double> dec = be.decrypt(*ct, static_cast<int64_t>(v.size()));
+  std::ofstream os(outdir + "/decrypted.f64", std::ios::binary);
+  os.write(reinterpret_cast<const char*>(dec.data()), static_cast<std::streamsize>(dec.size() * 8));
+  std::cout << "{\"values\": " << v.size() << "}\n";
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -397,6 +426,7 @@ int main(int argc, char** argv) {
     std::string mode = argv[1];
     if (mode == "prims") return mode_prims(argc, argv);
     if (mode == "net") return mode_net(argc, argv);
+    if (mode == "io") return mode_io(argc, argv);
   } catch (const Error& e) {
     std::cerr << "heg::Error(" << static_cast<int>(e.code()) << "): " << e.what() << "\n";
     return 1;

@@ -59,6 +59,8 @@ def lib():
         "hg_context_create": (C.c_int, [C.c_int64, C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int, C.c_int,
                                         C.POINTER(vp)]),
         "hg_context_destroy": (None, [vp]),
+        "hg_context_params": (C.c_int, [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_int),
+                                        C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         "hg_context_primes": (C.c_int, [vp, u64p, C.c_int, C.POINTER(C.c_int)]),
         "hg_context_relin_rows": (C.c_int, [vp, C.POINTER(C.c_int)]),
         "hg_context_set_stream": (C.c_int, [vp, vp]),
@@ -90,6 +92,11 @@ def lib():
         "hg_plan_output_async": (C.c_int, [vp, C.c_char_p, C.POINTER(vp)]),
         "hg_output_wait": (C.c_int, [vp, f64p, C.c_int64, C.POINTER(C.c_int64)]),
         "hg_output_count": (C.c_int, [vp, C.POINTER(C.c_int64)]),
+        "hg_keys_save": (C.c_int, [vp, vp, C.c_char_p]),
+        "hg_keys_load": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(vp), C.POINTER(vp)]),
+        "hg_ciphertext_save": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_double, C.c_char_p]),
+        "hg_ciphertext_load": (C.c_int, [vp, C.c_char_p, vp, C.c_int64, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                         C.POINTER(C.c_double)]),
         "hg_encode_batch": (C.c_int, [vp, vp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_double, vp]),
         "hg_encode_constant": (C.c_int, [vp, C.c_double, C.c_int, C.c_double, u64p]),
         "hg_encrypt": (C.c_int, [vp, vp, vp, u64p, C.c_int64, C.c_int, vp]),
@@ -139,10 +146,17 @@ def _ptr(x) -> int:
 class Context:
     """hg_context: primes + NTT tables in HBM (replaces heg::CryptoContext)."""
 
-    def __init__(self, n: int, bits, scale_bits: int = 30, security: int = 128, device: int = 0):
-        arr = (C.c_int * len(bits))(*bits)
-        h = vp()
-        _chk(lib().hg_context_create(n, arr, len(bits), scale_bits, security, device, C.byref(h)))
+    def __init__(self, n: int, bits, scale_bits: int = 30, security: int = 128, device: int = 0, _handle=None):
+        if _handle is None:
+            arr = (C.c_int * len(bits))(*bits)
+            h = vp()
+            _chk(lib().hg_context_create(n, arr, len(bits), scale_bits, security, device, C.byref(h)))
+        else:
+            h = _handle
+            nn, nb, sb, sec = C.c_int64(), C.c_int(), C.c_int(), C.c_int()
+            bb = (C.c_int * 64)()
+            _chk(lib().hg_context_params(h, C.byref(nn), bb, 64, C.byref(nb), C.byref(sb), C.byref(sec)))
+            n, bits, scale_bits, security = nn.value, list(bb[: nb.value]), sb.value, sec.value
         self._h = h
         self.n = n
         self.bits = list(bits)
@@ -215,12 +229,27 @@ class Context:
 class Keys:
     """hg_keys: secret/public/relin keys resident in HBM (ckks_backend.hpp:53-114)."""
 
-    def __init__(self, ctx: Context, seed: int, with_relin: bool = True):
-        h = vp()
-        _chk(lib().hg_keys_generate(ctx.handle, seed, 1 if with_relin else 0, C.byref(h)))
+    def __init__(self, ctx: Context, seed: int, with_relin: bool = True, _handle=None):
+        if _handle is None:
+            h = vp()
+            _chk(lib().hg_keys_generate(ctx.handle, seed, 1 if with_relin else 0, C.byref(h)))
+        else:
+            h = _handle
         self._h = h
         self.ctx = ctx
         self.with_relin = with_relin
+
+    def save(self, path: str):
+        """HEGK key file, byte-identical to the reference's save_keys (keyio.hpp:128-151)."""
+        _chk(lib().hg_keys_save(self.ctx.handle, self._h, path.encode()))
+
+    @staticmethod
+    def load(path: str, device: int = 0):
+        """load_keys (keyio.hpp:171-238) -> (Context, Keys) built from the file."""
+        hc, hk = vp(), vp()
+        _chk(lib().hg_keys_load(path.encode(), device, C.byref(hc), C.byref(hk)))
+        ctx = Context(0, [], _handle=hc, device=device)
+        return ctx, Keys(ctx, 0, True, _handle=hk)
 
     @property
     def handle(self):

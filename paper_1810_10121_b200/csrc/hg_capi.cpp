@@ -6,15 +6,9 @@
 #include <vector>
 
 #include "../../include/hegpu.h"
+#include "hg_handles.hpp"
 #include "hg_internal.hpp"
 
-struct hg_context {
-  std::unique_ptr<hg::Context> c;
-  cudaStream_t stream() const { return c->stream(); }
-};
-struct hg_keys {
-  std::unique_ptr<hg::Keys> k;
-};
 
 namespace {
 thread_local std::string g_err;
@@ -80,6 +74,20 @@ int hg_context_create(int64_t n, const int* bits, int nbits, int scale_bits, int
 }
 
 void hg_context_destroy(hg_context* ctx) { delete ctx; }
+
+int hg_context_params(const hg_context* ctx, int64_t* n, int* bits, int cap, int* nbits, int* scale_bits,
+                      int* security) {
+  return guard([&] {
+    need(ctx, "ctx");
+    const auto& p = ctx->c->params();
+    if (n) *n = p.n;
+    if (nbits) *nbits = static_cast<int>(p.bits.size());
+    if (bits)
+      for (int i = 0; i < cap && i < static_cast<int>(p.bits.size()); ++i) bits[i] = p.bits[static_cast<size_t>(i)];
+    if (scale_bits) *scale_bits = p.scale_bits;
+    if (security) *security = p.security;
+  });
+}
 
 int hg_context_primes(const hg_context* ctx, uint64_t* primes, int cap, int* count) {
   return guard([&] {

@@ -488,6 +488,39 @@ static void sample_uniform_ntt(const Context& c, Rng& r, uint64_t* out) {
   }
 }
 
+// Key-switch companions of the resident relin rows (one-time, host): Shoup constants
+// (packed with the value for 32-bit limbs) and the Montgomery form for the shared-memory MAC.
+void finish_relin_keys(const Context& c, Keys& k) {
+  Keys* keys = &k;
+  const int64_t n = c.n();
+  const int nl = c.max_level() + 1;
+  const int64_t pw = static_cast<int64_t>(nl) * n;
+  const int rows = c.relin_rows();
+  std::vector<uint64_t> kv(static_cast<size_t>(rows) * 2 * pw), kp(kv.size());
+  std::vector<uint32_t> km(kv.size(), 0);  // Montgomery form w 2^32 mod q (32-bit limbs)
+  HG_CUDA(cudaMemcpy(kv.data(), keys->relin.p, kv.size() * 8, cudaMemcpyDeviceToHost));
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  std::vector<std::thread> pool;
+  for (unsigned t = 0; t < hw; ++t)
+    pool.emplace_back([&, t] {
+      for (size_t w = t; w < kv.size(); w += hw) {
+        const int limb = static_cast<int>((w / n) % nl);
+        const uint64_t q = c.primes()[limb], v = kv[w];
+        if (q < (uint64_t(1) << 30)) {
+          kp[w] = (static_cast<uint64_t>((u128(v) << 32) / q) << 32) | v;
+          km[w] = static_cast<uint32_t>((u128(v) << 32) % q);
+        } else {
+          kp[w] = static_cast<uint64_t>((u128(v) << 64) / q);
+        }
+      }
+    });
+  for (auto& th : pool) th.join();
+  keys->relin_pack.alloc(kp.size() * 8);
+  HG_CUDA(cudaMemcpy(keys->relin_pack.p, kp.data(), kp.size() * 8, cudaMemcpyHostToDevice));
+  keys->relin_mont.alloc(km.size() * 4);
+  HG_CUDA(cudaMemcpy(keys->relin_mont.p, km.data(), km.size() * 4, cudaMemcpyHostToDevice));
+}
+
 std::unique_ptr<Keys> generate_keys(const Context& c, uint64_t seed, bool with_relin) {
   const int L = c.max_level(), nl = L + 1;
   const int64_t n = c.n(), pw = nl * n;
@@ -535,30 +568,7 @@ std::unique_ptr<Keys> generate_keys(const Context& c, uint64_t seed, bool with_r
         HG_CUDA(cudaStreamSynchronize(s));  // host buffers are reused
       }
     }
-    // Shoup companions for the key-switch MAC (one-time, host)
-    std::vector<uint64_t> kv(static_cast<size_t>(rows) * 2 * pw), kp(kv.size());
-    std::vector<uint32_t> km(kv.size(), 0);  // Montgomery form w 2^32 mod q (32-bit limbs)
-    HG_CUDA(cudaMemcpy(kv.data(), keys->relin.p, kv.size() * 8, cudaMemcpyDeviceToHost));
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    std::vector<std::thread> pool;
-    for (unsigned t = 0; t < hw; ++t)
-      pool.emplace_back([&, t] {
-        for (size_t w = t; w < kv.size(); w += hw) {
-          const int limb = static_cast<int>((w / n) % nl);
-          const uint64_t q = c.primes()[limb], v = kv[w];
-          if (q < (uint64_t(1) << 30)) {
-            kp[w] = (static_cast<uint64_t>((u128(v) << 32) / q) << 32) | v;
-            km[w] = static_cast<uint32_t>((u128(v) << 32) % q);
-          } else {
-            kp[w] = static_cast<uint64_t>((u128(v) << 64) / q);
-          }
-        }
-      });
-    for (auto& th : pool) th.join();
-    keys->relin_pack.alloc(kp.size() * 8);
-    HG_CUDA(cudaMemcpy(keys->relin_pack.p, kp.data(), kp.size() * 8, cudaMemcpyHostToDevice));
-    keys->relin_mont.alloc(km.size() * 4);
-    HG_CUDA(cudaMemcpy(keys->relin_mont.p, km.data(), km.size() * 4, cudaMemcpyHostToDevice));
+    finish_relin_keys(c, *keys);
     keys->has_relin = true;
   }
   HG_CUDA(cudaStreamSynchronize(s));

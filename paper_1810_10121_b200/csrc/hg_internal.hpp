@@ -248,6 +248,8 @@ struct Keys {
   bool has_relin = false;
 };
 std::unique_ptr<Keys> generate_keys(const Context& ctx, uint64_t seed, bool with_relin);
+// relin_pack / relin_mont from the resident relin rows (keygen and key-file loading)
+void finish_relin_keys(const Context& c, Keys& keys);
 
 // host samplers (poly.hpp:247-276): signed coefficient streams
 void sample_ternary(Rng& r, int64_t n, int64_t* out);

@@ -121,9 +121,27 @@ def make_nets(which=None):
             print("wrote net", name, "execute_ms", res["execute_ms"])
 
 
+# The reference's own HEGK / HEGC files (keyio.hpp) for the GPU key/ciphertext I/O tests:
+# N=1024, primes {30, 30}, keys seed 7, one encryption (seed 11) of 512 seeded slot values,
+# plus the reference's decrypt of it.
+IO_CASE = {"dir": "io_n1024", "n": 1024, "scale_bits": 30, "bits": [30, 30], "key_seed": 7, "enc_seed": 11}
+
+
+def make_io():
+    d = os.path.join(HERE, IO_CASE["dir"])
+    os.makedirs(d, exist_ok=True)
+    subprocess.check_call([HARNESS, "io", d, str(IO_CASE["n"]), str(IO_CASE["scale_bits"]),
+                           ",".join(map(str, IO_CASE["bits"])), str(IO_CASE["key_seed"]), str(IO_CASE["enc_seed"])])
+    with open(os.path.join(d, "case.json"), "w") as f:
+        json.dump(IO_CASE, f, indent=1)
+    print("wrote", d)
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "prims"
     if what == "prims":
         make_prims()
     elif what == "nets":
         make_nets(sys.argv[2:] or None)
+    elif what == "io":
+        make_io()

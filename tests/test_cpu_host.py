@@ -107,5 +107,5 @@ def test_config5_weight_mix():
 
 def test_golden_fixtures_are_small():
     gdir = os.path.join(ROOT, "tests", "golden")
-    total = sum(os.path.getsize(os.path.join(gdir, f)) for f in os.listdir(gdir))
+    total = sum(os.path.getsize(os.path.join(d, f)) for d, _, fs in os.walk(gdir) for f in fs)
     assert total < 2_000_000
