@@ -34,7 +34,7 @@ struct Cfg {
   static constexpr size_t tw_bytes = (size_t)N * sizeof(lz::TWT<W>);
   static constexpr bool TWS = data_bytes + tw_bytes <= kSmemCap;
   static constexpr size_t smem = data_bytes + (TWS ? tw_bytes : 0);
-  static constexpr int threads = N / 16 < 512 ? N / 16 : 512;
+  static constexpr int threads = lz::lz_threads<LOGN>();
   static constexpr int min_blocks = (sizeof(W) == 4 && 2 * smem <= kSmemCap && threads <= 512) ? 2 : 1;
 };
 
@@ -104,7 +104,7 @@ HG_KERNEL k_lift_ntt_t(const int64_t* __restrict__ src, uint64_t* __restrict__ o
   const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
   for (int r = c.r0; r < c.r1; ++r) {
     const int64_t* g = src + (int64_t)r * n;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) c.s[lz::padw<W>(i)] = (W)lift_signed(g[i], *c.L);
+    for (int i = threadIdx.x; i < n; i += lz::lz_threads<LOGN>()) c.s[lz::padw<W>(i)] = (W)lift_signed(g[i], *c.L);
     __syncthreads();
     lz::fwd<W, LOGN>(c.s, c.tw, q, q2);
     lz::store<W, LOGN>(out + ((int64_t)r * nl + c.limb) * n, c.s);
@@ -125,7 +125,7 @@ HG_KERNEL k_rescale_top_t(const uint64_t* __restrict__ in, int64_t* __restrict__
     __syncthreads();
     lz::inv<W, LOGN>(c.s, c.tw, Lz<W>::ninv(*c.L), q, q2);
     int64_t* o = cen + (int64_t)r * n;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    for (int i = threadIdx.x; i < n; i += lz::lz_threads<LOGN>()) {
       const uint64_t v = c.s[lz::padw<W>(i)];
       o[i] = v > half ? (int64_t)v - (int64_t)c.L->q : (int64_t)v;
     }
@@ -154,7 +154,7 @@ HG_KERNEL k_rescale_rest_t(const uint64_t* __restrict__ in, const int64_t* __res
     lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2);
     const uint64_t* x = in + ((int64_t)r * nl + j) * n;
     uint64_t* o = out + ((int64_t)r * t + j) * n;
-    for (int vt = threadIdx.x; vt < (n >> 4); vt += blockDim.x) {
+    for (int vt = threadIdx.x; vt < (n >> 4); vt += lz::lz_threads<LOGN>()) {
       W y[16];
       lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, y);
       const ulonglong2* x2 = reinterpret_cast<const ulonglong2*>(x + (vt << 4));
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_block
     lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2);
     const uint64_t* x = in + ((int64_t)r * nl + j) * nfull + (int64_t)half * n;
     uint64_t* o = out + ((int64_t)r * t + j) * nfull + (int64_t)half * n;
-    for (int vt = threadIdx.x; vt < (n >> 4); vt += blockDim.x) {
+    for (int vt = threadIdx.x; vt < (n >> 4); vt += lz::lz_threads<LOGN>()) {
       W y[16];
       lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, y);
       const ulonglong2* x2 = reinterpret_cast<const ulonglong2*>(x + (vt << 4));
@@ -231,7 +231,7 @@ HG_KERNEL k_relin_c2_t(const uint64_t* __restrict__ a, const uint64_t* __restric
   for (int r = c.r0; r < c.r1; ++r) {
     const uint64_t* x1 = a + r * a_stride + a1_off + (int64_t)c.limb * n;
     const uint64_t* y1 = b + r * b_stride + b1_off + (int64_t)c.limb * n;
-    for (int k = threadIdx.x; k < n; k += blockDim.x) c.s[lz::padw<W>(k)] = (W)mul_mod(x1[k], y1[k], *c.L);
+    for (int k = threadIdx.x; k < n; k += lz::lz_threads<LOGN>()) c.s[lz::padw<W>(k)] = (W)mul_mod(x1[k], y1[k], *c.L);
     __syncthreads();
     lz::inv<W, LOGN>(c.s, c.tw, Lz<W>::ninv(*c.L), q, q2);
     lz::store<W, LOGN>(c2 + ((int64_t)r * nl + c.limb) * n, c.s);
@@ -262,7 +262,7 @@ struct RelinC {
 template <typename W, int LOGN, bool SPLIT = false>
 struct RelinCfg {
   // thread vt owns evaluation groups vt + g threads (16 evaluations each), g < GPT
-  static constexpr int threads = (1 << LOGN) / 16 < 512 ? (1 << LOGN) / 16 : 512;
+  static constexpr int threads = lz::lz_threads<LOGN>();
   static constexpr int GPT = (1 << LOGN) / 16 / threads;
   static constexpr bool ACC_GLOBAL = sizeof(W) == 8 && LOGN >= 14;
   // stage each source residue of c2 once in shared memory (cp.async, prefetched
@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT>::threads, 1)
   (void)ks;
   (void)kmont;
   auto stage_c2 = [&](const uint64_t* gsrc) {
-    for (int k = threadIdx.x * 2; k < n; k += blockDim.x * 2) cp_async16(c2s + k, gsrc + k);
+    for (int k = threadIdx.x * 2; k < n; k += lz::lz_threads<LOGN>() * 2) cp_async16(c2s + k, gsrc + k);
     cp_async_commit();
   };
   (void)c2s;
@@ -344,7 +344,7 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT>::threads, 1)
     if constexpr (AG) {
 #pragma unroll
       for (int gi = 0; gi < GPT; ++gi) {
-        uint64_t* o0 = obase + ((threadIdx.x + gi * blockDim.x) << 4);
+        uint64_t* o0 = obase + ((threadIdx.x + gi * lz::lz_threads<LOGN>()) << 4);
 #pragma unroll
         for (int r = 0; r < 16; ++r) { o0[r] = 0; o0[pw + r] = 0; }
       }
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT>::threads, 1)
           // this digit's key row (b then a) -> shared memory, behind the NTT below
           const uint4* kb = reinterpret_cast<const uint4*>(kmont + (int64_t)row * 2 * K.key_poly_words + (int64_t)j * nfull + hoff);
           const uint4* ka = reinterpret_cast<const uint4*>(kmont + ((int64_t)row * 2 + 1) * K.key_poly_words + (int64_t)j * nfull + hoff);
-          for (int ch = threadIdx.x; ch < n / 4; ch += blockDim.x) {
+          for (int ch = threadIdx.x; ch < n / 4; ch += lz::lz_threads<LOGN>()) {
             cp_async16(ks + key_slot(ch), kb + ch);
             cp_async16(ks + n / 4 + key_slot(ch), ka + ch);
           }
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT>::threads, 1)
         (void)c2_staged;
 #pragma unroll
         for (int gi = 0; gi < GPT; ++gi) {
-          const int vt = threadIdx.x + gi * blockDim.x, k0 = vt << 4;
+          const int vt = threadIdx.x + gi * lz::lz_threads<LOGN>(), k0 = vt << 4;
           uint64_t* o0 = obase + k0;
           uint64_t* o1 = o0 + pw;
           (void)o0;
@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT>::threads, 1)
     // epilogue: + d0, d1; canonical store
 #pragma unroll
     for (int gi = 0; gi < GPT; ++gi) {
-      const int k0 = (threadIdx.x + gi * blockDim.x) << 4;
+      const int k0 = (threadIdx.x + gi * lz::lz_threads<LOGN>()) << 4;
       uint64_t* o0 = obase + k0;
       uint64_t* o1 = o0 + pw;
       const uint64_t* p0 = a + (int64_t)item * a_stride + (int64_t)j * nfull + hoff + k0;

@@ -33,6 +33,12 @@ __host__ __device__ constexpr int smem_words() { return (1 << LOGN) + (1 << (LOG
 template <typename W>
 using TWT = typename Lz<W>::TW;
 
+// Every kernel built on these passes runs lz_threads<LOGN>() threads per CTA
+// (hg_kernels2.cu Cfg / RelinCfg), so the per-thread loops below have a
+// compile-time trip count and unroll.
+template <int LOGN>
+__host__ __device__ constexpr int lz_threads() { return (1 << LOGN) / 16 < 512 ? (1 << LOGN) / 16 : 512; }
+
 // the second modulus constant the lazy passes take: 2q (integer lanes) or 1/q (fp64 lane)
 template <typename W>
 __device__ __forceinline__ W q2_of(const LimbInfo& L) {
@@ -59,7 +65,8 @@ __device__ __forceinline__ void fwd_group(W (&x)[1 << K], int g, const TWT<W>* t
 template <typename W, int LOGN, int K, int S0>
 __device__ __forceinline__ void fwd_pass(W* s, const TWT<W>* tw, W q, W q2) {
   constexpr int R = 1 << K, TL = LOGN - S0 - K;
-  for (int vt = threadIdx.x; vt < (1 << (LOGN - K)); vt += blockDim.x) {
+#pragma unroll
+  for (int vt = threadIdx.x; vt < (1 << (LOGN - K)); vt += lz_threads<LOGN>()) {
     const int g = vt >> TL;
     const int pb = padw<W>((g << (LOGN - S0)) + (vt & ((1 << TL) - 1)));
     W x[R];
@@ -100,7 +107,8 @@ __device__ __forceinline__ void fwd_but_last(W* s, const TWT<W>* tw, W q, W q2) 
 template <typename W, int LOGN, typename Get>
 __device__ __forceinline__ void fwd_first_from(W* s, Get get, const TWT<W>* tw, W q, W q2) {
   constexpr int K = (LOGN & 3) ? (LOGN & 3) : 4, R = 1 << K, TL = LOGN - K;
-  for (int vt = threadIdx.x; vt < (1 << TL); vt += blockDim.x) {
+#pragma unroll
+  for (int vt = threadIdx.x; vt < (1 << TL); vt += lz_threads<LOGN>()) {
     const int pb = padw<W>(vt);
     W x[R];
 #pragma unroll
@@ -146,7 +154,7 @@ __device__ __forceinline__ void fwd_last(const W* s, int vt, const TWT<W>* tw, W
 template <typename W, int LOGN>
 __device__ __forceinline__ void fwd(W* s, const TWT<W>* tw, W q, W q2) {
   fwd_but_last<W, LOGN>(s, tw, q, q2);
-  for (int vt = threadIdx.x; vt < (1 << (LOGN - 4)); vt += blockDim.x) {
+  for (int vt = threadIdx.x; vt < (1 << (LOGN - 4)); vt += lz_threads<LOGN>()) {
     W x[16];
     fwd_last<W, LOGN>(s, vt, tw, q, q2, x);
     const int pb = padw<W>(vt << 4);
@@ -175,7 +183,8 @@ __device__ __forceinline__ void inv_group(W (&x)[1 << K], int gi, const TWT<W>* 
 template <typename W, int LOGN, int K, int S0, bool LAST>
 __device__ __forceinline__ void inv_pass(W* s, const TWT<W>* tw, TWT<W> ninv, W q, W q2) {
   constexpr int R = 1 << K;
-  for (int vt = threadIdx.x; vt < (1 << (LOGN - K)); vt += blockDim.x) {
+#pragma unroll
+  for (int vt = threadIdx.x; vt < (1 << (LOGN - K)); vt += lz_threads<LOGN>()) {
     const int gi = vt >> S0;
     const int pb = padw<W>((gi << (S0 + K)) + (vt & ((1 << S0) - 1)));
     W x[R];
@@ -224,7 +233,7 @@ __device__ __forceinline__ void inv(W* s, const TWT<W>* tw, TWT<W> ninv, W q, W 
 template <typename W, int LOGN>
 __device__ __forceinline__ void load(W* s, const uint64_t* __restrict__ g) {
   const ulonglong2* g2 = reinterpret_cast<const ulonglong2*>(g);
-  for (int i = threadIdx.x; i < (1 << (LOGN - 1)); i += blockDim.x) {
+  for (int i = threadIdx.x; i < (1 << (LOGN - 1)); i += lz_threads<LOGN>()) {
     const ulonglong2 v = g2[i];
     const int p = padw<W>(2 * i);
     s[p] = (W)v.x;
@@ -234,7 +243,7 @@ __device__ __forceinline__ void load(W* s, const uint64_t* __restrict__ g) {
 template <typename W, int LOGN>
 __device__ __forceinline__ void store(uint64_t* __restrict__ g, const W* s) {
   ulonglong2* g2 = reinterpret_cast<ulonglong2*>(g);
-  for (int i = threadIdx.x; i < (1 << (LOGN - 1)); i += blockDim.x) {
+  for (int i = threadIdx.x; i < (1 << (LOGN - 1)); i += lz_threads<LOGN>()) {
     const int p = padw<W>(2 * i);
     g2[i] = make_ulonglong2((uint64_t)s[p], (uint64_t)s[p + 1]);
   }
