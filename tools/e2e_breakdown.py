@@ -17,7 +17,7 @@ keys = P.Keys(ctx, spec["key_seed"])
 plan = P.Plan(ctx, keys, g, spec["batch"], spec["exec_seed"])
 xh = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).pin_memory()
 out_id = "logits" if config == "c3" else g["outputs"][0] if "outputs" in g else "logits"
-for it in range(5):
+for it in range(int(os.environ.get("ITERS", "5"))):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     plan.bind_input("x", xh)
