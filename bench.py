@@ -186,8 +186,18 @@ def roofline_from_stats(stats: dict, peaks: dict, int_peak32: float):
     sec = st["total_ms"] / 1e3
     gbs = st["alg_bytes"] / sec / 1e9 if sec > 0 else 0.0
     hbm = peaks.get("hbm_gbs", 6552.6)
+    # DRAM bytes per launch of this kernel from the committed ncu --set full capture (profiles/)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            ent = json.load(f).get(name)
+        if ent:
+            traffic = ent["dram_bytes_per_launch"]
     rl = {"kernel": name, "bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
-          "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)",
+          "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/)",
+          "alg_bytes_per_launch": st["alg_bytes"] / max(1, st["launches"]),
+          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)",
           "launches_in_timed_region": st["launches"], "avg_launch_ms": st["total_ms"] / max(1, st["launches"])}
     mm = st["alg_modmuls"] / sec / 1e9 if sec > 0 else 0.0
     rl_int = {"kernel": name, "bound": "int-modmul", "achieved": mm, "peak": int_peak32 / 1e9,
