@@ -347,14 +347,18 @@ void ntt(const Context& c, uint64_t* base, int64_t rows_per_limb, int nl, int li
 void lift_ntt(const Context& c, const int64_t* src, uint64_t* out, int64_t items, int nl, cudaStream_t s);
 void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys, int nl, int64_t* cen, cudaStream_t s);
 void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_stride, int64_t b_stride,
-              int64_t a1_off, int64_t b1_off, uint64_t* c2, int64_t items, int nl, cudaStream_t s);
+              int64_t a1_off, int64_t b1_off, uint64_t* c2, int64_t items, int nl, cudaStream_t s,
+              uint64_t* d = nullptr);
 // grouped modular GEMM (same contract as k::gemm_groups), IMAD.WIDE accumulation
 void gemm(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* idx, const uint64_t* w,
           int64_t w_group_stride, const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt, int nl,
           cudaStream_t s);
-// given_d: a = size-3 input (d0, d1 taken from it); else d0/d1 from the tensor of a and b
+// given_d: a = size-3 input (d0, d1 taken from it); else d0/d1 from the tensor of a and b,
+// or, with d_in_out, already in `out` (written by relin_c2 with d = out) for the lanes
+// relin_d_in_out admits
 void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, int64_t a_stride,
-           int64_t b_stride, bool given_d, const uint64_t* c2, uint64_t* out, int64_t items, int nl, cudaStream_t s);
+           int64_t b_stride, bool given_d, const uint64_t* c2, uint64_t* out, int64_t items, int nl, cudaStream_t s,
+           bool d_in_out = false);
 
 // tcgen05 byte-split GEMM (hg_gemm_tc.cu).  Limbs are processed per residue
 // width (bytes = ceil(bits(q)/8)); weights pre-packed by pack_weights_tc for

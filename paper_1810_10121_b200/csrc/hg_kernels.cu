@@ -885,8 +885,11 @@ void mul_relin(const Context& c, const Keys& keys, const uint64_t* a, const uint
   check(keys.has_relin, HG_EINTERNAL, "relinearisation key missing");
   const int64_t pw = (int64_t)nl * c.n();
   if (c.logn() <= 14) {
-    k2::relin_c2(c, a, b, 2 * pw, 2 * pw, pw, pw, c2, items, nl, s);
-    k2::relin(c, keys, a, b, 2 * pw, 2 * pw, false, c2, out, items, nl, s);
+    // out must not alias the inputs: the prologue writes d0, d1 into it
+    check(out + items * 2 * pw <= a || a + items * 2 * pw <= out, HG_EINTERNAL, "relin output aliases its input");
+    check(out + items * 2 * pw <= b || b + items * 2 * pw <= out, HG_EINTERNAL, "relin output aliases its input");
+    k2::relin_c2(c, a, b, 2 * pw, 2 * pw, pw, pw, c2, items, nl, s, out);
+    k2::relin(c, keys, a, b, 2 * pw, 2 * pw, false, c2, out, items, nl, s, true);
     return;
   }
   const size_t sm = limb_smem(c);

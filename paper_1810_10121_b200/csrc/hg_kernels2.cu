@@ -220,18 +220,52 @@ __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_block
   }
 }
 
-// relinearisation prologue: c2 = INTT(a1 * b1) per (item, limb i)  (ckks_backend.hpp:509)
+// relinearisation prologue: c2 = INTT(a1 * b1) per (item, limb i)  (ckks_backend.hpp:509).
+// With d != nullptr it also writes the tensor terms d0 = a0 b0, d1 = a0 b1 + a1 b0
+// (ckks_backend.hpp:306-318) as out[item][2][nl][N], so the key switch only adds its
+// accumulators to them: the products leave the key-switch epilogue, where every warp
+// of the (one-CTA-per-SM) key switch would wait on their loads at once.
 HG_KERNEL k_relin_c2_t(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int64_t a_stride,
                        int64_t b_stride, int64_t a1_off, int64_t b1_off, uint64_t* __restrict__ c2, int nl,
-                       int64_t items, int G, const LimbList LL, const CtxParams P) {
+                       int64_t items, int G, const LimbList LL, const CtxParams P, uint64_t* __restrict__ d) {
   extern __shared__ __align__(16) uint64_t smem[];
   Cta<W, LOGN> c(smem, LL, items, G, P, true);
   constexpr int n = 1 << LOGN;
   const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
+  const bool square = a == b && a_stride == b_stride && a1_off == b1_off;
+  const uint64_t Q = c.L->q;
   for (int r = c.r0; r < c.r1; ++r) {
     const uint64_t* x1 = a + r * a_stride + a1_off + (int64_t)c.limb * n;
     const uint64_t* y1 = b + r * b_stride + b1_off + (int64_t)c.limb * n;
-    for (int k = threadIdx.x; k < n; k += lz::lz_threads<LOGN>()) c.s[lz::padw<W>(k)] = (W)mul_mod(x1[k], y1[k], *c.L);
+    if (d != nullptr) {
+      const uint64_t* x0 = a + r * a_stride + (int64_t)c.limb * n;
+      const uint64_t* y0 = b + r * b_stride + (int64_t)c.limb * n;
+      uint64_t* d0 = d + (int64_t)r * 2 * nl * n + (int64_t)c.limb * n;
+      uint64_t* d1 = d0 + (int64_t)nl * n;
+      const ulonglong2* x02 = reinterpret_cast<const ulonglong2*>(x0);
+      const ulonglong2* x12 = reinterpret_cast<const ulonglong2*>(x1);
+      const ulonglong2* y02 = reinterpret_cast<const ulonglong2*>(y0);
+      const ulonglong2* y12 = reinterpret_cast<const ulonglong2*>(y1);
+      for (int k = threadIdx.x; k < n / 2; k += lz::lz_threads<LOGN>()) {
+        const ulonglong2 u0 = __ldg(x02 + k), u1 = __ldg(x12 + k);
+        const ulonglong2 v0 = square ? u0 : __ldg(y02 + k), v1 = square ? u1 : __ldg(y12 + k);
+        uint64_t e0[2], e1[2], e2[2];
+        const uint64_t a0_[2] = {u0.x, u0.y}, a1_[2] = {u1.x, u1.y}, b0_[2] = {v0.x, v0.y}, b1_[2] = {v1.x, v1.y};
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          e0[e] = mul_mod(a0_[e], b0_[e], *c.L);
+          const uint64_t m01 = mul_mod(a0_[e], b1_[e], *c.L);
+          e1[e] = square ? add_mod(m01, m01, Q) : add_mod(m01, mul_mod(a1_[e], b0_[e], *c.L), Q);
+          e2[e] = mul_mod(a1_[e], b1_[e], *c.L);
+        }
+        reinterpret_cast<ulonglong2*>(d0)[k] = make_ulonglong2(e0[0], e0[1]);
+        reinterpret_cast<ulonglong2*>(d1)[k] = make_ulonglong2(e1[0], e1[1]);
+        c.s[lz::padw<W>(2 * k)] = (W)e2[0];
+        c.s[lz::padw<W>(2 * k + 1)] = (W)e2[1];
+      }
+    } else {
+      for (int k = threadIdx.x; k < n; k += lz::lz_threads<LOGN>()) c.s[lz::padw<W>(k)] = (W)mul_mod(x1[k], y1[k], *c.L);
+    }
     __syncthreads();
     lz::inv<W, LOGN>(c.s, c.tw, Lz<W>::ninv(*c.L), q, q2);
     lz::store<W, LOGN>(c2 + ((int64_t)r * nl + c.limb) * n, c.s);
@@ -249,7 +283,8 @@ HG_KERNEL k_relin_c2_t(const uint64_t* __restrict__ a, const uint64_t* __restric
 // which is L2-resident while the CTA works on it).
 //   32-bit limbs: packed key words (ws32 << 32 | w); acc += lazy Shoup in [0, 2q)
 //   64-bit limbs: key value + 64-bit Shoup constant; acc canonical
-// Epilogue adds d0 = a0 b0, d1 = a0 b1 + a1 b0 (or given d0, d1).
+// Epilogue adds d0 = a0 b0, d1 = a0 b1 + a1 b0 (or given d0, d1; `a` may then be `out`
+// itself, each word read and rewritten by the same thread).
 // ---------------------------------------------------------------------------
 struct RelinC {
   int rows0[HG_MAX_LIMBS];
@@ -276,6 +311,13 @@ struct RelinCfg {
   static constexpr size_t smem = Cfg<W, LOGN>::smem + (C2S ? ((size_t)8 << LOGN) : 0) + (KS ? key_bytes : 0);
   static constexpr size_t ks_off = Cfg<W, LOGN>::smem + (C2S ? ((size_t)8 << LOGN) : 0);
 };
+// Lanes whose key switch (ring degree 2^LOGN) keeps its accumulators in registers: there the
+// relin prologue writes d0, d1 into the output and the key switch adds to them in place.
+// (64-bit limbs at 2^14 accumulate in the output itself, so they compute d0, d1 at the end.)
+template <typename W, int LOGN>
+constexpr bool relin_d_in_out() {
+  return !(std::is_integral_v<W> && sizeof(W) == 8 && LOGN >= 14);
+}
 // conflict-free slot of 16-byte key chunk c (thread t reads chunks 4t .. 4t+3 with LDS.128)
 __device__ __forceinline__ int key_slot(int c) { return c ^ ((c >> 2) & 7); }
 // -q^{-1} mod 2^32 (Newton), for the Montgomery key MAC
@@ -290,14 +332,18 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
 }
+// bulk prefetch of [p, p + bytes) into L2 (bytes a multiple of 16)
+__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 template <typename W, int LOGN, bool GIVEN_D, bool SPLIT = false>
 __global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT>::threads, 1)
-    k_relin_t(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int64_t a_stride, int64_t b_stride,
+    k_relin_t(const uint64_t* a, const uint64_t* __restrict__ b, int64_t a_stride, int64_t b_stride,
               const uint64_t* __restrict__ c2, const uint64_t* __restrict__ kval,
-              const uint64_t* __restrict__ kpack, const uint32_t* __restrict__ kmont, uint64_t* __restrict__ out,
+              const uint64_t* __restrict__ kpack, const uint32_t* __restrict__ kmont, uint64_t* out,
               int nl, int64_t items, int G, const RelinC K, const LimbList LL, const CtxParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
   const int half = SPLIT ? (int)(blockIdx.x & 1) : 0;
@@ -352,6 +398,14 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT>::threads, 1)
     const uint64_t* c2item = c2 + (int64_t)item * pw;
     for (int i = 0; i < nl; ++i) {
       const uint64_t* src = c2item + (int64_t)i * nfull;
+      if constexpr (GIVEN_D) {
+        // the epilogue's d0, d1 rows -> L2 while the last residue's digits run
+        if (i == nl - 1 && threadIdx.x == 0) {
+          const uint64_t* p0 = a + (int64_t)item * a_stride + (int64_t)j * nfull + hoff;
+          l2_prefetch(p0, n * 8);
+          l2_prefetch(p0 + pw, n * 8);
+        }
+      }
       if constexpr (C2S) {
         if (item == c.r0 && i == 0) stage_c2(src);  // first residue of the group: nothing prefetched yet
         cp_async_wait_all();
@@ -504,6 +558,18 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT>::threads, 1)
       uint64_t* o1 = o0 + pw;
       const uint64_t* p0 = a + (int64_t)item * a_stride + (int64_t)j * nfull + hoff + k0;
       const uint64_t* p1 = p0 + pw;
+      uint64_t dv0[16], dv1[16];
+      if constexpr (GIVEN_D) {
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          const ulonglong2 v0 = reinterpret_cast<const ulonglong2*>(p0)[h];
+          const ulonglong2 v1 = reinterpret_cast<const ulonglong2*>(p1)[h];
+          dv0[2 * h] = v0.x;
+          dv0[2 * h + 1] = v0.y;
+          dv1[2 * h] = v1.x;
+          dv1[2 * h + 1] = v1.y;
+        }
+      }
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
         uint64_t r0, r1;
@@ -525,16 +591,28 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT>::threads, 1)
         }
         uint64_t d0, d1;
         if constexpr (GIVEN_D) {
-          d0 = p0[r];
-          d1 = p1[r];
+          d0 = dv0[r];
+          d1 = dv1[r];
         } else {
           const uint64_t* q0 = b + (int64_t)item * b_stride + (int64_t)j * nfull + hoff + k0;
           const uint64_t x0 = p0[r], x1 = p1[r], y0 = q0[r], y1 = q0[pw + r];
           d0 = mul_mod(x0, y0, *c.L);
           d1 = add_mod(mul_mod(x0, y1, *c.L), mul_mod(x1, y0, *c.L), Q);
         }
-        o0[r] = add_mod(r0, d0, Q);
-        o1[r] = add_mod(r1, d1, Q);
+        if constexpr (GIVEN_D) {
+          dv0[r] = add_mod(r0, d0, Q);
+          dv1[r] = add_mod(r1, d1, Q);
+        } else {
+          o0[r] = add_mod(r0, d0, Q);
+          o1[r] = add_mod(r1, d1, Q);
+        }
+      }
+      if constexpr (GIVEN_D) {
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          reinterpret_cast<ulonglong2*>(o0)[h] = make_ulonglong2(dv0[2 * h], dv0[2 * h + 1]);
+          reinterpret_cast<ulonglong2*>(o1)[h] = make_ulonglong2(dv1[2 * h], dv1[2 * h + 1]);
+        }
       }
     }
   }
@@ -992,7 +1070,8 @@ static RelinC relin_consts(const Context& c, int nl) {
 bool relin_supported(const Context& c) { return c.logn() >= 10 && c.logn() <= 14; }
 
 void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, int64_t a_stride,
-           int64_t b_stride, bool given_d, const uint64_t* c2, uint64_t* out, int64_t items, int nl, cudaStream_t s) {
+           int64_t b_stride, bool given_d, const uint64_t* c2, uint64_t* out, int64_t items, int nl, cudaStream_t s,
+           bool d_in_out) {
   check(relin_supported(c), HG_EINTERNAL, "key switch: ring degree outside 2^10..2^14");
   if (items <= 0) return;
   const RelinC K = relin_consts(c, nl);
@@ -1015,15 +1094,20 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
         const int G = (int)std::max<int64_t>(
             1, std::min<int64_t>(16, (items * LL.count * halves + target - 1) / target));
         const unsigned grid = (unsigned)(LL.count * ((items + G - 1) / G) * halves);
+        // d_in_out: relin_c2 already wrote d0, d1 into `out` for this lane; add to them in place
+        const bool in_out = !given_d && d_in_out && relin_d_in_out<W_, LOGN>();
+        const bool gd = given_d || in_out;
+        const uint64_t* aa = in_out ? out : a;
+        const int64_t as = in_out ? 2LL * nl * c.n() : a_stride;
         const void* fn =
-            given_d ? (const void*)k_relin_t<W_, LT, true, SPLIT> : (const void*)k_relin_t<W_, LT, false, SPLIT>;
+            gd ? (const void*)k_relin_t<W_, LT, true, SPLIT> : (const void*)k_relin_t<W_, LT, false, SPLIT>;
         set_smem_attr(fn, Cf::smem);
         const double frac = (double)LL.count / nl;
         c.kt_begin(std::is_floating_point_v<W_> ? "k_relin_t/f64" : sizeof(W_) == 4 ? "k_relin_t/u32" : "k_relin_t/u64", s, frac * (items * pw8 * 7 + (double)sd * 2 * pw8),
                    (double)items * LL.count * (sd * (bfly(c) + 2.0 * c.n()) + 3.0 * c.n()));
-        if (given_d)
+        if (gd)
           k_relin_t<W_, LT, true, SPLIT><<<grid, threads, Cf::smem, s>>>(
-              a, b, a_stride, b_stride, c2, keys.relin.as<uint64_t>(), keys.relin_pack.as<uint64_t>(),
+              aa, b, as, b_stride, c2, keys.relin.as<uint64_t>(), keys.relin_pack.as<uint64_t>(),
               keys.relin_mont.as<uint32_t>(), out, nl, items, G, K, LL, c.kp());
         else
           k_relin_t<W_, LT, false, SPLIT><<<grid, threads, Cf::smem, s>>>(
@@ -1040,7 +1124,7 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
 }
 
 void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_stride, int64_t b_stride,
-              int64_t a1_off, int64_t b1_off, uint64_t* c2, int64_t items, int nl, cudaStream_t s) {
+              int64_t a1_off, int64_t b1_off, uint64_t* c2, int64_t items, int nl, cudaStream_t s, uint64_t* d) {
   if (items <= 0) return;
   const Classes cl = classify(c, 0, nl, fp64_lane());
   const double nw = (double)c.n() * 8;
@@ -1052,10 +1136,15 @@ void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_
       unsigned grid;
       int G;
       grid_for<W_, LOGN>(LL, items, grid, G);
+      // the tensor terms go to d only for lanes whose key switch adds to them (relin_d_in_out)
+      uint64_t* dd = d != nullptr && relin_d_in_out<W_, LOGN>() ? d : nullptr;
+      const bool sq = a == b && a_stride == b_stride && a1_off == b1_off;
       set_smem_attr((const void*)k_relin_c2_t<W_, LOGN>, Cf::smem);
-      c.kt_begin(std::is_floating_point_v<W_> ? "k_relin_c2_t/f64" : sizeof(W_) == 4 ? "k_relin_c2_t/u32" : "k_relin_c2_t/u64", s, (double)items * LL.count * 3 * nw, (double)items * LL.count * (bfly(c) + c.n()));
+      c.kt_begin(std::is_floating_point_v<W_> ? "k_relin_c2_t/f64" : sizeof(W_) == 4 ? "k_relin_c2_t/u32" : "k_relin_c2_t/u64", s,
+                 (double)items * LL.count * (dd ? (sq ? 5 : 7) : 3) * nw,
+                 (double)items * LL.count * (bfly(c) + c.n() * (dd ? 4 : 1)));
       k_relin_c2_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(a, b, a_stride, b_stride, a1_off, b1_off, c2, nl,
-                                                                 items, G, LL, c.kp());
+                                                                 items, G, LL, c.kp(), dd);
       c.kt_end(s);
       HG_CUDA(cudaGetLastError());
     });
