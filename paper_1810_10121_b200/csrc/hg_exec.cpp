@@ -556,6 +556,15 @@ struct hg_plan {
   uint64_t seed = 1;
   hg::Rng rng{1};
   std::map<std::string, hg::Val> bound;
+  // per-parameter device buffers kept across bind_input calls of the same shape (staged
+  // values, plaintexts, ciphertexts): re-binding reuses them instead of growing the
+  // stream-ordered pool while the previous binding is still alive
+  struct BindBufs {
+    std::shared_ptr<hg::DevArr> staged, pt;
+    size_t staged_bytes = 0, pt_bytes = 0;
+    std::shared_ptr<hg::CtT> ct;
+  };
+  std::map<std::string, BindBufs> bind_bufs;
   std::map<std::string, hg::Val> outputs;
   std::map<std::string, hg::NodeCache> cache;
   hg::Profile prof;
@@ -572,6 +581,7 @@ struct hg_plan {
   // (a non-zero count re-runs the step with synchronous sampling)
   int* sample_flags = nullptr;  // pinned host ints
   int sample_flag_cap = 0, sample_flag_used = 0;
+  int64_t sampler_reruns = 0;  // runs redone with host sampler fix-ups (diagnostic, cumulative)
   bool in_run = false, sync_sampling = false;
   std::map<std::string, hg::Val>* live = nullptr;  // the running step's values (in-process group transport)
 };
@@ -726,12 +736,14 @@ void host_parallel(int64_t n, const std::function<void(int64_t)>& body) {
 // array [cols][nl][N] (ckks_backend.hpp:182-197): bit-exact fp64 FFT + llround
 // on the GPU (hg_encode.cu), then lift + forward NTT per limb.
 std::shared_ptr<DevArr> encode_device(hg_plan* P, const double* dvals, int64_t cols, int64_t count, int64_t col_stride,
-                                      int64_t elem_stride, int level, double scale) {
+                                      int64_t elem_stride, int level, double scale,
+                                      std::shared_ptr<DevArr> reuse = nullptr) {
   const Context& c = *P->ctx;
   const int64_t n = c.n();
   check(level >= 0 && level <= c.max_level(), HG_EVALIDATION, "level outside the modulus chain");
   check(scale > 0.0, HG_EVALIDATION, "encoding scale must be positive");
-  auto pt = std::make_shared<DevArr>(static_cast<size_t>(cols) * (level + 1) * n * 8, S(P));
+  // reuse: a caller-owned array of exactly cols * (level + 1) * N words
+  auto pt = reuse ? std::move(reuse) : std::make_shared<DevArr>(static_cast<size_t>(cols) * (level + 1) * n * 8, S(P));
   if (cols == 0) return pt;
   DevArr ci(static_cast<size_t>(cols * n) * 8, S(P));
   DevArr flag(sizeof(int), S(P));
@@ -2141,6 +2153,7 @@ void run_plan(hg_plan* P) {
   arm_sample_flags(P);
   run_plan_once(P);
   if (sample_flags_hit(P)) {  // rare (values within 1e-9 of a rounding boundary): redo with host fix-ups
+    P->sampler_reruns += 1;
     P->sync_sampling = true;
     try {
       run_plan_once(P);
@@ -2322,15 +2335,33 @@ int hg_plan_bind_input(hg_plan* P, const char* param_id, const double* values, i
     cudaPointerAttributes pa{};
     const bool on_device = cudaPointerGetAttributes(&pa, values) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
     (void)cudaGetLastError();
-    std::unique_ptr<hg::DevArr> staged;
+    auto& bb = P->bind_bufs[param_id];
     const double* dvals = values;
     if (!on_device) {
-      staged = std::make_unique<hg::DevArr>(static_cast<size_t>(count) * 8, hg::S(P));
-      HG_CUDA(cudaMemcpyAsync(staged->p, values, static_cast<size_t>(count) * 8, cudaMemcpyHostToDevice, hg::S(P)));
-      dvals = staged->as<double>();
+      const size_t sb = static_cast<size_t>(count) * 8;
+      if (!bb.staged || bb.staged_bytes != sb) {
+        bb.staged = std::make_shared<hg::DevArr>(sb, hg::S(P));
+        bb.staged_bytes = sb;
+      }
+      HG_CUDA(cudaMemcpyAsync(bb.staged->p, values, sb, cudaMemcpyHostToDevice, hg::S(P)));
+      dvals = bb.staged->as<double>();
     }
-    auto pt = hg::encode_device(P, dvals, nb, P->batch, 1, nb, L, c.default_scale());
-    auto ct = hg::new_ct(P, nb, L, c.default_scale());
+    const size_t pb = static_cast<size_t>(nb) * (L + 1) * c.n() * 8;
+    if (!bb.pt || bb.pt_bytes != pb) {
+      bb.pt = std::make_shared<hg::DevArr>(pb, hg::S(P));
+      bb.pt_bytes = pb;
+    }
+    auto pt = hg::encode_device(P, dvals, nb, P->batch, 1, nb, L, c.default_scale(), bb.pt);
+    // the previous ciphertexts are rewritten in place when only the plan holds them (the
+    // bound value and this cache); stream order puts the writes after earlier runs' reads
+    auto bt = P->bound.find(param_id);
+    const long holders = (bt != P->bound.end() && bt->second.ct == bb.ct) ? 2 : 1;
+    std::shared_ptr<hg::CtT> ct;
+    if (bb.ct && bb.ct->count == nb && bb.ct->level == L && bb.ct.use_count() == holders &&
+        bb.ct->scale == c.default_scale())
+      ct = bb.ct;
+    else
+      ct = bb.ct = hg::new_ct(P, nb, L, c.default_scale());
     hg::encrypt_items(P, seeds, pt->as<uint64_t>(), L, ct->p);
     hg::Val v;
     v.shape = shape;
@@ -2648,7 +2679,8 @@ int hg_plan_profile_json(hg_plan* P, char* buf, size_t cap) {
                         {"peak_elements", P->prof.peak_elements},
                         {"total_wall_ms", P->prof.total_wall_ms},
                         {"host_issue_ms", host},
-                        {"gpu_launches", P->launches}};
+                        {"gpu_launches", P->launches},
+                        {"sampler_reruns", P->sampler_reruns}};
     const std::string s = j.dump();
     hg::check(s.size() + 1 <= cap, HG_E_VALIDATION, "profile buffer too small");
     std::memcpy(buf, s.c_str(), s.size() + 1);

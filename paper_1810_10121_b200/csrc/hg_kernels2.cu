@@ -101,18 +101,61 @@ __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_block
   }
 }
 
-// lift signed int64 polys (one per item) into limb j, forward NTT: out[item][nl][N]
+struct RescaleC {
+  uint64_t inv[HG_MAX_LIMBS];
+  uint64_t inv_s[HG_MAX_LIMBS];
+  uint32_t inv_s32[HG_MAX_LIMBS];  // floor(inv 2^32 / q_j) for q_j < 2^30
+};
+
+// the centred top-limb value v as a residue of limb j in the lane's lazy input range
+template <typename W, typename CT>
+__device__ __forceinline__ W lift_cen(CT v, const LimbInfo& L, uint32_t mu32) {
+  if constexpr (sizeof(CT) == 4 && std::is_floating_point_v<W>) {
+    return (double)v;  // |v| < 2^30 <= q_j: a signed fp64-lane residue
+  } else if constexpr (sizeof(CT) == 4 && sizeof(W) == 4) {
+    // |v| < 2^30, q_j < 2^30: |v| mod q_j by a Shoup product with 1 (mu32 = floor(2^32 / q_j))
+    const uint32_t q = (uint32_t)L.q, av = (uint32_t)(v < 0 ? -v : v);
+    uint32_t r = av - __umulhi(av, mu32) * q;
+    r = r >= q ? r - q : r;
+    return (v < 0 && r != 0) ? q - r : r;
+  } else {
+    return (W)lift_signed((int64_t)v, L);
+  }
+}
+
+// lift signed int64 polys (one per item) into limb j, forward NTT: out[item][nl][N].
+// The lift is fused into the first pass (int32-range coefficients, the common case
+// for encoded values, take the 32-bit path) and the last pass stores from registers.
 HG_KERNEL k_lift_ntt_t(const int64_t* __restrict__ src, uint64_t* __restrict__ out, int nl, int64_t items, int G,
                        const LimbList LL, const CtxParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
   Cta<W, LOGN> c(smem, LL, items, G, P, false);
   constexpr int n = 1 << LOGN;
   const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
+  const uint32_t mu32 = (uint32_t)((1ULL << 32) / c.L->q);
+  const int64_t small = std::is_floating_point_v<W> ? (int64_t)c.L->q : ((int64_t)1 << 31);
   for (int r = c.r0; r < c.r1; ++r) {
     const int64_t* g = src + (int64_t)r * n;
-    for (int i = threadIdx.x; i < n; i += lz::lz_threads<LOGN>()) c.s[lz::padw<W>(i)] = (W)lift_signed(g[i], *c.L);
+    lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
+      const int64_t v = __ldg(g + k);
+      // |v| < 2^31 (32-bit lane) or |v| < q (fp64 lane): the cheap centred-lift path
+      if (v > -small && v < small) {
+        if constexpr (std::is_floating_point_v<W>) return (double)v;  // a signed fp64-lane residue
+        else return lift_cen<W, int32_t>((int32_t)v, *c.L, mu32);
+      }
+      return (W)lift_signed(v, *c.L);
+    }, c.tw, q, q2);
+    lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2);
+    // last pass back to shared memory, then coalesced 16-byte stores (measured faster than
+    // storing each thread's 16 consecutive words straight from registers)
+    for (int vt = threadIdx.x; vt < (n >> 4); vt += lz::lz_threads<LOGN>()) {
+      W y[16];
+      lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, y);
+      const int pb = lz::padw<W>(vt << 4);
+#pragma unroll
+      for (int h = 0; h < 16; ++h) c.s[pb + h] = canon4<W>(y[h], q, q2);
+    }
     __syncthreads();
-    lz::fwd<W, LOGN>(c.s, c.tw, q, q2);
     lz::store<W, LOGN>(out + ((int64_t)r * nl + c.limb) * n, c.s);
     __syncthreads();
   }
@@ -139,28 +182,6 @@ __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_block
       o[i] = (CT)(v > half ? (int64_t)v - (int64_t)c.L->q : (int64_t)v);
     }
     __syncthreads();
-  }
-}
-
-struct RescaleC {
-  uint64_t inv[HG_MAX_LIMBS];
-  uint64_t inv_s[HG_MAX_LIMBS];
-  uint32_t inv_s32[HG_MAX_LIMBS];  // floor(inv 2^32 / q_j) for q_j < 2^30
-};
-
-// the centred top-limb value v as a residue of limb j in the lane's lazy input range
-template <typename W, typename CT>
-__device__ __forceinline__ W lift_cen(CT v, const LimbInfo& L, uint32_t mu32) {
-  if constexpr (sizeof(CT) == 4 && std::is_floating_point_v<W>) {
-    return (double)v;  // |v| < 2^30 <= q_j: a signed fp64-lane residue
-  } else if constexpr (sizeof(CT) == 4 && sizeof(W) == 4) {
-    // |v| < 2^30, q_j < 2^30: |v| mod q_j by a Shoup product with 1 (mu32 = floor(2^32 / q_j))
-    const uint32_t q = (uint32_t)L.q, av = (uint32_t)(v < 0 ? -v : v);
-    uint32_t r = av - __umulhi(av, mu32) * q;
-    r = r >= q ? r - q : r;
-    return (v < 0 && r != 0) ? q - r : r;
-  } else {
-    return (W)lift_signed((int64_t)v, L);
   }
 }
 

@@ -29,7 +29,7 @@ for it in range(int(os.environ.get("ITERS", "5"))):
     out = plan.output(out_id)
     t3 = time.perf_counter()
     print(f"iter {it}: bind {1e3 * (t1 - t0):.2f} ms  run {1e3 * (t2 - t1):.2f} ms  output {1e3 * (t3 - t2):.2f} ms  "
-          f"total {1e3 * (t3 - t0):.2f} ms")
+          f"total {1e3 * (t3 - t0):.2f} ms  reruns {plan.profile().get('sampler_reruns')}")
 ctx.kernel_timing(True)
 ctx.kernel_stats()
 plan.bind_input("x", xh)
