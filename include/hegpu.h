@@ -113,6 +113,13 @@ int hg_square_relin_rescale(hg_context* ctx, const hg_keys* keys, const uint64_t
  * w: device residues [(groups*mg)*kt][nl]; idx: device int32 [groups*kt]. out has nl-1 limbs. */
 int hg_weighted_sum(hg_context* ctx, const uint64_t* x, const int32_t* idx, const uint64_t* w, uint64_t* out,
                     int64_t groups, int mg, int kt, int nl);
+/* Ciphertext-weight sum (weighted_sum_cipher, ckks_backend.hpp:413-450; the EncryptedBoth /
+ * EncryptedModel contraction, runtime.hpp:1053-1073, 605-617):
+ *   out[g] = rescale( relinearize( sum_t  x[xidx[g*kt+t]] (x) w[widx[g*kt+t]] ) )
+ * x, w: size-2 items at nl limbs, same level and scales; xidx, widx: device int32 [groups*kt].
+ * The size-3 products are accumulated exactly, relinearised ONCE and rescaled once. */
+int hg_weighted_sum_cipher(hg_context* ctx, const hg_keys* keys, const uint64_t* x, const int32_t* xidx,
+                           const uint64_t* w, const int32_t* widx, uint64_t* out, int64_t groups, int kt, int nl);
 
 /* ---- encoding / encryption (ckks_backend.hpp:182-249) ---- */
 /* values (host or device) -> device plaintext (NTT form, nl = level+1 limbs).  Replaces

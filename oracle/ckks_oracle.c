@@ -891,3 +891,21 @@ int oc_weighted_sum(const oc_ctx* c, int level, int terms, const uint64_t* const
   free(acc); free(pt);
   return 0;
 }
+
+void oc_weighted_sum_cipher(const oc_ctx* c, const oc_keys* k, int level, int terms, const uint64_t* const* xs,
+                            const uint64_t* const* ws, uint64_t* out) { /* ckks_backend.hpp:413-450 */
+  /* size-3 accumulation of every x_t (x) w_t tensor product (poly_mul_acc, 437-440), one
+     relinearisation (446), one rescale of each poly (448-450) */
+  const int64_t W = (int64_t)(level + 1) * c->n;
+  uint64_t* acc = calloc((size_t)(3 * W), sizeof(uint64_t));
+  uint64_t* r2 = malloc(sizeof(uint64_t) * 2 * W);
+  for (int t = 0; t < terms; ++t) {
+    pw_mul_acc(c, level, xs[t], ws[t], acc);
+    pw_mul_acc(c, level, xs[t], ws[t] + W, acc + W);
+    pw_mul_acc(c, level, xs[t] + W, ws[t], acc + W);
+    pw_mul_acc(c, level, xs[t] + W, ws[t] + W, acc + 2 * W);
+  }
+  oc_relinearize(c, k, level, acc, r2);
+  oc_rescale_ct(c, level, 2, r2, out);
+  free(acc); free(r2);
+}

@@ -125,6 +125,9 @@ void oc_relinearize(const oc_ctx* c, const oc_keys* k, int level, const uint64_t
 void oc_rescale_ct(const oc_ctx* c, int level, int size, const uint64_t* in, uint64_t* out);
 /* fused weighted sum (ckks_backend.hpp:381-411): xs[t] size-2 at level, weights as scalars
  * encoded with encode_constant(w[t], level, q_level); output rescaled to level-1. */
+/* sum_t x_t (x) w_t (size 3), relinearised once, rescaled: ct x ct weighted sum (ckks_backend.hpp:413-450) */
+void oc_weighted_sum_cipher(const oc_ctx* c, const oc_keys* k, int level, int terms, const uint64_t* const* xs,
+                            const uint64_t* const* ws, uint64_t* out);
 int oc_weighted_sum(const oc_ctx* c, int level, int terms, const uint64_t* const* xs, const double* w,
                     uint64_t* out);
 

@@ -72,6 +72,8 @@ def lib():
         L.oc_multiply_norelin.argtypes = [C.c_void_p, C.c_int, u64p, u64p, u64p]
         L.oc_relinearize.argtypes = [C.c_void_p, C.c_void_p, C.c_int, u64p, u64p]
         L.oc_rescale_ct.argtypes = [C.c_void_p, C.c_int, C.c_int, u64p, u64p]
+        L.oc_weighted_sum_cipher.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.POINTER(u64p),
+                                             C.POINTER(u64p), u64p]
         L.oc_weighted_sum.restype = C.c_int
         L.oc_weighted_sum.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(u64p), f64p, u64p]
         L.oc_crt_centered.restype = C.c_double
@@ -216,6 +218,14 @@ class Context:
     def rescale(self, level, ct, size=2):
         o = np.empty(size * level * self.n, dtype=np.uint64)
         lib().oc_rescale_ct(self._h, level, size, _p(ct), _p(o))
+        return o
+
+    def weighted_sum_cipher(self, keys, level, xs, ws):
+        """sum_t xs[t] (x) ws[t] relinearised once and rescaled (ckks_backend.hpp:413-450)."""
+        xa = (u64p * len(xs))(*[_p(x) for x in xs])
+        wa = (u64p * len(ws))(*[_p(w) for w in ws])
+        o = np.empty(2 * level * self.n, dtype=np.uint64)
+        lib().oc_weighted_sum_cipher(self._h, keys._h, level, len(xs), xa, wa, _p(o))
         return o
 
     def weighted_sum(self, level, xs, ws):

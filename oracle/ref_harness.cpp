@@ -201,6 +201,19 @@ int mode_prims(int argc, char** argv) {
   d.u64("weighted_sum", flat_ct(*wsum));
   d.meta("weighted_sum_meta", ct_meta(*wsum));
 
+  // ct x ct weighted sum (weighted_sum_cipher, ckks_backend.hpp:413-450): the first three
+  // encryptions above against encrypted constant weights, as the executor's cipher_handles
+  // makes them (encode_constant at the top level and default scale, then encrypt).
+  std::vector<CiphertextPtr> cxs, cws;
+  for (int t = 0; t < 3; ++t) {
+    cxs.push_back(xs[static_cast<size_t>(t)]);
+    cws.push_back(be.encrypt(*be.encode_constant(wv[static_cast<size_t>(t)], L, scale), 4000 + t));
+    d.u64("wsc_w" + std::to_string(t), flat_ct(*cws.back()));
+  }
+  auto wsc = be.weighted_sum_cipher(cxs, cws);
+  d.u64("weighted_sum_cipher", flat_ct(*wsc));
+  d.meta("weighted_sum_cipher_meta", ct_meta(*wsc));
+
   // Decrypt.
   d.f64("dec_ct1", be.decrypt(*c1, slots));
   d.f64("dec_mul_relin_rescale", be.decrypt(*mr, slots));

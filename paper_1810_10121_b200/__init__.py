@@ -84,6 +84,7 @@ def lib():
         "hg_relinearize": (C.c_int, [vp, vp, vp, vp, C.c_int64, C.c_int]),
         "hg_square_relin_rescale": (C.c_int, [vp, vp, vp, vp, C.c_int64, C.c_int]),
         "hg_weighted_sum": (C.c_int, [vp, vp, vp, vp, vp, C.c_int64, C.c_int, C.c_int, C.c_int]),
+        "hg_weighted_sum_cipher": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, C.c_int64, C.c_int, C.c_int]),
         "hg_encode": (C.c_int, [vp, f64p, C.c_int64, C.c_int, C.c_double, vp]),
         "hg_comm_unique_id": (C.c_int, [vp]),
         "hg_plan_set_comm": (C.c_int, [vp, C.c_int, C.c_int, vp]),

@@ -236,6 +236,25 @@ int hg_weighted_sum(hg_context* ctx, const uint64_t* x, const int32_t* idx, cons
   });
 }
 
+int hg_weighted_sum_cipher(hg_context* ctx, const hg_keys* keys, const uint64_t* x, const int32_t* xidx,
+                           const uint64_t* w, const int32_t* widx, uint64_t* out, int64_t groups, int kt, int nl) {
+  return guard([&] {
+    hg::check(nl >= 2, HG_E_DEPTH, "multiplicative depth exceeded: no level left to rescale");
+    hg::check(groups >= 0 && kt >= 1, HG_E_VALIDATION, "weighted sum needs matching non-empty operands");
+    hg::check(keys->k->has_relin, HG_E_VALIDATION, "weighted_sum_cipher needs a relinearisation key");
+    hg::Context& c = *ctx->c;
+    if (groups == 0) return;
+    const int64_t pw = static_cast<int64_t>(nl) * c.n();
+    auto* acc3 = static_cast<uint64_t*>(c.scratch(static_cast<size_t>(groups * 3 * pw * 8), 3));
+    auto* c2 = static_cast<uint64_t*>(c.scratch(static_cast<size_t>(groups * pw * 8), 2));
+    auto* r2 = static_cast<uint64_t*>(c.scratch(static_cast<size_t>(groups * 2 * pw * 8), 4));
+    auto* sc = static_cast<int64_t*>(c.scratch(static_cast<size_t>(groups * 2 * c.n() * 8), 1));
+    hg::k::tensor_acc(c, x, xidx, w, widx, acc3, groups, kt, nl, ctx->stream());
+    hg::k::relin3(c, *keys->k, acc3, r2, groups, nl, c2, ctx->stream());
+    hg::k::rescale(c, r2, out, groups * 2, nl, sc, ctx->stream());
+  });
+}
+
 static void encode_batch_impl(hg_context* ctx, const double* values, int64_t cols, int64_t count, int64_t col_stride,
                               int64_t elem_stride, int level, double scale, uint64_t* pt_dev) {
   hg::Context& c = *ctx->c;

@@ -307,6 +307,9 @@ void mul_relin(const Context& c, const Keys& keys, const uint64_t* a, const uint
 void mul_tensor(const Context& c, const uint64_t* a, const uint64_t* b, uint64_t* out, int64_t items, int nl,
                 cudaStream_t s);
 // relinearize size-3 items -> size-2
+// sum_t x[xi[g kt + t]] (x) w[wi[g kt + t]] -> out3[g][3][nl][N] (weighted_sum_cipher accumulation)
+void tensor_acc(const Context& c, const uint64_t* x, const int32_t* xi, const uint64_t* w, const int32_t* wi,
+                uint64_t* out3, int64_t groups, int kt, int nl, cudaStream_t s);
 void relin3(const Context& c, const Keys& keys, const uint64_t* in3, uint64_t* out2, int64_t items, int nl,
             uint64_t* c2scratch, cudaStream_t s);
 // fresh encryption from host samples (int64 [items][3][N]: u, e0, e1) at nl limbs; optional plaintext per item

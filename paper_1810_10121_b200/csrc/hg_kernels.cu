@@ -571,6 +571,32 @@ __global__ void k_tensor(const uint64_t* __restrict__ a, const uint64_t* __restr
   }
 }
 
+// sum over kt terms of ct x ct tensor products (the size-3 accumulation of
+// weighted_sum_cipher, ckks_backend.hpp:428-441): out[g][3][nl][N]
+__global__ void k_tensor_acc(const uint64_t* __restrict__ x, const int32_t* __restrict__ xi,
+                             const uint64_t* __restrict__ w, const int32_t* __restrict__ wi, uint64_t* __restrict__ out,
+                             int64_t groups, int kt, int nl, const CtxParams P) {
+  const int64_t n = P.n, pw = nl * n;
+  const int64_t words = groups * pw;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < words; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = v / pw, lw = v - g * pw;
+    const LimbInfo& L = P.limb[lw / n];
+    uint64_t a0 = 0, a1 = 0, a2 = 0;
+    for (int t = 0; t < kt; ++t) {
+      const uint64_t* xp = x + (int64_t)xi[g * kt + t] * 2 * pw + lw;
+      const uint64_t* wp = w + (int64_t)wi[g * kt + t] * 2 * pw + lw;
+      const uint64_t x0 = xp[0], x1 = xp[pw], y0 = wp[0], y1 = wp[pw];
+      a0 = add_mod(a0, mul_mod(x0, y0, L), L.q);
+      a1 = add_mod(a1, add_mod(mul_mod(x0, y1, L), mul_mod(x1, y0, L), L.q), L.q);
+      a2 = add_mod(a2, mul_mod(x1, y1, L), L.q);
+    }
+    uint64_t* o = out + g * 3 * pw + lw;
+    o[0] = a0;
+    o[pw] = a1;
+    o[2 * pw] = a2;
+  }
+}
+
 // --------------------------------------------------------------------------
 // Encryption / decryption / keygen pointwise kernels
 // --------------------------------------------------------------------------
@@ -911,14 +937,24 @@ void mul_tensor(const Context& c, const uint64_t* a, const uint64_t* b, uint64_t
   HG_CUDA(cudaGetLastError());
 }
 
+void tensor_acc(const Context& c, const uint64_t* x, const int32_t* xi, const uint64_t* w, const int32_t* wi,
+                uint64_t* out3, int64_t groups, int kt, int nl, cudaStream_t s) {
+  const int64_t words = groups * nl * c.n();
+  if (words <= 0) return;
+  c.kt_begin("k_tensor_acc", s, (double)(groups * kt * 4 + groups * 3) * nl * c.n() * 8,
+             (double)groups * kt * 4 * nl * c.n());
+  k_tensor_acc<<<ew_blocks(words, 256), 256, 0, s>>>(x, xi, w, wi, out3, groups, kt, nl, c.kp());
+  c.kt_end(s);
+  HG_CUDA(cudaGetLastError());
+}
+
 void relin3(const Context& c, const Keys& keys, const uint64_t* in3, uint64_t* out2, int64_t items, int nl,
             uint64_t* c2, cudaStream_t s) {
   if (items <= 0) return;
   check(keys.has_relin, HG_EINTERNAL, "relinearisation key missing");
   const int64_t pw = (int64_t)nl * c.n();
-  // c2 = INTT(d2): copy d2 rows then inverse NTT
-  for (int64_t it = 0; it < items; ++it)
-    HG_CUDA(cudaMemcpyAsync(c2 + it * pw, in3 + it * 3 * pw + 2 * pw, pw * 8, cudaMemcpyDeviceToDevice, s));
+  // c2 = INTT(d2): copy d2 rows (one strided copy) then inverse NTT
+  HG_CUDA(cudaMemcpy2DAsync(c2, pw * 8, in3 + 2 * pw, 3 * pw * 8, pw * 8, items, cudaMemcpyDeviceToDevice, s));
   ntt(c, c2, items * nl, nl, true, s);
   if (c.logn() <= 14) {
     k2::relin(c, keys, in3, nullptr, 3 * pw, 0, true, c2, out2, items, nl, s);

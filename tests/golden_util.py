@@ -99,6 +99,11 @@ def oracle_prims(name: str) -> dict:
         out[f"ws_x{t}"] = xs[-1]
     out["ws_weights"] = np.array(wv)
     out["weighted_sum"] = ctx.weighted_sum(L, xs, wv)
+    cws = []
+    for t in range(3):
+        cws.append(ctx.encrypt(keys, ctx.encode_constant(wv[t], L, scale), L, 4000 + t))
+        out[f"wsc_w{t}"] = cws[-1]
+    out["weighted_sum_cipher"] = ctx.weighted_sum_cipher(keys, L, xs[:3], cws)
     out["dec_ct1"] = ctx.decrypt(keys, c1, L, scale, slots)
     mr_scale = scale * scale / float(ctx.primes[L])
     out["dec_mul_relin_rescale"] = ctx.decrypt(keys, mr, L - 1, mr_scale, slots)

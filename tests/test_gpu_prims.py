@@ -196,6 +196,66 @@ def test_weighted_sum(case):
     expect(g, "weighted_sum", host(out))
 
 
+def test_weighted_sum_cipher(case):
+    """ct x ct weighted sum (ckks_backend.hpp:413-450): one relinearisation, one rescale,
+    bit-exact against the reference's weighted_sum_cipher."""
+    import paper_1810_10121_b200 as P
+
+    g, ctx, keys = case
+    L, nl, n = ctx.L, ctx.L + 1, ctx.n
+    xs, ws = [], []
+    wv = [0.37, -1.25, 0.0625]
+    for t in range(3):
+        v = np.full(n // 2, 0.1 * (t + 1))
+        pt = empty(ctx.words(L))
+        P.call("hg_encode", ctx, v.ctypes.data_as(P.f64p), v.size, L, ctx.default_scale, pt)
+        c = empty(2 * ctx.words(L))
+        seeds = np.array([3000 + t], dtype=np.uint64)
+        P.call("hg_encrypt", ctx, keys, pt, seeds.ctypes.data_as(P.u64p), 1, L, c)
+        xs.append(host(c))
+        r = np.zeros(nl, dtype=np.uint64)
+        P.call("hg_encode_constant", ctx, wv[t], L, ctx.default_scale, r.ctypes.data_as(P.u64p))
+        ptw = np.repeat(r, n)  # a constant plaintext: every NTT coefficient equals the residue
+        cw = empty(2 * ctx.words(L))
+        seeds = np.array([4000 + t], dtype=np.uint64)
+        P.call("hg_encrypt", ctx, keys, dev(ptw), seeds.ctypes.data_as(P.u64p), 1, L, cw)
+        ws.append(host(cw))
+    for t in range(3):
+        expect(g, f"wsc_w{t}", ws[t])
+    idx = _torch().tensor([0, 1, 2], dtype=_torch().int32, device="cuda")
+    out = empty(2 * ctx.words(L - 1))
+    P.call("hg_weighted_sum_cipher", ctx, keys, dev(np.concatenate(xs)), idx, dev(np.concatenate(ws)), idx, out, 1, 3,
+           nl)
+    expect(g, "weighted_sum_cipher", host(out))
+
+
+def test_weighted_sum_cipher_groups_match_oracle(cuda_ok):
+    """Several output groups with shared, permuted operand lists vs the C oracle."""
+    import paper_1810_10121_b200 as P
+    from oracle import oracle as O
+
+    n, bits, sb = 2048, [36, 26, 26, 36], 26
+    ctx = P.Context(n, bits, sb, security=0)
+    keys = P.Keys(ctx, 9)
+    octx = O.Context(n, bits, sb)
+    okeys = O.Keys(octx, 9)
+    L = octx.L
+    rng = np.random.default_rng(3)
+    cts = [octx.encrypt(okeys, octx.encode(rng.uniform(-1, 1, n // 2), L, octx.scale), L, 50 + i) for i in range(6)]
+    xi = np.array([0, 1, 2, 3, 2, 5, 4, 0], dtype=np.int32)  # 4 groups x 2 terms
+    wi = np.array([5, 4, 3, 2, 1, 0, 1, 1], dtype=np.int32)
+    X = dev(np.concatenate(cts))
+    out = empty(4 * 2 * octx.words(L - 1))
+    t = _torch()
+    P.call("hg_weighted_sum_cipher", ctx, keys, X, t.tensor(xi, device="cuda"), X, t.tensor(wi, device="cuda"), out, 4,
+           2, L + 1)
+    got = host(out).reshape(4, -1)
+    for gi in range(4):
+        want = octx.weighted_sum_cipher(okeys, L, [cts[xi[2 * gi]], cts[xi[2 * gi + 1]]],
+                                        [cts[wi[2 * gi]], cts[wi[2 * gi + 1]]])
+        assert np.array_equal(got[gi], want), f"group {gi}"
+
+
 def test_batched_square_matches_oracle(case, cuda_ok):
     """multiply_rescale(x, x) on a batch of 3 ciphertexts vs the C oracle."""
     import paper_1810_10121_b200 as P
