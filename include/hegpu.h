@@ -157,6 +157,11 @@ int hg_plan_create(hg_context* ctx, const hg_keys* keys, const char* graph_json,
                    hg_plan** out);
 void hg_plan_destroy(hg_plan* plan);
 /* encode + encrypt a Parameter's batch (host row-major values, batch * prod(shape[1:]))  */
+/* ExecOptions (runtime.hpp:158-166) as JSON, before binding inputs: {"paradigm": "encrypted-data" |
+ * "encrypted-model" | "encrypted-both", "bypass": {"optimized_multiply": bool,
+ * "optimized_addition": bool, "epsilon": double}}.  Replaces the ExecOptions argument of
+ * heg::execute (runtime.hpp:1970-1974); the default is encrypted-data with bypass on, eps 0. */
+int hg_plan_set_options(hg_plan* plan, const char* options_json);
 int hg_plan_bind_input(hg_plan* plan, const char* param_id, const double* values, int64_t count);
 /* server-side graph run: ciphertexts stay in HBM, no host round trip between nodes */
 int hg_plan_run(hg_plan* plan);

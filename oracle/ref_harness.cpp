@@ -304,11 +304,13 @@ int mode_net(int argc, char** argv) {
   const std::string outprefix = argv[12];
   bool dump = true;
   int repeat = 1, warmup = 0;
+  std::string paradigm = "encrypted-data";
   for (int a = 13; a < argc; ++a) {
     const std::string f = argv[a];
     if (f == "--no-dump") dump = false;
     else if (f.rfind("--repeat=", 0) == 0) repeat = std::max(1, std::stoi(f.substr(9)));
     else if (f.rfind("--warmup=", 0) == 0) warmup = std::max(0, std::stoi(f.substr(9)));
+    else if (f.rfind("--paradigm=", 0) == 0) paradigm = f.substr(11);
   }
 
   Graph graph = graph_from_json(load_json_file(graph_path));
@@ -338,6 +340,7 @@ int mode_net(int argc, char** argv) {
   ExecOptions opts;
   opts.threads = threads;
   opts.seed = exec_seed;
+  opts.paradigm = parse_paradigm(paradigm);
   // untimed warm-up executes, then `repeat` timed ones (bench.py --impl reference)
   std::vector<double> runs_ms;
   for (int w = 0; w < warmup; ++w) {

@@ -106,6 +106,7 @@ def lib():
         "hg_plan_create": (C.c_int, [vp, vp, C.c_char_p, C.c_int64, C.c_uint64, C.POINTER(vp)]),
         "hg_plan_destroy": (None, [vp]),
         "hg_plan_bind_input": (C.c_int, [vp, C.c_char_p, vp, C.c_int64]),
+        "hg_plan_set_options": (C.c_int, [vp, C.c_char_p]),
         "hg_plan_run": (C.c_int, [vp]),
         "hg_plan_output": (C.c_int, [vp, C.c_char_p, f64p, C.c_int64, C.POINTER(C.c_int64)]),
         "hg_plan_output_info": (C.c_int, [vp, C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int),
@@ -289,6 +290,17 @@ class Plan:
         self.ctx = ctx
         self.keys = keys
         self.batch = batch
+
+    def set_options(self, paradigm: str | None = None, bypass: dict | None = None):
+        """ExecOptions (runtime.hpp:158-166): paradigm and bypass config, before bind_input."""
+        import json as _json
+
+        opts = {}
+        if paradigm is not None:
+            opts["paradigm"] = paradigm
+        if bypass is not None:
+            opts["bypass"] = bypass
+        _chk(lib().hg_plan_set_options(self._h, _json.dumps(opts).encode()))
 
     def bind_input(self, param_id: str, values):
         """values: [batch, *shape] float64 -- numpy, or a contiguous torch tensor (pinned host or cuda)."""

@@ -572,6 +572,11 @@ struct hg_plan {
   // bypass config (runtime.hpp:84-88 defaults)
   bool opt_mul = true, opt_add = true;
   double eps = 0.0;
+  // ExecOptions::paradigm (runtime.hpp:44-52): 0 EncryptedData, 1 EncryptedModel, 2 EncryptedBoth
+  int paradigm = 0;
+  // encrypted model constants, per producing node and element count (cipher_handles,
+  // runtime.hpp:413-435); a pure function of the seed, so kept across runs (model load)
+  std::map<std::string, std::shared_ptr<hg::CtT>> const_cipher;
   // output-sharded execution over `world` ranks (one GPU each); the transport
   // all-gathers a sharded tensor where a consumer needs every element
   int rank = 0, world = 1;
@@ -821,6 +826,69 @@ std::shared_ptr<CtT> rescale_t(hg_plan* P, const std::shared_ptr<CtT>& x) {  // 
 }
 
 // ---------------------------------------------------------------------------
+// Paradigms (runtime.hpp:44-52, 370-377, 413-435): under EncryptedModel and
+// EncryptedBoth the graph's constants are encrypted where they meet the data.
+// ---------------------------------------------------------------------------
+enum class Side { Cipher, Numbers };
+bool constants_stay_plain(const hg_plan* P) { return P->paradigm == 0; }  // runtime.hpp:257-259
+Side side_of(const hg_plan* P, const Val& v) {                              // runtime.hpp:373-377
+  if (v.is_cipher()) return Side::Cipher;
+  return (v.from_constants && !constants_stay_plain(P)) ? Side::Cipher : Side::Numbers;
+}
+
+// encode_raw(rv, e, level, scale) for every element e < m: batch columns through the GPU
+// encoder, scalars as encode_constant rows (runtime.hpp:406-409) -> [m][level+1][N]
+std::shared_ptr<DevArr> encode_raw_all(hg_plan* P, const RawView& rv, int64_t m, int level, double scale) {
+  const Context& c = *P->ctx;
+  const int nl = level + 1;
+  if (rv.column) {
+    DevArr d(static_cast<size_t>(rv.t->count()) * 8, S(P));
+    HG_CUDA(cudaMemcpyAsync(d.p, rv.t->v.data(), static_cast<size_t>(rv.t->count()) * 8, cudaMemcpyHostToDevice, S(P)));
+    // column e, slot b at values[b * m + e] (packing.hpp:57-63)
+    return encode_device(P, d.as<double>(), m, P->batch, 1, m, level, scale);  // synchronises
+  }
+  std::vector<uint64_t> res(static_cast<size_t>(m) * nl);
+  for (int64_t e = 0; e < m; ++e) {
+    const int64_t q = llround_checked(rv.t->v[e], scale);
+    for (int j = 0; j < nl; ++j) res[e * nl + j] = lift_signed_h(q, c.primes()[j]);
+  }
+  DevArr dres(res.size() * 8, S(P));
+  HG_CUDA(cudaMemcpyAsync(dres.p, res.data(), res.size() * 8, cudaMemcpyHostToDevice, S(P)));
+  auto pt = std::make_shared<DevArr>(static_cast<size_t>(m) * nl * c.n() * 8, S(P));
+  k::expand_rows(c, dres.as<uint64_t>(), pt->as<uint64_t>(), m * nl, S(P));
+  P->launches += 1;
+  HG_CUDA(cudaStreamSynchronize(S(P)));  // `res` is pageable
+  return pt;
+}
+
+// Ciphertext handles of an operand: its own ciphertexts, or its constants encrypted at the
+// top level and default scale with seeds rng.fork("constants").fork(id#m) (runtime.hpp:413-435)
+std::shared_ptr<CtT> cipher_handles(hg_plan* P, const Val& v, const std::string& id, int64_t m) {
+  if (v.is_cipher()) {
+    check(v.ct->count == m, HG_EVALIDATION,
+          "a batch-packed tensor cannot be used where " + std::to_string(m) + " independent elements are expected");
+    return v.ct;
+  }
+  check(v.is_raw(), HG_EINTERNAL, "cipher handles of a scheme-plaintext value");
+  const std::string key = id + "#" + std::to_string(m);
+  auto it = P->const_cipher.find(key);
+  if (it != P->const_cipher.end()) return it->second;
+  const Context& c = *P->ctx;
+  const int L = c.max_level();
+  const double scale = c.default_scale();
+  const RawView rv = raw_view(P, v, m);
+  auto pt = encode_raw_all(P, rv, m, L, scale);
+  Rng rng = P->rng.fork("constants").fork(key);
+  std::vector<uint64_t> seeds(static_cast<size_t>(m));
+  for (auto& sd : seeds) sd = rng.next();
+  auto ct = new_ct(P, m, L, scale);
+  encrypt_items(P, seeds, pt->as<uint64_t>(), L, ct->p);
+  P->launches += 2;
+  P->const_cipher.emplace(key, ct);
+  return ct;
+}
+
+// ---------------------------------------------------------------------------
 // Node kernels
 // ---------------------------------------------------------------------------
 
@@ -831,11 +899,90 @@ struct TermPlan {  // runtime.hpp:475-481
   int64_t skipped = 0;
 };
 
+// Contractions with an encrypted weight side (runtime.hpp:1053-1073, 1090-1129):
+//   Cipher x Cipher  -> weighted_sum_cipher per output (size-3 sum, one relin, one rescale)
+//   Numbers x Cipher -> weighted_sum of the encrypted weights with the data's batch columns
+//                       encoded at the operand scale (EncryptedModel's first contraction)
+Val contraction_paradigm(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_shape, bool out_batched,
+                         const Val& x, const Val& w, int64_t groups, int mg, int kt,
+                         const std::function<void(int64_t g, int m, int64_t& out_e)>& out_index,
+                         const std::function<void(int64_t g, int t, int64_t& x_e)>& x_index,
+                         const std::function<void(int64_t g, int m, int t, int64_t& w_e)>& w_index) {
+  const Context& c = *P->ctx;
+  check(P->world == 1, HG_EVALIDATION,
+        "node '" + node.id + "': encrypted-weight contractions are not sharded on the GPU path");
+  const Side sx = side_of(P, x), sw = side_of(P, w);
+  const int64_t m_out = groups * mg;
+  const int64_t x_space = x.is_cipher() ? x.ct->count : (x.batched ? x.raw->count() / P->batch : x.raw->count());
+  const int64_t w_space = w.is_cipher() ? w.ct->count : (w.batched ? w.raw->count() / P->batch : w.raw->count());
+  // term lists by output element (terms_of, runtime.hpp:1029-1035)
+  std::vector<int32_t> xi(static_cast<size_t>(m_out * kt)), wi(static_cast<size_t>(m_out * kt));
+  for (int64_t g = 0; g < groups; ++g)
+    for (int m = 0; m < mg; ++m) {
+      int64_t oe;
+      out_index(g, m, oe);
+      check(oe >= 0 && oe < m_out, HG_EINTERNAL, "contraction output index out of range");
+      for (int t = 0; t < kt; ++t) {
+        int64_t xe, we;
+        x_index(g, t, xe);
+        w_index(g, m, t, we);
+        xi[oe * kt + t] = static_cast<int32_t>(xe);
+        wi[oe * kt + t] = static_cast<int32_t>(we);
+      }
+    }
+  DevArr dxi(xi.size() * 4, S(P)), dwi(wi.size() * 4, S(P));
+  HG_CUDA(cudaMemcpyAsync(dxi.p, xi.data(), xi.size() * 4, cudaMemcpyHostToDevice, S(P)));
+  HG_CUDA(cudaMemcpyAsync(dwi.p, wi.data(), wi.size() * 4, cudaMemcpyHostToDevice, S(P)));
+  Val out;
+  out.shape = out_shape;
+  out.batched = out_batched;
+  if (sx == Side::Cipher && sw == Side::Cipher) {
+    auto cx = cipher_handles(P, x, node.inputs[0], x_space);
+    auto cw = cipher_handles(P, w, node.inputs[1], w_space);
+    const int level = std::min(cx->level, cw->level);
+    require_mul_headroom(level);
+    cx = drop_to(P, cx, level);
+    cw = drop_to(P, cw, level);
+    P->prof.mul_ct += m_out * kt;
+    P->prof.add += m_out * (kt - 1);
+    const int nl = level + 1;
+    const int64_t pw = static_cast<int64_t>(nl) * c.n();
+    DevArr acc3(static_cast<size_t>(m_out * 3 * pw) * 8, S(P)), c2(static_cast<size_t>(m_out * pw) * 8, S(P));
+    auto r2 = new_ct(P, m_out, level, cx->scale * cw->scale);
+    k::tensor_acc(c, cx->p, dxi.as<int32_t>(), cw->p, dwi.as<int32_t>(), acc3.as<uint64_t>(), m_out, kt, nl, S(P));
+    k::relin3(c, *P->keys, acc3.as<uint64_t>(), r2->p, m_out, nl, c2.as<uint64_t>(), S(P));
+    P->launches += 4;
+    out.ct = rescale_t(P, r2);
+    HG_CUDA(cudaStreamSynchronize(S(P)));  // the host index vectors go out of scope
+    return out;
+  }
+  check(sx == Side::Numbers && sw == Side::Cipher, HG_EINTERNAL, "unsupported operand combination in contraction");
+  check(!x.from_constants, HG_EVALIDATION,
+        "node '" + node.id + "': constant x encrypted-data contractions are not supported on the GPU path");
+  auto cw = cipher_handles(P, w, node.inputs[1], w_space);
+  const int level = cw->level;
+  require_mul_headroom(level);
+  const RawView rv = raw_view(P, x, x_space);
+  const double w_scale = static_cast<double>(c.primes()[level]);  // operand_scale(level)
+  auto pts = encode_raw_all(P, rv, x_space, level, w_scale);
+  P->prof.mul_pt += m_out * kt;  // no bypass: the data side is not from constants
+  P->prof.add += m_out * (kt - 1);
+  auto prod = new_ct(P, m_out, level, cw->scale * w_scale);
+  k::ctpt_acc(c, cw->p, dwi.as<int32_t>(), pts->as<uint64_t>(), dxi.as<int32_t>(), prod->p, m_out, kt, level + 1,
+              S(P));
+  P->launches += 1;
+  out.ct = rescale_t(P, prod);
+  HG_CUDA(cudaStreamSynchronize(S(P)));
+  return out;
+}
+
 Val contraction(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_shape, bool out_batched, const Val& x,
                 const Val& w, int64_t groups, int mg, int kt,
                 const std::function<void(int64_t g, int m, int64_t& out_e)>& out_index,
                 const std::function<void(int64_t g, int t, int64_t& x_e)>& x_index,
                 const std::function<void(int64_t g, int m, int t, int64_t& w_e)>& w_index, bool w_shared) {
+  if (side_of(P, w) == Side::Cipher || side_of(P, x) == Side::Numbers)
+    return contraction_paradigm(P, node, out_shape, out_batched, x, w, groups, mg, kt, out_index, x_index, w_index);
   check(x.is_cipher(), HG_EVALIDATION, "node '" + node.id + "': only encrypted data x plaintext weights is supported");
   check(w.is_raw(), HG_EVALIDATION, "node '" + node.id + "': weights must be plaintext numbers (EncryptedData)");
   const Context& c = *P->ctx;
@@ -1314,6 +1461,31 @@ Val kernel_add_sub(hg_plan* P, const GNode& node, const std::vector<int64_t>& ou
   Val out;
   out.shape = out_shape;
   out.batched = out_batched;
+  if (side_of(P, a) == Side::Cipher && side_of(P, b) == Side::Cipher && (a.is_raw() || b.is_raw())) {
+    // an encrypted-model constant joins an addition: encrypted per element at the exact level
+    // and scale of the ciphertext it meets, seeds rng.fork("addend").fork(node).fork(e) (runtime.hpp:728-752)
+    const bool a_raw = a.is_raw();
+    const Val& cv = a_raw ? b : a;
+    const Val& rv_v = a_raw ? a : b;
+    check(cv.handles() == m, HG_EINTERNAL, "ciphertext operand layout mismatch");
+    const RawView rv = raw_view(P, rv_v, m);
+    const auto& x = cv.ct;
+    P->prof.add += m;
+    auto pt = encode_raw_all(P, rv, m, x->level, x->scale);
+    Rng node_rng = P->rng.fork("addend").fork(node.id);
+    std::vector<uint64_t> seeds(static_cast<size_t>(m));
+    for (int64_t e = 0; e < m; ++e) seeds[e] = node_rng.fork(static_cast<uint64_t>(e)).next();
+    auto kc = new_ct(P, m, x->level, x->scale);
+    encrypt_items(P, seeds, pt->as<uint64_t>(), x->level, kc->p);
+    auto o = new_ct(P, m, x->level, x->scale);
+    const uint64_t* lhs = a_raw ? kc->p : x->p;
+    const uint64_t* rhs = a_raw ? x->p : kc->p;
+    if (subtract) k::sub(c, lhs, rhs, o->p, o->words(), x->nl(), S(P));
+    else k::add(c, lhs, rhs, o->p, o->words(), x->nl(), S(P));
+    P->launches += 3;
+    out.ct = o;
+    return out;
+  }
   if (a.is_cipher() && b.is_cipher()) {
     P->prof.add += m;
     const int lv = std::min(a.ct->level, b.ct->level);
@@ -1326,15 +1498,16 @@ Val kernel_add_sub(hg_plan* P, const GNode& node, const std::vector<int64_t>& ou
     out.ct = o;
     return out;
   }
-  const bool raw_on_rhs = b.is_raw();
-  check((a.is_cipher() && b.is_raw()) || (a.is_raw() && b.is_cipher()), HG_EINTERNAL,
+  const Side sa = side_of(P, a), sb = side_of(P, b);
+  check((sa == Side::Cipher && sb == Side::Numbers) || (sa == Side::Numbers && sb == Side::Cipher), HG_EINTERNAL,
         "unsupported operand combination in add/subtract");
+  const bool raw_on_rhs = sb == Side::Numbers;
   const Val& cv = raw_on_rhs ? a : b;
   const Val& rv_v = raw_on_rhs ? b : a;
-  check(cv.handles() == m, HG_EVALIDATION, "a batch-packed tensor cannot be used here");
+  // the cipher side may be a model constant to encrypt (cipher_handles, runtime.hpp:778)
+  const auto x = cipher_handles(P, cv, node.inputs[raw_on_rhs ? 0 : 1], m);
   const RawView rv = raw_view(P, rv_v, m);
   const bool can_bypass = rv_v.from_constants;
-  const auto& x = cv.ct;
   NodeCache& C = P->cache[node.id];
   // counts + plaintexts (bypassed elements get a zero plaintext: x + 0 == x bit for bit)
   std::vector<std::vector<double>> cols;
@@ -1388,14 +1561,17 @@ Val kernel_add_sub(hg_plan* P, const GNode& node, const std::vector<int64_t>& ou
   return out;
 }
 
-Val kernel_negate(hg_plan* P, const Val& a) {
-  check(a.is_cipher(), HG_EVALIDATION, "negate expects a bound operand");
-  P->prof.negate += a.handles();
+Val kernel_negate(hg_plan* P, const GNode& node, const Val& a) {
   Val out;
   out.shape = a.shape;
   out.batched = a.batched;
-  auto o = new_ct(P, a.ct->count, a.ct->level, a.ct->scale);
-  k::negate(*P->ctx, a.ct->p, o->p, o->words(), o->nl(), S(P));
+  // raw constants under a model-encrypting paradigm: negated homomorphically (runtime.hpp:1005-1013)
+  const std::shared_ptr<CtT> x =
+      a.is_cipher() ? a.ct : cipher_handles(P, a, node.inputs[0], space_count(a.shape, a.batched));
+  check(x != nullptr, HG_EVALIDATION, "negate expects a bound operand");
+  P->prof.negate += x->count;
+  auto o = new_ct(P, x->count, x->level, x->scale);
+  k::negate(*P->ctx, x->p, o->p, o->words(), o->nl(), S(P));
   P->launches += 1;
   out.ct = o;
   return out;
@@ -1409,11 +1585,13 @@ Val kernel_multiply(hg_plan* P, const GNode& node, const std::vector<int64_t>& o
   Val out;
   out.shape = out_shape;
   out.batched = out_batched;
-  if (a.is_cipher() && b.is_cipher()) {
+  if (side_of(P, a) == Side::Cipher && side_of(P, b) == Side::Cipher) {
+    // multiply_rescale of the (lazily encrypted) handles at their common level (runtime.hpp:868-880)
+    auto ca = cipher_handles(P, a, node.inputs[0], m), cb = cipher_handles(P, b, node.inputs[1], m);
     P->prof.mul_ct += m;
-    const int lv = std::min(a.ct->level, b.ct->level);
+    const int lv = std::min(ca->level, cb->level);
     require_mul_headroom(lv);
-    auto xa = drop_to(P, a.ct, lv), xb = drop_to(P, b.ct, lv);
+    auto xa = drop_to(P, ca, lv), xb = drop_to(P, cb, lv);
     auto prod = new_ct(P, m, lv, xa->scale * xb->scale);
     DevArr c2(static_cast<size_t>(m) * (lv + 1) * c.n() * 8, S(P));
     k::mul_relin(c, *P->keys, xa->p, xb->p, prod->p, m, lv + 1, c2.as<uint64_t>(), S(P));
@@ -1421,12 +1599,14 @@ Val kernel_multiply(hg_plan* P, const GNode& node, const std::vector<int64_t>& o
     out.ct = rescale_t(P, prod);
     return out;
   }
-  const Val& cv = a.is_cipher() ? a : b;
-  const Val& rv_v = a.is_cipher() ? b : a;
-  check(cv.is_cipher() && rv_v.is_raw(), HG_EINTERNAL, "unsupported operand combination in multiply");
+  const bool a_cipher = side_of(P, a) == Side::Cipher;
+  const Val& cv = a_cipher ? a : b;
+  const Val& rv_v = a_cipher ? b : a;
+  check(side_of(P, cv) == Side::Cipher && rv_v.is_raw() && side_of(P, rv_v) == Side::Numbers, HG_EINTERNAL,
+        "unsupported operand combination in multiply");
+  const auto x = cipher_handles(P, cv, node.inputs[a_cipher ? 0 : 1], m);
   const RawView rv = raw_view(P, rv_v, m);
   const bool can_bypass = rv_v.from_constants;
-  const auto& x = cv.ct;
   std::vector<Action> act(static_cast<size_t>(m), Action::Proceed);
   int n_proceed = 0, n_one = 0, n_neg = 0, n_zero = 0;
   for (int64_t e = 0; e < m; ++e) {
@@ -1908,7 +2088,7 @@ bool pm_one_constant(const Graph& g, const std::string& id) {
 }
 
 void admit_depth(const hg_plan* P) {
-  const bool aware = P->opt_mul;  // EncryptedData keeps constants plain
+  const bool aware = P->opt_mul && P->paradigm == 0;  // runtime.hpp:299: only plain constants bypass
   std::set<std::string> reach;
   std::map<std::string, int64_t> depth;
   std::map<std::string, std::string> argmax;
@@ -1980,12 +2160,15 @@ Val exec_node(hg_plan* P, const GNode& node, const std::vector<const Val*>& in) 
     v.raw = node.data;
     return v;
   }
-  bool all_raw = !in.empty(), all_const = true;
+  bool all_raw = !in.empty(), all_const = true, any_const = false;
   for (const Val* v : in) {
     all_raw = all_raw && v->is_raw();
     all_const = all_const && v->from_constants;
+    any_const = any_const || v->from_constants;
   }
-  if (all_raw) {  // constant folding on host (runtime.hpp:654-672)
+  // constant folding and EncryptedModel's client-side plain data path on host (runtime.hpp:648-672);
+  // model constants meeting plain data under a model-encrypting paradigm go to the kernels
+  if (all_raw && (constants_stay_plain(P) || all_const || !any_const)) {
     std::vector<const HTensor*> tin;
     for (const Val* v : in) tin.push_back(v->raw.get());
     Val out;
@@ -2008,13 +2191,9 @@ Val exec_node(hg_plan* P, const GNode& node, const std::vector<const Val*>& in) 
     case Op::Add:
     case Op::Subtract: return kernel_add_sub(P, node, out_shape, *in[0], *in[1], node.op == Op::Subtract);
     case Op::Multiply: return kernel_multiply(P, node, out_shape, *in[0], *in[1]);
-    case Op::Negate: return kernel_negate(P, *in[0]);
-    case Op::Dot:
-      if (in[1]->is_cipher()) fail(HG_EVALIDATION, "encrypted-model Dot is not supported on the GPU path");
-      return kernel_dot(P, node, out_shape, *in[0], *in[1]);
-    case Op::Convolution:
-      if (in[1]->is_cipher()) fail(HG_EVALIDATION, "encrypted-model Convolution is not supported on the GPU path");
-      return kernel_conv(P, node, out_shape, *in[0], *in[1]);
+    case Op::Negate: return kernel_negate(P, node, *in[0]);
+    case Op::Dot: return kernel_dot(P, node, out_shape, *in[0], *in[1]);
+    case Op::Convolution: return kernel_conv(P, node, out_shape, *in[0], *in[1]);
     case Op::AvgPool:
     case Op::ScaledMeanPool: return kernel_pool(P, node, out_shape, *in[0]);
     case Op::PolyAct: return kernel_poly_act(P, node, out_shape, *in[0]);
@@ -2154,6 +2333,7 @@ void run_plan(hg_plan* P) {
   run_plan_once(P);
   if (sample_flags_hit(P)) {  // rare (values within 1e-9 of a rounding boundary): redo with host fix-ups
     P->sampler_reruns += 1;
+    P->const_cipher.clear();  // re-encrypted with the synchronous fix-ups
     P->sync_sampling = true;
     try {
       run_plan_once(P);
@@ -2307,6 +2487,35 @@ int hg_plan_create(hg_context* ctx, const hg_keys* keys, const char* graph_json,
   });
 }
 
+int hg_plan_set_options(hg_plan* P, const char* options_json) {
+  // ExecOptions (runtime.hpp:158-166): {"paradigm": "encrypted-data" | "encrypted-model" |
+  // "encrypted-both", "bypass": {"optimized_multiply": b, "optimized_addition": b, "epsilon": x}}
+  return guard_x([&] {
+    hg::check(P && options_json, HG_E_VALIDATION, "null argument");
+    const auto j = hg::json::parse(options_json);
+    if (j.contains("paradigm")) {
+      const std::string name = j.at("paradigm").get<std::string>();
+      int pd = -1;
+      if (name == "encrypted-data" || name == "EncryptedData") pd = 0;
+      else if (name == "encrypted-model" || name == "EncryptedModel") pd = 1;
+      else if (name == "encrypted-both" || name == "EncryptedBoth") pd = 2;
+      hg::check(pd >= 0, HG_E_VALIDATION, "unknown paradigm '" + name + "' (plain-debug has no GPU path)");
+      hg::check(P->bound.empty(), HG_E_VALIDATION, "set the paradigm before binding inputs");
+      P->paradigm = pd;
+      P->const_cipher.clear();
+      P->cache.clear();
+    }
+    if (j.contains("bypass")) {
+      const auto& b = j.at("bypass");
+      if (b.contains("optimized_multiply")) P->opt_mul = b.at("optimized_multiply").get<bool>();
+      if (b.contains("optimized_addition")) P->opt_add = b.at("optimized_addition").get<bool>();
+      if (b.contains("epsilon")) P->eps = b.at("epsilon").get<double>();
+      P->cache.clear();
+    }
+    hg::admit_depth(P);
+  });
+}
+
 void hg_plan_destroy(hg_plan* plan) {
   if (!plan) return;
   cudaStreamSynchronize(plan->ctx->stream());
@@ -2335,6 +2544,21 @@ int hg_plan_bind_input(hg_plan* P, const char* param_id, const double* values, i
     cudaPointerAttributes pa{};
     const bool on_device = cudaPointerGetAttributes(&pa, values) == cudaSuccess && pa.type == cudaMemoryTypeDevice;
     (void)cudaGetLastError();
+    if (P->paradigm == 1) {
+      // EncryptedModel: the data stays in the clear (bind_parameter, runtime.hpp:358-360)
+      auto t = std::make_shared<hg::HTensor>();
+      t->shape = shape;
+      t->v.resize(static_cast<size_t>(count));
+      HG_CUDA(cudaMemcpy(t->v.data(), values, static_cast<size_t>(count) * 8,
+                         on_device ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+      hg::Val v;
+      v.shape = shape;
+      v.batched = true;
+      v.from_constants = false;
+      v.raw = t;
+      P->bound[param_id] = v;
+      return;
+    }
     auto& bb = P->bind_bufs[param_id];
     const double* dvals = values;
     if (!on_device) {

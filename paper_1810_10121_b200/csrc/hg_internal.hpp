@@ -310,6 +310,11 @@ void mul_tensor(const Context& c, const uint64_t* a, const uint64_t* b, uint64_t
 // sum_t x[xi[g kt + t]] (x) w[wi[g kt + t]] -> out3[g][3][nl][N] (weighted_sum_cipher accumulation)
 void tensor_acc(const Context& c, const uint64_t* x, const int32_t* xi, const uint64_t* w, const int32_t* wi,
                 uint64_t* out3, int64_t groups, int kt, int nl, cudaStream_t s);
+// sum_t ct[ci[g kt + t]] * pt[pi[g kt + t]] -> out2[g][2][nl][N] (weighted_sum with poly weights)
+void ctpt_acc(const Context& c, const uint64_t* ct, const int32_t* ci, const uint64_t* pt, const int32_t* pi,
+              uint64_t* out2, int64_t groups, int kt, int nl, cudaStream_t s);
+// rows[r][N] = residues[r] (device arrays)
+void expand_rows(const Context& c, const uint64_t* residues, uint64_t* rows, int64_t nrows, cudaStream_t s);
 void relin3(const Context& c, const Keys& keys, const uint64_t* in3, uint64_t* out2, int64_t items, int nl,
             uint64_t* c2scratch, cudaStream_t s);
 // fresh encryption from host samples (int64 [items][3][N]: u, e0, e1) at nl limbs; optional plaintext per item

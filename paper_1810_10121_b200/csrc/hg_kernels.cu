@@ -597,6 +597,35 @@ __global__ void k_tensor_acc(const uint64_t* __restrict__ x, const int32_t* __re
   }
 }
 
+// sum over kt terms of ct x pt products (weighted_sum with per-term plaintexts,
+// ckks_backend.hpp:381-404): out[g][2][nl][N] = sum_t ct[ci[g kt + t]] * pt[pi[g kt + t]]
+__global__ void k_ctpt_acc(const uint64_t* __restrict__ ct, const int32_t* __restrict__ ci,
+                           const uint64_t* __restrict__ pt, const int32_t* __restrict__ pi, uint64_t* __restrict__ out,
+                           int64_t groups, int kt, int nl, const CtxParams P) {
+  const int64_t n = P.n, pw = nl * n;
+  const int64_t words = groups * pw;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < words; v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = v / pw, lw = v - g * pw;
+    const LimbInfo& L = P.limb[lw / n];
+    uint64_t a0 = 0, a1 = 0;
+    for (int t = 0; t < kt; ++t) {
+      const uint64_t* cp = ct + (int64_t)ci[g * kt + t] * 2 * pw + lw;
+      const uint64_t w = pt[(int64_t)pi[g * kt + t] * pw + lw];
+      a0 = add_mod(a0, mul_mod(cp[0], w, L), L.q);
+      a1 = add_mod(a1, mul_mod(cp[pw], w, L), L.q);
+    }
+    out[g * 2 * pw + lw] = a0;
+    out[g * 2 * pw + pw + lw] = a1;
+  }
+}
+
+// rows[r][N] = residues[r] (a constant plaintext in NTT form: every evaluation equals it)
+__global__ void k_expand_rows(const uint64_t* __restrict__ residues, uint64_t* __restrict__ rows, int64_t nrows,
+                              int64_t n) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nrows * n; v += (int64_t)gridDim.x * blockDim.x)
+    rows[v] = residues[v / n];
+}
+
 // --------------------------------------------------------------------------
 // Encryption / decryption / keygen pointwise kernels
 // --------------------------------------------------------------------------
@@ -944,6 +973,25 @@ void tensor_acc(const Context& c, const uint64_t* x, const int32_t* xi, const ui
   c.kt_begin("k_tensor_acc", s, (double)(groups * kt * 4 + groups * 3) * nl * c.n() * 8,
              (double)groups * kt * 4 * nl * c.n());
   k_tensor_acc<<<ew_blocks(words, 256), 256, 0, s>>>(x, xi, w, wi, out3, groups, kt, nl, c.kp());
+  c.kt_end(s);
+  HG_CUDA(cudaGetLastError());
+}
+
+void ctpt_acc(const Context& c, const uint64_t* ct, const int32_t* ci, const uint64_t* pt, const int32_t* pi,
+              uint64_t* out2, int64_t groups, int kt, int nl, cudaStream_t s) {
+  const int64_t words = groups * nl * c.n();
+  if (words <= 0) return;
+  c.kt_begin("k_ctpt_acc", s, (double)(groups * kt * 3 + groups * 2) * nl * c.n() * 8,
+             (double)groups * kt * 2 * nl * c.n());
+  k_ctpt_acc<<<ew_blocks(words, 256), 256, 0, s>>>(ct, ci, pt, pi, out2, groups, kt, nl, c.kp());
+  c.kt_end(s);
+  HG_CUDA(cudaGetLastError());
+}
+
+void expand_rows(const Context& c, const uint64_t* residues, uint64_t* rows, int64_t nrows, cudaStream_t s) {
+  if (nrows <= 0) return;
+  c.kt_begin("k_expand_rows", s, (double)nrows * c.n() * 8, 0.0);
+  k_expand_rows<<<ew_blocks(nrows * c.n(), 256), 256, 0, s>>>(residues, rows, nrows, c.n());
   c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }

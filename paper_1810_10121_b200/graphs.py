@@ -251,6 +251,27 @@ def mini(seed: int, batch: int):
     return g.json(["mul", "fc"]), x
 
 
+def pmodel(seed: int, batch: int):
+    """Paradigm coverage graph (test-only; N=2048): Conv + channel bias, x^2, Dot + bias.  Run under
+    EncryptedModel (data in the clear, constants encrypted) and EncryptedBoth (both encrypted)."""
+    wr = Rng(seed).fork("pmodel")
+    g = G("paradigm_conv_dot")
+    g.param("x", [1, 1, 5, 5])
+    g.const("w1", gaussian_tensor(wr.fork("w1"), (2, 1, 3, 3), 1.0 / 9))
+    g.op("conv", "Convolution", ["x", "w1"], stride=1)
+    bias = g.channel_bias("b1", gaussian_tensor(wr.fork("b1"), (2,), 0.1), [1, 2, 3, 3], 1)
+    g.op("conv_b", "Add", ["conv", bias])
+    g.op("act", "PolyAct", ["conv_b"], a=1.0, b=0.0, c=0.0)
+    g.op("flat", "Reshape", ["act"], shape=[-1, 18])
+    g.const("w2", gaussian_tensor(wr.fork("w2"), (18, 3), 1.0 / 18))
+    g.op("fc", "Dot", ["flat", "w2"])
+    g.const("b2", gaussian_tensor(wr.fork("b2"), (3,), 0.1))
+    g.op("b2b", "Broadcast", ["b2"], shape=[-1, 3], axes=[0])
+    g.op("out", "Add", ["fc", "b2b"])
+    x = uniform_tensor(Rng(seed).fork("inputs").fork("x"), (batch, 1, 5, 5), -1.0, 1.0)
+    return g.json(["out"]), x
+
+
 def ops2(seed: int, batch: int):
     """Second coverage graph (test-only; N=2048): BatchNormInference, Sum, Negate and a
     Concat that promotes a batch-column constant to fresh encryptions."""
@@ -286,8 +307,8 @@ def key_seed(seed: int) -> int:
 def build(spec: dict):
     """spec: {"config": "c1"|"c3"|"c4"|"c5"|"mini", "batch": B, "seed": s} -> (graph, x, ctx params)."""
     cfg = spec["config"]
-    if cfg in ("mini", "ops2"):
-        g, x = (mini if cfg == "mini" else ops2)(spec["seed"], spec["batch"])
+    if cfg in ("mini", "ops2", "pmodel"):
+        g, x = {"mini": mini, "ops2": ops2, "pmodel": pmodel}[cfg](spec["seed"], spec["batch"])
         ctxp = dict(MINI_CONTEXT)
     else:
         g, x = CONFIGS[cfg](spec["seed"], spec["batch"])
@@ -307,6 +328,9 @@ def _spec(config, batch, seed=1, **kw):
 GOLDEN_NETS = {
     "mini": _spec("mini", 16, seed=3),
     "ops2": _spec("ops2", 16, seed=4),
+    "pmodel_m": _spec("pmodel", 16, seed=5, paradigm="encrypted-model"),
+    "pmodel_b": _spec("pmodel", 16, seed=5, paradigm="encrypted-both"),
+    "mini_b": _spec("mini", 16, seed=3, paradigm="encrypted-both"),
     "c1": _spec("c1", 4096),
     "c3_n2048": _spec("c3", 64, n=2048),
     "c5_n2048": _spec("c5", 64, n=2048),

@@ -97,7 +97,8 @@ def make_nets(which=None):
             pre = os.path.join(d, "out")
             subprocess.check_call([HARNESS, "net", gp, xp, str(spec["batch"]), str(ctxp["n"]), str(ctxp["scale_bits"]),
                                    ",".join(map(str, ctxp["bits"])), str(ctxp["security"]), str(spec["key_seed"]),
-                                   str(spec["exec_seed"]), str(spec.get("threads", os.cpu_count())), pre])
+                                   str(spec["exec_seed"]), str(spec.get("threads", os.cpu_count())), pre] +
+                                  ([f"--paradigm={spec['paradigm']}"] if "paradigm" in spec else []))
             with open(pre + ".json") as f:
                 res = json.load(f)
             cts = np.fromfile(pre + ".ct.bin", dtype=np.uint64)
