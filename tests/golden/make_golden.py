@@ -35,6 +35,9 @@ PRIM_CASES = {
     "n8192_40_30_40": (8192, 30, [40, 30, 40], 5),
     "n4096_30x4": (4096, 30, [30, 30, 30, 30], 17),
     "n16384_50_30x2_50": (16384, 30, [50, 30, 30, 50], 19),
+    # BASELINE config 2 (primitive sweep) shapes: 30-bit chains, L = 7 and L = 15, up to N = 2^15
+    "n16384_30x8": (16384, 30, [30] * 8, 29),
+    "n32768_30x16": (32768, 30, [30] * 16, 23),
 }
 
 
@@ -57,8 +60,10 @@ def sha(a: np.ndarray) -> str:
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
-def make_prims():
+def make_prims(only=None):
     for name, (n, sb, bits, key_seed) in PRIM_CASES.items():
+        if only and name not in only:
+            continue
         with tempfile.TemporaryDirectory() as d:
             subprocess.check_call([HARNESS, "prims", d, str(n), str(sb), ",".join(map(str, bits)), str(key_seed)])
             dump = load_dump(d)
@@ -141,7 +146,7 @@ def make_io():
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "prims"
     if what == "prims":
-        make_prims()
+        make_prims(sys.argv[2:] or None)
     elif what == "nets":
         make_nets(sys.argv[2:] or None)
     elif what == "io":
