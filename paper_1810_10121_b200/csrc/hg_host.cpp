@@ -341,11 +341,11 @@ Context::Context(const ContextParamsH& p, int device) : m_p(p), m_device(device)
           for (int64_t gi = 0; gi < nbi; ++gi)
             for (int64_t ii = 0; ii < per_i; ++ii) put(iwp, iwp32, iw, iw32, h + ii * nbi + gi, h + gi * per_i + ii);
         }
-      // Half transforms (N >= 2^14): after the first forward stage (distance N/2, twiddle
+      // Half transforms (N >= 2^12): after the first forward stage (distance N/2, twiddle
       // psi_1), the halves h = 0, 1 are independent (N/2)-point transforms whose stage-s
       // twiddles are tw[2^s + h 2^(s-1) + j'] -> as a table of their own, T_h[2^(s-1) + j'],
       // pass-ordered for logn - 1 like the tables above.
-      if (logn >= 14) {
+      if (logn >= 12) {
         const int lh = logn - 1, remh = lh & 3;
         const int64_t nh = n / 2;
         std::vector<std::pair<int, int>> ph;

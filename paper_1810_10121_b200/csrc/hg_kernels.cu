@@ -89,80 +89,107 @@ __global__ void __launch_bounds__(kNttThreads) k_lift_ntt(const int64_t* __restr
 // --------------------------------------------------------------------------
 // Elementwise (poly.hpp:87-152)
 // --------------------------------------------------------------------------
+// Row-vectorised: grid thread g handles the 16-byte vector g (two words) of the
+// [row][N] array; row = g >> (logn - 1) indexes [item][poly][limb], and the limb
+// (and item / poly) come from 32-bit divisions by small constants, once per vector.
+// Products of 32-bit limbs reduce with one 64-bit Barrett step (mulmod_ew);
+// wider limbs take the 128-bit Barrett of ring.hpp:52-63.
+
+// a * b mod q for a, b < q.  q < 2^32: p = a b < 2^64, floor(p / q) - 2 <= umulhi(p, br_hi)
+// with br_hi = floor(2^64 / q) (the high word of the Barrett constant floor(2^128 / q)).
+__device__ __forceinline__ uint64_t mulmod_ew(uint64_t a, uint64_t b, const LimbInfo& L) {
+  if (L.q >> 32) return mul_mod(a, b, L);
+  const uint64_t p = a * b;
+  uint64_t r = p - __umul64hi(p, L.br_hi) * L.q;
+  r = r >= L.q ? r - L.q : r;
+  return r >= L.q ? r - L.q : r;
+}
+
 template <int OP>  // 0 add, 1 sub, 2 negate
-__global__ void k_elementwise(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, uint64_t* __restrict__ o,
-                              int64_t words, int nl, const CtxParams P) {
-  const int64_t n = P.n;
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t q = P.limb[(w / n) % nl].q;
-    const uint64_t x = a[w];
-    if (OP == 0) o[w] = add_mod(x, b[w], q);
-    else if (OP == 1) o[w] = sub_mod(x, b[w], q);
-    else o[w] = neg_mod(x, q);
+__global__ void k_elementwise(const ulonglong2* __restrict__ a, const ulonglong2* __restrict__ b,
+                              ulonglong2* __restrict__ o, int64_t vecs, int nl, const CtxParams P) {
+  const int sh = P.logn - 1;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < vecs; g += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t q = P.limb[(int)((uint32_t)(g >> sh) % (uint32_t)nl)].q;
+    const ulonglong2 x = a[g];
+    ulonglong2 r;
+    if (OP == 0) {
+      const ulonglong2 y = b[g];
+      r = make_ulonglong2(add_mod(x.x, y.x, q), add_mod(x.y, y.y, q));
+    } else if (OP == 1) {
+      const ulonglong2 y = b[g];
+      r = make_ulonglong2(sub_mod(x.x, y.x, q), sub_mod(x.y, y.y, q));
+    } else {
+      r = make_ulonglong2(neg_mod(x.x, q), neg_mod(x.y, q));
+    }
+    o[g] = r;
   }
 }
 
 // ct (+/-) pt on poly 0 (ckks_backend.hpp:580-589); other polys copied
-__global__ void k_add_plain(const uint64_t* __restrict__ ct, const uint64_t* __restrict__ pt, uint64_t* __restrict__ o,
-                            int64_t items, int size, int nl, int pt_per_item, int subtract, const CtxParams P) {
-  const int64_t n = P.n;
-  const int64_t poly_words = nl * n;
-  const int64_t words = items * size * poly_words;
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t item = w / (size * poly_words);
-    const int64_t r = w - item * size * poly_words;
-    const int p = (int)(r / poly_words);
-    const int64_t lw = r - p * poly_words;
-    const uint64_t x = ct[w];
-    if (p == 0) {
-      const uint64_t q = P.limb[lw / n].q;
-      const uint64_t y = pt[(pt_per_item ? item * poly_words : 0) + lw];
-      o[w] = subtract ? sub_mod(x, y, q) : add_mod(x, y, q);
+__global__ void k_add_plain(const ulonglong2* __restrict__ ct, const ulonglong2* __restrict__ pt,
+                            ulonglong2* __restrict__ o, int64_t vecs, int size, int nl, int pt_per_item, int subtract,
+                            const CtxParams P) {
+  const int sh = P.logn - 1;
+  const int64_t vmask = ((int64_t)1 << sh) - 1;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < vecs; g += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t row = (uint32_t)(g >> sh), per = (uint32_t)(size * nl);
+    const uint32_t item = row / per, rem = row - item * per;
+    const ulonglong2 x = ct[g];
+    if (rem < (uint32_t)nl) {  // poly 0, limb rem
+      const uint64_t q = P.limb[rem].q;
+      const ulonglong2 y = pt[(((int64_t)(pt_per_item ? item * nl : 0) + rem) << sh) + (g & vmask)];
+      o[g] = subtract ? make_ulonglong2(sub_mod(x.x, y.x, q), sub_mod(x.y, y.y, q))
+                      : make_ulonglong2(add_mod(x.x, y.x, q), add_mod(x.y, y.y, q));
     } else {
-      o[w] = x;
+      o[g] = x;
     }
   }
 }
 
 // every poly times plaintext (ckks_backend.hpp:299-310, poly_mul NTT branch poly.hpp:130-136)
-__global__ void k_mul_plain(const uint64_t* __restrict__ ct, const uint64_t* __restrict__ pt, uint64_t* __restrict__ o,
-                            int64_t items, int size, int nl, int pt_per_item, const CtxParams P) {
-  const int64_t n = P.n;
-  const int64_t poly_words = nl * n;
-  const int64_t words = items * size * poly_words;
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t item = w / (size * poly_words);
-    const int64_t lw = (w - item * size * poly_words) % poly_words;
-    const LimbInfo& L = P.limb[lw / n];
-    o[w] = mul_mod(ct[w], pt[(pt_per_item ? item * poly_words : 0) + lw], L);
+__global__ void k_mul_plain(const ulonglong2* __restrict__ ct, const ulonglong2* __restrict__ pt,
+                            ulonglong2* __restrict__ o, int64_t vecs, int size, int nl, int pt_per_item,
+                            const CtxParams P) {
+  const int sh = P.logn - 1;
+  const int64_t vmask = ((int64_t)1 << sh) - 1;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < vecs; g += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t row = (uint32_t)(g >> sh), per = (uint32_t)(size * nl);
+    const uint32_t item = row / per, limb = (row - item * per) % (uint32_t)nl;
+    const LimbInfo& L = P.limb[limb];
+    const ulonglong2 x = ct[g];
+    const ulonglong2 y = pt[(((int64_t)(pt_per_item ? item * nl : 0) + limb) << sh) + (g & vmask)];
+    o[g] = make_ulonglong2(mulmod_ew(x.x, y.x, L), mulmod_ew(x.y, y.y, L));
   }
 }
 
 // every poly times a per-limb scalar (encode_constant in NTT form: ckks_backend.hpp:199-216)
-__global__ void k_mul_scalar(const uint64_t* __restrict__ ct, const uint64_t* __restrict__ wl, uint64_t* __restrict__ o,
-                             int64_t words, int nl, const CtxParams P) {
-  const int64_t n = P.n;
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
-    const int limb = (int)((w / n) % nl);
-    o[w] = mul_mod(ct[w], wl[limb], P.limb[limb]);
+__global__ void k_mul_scalar(const ulonglong2* __restrict__ ct, const uint64_t* __restrict__ wl,
+                             ulonglong2* __restrict__ o, int64_t vecs, int nl, const CtxParams P) {
+  const int sh = P.logn - 1;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < vecs; g += (int64_t)gridDim.x * blockDim.x) {
+    const int limb = (int)((uint32_t)(g >> sh) % (uint32_t)nl);
+    const LimbInfo& L = P.limb[limb];
+    const uint64_t w = wl[limb];
+    const ulonglong2 x = ct[g];
+    o[g] = make_ulonglong2(mulmod_ew(x.x, w, L), mulmod_ew(x.y, w, L));
   }
 }
 
 // per-item scalars (encode_constant residues of one value per element): every poly of
 // item i times w[i][limb], or poly 0 of item i plus w[i][limb]
-__global__ void k_scalar_items(const uint64_t* __restrict__ ct, const uint64_t* __restrict__ w,
-                               uint64_t* __restrict__ o, int64_t items, int size, int nl, int add, const CtxParams P) {
-  const int64_t n = P.n;
-  const int64_t words = items * size * nl * n;
-  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < words; x += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = x / n;
-    const int limb = (int)(row % nl);
-    const int poly = (int)((row / nl) % size);
-    const int64_t item = row / ((int64_t)nl * size);
-    const uint64_t wv = w[item * nl + limb];
+__global__ void k_scalar_items(const ulonglong2* __restrict__ ct, const uint64_t* __restrict__ w,
+                               ulonglong2* __restrict__ o, int64_t vecs, int size, int nl, int add,
+                               const CtxParams P) {
+  const int sh = P.logn - 1;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < vecs; g += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t row = (uint32_t)(g >> sh), per = (uint32_t)(size * nl);
+    const uint32_t item = row / per, rem = row - item * per, limb = rem % (uint32_t)nl;
+    const uint64_t wv = w[(int64_t)item * nl + limb];
     const LimbInfo& L = P.limb[limb];
-    if (add) o[x] = poly == 0 ? add_mod(ct[x], wv, L.q) : ct[x];
-    else o[x] = mul_mod(ct[x], wv, L);
+    const ulonglong2 x = ct[g];
+    if (add) o[g] = rem < (uint32_t)nl ? make_ulonglong2(add_mod(x.x, wv, L.q), add_mod(x.y, wv, L.q)) : x;
+    else o[g] = make_ulonglong2(mulmod_ew(x.x, wv, L), mulmod_ew(x.y, wv, L));
   }
 }
 
@@ -766,24 +793,30 @@ void lift_ntt(const Context& c, const int64_t* src, uint64_t* out, int64_t count
   HG_CUDA(cudaGetLastError());
 }
 
+static inline const ulonglong2* V2(const uint64_t* p) { return reinterpret_cast<const ulonglong2*>(p); }
+static inline ulonglong2* V2o(uint64_t* p) { return reinterpret_cast<ulonglong2*>(p); }
+
 void add(const Context& c, const uint64_t* a, const uint64_t* b, uint64_t* o, int64_t words, int nl, cudaStream_t s) {
   if (words <= 0) return;
+  check(words % c.n() == 0, HG_EVALIDATION, "word count must be a whole number of N-word rows");
   c.kt_begin("k_elementwise", s);
-  k_elementwise<0><<<ew_blocks(words, 256), 256, 0, s>>>(a, b, o, words, nl, c.kp());
+  k_elementwise<0><<<ew_blocks(words / 2, 256), 256, 0, s>>>(V2(a), V2(b), V2o(o), words / 2, nl, c.kp());
   c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
 void sub(const Context& c, const uint64_t* a, const uint64_t* b, uint64_t* o, int64_t words, int nl, cudaStream_t s) {
   if (words <= 0) return;
+  check(words % c.n() == 0, HG_EVALIDATION, "word count must be a whole number of N-word rows");
   c.kt_begin("k_elementwise", s);
-  k_elementwise<1><<<ew_blocks(words, 256), 256, 0, s>>>(a, b, o, words, nl, c.kp());
+  k_elementwise<1><<<ew_blocks(words / 2, 256), 256, 0, s>>>(V2(a), V2(b), V2o(o), words / 2, nl, c.kp());
   c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
 void negate(const Context& c, const uint64_t* a, uint64_t* o, int64_t words, int nl, cudaStream_t s) {
   if (words <= 0) return;
+  check(words % c.n() == 0, HG_EVALIDATION, "word count must be a whole number of N-word rows");
   c.kt_begin("k_elementwise", s);
-  k_elementwise<2><<<ew_blocks(words, 256), 256, 0, s>>>(a, nullptr, o, words, nl, c.kp());
+  k_elementwise<2><<<ew_blocks(words / 2, 256), 256, 0, s>>>(V2(a), nullptr, V2o(o), words / 2, nl, c.kp());
   c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
@@ -792,7 +825,8 @@ void add_plain(const Context& c, const uint64_t* ct, const uint64_t* pt, uint64_
   const int64_t words = items * size * nl * c.n();
   if (words <= 0) return;
   c.kt_begin("k_add_plain", s);
-  k_add_plain<<<ew_blocks(words, 256), 256, 0, s>>>(ct, pt, o, items, size, nl, per_item, subtract, c.kp());
+  k_add_plain<<<ew_blocks(words / 2, 256), 256, 0, s>>>(V2(ct), V2(pt), V2o(o), words / 2, size, nl, per_item, subtract,
+                                                           c.kp());
   c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
@@ -801,7 +835,7 @@ void mul_plain(const Context& c, const uint64_t* ct, const uint64_t* pt, uint64_
   const int64_t words = items * size * nl * c.n();
   if (words <= 0) return;
   c.kt_begin("k_mul_plain", s);
-  k_mul_plain<<<ew_blocks(words, 256), 256, 0, s>>>(ct, pt, o, items, size, nl, per_item, c.kp());
+  k_mul_plain<<<ew_blocks(words / 2, 256), 256, 0, s>>>(V2(ct), V2(pt), V2o(o), words / 2, size, nl, per_item, c.kp());
   c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
@@ -810,7 +844,7 @@ void mul_scalar(const Context& c, const uint64_t* ct, const uint64_t* w, uint64_
   const int64_t words = items * size * nl * c.n();
   if (words <= 0) return;
   c.kt_begin("k_mul_scalar", s);
-  k_mul_scalar<<<ew_blocks(words, 256), 256, 0, s>>>(ct, w, o, words, nl, c.kp());
+  k_mul_scalar<<<ew_blocks(words / 2, 256), 256, 0, s>>>(V2(ct), w, V2o(o), words / 2, nl, c.kp());
   c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
@@ -820,7 +854,8 @@ void scalar_items(const Context& c, const uint64_t* ct, const uint64_t* w, uint6
   const int64_t words = items * size * nl * c.n();
   if (words <= 0) return;
   c.kt_begin(add ? "k_add_scalar_items" : "k_mul_scalar_items", s, 2.0 * words * 8, add ? 0.0 : (double)words);
-  k_scalar_items<<<ew_blocks(words, 256), 256, 0, s>>>(ct, w, o, items, size, nl, add ? 1 : 0, c.kp());
+  k_scalar_items<<<ew_blocks(words / 2, 256), 256, 0, s>>>(V2(ct), w, V2o(o), words / 2, size, nl, add ? 1 : 0,
+                                                              c.kp());
   c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
@@ -939,7 +974,7 @@ void mul_relin(const Context& c, const Keys& keys, const uint64_t* a, const uint
   if (items <= 0) return;
   check(keys.has_relin, HG_EINTERNAL, "relinearisation key missing");
   const int64_t pw = (int64_t)nl * c.n();
-  if (c.logn() <= 14) {
+  if (c.logn() <= 15) {
     // out must not alias the inputs: the prologue writes d0, d1 into it
     check(out + items * 2 * pw <= a || a + items * 2 * pw <= out, HG_EINTERNAL, "relin output aliases its input");
     check(out + items * 2 * pw <= b || b + items * 2 * pw <= out, HG_EINTERNAL, "relin output aliases its input");
@@ -1004,7 +1039,7 @@ void relin3(const Context& c, const Keys& keys, const uint64_t* in3, uint64_t* o
   // c2 = INTT(d2): copy d2 rows (one strided copy) then inverse NTT
   HG_CUDA(cudaMemcpy2DAsync(c2, pw * 8, in3 + 2 * pw, 3 * pw * 8, pw * 8, items, cudaMemcpyDeviceToDevice, s));
   ntt(c, c2, items * nl, nl, true, s);
-  if (c.logn() <= 14) {
+  if (c.logn() <= 15) {
     k2::relin(c, keys, in3, nullptr, 3 * pw, 0, true, c2, out2, items, nl, s);
     return;
   }

@@ -417,6 +417,9 @@ struct RelinCfg {
                              Cfg<W, LOGN>::smem + (C2S ? ((size_t)8 << LOGN) : 0) + key_bytes <= kSmemCap;
   static constexpr size_t smem = Cfg<W, LOGN>::smem + (C2S ? ((size_t)8 << LOGN) : 0) + (KS ? key_bytes : 0);
   static constexpr size_t ks_off = Cfg<W, LOGN>::smem + (C2S ? ((size_t)8 << LOGN) : 0);
+  // CTAs of <= 256 threads (2^12 rows, half rows of a 2^13 ring) fit twice per SM by shared
+  // memory: cap registers at 128 so the register file holds both (measured: +3..15% ct ops/s)
+  static constexpr int min_blocks = (threads <= 256 && 2 * smem <= kSmemCap) ? 2 : 1;
 };
 // Lanes whose key switch (ring degree 2^LOGN) keeps its accumulators in registers: there the
 // relin prologue writes d0, d1 into the output and the key switch adds to them in place.
@@ -443,7 +446,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 template <typename W, int LOGN, bool GIVEN_D, bool SPLIT = false>
-__global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT>::threads, 1)
+__global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT>::threads, RelinCfg<W, LOGN, SPLIT>::min_blocks)
     k_relin_t(const uint64_t* a, const uint64_t* __restrict__ b, int64_t a_stride, int64_t b_stride,
               const uint64_t* __restrict__ c2, const uint64_t* __restrict__ kval,
               const uint64_t* __restrict__ kpack, const uint32_t* __restrict__ kmont, uint64_t* out,
@@ -1007,6 +1010,9 @@ static void set_smem_attr(const void* fn, size_t bytes) {
   static std::map<const void*, size_t> done;
   auto it = done.find(fn);
   if (it != done.end() && it->second >= bytes) return;
+  check(bytes <= kSmemCap, HG_EVALIDATION,
+        "ring degree 2^15 with limbs of 30 bits or more is not supported by the GPU path (a 2^15-point "
+        "64-bit transform exceeds one CTA's shared memory); use limbs below 2^30 at N = 32768");
   HG_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   done[fn] = bytes;
 }
@@ -1182,12 +1188,22 @@ static RelinC relin_consts(const Context& c, int nl) {
   return K;
 }
 
-bool relin_supported(const Context& c) { return c.logn() >= 10 && c.logn() <= 14; }
+// 2^13 key switch: half-row CTAs (default; c3 relin f64 1.31 -> 1.04 ms, u32 2.48 -> 2.41 ms
+// per step) or whole-row CTAs (HG_RELIN_SPLIT13=0)
+static bool relin_split13() {
+  static const bool on = [] {
+    const char* e = std::getenv("HG_RELIN_SPLIT13");
+    return e ? e[0] != '0' : true;
+  }();
+  return on;
+}
+
+bool relin_supported(const Context& c) { return c.logn() >= 10 && c.logn() <= 15; }
 
 void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, int64_t a_stride,
            int64_t b_stride, bool given_d, const uint64_t* c2, uint64_t* out, int64_t items, int nl, cudaStream_t s,
            bool d_in_out) {
-  check(relin_supported(c), HG_EINTERNAL, "key switch: ring degree outside 2^10..2^14");
+  check(relin_supported(c), HG_EINTERNAL, "key switch: ring degree outside 2^10..2^15");
   if (items <= 0) return;
   const RelinC K = relin_consts(c, nl);
   const Classes cl = classify(c, 0, nl, fp64_lane());
@@ -1198,9 +1214,7 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
     using W = decltype(wtag);
     if (LL.count == 0) return;
     by_logn<W>(c, [&]<typename W_, int LOGN>() {
-      if constexpr (LOGN <= 14) {
-        // 2^14: two CTAs per row, one per half of the evaluations (2^13-point half transforms)
-        constexpr bool SPLIT = LOGN == 14 && !std::is_same_v<W_, uint64_t>;
+      auto go = [&]<bool SPLIT>() {
         constexpr int LT = SPLIT ? LOGN - 1 : LOGN;
         using Cf = RelinCfg<W_, LT, SPLIT>;
         const int threads = Cf::threads;
@@ -1231,6 +1245,16 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
               keys.relin_mont.as<uint32_t>(), out, nl, items, G, K, LL, c.kp());
         c.kt_end(s);
         HG_CUDA(cudaGetLastError());
+      };
+      // 2^14, 2^15: two CTAs per row, one per half of the evaluations (2^13- / 2^14-point half
+      // transforms); a whole 2^15-point row does not fit one CTA's shared memory.  2^13: half-row
+      // CTAs run two per SM, with their own barriers (relin_split13())
+      if constexpr (LOGN == 15 || (LOGN == 14 && !std::is_same_v<W_, uint64_t>)) go.template operator()<true>();
+      else if constexpr (LOGN == 13 && !std::is_same_v<W_, uint64_t>) {
+        if (relin_split13()) go.template operator()<true>();
+        else go.template operator()<false>();
+      } else {
+        go.template operator()<false>();
       }
     });
   };

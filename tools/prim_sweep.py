@@ -142,8 +142,12 @@ def main():
                                              + resc_mm(2 * B)),
                 }
                 for name, (fn, units, abytes, amm) in ops.items():
-                    fn()
-                    torch.cuda.synchronize()
+                    try:
+                        fn()
+                        torch.cuda.synchronize()
+                    except P.HEError as e:
+                        emit({"kind": "error", "n": n, "L": L, "op": name, "batch": B, "error": str(e)})
+                        continue
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     e0.record(stream)
                     fn()
