@@ -763,6 +763,23 @@ std::shared_ptr<DevArr> encode_device(hg_plan* P, const double* dvals, int64_t c
   return pt;
 }
 
+// The encoder's signed coefficients only ([cols][N] int64, the input of the NTT in
+// encode_device), for callers that fold them into an encryption (encrypt_items mcoef).
+void encode_coeffs(hg_plan* P, const double* dvals, int64_t cols, int64_t count, int64_t col_stride,
+                   int64_t elem_stride, double scale, int64_t* ci) {
+  const Context& c = *P->ctx;
+  check(scale > 0.0, HG_EVALIDATION, "encoding scale must be positive");
+  if (cols == 0) return;
+  DevArr flag(sizeof(int), S(P));
+  HG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), S(P)));
+  k::encode_fft(c, dvals, cols, count, col_stride, elem_stride, scale, ci, flag.as<int>(), S(P));
+  P->launches += 1;
+  int overflow = 0;
+  HG_CUDA(cudaMemcpyAsync(&overflow, flag.p, sizeof(int), cudaMemcpyDeviceToHost, S(P)));
+  HG_CUDA(cudaStreamSynchronize(S(P)));
+  check(overflow == 0, HG_EVALIDATION, "encoded coefficient overflows the integer range");
+}
+
 // Encode host batch columns (bias columns, runtime.hpp:386-409): staged to the device, encoded there.
 std::shared_ptr<DevArr> encode_columns(hg_plan* P, const std::vector<std::vector<double>>& cols, int level,
                                        double scale) {
@@ -780,7 +797,7 @@ std::shared_ptr<DevArr> encode_columns(hg_plan* P, const std::vector<std::vector
 // Fresh encryptions of zero (or of per-item plaintexts) from per-item seeds
 // (ckks_backend.hpp:223-236, 470-490).
 void encrypt_items(hg_plan* P, const std::vector<uint64_t>& seeds, const uint64_t* pt, int level, uint64_t* out,
-                   const uint64_t* seeds_dev = nullptr) {
+                   const uint64_t* seeds_dev = nullptr, const int64_t* mcoef = nullptr) {
   const Context& c = *P->ctx;
   const int64_t n = c.n(), m = static_cast<int64_t>(seeds.size());
   if (m == 0) return;
@@ -789,7 +806,8 @@ void encrypt_items(hg_plan* P, const std::vector<uint64_t>& seeds, const uint64_
   if (P->in_run && !P->sync_sampling && P->sample_flag_used < P->sample_flag_cap)
     deferred = &P->sample_flags[P->sample_flag_used++];
   k::sample_encryption_gpu(c, seeds.data(), m, d.as<int64_t>(), S(P), deferred, seeds_dev);
-  k::encrypt(c, *P->keys, d.as<int64_t>(), pt, out, m, level + 1, S(P));
+  // mcoef: plaintexts as signed coefficients, folded into the e0 transform (one NTT fewer)
+  k2::encrypt(c, *P->keys, d.as<int64_t>(), mcoef, pt, out, m, level + 1, S(P));
 }
 
 std::shared_ptr<CtT> new_ct(hg_plan* P, int64_t count, int level, double scale) {
@@ -2570,12 +2588,13 @@ int hg_plan_bind_input(hg_plan* P, const char* param_id, const double* values, i
       HG_CUDA(cudaMemcpyAsync(bb.staged->p, values, sb, cudaMemcpyHostToDevice, hg::S(P)));
       dvals = bb.staged->as<double>();
     }
-    const size_t pb = static_cast<size_t>(nb) * (L + 1) * c.n() * 8;
+    // the encoder's coefficients [nb][N] (encrypt folds them into its e0 transform)
+    const size_t pb = static_cast<size_t>(nb) * c.n() * 8;
     if (!bb.pt || bb.pt_bytes != pb) {
       bb.pt = std::make_shared<hg::DevArr>(pb, hg::S(P));
       bb.pt_bytes = pb;
     }
-    auto pt = hg::encode_device(P, dvals, nb, P->batch, 1, nb, L, c.default_scale(), bb.pt);
+    hg::encode_coeffs(P, dvals, nb, P->batch, 1, nb, c.default_scale(), bb.pt->as<int64_t>());
     // the previous ciphertexts are rewritten in place when only the plan holds them (the
     // bound value and this cache); stream order puts the writes after earlier runs' reads
     auto bt = P->bound.find(param_id);
@@ -2586,7 +2605,7 @@ int hg_plan_bind_input(hg_plan* P, const char* param_id, const double* values, i
       ct = bb.ct;
     else
       ct = bb.ct = hg::new_ct(P, nb, L, c.default_scale());
-    hg::encrypt_items(P, seeds, pt->as<uint64_t>(), L, ct->p);
+    hg::encrypt_items(P, seeds, nullptr, L, ct->p, nullptr, bb.pt->as<int64_t>());
     hg::Val v;
     v.shape = shape;
     v.batched = true;

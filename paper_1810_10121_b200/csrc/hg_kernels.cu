@@ -656,26 +656,6 @@ __global__ void k_expand_rows(const uint64_t* __restrict__ residues, uint64_t* _
 // --------------------------------------------------------------------------
 // Encryption / decryption / keygen pointwise kernels
 // --------------------------------------------------------------------------
-// ntt3: [items][3][nl][N] (u, e0, e1 in NTT form) -> out [items][2][nl][N]
-__global__ void k_encrypt_combine(const uint64_t* __restrict__ ntt3, const uint64_t* __restrict__ pk,
-                                  const uint64_t* __restrict__ pt, uint64_t* __restrict__ out, int64_t items, int nl,
-                                  int64_t key_poly_words, const CtxParams P) {
-  const int64_t n = P.n, pw = nl * n;
-  const int64_t words = items * pw;
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t item = w / pw, lw = w - item * pw;
-    const LimbInfo& L = P.limb[lw / n];
-    const uint64_t u = ntt3[item * 3 * pw + lw];
-    const uint64_t e0 = ntt3[item * 3 * pw + pw + lw];
-    const uint64_t e1 = ntt3[item * 3 * pw + 2 * pw + lw];
-    uint64_t c0 = add_mod(mul_mod(pk[lw], u, L), e0, L.q);
-    if (pt) c0 = add_mod(c0, pt[item * pw + lw], L.q);
-    const uint64_t c1 = add_mod(mul_mod(pk[key_poly_words + lw], u, L), e1, L.q);
-    out[item * 2 * pw + lw] = c0;
-    out[item * 2 * pw + pw + lw] = c1;
-  }
-}
-
 // m = c0 + c1 s + c2 s^2 (+...) (ckks_backend.hpp:238-247), NTT form
 __global__ void k_decrypt_dot(const uint64_t* __restrict__ ct, const uint64_t* __restrict__ sk, uint64_t* __restrict__ m,
                               int64_t items, int size, int nl, const CtxParams P) {
@@ -1065,15 +1045,7 @@ void relin3(const Context& c, const Keys& keys, const uint64_t* in3, uint64_t* o
 void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const uint64_t* pt, uint64_t* out,
              int64_t items, int nl, cudaStream_t s) {
   if (items <= 0) return;
-  const int64_t pw = (int64_t)nl * c.n();
-  uint64_t* tmp = static_cast<uint64_t*>(const_cast<Context&>(c).scratch((size_t)(items * 3 * pw * 8), 7));
-  lift_ntt(c, samples, tmp, items * 3, nl, s);
-  const int64_t words = items * pw;
-  c.kt_begin("k_encrypt_combine", s);
-  k_encrypt_combine<<<ew_blocks(words, 256), 256, 0, s>>>(tmp, keys.pk.as<uint64_t>(), pt, out, items, nl,
-                                                          (int64_t)(c.max_level() + 1) * c.n(), c.kp());
-  c.kt_end(s);
-  HG_CUDA(cudaGetLastError());
+  k2::encrypt(c, keys, samples, nullptr, pt, out, items, nl, s);
 }
 
 void decrypt(const Context& c, const Keys& keys, const uint64_t* ct, uint64_t* m, int64_t items, int size, int nl,

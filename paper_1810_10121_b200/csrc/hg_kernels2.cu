@@ -326,6 +326,97 @@ struct ProdMod {
   }
 };
 
+// Fused public-key encryption (fresh_encryption + encrypt, ckks_backend.hpp:223-236, 470-490),
+// one CTA per (limb j, item group):
+//   c0 = pk_b NTT(u) + NTT(e0) [+ NTT(m)] [+ pt],   c1 = pk_a NTT(u) + NTT(e1)
+// NTT(u) stays in registers across the three transforms.  A plaintext given as signed
+// coefficients (mcoef, the encoder's output) is lifted into the e0 transform: NTT is linear
+// mod q_j, so NTT(e0 + m) = NTT(e0) + NTT(m) word for word, and one transform is saved.
+// The outputs are canonical residues, identical to the reference's.
+template <typename W>
+__device__ __forceinline__ W lift_any(int64_t v, const LimbInfo& L, uint32_t mu32) {
+  // |v| < 2^31 (32-bit lane) or |v| < q (fp64 lane): the cheap centred-lift path
+  const int64_t small = std::is_floating_point_v<W> ? (int64_t)L.q : ((int64_t)1 << 31);
+  if (v > -small && v < small) {
+    if constexpr (std::is_floating_point_v<W>) return (double)v;  // a signed fp64-lane residue
+    else return lift_cen<W, int32_t>((int32_t)v, L, mu32);
+  }
+  if constexpr (std::is_floating_point_v<W>) return (double)lift_signed(v, L);
+  else return (W)lift_signed(v, L);
+}
+
+HG_KERNEL k_encrypt_t(const int64_t* __restrict__ samples, const int64_t* __restrict__ mcoef,
+                      const uint64_t* __restrict__ pt, const uint64_t* __restrict__ pk, int64_t key_poly_words,
+                      uint64_t* __restrict__ out, int nl, int64_t items, int G, const LimbList LL,
+                      const CtxParams P) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  Cta<W, LOGN> c(smem, LL, items, G, P, false);
+  constexpr int n = 1 << LOGN, T = lz::lz_threads<LOGN>(), GPT = (n >> 4) / T;
+  const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
+  const uint32_t mu32 = (uint32_t)((1ULL << 32) / c.L->q);
+  const ProdMod<W> pm(*c.L);
+  const uint64_t Q = c.L->q;
+  const int j = c.limb;
+  const int64_t pw = (int64_t)nl * n;
+  for (int r = c.r0; r < c.r1; ++r) {
+    const int64_t* su = samples + (int64_t)r * 3 * n;
+    // ---- NTT(u) -> registers (canonical) ----
+    W u[GPT][16];
+    lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return lift_any<W>(__ldg(su + k), *c.L, mu32); }, c.tw, q, q2);
+    lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2);
+#pragma unroll
+    for (int gi = 0; gi < GPT; ++gi) {
+      W y[16];
+      lz::fwd_last<W, LOGN>(c.s, threadIdx.x + gi * T, c.tw, q, q2, y);
+#pragma unroll
+      for (int h = 0; h < 16; ++h) u[gi][h] = canon4<W>(y[h], q, q2);
+    }
+#pragma unroll 1
+    for (int p = 0; p < 2; ++p) {
+      __syncthreads();  // the previous transform's last pass has read shared memory
+      const int64_t* se = su + (int64_t)(1 + p) * n;
+      const int64_t* mc = (p == 0 && mcoef) ? mcoef + (int64_t)r * n : nullptr;
+      lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
+        W v = lift_any<W>(__ldg(se + k), *c.L, mu32);
+        if (mc) {
+          const W m = lift_any<W>(__ldg(mc + k), *c.L, mu32);
+          if constexpr (std::is_floating_point_v<W>) v = reduce_f64(__dadd_rn(v, m), q, q2);
+          else v = csub<W>((W)(v + m), q);
+        }
+        return v;
+      }, c.tw, q, q2);
+      lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2);
+      const uint64_t* kp = pk + (int64_t)p * key_poly_words + (int64_t)j * n;
+      const uint64_t* pp = (p == 0 && pt) ? pt + (int64_t)r * pw + (int64_t)j * n : nullptr;
+#pragma unroll
+      for (int gi = 0; gi < GPT; ++gi) {
+        const int vt = threadIdx.x + gi * T, k0 = vt << 4;
+        W y[16];
+        lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, y);
+        const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(kp + k0);
+        const ulonglong2* p2 = pp ? reinterpret_cast<const ulonglong2*>(pp + k0) : nullptr;
+        const int pb = lz::padw<W>(k0);
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          const ulonglong2 kv = __ldg(k2 + h);
+          ulonglong2 pv = make_ulonglong2(0, 0);
+          if (p2) pv = __ldg(p2 + h);
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const uint64_t a = pm(e ? kv.y : kv.x, (uint64_t)u[gi][2 * h + e]);
+            uint64_t v = add_mod(a, (uint64_t)canon4<W>(y[2 * h + e], q, q2), Q);
+            if (p2) v = add_mod(v, e ? pv.y : pv.x, Q);
+            c.s[pb + 2 * h + e] = (W)v;  // the last pass read its own 16 slots only
+          }
+        }
+      }
+      __syncthreads();
+      lz::store<W, LOGN>(out + ((int64_t)r * 2 + p) * pw + (int64_t)j * n, c.s);
+    }
+    __syncthreads();
+  }
+}
+
 // relinearisation prologue: c2 = INTT(a1 * b1) per (item, limb i)  (ckks_backend.hpp:509).
 // With d != nullptr it also writes the tensor terms d0 = a0 b0, d1 = a0 b1 + a1 b0
 // (ckks_backend.hpp:306-318) as out[item][2][nl][N], so the key switch only adds its
@@ -1090,6 +1181,36 @@ void lift_ntt(const Context& c, const int64_t* src, uint64_t* out, int64_t items
       set_smem_attr((const void*)k_lift_ntt_t<W_, LOGN>, Cf::smem);
       c.kt_begin(std::is_floating_point_v<W_> ? "k_lift_ntt_t/f64" : sizeof(W_) == 4 ? "k_lift_ntt_t/u32" : "k_lift_ntt_t/u64", s, (double)items * LL.count * 2 * nw, (double)items * LL.count * bfly(c));
       k_lift_ntt_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(src, out, nl, items, G, LL, c.kp());
+      c.kt_end(s);
+      HG_CUDA(cudaGetLastError());
+    });
+  };
+  run(cl.small, uint32_t{});
+  run(cl.fp, double{});
+  run(cl.wide, uint64_t{});
+}
+
+void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const int64_t* mcoef, const uint64_t* pt,
+             uint64_t* out, int64_t items, int nl, cudaStream_t s) {
+  if (items <= 0) return;
+  const Classes cl = classify(c, 0, nl, fp64_lane());
+  const double nw = (double)c.n() * 8;
+  const int64_t kpw = (int64_t)(c.max_level() + 1) * c.n();
+  auto run = [&](const LimbList& LL, auto wtag) {
+    using W = decltype(wtag);
+    if (LL.count == 0) return;
+    by_logn<W>(c, [&]<typename W_, int LOGN>() {
+      using Cf = Cfg<W_, LOGN>;
+      unsigned grid;
+      int G;
+      grid_for<W_, LOGN>(LL, items, grid, G);
+      set_smem_attr((const void*)k_encrypt_t<W_, LOGN>, Cf::smem);
+      // bytes: samples (3 N, + m N) read, 2 polys written (+ pt read); modmuls: 3 transforms + 2 N key products
+      c.kt_begin(std::is_floating_point_v<W_> ? "k_encrypt_t/f64" : sizeof(W_) == 4 ? "k_encrypt_t/u32" : "k_encrypt_t/u64", s,
+                 (double)items * LL.count * (2 + (pt ? 1 : 0)) * nw + (double)items * (3 + (mcoef ? 1 : 0)) * nw,
+                 (double)items * LL.count * (3 * bfly(c) + 2.0 * c.n()));
+      k_encrypt_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(samples, mcoef, pt, keys.pk.as<uint64_t>(), kpw, out,
+                                                                nl, items, G, LL, c.kp());
       c.kt_end(s);
       HG_CUDA(cudaGetLastError());
     });
