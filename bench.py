@@ -198,7 +198,7 @@ def roofline_from_stats(stats: dict, peaks: dict, int_peak32: float):
           "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/)",
           "alg_bytes_per_launch": st["alg_bytes"] / max(1, st["launches"]),
           "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)",
-          "launches_in_timed_region": st["launches"], "avg_launch_ms": st["total_ms"] / max(1, st["launches"])}
+          "launches_in_region": st["launches"], "avg_launch_ms": st["total_ms"] / max(1, st["launches"])}
     mm = st["alg_modmuls"] / sec / 1e9 if sec > 0 else 0.0
     rl_int = {"kernel": name, "bound": "int-modmul", "achieved": mm, "peak": int_peak32 / 1e9,
               "unit": "Gmodmul/s", "frac": mm / (int_peak32 / 1e9) if int_peak32 else None,
@@ -246,8 +246,6 @@ def ours_arm(args):
     # ---- value: server-side graph, inputs resident in HBM ----
     for _ in range(args.warmup):
         plan.run()
-    ctx.kernel_timing(True)
-    ctx.kernel_stats()  # clear
     launches0 = ctx.kernel_launches()
     barrier()
     torch.cuda.synchronize()
@@ -261,9 +259,23 @@ def ours_arm(args):
         torch.cuda.synchronize()
     barrier()
     launches = ctx.kernel_launches() - launches0
+    ms_total = e0.elapsed_time(e1)
+    # the same K steps again with a CUDA event pair around every launch (on the launching
+    # stream): per-kernel durations for the roofline.  Kept out of the `value` region, where
+    # the ~80 extra event records per step would add their own gaps.
+    ctx.kernel_timing(True)
+    ctx.kernel_stats()  # clear
+    torch.cuda.synchronize()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        plan.run()
+    f1.record(stream)
+    torch.cuda.synchronize()
     ctx.kernel_timing(False)
     stats = ctx.kernel_stats()
-    ms_total = e0.elapsed_time(e1)
+    ms_kernel_region = f0.elapsed_time(f1) / args.steps
     if ws > 1:
         t = torch.tensor([ms_total], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -340,6 +352,7 @@ def ours_arm(args):
                     "sampler_reruns_total": plan.profile().get("sampler_reruns")},
             "gpu_launches": launches,
             "kernels": stats,
+            "kernels_region_ms_per_step": ms_kernel_region,
             "clocks": clocks.summary(),
             "profile_ms": plan.profile()["wall_ms"],
         }

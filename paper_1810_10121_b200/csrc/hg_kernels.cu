@@ -193,6 +193,24 @@ __global__ void k_scalar_items(const ulonglong2* __restrict__ ct, const uint64_t
   }
 }
 
+// one-term weighted sums (kt = 1): out[g mg + m] = w[g][m][limb] * x[idx[g]] -- a gathered
+// per-item scalar product on 16-byte vectors (weighted_sum with single-term outputs)
+__global__ void k_scale_gather(const ulonglong2* __restrict__ x, const int32_t* __restrict__ idx,
+                               const uint64_t* __restrict__ w, int64_t w_group_stride, ulonglong2* __restrict__ o,
+                               int64_t vecs, int mg, int nl, const CtxParams P) {
+  const int sh = P.logn - 1;
+  const int64_t vmask = ((int64_t)1 << sh) - 1;
+  const uint32_t per = (uint32_t)(2 * nl);
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < vecs; g += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t row = (uint32_t)(g >> sh), item = row / per, rem = row - item * per;
+    const uint32_t limb = rem % (uint32_t)nl, grp = item / (uint32_t)mg, m = item - grp * (uint32_t)mg;
+    const LimbInfo& L = P.limb[limb];
+    const uint64_t wv = w[(int64_t)grp * w_group_stride + (int64_t)m * nl + limb];
+    const ulonglong2 v = x[((((int64_t)idx[grp]) * per + rem) << sh) + (g & vmask)];
+    o[g] = make_ulonglong2(mulmod_ew(v.x, wv, L), mulmod_ew(v.y, wv, L));
+  }
+}
+
 // --------------------------------------------------------------------------
 // Rescale (poly.hpp:190-228)
 // --------------------------------------------------------------------------
@@ -881,6 +899,16 @@ void gemm_groups(const Context& c, const uint64_t* x, int64_t x_items, const int
                  int64_t w_group_stride, const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt, int nl,
                  cudaStream_t s) {
   if (groups <= 0 || mg <= 0) return;
+  if (kt == 1 && oidx == nullptr) {  // single-term outputs: a gathered scalar product
+    const int64_t vecs = groups * mg * 2 * nl * c.n() / 2;
+    c.kt_begin("k_scale_gather", s, 2.0 * vecs * 16, (double)vecs * 2);
+    k_scale_gather<<<ew_blocks(vecs, 256), 256, 0, s>>>(reinterpret_cast<const ulonglong2*>(x), idx, w,
+                                                         w_group_stride, reinterpret_cast<ulonglong2*>(out), vecs,
+                                                         mg, nl, c.kp());
+    c.kt_end(s);
+    HG_CUDA(cudaGetLastError());
+    return;
+  }
   if (c.n() % 2048 == 0) {  // IMAD.WIDE kernel (hg_kernels2.cu)
     k2::gemm(c, x, x_items, idx, w, w_group_stride, oidx, out, groups, mg, kt, nl, s);
     return;
