@@ -447,6 +447,19 @@ Context::~Context() {
   m_scratch.clear();
   m_tables.release();
   if (m_stream) cudaStreamDestroy(m_stream);
+  for (cudaStream_t x : m_lane_s)
+    if (x) cudaStreamDestroy(x);
+  for (cudaEvent_t e : m_lane_e)
+    if (e) cudaEventDestroy(e);
+}
+
+cudaStream_t Context::lane_stream(int k) const {
+  if (!m_lane_s[k]) HG_CUDA(cudaStreamCreateWithFlags(&m_lane_s[k], cudaStreamNonBlocking));
+  return m_lane_s[k];
+}
+cudaEvent_t Context::lane_event(int k) const {
+  if (!m_lane_e[k]) HG_CUDA(cudaEventCreateWithFlags(&m_lane_e[k], cudaEventDisableTiming));
+  return m_lane_e[k];
 }
 
 double Context::default_scale() const { return std::ldexp(1.0, m_p.scale_bits); }

@@ -201,6 +201,10 @@ class Context {
   // per kernel name; synchronises and clears the records
   std::map<std::string, KtStat> kt_collect() const;
   int64_t kt_launches() const { return m_kt_launches; }
+  // auxiliary streams (k = 0, 1) and events (0 fork, 1..2 joins) for running the arithmetic
+  // lanes of one op concurrently (hg_kernels2.cu LaneFork); created on first use
+  cudaStream_t lane_stream(int k) const;
+  cudaEvent_t lane_event(int k) const;
   void kt_reset_launches() const { m_kt_launches = 0; }
 
  private:
@@ -219,6 +223,8 @@ class Context {
   int m_logn = 0;
   int m_device = 0;
   cudaStream_t m_stream = nullptr;
+  mutable cudaStream_t m_lane_s[2] = {nullptr, nullptr};
+  mutable cudaEvent_t m_lane_e[3] = {nullptr, nullptr, nullptr};
   cudaStream_t m_ext = nullptr;
   bool m_use_ext = false;
   std::vector<uint64_t> m_q;

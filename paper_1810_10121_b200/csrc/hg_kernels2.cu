@@ -1097,6 +1097,45 @@ static bool fp64_lane() {
   return on;
 }
 
+// Arithmetic lanes of one op run concurrently: the fp64 and 64-bit lanes' launches go to
+// auxiliary streams forked from s and are joined back into s when the LaneFork goes out of
+// scope.  u32 CTAs issue IMAD / ALU work and fp64 CTAs DFMA / DADD, so co-resident on an SM
+// they fill different pipes.  HG_LANE_OVERLAP=0 serialises the lanes on s.
+static bool lane_overlap() {
+  static const bool on = [] {
+    const char* e = std::getenv("HG_LANE_OVERLAP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+class LaneFork {
+ public:
+  LaneFork(const Context& c, cudaStream_t s, const Classes& cl) : c_(c), s_(s) {
+    const int lanes = (cl.small.count > 0) + (cl.fp.count > 0) + (cl.wide.count > 0);
+    if (lanes < 2 || !lane_overlap()) return;
+    on_ = true;
+    HG_CUDA(cudaEventRecord(c.lane_event(0), s));
+    for (int k = 0; k < 2; ++k) HG_CUDA(cudaStreamWaitEvent(c.lane_stream(k), c.lane_event(0), 0));
+  }
+  LaneFork(const LaneFork&) = delete;
+  LaneFork& operator=(const LaneFork&) = delete;
+  cudaStream_t small() const { return s_; }
+  cudaStream_t fp() const { return on_ ? c_.lane_stream(0) : s_; }
+  cudaStream_t wide() const { return on_ ? c_.lane_stream(1) : s_; }
+  ~LaneFork() {
+    if (!on_) return;
+    for (int k = 0; k < 2; ++k) {  // no-throw: a failure here resurfaces at the next checked call
+      cudaEventRecord(c_.lane_event(1 + k), c_.lane_stream(k));
+      cudaStreamWaitEvent(s_, c_.lane_event(1 + k), 0);
+    }
+  }
+
+ private:
+  const Context& c_;
+  cudaStream_t s_;
+  bool on_ = false;
+};
+
 static void set_smem_attr(const void* fn, size_t bytes) {
   static std::map<const void*, size_t> done;
   auto it = done.find(fn);
@@ -1144,7 +1183,7 @@ void ntt(const Context& c, uint64_t* base, int64_t rows_per_limb, int nl, int li
   if (rows_per_limb <= 0) return;
   const Classes cl = classify(c, limb_begin, limb_end, fp64_lane());
   const double nw = (double)c.n() * 8;
-  auto run = [&](const LimbList& LL, auto wtag) {
+  auto run = [&](const LimbList& LL, auto wtag, cudaStream_t s) {
     using W = decltype(wtag);
     if (LL.count == 0) return;
     by_logn<W>(c, [&]<typename W_, int LOGN>() {
@@ -1161,16 +1200,17 @@ void ntt(const Context& c, uint64_t* base, int64_t rows_per_limb, int nl, int li
       HG_CUDA(cudaGetLastError());
     });
   };
-  run(cl.small, uint32_t{});
-  run(cl.fp, double{});
-  run(cl.wide, uint64_t{});
+  LaneFork lf(c, s, cl);
+  run(cl.small, uint32_t{}, lf.small());
+  run(cl.fp, double{}, lf.fp());
+  run(cl.wide, uint64_t{}, lf.wide());
 }
 
 void lift_ntt(const Context& c, const int64_t* src, uint64_t* out, int64_t items, int nl, cudaStream_t s) {
   if (items <= 0) return;
   const Classes cl = classify(c, 0, nl, fp64_lane());
   const double nw = (double)c.n() * 8;
-  auto run = [&](const LimbList& LL, auto wtag) {
+  auto run = [&](const LimbList& LL, auto wtag, cudaStream_t s) {
     using W = decltype(wtag);
     if (LL.count == 0) return;
     by_logn<W>(c, [&]<typename W_, int LOGN>() {
@@ -1185,9 +1225,10 @@ void lift_ntt(const Context& c, const int64_t* src, uint64_t* out, int64_t items
       HG_CUDA(cudaGetLastError());
     });
   };
-  run(cl.small, uint32_t{});
-  run(cl.fp, double{});
-  run(cl.wide, uint64_t{});
+  LaneFork lf(c, s, cl);
+  run(cl.small, uint32_t{}, lf.small());
+  run(cl.fp, double{}, lf.fp());
+  run(cl.wide, uint64_t{}, lf.wide());
 }
 
 void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const int64_t* mcoef, const uint64_t* pt,
@@ -1196,7 +1237,7 @@ void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const i
   const Classes cl = classify(c, 0, nl, fp64_lane());
   const double nw = (double)c.n() * 8;
   const int64_t kpw = (int64_t)(c.max_level() + 1) * c.n();
-  auto run = [&](const LimbList& LL, auto wtag) {
+  auto run = [&](const LimbList& LL, auto wtag, cudaStream_t s) {
     using W = decltype(wtag);
     if (LL.count == 0) return;
     by_logn<W>(c, [&]<typename W_, int LOGN>() {
@@ -1215,9 +1256,10 @@ void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const i
       HG_CUDA(cudaGetLastError());
     });
   };
-  run(cl.small, uint32_t{});
-  run(cl.fp, double{});
-  run(cl.wide, uint64_t{});
+  LaneFork lf(c, s, cl);
+  run(cl.small, uint32_t{}, lf.small());
+  run(cl.fp, double{}, lf.fp());
+  run(cl.wide, uint64_t{}, lf.wide());
 }
 
 template <typename CT>
@@ -1226,7 +1268,7 @@ static void rescale_t(const Context& c, const uint64_t* in, uint64_t* out, int64
   const int t = nl - 1;
   const double nw = (double)c.n() * 8;
   const Classes top = classify(c, t, t + 1, fp64_lane()), rest = classify(c, 0, t, fp64_lane());
-  auto run_top = [&](const LimbList& LL, auto wtag) {
+  auto run_top = [&](const LimbList& LL, auto wtag, cudaStream_t s) {
     using W = decltype(wtag);
     if (LL.count == 0) return;
     by_logn<W>(c, [&]<typename W_, int LOGN>() {
@@ -1241,7 +1283,7 @@ static void rescale_t(const Context& c, const uint64_t* in, uint64_t* out, int64
       HG_CUDA(cudaGetLastError());
     });
   };
-  auto run_rest = [&](const LimbList& LL, auto wtag) {
+  auto run_rest = [&](const LimbList& LL, auto wtag, cudaStream_t s) {
     using W = decltype(wtag);
     if (LL.count == 0) return;
     by_logn<W>(c, [&]<typename W_, int LOGN>() {
@@ -1273,12 +1315,13 @@ static void rescale_t(const Context& c, const uint64_t* in, uint64_t* out, int64
       HG_CUDA(cudaGetLastError());
     });
   };
-  run_top(top.small, uint32_t{});
-  run_top(top.fp, double{});
-  run_top(top.wide, uint64_t{});
-  run_rest(rest.small, uint32_t{});
-  run_rest(rest.fp, double{});
-  run_rest(rest.wide, uint64_t{});
+  run_top(top.small, uint32_t{}, s);  // one limb: a single lane
+  run_top(top.fp, double{}, s);
+  run_top(top.wide, uint64_t{}, s);
+  LaneFork lf(c, s, rest);
+  run_rest(rest.small, uint32_t{}, lf.small());
+  run_rest(rest.fp, double{}, lf.fp());
+  run_rest(rest.wide, uint64_t{}, lf.wide());
 }
 
 void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys, int nl, int64_t* cen,
@@ -1331,7 +1374,7 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
   int sd = 0;
   for (int i = 0; i < nl; ++i) sd += c.digits(i);
   const double pw8 = (double)nl * c.n() * 8;
-  auto run = [&](const LimbList& LL, auto wtag) {
+  auto run = [&](const LimbList& LL, auto wtag, cudaStream_t s) {
     using W = decltype(wtag);
     if (LL.count == 0) return;
     by_logn<W>(c, [&]<typename W_, int LOGN>() {
@@ -1379,9 +1422,10 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
       }
     });
   };
-  run(cl.small, uint32_t{});
-  run(cl.fp, double{});
-  run(cl.wide, uint64_t{});
+  LaneFork lf(c, s, cl);
+  run(cl.small, uint32_t{}, lf.small());
+  run(cl.fp, double{}, lf.fp());
+  run(cl.wide, uint64_t{}, lf.wide());
 }
 
 void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_stride, int64_t b_stride,
@@ -1389,7 +1433,7 @@ void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_
   if (items <= 0) return;
   const Classes cl = classify(c, 0, nl, fp64_lane());
   const double nw = (double)c.n() * 8;
-  auto run = [&](const LimbList& LL, auto wtag) {
+  auto run = [&](const LimbList& LL, auto wtag, cudaStream_t s) {
     using W = decltype(wtag);
     if (LL.count == 0) return;
     by_logn<W>(c, [&]<typename W_, int LOGN>() {
@@ -1410,9 +1454,10 @@ void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_
       HG_CUDA(cudaGetLastError());
     });
   };
-  run(cl.small, uint32_t{});
-  run(cl.fp, double{});
-  run(cl.wide, uint64_t{});
+  LaneFork lf(c, s, cl);
+  run(cl.small, uint32_t{}, lf.small());
+  run(cl.fp, double{}, lf.fp());
+  run(cl.wide, uint64_t{}, lf.wide());
 }
 
 void gemm(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* idx, const uint64_t* w,
@@ -1423,7 +1468,7 @@ void gemm(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* i
   const int64_t n = c.n();
   const double item_bytes = 2.0 * nl * n * 8;
   const double in_items = std::min<double>((double)groups * kt, (double)x_items);
-  auto launch = [&](const LimbList& LL, bool wide) {
+  auto launch = [&](const LimbList& LL, bool wide, cudaStream_t s) {
     if (LL.count == 0) return;
     const double frac = (double)LL.count / nl;
     const double gb = frac * (in_items + (double)groups * mg) * item_bytes;
@@ -1449,9 +1494,11 @@ void gemm(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* i
     c.kt_end(s);
     HG_CUDA(cudaGetLastError());
   };
-  launch(cl.small, false);
-  launch(cl.wide, true);
+  LaneFork lf(c, s, cl);
+  launch(cl.small, false, lf.small());
+  launch(cl.wide, true, lf.wide());
   if (cl.fp.count > 0) {
+    const cudaStream_t s = lf.fp();
     const LimbList& LL = cl.fp;
     const double frac = (double)LL.count / nl;
     const int MT = mg <= 4 ? 4 : mg == 5 ? 5 : 8, C = 2;
