@@ -262,7 +262,9 @@ def ours_arm(args):
     ms_total = e0.elapsed_time(e1)
     # the same K steps again with a CUDA event pair around every launch (on the launching
     # stream): per-kernel durations for the roofline.  Kept out of the `value` region, where
-    # the ~80 extra event records per step would add their own gaps.
+    # the ~80 extra event records per step would add their own gaps; with timing on, the
+    # executor serialises the u32 / fp64 lanes it otherwise overlaps, so each event pair
+    # brackets one kernel alone.
     ctx.kernel_timing(True)
     ctx.kernel_stats()  # clear
     torch.cuda.synchronize()

@@ -547,6 +547,10 @@ int tc_min_terms() {
 // the plan
 // ===========================================================================
 struct hg_plan {
+  // host-to-device copies of bound inputs run on their own stream, so a caller's next input
+  // crosses PCIe while the previous run still computes (created on first use)
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t copy_done = nullptr;
   hg_context* hctx = nullptr;
   hg::Context* ctx = nullptr;
   const hg::Keys* keys = nullptr;
@@ -2537,6 +2541,11 @@ int hg_plan_set_options(hg_plan* P, const char* options_json) {
 void hg_plan_destroy(hg_plan* plan) {
   if (!plan) return;
   cudaStreamSynchronize(plan->ctx->stream());
+  if (plan->copy_stream) {
+    cudaStreamSynchronize(plan->copy_stream);
+    cudaStreamDestroy(plan->copy_stream);
+  }
+  if (plan->copy_done) cudaEventDestroy(plan->copy_done);
   if (plan->sample_flags) cudaFreeHost(plan->sample_flags);
   delete plan;
 }
@@ -2581,11 +2590,25 @@ int hg_plan_bind_input(hg_plan* P, const char* param_id, const double* values, i
     const double* dvals = values;
     if (!on_device) {
       const size_t sb = static_cast<size_t>(count) * 8;
+      bool fresh = false;
       if (!bb.staged || bb.staged_bytes != sb) {
         bb.staged = std::make_shared<hg::DevArr>(sb, hg::S(P));
         bb.staged_bytes = sb;
+        fresh = true;
       }
-      HG_CUDA(cudaMemcpyAsync(bb.staged->p, values, sb, cudaMemcpyHostToDevice, hg::S(P)));
+      // the staging buffer is free: the previous bind of this input synchronised after its
+      // encode read it.  The copy runs on the plan's copy stream; the encode waits for it.
+      if (!P->copy_stream) {
+        HG_CUDA(cudaStreamCreateWithFlags(&P->copy_stream, cudaStreamNonBlocking));
+        HG_CUDA(cudaEventCreateWithFlags(&P->copy_done, cudaEventDisableTiming));
+      }
+      if (fresh) {  // a stream-ordered allocation on S(P): the copy stream waits for it
+        HG_CUDA(cudaEventRecord(P->copy_done, hg::S(P)));
+        HG_CUDA(cudaStreamWaitEvent(P->copy_stream, P->copy_done, 0));
+      }
+      HG_CUDA(cudaMemcpyAsync(bb.staged->p, values, sb, cudaMemcpyHostToDevice, P->copy_stream));
+      HG_CUDA(cudaEventRecord(P->copy_done, P->copy_stream));
+      HG_CUDA(cudaStreamWaitEvent(hg::S(P), P->copy_done, 0));
       dvals = bb.staged->as<double>();
     }
     // the encoder's coefficients [nb][N] (encrypt folds them into its e0 transform)

@@ -1112,7 +1112,9 @@ class LaneFork {
  public:
   LaneFork(const Context& c, cudaStream_t s, const Classes& cl) : c_(c), s_(s) {
     const int lanes = (cl.small.count > 0) + (cl.fp.count > 0) + (cl.wide.count > 0);
-    if (lanes < 2 || !lane_overlap()) return;
+    // per-kernel timing (the bench's roofline pass) serialises the lanes, so each kernel's
+    // event pair brackets that kernel alone
+    if (lanes < 2 || !lane_overlap() || c.kt_enabled()) return;
     on_ = true;
     HG_CUDA(cudaEventRecord(c.lane_event(0), s));
     for (int k = 0; k < 2; ++k) HG_CUDA(cudaStreamWaitEvent(c.lane_stream(k), c.lane_event(0), 0));
