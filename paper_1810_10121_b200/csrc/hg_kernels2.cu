@@ -536,15 +536,16 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-template <typename W, int LOGN, bool GIVEN_D, bool SPLIT = false>
-__global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT>::threads, RelinCfg<W, LOGN, SPLIT>::min_blocks)
-    k_relin_t(const uint64_t* a, const uint64_t* __restrict__ b, int64_t a_stride, int64_t b_stride,
-              const uint64_t* __restrict__ c2, const uint64_t* __restrict__ kval,
-              const uint64_t* __restrict__ kpack, const uint32_t* __restrict__ kmont, uint64_t* out,
-              int nl, int64_t items, int G, const RelinC K, const LimbList LL, const CtxParams P) {
+// the key switch of CTA `vb` (k_relin_t passes blockIdx.x)
+template <typename W, int LOGN, bool GIVEN_D, bool SPLIT>
+__device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, const uint64_t* __restrict__ b,
+                                           int64_t a_stride, int64_t b_stride, const uint64_t* __restrict__ c2,
+                                           const uint64_t* __restrict__ kval, const uint64_t* __restrict__ kpack,
+                                           const uint32_t* __restrict__ kmont, uint64_t* out, int nl, int64_t items,
+                                           int G, const RelinC& K, const LimbList& LL, const CtxParams& P) {
   extern __shared__ __align__(16) uint64_t smem[];
-  const int half = SPLIT ? (int)(blockIdx.x & 1) : 0;
-  Cta<W, LOGN> c(smem, LL, items, G, P, false, SPLIT ? (int)(blockIdx.x >> 1) : -1, SPLIT ? half : -1);
+  const int half = SPLIT ? (vb & 1) : 0;
+  Cta<W, LOGN> c(smem, LL, items, G, P, false, SPLIT ? (vb >> 1) : vb, SPLIT ? half : -1);
   constexpr int n = 1 << LOGN;                     // evaluations handled by this CTA
   constexpr int nfull = SPLIT ? 2 * n : n;          // ring degree
   constexpr bool AG = RelinCfg<W, LOGN, SPLIT>::ACC_GLOBAL;
@@ -813,6 +814,16 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT>::threads, RelinCfg<W,
       }
     }
   }
+}
+
+template <typename W, int LOGN, bool GIVEN_D, bool SPLIT = false>
+__global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT>::threads, RelinCfg<W, LOGN, SPLIT>::min_blocks)
+    k_relin_t(const uint64_t* a, const uint64_t* __restrict__ b, int64_t a_stride, int64_t b_stride,
+              const uint64_t* __restrict__ c2, const uint64_t* __restrict__ kval,
+              const uint64_t* __restrict__ kpack, const uint32_t* __restrict__ kmont, uint64_t* out,
+              int nl, int64_t items, int G, const RelinC K, const LimbList LL, const CtxParams P) {
+  relin_body<W, LOGN, GIVEN_D, SPLIT>((int)blockIdx.x, a, b, a_stride, b_stride, c2, kval, kpack, kmont, out, nl,
+                                      items, G, K, LL, P);
 }
 
 // ---------------------------------------------------------------------------
