@@ -77,6 +77,10 @@ struct Cta {
 __device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
 }
+// the next row's operands -> L2 while this row computes (one thread per CTA issues it)
+__device__ __forceinline__ void l2_next(bool more, const void* p, unsigned bytes) {
+  if (more && threadIdx.x == 0) l2_prefetch(p, bytes);
+}
 
 #define HG_KERNEL template <typename W, int LOGN> __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_blocks)
 
@@ -92,6 +96,7 @@ __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_block
   const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
   for (int r = c.r0; r < c.r1; ++r) {
     uint64_t* g = base + ((int64_t)r * nl + c.limb) * n;
+    l2_next(r + 1 < c.r1, g + (int64_t)nl * n, n * 8);
     lz::load<W, LOGN>(c.s, g);
     __syncthreads();
     if (INV) lz::inv<W, LOGN>(c.s, c.tw, Lz<W>::ninv(*c.L), q, q2);
@@ -136,6 +141,7 @@ HG_KERNEL k_lift_ntt_t(const int64_t* __restrict__ src, uint64_t* __restrict__ o
   const int64_t small = std::is_floating_point_v<W> ? (int64_t)c.L->q : ((int64_t)1 << 31);
   for (int r = c.r0; r < c.r1; ++r) {
     const int64_t* g = src + (int64_t)r * n;
+    l2_next(r + 1 < c.r1, g + n, n * 8);
     lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
       const int64_t v = __ldg(g + k);
       // |v| < 2^31 (32-bit lane) or |v| < q (fp64 lane): the cheap centred-lift path
@@ -173,6 +179,7 @@ __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_block
   const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
   const uint64_t half = c.L->q / 2;
   for (int r = c.r0; r < c.r1; ++r) {
+    l2_next(r + 1 < c.r1, in + ((int64_t)(r + 1) * nl + c.limb) * n, n * 8);
     lz::load<W, LOGN>(c.s, in + ((int64_t)r * nl + c.limb) * n);
     __syncthreads();
     lz::inv<W, LOGN>(c.s, c.tw, Lz<W>::ninv(*c.L), q, q2);
@@ -213,6 +220,8 @@ __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_block
   for (int r = c.r0; r < c.r1; ++r) {
     const CT* cv = cen + (int64_t)r * n;
     const uint64_t* x = in + ((int64_t)r * nl + j) * n;
+    l2_next(r + 1 < c.r1, cv + n, n * sizeof(CT));
+    l2_next(r + 1 < c.r1, x + (int64_t)nl * n, n * 8);
     lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return lift_cen<W, CT>(__ldg(cv + k), *c.L, mu32); }, c.tw, q, q2);
     lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2);
     uint64_t* o = out + ((int64_t)r * t + j) * n;
@@ -261,6 +270,8 @@ __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_block
   const lz::TWT<W> psi1 = first_twiddle<W>(*c.L);
   for (int r = c.r0; r < c.r1; ++r) {
     const CT* cv = cen + (int64_t)r * nfull;
+    l2_next(r + 1 < c.r1, cv + nfull, nfull * sizeof(CT));
+    l2_next(r + 1 < c.r1, in + ((int64_t)(r + 1) * nl + j) * nfull + (int64_t)half * n, n * 8);
     lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
       W x0 = lift_cen<W, CT>(__ldg(cv + k), *c.L, mu32), x1 = lift_cen<W, CT>(__ldg(cv + k + n), *c.L, mu32);
       ct_lz<W>(x0, x1, psi1, q, q2);
@@ -360,6 +371,9 @@ HG_KERNEL k_encrypt_t(const int64_t* __restrict__ samples, const int64_t* __rest
   const int64_t pw = (int64_t)nl * n;
   for (int r = c.r0; r < c.r1; ++r) {
     const int64_t* su = samples + (int64_t)r * 3 * n;
+    l2_next(r + 1 < c.r1, su + 3 * n, 3 * n * 8);
+    if (mcoef) l2_next(r + 1 < c.r1, mcoef + (int64_t)(r + 1) * n, n * 8);
+    if (pt) l2_next(r + 1 < c.r1, pt + (int64_t)(r + 1) * pw + (int64_t)j * n, n * 8);
     // ---- NTT(u) -> registers (canonical) ----
     W u[GPT][16];
     lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return lift_any<W>(__ldg(su + k), *c.L, mu32); }, c.tw, q, q2);
@@ -435,6 +449,12 @@ HG_KERNEL k_relin_c2_t(const uint64_t* __restrict__ a, const uint64_t* __restric
   for (int r = c.r0; r < c.r1; ++r) {
     const uint64_t* x1 = a + r * a_stride + a1_off + (int64_t)c.limb * n;
     const uint64_t* y1 = b + r * b_stride + b1_off + (int64_t)c.limb * n;
+    l2_next(r + 1 < c.r1, x1 + a_stride, n * 8);
+    if (!square) l2_next(r + 1 < c.r1, y1 + b_stride, n * 8);
+    if (d != nullptr) {
+      l2_next(r + 1 < c.r1, x1 - a1_off + a_stride, n * 8);
+      if (!square) l2_next(r + 1 < c.r1, y1 - b1_off + b_stride, n * 8);
+    }
     if (d != nullptr) {
       const uint64_t* x0 = a + r * a_stride + (int64_t)c.limb * n;
       const uint64_t* y0 = b + r * b_stride + (int64_t)c.limb * n;
@@ -596,6 +616,10 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
     const uint64_t* c2item = c2 + (int64_t)item * pw;
     for (int i = 0; i < nl; ++i) {
       const uint64_t* src = c2item + (int64_t)i * nfull;
+      if constexpr (!C2S) {  // the next residue's c2 row -> L2 behind this residue's digits
+        if (i + 1 < nl) l2_next(true, src + nfull, nfull * 8);
+        else l2_next(item + 1 < c.r1, c2 + (int64_t)(item + 1) * pw, nfull * 8);
+      }
       if constexpr (GIVEN_D) {
         // the epilogue's d0, d1 rows -> L2 while the last residue's digits run
         if (i == nl - 1 && threadIdx.x == 0) {
