@@ -986,8 +986,9 @@ void mul_relin(const Context& c, const Keys& keys, const uint64_t* a, const uint
     // out must not alias the inputs: the prologue writes d0, d1 into it
     check(out + items * 2 * pw <= a || a + items * 2 * pw <= out, HG_EINTERNAL, "relin output aliases its input");
     check(out + items * 2 * pw <= b || b + items * 2 * pw <= out, HG_EINTERNAL, "relin output aliases its input");
-    k2::relin_c2(c, a, b, 2 * pw, 2 * pw, pw, pw, c2, items, nl, s, out);
-    k2::relin(c, keys, a, b, 2 * pw, 2 * pw, false, c2, out, items, nl, s, true);
+    const bool dig = k2::relin_digits_ok(c, nl);  // c2 as u16 digit rows (2^13)
+    k2::relin_c2(c, a, b, 2 * pw, 2 * pw, pw, pw, c2, items, nl, s, out, dig);
+    k2::relin(c, keys, a, b, 2 * pw, 2 * pw, false, c2, out, items, nl, s, true, dig);
     return;
   }
   const size_t sm = limb_smem(c);

@@ -436,9 +436,17 @@ HG_KERNEL k_encrypt_t(const int64_t* __restrict__ samples, const int64_t* __rest
 // (ckks_backend.hpp:306-318) as out[item][2][nl][N], so the key switch only adds its
 // accumulators to them: the products leave the key-switch epilogue, where every warp
 // of the (one-CTA-per-SM) key switch would wait on their loads at once.
+// digit rows of c2 (dig != nullptr): residue i's digits (c2_i >> 15d) & 0x7FFF, d < D_i, as u16
+// rows [item][rows0[i] + d][N] (ckks_backend.hpp:520-521), the key switch's only use of c2
+struct DigRows {
+  int rows0[HG_MAX_LIMBS];
+  int digits[HG_MAX_LIMBS];
+  int sd;
+};
 HG_KERNEL k_relin_c2_t(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int64_t a_stride,
                        int64_t b_stride, int64_t a1_off, int64_t b1_off, uint64_t* __restrict__ c2, int nl,
-                       int64_t items, int G, const LimbList LL, const CtxParams P, uint64_t* __restrict__ d) {
+                       int64_t items, int G, const LimbList LL, const CtxParams P, uint64_t* __restrict__ d,
+                       uint16_t* __restrict__ dig, const DigRows DR) {
   extern __shared__ __align__(16) uint64_t smem[];
   Cta<W, LOGN> c(smem, LL, items, G, P, true);
   constexpr int n = 1 << LOGN;
@@ -486,7 +494,23 @@ HG_KERNEL k_relin_c2_t(const uint64_t* __restrict__ a, const uint64_t* __restric
     }
     __syncthreads();
     lz::inv<W, LOGN>(c.s, c.tw, Lz<W>::ninv(*c.L), q, q2);
-    lz::store<W, LOGN>(c2 + ((int64_t)r * nl + c.limb) * n, c.s);
+    if (dig != nullptr) {
+      const int nd = DR.digits[c.limb];
+      uint16_t* drow = dig + ((int64_t)r * DR.sd + DR.rows0[c.limb]) * n;
+      for (int k4 = threadIdx.x; k4 < n / 4; k4 += lz::lz_threads<LOGN>()) {
+        uint64_t v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e] = (uint64_t)c.s[lz::padw<W>(4 * k4 + e)];
+        for (int dd = 0; dd < nd; ++dd) {
+          const int sh = 15 * dd;
+          reinterpret_cast<ushort4*>(drow + (int64_t)dd * n)[k4] =
+              make_ushort4((unsigned short)((v[0] >> sh) & 0x7FFF), (unsigned short)((v[1] >> sh) & 0x7FFF),
+                           (unsigned short)((v[2] >> sh) & 0x7FFF), (unsigned short)((v[3] >> sh) & 0x7FFF));
+        }
+      }
+    } else {
+      lz::store<W, LOGN>(c2 + ((int64_t)r * nl + c.limb) * n, c.s);
+    }
     __syncthreads();
   }
 }
@@ -512,7 +536,7 @@ struct RelinC {
 
 // SPLIT: LOGN is the half transform of a 2^(LOGN+1)-point ring (two CTAs per row, one per
 // half of the evaluations; the first forward stage is applied while reading the digits)
-template <typename W, int LOGN, bool SPLIT = false>
+template <typename W, int LOGN, bool SPLIT = false, bool DIG = false>
 struct RelinCfg {
   // thread vt owns evaluation groups vt + g threads (16 evaluations each), g < GPT
   static constexpr int threads = lz::lz_threads<LOGN>();
@@ -526,8 +550,12 @@ struct RelinCfg {
   static constexpr size_t key_bytes = (size_t)8 << LOGN;
   static constexpr bool KS = sizeof(W) == 4 && (C2S || SPLIT) &&
                              Cfg<W, LOGN>::smem + (C2S ? ((size_t)8 << LOGN) : 0) + key_bytes <= kSmemCap;
-  static constexpr size_t smem = Cfg<W, LOGN>::smem + (C2S ? ((size_t)8 << LOGN) : 0) + (KS ? key_bytes : 0);
+  // DIG: the 15-bit digit rows come from relin_c2 as u16 [item][row][N]; each row (the whole
+  // ring, both halves) is staged by cp.async one digit ahead
+  static constexpr size_t ds_bytes = DIG ? ((size_t)2 << LOGN) * (SPLIT ? 2 : 1) : 0;
   static constexpr size_t ks_off = Cfg<W, LOGN>::smem + (C2S ? ((size_t)8 << LOGN) : 0);
+  static constexpr size_t ds_off = ks_off + (KS ? key_bytes : 0);
+  static constexpr size_t smem = ds_off + ds_bytes;
   // CTAs of <= 256 threads (2^12 rows, half rows of a 2^13 ring) fit twice per SM by shared
   // memory: cap registers at 128 so the register file holds both (measured: +3..15% ct ops/s)
   static constexpr int min_blocks = (threads <= 256 && 2 * smem <= kSmemCap) ? 2 : 1;
@@ -557,7 +585,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 // the key switch of CTA `vb` (k_relin_t passes blockIdx.x)
-template <typename W, int LOGN, bool GIVEN_D, bool SPLIT>
+template <typename W, int LOGN, bool GIVEN_D, bool SPLIT, bool DIG>
 __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, const uint64_t* __restrict__ b,
                                            int64_t a_stride, int64_t b_stride, const uint64_t* __restrict__ c2,
                                            const uint64_t* __restrict__ kval, const uint64_t* __restrict__ kpack,
@@ -568,11 +596,32 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
   Cta<W, LOGN> c(smem, LL, items, G, P, false, SPLIT ? (vb >> 1) : vb, SPLIT ? half : -1);
   constexpr int n = 1 << LOGN;                     // evaluations handled by this CTA
   constexpr int nfull = SPLIT ? 2 * n : n;          // ring degree
-  constexpr bool AG = RelinCfg<W, LOGN, SPLIT>::ACC_GLOBAL;
-  constexpr bool C2S = RelinCfg<W, LOGN, SPLIT>::C2S;
-  constexpr bool KS = RelinCfg<W, LOGN, SPLIT>::KS;
+  using RC = RelinCfg<W, LOGN, SPLIT, DIG>;
+  constexpr bool AG = RC::ACC_GLOBAL;
+  constexpr bool C2S = RC::C2S && !DIG;
+  constexpr bool KS = RC::KS;
+  static_assert(!DIG || SPLIT, "digit rows are staged for half-row CTAs");
+  // DIG: c2 holds u16 digit rows [item][sd][nfull] (relin_c2 with digits); ds stages one row
+  const uint16_t* const dig = reinterpret_cast<const uint16_t*>(c2);
+  uint16_t* const ds = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(smem) + RC::ds_off);
+  const int sd = K.rows0[nl - 1] + K.digits[nl - 1];
+  auto stage_dig = [&](int it, int row) {  // digit row -> ds, 16 bytes per cp.async
+    const uint4* g = reinterpret_cast<const uint4*>(dig + ((int64_t)it * sd + row) * nfull);
+    for (int ch = threadIdx.x; ch < nfull / 8; ch += lz::lz_threads<LOGN>())
+      cp_async16(reinterpret_cast<uint4*>(ds) + ch, g + ch);
+    cp_async_commit();
+  };
+  (void)dig;
+  (void)ds;
+  (void)sd;
+  (void)stage_dig;
+  if constexpr (DIG) {
+    stage_dig(c.r0, 0);
+    cp_async_wait_all();
+    __syncthreads();  // (also orders the twiddle staging)
+  }
   uint64_t* c2s = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(smem) + Cfg<W, LOGN>::smem);
-  uint4* ks = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(smem) + RelinCfg<W, LOGN, SPLIT>::ks_off);
+  uint4* ks = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(smem) + RC::ks_off);
   const int64_t hoff = (int64_t)half * n;           // this CTA's evaluation offset
   (void)ks;
   (void)kmont;
@@ -586,7 +635,7 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
   const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
   const uint64_t Q = c.L->q;
   const int64_t pw = (int64_t)nl * nfull;
-  constexpr int GPT = RelinCfg<W, LOGN, SPLIT>::GPT;
+  constexpr int GPT = RC::GPT;
   // SPLIT: the first forward stage, x_k +/- psi_1 x_{k+N/2}, fused into the digit read
   using TWW = lz::TWT<W>;
   TWW psi1{};
@@ -616,7 +665,7 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
     const uint64_t* c2item = c2 + (int64_t)item * pw;
     for (int i = 0; i < nl; ++i) {
       const uint64_t* src = c2item + (int64_t)i * nfull;
-      if constexpr (!C2S) {  // the next residue's c2 row -> L2 behind this residue's digits
+      if constexpr (!C2S && !DIG) {  // the next residue's c2 row -> L2 behind this residue's digits
         if (i + 1 < nl) l2_next(true, src + nfull, nfull * 8);
         else l2_next(item + 1 < c.r1, c2 + (int64_t)(item + 1) * pw, nfull * 8);
       }
@@ -655,6 +704,17 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
             if (i + 1 < nl) { stage_c2(src + n); c2_staged = true; }
             else if (item + 1 < c.r1) { stage_c2(c2 + (int64_t)(item + 1) * pw); c2_staged = true; }
           }
+        } else if constexpr (DIG) {
+          lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
+            const W x0 = (W)(uint32_t)ds[k];
+            W x1 = (W)(uint32_t)ds[k + n];
+            W x0b = x0;
+            ct_lz<W>(x0b, x1, psi1, q, q2);  // (x0 + psi x1, x0 - psi x1), lazy
+            return half ? x1 : x0b;
+          }, c.tw, q, q2);
+          // row consumed (fwd_first_from ends with a barrier): stage the next one behind this NTT
+          if (row + 1 < sd) { stage_dig(item, row + 1); c2_staged = true; }
+          else if (item + 1 < c.r1) { stage_dig(item + 1, 0); c2_staged = true; }
         } else if constexpr (SPLIT) {
           lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
             const W x0 = (W)(uint32_t)((__ldg(src + k) >> sh) & 0x7FFF);
@@ -769,6 +829,7 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
             }
           }
         }
+        if constexpr (DIG) cp_async_wait_all();  // the next digit row (staged behind this NTT)
         __syncthreads();  // smem reused by the next digit
       }
     }
@@ -840,13 +901,13 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
   }
 }
 
-template <typename W, int LOGN, bool GIVEN_D, bool SPLIT = false>
-__global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT>::threads, RelinCfg<W, LOGN, SPLIT>::min_blocks)
+template <typename W, int LOGN, bool GIVEN_D, bool SPLIT = false, bool DIG = false>
+__global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT, DIG>::threads, RelinCfg<W, LOGN, SPLIT, DIG>::min_blocks)
     k_relin_t(const uint64_t* a, const uint64_t* __restrict__ b, int64_t a_stride, int64_t b_stride,
               const uint64_t* __restrict__ c2, const uint64_t* __restrict__ kval,
               const uint64_t* __restrict__ kpack, const uint32_t* __restrict__ kmont, uint64_t* out,
               int nl, int64_t items, int G, const RelinC K, const LimbList LL, const CtxParams P) {
-  relin_body<W, LOGN, GIVEN_D, SPLIT>((int)blockIdx.x, a, b, a_stride, b_stride, c2, kval, kpack, kmont, out, nl,
+  relin_body<W, LOGN, GIVEN_D, SPLIT, DIG>((int)blockIdx.x, a, b, a_stride, b_stride, c2, kval, kpack, kmont, out, nl,
                                       items, G, K, LL, P);
 }
 
@@ -1401,10 +1462,19 @@ static bool relin_split13() {
 
 bool relin_supported(const Context& c) { return c.logn() >= 10 && c.logn() <= 15; }
 
+bool relin_digits_ok(const Context& c, int nl) {
+  static const bool on = [] {
+    const char* e = std::getenv("HG_RELIN_DIG");
+    return !(e && e[0] == '0');
+  }();
+  return on && c.logn() == 13 && relin_split13() && classify(c, 0, nl, fp64_lane()).wide.count == 0;
+}
+
 void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, int64_t a_stride,
            int64_t b_stride, bool given_d, const uint64_t* c2, uint64_t* out, int64_t items, int nl, cudaStream_t s,
-           bool d_in_out) {
+           bool d_in_out, bool digits) {
   check(relin_supported(c), HG_EINTERNAL, "key switch: ring degree outside 2^10..2^15");
+  check(!digits || relin_digits_ok(c, nl), HG_EINTERNAL, "key switch: digit rows outside the 2^13 half-row layout");
   if (items <= 0) return;
   const RelinC K = relin_consts(c, nl);
   const Classes cl = classify(c, 0, nl, fp64_lane());
@@ -1415,9 +1485,9 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
     using W = decltype(wtag);
     if (LL.count == 0) return;
     by_logn<W>(c, [&]<typename W_, int LOGN>() {
-      auto go = [&]<bool SPLIT>() {
+      auto go = [&]<bool SPLIT, bool DIG = false>() {
         constexpr int LT = SPLIT ? LOGN - 1 : LOGN;
-        using Cf = RelinCfg<W_, LT, SPLIT>;
+        using Cf = RelinCfg<W_, LT, SPLIT, DIG>;
         const int threads = Cf::threads;
         const int64_t target = 148LL * 3;
         const int halves = SPLIT ? 2 : 1;
@@ -1429,19 +1499,19 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
         const bool gd = given_d || in_out;
         const uint64_t* aa = in_out ? out : a;
         const int64_t as = in_out ? 2LL * nl * c.n() : a_stride;
-        const void* fn =
-            gd ? (const void*)k_relin_t<W_, LT, true, SPLIT> : (const void*)k_relin_t<W_, LT, false, SPLIT>;
+        const void* fn = gd ? (const void*)k_relin_t<W_, LT, true, SPLIT, DIG>
+                            : (const void*)k_relin_t<W_, LT, false, SPLIT, DIG>;
         set_smem_attr(fn, Cf::smem);
         const double frac = (double)LL.count / nl;
         // bytes: c2 + (a, b | d0, d1) + out once, key rows once; modmuls: digit NTTs + key MACs (+ tensor)
         c.kt_begin(std::is_floating_point_v<W_> ? "k_relin_t/f64" : sizeof(W_) == 4 ? "k_relin_t/u32" : "k_relin_t/u64", s, frac * (items * pw8 * (gd ? 5 : 7) + (double)sd * 2 * pw8),
                    (double)items * LL.count * (sd * (bfly(c) + 2.0 * c.n()) + (gd ? 0.0 : 3.0 * c.n())));
         if (gd)
-          k_relin_t<W_, LT, true, SPLIT><<<grid, threads, Cf::smem, s>>>(
+          k_relin_t<W_, LT, true, SPLIT, DIG><<<grid, threads, Cf::smem, s>>>(
               aa, b, as, b_stride, c2, keys.relin.as<uint64_t>(), keys.relin_pack.as<uint64_t>(),
               keys.relin_mont.as<uint32_t>(), out, nl, items, G, K, LL, c.kp());
         else
-          k_relin_t<W_, LT, false, SPLIT><<<grid, threads, Cf::smem, s>>>(
+          k_relin_t<W_, LT, false, SPLIT, DIG><<<grid, threads, Cf::smem, s>>>(
               a, b, a_stride, b_stride, c2, keys.relin.as<uint64_t>(), keys.relin_pack.as<uint64_t>(),
               keys.relin_mont.as<uint32_t>(), out, nl, items, G, K, LL, c.kp());
         c.kt_end(s);
@@ -1452,7 +1522,8 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
       // CTAs run two per SM, with their own barriers (relin_split13())
       if constexpr (LOGN == 15 || (LOGN == 14 && !std::is_same_v<W_, uint64_t>)) go.template operator()<true>();
       else if constexpr (LOGN == 13 && !std::is_same_v<W_, uint64_t>) {
-        if (relin_split13()) go.template operator()<true>();
+        if (digits) go.template operator()<true, true>();
+        else if (relin_split13()) go.template operator()<true>();
         else go.template operator()<false>();
       } else {
         go.template operator()<false>();
@@ -1466,8 +1537,16 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
 }
 
 void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_stride, int64_t b_stride,
-              int64_t a1_off, int64_t b1_off, uint64_t* c2, int64_t items, int nl, cudaStream_t s, uint64_t* d) {
+              int64_t a1_off, int64_t b1_off, uint64_t* c2, int64_t items, int nl, cudaStream_t s, uint64_t* d,
+              bool digits) {
   if (items <= 0) return;
+  DigRows DR{};
+  for (int i = 0; i < nl; ++i) {
+    DR.rows0[i] = c.relin_row(i, 0);
+    DR.digits[i] = c.digits(i);
+  }
+  DR.sd = DR.rows0[nl - 1] + DR.digits[nl - 1];
+  uint16_t* dig = digits ? reinterpret_cast<uint16_t*>(c2) : nullptr;
   const Classes cl = classify(c, 0, nl, fp64_lane());
   const double nw = (double)c.n() * 8;
   auto run = [&](const LimbList& LL, auto wtag, cudaStream_t s) {
@@ -1486,7 +1565,7 @@ void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_
                  (double)items * LL.count * (dd ? (sq ? 5 : 7) : 3) * nw,
                  (double)items * LL.count * (bfly(c) + c.n() * (dd ? 4 : 1)));
       k_relin_c2_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(a, b, a_stride, b_stride, a1_off, b1_off, c2, nl,
-                                                                 items, G, LL, c.kp(), dd);
+                                                                 items, G, LL, c.kp(), dd, dig, DR);
       c.kt_end(s);
       HG_CUDA(cudaGetLastError());
     });
