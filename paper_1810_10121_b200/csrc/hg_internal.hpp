@@ -368,7 +368,7 @@ void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_
               int64_t a1_off, int64_t b1_off, uint64_t* c2, int64_t items, int nl, cudaStream_t s,
               uint64_t* d = nullptr, bool digits = false);
 // digits: relin_c2 writes the key switch's u16 digit rows into the c2 buffer instead of c2
-// (2 D_i bytes per residue coefficient <= 8), and relin stages them (2^13 half-row layout)
+// (2 D_i bytes per residue coefficient <= 8), and relin stages them (2^13 / 2^14 half rows)
 bool relin_digits_ok(const Context& c, int nl);
 // grouped modular GEMM (same contract as k::gemm_groups), IMAD.WIDE accumulation
 void gemm(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* idx, const uint64_t* w,

@@ -1467,7 +1467,9 @@ bool relin_digits_ok(const Context& c, int nl) {
     const char* e = std::getenv("HG_RELIN_DIG");
     return !(e && e[0] == '0');
   }();
-  return on && c.logn() == 13 && relin_split13() && classify(c, 0, nl, fp64_lane()).wide.count == 0;
+  // half-row layouts with room for a staged digit row: 2^13 (split13) and 2^14
+  return on && ((c.logn() == 13 && relin_split13()) || c.logn() == 14) &&
+         classify(c, 0, nl, fp64_lane()).wide.count == 0;
 }
 
 void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, int64_t a_stride,
@@ -1520,7 +1522,11 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
       // 2^14, 2^15: two CTAs per row, one per half of the evaluations (2^13- / 2^14-point half
       // transforms); a whole 2^15-point row does not fit one CTA's shared memory.  2^13: half-row
       // CTAs run two per SM, with their own barriers (relin_split13())
-      if constexpr (LOGN == 15 || (LOGN == 14 && !std::is_same_v<W_, uint64_t>)) go.template operator()<true>();
+      if constexpr (LOGN == 15) go.template operator()<true>();
+      else if constexpr (LOGN == 14 && !std::is_same_v<W_, uint64_t>) {
+        if (digits) go.template operator()<true, true>();
+        else go.template operator()<true>();
+      }
       else if constexpr (LOGN == 13 && !std::is_same_v<W_, uint64_t>) {
         if (digits) go.template operator()<true, true>();
         else if (relin_split13()) go.template operator()<true>();
