@@ -205,7 +205,9 @@ def roofline_from_stats(stats: dict, peaks: dict, int_peak32: float):
           "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/)",
           "alg_bytes_per_launch": st["alg_bytes"] / max(1, st["launches"]),
           "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)",
-          "launches_in_region": st["launches"], "avg_launch_ms": st["total_ms"] / max(1, st["launches"])}
+          "launches_in_region": st["launches"], "avg_launch_ms": st["total_ms"] / max(1, st["launches"]),
+          "note": "integer-modmul-bound kernels (key switch, NTT; SURVEY 8(d)) bind on roofline_modmul.frac; "
+                  "this object is the HBM view of the same launches"}
     mm = st["alg_modmuls"] / sec / 1e9 if sec > 0 else 0.0
     rl_int = {"kernel": name, "bound": "int-modmul", "achieved": mm, "peak": int_peak32 / 1e9,
               "unit": "Gmodmul/s", "frac": mm / (int_peak32 / 1e9) if int_peak32 else None,
