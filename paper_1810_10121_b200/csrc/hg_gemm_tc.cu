@@ -348,6 +348,7 @@ __global__ void __launch_bounds__(kTcThreadsWS, 1)
           v = (v << 8) % q;
         }
       }
+      const uint64_t brh = L.br_hi;
       const int nlo = half * (NT / 2), nhi = nlo + NT / 2;
       for (int n0 = nlo; n0 < nhi; n0 += 8) {
         uint32_t d[Cf::S][8];
@@ -363,21 +364,26 @@ __global__ void __launch_bounds__(kTcThreadsWS, 1)
         for (int e = 0; e < 8; ++e) {
           const int m = T.nt * NT + n0 + e;
           if (m >= mg) break;
+          // one 64-bit Barrett step (brh = floor(2^64 / q)): for x < 2^64 the quotient estimate
+          // is at most 2 short, so x - est q < 3q
+          auto red64 = [&](uint64_t x) {
+            uint64_t r = x - __umul64hi(x, brh) * q;
+            r = r >= q ? r - q : r;
+            return r >= q ? r - q : r;
+          };
           uint64_t res;
           if (q < (1ull << 30)) {
             uint64_t acc64 = 0;
 #pragma unroll
             for (int sg = 0; sg < Cf::S; ++sg) acc64 += (uint64_t)d[sg][e] * pw32[sg];
-            res = reduce128(acc64, 0, L);
+            res = red64(acc64);
           } else {
-            uint64_t accq = 0, pw = 1;
-            const uint64_t b256 = 256 % q;
+            // Horner over the shift groups, highest first: acc = acc 2^8 + D_s (mod q); acc < q
+            // < 2^50 and D_s < 2^31 keep every step below 2^59
+            uint64_t acc = 0;
 #pragma unroll
-            for (int sg = 0; sg < Cf::S; ++sg) {
-              accq = add_mod(accq, mul_mod(d[sg][e], pw, L), q);
-              pw = mul_mod(pw, b256, L);
-            }
-            res = accq;
+            for (int sg = Cf::S - 1; sg >= 0; --sg) acc = red64((acc << 8) + d[sg][e]);
+            res = acc;
           }
           const int64_t oi = oidx ? (int64_t)oidx[T.g * mg + m] : T.g * mg + m;
           out[(oi * 2 * nl + (int64_t)T.p * nl + limb) * n + col] = res;
