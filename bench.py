@@ -186,14 +186,31 @@ def workload_config(args, ctxp) -> dict:
                             f"NCCL all-gather-v of activations between layers")}
 
 
-def roofline_from_stats(stats: dict, peaks: dict, int_peak32: float):
-    """Dominant kernel by device time; achieved = algorithmic bytes (and modmuls) / time."""
-    dom = max(stats.items(), key=lambda kv: kv[1]["total_ms"])
-    name, st = dom
+def lane_peak(name: str, int_peaks: dict) -> float:
+    """modmul/s peak of the arithmetic lane a kernel runs in (name suffix /u32, /f64, /u64)."""
+    if name.endswith("/f64"):
+        return int_peaks["modmulf64_per_s"]
+    if name.endswith("/u64"):
+        return int_peaks["modmul64_per_s"]
+    return int_peaks["modmul32_per_s"]
+
+
+def roofline_from_stats(stats: dict, peaks: dict, int_peaks: dict, steps: int):
+    """Dominant kernel by device time.  The key switch and the NTTs are integer-modmul-bound
+    (SURVEY 8(d)), so the roofline object is the modmul view against the measured peak of the
+    kernel's arithmetic lane; the HBM view of the same launches is kept beside it.  `traffic`
+    (ncu DRAM bytes of the captured launch, profiles/ncu_traffic.json) is set against the
+    algorithmic bytes of that same launch: the first launch of the kernel in a step."""
+    total = sum(st["total_ms"] for st in stats.values())
+    name, st = max(stats.items(), key=lambda kv: kv[1]["total_ms"])
     sec = st["total_ms"] / 1e3
+    hbm = peaks.get("hbm_gbs", 6550.1)
+    peak_mm = lane_peak(name, int_peaks)
+    mm = st["alg_modmuls"] / sec if sec > 0 else 0.0
     gbs = st["alg_bytes"] / sec / 1e9 if sec > 0 else 0.0
-    hbm = peaks.get("hbm_gbs", 6552.6)
-    # DRAM bytes per launch of this kernel from the committed ncu --set full capture (profiles/)
+    first = st.get("first") or [[st["total_ms"] / max(1, st["launches"]), st["alg_bytes"] / max(1, st["launches"]),
+                                 st["alg_modmuls"] / max(1, st["launches"])]]
+    l0_ms, l0_bytes, l0_mm = first[0]
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
@@ -201,18 +218,32 @@ def roofline_from_stats(stats: dict, peaks: dict, int_peak32: float):
             ent = json.load(f).get(name)
         if ent:
             traffic = ent["dram_bytes_per_launch"]
-    rl = {"kernel": name, "bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
-          "traffic": traffic, "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/)",
-          "alg_bytes_per_launch": st["alg_bytes"] / max(1, st["launches"]),
-          "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)",
-          "launches_in_region": st["launches"], "avg_launch_ms": st["total_ms"] / max(1, st["launches"]),
-          "note": "integer-modmul-bound kernels (key switch, NTT; SURVEY 8(d)) bind on roofline_modmul.frac; "
-                  "this object is the HBM view of the same launches"}
-    mm = st["alg_modmuls"] / sec / 1e9 if sec > 0 else 0.0
-    rl_int = {"kernel": name, "bound": "int-modmul", "achieved": mm, "peak": int_peak32 / 1e9,
-              "unit": "Gmodmul/s", "frac": mm / (int_peak32 / 1e9) if int_peak32 else None,
-              "peak_source": "register-only 32-bit Shoup modmul microkernel on this GPU (hg_bench_modmul)"}
-    return rl, rl_int
+    rl = {"kernel": name, "bound": "int-modmul", "achieved": mm / 1e9, "peak": peak_mm / 1e9, "unit": "Gmodmul/s",
+          "frac": mm / peak_mm if peak_mm else None,
+          "peak_source": "register-only modmul microkernel of this kernel's lane on this GPU (hg_bench_modmul); "
+                         "MEASURED_PEAKS.json has no integer figure",
+          "traffic": traffic,
+          "traffic_unit": "DRAM bytes of the first launch per step (ncu dram__bytes_read+write, profiles/)",
+          "alg_bytes_first_launch": l0_bytes,
+          "traffic_over_alg": traffic / l0_bytes if traffic and l0_bytes else None,
+          "first_launch": {"ms": l0_ms, "alg_bytes": l0_bytes, "alg_modmuls": l0_mm,
+                           "frac": (l0_mm / (l0_ms / 1e3)) / peak_mm if l0_ms > 0 and peak_mm else None},
+          "launches_in_region": st["launches"], "launches_per_step": st["launches"] / max(1, steps),
+          "avg_launch_ms": st["total_ms"] / max(1, st["launches"]),
+          "share_of_kernel_time": st["total_ms"] / total if total else None,
+          "hbm_view": {"achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                       "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy bandwidth)"}}
+    # every kernel above 3% of the kernel time, in both views
+    per = {}
+    for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["total_ms"]):
+        if not total or v["total_ms"] < 0.03 * total:
+            continue
+        sk = v["total_ms"] / 1e3
+        pk = lane_peak(k, int_peaks)
+        per[k] = {"share": v["total_ms"] / total, "ms_per_step": v["total_ms"] / max(1, steps),
+                  "modmul_frac": (v["alg_modmuls"] / sk) / pk if sk > 0 and pk else None,
+                  "hbm_frac": (v["alg_bytes"] / sk / 1e9) / hbm if sk > 0 else None}
+    return rl, per
 
 
 def ours_arm(args):
@@ -333,9 +364,9 @@ def ours_arm(args):
     d2h = o_elems * (o_level + 1) * n * 8  # decrypted coefficient-domain outputs (c3: 10 logits, 2 limbs)
 
     # ---- roofline + CPU baseline (rank 0, N=1 only for the CPU leg) ----
-    int_peak32 = ctx.modmul_peak(False)
-    int_peak64 = ctx.modmul_peak(True)
-    rl, rl_int = roofline_from_stats(stats, peaks, int_peak32)
+    int_peaks = {"modmul32_per_s": ctx.modmul_peak(0), "modmul64_per_s": ctx.modmul_peak(1),
+                 "modmulf64_per_s": ctx.modmul_peak(2)}
+    rl, per_kernel = roofline_from_stats(stats, peaks, int_peaks, args.steps)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu and os.path.exists(REF_HARNESS):
         try:
@@ -346,6 +377,12 @@ def ours_arm(args):
                    "sample": f"one full heg::execute of the same config-3 graph (batch {spec['batch']}) through the "
                              f"unmodified reference CkksBackend on {threads} host threads "
                              f"({res['execute_ms'] / 1e3:.1f} s)"}
+            # the same run at ExecOptions.threads = 1
+            if not args.no_cpu_single:
+                r1 = run_reference_harness(g, x, spec, ctxp, 1, 0, 1)
+                cpu["single_thread"] = {"value": spec["batch"] / (r1["execute_ms"] / 1e3), "unit": "images/s",
+                                        "cores": 1, "sample": f"one full heg::execute at threads=1 "
+                                                              f"({r1['execute_ms'] / 1e3:.1f} s)"}
         except Exception as e:  # the CPU leg is a report, never a reason to lose the GPU line
             cpu = {"value": None, "unit": "images/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
@@ -356,8 +393,8 @@ def ours_arm(args):
             "scaling": "strong" if shard else "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic (seeded pixels k/255, weights N(0,1/fan_in))",
             "config": workload_config(args, ctxp),
-            "roofline": rl, "roofline_modmul": rl_int,
-            "int_peaks": {"modmul32_per_s": int_peak32, "modmul64_per_s": int_peak64},
+            "roofline": rl, "roofline_kernels": per_kernel,
+            "int_peaks": int_peaks,
             "cpu_baseline": cpu,
             "e2e": {"value": images / e2e_s, "unit": "images/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3,
@@ -384,6 +421,7 @@ def main():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--batch", type=int, default=4096)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-cpu-single", action="store_true", help="skip the threads=1 figure of the cpu_baseline leg")
     ap.add_argument("--mode", default="shard", choices=["shard", "replicas"],
                     help="N>1: shard each Dot/Conv by outputs (NCCL gathers) or run independent replicas")
     args = ap.parse_args()

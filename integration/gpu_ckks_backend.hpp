@@ -19,6 +19,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -135,17 +136,53 @@ class GpuCkksBackend final : public HEBackend {
   // --- primitives (ckks_backend.hpp:253-340) --------------------------------------
   CiphertextPtr add(const HECiphertext& a, const HECiphertext& b) const override { return add_sub(a, b, false); }
   CiphertextPtr sub(const HECiphertext& a, const HECiphertext& b) const override { return add_sub(a, b, true); }
+  // out_size = |x| + |y| - 1 with d[i+j] += x_i y_j; only a size-3 result is relinearised
+  // (ckks_backend.hpp:261-281)
   CiphertextPtr multiply(const HECiphertext& a, const HECiphertext& b) const override {
     std::lock_guard<std::mutex> l(m_mu);
     const auto& x = ct(a);
     const auto& y = ct(b);
     require_same_level(x.level(), y.level(), "multiply");
     require_mul_headroom(x.level());
-    check(x.size() == 2 && y.size() == 2, errc::validation, "GPU multiply takes size-2 ciphertexts");
-    Buf o = words(x.level(), 2);
-    hg_ok(hg_multiply_relin(m_ctx, m_keys, x.buf()->p, y.buf()->p, o->p, 1, x.level() + 1));
     const NoiseEstimate noise{m_noise.multiply_bound(x.noise().bound, x.scale(), y.noise().bound, y.scale())};
-    return std::make_shared<GpuCiphertext>(x.level(), x.scale() * y.scale(), 2, noise, o);
+    const int nl = x.level() + 1;
+    if (x.size() == 2 && y.size() == 2) {  // the fused tensor + key switch
+      Buf o = words(x.level(), 2);
+      hg_ok(hg_multiply_relin(m_ctx, m_keys, x.buf()->p, y.buf()->p, o->p, 1, nl));
+      return std::make_shared<GpuCiphertext>(x.level(), x.scale() * y.scale(), 2, noise, o);
+    }
+    const size_t out_size = x.size() + y.size() - 1;
+    const size_t pw = poly_words(x.level());
+    Buf o = words(x.level(), out_size);
+    Buf prod = words(x.level(), 1);
+    std::vector<bool> written(out_size, false);
+    for (size_t i = 0; i < x.size(); ++i)
+      for (size_t j = 0; j < y.size(); ++j) {  // poly_mul_acc(x_i, y_j, d[i+j]): exact modular sums
+        uint64_t* d = o->p + (i + j) * pw;
+        if (!written[i + j]) {
+          hg_ok(hg_multiply_plain(m_ctx, x.buf()->p + i * pw, y.buf()->p + j * pw, d, 1, 1, nl, 0));
+          written[i + j] = true;
+        } else {
+          hg_ok(hg_multiply_plain(m_ctx, x.buf()->p + i * pw, y.buf()->p + j * pw, prod->p, 1, 1, nl, 0));
+          hg_ok(hg_add(m_ctx, d, prod->p, d, static_cast<int64_t>(pw), nl));
+        }
+      }
+    hg_ok(hg_sync(m_ctx));  // `prod` is freed on return
+    return std::make_shared<GpuCiphertext>(x.level(), x.scale() * y.scale(), out_size, noise, o);
+  }
+  // the unrelinearised size-3 product (what CkksBackend::multiply returns without a relin key);
+  // an adapter extra, like CkksBackend::schoolbook_multiply
+  CiphertextPtr tensor3(const HECiphertext& a, const HECiphertext& b) const {
+    std::lock_guard<std::mutex> l(m_mu);
+    const auto& x = ct(a);
+    const auto& y = ct(b);
+    require_same_level(x.level(), y.level(), "multiply");
+    require_mul_headroom(x.level());
+    check(x.size() == 2 && y.size() == 2, errc::validation, "tensor3 takes size-2 ciphertexts");
+    Buf o = words(x.level(), 3);
+    hg_ok(hg_multiply_tensor(m_ctx, x.buf()->p, y.buf()->p, o->p, 1, x.level() + 1));
+    const NoiseEstimate noise{m_noise.multiply_bound(x.noise().bound, x.scale(), y.noise().bound, y.scale())};
+    return std::make_shared<GpuCiphertext>(x.level(), x.scale() * y.scale(), 3, noise, o);
   }
   CiphertextPtr negate(const HECiphertext& a) const override {
     std::lock_guard<std::mutex> l(m_mu);
@@ -265,6 +302,49 @@ class GpuCkksBackend final : public HEBackend {
                                            NoiseEstimate{m_noise.rescale_bound(noise, dropped)}, o);
   }
 
+  // ct x ct weighted sum: size-3 products accumulated exactly, relinearised ONCE, rescaled once
+  // (ckks_backend.hpp:413-450); the default (per-product relin) only where CkksBackend falls back
+  CiphertextPtr weighted_sum_cipher(const std::vector<CiphertextPtr>& xs,
+                                    const std::vector<CiphertextPtr>& ws) const override {
+    check(!xs.empty() && xs.size() == ws.size(), errc::internal, "weighted sum needs matching non-empty operands");
+    for (const CiphertextPtr& x : xs)
+      if (x->size() != 2) return weighted_sum_cipher_default(xs, ws);
+    for (const CiphertextPtr& w : ws)
+      if (w->size() != 2) return weighted_sum_cipher_default(xs, ws);
+    std::lock_guard<std::mutex> l(m_mu);
+    const auto& first = ct(*xs[0]);
+    const int level = first.level();
+    require_mul_headroom(level);
+    const double x_scale = first.scale(), w_scale = ct(*ws[0]).scale();
+    const size_t item = 2 * poly_words(level);
+    Buf xbuf = std::make_shared<DevWords>(item * xs.size());
+    Buf wbuf = std::make_shared<DevWords>(item * ws.size());
+    double noise = 0.0;
+    for (size_t i = 0; i < xs.size(); ++i) {
+      const auto& x = ct(*xs[i]);
+      const auto& w = ct(*ws[i]);
+      require_same_level(x.level(), level, "weighted_sum_cipher");
+      require_same_level(w.level(), level, "weighted_sum_cipher");
+      require_same_scale(x.scale(), x_scale, "weighted_sum_cipher");
+      require_same_scale(w.scale(), w_scale, "weighted_sum_cipher");
+      cudaMemcpy(xbuf->p + i * item, x.buf()->p, item * 8, cudaMemcpyDeviceToDevice);
+      cudaMemcpy(wbuf->p + i * item, w.buf()->p, item * 8, cudaMemcpyDeviceToDevice);
+      noise += m_noise.multiply_bound(x.noise().bound, x.scale(), w.noise().bound, w.scale());
+    }
+    std::vector<int32_t> idx(xs.size());
+    for (size_t i = 0; i < idx.size(); ++i) idx[i] = static_cast<int32_t>(i);
+    Buf ibuf = std::make_shared<DevWords>((idx.size() + 1) / 2);
+    cudaMemcpy(ibuf->p, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice);
+    const auto* ip = reinterpret_cast<const int32_t*>(ibuf->p);
+    Buf o = words(level - 1, 2);
+    hg_ok(hg_weighted_sum_cipher(m_ctx, m_keys, xbuf->p, ip, wbuf->p, ip, o->p, 1, static_cast<int>(xs.size()),
+                                 level + 1));
+    hg_ok(hg_sync(m_ctx));
+    const double dropped = static_cast<double>(m_context->moduli()[static_cast<size_t>(level)].value());
+    return std::make_shared<GpuCiphertext>(level - 1, x_scale * w_scale / dropped, 2,
+                                           NoiseEstimate{m_noise.rescale_bound(noise, dropped)}, o);
+  }
+
  private:
   static const GpuCiphertext& ct(const HECiphertext& c) {
     const auto* p = dynamic_cast<const GpuCiphertext*>(&c);
@@ -280,18 +360,35 @@ class GpuCkksBackend final : public HEBackend {
     return std::make_shared<DevWords>(polys * static_cast<size_t>(level + 1) *
                                       static_cast<size_t>(m_context->poly_degree()));
   }
+  size_t poly_words(int level) const {
+    return static_cast<size_t>(level + 1) * static_cast<size_t>(m_context->poly_degree());
+  }
+  // size = max(|x|, |y|); polys present in one operand only are copied (negated for y under
+  // subtraction), as ckks_backend.hpp:556-578
   CiphertextPtr add_sub(const HECiphertext& a, const HECiphertext& b, bool subtract) const {
     std::lock_guard<std::mutex> l(m_mu);
     const auto& x = ct(a);
     const auto& y = ct(b);
     require_same_level(x.level(), y.level(), subtract ? "sub" : "add");
     require_same_scale(x.scale(), y.scale(), subtract ? "sub" : "add");
-    check(x.size() == y.size(), errc::validation, "GPU add/sub takes equal-size ciphertexts");
-    Buf o = words(x.level(), x.size());
-    hg_ok((subtract ? hg_sub : hg_add)(m_ctx, x.buf()->p, y.buf()->p, o->p, static_cast<int64_t>(o->words),
-                                       x.level() + 1));
+    const size_t size = std::max(x.size(), y.size()), common = std::min(x.size(), y.size());
+    const size_t pw = poly_words(x.level());
+    const int nl = x.level() + 1;
+    Buf o = words(x.level(), size);
+    hg_ok((subtract ? hg_sub : hg_add)(m_ctx, x.buf()->p, y.buf()->p, o->p, static_cast<int64_t>(common * pw), nl));
+    if (size > common) {
+      const uint64_t* tail = (x.size() > common ? x.buf()->p : y.buf()->p) + common * pw;
+      const int64_t tw = static_cast<int64_t>((size - common) * pw);
+      if (y.size() > common && subtract) {
+        hg_ok(hg_negate(m_ctx, tail, o->p + common * pw, tw, nl));
+      } else {
+        hg_ok(hg_sync(m_ctx));
+        if (cudaMemcpy(o->p + common * pw, tail, static_cast<size_t>(tw) * 8, cudaMemcpyDeviceToDevice) != cudaSuccess)
+          fail(errc::internal, "cudaMemcpy failed");
+      }
+    }
     const NoiseEstimate noise{m_noise.add_bound(x.noise().bound, y.noise().bound)};
-    return std::make_shared<GpuCiphertext>(x.level(), x.scale(), x.size(), noise, o);
+    return std::make_shared<GpuCiphertext>(x.level(), x.scale(), size, noise, o);
   }
   CiphertextPtr add_sub_plain(const HECiphertext& a, const HEPlaintext& b, bool subtract) const {
     std::lock_guard<std::mutex> l(m_mu);

@@ -305,9 +305,12 @@ int mode_net(int argc, char** argv) {
   bool dump = true;
   int repeat = 1, warmup = 0;
   std::string paradigm = "encrypted-data";
+  bool opt_add = true, opt_mult = true;
   for (int a = 13; a < argc; ++a) {
     const std::string f = argv[a];
     if (f == "--no-dump") dump = false;
+    else if (f == "--no-opt-add") opt_add = false;
+    else if (f == "--no-opt-mult") opt_mult = false;
     else if (f.rfind("--repeat=", 0) == 0) repeat = std::max(1, std::stoi(f.substr(9)));
     else if (f.rfind("--warmup=", 0) == 0) warmup = std::max(0, std::stoi(f.substr(9)));
     else if (f.rfind("--paradigm=", 0) == 0) paradigm = f.substr(11);
@@ -341,6 +344,8 @@ int mode_net(int argc, char** argv) {
   opts.threads = threads;
   opts.seed = exec_seed;
   opts.paradigm = parse_paradigm(paradigm);
+  opts.bypass.optimized_addition = opt_add;
+  opts.bypass.optimized_multiply = opt_mult;
   // untimed warm-up executes, then `repeat` timed ones (bench.py --impl reference)
   std::vector<double> runs_ms;
   for (int w = 0; w < warmup; ++w) {

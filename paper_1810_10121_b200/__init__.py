@@ -203,7 +203,7 @@ class Context:
         _chk(lib().hg_kernel_timing(self._h, 1 if on else 0))
 
     def kernel_stats(self) -> dict:
-        buf = C.create_string_buffer(1 << 16)
+        buf = C.create_string_buffer(1 << 20)
         _chk(lib().hg_kernel_stats_json(self._h, buf, len(buf)))
         return json.loads(buf.value.decode())
 

@@ -78,6 +78,7 @@ void hg_context_destroy(hg_context* ctx) { delete ctx; }
 int hg_context_params(const hg_context* ctx, int64_t* n, int* bits, int cap, int* nbits, int* scale_bits,
                       int* security) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     need(ctx, "ctx");
     const auto& p = ctx->c->params();
     if (n) *n = p.n;
@@ -91,6 +92,7 @@ int hg_context_params(const hg_context* ctx, int64_t* n, int* bits, int cap, int
 
 int hg_context_primes(const hg_context* ctx, uint64_t* primes, int cap, int* count) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     need(ctx, "ctx");
     const auto& q = ctx->c->primes();
     if (count) *count = static_cast<int>(q.size());
@@ -100,6 +102,7 @@ int hg_context_primes(const hg_context* ctx, uint64_t* primes, int cap, int* cou
 
 int hg_context_relin_rows(const hg_context* ctx, int* rows) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     need(ctx, "ctx");
     *rows = ctx->c->relin_rows();
   });
@@ -107,6 +110,7 @@ int hg_context_relin_rows(const hg_context* ctx, int* rows) {
 
 int hg_context_use_private_stream(hg_context* ctx) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     need(ctx, "ctx");
     ctx->c->set_stream(nullptr, false);
   });
@@ -114,6 +118,7 @@ int hg_context_use_private_stream(hg_context* ctx) {
 
 int hg_context_set_stream(hg_context* ctx, void* s) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     need(ctx, "ctx");
     ctx->c->set_stream(static_cast<cudaStream_t>(s), true);
   });
@@ -121,11 +126,13 @@ int hg_context_set_stream(hg_context* ctx, void* s) {
 void* hg_context_stream(const hg_context* ctx) { return ctx ? ctx->stream() : nullptr; }
 
 int hg_sync(const hg_context* ctx) {
-  return guard([&] { HG_CUDA(cudaStreamSynchronize(ctx->stream())); });
+  return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1); HG_CUDA(cudaStreamSynchronize(ctx->stream())); });
 }
 
 int hg_keys_generate(hg_context* ctx, uint64_t seed, int with_relin, hg_keys** out) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     need(ctx, "ctx");
     auto* k = new hg_keys;
     try {
@@ -141,6 +148,7 @@ void hg_keys_destroy(hg_keys* keys) { delete keys; }
 
 int hg_keys_export(const hg_context* ctx, const hg_keys* keys, uint64_t* secret, uint64_t* pk, uint64_t* relin) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     need(ctx, "ctx");
     need(keys, "keys");
     const hg::Keys& K = *keys->k;
@@ -151,36 +159,44 @@ int hg_keys_export(const hg_context* ctx, const hg_keys* keys, uint64_t* secret,
 }
 
 int hg_ntt_forward(hg_context* ctx, uint64_t* dev, int64_t rows, int nl) {
-  return guard([&] { hg::k::ntt(*ctx->c, dev, rows, nl, false, ctx->stream()); });
+  return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1); hg::k::ntt(*ctx->c, dev, rows, nl, false, ctx->stream()); });
 }
 int hg_ntt_inverse(hg_context* ctx, uint64_t* dev, int64_t rows, int nl) {
-  return guard([&] { hg::k::ntt(*ctx->c, dev, rows, nl, true, ctx->stream()); });
+  return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1); hg::k::ntt(*ctx->c, dev, rows, nl, true, ctx->stream()); });
 }
 
 int hg_add(hg_context* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out, int64_t words, int nl) {
-  return guard([&] { hg::k::add(*ctx->c, a, b, out, words, nl, ctx->stream()); });
+  return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1); hg::k::add(*ctx->c, a, b, out, words, nl, ctx->stream()); });
 }
 int hg_sub(hg_context* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out, int64_t words, int nl) {
-  return guard([&] { hg::k::sub(*ctx->c, a, b, out, words, nl, ctx->stream()); });
+  return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1); hg::k::sub(*ctx->c, a, b, out, words, nl, ctx->stream()); });
 }
 int hg_negate(hg_context* ctx, const uint64_t* a, uint64_t* out, int64_t words, int nl) {
-  return guard([&] { hg::k::negate(*ctx->c, a, out, words, nl, ctx->stream()); });
+  return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1); hg::k::negate(*ctx->c, a, out, words, nl, ctx->stream()); });
 }
 int hg_add_plain(hg_context* ctx, const uint64_t* ct, const uint64_t* pt, uint64_t* out, int64_t items, int size,
                  int nl, int per_item, int subtract) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     hg::k::add_plain(*ctx->c, ct, pt, out, items, size, nl, per_item != 0, subtract != 0, ctx->stream());
   });
 }
 int hg_multiply_plain(hg_context* ctx, const uint64_t* ct, const uint64_t* pt, uint64_t* out, int64_t items, int size,
                       int nl, int per_item) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     hg::check(nl >= 2, HG_E_DEPTH, "multiplicative depth exceeded: no level left to rescale");
     hg::k::mul_plain(*ctx->c, ct, pt, out, items, size, nl, per_item != 0, ctx->stream());
   });
 }
 int hg_rescale(hg_context* ctx, const uint64_t* in, uint64_t* out, int64_t polys, int nl) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     hg::check(nl >= 2, HG_E_DEPTH, "multiplicative depth exceeded: no level left to rescale");
     auto* sc = static_cast<int64_t*>(ctx->c->scratch(static_cast<size_t>(polys * ctx->c->n() * 8), 1));
     hg::k::rescale(*ctx->c, in, out, polys, nl, sc, ctx->stream());
@@ -188,6 +204,7 @@ int hg_rescale(hg_context* ctx, const uint64_t* in, uint64_t* out, int64_t polys
 }
 int hg_mod_switch(hg_context* ctx, const uint64_t* in, uint64_t* out, int64_t polys, int nl_in, int nl_out) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     hg::check(nl_out >= 1 && nl_out <= nl_in, HG_E_VALIDATION, "modulus switch cannot raise the level");
     hg::k::mod_switch(*ctx->c, in, out, polys, nl_in, nl_out, ctx->stream());
   });
@@ -195,16 +212,19 @@ int hg_mod_switch(hg_context* ctx, const uint64_t* in, uint64_t* out, int64_t po
 int hg_multiply_relin(hg_context* ctx, const hg_keys* keys, const uint64_t* a, const uint64_t* b, uint64_t* out,
                       int64_t items, int nl) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     hg::check(nl >= 2, HG_E_DEPTH, "multiplicative depth exceeded: no level left to rescale");
     auto* c2 = static_cast<uint64_t*>(ctx->c->scratch(static_cast<size_t>(items * nl * ctx->c->n() * 8), 2));
     hg::k::mul_relin(*ctx->c, *keys->k, a, b, out, items, nl, c2, ctx->stream());
   });
 }
 int hg_multiply_tensor(hg_context* ctx, const uint64_t* a, const uint64_t* b, uint64_t* out3, int64_t items, int nl) {
-  return guard([&] { hg::k::mul_tensor(*ctx->c, a, b, out3, items, nl, ctx->stream()); });
+  return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1); hg::k::mul_tensor(*ctx->c, a, b, out3, items, nl, ctx->stream()); });
 }
 int hg_relinearize(hg_context* ctx, const hg_keys* keys, const uint64_t* in3, uint64_t* out2, int64_t items, int nl) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     auto* c2 = static_cast<uint64_t*>(ctx->c->scratch(static_cast<size_t>(items * nl * ctx->c->n() * 8), 2));
     hg::k::relin3(*ctx->c, *keys->k, in3, out2, items, nl, c2, ctx->stream());
   });
@@ -212,6 +232,7 @@ int hg_relinearize(hg_context* ctx, const hg_keys* keys, const uint64_t* in3, ui
 int hg_square_relin_rescale(hg_context* ctx, const hg_keys* keys, const uint64_t* in, uint64_t* out, int64_t items,
                             int nl) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     hg::check(nl >= 2, HG_E_DEPTH, "multiplicative depth exceeded: no level left to rescale");
     hg::Context& c = *ctx->c;
     const size_t pw = static_cast<size_t>(nl) * c.n();
@@ -225,6 +246,7 @@ int hg_square_relin_rescale(hg_context* ctx, const hg_keys* keys, const uint64_t
 int hg_weighted_sum(hg_context* ctx, const uint64_t* x, const int32_t* idx, const uint64_t* w, uint64_t* out,
                     int64_t groups, int mg, int kt, int nl) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     hg::check(nl >= 2, HG_E_DEPTH, "multiplicative depth exceeded: no level left to rescale");
     hg::Context& c = *ctx->c;
     const int64_t items = groups * mg;
@@ -239,6 +261,7 @@ int hg_weighted_sum(hg_context* ctx, const uint64_t* x, const int32_t* idx, cons
 int hg_weighted_sum_cipher(hg_context* ctx, const hg_keys* keys, const uint64_t* x, const int32_t* xidx,
                            const uint64_t* w, const int32_t* widx, uint64_t* out, int64_t groups, int kt, int nl) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     hg::check(nl >= 2, HG_E_DEPTH, "multiplicative depth exceeded: no level left to rescale");
     hg::check(groups >= 0 && kt >= 1, HG_E_VALIDATION, "weighted sum needs matching non-empty operands");
     hg::check(keys->k->has_relin, HG_E_VALIDATION, "weighted_sum_cipher needs a relinearisation key");
@@ -286,16 +309,19 @@ static void encode_batch_impl(hg_context* ctx, const double* values, int64_t col
 
 int hg_encode(hg_context* ctx, const double* values, int64_t count, int level, double scale, uint64_t* pt_dev) {
   // CkksBackend::encode (ckks_backend.hpp:182-197), encoded on the GPU
-  return guard([&] { encode_batch_impl(ctx, values, 1, count, count, 1, level, scale, pt_dev); });
+  return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1); encode_batch_impl(ctx, values, 1, count, count, 1, level, scale, pt_dev); });
 }
 
 int hg_encode_batch(hg_context* ctx, const double* values, int64_t cols, int64_t count, int64_t col_stride,
                     int64_t elem_stride, int level, double scale, uint64_t* pt_dev) {
-  return guard([&] { encode_batch_impl(ctx, values, cols, count, col_stride, elem_stride, level, scale, pt_dev); });
+  return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1); encode_batch_impl(ctx, values, cols, count, col_stride, elem_stride, level, scale, pt_dev); });
 }
 
 int hg_encode_constant(hg_context* ctx, double value, int level, double scale, uint64_t* residues) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     hg::Context& c = *ctx->c;
     level_ok(c, level);
     hg::check(scale > 0.0, HG_E_VALIDATION, "encoding scale must be positive");
@@ -309,6 +335,7 @@ int hg_encode_constant(hg_context* ctx, double value, int level, double scale, u
 int hg_encrypt(hg_context* ctx, const hg_keys* keys, const uint64_t* pt_dev, const uint64_t* seeds, int64_t items,
                int level, uint64_t* out) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     hg::Context& c = *ctx->c;
     level_ok(c, level);
     const int64_t n = c.n();
@@ -322,6 +349,7 @@ int hg_encrypt(hg_context* ctx, const hg_keys* keys, const uint64_t* pt_dev, con
 int hg_decrypt_coeffs(hg_context* ctx, const hg_keys* keys, const uint64_t* ct, int64_t items, int size, int level,
                       uint64_t* m_host) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     hg::Context& c = *ctx->c;
     level_ok(c, level);
     const size_t words = static_cast<size_t>(items) * (level + 1) * c.n();
@@ -335,6 +363,7 @@ int hg_decrypt_coeffs(hg_context* ctx, const hg_keys* keys, const uint64_t* ct, 
 int hg_decrypt(hg_context* ctx, const hg_keys* keys, const uint64_t* ct, int64_t items, int size, int level,
                double scale, int64_t count, double* values) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     hg::Context& c = *ctx->c;
     level_ok(c, level);
     const int64_t n = c.n();
@@ -352,6 +381,7 @@ extern "C" {
 
 int hg_kernel_timing(hg_context* ctx, int on) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     need(ctx, "ctx");
     ctx->c->kt_enable(on != 0);
   });
@@ -359,6 +389,7 @@ int hg_kernel_timing(hg_context* ctx, int on) {
 
 int hg_kernel_stats_json(hg_context* ctx, char* buf, size_t cap) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     need(ctx, "ctx");
     auto st = ctx->c->kt_collect();
     std::string s = "{";
@@ -367,9 +398,15 @@ int hg_kernel_stats_json(hg_context* ctx, char* buf, size_t cap) {
       if (!first) s += ",";
       first = false;
       char tmp[384];
-      snprintf(tmp, sizeof tmp, "\"%s\":{\"launches\":%lld,\"total_ms\":%.6f,\"alg_bytes\":%.0f,\"alg_modmuls\":%.0f}",
+      snprintf(tmp, sizeof tmp, "\"%s\":{\"launches\":%lld,\"total_ms\":%.6f,\"alg_bytes\":%.0f,\"alg_modmuls\":%.0f,",
                name.c_str(), static_cast<long long>(v.launches), v.ms, v.bytes, v.modmuls);
       s += tmp;
+      s += "\"first\":[";
+      for (size_t i = 0; i < v.first.size(); ++i) {
+        snprintf(tmp, sizeof tmp, "%s[%.6f,%.0f,%.0f]", i ? "," : "", v.first[i][0], v.first[i][1], v.first[i][2]);
+        s += tmp;
+      }
+      s += "]}";
     }
     s += "}";
     hg::check(s.size() + 1 <= cap, HG_E_VALIDATION, "stats buffer too small");
@@ -379,6 +416,7 @@ int hg_kernel_stats_json(hg_context* ctx, char* buf, size_t cap) {
 
 int hg_bench_modmul(hg_context* ctx, int wide, double* modmul_per_s) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     need(ctx, "ctx");
     *modmul_per_s = hg::k::modmul_peak(*ctx->c, wide, ctx->stream());
   });
@@ -392,6 +430,7 @@ extern "C" {
 // fresh-encryption samples (u, e0, e1) as signed int64 [items][3][N] on the device (GPU sampler)
 int hg_sample_encryption(hg_context* ctx, const uint64_t* seeds, int64_t items, int64_t* out_dev) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     need(ctx, "ctx");
     hg::k::sample_encryption_gpu(*ctx->c, seeds, items, out_dev, ctx->stream());
   });
@@ -399,6 +438,7 @@ int hg_sample_encryption(hg_context* ctx, const uint64_t* seeds, int64_t items, 
 // the host reference sampler (same streams), for parity tests
 int hg_sample_encryption_host(hg_context* ctx, const uint64_t* seeds, int64_t items, int64_t* out_host) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     need(ctx, "ctx");
     const int64_t n = ctx->c->n();
     for (int64_t it = 0; it < items; ++it)
@@ -410,6 +450,7 @@ int hg_sample_encryption_host(hg_context* ctx, const uint64_t* seeds, int64_t it
 // decode one NTT-form plaintext (CkksBackend::decode, ckks_backend.hpp:218-221)
 int hg_decode(hg_context* ctx, const uint64_t* pt_dev, int level, double scale, int64_t count, double* values) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     hg::Context& c = *ctx->c;
     level_ok(c, level);
     const int64_t n = c.n(), words = (int64_t)(level + 1) * n;
@@ -426,6 +467,7 @@ int hg_decode(hg_context* ctx, const uint64_t* pt_dev, int level, double scale, 
 // fill a device plaintext with encode_constant residues (the same word in every slot, NTT form)
 int hg_fill_constant(hg_context* ctx, const uint64_t* residues, int level, uint64_t* pt_dev) {
   return guard([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     hg::Context& c = *ctx->c;
     level_ok(c, level);
     const int64_t n = c.n();

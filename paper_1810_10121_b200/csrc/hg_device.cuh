@@ -3,8 +3,10 @@
 // Storage is one uint64 word per residue (the reference's word size,
 // ring.hpp:42) so HEGC-layout buffers move to/from HBM unchanged.  Limbs whose
 // prime is below 2^31 ("small": the 26/30-bit rescale primes of every BASELINE
-// config) run 32-bit Shoup/IMAD arithmetic on the low word; wider primes
-// (36/40/50-bit) use 64-bit Shoup with __umul64hi.  Every value leaving a
+// config) run 32-bit Shoup/IMAD arithmetic on the low word; 36-50-bit primes
+// run on the fp64 lane (exact FMA-residual modmul on integers held in doubles,
+// mulmod_f64); primes of 2^50 and above use 64-bit Shoup with __umul64hi
+// (HG_FP64_LANE=0 sends the 36-50-bit ones there too).  Every value leaving a
 // kernel is canonical in [0, q), so results are
 // bit-identical to the reference regardless of internal lazy ranges.
 #pragma once

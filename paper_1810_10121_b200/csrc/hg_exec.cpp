@@ -384,6 +384,109 @@ HTensor eval_node(const GNode& n, const std::vector<const HTensor*>& in, int64_t
         }
       return out;
     }
+    case Op::Convolution: {  // eval_convolution (eval.hpp:76-96), same summation order
+      const auto& x = *in[0];
+      const auto& w = *in[1];
+      if (x.shape.size() != 4 || w.shape.size() != 4)
+        fail(HG_EVALIDATION, "node '" + n.id + "' convolution folding needs 4-d operands");
+      const int64_t stride = attr_i64(n, "stride");
+      const int64_t nb = x.shape[0], ch = x.shape[1], h = x.shape[2], wd = x.shape[3];
+      const int64_t f = w.shape[0], kh = w.shape[2], kw = w.shape[3], oh = out.shape[2], ow = out.shape[3];
+      for (int64_t b = 0; b < nb; ++b)
+        for (int64_t fi = 0; fi < f; ++fi)
+          for (int64_t y = 0; y < oh; ++y)
+            for (int64_t xo = 0; xo < ow; ++xo) {
+              double acc = 0.0;
+              for (int64_t c = 0; c < ch; ++c)
+                for (int64_t dy = 0; dy < kh; ++dy)
+                  for (int64_t dx = 0; dx < kw; ++dx)
+                    acc += x.v[((b * ch + c) * h + y * stride + dy) * wd + xo * stride + dx] *
+                           w.v[((fi * ch + c) * kh + dy) * kw + dx];
+              out.v[((b * f + fi) * oh + y) * ow + xo] = acc;
+            }
+      return out;
+    }
+    case Op::AvgPool:
+    case Op::ScaledMeanPool: {  // eval_pool (eval.hpp:98-116); AvgPool scales by 1/(w1 w2)
+      const auto& x = *in[0];
+      if (x.shape.size() != 4) fail(HG_EVALIDATION, "node '" + n.id + "' pool folding needs a 4-d operand");
+      const auto win = attr_ints(n, "window");
+      const int64_t stride = attr_i64(n, "stride");
+      const double scale = n.op == Op::AvgPool ? 1.0 / static_cast<double>(win[0] * win[1]) : 1.0;
+      const int64_t nb = x.shape[0], ch = x.shape[1], h = x.shape[2], wd = x.shape[3];
+      const int64_t oh = out.shape[2], ow = out.shape[3];
+      for (int64_t b = 0; b < nb; ++b)
+        for (int64_t c = 0; c < ch; ++c)
+          for (int64_t y = 0; y < oh; ++y)
+            for (int64_t xo = 0; xo < ow; ++xo) {
+              double acc = 0.0;
+              for (int64_t dy = 0; dy < win[0]; ++dy)
+                for (int64_t dx = 0; dx < win[1]; ++dx)
+                  acc += x.v[((b * ch + c) * h + y * stride + dy) * wd + xo * stride + dx];
+              out.v[((b * ch + c) * oh + y) * ow + xo] = acc * scale;
+            }
+      return out;
+    }
+    case Op::BatchNormInference: {  // eval.hpp:159-180
+      const auto& x = *in[0];
+      const double eps = attr_f64(n, "epsilon");
+      const int64_t channels = x.shape[1];
+      int64_t inner = 1;
+      for (size_t a = 2; a < x.shape.size(); ++a) inner *= x.shape[a];
+      const int64_t nb = x.shape[0];
+      for (int64_t b = 0; b < nb; ++b)
+        for (int64_t c = 0; c < channels; ++c) {
+          const double g = in[1]->v[c] / std::sqrt(in[4]->v[c] + eps);
+          const double bb = in[2]->v[c] - g * in[3]->v[c];
+          for (int64_t i = 0; i < inner; ++i) {
+            const int64_t off = (b * channels + c) * inner + i;
+            out.v[off] = g * x.v[off] + bb;
+          }
+        }
+      return out;
+    }
+    case Op::Concat: {  // eval.hpp:194-207
+      const size_t axis = static_cast<size_t>(attr_i64(n, "axis"));
+      int64_t offset = 0;
+      for (const HTensor* part : in) {
+        for_each_index(part->shape, [&](const std::vector<int64_t>& idx, int64_t flat) {
+          std::vector<int64_t> dst = idx;
+          dst[axis] += offset;
+          out.v[flat_index(out.shape, dst)] = part->v[flat];
+        });
+        offset += part->shape[axis];
+      }
+      return out;
+    }
+    case Op::Reverse: {  // eval.hpp:221-232
+      auto axes = attr_ints(n, "axes");
+      for_each_index(out.shape, [&](const std::vector<int64_t>& idx, int64_t flat) {
+        std::vector<int64_t> src = idx;
+        for (int64_t a : axes) src[a] = in[0]->shape[a] - 1 - idx[a];
+        out.v[flat] = in[0]->v[flat_index(in[0]->shape, src)];
+      });
+      return out;
+    }
+    case Op::Slice: {  // eval.hpp:233-242
+      auto begin = attr_ints(n, "begin");
+      for_each_index(out.shape, [&](const std::vector<int64_t>& idx, int64_t flat) {
+        std::vector<int64_t> src = idx;
+        for (size_t a = 0; a < src.size(); ++a) src[a] += begin[a];
+        out.v[flat] = in[0]->v[flat_index(in[0]->shape, src)];
+      });
+      return out;
+    }
+    case Op::Sum: {  // eval.hpp:243-254, accumulation in input order
+      auto axes = attr_ints(n, "axes");
+      std::set<int64_t> ax(axes.begin(), axes.end());
+      for_each_index(in[0]->shape, [&](const std::vector<int64_t>& idx, int64_t flat) {
+        std::vector<int64_t> dst;
+        for (size_t a = 0; a < idx.size(); ++a)
+          if (!ax.count(static_cast<int64_t>(a))) dst.push_back(idx[a]);
+        out.v[flat_index(out.shape, dst)] += in[0]->v[flat];
+      });
+      return out;
+    }
     default:
       fail(HG_EVALIDATION, "constant folding of this op is not supported by the GPU executor");
   }
@@ -506,6 +609,12 @@ struct NodeCache {
   std::vector<uint8_t> cls;
   int64_t d_bmult = 0, d_badd = 0, d_mulpt = 0, d_neg = 0, d_add = 0;
   int64_t n_general = 0, n_pass_only = 0, n_empty = 0, n_fresh = 0;
+  // fresh encryptions of zero joining this rank's outputs (zero terms with optimized_addition off,
+  // and empty sums; runtime.hpp:553-560): one seed per fresh zero, summed into local positions
+  std::vector<uint64_t> fz_seeds;
+  std::shared_ptr<DevArr> fz_idx, fz_w, fz_oidx;
+  int64_t fz_groups = 0;
+  int fz_kt = 0;
   // tensor-core GEMM: byte-split weights packed per residue width class
   struct TcClass {
     int bytes = 0;
@@ -593,6 +702,9 @@ struct hg_plan {
   int64_t sampler_reruns = 0;  // runs redone with host sampler fix-ups (diagnostic, cumulative)
   bool in_run = false, sync_sampling = false;
   std::map<std::string, hg::Val>* live = nullptr;  // the running step's values (in-process group transport)
+  // per-node timing events, created once and reused by every run (ev_used: taken this run)
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
 };
 
 namespace hg {
@@ -1065,10 +1177,9 @@ Val contraction(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_s
   P->prof.mul_pt += C.d_mulpt;
   P->prof.negate += C.d_neg;
   P->prof.add += C.d_add;
-  check(C.n_fresh == 0, HG_EVALIDATION,
-        "node '" + node.id + "': fresh-zero terms (optimized_addition off) are not supported on the GPU path");
-  check(C.n_empty == 0, HG_EVALIDATION, "node '" + node.id + "': outputs whose every term is skipped are not supported");
-  check(C.n_general == 0 || C.n_pass_only == 0, HG_EVALIDATION,
+  // outputs without a general term stay at the input level (no rescale, runtime.hpp:557-568); with
+  // general outputs elsewhere in the node the reference returns a mixed-level tensor
+  check(C.n_general == 0 || C.n_pass_only + C.n_empty == 0, HG_EVALIDATION,
         "node '" + node.id + "': mixing rescaled and pass-through-only outputs yields mixed levels (unsupported)");
   const bool rescale = C.n_general > 0;
   if (rescale) require_mul_headroom(level);
@@ -1147,6 +1258,60 @@ Val contraction(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_s
       for (auto& o : oi) o = static_cast<int32_t>(std::lower_bound(mine.begin(), mine.end(), o) - mine.begin());
       C.shard = map;
     }
+    // fresh zeros of this rank's outputs, in term order per output (plan.zeros, then the empty
+    // sum's single draw): seeds node_rng.fork(e).next()... (runtime.hpp:553-560, 1123)
+    C.fz_seeds.clear();
+    C.fz_groups = 0;
+    C.fz_kt = 0;
+    if (C.n_fresh > 0 || C.n_empty > 0) {
+      const Rng node_rng = P->rng.fork("node").fork(node.id);
+      std::vector<std::vector<int32_t>> lists;
+      std::vector<int32_t> pos;
+      for (int64_t gl = 0; gl < lg; ++gl)
+        for (int ml = 0; ml < lmg; ++ml) {
+          const int64_t g = part.g0 + gl;
+          const int m = static_cast<int>(part.m0) + ml;
+          int64_t oe;
+          out_index(g, m, oe);
+          Rng er = node_rng.fork(static_cast<uint64_t>(oe));
+          std::vector<int32_t> mine;
+          bool any = false;
+          for (int t = 0; t < kt; ++t) {
+            int64_t we;
+            w_index(g, m, t, we);
+            if (cls[we] != 3) any = true;
+            if (cls[we] == 3 && !P->opt_add) {
+              mine.push_back(static_cast<int32_t>(C.fz_seeds.size()));
+              C.fz_seeds.push_back(er.next());
+            }
+          }
+          if (!any && mine.empty()) {  // every term skipped: the empty sum is a fresh zero
+            mine.push_back(static_cast<int32_t>(C.fz_seeds.size()));
+            C.fz_seeds.push_back(er.next());
+          }
+          if (mine.empty()) continue;
+          C.fz_kt = std::max<int>(C.fz_kt, static_cast<int>(mine.size()));
+          lists.push_back(std::move(mine));
+          pos.push_back(oi[gl * lmg + ml]);
+        }
+      // a unit-weight sum per output over its fresh zeros (padding terms have weight 0)
+      const int onl = (C.n_general > 0 ? level : level + 1);
+      C.fz_groups = static_cast<int64_t>(lists.size());
+      std::vector<int32_t> fi(static_cast<size_t>(C.fz_groups * C.fz_kt), 0);
+      std::vector<uint64_t> fw(static_cast<size_t>(C.fz_groups * C.fz_kt * onl), 0);
+      for (int64_t g = 0; g < C.fz_groups; ++g)
+        for (size_t t = 0; t < lists[g].size(); ++t) {
+          fi[g * C.fz_kt + t] = lists[g][t];
+          for (int j = 0; j < onl; ++j) fw[(g * C.fz_kt + t) * onl + j] = 1;
+        }
+      C.fz_idx = std::make_shared<DevArr>(fi.size() * 4, S(P));
+      C.fz_w = std::make_shared<DevArr>(fw.size() * 8, S(P));
+      C.fz_oidx = std::make_shared<DevArr>(pos.size() * 4, S(P));
+      HG_CUDA(cudaMemcpyAsync(C.fz_idx->p, fi.data(), fi.size() * 4, cudaMemcpyHostToDevice, S(P)));
+      HG_CUDA(cudaMemcpyAsync(C.fz_w->p, fw.data(), fw.size() * 8, cudaMemcpyHostToDevice, S(P)));
+      HG_CUDA(cudaMemcpyAsync(C.fz_oidx->p, pos.data(), pos.size() * 4, cudaMemcpyHostToDevice, S(P)));
+      HG_CUDA(cudaStreamSynchronize(S(P)));
+    }
     C.w = std::make_shared<DevArr>(wres.size() * 8, S(P));
     C.idx = std::make_shared<DevArr>(xi.size() * 4, S(P));
     C.oidx = std::make_shared<DevArr>(oi.size() * 4, S(P));
@@ -1154,7 +1319,7 @@ Val contraction(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_s
     HG_CUDA(cudaMemcpyAsync(C.idx->p, xi.data(), xi.size() * 4, cudaMemcpyHostToDevice, S(P)));
     HG_CUDA(cudaMemcpyAsync(C.oidx->p, oi.data(), oi.size() * 4, cudaMemcpyHostToDevice, S(P)));
     C.tc.clear();
-    if (tc_enabled() && lmg >= tc_min_outputs() && kt >= tc_min_terms() && k2::gemm_tc_supported(c, lmg, kt)) {
+    if (tc_enabled() && lmg >= tc_min_outputs() && kt >= tc_min_terms() && k2::gemm_tc_supported(c, lmg, kt, nl)) {
       std::map<int, std::vector<int>> by_bytes;
       for (int j = 0; j < nl; ++j) by_bytes[k2::tc_bytes(c, j)].push_back(j);
       for (auto& [bytes, limbs] : by_bytes) {
@@ -1200,6 +1365,22 @@ Val contraction(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_s
     const double ws = static_cast<double>(c.primes()[level]);
     res = C.local_count > 0 ? rescale_t(P, acc) : new_ct(P, 0, level - 1, xt->scale);
     res->scale = xt->scale * ws / ws;
+  }
+  if (C.fz_groups > 0) {
+    // fresh encryptions of zero at the output level (the level-l encryption dropped to l-1 is
+    // the level-(l-1) encryption limb for limb), summed per output and added after the rescale
+    const int onl = res->nl();
+    DevArr z(static_cast<size_t>(C.fz_seeds.size()) * res->item_words() * 8, S(P));
+    encrypt_items(P, C.fz_seeds, nullptr, res->level, z.as<uint64_t>());
+    auto zs = new_ct(P, res->count, res->level, res->scale);
+    HG_CUDA(cudaMemsetAsync(zs->p, 0, static_cast<size_t>(zs->words()) * 8, S(P)));
+    k::gemm_groups(c, z.as<uint64_t>(), static_cast<int64_t>(C.fz_seeds.size()), C.fz_idx->as<int32_t>(),
+                   C.fz_w->as<uint64_t>(), static_cast<int64_t>(C.fz_kt) * onl, C.fz_oidx->as<int32_t>(), zs->p,
+                   C.fz_groups, 1, C.fz_kt, onl, S(P));
+    auto sum = new_ct(P, res->count, res->level, res->scale);
+    k::add(c, res->p, zs->p, sum->p, res->words(), onl, S(P));
+    P->launches += 4;
+    res = sum;
   }
   if (sharded) {
     // place this rank's (sorted, compact) outputs at their element positions
@@ -2239,7 +2420,17 @@ struct RunState {
   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> timing;
 };
 
+cudaEvent_t pool_event(hg_plan* P) {
+  if (P->ev_used == P->ev_pool.size()) {
+    cudaEvent_t e;
+    HG_CUDA(cudaEventCreate(&e));
+    P->ev_pool.push_back(e);
+  }
+  return P->ev_pool[P->ev_used++];
+}
+
 void run_begin(hg_plan* P, RunState& st) {
+  P->ev_used = 0;  // a failed run's events are simply reused
   P->prof = Profile{};
   P->launches = 0;
   P->outputs.clear();
@@ -2253,9 +2444,7 @@ void run_begin(hg_plan* P, RunState& st) {
 
 void run_node(hg_plan* P, RunState& st, const std::string& id) {
   const GNode& node = P->g.nodes.at(id);
-  cudaEvent_t e0, e1;
-  HG_CUDA(cudaEventCreate(&e0));
-  HG_CUDA(cudaEventCreate(&e1));
+  cudaEvent_t e0 = pool_event(P), e1 = pool_event(P);
   HG_CUDA(cudaEventRecord(e0, S(P)));
   const auto h0 = std::chrono::steady_clock::now();
   Val v;
@@ -2310,8 +2499,6 @@ void run_end(hg_plan* P, RunState& st) {
     HG_CUDA(cudaEventElapsedTime(&ms, ev.first, ev.second));
     P->prof.wall_ms[id] += ms;
     P->prof.total_wall_ms += ms;
-    cudaEventDestroy(ev.first);
-    cudaEventDestroy(ev.second);
   }
   st.timing.clear();
   P->live = nullptr;
@@ -2513,6 +2700,7 @@ int hg_plan_set_options(hg_plan* P, const char* options_json) {
   // ExecOptions (runtime.hpp:158-166): {"paradigm": "encrypted-data" | "encrypted-model" |
   // "encrypted-both", "bypass": {"optimized_multiply": b, "optimized_addition": b, "epsilon": x}}
   return guard_x([&] {
+    hg::DeviceGuard dg_(P ? P->ctx->device() : -1);
     hg::check(P && options_json, HG_E_VALIDATION, "null argument");
     const auto j = hg::json::parse(options_json);
     if (j.contains("paradigm")) {
@@ -2547,12 +2735,14 @@ void hg_plan_destroy(hg_plan* plan) {
   }
   if (plan->copy_done) cudaEventDestroy(plan->copy_done);
   if (plan->sample_flags) cudaFreeHost(plan->sample_flags);
+  for (cudaEvent_t e : plan->ev_pool) cudaEventDestroy(e);
   delete plan;
 }
 
 int hg_plan_bind_input(hg_plan* P, const char* param_id, const double* values, int64_t count) {
   // bind_parameter + pack_cipher (runtime.hpp:345-368, packing.hpp:85-102)
   return guard_x([&] {
+    hg::DeviceGuard dg_(P ? P->ctx->device() : -1);
     hg::check(P && param_id, HG_E_VALIDATION, "null argument");
     auto it = P->g.nodes.find(param_id);
     hg::check(it != P->g.nodes.end() && it->second.op == hg::Op::Parameter, HG_E_VALIDATION,
@@ -2639,6 +2829,7 @@ int hg_plan_bind_input(hg_plan* P, const char* param_id, const double* values, i
 
 int hg_plan_input_info(hg_plan* P, const char* param_id, int64_t* elements, int* level) {
   return guard_x([&] {
+    hg::DeviceGuard dg_(P ? P->ctx->device() : -1);
     auto it = P->g.nodes.find(param_id);
     hg::check(it != P->g.nodes.end() && it->second.op == hg::Op::Parameter, HG_E_VALIDATION, "no such parameter");
     auto shape = hg::attr_ints(it->second, "shape");
@@ -2649,6 +2840,7 @@ int hg_plan_input_info(hg_plan* P, const char* param_id, int64_t* elements, int*
 
 int hg_plan_set_input_ciphertexts(hg_plan* P, const char* param_id, const uint64_t* src, int src_is_device) {
   return guard_x([&] {
+    hg::DeviceGuard dg_(P ? P->ctx->device() : -1);
     auto it = P->g.nodes.find(param_id);
     hg::check(it != P->g.nodes.end() && it->second.op == hg::Op::Parameter, HG_E_VALIDATION, "no such parameter");
     auto shape = hg::attr_ints(it->second, "shape");
@@ -2670,7 +2862,8 @@ int hg_plan_set_input_ciphertexts(hg_plan* P, const char* param_id, const uint64
 }
 
 int hg_plan_run(hg_plan* P) {
-  return guard_x([&] { hg::run_plan(P); });
+  return guard_x([&] {
+    hg::DeviceGuard dg_(P ? P->ctx->device() : -1); hg::run_plan(P); });
 }
 
 int hg_comm_unique_id(void* id_out) {
@@ -2684,6 +2877,7 @@ int hg_comm_unique_id(void* id_out) {
 
 int hg_plan_set_comm(hg_plan* P, int rank, int world, const void* id) {
   return guard_x([&] {
+    hg::DeviceGuard dg_(P ? P->ctx->device() : -1);
     hg::check(P && world >= 1 && rank >= 0 && rank < world, HG_E_VALIDATION, "invalid rank/world");
     P->cache.clear();  // contraction blocks depend on the partition
     P->rank = rank;
@@ -2751,6 +2945,7 @@ int hg_shard_partition(int64_t groups, int64_t mg, int world, int rank, int64_t*
 
 int hg_plan_output_info(hg_plan* P, const char* id, int64_t* elements, int* level, double* scale) {
   return guard_x([&] {
+    hg::DeviceGuard dg_(P ? P->ctx->device() : -1);
     auto it = P->outputs.find(id);
     hg::check(it != P->outputs.end(), HG_E_VALIDATION, std::string("no output '") + id + "' (run the plan first)");
     const hg::Val& v = it->second;
@@ -2763,6 +2958,7 @@ int hg_plan_output_info(hg_plan* P, const char* id, int64_t* elements, int* leve
 
 int hg_plan_output_ciphertexts(hg_plan* P, const char* id, uint64_t* dst, int dst_is_device) {
   return guard_x([&] {
+    hg::DeviceGuard dg_(P ? P->ctx->device() : -1);
     auto it = P->outputs.find(id);
     hg::check(it != P->outputs.end() && it->second.is_cipher(), HG_E_VALIDATION, "no ciphertext output");
     const auto& ct = it->second.ct;
@@ -2775,6 +2971,7 @@ int hg_plan_output_ciphertexts(hg_plan* P, const char* id, uint64_t* dst, int ds
 int hg_plan_output(hg_plan* P, const char* id, double* values, int64_t capacity, int64_t* count) {
   // value_to_tensor (runtime.hpp:1942-1957): decrypt each element, scatter b*m + e
   return guard_x([&] {
+    hg::DeviceGuard dg_(P ? P->ctx->device() : -1);
     auto it = P->outputs.find(id);
     hg::check(it != P->outputs.end(), HG_E_VALIDATION, std::string("no output '") + id + "' (run the plan first)");
     const hg::Val& v = it->second;
@@ -2858,6 +3055,7 @@ struct hg_output {
 
 int hg_plan_output_async(hg_plan* P, const char* id, hg_output** out) {
   return guard_x([&] {
+    hg::DeviceGuard dg_(P ? P->ctx->device() : -1);
     hg::check(out != nullptr, HG_E_VALIDATION, "null argument");
     *out = nullptr;
     auto it = P->outputs.find(id);
@@ -2934,6 +3132,7 @@ int hg_output_wait(hg_output* t, double* values, int64_t capacity, int64_t* coun
 
 int hg_plan_profile_json(hg_plan* P, char* buf, size_t cap) {
   return guard_x([&] {
+    hg::DeviceGuard dg_(P ? P->ctx->device() : -1);
     nlohmann::json wall = nlohmann::json::object(), host = nlohmann::json::object();
     for (const auto& [id, ms] : P->prof.wall_ms) wall[id] = ms;
     for (const auto& [id, ms] : P->prof.host_ms) host[id] = ms;

@@ -8,8 +8,12 @@
 //   sum_k W X = sum_s 2^8s D_s,   D_s = sum_{a+b=s} sum_k w_a[m][k] x_b[k][col]
 // Each D_s is an exact u8 x u8 -> s32 tensor-core GEMM (K <= 4096 keeps it
 // below 2^31), accumulated in TMEM by tcgen05.mma.kind::i8; the epilogue
-// recombines the shift groups in 128-bit integers and reduces mod q_j, so the
-// result is the exact canonical residue (bit-identical to the reference).
+// recombines the shift groups and reduces mod q_j, so the result is the exact
+// canonical residue (bit-identical to the reference):
+//   q < 2^30: sum_s D_s (2^8s mod q) < 7 * 2^31 * 2^30 < 2^64, then one 64-bit Barrett step;
+//   2^30 <= q < 2^55: Horner acc = red(acc 2^8 + D_s), highest group first; acc < q and
+//   D_s < 2^31 keep (acc << 8) + D_s < 2^63 + 2^31 < 2^64.  Wider primes use the IMAD GEMM
+//   (gemm_tc_supported).
 //
 // MMA orientation: M = 128 ciphertext coefficients (columns), N = output
 // neurons/filters (N_TILE), K = 32 terms per step.  A = X bytes, MN-major
@@ -379,7 +383,7 @@ __global__ void __launch_bounds__(kTcThreadsWS, 1)
             res = red64(acc64);
           } else {
             // Horner over the shift groups, highest first: acc = acc 2^8 + D_s (mod q); acc < q
-            // < 2^50 and D_s < 2^31 keep every step below 2^59
+            // < 2^55 (gemm_tc_supported) and D_s < 2^31 keep every step below 2^64
             uint64_t acc = 0;
 #pragma unroll
             for (int sg = Cf::S - 1; sg >= 0; --sg) acc = red64((acc << 8) + d[sg][e]);
@@ -467,8 +471,17 @@ static void launch_tc(const Context& c, const uint64_t* x, int64_t x_items, cons
   HG_CUDA(cudaGetLastError());
 }
 
-bool gemm_tc_supported(const Context& c, int mg, int kt) {
-  return c.n() % kTcM == 0 && kt <= 4096 && mg >= 1;
+// The kernel instantiates 4..7-byte residues; the wide-limb Horner step (acc << 8) + D_s stays
+// below 2^64 only while q < 2^55 (acc < q, D_s < 2^31).  Other widths (<= 24-bit or >= 55-bit
+// primes, which the reference accepts, ring.hpp:171-196) run on the IMAD GEMM.
+bool gemm_tc_supported(const Context& c, int mg, int kt, int nl) {
+  if (c.n() % kTcM != 0 || kt > 4096 || mg < 1) return false;
+  for (int j = 0; j < nl; ++j) {
+    const uint64_t q = c.primes()[j];
+    const int b = limb_bytes(q);
+    if (b < 4 || b > 7 || q >= (1ull << 55)) return false;
+  }
+  return true;
 }
 
 int tc_bytes(const Context& c, int limb) { return limb_bytes(c.primes()[limb]); }

@@ -738,6 +738,7 @@ std::map<std::string, Context::KtStat> Context::kt_collect() const {
     slot.ms += ms;
     slot.bytes += r.bytes;
     slot.modmuls += r.modmuls;
+    if (slot.first.size() < 16) slot.first.push_back({static_cast<double>(ms), r.bytes, r.modmuls});
     m_kt_pool.push_back(r.a);
     m_kt_pool.push_back(r.b);
   }

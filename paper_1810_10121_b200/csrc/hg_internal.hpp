@@ -7,6 +7,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <array>
+
 #include <cstdint>
 #include <map>
 #include <memory>
@@ -16,6 +18,25 @@
 #include <vector>
 
 #include "hg_device.cuh"
+
+namespace hg {
+// Makes `device` current for the scope of one C-ABI call (lazily created streams, events and
+// launches must target the context's GPU in a process holding contexts on several GPUs) and
+// restores the caller's device; -1 = no-op.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int device) {
+    if (device < 0) return;
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != device && cudaSetDevice(device) == cudaSuccess) prev = cur;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+}  // namespace hg
 
 namespace hg {
 
@@ -197,6 +218,9 @@ class Context {
   struct KtStat {
     int64_t launches = 0;
     double ms = 0.0, bytes = 0.0, modmuls = 0.0;
+    // the first launches one by one (ms, algorithmic bytes, modmuls): a kernel launched at several
+    // sizes per step (e.g. the key switch of act1 and act2) is compared per launch with ncu
+    std::vector<std::array<double, 3>> first;
   };
   // per kernel name; synchronises and clears the records
   std::map<std::string, KtStat> kt_collect() const;
@@ -384,7 +408,7 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
 // tcgen05 byte-split GEMM (hg_gemm_tc.cu).  Limbs are processed per residue
 // width (bytes = ceil(bits(q)/8)); weights pre-packed by pack_weights_tc for
 // exactly `limbs` (wres = [wgroups][mg][kt][nl] residues).
-bool gemm_tc_supported(const Context& c, int mg, int kt);
+bool gemm_tc_supported(const Context& c, int mg, int kt, int nl);
 int tc_bytes(const Context& c, int limb);
 int tc_ntile(int bytes, int mg);
 void pack_weights_tc(const std::vector<uint64_t>& wres, int64_t wgroups, int mg, int kt, int nl,

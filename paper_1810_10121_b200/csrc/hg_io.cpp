@@ -139,6 +139,7 @@ extern "C" {
 
 int hg_keys_save(const hg_context* ctx, const hg_keys* keys, const char* path) {
   return hg::guard_io([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     hg::check(ctx && keys && path, HG_E_VALIDATION, "null argument");
     const hg::Context& c = *ctx->c;
     const hg::Keys& K = *keys->k;
@@ -251,6 +252,7 @@ int hg_keys_load(const char* path, int device, hg_context** ctx_out, hg_keys** k
 int hg_ciphertext_save(hg_context* ctx, const uint64_t* ct_dev, int size, int level, double scale,
                        const char* path) {
   return hg::guard_io([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     hg::check(ctx && ct_dev && path, HG_E_VALIDATION, "null argument");
     const hg::Context& c = *ctx->c;
     hg::check(level >= 0 && level <= c.max_level(), HG_E_VALIDATION, "level outside the modulus chain");
@@ -275,6 +277,7 @@ int hg_ciphertext_save(hg_context* ctx, const uint64_t* ct_dev, int size, int le
 int hg_ciphertext_load(hg_context* ctx, const char* path, uint64_t* ct_dev, int64_t capacity_words, int* size,
                        int* level, double* scale) {
   return hg::guard_io([&] {
+    hg::DeviceGuard dg_(ctx ? ctx->c->device() : -1);
     hg::check(ctx && path, HG_E_VALIDATION, "null argument");
     const hg::Context& c = *ctx->c;
     const std::string what = path;

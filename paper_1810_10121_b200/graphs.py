@@ -203,6 +203,31 @@ def config4(seed: int, batch: int):
     return g.json(["logits"]), x
 
 
+def config4_small(seed: int, batch: int):
+    """Config 4's layer chain and context (N=16384, {50, 30x7, 50}, L=8: conv K=27 and K=144, x^2
+    relinearisations at levels 7 and 4, AvgPool at 6 and 3, Dense at 2) on 3x8x8 images, so the
+    reference finishes in about a minute on the host; same weights draw as config 4 with the
+    Dense fan-in 32*2*2 = 128."""
+    wr = Rng(seed).fork("config4")
+    g = G("config4_convnet_8x8")
+    g.param("x", [1, 3, 8, 8])
+    g.op("pad1", "Pad", ["x"], pad_below=[0, 0, 1, 1], pad_above=[0, 0, 1, 1])
+    g.const("w1", gaussian_tensor(wr.fork("w1"), (16, 3, 3, 3), 1.0 / 27))
+    g.op("conv1", "Convolution", ["pad1", "w1"], stride=1)
+    g.op("act1", "PolyAct", ["conv1"], a=1.0, b=0.0, c=0.0)
+    g.op("pool1", "AvgPool", ["act1"], window=[2, 2], stride=2)
+    g.op("pad2", "Pad", ["pool1"], pad_below=[0, 0, 1, 1], pad_above=[0, 0, 1, 1])
+    g.const("w2", gaussian_tensor(wr.fork("w2"), (32, 16, 3, 3), 1.0 / 144))
+    g.op("conv2", "Convolution", ["pad2", "w2"], stride=1)
+    g.op("act2", "PolyAct", ["conv2"], a=1.0, b=0.0, c=0.0)
+    g.op("pool2", "AvgPool", ["act2"], window=[2, 2], stride=2)
+    g.op("flat", "Reshape", ["pool2"], shape=[-1, 128])
+    g.const("w3", gaussian_tensor(wr.fork("w3"), (128, 10), 1.0 / 128))
+    g.op("logits", "Dot", ["flat", "w3"])
+    x = uniform_tensor(Rng(seed).fork("inputs").fork("x"), (batch, 3, 8, 8), 0.0, 1.0)
+    return g.json(["logits"]), x
+
+
 def config5(seed: int, batch: int):
     wr = Rng(seed).fork("config5")
     g = G("config5_mlp")
@@ -296,7 +321,71 @@ def ops2(seed: int, batch: int):
     return g.json(["fc", "cat"]), x
 
 
-CONFIGS = {"c1": config1, "c3": config3, "c4": config4, "c5": config5}
+def wide(seed: int, batch: int):
+    """Prime-width coverage graph (test-only): a 96-term Dot (the tensor-core GEMM's K >= 64
+    range), x^2 and a small Dot, run in contexts whose primes fall outside the GEMM's 4..7-byte,
+    < 2^55 range (<= 24-bit and >= 55-bit primes: the IMAD GEMM and the 64-bit lane)."""
+    wr = Rng(seed).fork("wide")
+    g = G("wide_primes")
+    g.param("x", [1, 96])
+    g.const("w1", gaussian_tensor(wr.fork("w1"), (96, 8), 1.0 / 96))
+    g.op("fc1", "Dot", ["x", "w1"])
+    g.op("act", "PolyAct", ["fc1"], a=1.0, b=0.0, c=0.0)
+    g.const("w2", gaussian_tensor(wr.fork("w2"), (8, 4), 1.0 / 8))
+    g.op("fc2", "Dot", ["act", "w2"])
+    x = uniform_tensor(Rng(seed).fork("inputs").fork("x"), (batch, 96), -1.0, 1.0)
+    return g.json(["fc2", "fc1"]), x
+
+
+def ops3(seed: int, batch: int):
+    """Third coverage graph (test-only; N=2048): Reverse and Slice of ciphertexts; a weight built
+    by constant folding through Convolution, AvgPool, BatchNormInference, Reverse, Concat, Sum,
+    Add and Multiply (eval.hpp:127-265); a convolution whose weights hold exact 0 and +/-1 inside
+    general sums; PolyAct with general coefficients; and a Dot without general terms (one column
+    all-zero: the empty sum is a fresh zero; two pass-through-only columns), so it stays at the
+    input level (runtime.hpp:553-568).  Run with optimized_addition on and off."""
+    wr = Rng(seed).fork("ops3")
+    g = G("ops3_rearrange_fold")
+    g.param("x", [1, 2, 6, 6])
+    g.op("rev", "Reverse", ["x"], axes=[3])
+    g.op("sl", "Slice", ["rev"], begin=[0, 0, 1, 0], end=[batch, 2, 6, 5])
+    g.const("c0", gaussian_tensor(wr.fork("c0"), (1, 2, 6, 6), 0.5))
+    g.const("k", gaussian_tensor(wr.fork("k"), (2, 2, 3, 3), 0.1))
+    g.op("cf", "Convolution", ["c0", "k"], stride=1)
+    g.op("cp", "AvgPool", ["cf"], window=[2, 2], stride=2)
+    g.const("gamma", np.array([1.25, 0.5]))
+    g.const("beta", np.array([0.1, -0.2]))
+    g.const("mean", np.array([0.05, 0.0]))
+    g.const("var", np.array([1.5, 0.75]))
+    g.op("bn", "BatchNormInference", ["cp", "gamma", "beta", "mean", "var"], epsilon=1e-5)
+    g.op("bnr", "Reverse", ["bn"], axes=[1])
+    g.op("cc", "Concat", ["bn", "bnr"], axis=0)
+    g.const("s5", gaussian_tensor(wr.fork("s5"), (2, 2, 3, 2), 0.05))
+    g.op("s4", "Sum", ["s5"], axes=[2])
+    g.op("s1", "Reshape", ["s4"], shape=[2, 2, 2, 1])
+    g.op("s1b", "Concat", ["s1", "s1"], axis=3)
+    g.op("wa", "Add", ["cc", "s1b"])
+    mask = np.ones((2, 2, 2, 2))
+    pm = np.zeros((2, 2, 2, 2))
+    for i, (pos, v) in enumerate([((0, 0, 0, 1), 0.0), ((0, 1, 1, 0), 1.0), ((1, 0, 1, 1), -1.0), ((1, 1, 0, 0), 0.0)]):
+        mask[pos] = 0.0
+        pm[pos] = v
+    g.const("mask", mask)
+    g.const("pm", pm)
+    g.op("wm", "Multiply", ["wa", "mask"])
+    g.op("w1", "Add", ["wm", "pm"])
+    g.op("conv", "Convolution", ["sl", "w1"], stride=1)
+    g.op("act", "PolyAct", ["conv"], a=0.5, b=-0.25, c=0.125)
+    g.op("flat", "Reshape", ["act"], shape=[-1, 32])
+    wd = np.zeros((32, 3))
+    wd[3, 1], wd[17, 1], wd[30, 2] = 1.0, -1.0, 1.0
+    g.const("wd", wd)
+    g.op("fc", "Dot", ["flat", "wd"])
+    x = uniform_tensor(Rng(seed).fork("inputs").fork("x"), (batch, 2, 6, 6), -1.0, 1.0)
+    return g.json(["fc", "act"]), x
+
+
+CONFIGS = {"c1": config1, "c3": config3, "c4": config4, "c4s": config4_small, "c5": config5}
 MINI_CONTEXT = {"n": 2048, "bits": [45, 30, 30, 30, 30, 45], "scale_bits": 30, "security": 0}
 
 
@@ -307,12 +396,16 @@ def key_seed(seed: int) -> int:
 def build(spec: dict):
     """spec: {"config": "c1"|"c3"|"c4"|"c5"|"mini", "batch": B, "seed": s} -> (graph, x, ctx params)."""
     cfg = spec["config"]
-    if cfg in ("mini", "ops2", "pmodel"):
-        g, x = {"mini": mini, "ops2": ops2, "pmodel": pmodel}[cfg](spec["seed"], spec["batch"])
+    if cfg in ("mini", "ops2", "ops3", "pmodel", "wide"):
+        g, x = {"mini": mini, "ops2": ops2, "ops3": ops3, "pmodel": pmodel, "wide": wide}[cfg](spec["seed"],
+                                                                                              spec["batch"])
         ctxp = dict(MINI_CONTEXT)
     else:
         g, x = CONFIGS[cfg](spec["seed"], spec["batch"])
-        ctxp = dict(CONTEXTS[cfg])
+        ctxp = dict(CONTEXTS["c4" if cfg == "c4s" else cfg])
+    for k in ("bits", "scale_bits"):  # context overrides (prime-width coverage)
+        if k in spec:
+            ctxp[k] = spec[k]
     if "n" in spec:  # reduced ring for fast parity tests (same primes bit sizes)
         ctxp["n"] = spec["n"]
         ctxp["security"] = 0
@@ -328,6 +421,11 @@ def _spec(config, batch, seed=1, **kw):
 GOLDEN_NETS = {
     "mini": _spec("mini", 16, seed=3),
     "ops2": _spec("ops2", 16, seed=4),
+    "ops3": _spec("ops3", 16, seed=8),
+    # the same graph with optimized_addition off: zero weights become fresh-zero terms
+    "ops3_na": _spec("ops3", 16, seed=8, bypass={"optimized_addition": False}),
+    # mini with both bypass shortcuts off: every term is a real product
+    "mini_nb": _spec("mini", 16, seed=3, bypass={"optimized_addition": False, "optimized_multiply": False}),
     "pmodel_m": _spec("pmodel", 16, seed=5, paradigm="encrypted-model"),
     "pmodel_b": _spec("pmodel", 16, seed=5, paradigm="encrypted-both"),
     "mini_b": _spec("mini", 16, seed=3, paradigm="encrypted-both"),
@@ -335,6 +433,15 @@ GOLDEN_NETS = {
     "c3_n2048": _spec("c3", 64, n=2048),
     "c5_n2048": _spec("c5", 64, n=2048),
     "c4_n2048": _spec("c4", 32, n=2048),
+    # config 4's full context and chain (N=16384, {50, 30x7, 50}) on 3x8x8 images
+    "c4s": _spec("c4s", 8192),
+    # primes outside the tensor-core GEMM's range: <= 24-bit and 56/60-bit limbs
+    "wide_p20": _spec("wide", 16, seed=6, bits=[24, 20, 20, 24], scale_bits=20),
+    "wide_p56": _spec("wide", 16, seed=6, bits=[56, 36, 36, 56]),
+    "wide_p60": _spec("wide", 16, seed=6, bits=[60, 40, 40, 60]),
     "c3": _spec("c3", 4096),
     "c5": _spec("c5", 8192),
+    # config 4 at full size (8192 images of 3x32x32): the reference run needs ~65 GB of RAM, so this
+    # golden is produced on a GPU-box host (HG_GOLDEN_OUT=gpurun_out make_golden.py nets c4)
+    "c4": _spec("c4", 8192),
 }

@@ -26,6 +26,9 @@ ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 
 HARNESS = os.path.join(ROOT, "oracle", "_ref", "ref_harness")
+# where the fixtures are written (HG_GOLDEN_OUT lets a GPU-box host with more RAM produce a golden
+# into gpurun_out/, e.g. the full config-4 net, whose reference run needs ~65 GB)
+OUT = os.environ.get("HG_GOLDEN_OUT", HERE)
 
 PRIM_CASES = {
     # name: (n, scale_bits, bits, key_seed)
@@ -38,6 +41,8 @@ PRIM_CASES = {
     # BASELINE config 2 (primitive sweep) shapes: 30-bit chains, L = 7 and L = 15, up to N = 2^15
     "n16384_30x8": (16384, 30, [30] * 8, 29),
     "n32768_30x16": (32768, 30, [30] * 16, 23),
+    # BASELINE config 4's context: N = 2^14, {50, 30x7, 50} (L = 8, D = 4 digits for the 50-bit limbs)
+    "n16384_50_30x7_50": (16384, 30, [50] + [30] * 7 + [50], 31),
 }
 
 
@@ -81,7 +86,7 @@ def make_prims(only=None):
             g["arrays"][k]["head"] = [int(x) for x in dump[k][:8]]
         for k in ("dec_ct1", "dec_mul_relin_rescale"):
             g["arrays"][k]["head"] = [float(x) for x in dump[k][:16]]
-        with open(os.path.join(HERE, f"prims_{name}.json"), "w") as f:
+        with open(os.path.join(OUT, f"prims_{name}.json"), "w") as f:
             json.dump(g, f, indent=1)
         print("wrote", name)
 
@@ -103,7 +108,11 @@ def make_nets(which=None):
             subprocess.check_call([HARNESS, "net", gp, xp, str(spec["batch"]), str(ctxp["n"]), str(ctxp["scale_bits"]),
                                    ",".join(map(str, ctxp["bits"])), str(ctxp["security"]), str(spec["key_seed"]),
                                    str(spec["exec_seed"]), str(spec.get("threads", os.cpu_count())), pre] +
-                                  ([f"--paradigm={spec['paradigm']}"] if "paradigm" in spec else []))
+                                  ([f"--paradigm={spec['paradigm']}"] if "paradigm" in spec else []) +
+                                  (["--no-opt-add"] if not spec.get("bypass", {}).get("optimized_addition", True)
+                                   else []) +
+                                  (["--no-opt-mult"] if not spec.get("bypass", {}).get("optimized_multiply", True)
+                                   else []))
             with open(pre + ".json") as f:
                 res = json.load(f)
             cts = np.fromfile(pre + ".ct.bin", dtype=np.uint64)
@@ -119,10 +128,10 @@ def make_nets(which=None):
                 outs[o["id"]] = {"shape": o["shape"], "elements": o["elements"], "ct_sha256": digs,
                                  "values_sha256": sha(vals), "values_head": [float(v) for v in vals[:64]],
                                  "values_absmax": float(np.abs(vals).max())}
-                np.save(os.path.join(HERE, f"net_{name}_{o['id']}_values.npy"), vals[: min(vals.size, 64 * 16)])
+                np.save(os.path.join(OUT, f"net_{name}_{o['id']}_values.npy"), vals[: min(vals.size, 64 * 16)])
             golden = {"spec": spec, "ctx": ctxp, "profile": res["profile"], "outputs": outs,
                       "ref_execute_ms": res["execute_ms"], "threads": res["threads"]}
-            with open(os.path.join(HERE, f"net_{name}.json"), "w") as f:
+            with open(os.path.join(OUT, f"net_{name}.json"), "w") as f:
                 json.dump(golden, f, indent=1)
             print("wrote net", name, "execute_ms", res["execute_ms"])
 

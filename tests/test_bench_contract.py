@@ -7,22 +7,35 @@ import bench
 
 def _stats():
     return {
-        "k_relin_t/u32": {"launches": 20, "total_ms": 21.7, "alg_bytes": 1.5e10, "alg_modmuls": 4.0e10},
+        # act1 + act2 launches per step: the first launch of a step is the larger (act1)
+        "k_relin_t/u32": {"launches": 20, "total_ms": 21.7, "alg_bytes": 1.5e10, "alg_modmuls": 4.0e10,
+                          "first": [[1.4, 1.2e9, 3.2e9], [0.77, 0.3e9, 0.8e9]]},
+        "k_relin_t/f64": {"launches": 20, "total_ms": 9.0, "alg_bytes": 3.0e9, "alg_modmuls": 8.0e9},
         "k_gemm_tc": {"launches": 40, "total_ms": 6.1, "alg_bytes": 6.6e9, "alg_modmuls": 7.0e10},
     }
 
 
-def test_roofline_picks_dominant_kernel_and_reports_fractions():
-    rl, rl_int = bench.roofline_from_stats(_stats(), {"hbm_gbs": 6550.1}, 4.1e12)
+PEAKS = {"modmul32_per_s": 4.1e12, "modmul64_per_s": 0.96e12, "modmulf64_per_s": 2.8e12}
+
+
+def test_roofline_is_the_modmul_view_of_the_dominant_kernel():
+    rl, per = bench.roofline_from_stats(_stats(), {"hbm_gbs": 6550.1}, PEAKS, 10)
     assert rl["kernel"] == "k_relin_t/u32"
     for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
         assert k in rl
-    assert rl["bound"] == "hbm" and rl["unit"] == "GB/s"
+    assert rl["bound"] == "int-modmul" and rl["unit"] == "Gmodmul/s"
     sec = 21.7e-3
-    assert abs(rl["achieved"] - 1.5e10 / sec / 1e9) < 1e-6
-    assert abs(rl["frac"] - rl["achieved"] / 6550.1) < 1e-12
-    assert rl["launches_in_region"] == 20
-    assert abs(rl_int["frac"] - (4.0e10 / sec / 1e9) / (4.1e12 / 1e9)) < 1e-12
+    assert abs(rl["achieved"] - 4.0e10 / sec / 1e9) < 1e-6
+    assert abs(rl["frac"] - (4.0e10 / sec) / 4.1e12) < 1e-12
+    assert rl["launches_in_region"] == 20 and rl["launches_per_step"] == 2
+    # traffic is compared with the algorithmic bytes of the same (first) launch
+    assert rl["alg_bytes_first_launch"] == 1.2e9
+    if rl["traffic"] is not None:
+        assert abs(rl["traffic_over_alg"] - rl["traffic"] / 1.2e9) < 1e-12
+    assert abs(rl["hbm_view"]["frac"] - (1.5e10 / sec / 1e9) / 6550.1) < 1e-12
+    # each lane against its own peak
+    assert abs(per["k_relin_t/f64"]["modmul_frac"] - (8.0e9 / 9.0e-3) / 2.8e12) < 1e-12
+    assert abs(per["k_gemm_tc"]["modmul_frac"] - (7.0e10 / 6.1e-3) / 4.1e12) < 1e-12
 
 
 def test_workload_config_names_the_workload():

@@ -13,7 +13,8 @@ from tests import golden_util as G
 
 pytestmark = pytest.mark.gpu
 
-NETS = ["mini", "ops2", "pmodel_m", "pmodel_b", "mini_b", "c1", "c3_n2048", "c5_n2048", "c4_n2048", "c3", "c5"]
+NETS = ["mini", "mini_nb", "ops2", "ops3", "ops3_na", "pmodel_m", "pmodel_b", "mini_b", "wide_p20", "wide_p56", "wide_p60", "c1", "c3_n2048",
+        "c5_n2048", "c4_n2048", "c4s", "c3", "c5", "c4"]
 
 
 def _available(name):
@@ -33,8 +34,8 @@ def test_net_bit_exact(name, cuda_ok):
     ctx = P.Context(ctxp["n"], ctxp["bits"], ctxp["scale_bits"], security=ctxp["security"])
     keys = P.Keys(ctx, spec["key_seed"])
     plan = P.Plan(ctx, keys, graph, spec["batch"], spec["exec_seed"])
-    if "paradigm" in spec:
-        plan.set_options(paradigm=spec["paradigm"])
+    if "paradigm" in spec or "bypass" in spec:
+        plan.set_options(paradigm=spec.get("paradigm"), bypass=spec.get("bypass"))
     plan.bind_input("x", x)
     plan.run()
     prof = plan.profile()
