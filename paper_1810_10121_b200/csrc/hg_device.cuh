@@ -33,6 +33,7 @@ struct LimbInfo {
   uint32_t ninv32_s;     // floor(ninv 2^32 / q) for small primes
   uint32_t small;        // q < 2^30 (32-bit lazy word path)
   uint32_t fp;           // 2^30 <= q < 2^50: fp64 lane (exact FMA-based modmul, hg_ntt.cuh Lz<double>)
+  uint32_t c32, c32s;    // small primes: 2^32 mod q and floor(c32 2^32 / q) (wide-value lifts)
   double qd, qinvd;      // q and fl(1/q)
   double ninvd;          // N^{-1} mod q
   const double* fwpd;    // pass-ordered psi^brv / psi^-brv as doubles (fp64 lane)

@@ -396,6 +396,8 @@ Context::Context(const ContextParamsH& p, int device) : m_p(p), m_device(device)
     L.ninv32_s = static_cast<uint32_t>(L.ninv_s >> 32);
     L.small = small ? 1u : 0u;
     L.fp = (!small && q < (uint64_t(1) << 50)) ? 1u : 0u;
+    L.c32 = small ? static_cast<uint32_t>((uint64_t(1) << 32) % q) : 0u;
+    L.c32s = small ? static_cast<uint32_t>((static_cast<uint64_t>(L.c32) << 32) / q) : 0u;
     L.qd = static_cast<double>(q);
     L.qinvd = 1.0 / static_cast<double>(q);
     L.ninvd = static_cast<double>(L.ninv);

@@ -82,6 +82,13 @@ __device__ __forceinline__ void l2_next(bool more, const void* p, unsigned bytes
   if (more && threadIdx.x == 0) l2_prefetch(p, bytes);
 }
 
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 #define HG_KERNEL template <typename W, int LOGN> __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_blocks)
 
 // ---------------------------------------------------------------------------
@@ -123,6 +130,20 @@ __device__ __forceinline__ W lift_cen(CT v, const LimbInfo& L, uint32_t mu32) {
     uint32_t r = av - __umulhi(av, mu32) * q;
     r = r >= q ? r - q : r;
     return (v < 0 && r != 0) ? q - r : r;
+  } else if constexpr (sizeof(CT) == 8 && sizeof(W) == 4) {
+    // |v| < 2^63, q_j < 2^30 (a wide top limb lifted into a small one): |v| = hi 2^32 + lo with
+    // hi (2^32 mod q) and lo reduced by 32-bit Shoup products into [0, 2q) each; the sum is
+    // folded to the lazy range [0, 2q) and a negative v maps to 2q - r (first-pass inputs < 4q)
+    const uint32_t q = (uint32_t)L.q, q2 = q + q;
+    const uint64_t a = v < 0 ? 0 - (uint64_t)v : (uint64_t)v;
+    const uint32_t hi = (uint32_t)(a >> 32), lo = (uint32_t)a;
+    uint32_t r = (hi * L.c32 - __umulhi(hi, L.c32s) * q) + (lo - __umulhi(lo, mu32) * q);
+    r = min(r, r - q2);
+    return v < 0 ? q2 - r : r;
+  } else if constexpr (sizeof(CT) == 8 && std::is_floating_point_v<W>) {
+    // fp64 lane: |v| < 2^51 converts exactly and reduces to a signed residue in [-q/2, q/2]
+    if (v > -(int64_t(1) << 51) && v < (int64_t(1) << 51)) return reduce_f64((double)v, L.qd, L.qinvd);
+    return (W)lift_signed((int64_t)v, L);
   } else {
     return (W)lift_signed((int64_t)v, L);
   }
@@ -267,15 +288,14 @@ __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_block
   const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
   const uint64_t Q = c.L->q, inv = R.inv[j], inv_s = R.inv_s[j];
   const uint32_t inv_s32 = R.inv_s32[j], mu32 = (uint32_t)((1ULL << 32) / Q);
-  const lz::TWT<W> psi1 = first_twiddle<W>(*c.L);
+  const lz::TWT<W> psi1 = half_twiddle<W>(first_twiddle<W>(*c.L), q, half);
   for (int r = c.r0; r < c.r1; ++r) {
     const CT* cv = cen + (int64_t)r * nfull;
     l2_next(r + 1 < c.r1, cv + nfull, nfull * sizeof(CT));
     l2_next(r + 1 < c.r1, in + ((int64_t)(r + 1) * nl + j) * nfull + (int64_t)half * n, n * 8);
     lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
-      W x0 = lift_cen<W, CT>(__ldg(cv + k), *c.L, mu32), x1 = lift_cen<W, CT>(__ldg(cv + k + n), *c.L, mu32);
-      ct_lz<W>(x0, x1, psi1, q, q2);
-      return half ? x1 : x0;
+      return ct_one<W>(lift_cen<W, CT>(__ldg(cv + k), *c.L, mu32), lift_cen<W, CT>(__ldg(cv + k + n), *c.L, mu32),
+                       psi1, q, q2);
     }, c.tw, q, q2);
     lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2);
     const uint64_t* x = in + ((int64_t)r * nl + j) * nfull + (int64_t)half * n;
@@ -297,6 +317,91 @@ __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_block
       }
     }
     __syncthreads();
+  }
+}
+
+// rescale step 2, software-pipelined (one CTA per SM, G rows each): the next row's centred
+// lift and x_j stream into shared memory with cp.async while the current row transforms, so
+// the kernel overlaps its HBM traffic with the NTT instead of stalling on the loads (the
+// unpipelined kernels are latency-bound: long_scoreboard ~6 warps per issue).
+//   cbuf: the lift row (CT; both halves when SPLIT), xbuf: this CTA's x_j evaluations (u64,
+//   16-byte chunks swizzled so a thread's 8 chunks of 16 consecutive words are conflict-free)
+// Group order per row r: [cen(r+1)] after the first pass, [x(r+1)] after the last pass; the
+// row loop waits for cen with wait_group 1 and for x right before the last pass.
+template <typename W, int LOGN, typename CT, bool SPLIT>
+struct RescalePCfg {
+  static constexpr int n = 1 << LOGN, nfull = SPLIT ? 2 * n : n;
+  static constexpr size_t c_off = Cfg<W, LOGN>::smem;
+  static constexpr size_t x_off = c_off + ((size_t)nfull * sizeof(CT) + 15) / 16 * 16;
+  static constexpr size_t smem = x_off + (size_t)n * 8;
+  static constexpr bool fits = Cfg<W, LOGN>::TWS && smem <= kSmemCap;
+};
+__device__ __forceinline__ int xslot(int c) { return c ^ ((c >> 3) & 7); }
+
+template <typename W, int LOGN, typename CT, bool SPLIT>
+__global__ void __launch_bounds__(Cfg<W, LOGN>::threads, 1)
+    k_rescale_rest_p(const uint64_t* __restrict__ in, const CT* __restrict__ cen, uint64_t* __restrict__ out,
+                     int nl, int64_t polys, int G, const LimbList LL, const RescaleC R, const CtxParams P) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  using PC = RescalePCfg<W, LOGN, CT, SPLIT>;
+  constexpr int n = PC::n, nfull = PC::nfull, T = lz::lz_threads<LOGN>();
+  const int half = SPLIT ? (int)(blockIdx.x & 1) : 0;
+  Cta<W, LOGN> c(smem, LL, polys, G, P, false, SPLIT ? (int)(blockIdx.x >> 1) : -1, SPLIT ? half : -1);
+  const int t = nl - 1, j = c.limb;
+  const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
+  const uint64_t Q = c.L->q, inv = R.inv[j], inv_s = R.inv_s[j];
+  const uint32_t inv_s32 = R.inv_s32[j], mu32 = (uint32_t)((1ULL << 32) / Q);
+  lz::TWT<W> psi1{};
+  if constexpr (SPLIT) psi1 = half_twiddle<W>(first_twiddle<W>(*c.L), q, half);
+  (void)psi1;
+  CT* cbuf = reinterpret_cast<CT*>(reinterpret_cast<uint8_t*>(smem) + PC::c_off);
+  uint4* xbuf = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(smem) + PC::x_off);
+  auto stage_c = [&](int r) {
+    const uint4* g = reinterpret_cast<const uint4*>(cen + (int64_t)r * nfull);
+    for (int ch = threadIdx.x; ch < nfull * (int)sizeof(CT) / 16; ch += T) cp_async16(reinterpret_cast<uint4*>(cbuf) + ch, g + ch);
+    cp_async_commit();
+  };
+  auto stage_x = [&](int r) {
+    const uint4* g = reinterpret_cast<const uint4*>(in + ((int64_t)r * nl + j) * nfull + (int64_t)half * n);
+    for (int ch = threadIdx.x; ch < n / 2; ch += T) cp_async16(xbuf + xslot(ch), g + ch);
+    cp_async_commit();
+  };
+  if (c.r0 < c.r1) {
+    stage_c(c.r0);
+    stage_x(c.r0);
+  }
+  for (int r = c.r0; r < c.r1; ++r) {
+    const bool more = r + 1 < c.r1;
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // cen(r) landed (x(r) may be in flight)
+    __syncthreads();
+    if constexpr (SPLIT) {
+      lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
+        return ct_one<W>(lift_cen<W, CT>(cbuf[k], *c.L, mu32), lift_cen<W, CT>(cbuf[k + n], *c.L, mu32), psi1, q, q2);
+      }, c.tw, q, q2);
+    } else {
+      lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return lift_cen<W, CT>(cbuf[k], *c.L, mu32); }, c.tw, q, q2);
+    }
+    if (more) stage_c(r + 1);  // cbuf consumed (fwd_first_from ends with a barrier)
+    lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2, [&] {
+      if (more) asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // x(r); cen(r+1) may be in flight
+      else cp_async_wait_all();
+    });
+    uint64_t* o = out + ((int64_t)r * t + j) * nfull + (int64_t)half * n;
+    for (int vt = threadIdx.x; vt < (n >> 4); vt += T) {
+      W y[16];
+      lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, y);
+      ulonglong2* o2 = reinterpret_cast<ulonglong2*>(o + (vt << 4));
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        const uint4 xc = xbuf[xslot(8 * vt + h)];
+        const uint64_t x0 = ((uint64_t)xc.y << 32) | xc.x, x1 = ((uint64_t)xc.w << 32) | xc.z;
+        const uint64_t c0 = canon4<W>(y[2 * h], q, q2), c1 = canon4<W>(y[2 * h + 1], q, q2);
+        o2[h] = make_ulonglong2(rescale_word<W>(x0, c0, Q, inv, inv_s, inv_s32),
+                                rescale_word<W>(x1, c1, Q, inv, inv_s, inv_s32));
+      }
+    }
+    __syncthreads();  // xbuf and the data buffer consumed
+    if (more) stage_x(r + 1);
   }
 }
 
@@ -577,12 +682,6 @@ __device__ __forceinline__ uint32_t neg_qinv32(uint32_t q) {
   return 0u - inv;
 }
 
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
 // the key switch of CTA `vb` (k_relin_t passes blockIdx.x)
 template <typename W, int LOGN, bool GIVEN_D, bool SPLIT, bool DIG>
@@ -643,6 +742,7 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
     if constexpr (std::is_floating_point_v<W>) psi1 = (double)c.L->fw[1].x;
     else if constexpr (sizeof(W) == 4) psi1 = c.L->fw32[1];
     else psi1 = c.L->fw[1];
+    psi1 = half_twiddle<W>(psi1, q, half);  // this half's output of the first butterfly only
   }
   (void)psi1;
   const uint32_t qneg = neg_qinv32((uint32_t)Q);
@@ -706,22 +806,15 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
           }
         } else if constexpr (DIG) {
           lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
-            const W x0 = (W)(uint32_t)ds[k];
-            W x1 = (W)(uint32_t)ds[k + n];
-            W x0b = x0;
-            ct_lz<W>(x0b, x1, psi1, q, q2);  // (x0 + psi x1, x0 - psi x1), lazy
-            return half ? x1 : x0b;
+            return ct_one<W>((W)(uint32_t)ds[k], (W)(uint32_t)ds[k + n], psi1, q, q2);  // x0 +/- psi x1
           }, c.tw, q, q2);
           // row consumed (fwd_first_from ends with a barrier): stage the next one behind this NTT
           if (row + 1 < sd) { stage_dig(item, row + 1); c2_staged = true; }
           else if (item + 1 < c.r1) { stage_dig(item + 1, 0); c2_staged = true; }
         } else if constexpr (SPLIT) {
           lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
-            const W x0 = (W)(uint32_t)((__ldg(src + k) >> sh) & 0x7FFF);
-            W x1 = (W)(uint32_t)((__ldg(src + k + n) >> sh) & 0x7FFF);
-            W x0b = x0;
-            ct_lz<W>(x0b, x1, psi1, q, q2);  // (x0 + psi x1, x0 - psi x1), lazy
-            return half ? x1 : x0b;
+            return ct_one<W>((W)(uint32_t)((__ldg(src + k) >> sh) & 0x7FFF),
+                             (W)(uint32_t)((__ldg(src + k + n) >> sh) & 0x7FFF), psi1, q, q2);  // x0 +/- psi x1
           }, c.tw, q, q2);
         } else {
           lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return (W)(uint32_t)((__ldg(src + k) >> sh) & 0x7FFF); }, c.tw, q, q2);
@@ -1360,6 +1453,15 @@ void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const i
   run(cl.wide, uint64_t{}, lf.wide());
 }
 
+// HG_RESCALE_PIPE=0: the unpipelined rest-limb kernels (A/B measurements)
+static bool rescale_pipelined() {
+  static const bool on = [] {
+    const char* e = std::getenv("HG_RESCALE_PIPE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 template <typename CT>
 static void rescale_t(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys, int nl, CT* cen,
                       const RescaleC& R, cudaStream_t s) {
@@ -1385,6 +1487,27 @@ static void rescale_t(const Context& c, const uint64_t* in, uint64_t* out, int64
     using W = decltype(wtag);
     if (LL.count == 0) return;
     by_logn<W>(c, [&]<typename W_, int LOGN>() {
+      // pipelined variant: whole rows up to 2^13, half rows at 2^14 (when it fits in shared memory)
+      constexpr bool SPL = LOGN == 14;
+      constexpr int LP = SPL ? LOGN - 1 : LOGN;
+      using PC = RescalePCfg<W_, LP, CT, SPL>;
+      if constexpr (PC::fits && LOGN <= 14) {
+        if (rescale_pipelined()) {
+          const int halves = SPL ? 2 : 1;
+          const int64_t target = 148LL * 3;
+          const int G = (int)std::max<int64_t>(1, std::min<int64_t>(64, (polys * LL.count * halves + target - 1) / target));
+          const unsigned grid = (unsigned)(LL.count * ((polys + G - 1) / G) * halves);
+          set_smem_attr((const void*)k_rescale_rest_p<W_, LP, CT, SPL>, PC::smem);
+          c.kt_begin(std::is_floating_point_v<W_> ? "k_rescale_rest_t/f64" : sizeof(W_) == 4 ? "k_rescale_rest_t/u32" : "k_rescale_rest_t/u64", s,
+                     (double)polys * LL.count * (2 * nw + (double)c.n() * sizeof(CT)),
+                     (double)polys * LL.count * (bfly(c) + c.n()));
+          k_rescale_rest_p<W_, LP, CT, SPL><<<grid, Cfg<W_, LP>::threads, PC::smem, s>>>(in, cen, out, nl, polys, G, LL,
+                                                                                    R, c.kp());
+          c.kt_end(s);
+          HG_CUDA(cudaGetLastError());
+          return;
+        }
+      }
       if constexpr (LOGN == 14 && std::is_same_v<W_, uint32_t>) {
         // two CTAs per row, one per half of the evaluations (measured: helps the 32-bit
         // lane, whose 2^14 tables crowd shared memory; the fp64 lane is faster unsplit)

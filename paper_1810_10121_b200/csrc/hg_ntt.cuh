@@ -266,6 +266,21 @@ __device__ __forceinline__ void ct_lz(W& a, W& b, typename Lz<W>::TW w, W q, W q
     b = x - t + q2;
   }
 }
+// The first forward butterfly of a split (half-row) transform keeps ONE output: half 0 takes
+// a + psi b, half 1 takes a - psi b = a + (q - psi) b.  half_twiddle gives the twiddle of that
+// output (the Shoup constant of q - w is ~floor(w 2^k / q), since q does not divide w 2^k);
+// ct_one computes it, lazily reduced like ct_lz's first output.
+template <typename W>
+__device__ __forceinline__ typename Lz<W>::TW half_twiddle(typename Lz<W>::TW w, W q, int half) {
+  if constexpr (std::is_floating_point_v<W>) return half ? q - w : w;
+  else if constexpr (sizeof(W) == 4) return half ? make_uint2((uint32_t)q - w.x, ~w.y) : w;
+  else return half ? make_ulonglong2((uint64_t)q - w.x, ~w.y) : w;
+}
+template <typename W>
+__device__ __forceinline__ W ct_one(W a, W b, typename Lz<W>::TW w, W q, W q2) {
+  if constexpr (std::is_floating_point_v<W>) return __dadd_rn(reduce_f64(a, q, q2), mulmod_f64(b, w, q, q2));
+  else return csub(a, q2) + Lz<W>::mulw(b, w, q);
+}
 template <typename W>
 __device__ __forceinline__ void gs_lz(W& a, W& b, typename Lz<W>::TW w, W q, W q2) {
   if constexpr (std::is_floating_point_v<W>) {

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_prims.py tests/test_gpu_exec.py -m gpu -q -x > gpurun_out/r2e_pytest.log 2>&1; echo pytest_rc=$?
+python bench.py --no-cpu --steps 10 > gpurun_out/r2e_bench_pipe.log 2>&1; echo bench_rc=$?
+HG_RESCALE_PIPE=0 python bench.py --no-cpu --steps 10 > gpurun_out/r2e_bench_nopipe.log 2>&1; echo bench_rc=$?
