@@ -187,7 +187,10 @@ def workload_config(args, ctxp) -> dict:
 
 
 def lane_peak(name: str, int_peaks: dict) -> float:
-    """modmul/s peak of the arithmetic lane a kernel runs in (name suffix /u32, /f64, /u64)."""
+    """modmul/s peak of the arithmetic lane a kernel runs in (name suffix /u32, /f64, /u64); the
+    tcgen05 GEMM counts u8 x u8 MACs against the i8 tensor peak."""
+    if name.startswith("k_gemm_tc"):
+        return int_peaks["u8mac_per_s"]
     if name.endswith("/f64"):
         return int_peaks["modmulf64_per_s"]
     if name.endswith("/u64"):
@@ -218,10 +221,14 @@ def roofline_from_stats(stats: dict, peaks: dict, int_peaks: dict, steps: int):
             ent = json.load(f).get(name)
         if ent:
             traffic = ent["dram_bytes_per_launch"]
-    rl = {"kernel": name, "bound": "int-modmul", "achieved": mm / 1e9, "peak": peak_mm / 1e9, "unit": "Gmodmul/s",
+    tc = name.startswith("k_gemm_tc")
+    rl = {"kernel": name, "bound": "tensor" if tc else "int-modmul", "achieved": mm / 1e9, "peak": peak_mm / 1e9,
+          "unit": "Gu8MAC/s" if tc else "Gmodmul/s",
           "frac": mm / peak_mm if peak_mm else None,
-          "peak_source": "register-only modmul microkernel of this kernel's lane on this GPU (hg_bench_modmul); "
-                         "MEASURED_PEAKS.json has no integer figure",
+          "peak_source": ("i8 dense tensor rate = 2x the measured bf16 rate (MEASURED_PEAKS.json bf16_tflops), "
+                          "in u8 MACs" if tc else
+                          "register-only modmul microkernel of this kernel's lane on this GPU (hg_bench_modmul); "
+                          "MEASURED_PEAKS.json has no integer figure"),
           "traffic": traffic,
           "traffic_unit": "DRAM bytes of the first launch per step (ncu dram__bytes_read+write, profiles/)",
           "alg_bytes_first_launch": l0_bytes,
@@ -365,7 +372,9 @@ def ours_arm(args):
 
     # ---- roofline + CPU baseline (rank 0, N=1 only for the CPU leg) ----
     int_peaks = {"modmul32_per_s": ctx.modmul_peak(0), "modmul64_per_s": ctx.modmul_peak(1),
-                 "modmulf64_per_s": ctx.modmul_peak(2)}
+                 "modmulf64_per_s": ctx.modmul_peak(2),
+                 # i8 tensor rate (2x bf16 on sm_100) in u8 MACs/s = the bf16 FLOP/s figure
+                 "u8mac_per_s": peaks.get("bf16_tflops", 1666.1) * 1e12}
     rl, per_kernel = roofline_from_stats(stats, peaks, int_peaks, args.steps)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu and os.path.exists(REF_HARNESS):

@@ -1587,12 +1587,23 @@ Val kernel_poly_act(hg_plan* P, const GNode& node, const std::vector<int64_t>& o
   if (a != 0.0) {
     require_mul_headroom(level);
     const int nl = level + 1;
-    // multiply_rescale(x, x): tensor + relin, then rescale
-    auto prod = new_ct(P, m, level, xe->scale * xe->scale);
-    DevArr c2(static_cast<size_t>(m) * nl * c.n() * 8, S(P));
-    k::square_relin(c, *P->keys, xe->p, prod->p, m, nl, c2.as<uint64_t>(), S(P));
-    P->launches += 2;
-    acc = rescale_t(P, prod);
+    // multiply_rescale(x, x): tensor + relin, then rescale, in chunks of items so the transient
+    // product / digit / lift buffers stay a few GB (c4's act1 is 16384 ciphertexts at N = 2^14:
+    // unchunked they add ~56 GB to the live tensors and the allocator stalls near the 180 GB cap)
+    const double dropped = static_cast<double>(c.primes()[level]);
+    auto o = new_ct(P, m, level - 1, xe->scale * xe->scale / dropped);
+    const int64_t item_bytes = static_cast<int64_t>(2) * nl * c.n() * 8;
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(m, (int64_t(4) << 30) / item_bytes));
+    for (int64_t b0 = 0; b0 < m; b0 += chunk) {
+      const int64_t cnt = std::min(chunk, m - b0);
+      DevArr prod(static_cast<size_t>(cnt * item_bytes), S(P));
+      DevArr c2(static_cast<size_t>(cnt) * nl * c.n() * 8, S(P));
+      DevArr sc(static_cast<size_t>(cnt) * 2 * c.n() * 8, S(P));
+      k::square_relin(c, *P->keys, xe->item(b0), prod.as<uint64_t>(), cnt, nl, c2.as<uint64_t>(), S(P));
+      k::rescale(c, prod.as<uint64_t>(), o->item(b0), cnt * 2, nl, sc.as<int64_t>(), S(P));
+      P->launches += 4;
+    }
+    acc = o;
     if (a == -1.0) acc = negate_t(acc);
     else if (a != 1.0) acc = mul_const_rescale(acc, a, static_cast<double>(c.primes()[acc->level]));
     if (b != 0.0) {

@@ -491,6 +491,8 @@ int tc_ntile(int bytes, int mg) { return mg <= 16 ? 16 : (mg <= 32 || bytes > 4)
 void gemm_tc(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* idx, const uint8_t* wpk,
              int64_t w_group_stride, const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt, int nl,
              const std::vector<int>& limbs, int bytes, cudaStream_t s) {
+  // algorithmic work of the tensor-core launch: u8 x u8 MACs (residue MACs x bytes^2), the
+  // unit the i8 tensor peak is quoted in
   const double item_bytes = 2.0 * nl * c.n() * 8;
   const double frac = (double)limbs.size() / nl;
   const double in_items = std::min<double>((double)groups * kt, (double)x_items);
@@ -499,7 +501,7 @@ void gemm_tc(const Context& c, const uint64_t* x, int64_t x_items, const int32_t
   if (bytes == B && nt == NT) {                                                                       \
     launch_tc<B, NT>(c, x, x_items, idx, wpk, w_group_stride, oidx, out, groups, mg, kt, nl, limbs, s, \
                      frac * (in_items + (double)groups * mg) * item_bytes,                            \
-                     frac * (double)groups * mg * kt * 2.0 * nl * c.n());                             \
+                     frac * (double)groups * mg * kt * 2.0 * nl * c.n() * B * B);                     \
     return;                                                                                           \
   }
   HG_TC(4, 16) HG_TC(4, 32) HG_TC(4, 64)

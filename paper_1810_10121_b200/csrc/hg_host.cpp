@@ -532,8 +532,17 @@ void finish_relin_keys(const Context& c, Keys& k) {
   for (auto& th : pool) th.join();
   keys->relin_pack.alloc(kp.size() * 8);
   HG_CUDA(cudaMemcpy(keys->relin_pack.p, kp.data(), kp.size() * 8, cudaMemcpyHostToDevice));
-  keys->relin_mont.alloc(km.size() * 4);
-  HG_CUDA(cudaMemcpy(keys->relin_mont.p, km.data(), km.size() * 4, cudaMemcpyHostToDevice));
+  // stored pre-swizzled for the key switch's shared-memory MAC: within every group of 32
+  // 16-byte chunks, chunk c sits at key_slot(c) = c ^ ((c >> 2) & 7) (hg_kernels2.cu), so
+  // contiguous (bulk) copies land each chunk in its bank-conflict-free slot
+  std::vector<uint32_t> kms(km.size());
+  for (size_t g = 0; g < km.size(); g += 128)
+    for (int ch = 0; ch < 32 && g + 4 * ch < km.size(); ++ch) {
+      const int slot = ch ^ ((ch >> 2) & 7);
+      for (int e = 0; e < 4; ++e) kms[g + 4 * slot + e] = km[g + 4 * ch + e];
+    }
+  keys->relin_mont.alloc(kms.size() * 4);
+  HG_CUDA(cudaMemcpy(keys->relin_mont.p, kms.data(), kms.size() * 4, cudaMemcpyHostToDevice));
 }
 
 std::unique_ptr<Keys> generate_keys(const Context& c, uint64_t seed, bool with_relin) {

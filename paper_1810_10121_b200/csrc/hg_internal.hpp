@@ -390,7 +390,7 @@ void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const i
 void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys, int nl, int64_t* cen, cudaStream_t s);
 void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_stride, int64_t b_stride,
               int64_t a1_off, int64_t b1_off, uint64_t* c2, int64_t items, int nl, cudaStream_t s,
-              uint64_t* d = nullptr, bool digits = false);
+              uint64_t* d = nullptr, bool digits = false, uint32_t* d32 = nullptr);
 // digits: relin_c2 writes the key switch's u16 digit rows into the c2 buffer instead of c2
 // (2 D_i bytes per residue coefficient <= 8), and relin stages them (2^13 / 2^14 half rows)
 bool relin_digits_ok(const Context& c, int nl);
@@ -403,7 +403,7 @@ void gemm(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* i
 // relin_d_in_out admits
 void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, int64_t a_stride,
            int64_t b_stride, bool given_d, const uint64_t* c2, uint64_t* out, int64_t items, int nl, cudaStream_t s,
-           bool d_in_out = false, bool digits = false);
+           bool d_in_out = false, bool digits = false, const uint32_t* d32 = nullptr);
 
 // tcgen05 byte-split GEMM (hg_gemm_tc.cu).  Limbs are processed per residue
 // width (bytes = ceil(bits(q)/8)); weights pre-packed by pack_weights_tc for

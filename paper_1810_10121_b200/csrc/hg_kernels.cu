@@ -972,6 +972,15 @@ static void launch_relin(const Context& c, const Keys& keys, const uint64_t* a, 
   HG_CUDA(cudaGetLastError());
 }
 
+// HG_RELIN_D32=0: the tensor terms stay u64 words in `out` and the key switch adds them at the end
+static bool relin_d32() {
+  static const bool on = [] {
+    const char* e = std::getenv("HG_RELIN_D32");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 void square_relin(const Context& c, const Keys& keys, const uint64_t* in, uint64_t* out, int64_t items, int nl,
                   uint64_t* c2, cudaStream_t s) {
   mul_relin(c, keys, in, in, out, items, nl, c2, s);
@@ -987,8 +996,13 @@ void mul_relin(const Context& c, const Keys& keys, const uint64_t* a, const uint
     check(out + items * 2 * pw <= a || a + items * 2 * pw <= out, HG_EINTERNAL, "relin output aliases its input");
     check(out + items * 2 * pw <= b || b + items * 2 * pw <= out, HG_EINTERNAL, "relin output aliases its input");
     const bool dig = k2::relin_digits_ok(c, nl);  // c2 as u16 digit rows (2^13)
-    k2::relin_c2(c, a, b, 2 * pw, 2 * pw, pw, pw, c2, items, nl, s, out, dig);
-    k2::relin(c, keys, a, b, 2 * pw, 2 * pw, false, c2, out, items, nl, s, true, dig);
+    // the 32-bit lanes' tensor terms d0, d1 as u32 rows (half the bytes of u64 words in `out`),
+    // which the key switch loads into its accumulators up front
+    uint32_t* d32 = relin_d32() ? static_cast<uint32_t*>(const_cast<Context&>(c).scratch(
+                                       static_cast<size_t>(items * 2 * pw) * 4, 12))
+                                : nullptr;
+    k2::relin_c2(c, a, b, 2 * pw, 2 * pw, pw, pw, c2, items, nl, s, out, dig, d32);
+    k2::relin(c, keys, a, b, 2 * pw, 2 * pw, false, c2, out, items, nl, s, true, dig, d32);
     return;
   }
   const size_t sm = limb_smem(c);

@@ -88,6 +88,34 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+// one-thread bulk copies (TMA, no tensor map) completing on an mbarrier
+__device__ __forceinline__ void mb_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mb_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mb_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "HG_MBW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra HG_MBW_%=;\n\t}" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared, `bytes` a multiple of 16, both addresses 16-byte aligned; the generic-proxy
+// reads of the destination that precede it (ordered by a barrier) are fenced into the async proxy
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(sdst)),
+               "l"(gsrc), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
 
 #define HG_KERNEL template <typename W, int LOGN> __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_blocks)
 
@@ -551,7 +579,7 @@ struct DigRows {
 HG_KERNEL k_relin_c2_t(const uint64_t* __restrict__ a, const uint64_t* __restrict__ b, int64_t a_stride,
                        int64_t b_stride, int64_t a1_off, int64_t b1_off, uint64_t* __restrict__ c2, int nl,
                        int64_t items, int G, const LimbList LL, const CtxParams P, uint64_t* __restrict__ d,
-                       uint16_t* __restrict__ dig, const DigRows DR) {
+                       uint16_t* __restrict__ dig, const DigRows DR, uint32_t* __restrict__ d32) {
   extern __shared__ __align__(16) uint64_t smem[];
   Cta<W, LOGN> c(smem, LL, items, G, P, true);
   constexpr int n = 1 << LOGN;
@@ -564,15 +592,20 @@ HG_KERNEL k_relin_c2_t(const uint64_t* __restrict__ a, const uint64_t* __restric
     const uint64_t* y1 = b + r * b_stride + b1_off + (int64_t)c.limb * n;
     l2_next(r + 1 < c.r1, x1 + a_stride, n * 8);
     if (!square) l2_next(r + 1 < c.r1, y1 + b_stride, n * 8);
-    if (d != nullptr) {
+    const bool tensor = d != nullptr || d32 != nullptr;
+    if (tensor) {
       l2_next(r + 1 < c.r1, x1 - a1_off + a_stride, n * 8);
       if (!square) l2_next(r + 1 < c.r1, y1 - b1_off + b_stride, n * 8);
     }
-    if (d != nullptr) {
+    if (tensor) {
       const uint64_t* x0 = a + r * a_stride + (int64_t)c.limb * n;
       const uint64_t* y0 = b + r * b_stride + (int64_t)c.limb * n;
-      uint64_t* d0 = d + (int64_t)r * 2 * nl * n + (int64_t)c.limb * n;
-      uint64_t* d1 = d0 + (int64_t)nl * n;
+      uint64_t* d0 = d32 ? nullptr : d + (int64_t)r * 2 * nl * n + (int64_t)c.limb * n;
+      uint64_t* d1 = d32 ? nullptr : d0 + (int64_t)nl * n;
+      // 32-bit limbs with d32: the tensor terms as u32 rows [item][2][nl][N], loaded by the key
+      // switch into its accumulators at the start of the item
+      uint32_t* e0p = d32 ? d32 + (int64_t)r * 2 * nl * n + (int64_t)c.limb * n : nullptr;
+      uint32_t* e1p = d32 ? e0p + (int64_t)nl * n : nullptr;
       const ulonglong2* x02 = reinterpret_cast<const ulonglong2*>(x0);
       const ulonglong2* x12 = reinterpret_cast<const ulonglong2*>(x1);
       const ulonglong2* y02 = reinterpret_cast<const ulonglong2*>(y0);
@@ -589,8 +622,13 @@ HG_KERNEL k_relin_c2_t(const uint64_t* __restrict__ a, const uint64_t* __restric
           e1[e] = square ? add_mod(m01, m01, Q) : add_mod(m01, pm(a1_[e], b0_[e]), Q);
           e2[e] = pm(a1_[e], b1_[e]);
         }
-        reinterpret_cast<ulonglong2*>(d0)[k] = make_ulonglong2(e0[0], e0[1]);
-        reinterpret_cast<ulonglong2*>(d1)[k] = make_ulonglong2(e1[0], e1[1]);
+        if (d32) {
+          reinterpret_cast<uint2*>(e0p)[k] = make_uint2((uint32_t)e0[0], (uint32_t)e0[1]);
+          reinterpret_cast<uint2*>(e1p)[k] = make_uint2((uint32_t)e1[0], (uint32_t)e1[1]);
+        } else {
+          reinterpret_cast<ulonglong2*>(d0)[k] = make_ulonglong2(e0[0], e0[1]);
+          reinterpret_cast<ulonglong2*>(d1)[k] = make_ulonglong2(e1[0], e1[1]);
+        }
         c.s[lz::padw<W>(2 * k)] = (W)e2[0];
         c.s[lz::padw<W>(2 * k + 1)] = (W)e2[1];
       }
@@ -660,7 +698,8 @@ struct RelinCfg {
   static constexpr size_t ds_bytes = DIG ? ((size_t)2 << LOGN) * (SPLIT ? 2 : 1) : 0;
   static constexpr size_t ks_off = Cfg<W, LOGN>::smem + (C2S ? ((size_t)8 << LOGN) : 0);
   static constexpr size_t ds_off = ks_off + (KS ? key_bytes : 0);
-  static constexpr size_t smem = ds_off + ds_bytes;
+  static constexpr size_t bar_off = (ds_off + ds_bytes + 15) / 16 * 16;  // mbarriers of the bulk copies (DIG)
+  static constexpr size_t smem = bar_off + (DIG ? 16 : 0);
   // CTAs of <= 256 threads (2^12 rows, half rows of a 2^13 ring) fit twice per SM by shared
   // memory: cap registers at 128 so the register file holds both (measured: +3..15% ct ops/s)
   static constexpr int min_blocks = (threads <= 256 && 2 * smem <= kSmemCap) ? 2 : 1;
@@ -689,7 +728,8 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
                                            int64_t a_stride, int64_t b_stride, const uint64_t* __restrict__ c2,
                                            const uint64_t* __restrict__ kval, const uint64_t* __restrict__ kpack,
                                            const uint32_t* __restrict__ kmont, uint64_t* out, int nl, int64_t items,
-                                           int G, const RelinC& K, const LimbList& LL, const CtxParams& P) {
+                                           int G, const RelinC& K, const LimbList& LL, const CtxParams& P,
+                                           const uint32_t* __restrict__ d32) {
   extern __shared__ __align__(16) uint64_t smem[];
   const int half = SPLIT ? (vb & 1) : 0;
   Cta<W, LOGN> c(smem, LL, items, G, P, false, SPLIT ? (vb >> 1) : vb, SPLIT ? half : -1);
@@ -704,19 +744,33 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
   const uint16_t* const dig = reinterpret_cast<const uint16_t*>(c2);
   uint16_t* const ds = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(smem) + RC::ds_off);
   const int sd = K.rows0[nl - 1] + K.digits[nl - 1];
-  auto stage_dig = [&](int it, int row) {  // digit row -> ds, 16 bytes per cp.async
-    const uint4* g = reinterpret_cast<const uint4*>(dig + ((int64_t)it * sd + row) * nfull);
-    for (int ch = threadIdx.x; ch < nfull / 8; ch += lz::lz_threads<LOGN>())
-      cp_async16(reinterpret_cast<uint4*>(ds) + ch, g + ch);
-    cp_async_commit();
+  // DIG: the digit row (and, with KS, the digit's key rows) arrive by one-thread bulk copies on
+  // mbarriers mb[0] (digits) and mb[1] (keys); the phases flip once per digit
+  uint64_t* const mb = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(smem) + RC::bar_off);
+  uint32_t ds_ph = 0, ks_ph = 0;
+  (void)mb;
+  (void)ds_ph;
+  (void)ks_ph;
+  auto stage_dig = [&](int it, int row) {  // digit row -> ds (thread 0; after a barrier)
+    if (threadIdx.x == 0) {
+      mb_expect_tx(&mb[0], nfull * 2);
+      bulk_g2s(ds, dig + ((int64_t)it * sd + row) * nfull, nfull * 2, &mb[0]);
+    }
   };
   (void)dig;
   (void)ds;
   (void)sd;
   (void)stage_dig;
   if constexpr (DIG) {
+    if (threadIdx.x == 0) {
+      mb_init(&mb[0], 1);
+      mb_init(&mb[1], 1);
+      mb_fence_init();
+    }
+    __syncthreads();
     stage_dig(c.r0, 0);
-    cp_async_wait_all();
+    mb_wait(&mb[0], ds_ph);
+    ds_ph ^= 1;
     __syncthreads();  // (also orders the twiddle staging)
   }
   uint64_t* c2s = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(smem) + Cfg<W, LOGN>::smem);
@@ -747,12 +801,39 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
   (void)psi1;
   const uint32_t qneg = neg_qinv32((uint32_t)Q);
   (void)qneg;
+  // 32-bit limbs given d32: the accumulators start at d0, d1 (loaded here, consumed by the first
+  // MAC, so the loads overlap the first digit's transform) and the epilogue loads nothing
+  constexpr bool D32 = GIVEN_D && sizeof(W) == 4;
+  const bool use_d32 = D32 && d32 != nullptr;
+  (void)use_d32;
   for (int item = c.r0; item < c.r1; ++item) {
     W acc0[GPT][16], acc1[GPT][16];
+    if constexpr (D32) {
+      if (use_d32) {
 #pragma unroll
-    for (int gi = 0; gi < GPT; ++gi)
+        for (int gi = 0; gi < GPT; ++gi) {
+          const int k0 = (threadIdx.x + gi * lz::lz_threads<LOGN>()) << 4;
+          const uint4* e0 = reinterpret_cast<const uint4*>(d32 + ((int64_t)item * 2 * nl + j) * nfull + hoff + k0);
+          const uint4* e1 = reinterpret_cast<const uint4*>(reinterpret_cast<const uint32_t*>(e0) + (int64_t)nl * nfull);
 #pragma unroll
-      for (int r = 0; r < 16; ++r) { acc0[gi][r] = 0; acc1[gi][r] = 0; }
+          for (int h = 0; h < 4; ++h) {
+            const uint4 v0 = __ldg(e0 + h), v1 = __ldg(e1 + h);
+            acc0[gi][4 * h] = (W)v0.x; acc0[gi][4 * h + 1] = (W)v0.y; acc0[gi][4 * h + 2] = (W)v0.z; acc0[gi][4 * h + 3] = (W)v0.w;
+            acc1[gi][4 * h] = (W)v1.x; acc1[gi][4 * h + 1] = (W)v1.y; acc1[gi][4 * h + 2] = (W)v1.z; acc1[gi][4 * h + 3] = (W)v1.w;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int gi = 0; gi < GPT; ++gi)
+#pragma unroll
+          for (int r = 0; r < 16; ++r) { acc0[gi][r] = 0; acc1[gi][r] = 0; }
+      }
+    } else {
+#pragma unroll
+      for (int gi = 0; gi < GPT; ++gi)
+#pragma unroll
+        for (int r = 0; r < 16; ++r) { acc0[gi][r] = 0; acc1[gi][r] = 0; }
+    }
     uint64_t* const obase = out + (int64_t)item * 2 * pw + (int64_t)j * nfull + hoff;
     if constexpr (AG) {
 #pragma unroll
@@ -771,7 +852,7 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
       }
       if constexpr (GIVEN_D) {
         // the epilogue's d0, d1 rows -> L2 while the last residue's digits run
-        if (i == nl - 1 && threadIdx.x == 0) {
+        if (i == nl - 1 && threadIdx.x == 0 && !use_d32) {
           const uint64_t* p0 = a + (int64_t)item * a_stride + (int64_t)j * nfull + hoff;
           l2_prefetch(p0, n * 8);
           l2_prefetch(p0 + pw, n * 8);
@@ -787,14 +868,24 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
         const int sh = 15 * d;
         bool c2_staged = false;
         if constexpr (KS) {
-          // this digit's key row (b then a) -> shared memory, behind the NTT below
+          // this digit's key row (b then a) -> shared memory, behind the NTT below.  The rows are
+          // stored pre-swizzled (finish_relin_keys: chunk c at key_slot(c)), so a plain copy lands
+          // every 16-byte chunk in its conflict-free slot
           const uint4* kb = reinterpret_cast<const uint4*>(kmont + (int64_t)row * 2 * K.key_poly_words + (int64_t)j * nfull + hoff);
           const uint4* ka = reinterpret_cast<const uint4*>(kmont + ((int64_t)row * 2 + 1) * K.key_poly_words + (int64_t)j * nfull + hoff);
-          for (int ch = threadIdx.x; ch < n / 4; ch += lz::lz_threads<LOGN>()) {
-            cp_async16(ks + key_slot(ch), kb + ch);
-            cp_async16(ks + n / 4 + key_slot(ch), ka + ch);
+          if constexpr (DIG) {
+            if (threadIdx.x == 0) {
+              mb_expect_tx(&mb[1], 2 * n * 4);
+              bulk_g2s(ks, kb, n * 4, &mb[1]);
+              bulk_g2s(ks + n / 4, ka, n * 4, &mb[1]);
+            }
+          } else {
+            for (int ch = threadIdx.x; ch < n / 4; ch += lz::lz_threads<LOGN>()) {
+              cp_async16(ks + ch, kb + ch);
+              cp_async16(ks + n / 4 + ch, ka + ch);
+            }
+            cp_async_commit();
           }
-          cp_async_commit();
         }
 
         // digit (c2_i >> 15d) & 0x7FFF (ckks_backend.hpp:520-521), extracted inside the first NTT pass
@@ -819,7 +910,10 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
         } else {
           lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return (W)(uint32_t)((__ldg(src + k) >> sh) & 0x7FFF); }, c.tw, q, q2);
         }
-        if constexpr (KS) {
+        if constexpr (KS && DIG) {
+          lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2, [&] { mb_wait(&mb[1], ks_ph); });  // key rows landed
+          ks_ph ^= 1;
+        } else if constexpr (KS) {
           // key row landed (the c2 prefetch committed after it may still be in flight)
           lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2, [&] {
             if (c2_staged) asm volatile("cp.async.wait_group 1;\n" ::: "memory");
@@ -922,11 +1016,33 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
             }
           }
         }
-        if constexpr (DIG) cp_async_wait_all();  // the next digit row (staged behind this NTT)
+        if constexpr (DIG) {
+          if (c2_staged) {  // the next digit row (staged behind this NTT)
+            mb_wait(&mb[0], ds_ph);
+            ds_ph ^= 1;
+          }
+        }
         __syncthreads();  // smem reused by the next digit
       }
     }
     // epilogue: + d0, d1; canonical store
+    if constexpr (D32) {
+      if (use_d32) {  // d0, d1 already accumulated
+#pragma unroll
+        for (int gi = 0; gi < GPT; ++gi) {
+          const int k0 = (threadIdx.x + gi * lz::lz_threads<LOGN>()) << 4;
+          ulonglong2* o0 = reinterpret_cast<ulonglong2*>(obase + k0);
+          ulonglong2* o1 = reinterpret_cast<ulonglong2*>(obase + k0 + pw);
+          const uint32_t q32 = (uint32_t)Q;
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            o0[h] = make_ulonglong2(csub<uint32_t>((uint32_t)acc0[gi][2 * h], q32), csub<uint32_t>((uint32_t)acc0[gi][2 * h + 1], q32));
+            o1[h] = make_ulonglong2(csub<uint32_t>((uint32_t)acc1[gi][2 * h], q32), csub<uint32_t>((uint32_t)acc1[gi][2 * h + 1], q32));
+          }
+        }
+        continue;
+      }
+    }
 #pragma unroll
     for (int gi = 0; gi < GPT; ++gi) {
       const int k0 = (threadIdx.x + gi * lz::lz_threads<LOGN>()) << 4;
@@ -999,9 +1115,10 @@ __global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT, DIG>::threads, RelinC
     k_relin_t(const uint64_t* a, const uint64_t* __restrict__ b, int64_t a_stride, int64_t b_stride,
               const uint64_t* __restrict__ c2, const uint64_t* __restrict__ kval,
               const uint64_t* __restrict__ kpack, const uint32_t* __restrict__ kmont, uint64_t* out,
-              int nl, int64_t items, int G, const RelinC K, const LimbList LL, const CtxParams P) {
+              int nl, int64_t items, int G, const RelinC K, const LimbList LL, const CtxParams P,
+              const uint32_t* __restrict__ d32) {
   relin_body<W, LOGN, GIVEN_D, SPLIT, DIG>((int)blockIdx.x, a, b, a_stride, b_stride, c2, kval, kpack, kmont, out, nl,
-                                      items, G, K, LL, P);
+                                      items, G, K, LL, P, d32);
 }
 
 // ---------------------------------------------------------------------------
@@ -1597,7 +1714,7 @@ bool relin_digits_ok(const Context& c, int nl) {
 
 void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, int64_t a_stride,
            int64_t b_stride, bool given_d, const uint64_t* c2, uint64_t* out, int64_t items, int nl, cudaStream_t s,
-           bool d_in_out, bool digits) {
+           bool d_in_out, bool digits, const uint32_t* d32) {
   check(relin_supported(c), HG_EINTERNAL, "key switch: ring degree outside 2^10..2^15");
   check(!digits || relin_digits_ok(c, nl), HG_EINTERNAL, "key switch: digit rows outside the 2^13 half-row layout");
   if (items <= 0) return;
@@ -1622,6 +1739,8 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
         // d_in_out: relin_c2 already wrote d0, d1 into `out` for this lane; add to them in place
         const bool in_out = !given_d && d_in_out && relin_d_in_out<W_, LOGN>();
         const bool gd = given_d || in_out;
+        // 32-bit lanes of the square/multiply path: d0, d1 come as u32 rows (relin_c2 with d32)
+        const uint32_t* dd32 = (in_out && sizeof(W_) == 4) ? d32 : nullptr;
         const uint64_t* aa = in_out ? out : a;
         const int64_t as = in_out ? 2LL * nl * c.n() : a_stride;
         const void* fn = gd ? (const void*)k_relin_t<W_, LT, true, SPLIT, DIG>
@@ -1634,11 +1753,11 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
         if (gd)
           k_relin_t<W_, LT, true, SPLIT, DIG><<<grid, threads, Cf::smem, s>>>(
               aa, b, as, b_stride, c2, keys.relin.as<uint64_t>(), keys.relin_pack.as<uint64_t>(),
-              keys.relin_mont.as<uint32_t>(), out, nl, items, G, K, LL, c.kp());
+              keys.relin_mont.as<uint32_t>(), out, nl, items, G, K, LL, c.kp(), dd32);
         else
           k_relin_t<W_, LT, false, SPLIT, DIG><<<grid, threads, Cf::smem, s>>>(
               a, b, a_stride, b_stride, c2, keys.relin.as<uint64_t>(), keys.relin_pack.as<uint64_t>(),
-              keys.relin_mont.as<uint32_t>(), out, nl, items, G, K, LL, c.kp());
+              keys.relin_mont.as<uint32_t>(), out, nl, items, G, K, LL, c.kp(), nullptr);
         c.kt_end(s);
         HG_CUDA(cudaGetLastError());
       };
@@ -1667,7 +1786,7 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
 
 void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_stride, int64_t b_stride,
               int64_t a1_off, int64_t b1_off, uint64_t* c2, int64_t items, int nl, cudaStream_t s, uint64_t* d,
-              bool digits) {
+              bool digits, uint32_t* d32) {
   if (items <= 0) return;
   DigRows DR{};
   for (int i = 0; i < nl; ++i) {
@@ -1688,13 +1807,15 @@ void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_
       grid_for<W_, LOGN>(LL, items, grid, G);
       // the tensor terms go to d only for lanes whose key switch adds to them (relin_d_in_out)
       uint64_t* dd = d != nullptr && relin_d_in_out<W_, LOGN>() ? d : nullptr;
+      uint32_t* dd32 = (dd != nullptr && sizeof(W_) == 4) ? d32 : nullptr;
+      if (dd32) dd = nullptr;
       const bool sq = a == b && a_stride == b_stride && a1_off == b1_off;
       set_smem_attr((const void*)k_relin_c2_t<W_, LOGN>, Cf::smem);
       c.kt_begin(std::is_floating_point_v<W_> ? "k_relin_c2_t/f64" : sizeof(W_) == 4 ? "k_relin_c2_t/u32" : "k_relin_c2_t/u64", s,
-                 (double)items * LL.count * (dd ? (sq ? 5 : 7) : 3) * nw,
-                 (double)items * LL.count * (bfly(c) + c.n() * (dd ? 4 : 1)));
+                 (double)items * LL.count * ((dd || dd32) ? (sq ? 5 : 7) : 3) * nw,
+                 (double)items * LL.count * (bfly(c) + c.n() * ((dd || dd32) ? 4 : 1)));
       k_relin_c2_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(a, b, a_stride, b_stride, a1_off, b1_off, c2, nl,
-                                                                 items, G, LL, c.kp(), dd, dig, DR);
+                                                                 items, G, LL, c.kp(), dd, dig, DR, dd32);
       c.kt_end(s);
       HG_CUDA(cudaGetLastError());
     });

@@ -15,7 +15,7 @@ def _stats():
     }
 
 
-PEAKS = {"modmul32_per_s": 4.1e12, "modmul64_per_s": 0.96e12, "modmulf64_per_s": 2.8e12}
+PEAKS = {"modmul32_per_s": 4.1e12, "modmul64_per_s": 0.96e12, "modmulf64_per_s": 2.8e12, "u8mac_per_s": 1.666e15}
 
 
 def test_roofline_is_the_modmul_view_of_the_dominant_kernel():
@@ -35,7 +35,7 @@ def test_roofline_is_the_modmul_view_of_the_dominant_kernel():
     assert abs(rl["hbm_view"]["frac"] - (1.5e10 / sec / 1e9) / 6550.1) < 1e-12
     # each lane against its own peak
     assert abs(per["k_relin_t/f64"]["modmul_frac"] - (8.0e9 / 9.0e-3) / 2.8e12) < 1e-12
-    assert abs(per["k_gemm_tc"]["modmul_frac"] - (7.0e10 / 6.1e-3) / 4.1e12) < 1e-12
+    assert abs(per["k_gemm_tc"]["modmul_frac"] - (7.0e10 / 6.1e-3) / 1.666e15) < 1e-12
 
 
 def test_workload_config_names_the_workload():

@@ -28,6 +28,7 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__warps_active.avg.pct_of_peak_sustained_active", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_tensor_subpipe_imma_cycles_active_realtime.avg",
         "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "launch__registers_per_thread", "launch__grid_size",
@@ -38,6 +39,12 @@ lines = [f"ncu --set full --clock-control none capture: {os.path.basename(rep)}"
 for n in WANT:
     val, unit = m(n)
     lines.append(f"  {n:72s} {val:>18s} {unit}")
+# every tensor-pipe / TMEM metric the capture holds (the UMMA utilisation evidence on sm_100)
+extra = [n for n in h if ("tensor" in n or "tmem" in n or "_tc_" in n or "utc" in n) and n not in WANT]
+for n in extra[:40]:
+    val, unit = m(n)
+    if val not in ("", "n/a"):
+        lines.append(f"  {n:72s} {val:>18s} {unit}")
 st = []
 for i, n in enumerate(h):
     if "warps_issue_stalled" in n and n.endswith("per_issue_active.ratio"):
