@@ -1,18 +1,24 @@
 #!/usr/bin/env bash
 # Reproduce the round's GPU evidence on a B200 box (run from the repo root, e.g. through
 # gpurun).  Writes into gpurun_out/: the GPU test log, smoke, the bench lines (ours and the
-# reference arm), the config-2 sweep, the ncu launch list of the bench command and --set full
-# summaries (text only: a full .ncu-rep is ~60 MB) of the dominant kernels.  Copy what should be
-# judged into profiles/.
+# reference arm; c3 headline plus c4/c5), the ncu launch list of the bench command and
+# --set full summaries (text only: a full .ncu-rep is ~60 MB) of every kernel above 3% of a
+# step.  R names the round prefix (default r2).  Copy what should be judged into profiles/.
 set -x
+R=${R:-r2}
 mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest_rc=$?
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke_rc=$?
-python bench.py > gpurun_out/bench.log 2> gpurun_out/bench.err; echo bench_rc=$?
-python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_reference.log 2>&1; echo ref_rc=$?
-timeout 900 python tools/prim_sweep.py --out gpurun_out/sweep_c2.jsonl > /dev/null 2> gpurun_out/sweep.err
+if [ -z "$SKIP_TESTS" ]; then
+  timeout 1500 python -m pytest tests -m gpu -q -rs > gpurun_out/${R}_pytest_gpu.log 2>&1; echo pytest_rc=$?
+  python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${R}_smoke.log 2>&1; echo smoke_rc=$?
+fi
+if [ -z "$SKIP_BENCH" ]; then
+  python bench.py > gpurun_out/${R}_bench_c3.json 2> gpurun_out/${R}_bench_c3.err; echo bench_rc=$?
+  python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/${R}_bench_c3_reference.json 2>&1; echo ref_rc=$?
+  python bench.py --config c5 --batch 8192 --no-cpu > gpurun_out/${R}_bench_c5.json 2>&1
+  python bench.py --config c4 --batch 8192 --steps 5 --warmup 3 --no-cpu > gpurun_out/${R}_bench_c4.json 2>&1
+fi
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-  --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu > gpurun_out/ncu_launches.log 2>&1
+  --log-file gpurun_out/${R}_c3_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu > gpurun_out/ncu_launches.log 2>&1
 cap() {  # name kernel-regex launches-to-skip traffic-key workload-command...
   local name=$1 rx=$2 skip=$3 key=$4; shift 4
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:"$rx" -s "$skip" -c 1 \
@@ -22,10 +28,14 @@ cap() {  # name kernel-regex launches-to-skip traffic-key workload-command...
   rm -f /tmp/$name.ncu-rep
 }
 B="python bench.py --steps 1 --warmup 1 --no-cpu"
-cap r1_ncu_relin_u32 k_relin_t 0 k_relin_t/u32 $B
-cap r1_ncu_relin_f64 k_relin_t 1 k_relin_t/f64 $B
-cap r1_ncu_rescale_u32 k_rescale_rest_t 0 k_rescale_rest_t/u32 $B
-cap r1_ncu_gemm_tc k_gemm_tc 0 k_gemm_tc $B
-cap r1_ncu_gemm_tc_c5 k_gemm_tc 0 k_gemm_tc_c5 python tools/diag_step.py c5
-timeout 600 python tools/diag_step.py c5 > gpurun_out/diag_c5.log 2>&1
-timeout 900 python tools/diag_step.py c4 > gpurun_out/diag_c4.log 2>&1
+cap ${R}_ncu_relin_u32 k_relin_t 0 k_relin_t/u32 $B
+cap ${R}_ncu_relin_f64 k_relin_t 1 k_relin_t/f64 $B
+cap ${R}_ncu_rescale_u32 k_rescale_rest 0 k_rescale_rest_t/u32 $B
+cap ${R}_ncu_gemm_tc k_gemm_tc 0 k_gemm_tc $B
+cap ${R}_ncu_gemm_lz k_gemm_lz 0 k_gemm_lz $B
+cap ${R}_ncu_gemm_f64 k_gemm_f64 0 k_gemm_f64 $B
+cap ${R}_ncu_relin_c2_u32 k_relin_c2_t 0 k_relin_c2_t/u32 $B
+cap ${R}_ncu_scatter k_scatter_items 0 k_scatter_items $B
+cap ${R}_ncu_encode k_encode_fft 0 k_encode_fft_block python bench.py --steps 1 --warmup 1 --no-cpu
+cap ${R}_ncu_ntt k_ntt_t 12 k_ntt_t python tools/prim_sweep.py --ns 16384 --ls 7
+cap ${R}_ncu_gemm_tc_c5 k_gemm_tc 0 k_gemm_tc_c5 python tools/diag_step.py c5 1
