@@ -363,11 +363,12 @@ struct RescalePCfg {
   static constexpr size_t x_off = c_off + ((size_t)nfull * sizeof(CT) + 15) / 16 * 16;
   static constexpr size_t smem = x_off + (size_t)n * 8;
   static constexpr bool fits = Cfg<W, LOGN>::TWS && smem <= kSmemCap;
+  static constexpr int min_blocks = 2 * smem <= kSmemCap ? 2 : 1;  // half rows of 2^13: two CTAs per SM
 };
 __device__ __forceinline__ int xslot(int c) { return c ^ ((c >> 3) & 7); }
 
 template <typename W, int LOGN, typename CT, bool SPLIT>
-__global__ void __launch_bounds__(Cfg<W, LOGN>::threads, 1)
+__global__ void __launch_bounds__(Cfg<W, LOGN>::threads, (RescalePCfg<W, LOGN, CT, SPLIT>::min_blocks))
     k_rescale_rest_p(const uint64_t* __restrict__ in, const CT* __restrict__ cen, uint64_t* __restrict__ out,
                      int nl, int64_t polys, int G, const LimbList LL, const RescaleC R, const CtxParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
@@ -1570,6 +1571,14 @@ void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const i
   run(cl.wide, uint64_t{}, lf.wide());
 }
 
+// HG_RESCALE_SPLIT13=0: whole-row pipelined rest-limb CTAs at 2^13 (one per SM) instead of half rows
+static bool rescale_split13() {
+  static const bool on = [] {
+    const char* e = std::getenv("HG_RESCALE_SPLIT13");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 // HG_RESCALE_PIPE=0: the unpipelined rest-limb kernels (A/B measurements)
 static bool rescale_pipelined() {
   static const bool on = [] {
@@ -1604,12 +1613,13 @@ static void rescale_t(const Context& c, const uint64_t* in, uint64_t* out, int64
     using W = decltype(wtag);
     if (LL.count == 0) return;
     by_logn<W>(c, [&]<typename W_, int LOGN>() {
-      // pipelined variant: whole rows up to 2^13, half rows at 2^14 (when it fits in shared memory)
-      constexpr bool SPL = LOGN == 14;
-      constexpr int LP = SPL ? LOGN - 1 : LOGN;
-      using PC = RescalePCfg<W_, LP, CT, SPL>;
-      if constexpr (PC::fits && LOGN <= 14) {
-        if (rescale_pipelined()) {
+      // pipelined variant: whole rows up to 2^13, half rows at 2^14 and (32-bit limbs with a
+      // 32-bit lift, HG_RESCALE_SPLIT13) at 2^13, when it fits in shared memory
+      auto launch_p = [&]<int LP, bool SPL>() -> bool {
+        using PC = RescalePCfg<W_, LP, CT, SPL>;
+        if constexpr (!PC::fits) {
+          return false;
+        } else {
           const int halves = SPL ? 2 : 1;
           const int64_t target = 148LL * 3;
           const int G = (int)std::max<int64_t>(1, std::min<int64_t>(64, (polys * LL.count * halves + target - 1) / target));
@@ -1619,10 +1629,20 @@ static void rescale_t(const Context& c, const uint64_t* in, uint64_t* out, int64
                      (double)polys * LL.count * (2 * nw + (double)c.n() * sizeof(CT)),
                      (double)polys * LL.count * (bfly(c) + c.n()));
           k_rescale_rest_p<W_, LP, CT, SPL><<<grid, Cfg<W_, LP>::threads, PC::smem, s>>>(in, cen, out, nl, polys, G, LL,
-                                                                                    R, c.kp());
+                                                                                      R, c.kp());
           c.kt_end(s);
           HG_CUDA(cudaGetLastError());
-          return;
+          return true;
+        }
+      };
+      if (rescale_pipelined()) {
+        if constexpr (LOGN == 14) {
+          if (launch_p.template operator()<LOGN - 1, true>()) return;
+        } else if constexpr (LOGN == 13 && sizeof(W_) == 4 && sizeof(CT) == 4) {
+          if (rescale_split13() ? launch_p.template operator()<12, true>() : launch_p.template operator()<13, false>())
+            return;
+        } else if constexpr (LOGN <= 13) {
+          if (launch_p.template operator()<LOGN, false>()) return;
         }
       }
       if constexpr (LOGN == 14 && std::is_same_v<W_, uint32_t>) {

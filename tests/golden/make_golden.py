@@ -41,6 +41,16 @@ PRIM_CASES = {
     # BASELINE config 2 (primitive sweep) shapes: 30-bit chains, L = 7 and L = 15, up to N = 2^15
     "n16384_30x8": (16384, 30, [30] * 8, 29),
     "n32768_30x16": (32768, 30, [30] * 16, 23),
+    # the rest of config 2's (N, L) grid: L + 1 30-bit primes for N = 2^12 .. 2^15, L = 3 / 7 / 15
+    "n4096_30x8": (4096, 30, [30] * 8, 37),
+    "n4096_30x16": (4096, 30, [30] * 16, 41),
+    "n8192_30x4": (8192, 30, [30] * 4, 43),
+    "n8192_30x8": (8192, 30, [30] * 8, 47),
+    "n8192_30x16": (8192, 30, [30] * 16, 53),
+    "n16384_30x4": (16384, 30, [30] * 4, 59),
+    "n16384_30x16": (16384, 30, [30] * 16, 61),
+    "n32768_30x4": (32768, 30, [30] * 4, 67),
+    "n32768_30x8": (32768, 30, [30] * 8, 71),
     # BASELINE config 4's context: N = 2^14, {50, 30x7, 50} (L = 8, D = 4 digits for the 50-bit limbs)
     "n16384_50_30x7_50": (16384, 30, [50] + [30] * 7 + [50], 31),
 }

@@ -12,7 +12,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 GOLDEN = os.path.join(HERE, "golden")
 
 PRIM_CASES = ["n1024_30x3", "n1024_36_26x2_36", "n2048_50_30_50", "n8192_40_30_40", "n4096_30x4",
-              "n16384_50_30x2_50", "n16384_30x8", "n32768_30x16", "n16384_50_30x7_50"]
+              "n16384_50_30x2_50", "n16384_30x8", "n32768_30x16", "n16384_50_30x7_50",
+              # config 2's remaining (N, L) shapes
+              "n4096_30x8", "n4096_30x16", "n8192_30x4", "n8192_30x8", "n8192_30x16", "n16384_30x4",
+              "n16384_30x16", "n32768_30x4", "n32768_30x8"]
 
 
 def sha(a: np.ndarray) -> str:
