@@ -196,6 +196,14 @@ int64_t hg_plan_launches(const hg_plan* plan);
 int hg_comm_unique_id(void* id_out);
 /* join a `world`-rank group as `rank` on the plan's device; world == 1 turns sharding off */
 int hg_plan_set_comm(hg_plan* plan, int rank, int world, const void* id);
+/* host-mediated transport instead of NCCL (tests, or a deployment with its own collective): at
+ * every gather point the plan's stream is synchronised and fn is called with the tensor's device
+ * buffer `dev` (items of item_words uint64 words); ranges holds, rank by rank, counts[r] pairs of
+ * [begin, end) item ranges that rank r computed; fn must fill every other rank's ranges and
+ * return 0.  Same partition and gather schedule as hg_plan_set_comm. */
+typedef int (*hg_gather_fn)(void* user, const char* tensor_id, uint64_t* dev, int64_t item_words,
+                            const int64_t* ranges, const int32_t* counts, int world);
+int hg_plan_set_gather_callback(hg_plan* plan, int rank, int world, hg_gather_fn fn, void* user);
 /* in-process group on ONE device (checks the sharded path without NCCL): the plans, which
  * share one context, run in lockstep, each computing its shard; gathers are device copies */
 int hg_group_run(hg_plan** plans, int world);

@@ -43,6 +43,8 @@ u64p = C.POINTER(C.c_uint64)
 i32p = C.POINTER(C.c_int32)
 f64p = C.POINTER(C.c_double)
 vp = C.c_void_p
+# hg_gather_fn (include/hegpu.h): user, tensor id, device buffer, item words, ranges, counts, world
+GATHER_FN = C.CFUNCTYPE(C.c_int, vp, C.c_char_p, vp, C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.c_int)
 
 
 def lib():
@@ -88,6 +90,7 @@ def lib():
         "hg_encode": (C.c_int, [vp, f64p, C.c_int64, C.c_int, C.c_double, vp]),
         "hg_comm_unique_id": (C.c_int, [vp]),
         "hg_plan_set_comm": (C.c_int, [vp, C.c_int, C.c_int, vp]),
+        "hg_plan_set_gather_callback": (C.c_int, [vp, C.c_int, C.c_int, GATHER_FN, vp]),
         "hg_group_run": (C.c_int, [C.POINTER(vp), C.c_int]),
         "hg_shard_partition": (C.c_int, [C.c_int64, C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64)]),
         "hg_plan_output_async": (C.c_int, [vp, C.c_char_p, C.POINTER(vp)]),
@@ -320,6 +323,26 @@ class Plan:
         comm_id: the 128 bytes from comm_unique_id() on rank 0, shared by the caller."""
         buf = None if comm_id is None else C.create_string_buffer(bytes(comm_id), 128)
         _chk(lib().hg_plan_set_comm(self._h, rank, world, buf))
+
+    def set_gather(self, rank: int, world: int, gather):
+        """Shard like set_comm, but every all-gather-v goes through `gather(tensor_id, dev_ptr,
+        item_words, ranges)` on the host (ranges[r] = rank r's [(begin, end), ...] items); it must
+        fill every other rank's ranges of the device buffer (e.g. with torch.distributed/gloo)."""
+
+        def tramp(_user, tid, dev, item_words, ranges, counts, w):
+            try:
+                rr, off = [], 0
+                for r in range(w):
+                    rr.append([(ranges[2 * (off + i)], ranges[2 * (off + i) + 1]) for i in range(counts[r])])
+                    off += counts[r]
+                gather(tid.decode(), int(dev), int(item_words), rr)
+                return 0
+            except Exception as e:  # reported through hg_last_error by the executor
+                print(f"gather callback failed: {e!r}", flush=True)
+                return 1
+
+        self._gather_cb = GATHER_FN(tramp)  # keep alive as long as the plan
+        _chk(lib().hg_plan_set_gather_callback(self._h, rank, world, self._gather_cb, None))
 
     def output(self, out_id: str, shape=None) -> np.ndarray:
         n = C.c_int64()

@@ -16,6 +16,7 @@
 //  * AvgPool's window sum times encode_constant(1/(w1 w2)) == the weighted sum
 //    with that constant on every window term (exact modular arithmetic).
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -1043,27 +1044,61 @@ Val contraction_paradigm(hg_plan* P, const GNode& node, const std::vector<int64_
                          const std::function<void(int64_t g, int t, int64_t& x_e)>& x_index,
                          const std::function<void(int64_t g, int m, int t, int64_t& w_e)>& w_index) {
   const Context& c = *P->ctx;
-  check(P->world == 1, HG_EVALIDATION,
-        "node '" + node.id + "': encrypted-weight contractions are not sharded on the GPU path");
   const Side sx = side_of(P, x), sw = side_of(P, w);
   const int64_t m_out = groups * mg;
   const int64_t x_space = x.is_cipher() ? x.ct->count : (x.batched ? x.raw->count() / P->batch : x.raw->count());
   const int64_t w_space = w.is_cipher() ? w.ct->count : (w.batched ? w.raw->count() / P->batch : w.raw->count());
-  // term lists by output element (terms_of, runtime.hpp:1029-1035)
-  std::vector<int32_t> xi(static_cast<size_t>(m_out * kt)), wi(static_cast<size_t>(m_out * kt));
-  for (int64_t g = 0; g < groups; ++g)
-    for (int m = 0; m < mg; ++m) {
+  // this rank's outputs (everything when world == 1), in element order; sharded plans compute
+  // them compactly, place them at their positions and record every rank's ranges for the gathers
+  const bool sharded = P->world > 1;
+  const Part part = shard_part(groups, mg, P->world, P->rank);
+  std::vector<std::array<int64_t, 3>> loc;  // (element, g, m)
+  for (int64_t g = part.g0; g < part.g1; ++g)
+    for (int64_t m = part.m0; m < part.m1; ++m) {
       int64_t oe;
-      out_index(g, m, oe);
+      out_index(g, static_cast<int>(m), oe);
       check(oe >= 0 && oe < m_out, HG_EINTERNAL, "contraction output index out of range");
-      for (int t = 0; t < kt; ++t) {
-        int64_t xe, we;
-        x_index(g, t, xe);
-        w_index(g, m, t, we);
-        xi[oe * kt + t] = static_cast<int32_t>(xe);
-        wi[oe * kt + t] = static_cast<int32_t>(we);
-      }
+      loc.push_back({oe, g, m});
     }
+  std::sort(loc.begin(), loc.end());
+  const int64_t m_loc = static_cast<int64_t>(loc.size());
+  std::shared_ptr<ShardMap> smap;
+  if (sharded) {
+    smap = std::make_shared<ShardMap>();
+    for (int r = 0; r < P->world; ++r) {
+      const Part pr = shard_part(groups, mg, P->world, r);
+      std::vector<int64_t> els;
+      for (int64_t g = pr.g0; g < pr.g1; ++g)
+        for (int64_t m = pr.m0; m < pr.m1; ++m) {
+          int64_t oe;
+          out_index(g, static_cast<int>(m), oe);
+          els.push_back(oe);
+        }
+      smap->ranges.push_back(coalesce(std::move(els)));
+    }
+  }
+  // term lists by (local) output element (terms_of, runtime.hpp:1029-1035)
+  std::vector<int32_t> xi(static_cast<size_t>(m_loc * kt)), wi(static_cast<size_t>(m_loc * kt));
+  for (int64_t pI = 0; pI < m_loc; ++pI)
+    for (int t = 0; t < kt; ++t) {
+      int64_t xe, we;
+      x_index(loc[pI][1], t, xe);
+      w_index(loc[pI][1], static_cast<int>(loc[pI][2]), t, we);
+      xi[pI * kt + t] = static_cast<int32_t>(xe);
+      wi[pI * kt + t] = static_cast<int32_t>(we);
+    }
+  // the compact local result at its element positions of a full-size tensor
+  auto place = [&](const std::shared_ptr<CtT>& res) {
+    if (!sharded) return res;
+    auto full = new_ct(P, m_out, res->level, res->scale);
+    int64_t off = 0;
+    for (const auto& [b, e] : smap->ranges[static_cast<size_t>(P->rank)]) {
+      HG_CUDA(cudaMemcpyAsync(full->item(b), res->item(off), static_cast<size_t>((e - b) * res->item_words()) * 8,
+                              cudaMemcpyDeviceToDevice, S(P)));
+      off += e - b;
+    }
+    return full;
+  };
   DevArr dxi(xi.size() * 4, S(P)), dwi(wi.size() * 4, S(P));
   HG_CUDA(cudaMemcpyAsync(dxi.p, xi.data(), xi.size() * 4, cudaMemcpyHostToDevice, S(P)));
   HG_CUDA(cudaMemcpyAsync(dwi.p, wi.data(), wi.size() * 4, cudaMemcpyHostToDevice, S(P)));
@@ -1081,12 +1116,13 @@ Val contraction_paradigm(hg_plan* P, const GNode& node, const std::vector<int64_
     P->prof.add += m_out * (kt - 1);
     const int nl = level + 1;
     const int64_t pw = static_cast<int64_t>(nl) * c.n();
-    DevArr acc3(static_cast<size_t>(m_out * 3 * pw) * 8, S(P)), c2(static_cast<size_t>(m_out * pw) * 8, S(P));
-    auto r2 = new_ct(P, m_out, level, cx->scale * cw->scale);
-    k::tensor_acc(c, cx->p, dxi.as<int32_t>(), cw->p, dwi.as<int32_t>(), acc3.as<uint64_t>(), m_out, kt, nl, S(P));
-    k::relin3(c, *P->keys, acc3.as<uint64_t>(), r2->p, m_out, nl, c2.as<uint64_t>(), S(P));
+    DevArr acc3(static_cast<size_t>(m_loc * 3 * pw) * 8, S(P)), c2(static_cast<size_t>(m_loc * pw) * 8, S(P));
+    auto r2 = new_ct(P, m_loc, level, cx->scale * cw->scale);
+    k::tensor_acc(c, cx->p, dxi.as<int32_t>(), cw->p, dwi.as<int32_t>(), acc3.as<uint64_t>(), m_loc, kt, nl, S(P));
+    k::relin3(c, *P->keys, acc3.as<uint64_t>(), r2->p, m_loc, nl, c2.as<uint64_t>(), S(P));
     P->launches += 4;
-    out.ct = rescale_t(P, r2);
+    out.ct = place(m_loc > 0 ? rescale_t(P, r2) : new_ct(P, 0, level - 1, cx->scale * cw->scale / static_cast<double>(c.primes()[level])));
+    out.shard = smap;
     HG_CUDA(cudaStreamSynchronize(S(P)));  // the host index vectors go out of scope
     return out;
   }
@@ -1101,11 +1137,13 @@ Val contraction_paradigm(hg_plan* P, const GNode& node, const std::vector<int64_
   auto pts = encode_raw_all(P, rv, x_space, level, w_scale);
   P->prof.mul_pt += m_out * kt;  // no bypass: the data side is not from constants
   P->prof.add += m_out * (kt - 1);
-  auto prod = new_ct(P, m_out, level, cw->scale * w_scale);
-  k::ctpt_acc(c, cw->p, dwi.as<int32_t>(), pts->as<uint64_t>(), dxi.as<int32_t>(), prod->p, m_out, kt, level + 1,
+  auto prod = new_ct(P, m_loc, level, cw->scale * w_scale);
+  k::ctpt_acc(c, cw->p, dwi.as<int32_t>(), pts->as<uint64_t>(), dxi.as<int32_t>(), prod->p, m_loc, kt, level + 1,
               S(P));
   P->launches += 1;
-  out.ct = rescale_t(P, prod);
+  out.ct = place(m_loc > 0 ? rescale_t(P, prod)
+                           : new_ct(P, 0, level - 1, cw->scale * w_scale / static_cast<double>(c.primes()[level])));
+  out.shard = smap;
   HG_CUDA(cudaStreamSynchronize(S(P)));
   return out;
 }
@@ -2638,6 +2676,31 @@ struct NcclTransport final : Transport {
   }
 };
 
+// Host-mediated all-gather-v through a caller-supplied function (hg_plan_set_gather_callback):
+// the plan's stream is synchronised, so this rank's ranges are final in `dev`, then the callback
+// fills every other rank's ranges (e.g. D2H, a torch.distributed / gloo all-gather, H2D).  Same
+// gather points and ranges as the NCCL transport; used to exercise the sharded executor across
+// processes where one GPU per rank is not available.
+struct CallbackTransport final : Transport {
+  hg_gather_fn fn = nullptr;
+  void* user = nullptr;
+  void allgatherv(hg_plan* P, const std::string& id, CtT& ct, const ShardMap& m) override {
+    HG_CUDA(cudaStreamSynchronize(S(P)));
+    std::vector<int64_t> flat;
+    std::vector<int32_t> counts;
+    for (const auto& rr : m.ranges) {
+      counts.push_back(static_cast<int32_t>(rr.size()));
+      for (const auto& [b, e] : rr) {
+        flat.push_back(b);
+        flat.push_back(e);
+      }
+    }
+    const int rc = fn(user, id.c_str(), ct.p, ct.item_words(), flat.data(), counts.data(),
+                      static_cast<int>(m.ranges.size()));
+    check(rc == 0, HG_EINTERNAL, "gather callback failed for tensor '" + id + "'");
+  }
+};
+
 void run_group(const std::vector<hg_plan*>& ps) {
   std::vector<RunState> st(ps.size());
   for (size_t r = 0; r < ps.size(); ++r) run_begin(ps[r], st[r]);
@@ -2901,6 +2964,23 @@ int hg_plan_set_comm(hg_plan* P, int rank, int world, const void* id) {
     std::memcpy(&uid, id, sizeof(uid));
     HG_CUDA(cudaSetDevice(P->ctx->device()));
     hg::nccl_ok(hg::nccl().init(&t->comm, world, uid, rank), "ncclCommInitRank");
+    P->transport = t;
+  });
+}
+
+int hg_plan_set_gather_callback(hg_plan* P, int rank, int world, hg_gather_fn fn, void* user) {
+  return guard_x([&] {
+    hg::DeviceGuard dg_(P ? P->ctx->device() : -1);
+    hg::check(P && world >= 1 && rank >= 0 && rank < world, HG_E_VALIDATION, "invalid rank/world");
+    hg::check(world == 1 || fn != nullptr, HG_E_VALIDATION, "a gather function is required for world > 1");
+    P->cache.clear();  // contraction blocks depend on the partition
+    P->rank = rank;
+    P->world = world;
+    P->transport.reset();
+    if (world == 1) return;
+    auto t = std::make_shared<hg::CallbackTransport>();
+    t->fn = fn;
+    t->user = user;
     P->transport = t;
   });
 }

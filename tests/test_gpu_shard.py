@@ -13,7 +13,10 @@ from tests import golden_util as G
 
 pytestmark = pytest.mark.gpu
 
-CASES = [("mini", 2), ("ops2", 2), ("c1", 2), ("c1", 3), ("c3_n2048", 2), ("c3_n2048", 4), ("c5_n2048", 3), ("c4_n2048", 4), ("c3", 8)]
+CASES = [("mini", 2), ("ops2", 2), ("ops3", 2), ("ops3_na", 3), ("c1", 2), ("c1", 3), ("c3_n2048", 2), ("c3_n2048", 4),
+         ("c5_n2048", 3), ("c4_n2048", 4), ("c4s", 4), ("c3", 8),
+         # encrypted-weight contractions (EncryptedModel / EncryptedBoth) sharded by outputs
+         ("pmodel_m", 2), ("pmodel_b", 2), ("pmodel_b", 3), ("mini_b", 2)]
 
 
 def _available(name):
@@ -34,6 +37,8 @@ def test_shard_group_bit_exact(name, world, cuda_ok):
     keys = P.Keys(ctx, spec["key_seed"])
     plans = [P.Plan(ctx, keys, graph, spec["batch"], spec["exec_seed"]) for _ in range(world)]
     for p in plans:
+        if "paradigm" in spec or "bypass" in spec:
+            p.set_options(paradigm=spec.get("paradigm"), bypass=spec.get("bypass"))
         p.bind_input("x", x)
     for _ in range(2):  # the second run reuses the per-rank node caches
         P.group_run(plans)
