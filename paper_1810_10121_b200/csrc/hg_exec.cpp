@@ -1637,8 +1637,15 @@ Val kernel_poly_act(hg_plan* P, const GNode& node, const std::vector<int64_t>& o
       DevArr prod(static_cast<size_t>(cnt * item_bytes), S(P));
       DevArr c2(static_cast<size_t>(cnt) * nl * c.n() * 8, S(P));
       DevArr sc(static_cast<size_t>(cnt) * 2 * c.n() * 8, S(P));
-      k::square_relin(c, *P->keys, xe->item(b0), prod.as<uint64_t>(), cnt, nl, c2.as<uint64_t>(), S(P));
-      k::rescale(c, prod.as<uint64_t>(), o->item(b0), cnt * 2, nl, sc.as<int64_t>(), S(P));
+      if (k2::relin_rescale_fusable(c, nl)) {
+        // the rest-limb rescale inside the key switch (top limb first)
+        DevArr d32(static_cast<size_t>(cnt * item_bytes) / 2, S(P));
+        k2::mul_relin_rescale(c, *P->keys, xe->item(b0), xe->item(b0), o->item(b0), cnt, nl, prod.as<uint64_t>(),
+                              c2.as<uint64_t>(), d32.as<uint32_t>(), sc.as<int32_t>(), S(P));
+      } else {
+        k::square_relin(c, *P->keys, xe->item(b0), prod.as<uint64_t>(), cnt, nl, c2.as<uint64_t>(), S(P));
+        k::rescale(c, prod.as<uint64_t>(), o->item(b0), cnt * 2, nl, sc.as<int64_t>(), S(P));
+      }
       P->launches += 4;
     }
     acc = o;

@@ -404,6 +404,13 @@ void gemm(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* i
 void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, int64_t a_stride,
            int64_t b_stride, bool given_d, const uint64_t* c2, uint64_t* out, int64_t items, int nl, cudaStream_t s,
            bool d_in_out = false, bool digits = false, const uint32_t* d32 = nullptr);
+// multiply + relinearise + rescale with the rescale fused into the key switch (digit-row layouts,
+// top prime < 2^31).  Scratch: prod [items][2][nl][N], c2 (digit rows), d32 [items][2][nl][N] u32,
+// cen [items][2][N] int32.  out: [items][2][nl-1][N]
+bool relin_rescale_fusable(const Context& c, int nl);
+void mul_relin_rescale(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, uint64_t* out,
+                       int64_t items, int nl, uint64_t* prod, uint64_t* c2, uint32_t* d32, int32_t* cen,
+                       cudaStream_t s);
 
 // tcgen05 byte-split GEMM (hg_gemm_tc.cu).  Limbs are processed per residue
 // width (bytes = ceil(bits(q)/8)); weights pre-packed by pack_weights_tc for

@@ -724,13 +724,24 @@ __device__ __forceinline__ uint32_t neg_qinv32(uint32_t q) {
 
 
 // the key switch of CTA `vb` (k_relin_t passes blockIdx.x)
-template <typename W, int LOGN, bool GIVEN_D, bool SPLIT, bool DIG>
+// Fused rescale (RS): the key switch of limbs j < t = nl - 1 ends with the rescale of its own
+// output (poly_rescale, poly.hpp:190-228): out_j = (ks_j - NTT_j(lift(c))) q_t^{-1} mod q_j, where
+// c is the centred INTT of the top limb's key-switch output (computed before by a top-limb-only
+// launch and k_rescale_top_t).  The transform of the lift reuses the CTA's staged twiddles; the
+// un-rescaled output never goes to memory.
+struct RsArgs {
+  const int32_t* cen;  // [item][2][N] centred top-limb lift (q_t < 2^31)
+  uint64_t* out;       // [item][2][nl - 1][N] rescaled output
+  RescaleC R;
+};
+
+template <typename W, int LOGN, bool GIVEN_D, bool SPLIT, bool DIG, bool RS = false>
 __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, const uint64_t* __restrict__ b,
                                            int64_t a_stride, int64_t b_stride, const uint64_t* __restrict__ c2,
                                            const uint64_t* __restrict__ kval, const uint64_t* __restrict__ kpack,
                                            const uint32_t* __restrict__ kmont, uint64_t* out, int nl, int64_t items,
                                            int G, const RelinC& K, const LimbList& LL, const CtxParams& P,
-                                           const uint32_t* __restrict__ d32) {
+                                           const uint32_t* __restrict__ d32, const RsArgs& rs) {
   extern __shared__ __align__(16) uint64_t smem[];
   const int half = SPLIT ? (vb & 1) : 0;
   Cta<W, LOGN> c(smem, LL, items, G, P, false, SPLIT ? (vb >> 1) : vb, SPLIT ? half : -1);
@@ -1027,6 +1038,68 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
       }
     }
     // epilogue: + d0, d1; canonical store
+    if constexpr (RS) {
+      static_assert(DIG && GIVEN_D && GPT == 1, "fused rescale: digit-row key switch with given d0, d1");
+      const int vt = threadIdx.x, k0 = vt << 4;
+      // acc <- the canonical key-switch outputs (d0, d1 included)
+      if constexpr (D32) {
+        const uint32_t q32 = (uint32_t)Q;
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          acc0[0][r] = (W)csub<uint32_t>((uint32_t)acc0[0][r], q32);
+          acc1[0][r] = (W)csub<uint32_t>((uint32_t)acc1[0][r], q32);
+        }
+      } else {
+        const uint64_t* p0 = a + (int64_t)item * a_stride + (int64_t)j * nfull + hoff + k0;
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          const ulonglong2 v0 = reinterpret_cast<const ulonglong2*>(p0)[h];
+          const ulonglong2 v1 = reinterpret_cast<const ulonglong2*>(p0 + pw)[h];
+          const uint64_t dd0[2] = {v0.x, v0.y}, dd1[2] = {v1.x, v1.y};
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            uint64_t r0, r1;
+            if constexpr (std::is_floating_point_v<W>) {
+              r0 = (uint64_t)canon_f64((double)acc0[0][2 * h + e], q, q2);
+              r1 = (uint64_t)canon_f64((double)acc1[0][2 * h + e], q, q2);
+            } else {
+              r0 = (uint64_t)acc0[0][2 * h + e];
+              r1 = (uint64_t)acc1[0][2 * h + e];
+            }
+            acc0[0][2 * h + e] = (W)add_mod(r0, dd0[e], Q);
+            acc1[0][2 * h + e] = (W)add_mod(r1, dd1[e], Q);
+          }
+        }
+      }
+      const int t = nl - 1;
+      const uint64_t inv = rs.R.inv[j], inv_s = rs.R.inv_s[j];
+      const uint32_t inv_s32 = rs.R.inv_s32[j], mu32 = (uint32_t)((1ULL << 32) / Q);
+#pragma unroll 1
+      for (int p = 0; p < 2; ++p) {
+        const int32_t* cv = rs.cen + ((int64_t)item * 2 + p) * nfull;
+        if (p == 1) __syncthreads();  // the previous transform's last pass has read shared memory
+        lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
+          return ct_one<W>(lift_cen<W, int32_t>(__ldg(cv + k), *c.L, mu32),
+                           lift_cen<W, int32_t>(__ldg(cv + k + n), *c.L, mu32), psi1, q, q2);
+        }, c.tw, q, q2);
+        lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2);
+        W y[16];
+        lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, y);
+        ulonglong2* o2 = reinterpret_cast<ulonglong2*>(rs.out + (((int64_t)item * 2 + p) * t + j) * nfull + hoff + k0);
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          uint64_t v[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const W f = p ? acc1[0][2 * h + e] : acc0[0][2 * h + e];
+            v[e] = rescale_word<W>((uint64_t)f, (uint64_t)canon4<W>(y[2 * h + e], q, q2), Q, inv, inv_s, inv_s32);
+          }
+          o2[h] = make_ulonglong2(v[0], v[1]);
+        }
+      }
+      __syncthreads();  // shared memory reused by the next item
+      continue;
+    }
     if constexpr (D32) {
       if (use_d32) {  // d0, d1 already accumulated
 #pragma unroll
@@ -1111,15 +1184,15 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
   }
 }
 
-template <typename W, int LOGN, bool GIVEN_D, bool SPLIT = false, bool DIG = false>
+template <typename W, int LOGN, bool GIVEN_D, bool SPLIT = false, bool DIG = false, bool RS = false>
 __global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT, DIG>::threads, RelinCfg<W, LOGN, SPLIT, DIG>::min_blocks)
     k_relin_t(const uint64_t* a, const uint64_t* __restrict__ b, int64_t a_stride, int64_t b_stride,
               const uint64_t* __restrict__ c2, const uint64_t* __restrict__ kval,
               const uint64_t* __restrict__ kpack, const uint32_t* __restrict__ kmont, uint64_t* out,
               int nl, int64_t items, int G, const RelinC K, const LimbList LL, const CtxParams P,
-              const uint32_t* __restrict__ d32) {
-  relin_body<W, LOGN, GIVEN_D, SPLIT, DIG>((int)blockIdx.x, a, b, a_stride, b_stride, c2, kval, kpack, kmont, out, nl,
-                                      items, G, K, LL, P, d32);
+              const uint32_t* __restrict__ d32, const RsArgs rs) {
+  relin_body<W, LOGN, GIVEN_D, SPLIT, DIG, RS>((int)blockIdx.x, a, b, a_stride, b_stride, c2, kval, kpack, kmont, out,
+                                          nl, items, G, K, LL, P, d32, rs);
 }
 
 // ---------------------------------------------------------------------------
@@ -1272,7 +1345,12 @@ __global__ void __launch_bounds__(kGT) k_gemm_lz(const uint64_t* __restrict__ x,
                        ll = reduce128(acc[m][c][2], 0, L);
         r[c] = add_mod(add_mod(mul_mod(hh, c2b, L), mul_mod(md, cb, L), q), ll, q);
       } else {
-        r[c] = reduce128(acc[m][c][0], 0, L);
+        // q < 2^32: one 64-bit Barrett step (br_hi = floor(2^64 / q)); the estimate is at most
+        // 2 short, so two conditional subtractions give the canonical residue
+        const uint64_t a = acc[m][c][0];
+        uint64_t t = a - __umul64hi(a, L.br_hi) * q;
+        t = t >= q ? t - q : t;
+        r[c] = t >= q ? t - q : t;
       }
     }
     if (C == 1) {
@@ -1732,14 +1810,18 @@ bool relin_digits_ok(const Context& c, int nl) {
          classify(c, 0, nl, fp64_lane()).wide.count == 0;
 }
 
-void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, int64_t a_stride,
-           int64_t b_stride, bool given_d, const uint64_t* c2, uint64_t* out, int64_t items, int nl, cudaStream_t s,
-           bool d_in_out, bool digits, const uint32_t* d32) {
+// target limbs [lb, le) of the key switch; rs: fused rescale of those limbs (digit rows only)
+static void relin_impl(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, int64_t a_stride,
+                       int64_t b_stride, bool given_d, const uint64_t* c2, uint64_t* out, int64_t items, int nl,
+                       cudaStream_t s, bool d_in_out, bool digits, const uint32_t* d32, int lb, int le,
+                       const RsArgs* rs) {
   check(relin_supported(c), HG_EINTERNAL, "key switch: ring degree outside 2^10..2^15");
   check(!digits || relin_digits_ok(c, nl), HG_EINTERNAL, "key switch: digit rows outside the 2^13 half-row layout");
+  check(rs == nullptr || digits, HG_EINTERNAL, "fused rescale needs the digit-row key switch");
   if (items <= 0) return;
   const RelinC K = relin_consts(c, nl);
-  const Classes cl = classify(c, 0, nl, fp64_lane());
+  const Classes cl = classify(c, lb, le, fp64_lane());
+  const RsArgs rsa = rs ? *rs : RsArgs{};
   int sd = 0;
   for (int i = 0; i < nl; ++i) sd += c.digits(i);
   const double pw8 = (double)nl * c.n() * 8;
@@ -1747,7 +1829,7 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
     using W = decltype(wtag);
     if (LL.count == 0) return;
     by_logn<W>(c, [&]<typename W_, int LOGN>() {
-      auto go = [&]<bool SPLIT, bool DIG = false>() {
+      auto go = [&]<bool SPLIT, bool DIG = false, bool RS = false>() {
         constexpr int LT = SPLIT ? LOGN - 1 : LOGN;
         using Cf = RelinCfg<W_, LT, SPLIT, DIG>;
         const int threads = Cf::threads;
@@ -1763,21 +1845,26 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
         const uint32_t* dd32 = (in_out && sizeof(W_) == 4) ? d32 : nullptr;
         const uint64_t* aa = in_out ? out : a;
         const int64_t as = in_out ? 2LL * nl * c.n() : a_stride;
-        const void* fn = gd ? (const void*)k_relin_t<W_, LT, true, SPLIT, DIG>
+        const void* fn = gd ? (const void*)k_relin_t<W_, LT, true, SPLIT, DIG, RS>
                             : (const void*)k_relin_t<W_, LT, false, SPLIT, DIG>;
         set_smem_attr(fn, Cf::smem);
         const double frac = (double)LL.count / nl;
         // bytes: c2 + (a, b | d0, d1) + out once, key rows once; modmuls: digit NTTs + key MACs (+ tensor)
-        c.kt_begin(std::is_floating_point_v<W_> ? "k_relin_t/f64" : sizeof(W_) == 4 ? "k_relin_t/u32" : "k_relin_t/u64", s, frac * (items * pw8 * (gd ? 5 : 7) + (double)sd * 2 * pw8),
-                   (double)items * LL.count * (sd * (bfly(c) + 2.0 * c.n()) + (gd ? 0.0 : 3.0 * c.n())));
+        // RS: + the lift transform and the rescale product per poly; reads the lift, writes the
+        // rescaled limbs instead of the key-switch output
+        c.kt_begin(RS ? (std::is_floating_point_v<W_> ? "k_relin_rs_t/f64" : "k_relin_rs_t/u32")
+                      : (std::is_floating_point_v<W_> ? "k_relin_t/f64" : sizeof(W_) == 4 ? "k_relin_t/u32" : "k_relin_t/u64"),
+                   s, frac * (items * pw8 * (gd ? 5 : 7) + (double)sd * 2 * pw8) + (RS ? (double)items * 2 * c.n() * 4 : 0.0),
+                   (double)items * LL.count * (sd * (bfly(c) + 2.0 * c.n()) + (gd ? 0.0 : 3.0 * c.n()) +
+                                               (RS ? 2.0 * (bfly(c) + c.n()) : 0.0)));
         if (gd)
-          k_relin_t<W_, LT, true, SPLIT, DIG><<<grid, threads, Cf::smem, s>>>(
+          k_relin_t<W_, LT, true, SPLIT, DIG, RS><<<grid, threads, Cf::smem, s>>>(
               aa, b, as, b_stride, c2, keys.relin.as<uint64_t>(), keys.relin_pack.as<uint64_t>(),
-              keys.relin_mont.as<uint32_t>(), out, nl, items, G, K, LL, c.kp(), dd32);
-        else
+              keys.relin_mont.as<uint32_t>(), out, nl, items, G, K, LL, c.kp(), dd32, rsa);
+        else if constexpr (!RS)
           k_relin_t<W_, LT, false, SPLIT, DIG><<<grid, threads, Cf::smem, s>>>(
               a, b, a_stride, b_stride, c2, keys.relin.as<uint64_t>(), keys.relin_pack.as<uint64_t>(),
-              keys.relin_mont.as<uint32_t>(), out, nl, items, G, K, LL, c.kp(), nullptr);
+              keys.relin_mont.as<uint32_t>(), out, nl, items, G, K, LL, c.kp(), nullptr, rsa);
         c.kt_end(s);
         HG_CUDA(cudaGetLastError());
       };
@@ -1786,11 +1873,13 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
       // CTAs run two per SM, with their own barriers (relin_split13())
       if constexpr (LOGN == 15) go.template operator()<true>();
       else if constexpr (LOGN == 14 && !std::is_same_v<W_, uint64_t>) {
-        if (digits) go.template operator()<true, true>();
+        if (digits && rs) go.template operator()<true, true, true>();
+        else if (digits) go.template operator()<true, true>();
         else go.template operator()<true>();
       }
       else if constexpr (LOGN == 13 && !std::is_same_v<W_, uint64_t>) {
-        if (digits) go.template operator()<true, true>();
+        if (digits && rs) go.template operator()<true, true, true>();
+        else if (digits) go.template operator()<true, true>();
         else if (relin_split13()) go.template operator()<true>();
         else go.template operator()<false>();
       } else {
@@ -1802,6 +1891,75 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
   run(cl.small, uint32_t{}, lf.small());
   run(cl.fp, double{}, lf.fp());
   run(cl.wide, uint64_t{}, lf.wide());
+}
+
+void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, int64_t a_stride,
+           int64_t b_stride, bool given_d, const uint64_t* c2, uint64_t* out, int64_t items, int nl, cudaStream_t s,
+           bool d_in_out, bool digits, const uint32_t* d32) {
+  relin_impl(c, keys, a, b, a_stride, b_stride, given_d, c2, out, items, nl, s, d_in_out, digits, d32, 0, nl, nullptr);
+}
+
+// HG_RELIN_RESCALE=0: the x^2 node runs key switch and rescale as separate kernels
+static bool relin_rescale_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("HG_RELIN_RESCALE");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+bool relin_rescale_fusable(const Context& c, int nl) {
+  return relin_rescale_on() && nl >= 2 && relin_digits_ok(c, nl) && c.primes()[nl - 1] < (1ULL << 31);
+}
+
+// multiply (a, b) -> relinearise -> rescale with the rest-limb rescale fused into the key switch
+// (ckks_backend.hpp:261-281, 508-554; poly.hpp:190-228), top limb first:
+//   1. relin_c2: c2 digit rows, the tensor terms d0, d1 (u32 rows for 32-bit limbs, into prod else);
+//   2. the key switch of the top limb t alone -> prod (limb t);
+//   3. its centred INTT -> cen (k_rescale_top_t, int32 since q_t < 2^31);
+//   4. the key switch of limbs j < t ending in (ks_j - NTT_j(lift(cen))) q_t^{-1} -> out [items][2][t][N].
+// The un-rescaled limbs j < t are never written.  Bit-identical to multiply + relinearize + rescale.
+void mul_relin_rescale(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, uint64_t* out,
+                       int64_t items, int nl, uint64_t* prod, uint64_t* c2, uint32_t* d32, int32_t* cen,
+                       cudaStream_t s) {
+  check(relin_rescale_fusable(c, nl), HG_EINTERNAL, "fused key switch + rescale not available for this chain");
+  if (items <= 0) return;
+  const int64_t pw = (int64_t)nl * c.n();
+  const int t = nl - 1;
+  relin_c2(c, a, b, 2 * pw, 2 * pw, pw, pw, c2, items, nl, s, prod, true, d32);
+  relin_impl(c, keys, a, b, 2 * pw, 2 * pw, false, c2, prod, items, nl, s, true, true, d32, t, t + 1, nullptr);
+  {  // centred INTT of the top limb (rescale step 1)
+    const Classes top = classify(c, t, t + 1, fp64_lane());
+    const int64_t polys = items * 2;
+    const double nw = (double)c.n() * 8;
+    auto run_top = [&](const LimbList& LL, auto wtag) {
+      using W = decltype(wtag);
+      if (LL.count == 0) return;
+      by_logn<W>(c, [&]<typename W_, int LOGN>() {
+        using Cf = Cfg<W_, LOGN>;
+        unsigned grid;
+        int G;
+        grid_for<W_, LOGN>(LL, polys, grid, G);
+        set_smem_attr((const void*)k_rescale_top_t<W_, LOGN, int32_t>, Cf::smem);
+        c.kt_begin(std::is_floating_point_v<W_> ? "k_rescale_top_t/f64" : sizeof(W_) == 4 ? "k_rescale_top_t/u32" : "k_rescale_top_t/u64", s, 2.0 * polys * nw, (double)polys * bfly(c));
+        k_rescale_top_t<W_, LOGN, int32_t><<<grid, Cf::threads, Cf::smem, s>>>(prod, cen, nl, polys, G, LL, c.kp());
+        c.kt_end(s);
+        HG_CUDA(cudaGetLastError());
+      });
+    };
+    run_top(top.small, uint32_t{});
+    run_top(top.fp, double{});
+    run_top(top.wide, uint64_t{});
+  }
+  RsArgs rs{};
+  rs.cen = cen;
+  rs.out = out;
+  for (int j = 0; j < t; ++j) {
+    rs.R.inv[j] = c.inv_q(t, j);
+    rs.R.inv_s[j] = c.inv_q_shoup(t, j);
+    rs.R.inv_s32[j] = c.primes()[j] < (1ULL << 30) ? (uint32_t)((rs.R.inv[j] << 32) / c.primes()[j]) : 0;
+  }
+  relin_impl(c, keys, a, b, 2 * pw, 2 * pw, false, c2, prod, items, nl, s, true, true, d32, 0, t, &rs);
 }
 
 void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_stride, int64_t b_stride,
