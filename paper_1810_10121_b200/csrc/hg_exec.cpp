@@ -562,9 +562,13 @@ struct Val {
   std::shared_ptr<const HTensor> raw;
   std::shared_ptr<CtT> ct;
   std::shared_ptr<const ShardMap> shard;  // null: every element valid here
+  // a bound input encrypted straight into the layout of the Pad node it feeds (its only
+  // consumer): `ct` holds the padded tensor with the fill positions still unwritten
+  std::string prepad;
+  int64_t prepad_count = 0;  // the input's own element count (ExecProfile handles)
   bool is_raw() const { return raw != nullptr; }
   bool is_cipher() const { return ct != nullptr; }
-  int64_t handles() const { return ct ? ct->count : 0; }
+  int64_t handles() const { return ct ? (prepad.empty() ? ct->count : prepad_count) : 0; }
 };
 
 std::vector<int64_t> element_space(const std::vector<int64_t>& full, bool batched) {
@@ -626,6 +630,15 @@ struct NodeCache {
   std::vector<TcClass> tc;
 };
 
+// HG_PREPAD=0: bound inputs feeding a Pad are encrypted compactly and copied into place by the Pad
+bool prepad_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HG_PREPAD");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 // HG_GEMM_TC=0 disables the tcgen05 path (falls back to the IMAD GEMM, same results)
 bool tc_enabled() {
   static const bool on = [] {
@@ -677,6 +690,8 @@ struct hg_plan {
     std::shared_ptr<hg::DevArr> staged, pt;
     size_t staged_bytes = 0, pt_bytes = 0;
     std::shared_ptr<hg::CtT> ct;
+    std::shared_ptr<hg::DevArr> omap;  // input element -> position in the padded layout
+    int64_t padded = 0;                // padded element count (0: not pre-padded)
   };
   std::map<std::string, BindBufs> bind_bufs;
   std::map<std::string, hg::Val> outputs;
@@ -914,7 +929,7 @@ std::shared_ptr<DevArr> encode_columns(hg_plan* P, const std::vector<std::vector
 // Fresh encryptions of zero (or of per-item plaintexts) from per-item seeds
 // (ckks_backend.hpp:223-236, 470-490).
 void encrypt_items(hg_plan* P, const std::vector<uint64_t>& seeds, const uint64_t* pt, int level, uint64_t* out,
-                   const uint64_t* seeds_dev = nullptr, const int64_t* mcoef = nullptr) {
+                   const uint64_t* seeds_dev = nullptr, const int64_t* mcoef = nullptr, const int32_t* omap = nullptr) {
   const Context& c = *P->ctx;
   const int64_t n = c.n(), m = static_cast<int64_t>(seeds.size());
   if (m == 0) return;
@@ -924,7 +939,7 @@ void encrypt_items(hg_plan* P, const std::vector<uint64_t>& seeds, const uint64_
     deferred = &P->sample_flags[P->sample_flag_used++];
   k::sample_encryption_gpu(c, seeds.data(), m, d.as<int64_t>(), S(P), deferred, seeds_dev);
   // mcoef: plaintexts as signed coefficients, folded into the e0 transform (one NTT fewer)
-  k2::encrypt(c, *P->keys, d.as<int64_t>(), mcoef, pt, out, m, level + 1, S(P));
+  k2::encrypt(c, *P->keys, d.as<int64_t>(), mcoef, pt, out, m, level + 1, S(P), omap);
 }
 
 std::shared_ptr<CtT> new_ct(hg_plan* P, int64_t count, int level, double scale) {
@@ -1951,6 +1966,29 @@ Val gather(hg_plan* P, const std::vector<int64_t>& out_shape, bool out_batched, 
   return out;
 }
 
+// Pad element map (runtime.hpp:1804-1850): map[e] = the input element at padded position e, or -1
+// for a fill position
+std::vector<int64_t> pad_map(const GNode& node, const std::vector<int64_t>& in_full, bool batched,
+                             const std::vector<int64_t>& out_shape) {
+  const auto below = attr_ints(node, "pad_below");
+  const auto es = element_space(out_shape, batched);
+  std::vector<int64_t> map(static_cast<size_t>(prod(es)), -1);
+  for_each_index(es, [&](const std::vector<int64_t>& idx, int64_t flat) {
+    std::vector<int64_t> full;
+    if (batched) full.push_back(0);
+    full.insert(full.end(), idx.begin(), idx.end());
+    std::vector<int64_t> src = full;
+    for (size_t a = 0; a < src.size(); ++a) {
+      src[a] -= below[a];
+      if (src[a] < 0 || src[a] >= in_full[a]) return;
+    }
+    int64_t f = 0;
+    for (size_t a = batched ? 1 : 0; a < in_full.size(); ++a) f = f * in_full[a] + src[a];
+    map[flat] = f;
+  });
+  return map;
+}
+
 Val kernel_pad(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_shape, const Val& x) {
   check(x.is_cipher(), HG_EVALIDATION, "node '" + node.id + "': Pad of a plaintext tensor is not supported");
   const auto below = attr_ints(node, "pad_below"), above = attr_ints(node, "pad_above");
@@ -1961,21 +1999,8 @@ Val kernel_pad(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_sh
   const bool out_batched = x.batched;
   const auto es = element_space(out_shape, out_batched);
   const int64_t m_out = prod(es);
-  const auto& in_full = x.shape;
-  std::vector<int64_t> map(static_cast<size_t>(m_out), -1);
-  for_each_index(es, [&](const std::vector<int64_t>& idx, int64_t flat) {
-    std::vector<int64_t> full;
-    if (out_batched) full.push_back(0);
-    full.insert(full.end(), idx.begin(), idx.end());
-    std::vector<int64_t> src = full;
-    for (size_t a = 0; a < src.size(); ++a) {
-      src[a] -= below[a];
-      if (src[a] < 0 || src[a] >= in_full[a]) return;
-    }
-    int64_t f = 0;
-    for (size_t a = out_batched ? 1 : 0; a < in_full.size(); ++a) f = f * in_full[a] + src[a];
-    map[flat] = f;
-  });
+  const bool prepadded = x.prepad == node.id && x.ct->count == m_out;
+  const std::vector<int64_t> map = pad_map(node, x.shape, out_batched, out_shape);
   // fill elements: encrypt_zero_at(ref_level, ref_scale, node_rng.fork(e).next()) (runtime.hpp:1834-1838)
   const auto& xt = x.ct;
   const Context& c = *P->ctx;
@@ -2016,9 +2041,22 @@ Val kernel_pad(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_sh
     C.level = xt->level;
     C.local_count = xt->count;
   }
+  const int64_t ncopy = C.groups, nfill = static_cast<int64_t>(C.fill_pos.size());
+  if (prepadded) {
+    // the bound input already sits at its padded positions: encrypt the fills into the gaps
+    if (nfill > 0) {
+      std::vector<uint64_t> seeds(C.fill_pos.begin(), C.fill_pos.end());
+      encrypt_items(P, seeds, C.pt ? C.pt->as<uint64_t>() : nullptr, xt->level, xt->p, C.w->as<uint64_t>(), nullptr,
+                    C.oidx->as<int32_t>());
+    }
+    Val v;
+    v.shape = out_shape;
+    v.batched = out_batched;
+    v.ct = xt;
+    return v;
+  }
   // output = x's elements copied into place + the fresh fills (encrypted compactly, then placed)
   auto out = new_ct(P, m_out, xt->level, xt->scale);
-  const int64_t ncopy = C.groups, nfill = static_cast<int64_t>(C.fill_pos.size());
   k::scatter_items(c, xt->p, C.idx->as<int32_t>(), C.idx->as<int32_t>() + ncopy, out->p, ncopy, xt->item_words(), S(P));
   if (nfill > 0) {
     std::vector<uint64_t> seeds(C.fill_pos.begin(), C.fill_pos.end());
@@ -2889,21 +2927,61 @@ int hg_plan_bind_input(hg_plan* P, const char* param_id, const double* values, i
       bb.pt_bytes = pb;
     }
     hg::encode_coeffs(P, dvals, nb, P->batch, 1, nb, c.default_scale(), bb.pt->as<int64_t>());
+    // a Parameter whose only consumer is a Pad (and which is no graph output) is encrypted
+    // straight into the padded layout: the Pad then only encrypts its fills (no copy pass)
+    std::string pad_id;
+    {
+      int consumers = 0;
+      const hg::GNode* only = nullptr;
+      for (const auto& [nid, nd] : P->g.nodes)
+        for (const auto& in : nd.inputs)
+          if (in == param_id) {
+            ++consumers;
+            only = &nd;
+          }
+      const bool is_out = std::find(P->g.outputs.begin(), P->g.outputs.end(), param_id) != P->g.outputs.end();
+      if (consumers == 1 && only->op == hg::Op::Pad && !is_out && P->world == 1 && hg::prepad_enabled()) {
+        const auto below = hg::attr_ints(*only, "pad_below"), above = hg::attr_ints(*only, "pad_above");
+        if (below.size() == shape.size() && above.size() == shape.size() && below[0] == 0 && above[0] == 0)
+          pad_id = only->id;
+      }
+    }
+    int64_t count_ct = nb;
+    if (!pad_id.empty()) {
+      const hg::GNode& pn = P->g.nodes.at(pad_id);
+      auto oshape = shape;
+      const auto below = hg::attr_ints(pn, "pad_below"), above = hg::attr_ints(pn, "pad_above");
+      for (size_t a = 0; a < oshape.size(); ++a) oshape[a] += below[a] + above[a];
+      const auto map = hg::pad_map(pn, shape, true, oshape);
+      if (!bb.omap || bb.padded != static_cast<int64_t>(map.size())) {
+        std::vector<int32_t> om(static_cast<size_t>(nb), -1);
+        for (size_t e = 0; e < map.size(); ++e)
+          if (map[e] >= 0) om[static_cast<size_t>(map[e])] = static_cast<int32_t>(e);
+        bb.omap = std::make_shared<hg::DevArr>(om.size() * 4, hg::S(P));
+        HG_CUDA(cudaMemcpyAsync(bb.omap->p, om.data(), om.size() * 4, cudaMemcpyHostToDevice, hg::S(P)));
+        HG_CUDA(cudaStreamSynchronize(hg::S(P)));
+        bb.padded = static_cast<int64_t>(map.size());
+      }
+      count_ct = bb.padded;
+    }
     // the previous ciphertexts are rewritten in place when only the plan holds them (the
     // bound value and this cache); stream order puts the writes after earlier runs' reads
     auto bt = P->bound.find(param_id);
     const long holders = (bt != P->bound.end() && bt->second.ct == bb.ct) ? 2 : 1;
     std::shared_ptr<hg::CtT> ct;
-    if (bb.ct && bb.ct->count == nb && bb.ct->level == L && bb.ct.use_count() == holders &&
+    if (bb.ct && bb.ct->count == count_ct && bb.ct->level == L && bb.ct.use_count() == holders &&
         bb.ct->scale == c.default_scale())
       ct = bb.ct;
     else
-      ct = bb.ct = hg::new_ct(P, nb, L, c.default_scale());
-    hg::encrypt_items(P, seeds, nullptr, L, ct->p, nullptr, bb.pt->as<int64_t>());
+      ct = bb.ct = hg::new_ct(P, count_ct, L, c.default_scale());
+    hg::encrypt_items(P, seeds, nullptr, L, ct->p, nullptr, bb.pt->as<int64_t>(),
+                      pad_id.empty() ? nullptr : bb.omap->as<int32_t>());
     hg::Val v;
     v.shape = shape;
     v.batched = true;
     v.ct = ct;
+    v.prepad = pad_id;
+    v.prepad_count = nb;
     P->bound[param_id] = v;
   });
 }

@@ -386,7 +386,8 @@ void lift_ntt(const Context& c, const int64_t* src, uint64_t* out, int64_t items
 // fused encryption: samples [items][3][N] (u, e0, e1); mcoef [items][N] signed plaintext
 // coefficients or null; pt [items][nl][N] NTT-form plaintexts or null -> out [items][2][nl][N]
 void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const int64_t* mcoef, const uint64_t* pt,
-             uint64_t* out, int64_t items, int nl, cudaStream_t s);
+             uint64_t* out, int64_t items, int nl, cudaStream_t s,
+             const int32_t* omap = nullptr);
 void rescale(const Context& c, const uint64_t* in, uint64_t* out, int64_t polys, int nl, int64_t* cen, cudaStream_t s);
 void relin_c2(const Context& c, const uint64_t* a, const uint64_t* b, int64_t a_stride, int64_t b_stride,
               int64_t a1_off, int64_t b1_off, uint64_t* c2, int64_t items, int nl, cudaStream_t s,

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <type_traits>
 #include <vector>
@@ -356,23 +357,24 @@ __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_block
 //   16-byte chunks swizzled so a thread's 8 chunks of 16 consecutive words are conflict-free)
 // Group order per row r: [cen(r+1)] after the first pass, [x(r+1)] after the last pass; the
 // row loop waits for cen with wait_group 1 and for x right before the last pass.
-template <typename W, int LOGN, typename CT, bool SPLIT>
+template <typename W, int LOGN, typename CT, bool SPLIT, bool SC = true>
 struct RescalePCfg {
   static constexpr int n = 1 << LOGN, nfull = SPLIT ? 2 * n : n;
   static constexpr size_t c_off = Cfg<W, LOGN>::smem;
-  static constexpr size_t x_off = c_off + ((size_t)nfull * sizeof(CT) + 15) / 16 * 16;
+  // SC: the lift row is staged too; else the first pass reads it from L2 (it was just written)
+  static constexpr size_t x_off = c_off + (SC ? ((size_t)nfull * sizeof(CT) + 15) / 16 * 16 : 0);
   static constexpr size_t smem = x_off + (size_t)n * 8;
   static constexpr bool fits = Cfg<W, LOGN>::TWS && smem <= kSmemCap;
   static constexpr int min_blocks = 2 * smem <= kSmemCap ? 2 : 1;  // half rows of 2^13: two CTAs per SM
 };
 __device__ __forceinline__ int xslot(int c) { return c ^ ((c >> 3) & 7); }
 
-template <typename W, int LOGN, typename CT, bool SPLIT>
-__global__ void __launch_bounds__(Cfg<W, LOGN>::threads, (RescalePCfg<W, LOGN, CT, SPLIT>::min_blocks))
+template <typename W, int LOGN, typename CT, bool SPLIT, bool SC = true>
+__global__ void __launch_bounds__(Cfg<W, LOGN>::threads, (RescalePCfg<W, LOGN, CT, SPLIT, SC>::min_blocks))
     k_rescale_rest_p(const uint64_t* __restrict__ in, const CT* __restrict__ cen, uint64_t* __restrict__ out,
                      int nl, int64_t polys, int G, const LimbList LL, const RescaleC R, const CtxParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
-  using PC = RescalePCfg<W, LOGN, CT, SPLIT>;
+  using PC = RescalePCfg<W, LOGN, CT, SPLIT, SC>;
   constexpr int n = PC::n, nfull = PC::nfull, T = lz::lz_threads<LOGN>();
   const int half = SPLIT ? (int)(blockIdx.x & 1) : 0;
   Cta<W, LOGN> c(smem, LL, polys, G, P, false, SPLIT ? (int)(blockIdx.x >> 1) : -1, SPLIT ? half : -1);
@@ -386,6 +388,7 @@ __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, (RescalePCfg<W, LOGN, C
   CT* cbuf = reinterpret_cast<CT*>(reinterpret_cast<uint8_t*>(smem) + PC::c_off);
   uint4* xbuf = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(smem) + PC::x_off);
   auto stage_c = [&](int r) {
+    if constexpr (!SC) return;
     const uint4* g = reinterpret_cast<const uint4*>(cen + (int64_t)r * nfull);
     for (int ch = threadIdx.x; ch < nfull * (int)sizeof(CT) / 16; ch += T) cp_async16(reinterpret_cast<uint4*>(cbuf) + ch, g + ch);
     cp_async_commit();
@@ -401,18 +404,24 @@ __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, (RescalePCfg<W, LOGN, C
   }
   for (int r = c.r0; r < c.r1; ++r) {
     const bool more = r + 1 < c.r1;
-    asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // cen(r) landed (x(r) may be in flight)
+    if constexpr (SC) asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // cen(r) landed (x(r) may be in flight)
     __syncthreads();
+    const CT* cg = cen + (int64_t)r * nfull;  // !SC: the lift row from L2
+    (void)cg;
+    auto lift_at = [&](int k) -> CT {
+      if constexpr (SC) return cbuf[k];
+      else return __ldg(cg + k);
+    };
     if constexpr (SPLIT) {
       lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
-        return ct_one<W>(lift_cen<W, CT>(cbuf[k], *c.L, mu32), lift_cen<W, CT>(cbuf[k + n], *c.L, mu32), psi1, q, q2);
+        return ct_one<W>(lift_cen<W, CT>(lift_at(k), *c.L, mu32), lift_cen<W, CT>(lift_at(k + n), *c.L, mu32), psi1, q, q2);
       }, c.tw, q, q2);
     } else {
-      lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return lift_cen<W, CT>(cbuf[k], *c.L, mu32); }, c.tw, q, q2);
+      lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return lift_cen<W, CT>(lift_at(k), *c.L, mu32); }, c.tw, q, q2);
     }
     if (more) stage_c(r + 1);  // cbuf consumed (fwd_first_from ends with a barrier)
     lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2, [&] {
-      if (more) asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // x(r); cen(r+1) may be in flight
+      if (SC && more) asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // x(r); cen(r+1) may be in flight
       else cp_async_wait_all();
     });
     uint64_t* o = out + ((int64_t)r * t + j) * nfull + (int64_t)half * n;
@@ -493,7 +502,7 @@ __device__ __forceinline__ W lift_any(int64_t v, const LimbInfo& L, uint32_t mu3
 HG_KERNEL k_encrypt_t(const int64_t* __restrict__ samples, const int64_t* __restrict__ mcoef,
                       const uint64_t* __restrict__ pt, const uint64_t* __restrict__ pk, int64_t key_poly_words,
                       uint64_t* __restrict__ out, int nl, int64_t items, int G, const LimbList LL,
-                      const CtxParams P) {
+                      const CtxParams P, const int32_t* __restrict__ omap) {
   extern __shared__ __align__(16) uint64_t smem[];
   Cta<W, LOGN> c(smem, LL, items, G, P, false);
   constexpr int n = 1 << LOGN, T = lz::lz_threads<LOGN>(), GPT = (n >> 4) / T;
@@ -559,7 +568,9 @@ HG_KERNEL k_encrypt_t(const int64_t* __restrict__ samples, const int64_t* __rest
         }
       }
       __syncthreads();
-      lz::store<W, LOGN>(out + ((int64_t)r * 2 + p) * pw + (int64_t)j * n, c.s);
+      // omap: ciphertext r goes to item omap[r] of `out` (e.g. its position in a padded tensor)
+      const int64_t ro = omap ? (int64_t)omap[r] : (int64_t)r;
+      lz::store<W, LOGN>(out + (ro * 2 + p) * pw + (int64_t)j * n, c.s);
     }
     __syncthreads();
   }
@@ -1209,7 +1220,7 @@ constexpr int kGT = 256;  // threads per CTA
 constexpr int kKC = 32;   // terms staged per chunk
 constexpr int kTU = 4;    // terms unrolled per inner step (loads issued together)
 
-template <bool WIDE, int MT, int C>
+template <bool WIDE, int MT, int C, int TU = kTU>
 __global__ void __launch_bounds__(kGT) k_gemm_lz(const uint64_t* __restrict__ x, const int32_t* __restrict__ idx,
                                                  const uint64_t* __restrict__ w, int64_t w_group_stride,
                                                  const int32_t* __restrict__ oidx, uint64_t* __restrict__ out, int mg,
@@ -1235,7 +1246,7 @@ __global__ void __launch_bounds__(kGT) k_gemm_lz(const uint64_t* __restrict__ x,
   const uint64_t bmask = (1ull << b) - 1;
   // terms between folds: keeps every accumulator below 2^64
   const uint64_t Fq = WIDE ? ((1ull << 62) >> (2 * b)) : ((1ull << 63) / (q * q));
-  const int F = (int)max((uint64_t)kTU, min((uint64_t)1 << 30, Fq / kTU * kTU));
+  const int F = (int)max((uint64_t)TU, min((uint64_t)1 << 30, Fq / TU * TU));
   const uint64_t r32 = (1ull << 32) % q;
   int since = 0;
 
@@ -1266,9 +1277,9 @@ __global__ void __launch_bounds__(kGT) k_gemm_lz(const uint64_t* __restrict__ x,
     if (threadIdx.x < kKC) xs[threadIdx.x] = threadIdx.x < tc ? idx[g * kt + t0 + threadIdx.x] : idx[g * kt];
     __syncthreads();
     if (!live) continue;
-    const int tcu = (tc + kTU - 1) / kTU * kTU;
-    for (int f0 = 0; f0 < tcu; f0 += kTU) {
-      if (since + kTU > F) {
+    const int tcu = (tc + TU - 1) / TU * TU;
+    for (int f0 = 0; f0 < tcu; f0 += TU) {
+      if (since + TU > F) {
 #pragma unroll
         for (int m = 0; m < MT; ++m)
 #pragma unroll
@@ -1280,11 +1291,11 @@ __global__ void __launch_bounds__(kGT) k_gemm_lz(const uint64_t* __restrict__ x,
             }
         since = 0;
       }
-      since += kTU;
-      // issue the kTU term loads together, then the MACs
-      uint64_t xv[kTU][C];
+      since += TU;
+      // issue the TU term loads together, then the MACs
+      uint64_t xv[TU][C];
 #pragma unroll
-      for (int u = 0; u < kTU; ++u) {
+      for (int u = 0; u < TU; ++u) {
         const uint64_t* xp = xrow + (int64_t)xs[f0 + u] * item_words;
         if (C == 1) {
           xv[u][0] = __ldg(xp);
@@ -1298,7 +1309,7 @@ __global__ void __launch_bounds__(kGT) k_gemm_lz(const uint64_t* __restrict__ x,
         }
       }
 #pragma unroll
-      for (int u = 0; u < kTU; ++u) {
+      for (int u = 0; u < TU; ++u) {
         const int tt = f0 + u;
         if (WIDE) {
           uint32_t xl[C], xh[C];
@@ -1535,6 +1546,24 @@ static void set_smem_attr(const void* fn, size_t bytes) {
 }
 
 // rows per CTA so that the grid still covers every SM a few times over
+// Items per CTA when `rows` items are split into CTAs of G consecutive items per lane (limb x
+// half): the G in [1, gmax] minimising the per-slot critical path ceil(CTAs / slots) x G, i.e.
+// the wave quantisation of ceil(rows / G) x lanes CTAs on `slots` resident CTAs; ties go to the
+// larger G (fewer per-CTA twiddle stagings).
+static int pick_group(int64_t rows, int64_t lanes, int64_t slots, int gmax) {
+  int best = 1;
+  int64_t bc = INT64_MAX;
+  for (int g = 1; g <= gmax; ++g) {
+    const int64_t ctas = ((rows + g - 1) / g) * lanes;
+    const int64_t cost = ((ctas + slots - 1) / slots) * g;
+    if (cost <= bc) {
+      bc = cost;
+      best = g;
+    }
+  }
+  return best;
+}
+
 static int group_size(int64_t rows, int limbs, int ctas_per_sm) {
   const int64_t target = 148LL * ctas_per_sm * 3;
   int64_t g = (rows * limbs + target - 1) / target;
@@ -1619,7 +1648,7 @@ void lift_ntt(const Context& c, const int64_t* src, uint64_t* out, int64_t items
 }
 
 void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const int64_t* mcoef, const uint64_t* pt,
-             uint64_t* out, int64_t items, int nl, cudaStream_t s) {
+             uint64_t* out, int64_t items, int nl, cudaStream_t s, const int32_t* omap) {
   if (items <= 0) return;
   const Classes cl = classify(c, 0, nl, fp64_lane());
   const double nw = (double)c.n() * 8;
@@ -1638,7 +1667,7 @@ void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const i
                  (double)items * LL.count * (2 + (pt ? 1 : 0)) * nw + (double)items * (3 + (mcoef ? 1 : 0)) * nw,
                  (double)items * LL.count * (3 * bfly(c) + 2.0 * c.n()));
       k_encrypt_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(samples, mcoef, pt, keys.pk.as<uint64_t>(), kpw, out,
-                                                                nl, items, G, LL, c.kp());
+                                                                nl, items, G, LL, c.kp(), omap);
       c.kt_end(s);
       HG_CUDA(cudaGetLastError());
     });
@@ -1653,6 +1682,14 @@ void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const i
 static bool rescale_split13() {
   static const bool on = [] {
     const char* e = std::getenv("HG_RESCALE_SPLIT13");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+// HG_RESCALE_STAGE_LIFT=0: the half-row 2^13 rest-limb CTAs read the 32-bit lift from L2
+static bool rescale_stage_lift() {
+  static const bool on = [] {
+    const char* e = std::getenv("HG_RESCALE_STAGE_LIFT");
     return !(e && e[0] == '0');
   }();
   return on;
@@ -1693,20 +1730,19 @@ static void rescale_t(const Context& c, const uint64_t* in, uint64_t* out, int64
     by_logn<W>(c, [&]<typename W_, int LOGN>() {
       // pipelined variant: whole rows up to 2^13, half rows at 2^14 and (32-bit limbs with a
       // 32-bit lift, HG_RESCALE_SPLIT13) at 2^13, when it fits in shared memory
-      auto launch_p = [&]<int LP, bool SPL>() -> bool {
-        using PC = RescalePCfg<W_, LP, CT, SPL>;
+      auto launch_p = [&]<int LP, bool SPL, bool SC = true>() -> bool {
+        using PC = RescalePCfg<W_, LP, CT, SPL, SC>;
         if constexpr (!PC::fits) {
           return false;
         } else {
           const int halves = SPL ? 2 : 1;
-          const int64_t target = 148LL * 3;
-          const int G = (int)std::max<int64_t>(1, std::min<int64_t>(64, (polys * LL.count * halves + target - 1) / target));
+          const int G = pick_group(polys, (int64_t)LL.count * halves, 148LL * PC::min_blocks, 64);
           const unsigned grid = (unsigned)(LL.count * ((polys + G - 1) / G) * halves);
-          set_smem_attr((const void*)k_rescale_rest_p<W_, LP, CT, SPL>, PC::smem);
+          set_smem_attr((const void*)k_rescale_rest_p<W_, LP, CT, SPL, SC>, PC::smem);
           c.kt_begin(std::is_floating_point_v<W_> ? "k_rescale_rest_t/f64" : sizeof(W_) == 4 ? "k_rescale_rest_t/u32" : "k_rescale_rest_t/u64", s,
                      (double)polys * LL.count * (2 * nw + (double)c.n() * sizeof(CT)),
                      (double)polys * LL.count * (bfly(c) + c.n()));
-          k_rescale_rest_p<W_, LP, CT, SPL><<<grid, Cfg<W_, LP>::threads, PC::smem, s>>>(in, cen, out, nl, polys, G, LL,
+          k_rescale_rest_p<W_, LP, CT, SPL, SC><<<grid, Cfg<W_, LP>::threads, PC::smem, s>>>(in, cen, out, nl, polys, G, LL,
                                                                                       R, c.kp());
           c.kt_end(s);
           HG_CUDA(cudaGetLastError());
@@ -1717,7 +1753,13 @@ static void rescale_t(const Context& c, const uint64_t* in, uint64_t* out, int64
         if constexpr (LOGN == 14) {
           if (launch_p.template operator()<LOGN - 1, true>()) return;
         } else if constexpr (LOGN == 13 && sizeof(W_) == 4 && sizeof(CT) == 4) {
-          if (rescale_split13() ? launch_p.template operator()<12, true>() : launch_p.template operator()<13, false>())
+          if (rescale_split13() ? (rescale_stage_lift() ? launch_p.template operator()<12, true>()
+                                                        : launch_p.template operator()<12, true, false>())
+                                : launch_p.template operator()<13, false>())
+            return;
+        } else if constexpr (LOGN == 13 && sizeof(W_) == 4) {
+          // 64-bit lift (a wide top limb): half rows that read the lift from L2, two CTAs per SM
+          if (rescale_split13() ? launch_p.template operator()<12, true, false>() : launch_p.template operator()<13, false>())
             return;
         } else if constexpr (LOGN <= 13) {
           if (launch_p.template operator()<LOGN, false>()) return;
@@ -1833,10 +1875,8 @@ static void relin_impl(const Context& c, const Keys& keys, const uint64_t* a, co
         constexpr int LT = SPLIT ? LOGN - 1 : LOGN;
         using Cf = RelinCfg<W_, LT, SPLIT, DIG>;
         const int threads = Cf::threads;
-        const int64_t target = 148LL * 3;
         const int halves = SPLIT ? 2 : 1;
-        const int G = (int)std::max<int64_t>(
-            1, std::min<int64_t>(16, (items * LL.count * halves + target - 1) / target));
+        const int G = pick_group(items, (int64_t)LL.count * halves, 148LL * Cf::min_blocks, 16);
         const unsigned grid = (unsigned)(LL.count * ((items + G - 1) / G) * halves);
         // d_in_out: relin_c2 already wrote d0, d1 into `out` for this lane; add to them in place
         const bool in_out = !given_d && d_in_out && relin_d_in_out<W_, LOGN>();
@@ -2031,6 +2071,8 @@ void gemm(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* i
       else k_gemm_lz<true, 8, 1><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
     } else {
       if (MT == 4) k_gemm_lz<false, 4, 4><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
+      // 5 filters of 5 x 5 windows (CryptoNets conv): 5 terms per load batch, no padded terms
+      else if (MT == 5 && kt % 5 == 0 && kt <= kKC) k_gemm_lz<false, 5, 4, 5><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
       else if (MT == 5) k_gemm_lz<false, 5, 4><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
       else if (MT == 8) k_gemm_lz<false, 8, 4><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
       else k_gemm_lz<false, 16, 2><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
