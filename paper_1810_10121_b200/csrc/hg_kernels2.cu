@@ -1376,7 +1376,7 @@ __global__ void __launch_bounds__(kGT) k_gemm_lz(const uint64_t* __restrict__ x,
 // fp64-lane GEMM for 2^30 <= q < 2^50 (the same contract as k_gemm_lz): one exact
 // FMA-residual modmul (mulmod_f64) per MAC into a double accumulator, reduced every
 // F terms so |acc| stays below 2^52; canonicalised at the end.
-template <int MT, int C>
+template <int MT, int C, int TU = kTU>
 __global__ void __launch_bounds__(kGT) k_gemm_f64(const uint64_t* __restrict__ x, const int32_t* __restrict__ idx,
                                                   const uint64_t* __restrict__ w, int64_t w_group_stride,
                                                   const int32_t* __restrict__ oidx, uint64_t* __restrict__ out,
@@ -1416,19 +1416,19 @@ __global__ void __launch_bounds__(kGT) k_gemm_f64(const uint64_t* __restrict__ x
     if (threadIdx.x < kKC) xs[threadIdx.x] = threadIdx.x < tc ? idx[g * kt + t0 + threadIdx.x] : idx[g * kt];
     __syncthreads();
     if (!live) continue;
-    const int tcu = (tc + kTU - 1) / kTU * kTU;
-    for (int f0 = 0; f0 < tcu; f0 += kTU) {
-      if (since + kTU > F) {
+    const int tcu = (tc + TU - 1) / TU * TU;
+    for (int f0 = 0; f0 < tcu; f0 += TU) {
+      if (since + TU > F) {
 #pragma unroll
         for (int m = 0; m < MT; ++m)
 #pragma unroll
           for (int c = 0; c < C; ++c) acc[m][c] = reduce_f64(acc[m][c], q, qinv);
         since = 0;
       }
-      since += kTU;
-      double xv[kTU][C];
+      since += TU;
+      double xv[TU][C];
 #pragma unroll
-      for (int u = 0; u < kTU; ++u) {
+      for (int u = 0; u < TU; ++u) {
         const uint64_t* xp = xrow + (int64_t)xs[f0 + u] * item_words;
 #pragma unroll
         for (int c = 0; c < C; c += 2) {
@@ -1438,7 +1438,7 @@ __global__ void __launch_bounds__(kGT) k_gemm_f64(const uint64_t* __restrict__ x
         }
       }
 #pragma unroll
-      for (int u = 0; u < kTU; ++u) {
+      for (int u = 0; u < TU; ++u) {
 #pragma unroll
         for (int m = 0; m < MT; ++m) {
           const double wv = ws[f0 + u][m];
@@ -2094,6 +2094,7 @@ void gemm(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* i
     c.kt_begin("k_gemm_f64", s, frac * (in_items + (double)groups * mg) * item_bytes,
                frac * (double)groups * mg * kt * 2.0 * nl * n);
     if (MT == 4) k_gemm_f64<4, 2><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
+    else if (MT == 5 && kt % 5 == 0 && kt <= kKC) k_gemm_f64<5, 2, 5><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
     else if (MT == 5) k_gemm_f64<5, 2><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
     else k_gemm_f64<8, 2><<<grid, kGT, 0, s>>>(x, idx, w, w_group_stride, oidx, out, mg, kt, nl, LL, c.kp());
     c.kt_end(s);
