@@ -1381,7 +1381,7 @@ Val contraction(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_s
         tcc.limbs = limbs;
         std::vector<uint8_t> packed;
         k2::pack_weights_tc(wres, wgroups, lmg, kt, nl, limbs, bytes, k2::tc_ntile(bytes, lmg), packed,
-                            tcc.group_stride);
+                            tcc.group_stride, k2::tc_splitx(bytes), c.primes());
         if (w_shared) tcc.group_stride = 0;
         tcc.w = std::make_shared<DevArr>(packed.size(), S(P));
         HG_CUDA(cudaMemcpyAsync(tcc.w->p, packed.data(), packed.size(), cudaMemcpyHostToDevice, S(P)));

@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -103,12 +104,28 @@ constexpr int kATileBytes = kTcM * kTcK;  // 4 KB per byte plane
 template <int NT>
 constexpr int kBTileBytes = NT * kTcK;
 
-template <int XB, int WB, int NT>
+// SX (split x, residues of 5..7 bytes): x = x_lo + 2^32 x_hi with x_lo the planes 0..3 and x_hi the
+// planes 4..XB-1; the hi planes multiply the weight planes of w' = 2^32 w mod q, so
+//   x w = sum_{b<4} sum_a 2^8(a+b) x_b w_a + sum_{b>=4} sum_a 2^8(a+b-4) x_b w'_a  (mod q)
+// lands in S = WB + 3 shift groups instead of XB + WB - 1 (7-byte limbs: 10 instead of 13),
+// which lets the MMA N (TMEM columns S x NT <= 512) grow from 32 to 48 outputs.  Each group
+// still sums <= 7 byte products per term, so D_s < 7 K 2^16 < 2^31 for K <= 4096.
+template <int XB, int WB, bool SX>
+__host__ __device__ constexpr int tc_group(int a, int b) { return (SX && b >= 4) ? a + b - 4 : a + b; }
+template <int XB, int WB, bool SX>
+__host__ __device__ constexpr bool tc_first(int a, int b) {  // first (a, b) of the issue order in its group
+  for (int a2 = 0; a2 < WB; ++a2)
+    for (int b2 = 0; b2 < XB; ++b2)
+      if (tc_group<XB, WB, SX>(a2, b2) == tc_group<XB, WB, SX>(a, b)) return a2 == a && b2 == b;
+  return false;
+}
+
+template <int XB, int WB, int NT, bool SX = false>
 struct TcCfg {
-  static constexpr int S = XB + WB - 1;  // shift groups
+  static constexpr int S = SX ? WB + 3 : XB + WB - 1;  // shift groups
   static constexpr int COLS = S * NT <= 32 ? 32 : S * NT <= 64 ? 64 : S * NT <= 128 ? 128 : S * NT <= 256 ? 256 : 512;
   static constexpr int a_bytes = XB * kATileBytes;
-  static constexpr int w_bytes = WB * kBTileBytes<NT>;
+  static constexpr int w_bytes = (SX ? 2 : 1) * WB * kBTileBytes<NT>;  // SX: w then w' planes
   // A/W ring as deep as shared memory allows; loads run LOOK K steps ahead of the MMA
   // (L2 latency ~1-2 us vs ~0.3 us of MMA per step), a slot is refilled 2 steps after its MMA
   static constexpr int RING = (220 * 1024) / (a_bytes + w_bytes) < 12 ? (220 * 1024) / (a_bytes + w_bytes) : 12;
@@ -203,12 +220,12 @@ __device__ __forceinline__ TcTile tc_tile(int64_t t, int ntiles, int64_t ncol, i
 constexpr int kTcProducers = 224;
 constexpr int kTcThreadsWS = 512;  // + 8 epilogue warps: two per TMEM lane quadrant
 
-template <int XB, int WB, int NT>
+template <int XB, int WB, int NT, bool SX = false>
 __global__ void __launch_bounds__(kTcThreadsWS, 1)
     k_gemm_tc(const uint8_t* __restrict__ planes, const int32_t* __restrict__ idx, const uint8_t* __restrict__ wpk,
               const int32_t* __restrict__ oidx, uint64_t* __restrict__ out, int mg, int kt, int nl,
               const LimbListTc LL, int64_t groups, int64_t w_group_stride, const CtxParams P) {
-  using Cf = TcCfg<XB, WB, NT>;
+  using Cf = TcCfg<XB, WB, NT, SX>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cf::off_bar);
   uint64_t* empty = full + Cf::RING;
@@ -261,11 +278,11 @@ __global__ void __launch_bounds__(kTcThreadsWS, 1)
           for (int a = 0; a < WB; ++a) {
 #pragma unroll
             for (int b = 0; b < XB; ++b) {
-              const int sg = a + b;
-              const int a_first = sg - (XB - 1) > 0 ? sg - (XB - 1) : 0;  // first (a, b) pair reaching group sg
-              const uint32_t acc = (s > 0 || a != a_first) ? 1u : 0u;
+              const int sg = tc_group<XB, WB, SX>(a, b);
+              const int wpl = (SX && b >= 4) ? WB + a : a;  // SX: hi x planes meet the w' planes
+              const uint32_t acc = (s > 0 || !tc_first<XB, WB, SX>(a, b)) ? 1u : 0u;
               umma_i8(tmem + (uint32_t)(sg * NT), umma_desc(sa + b * kATileBytes, 1024, 128),
-                      umma_desc(sb + a * kBTileBytes<NT>, (NT / 8) * 128, 128), idesc, acc);
+                      umma_desc(sb + wpl * kBTileBytes<NT>, (NT / 8) * 128, 128), idesc, acc);
             }
           }
           umma_commit(&empty[slot]);
@@ -409,10 +426,12 @@ namespace k2 {
 // tensor-core GEMM: [group][limb_pos][n-tile][k-step][byte plane][NT x 32 bytes],
 // each NT x 32 block in the K-major core-matrix order the B descriptor expects.
 void pack_weights_tc(const std::vector<uint64_t>& wres, int64_t wgroups, int mg, int kt, int nl,
-                     const std::vector<int>& limbs, int WB, int NT, std::vector<uint8_t>& out, int64_t& group_stride) {
+                     const std::vector<int>& limbs, int WB, int NT, std::vector<uint8_t>& out, int64_t& group_stride,
+                     bool sx, const std::vector<uint64_t>& primes) {
   const int ntiles = (mg + NT - 1) / NT, ksteps = (kt + kTcK - 1) / kTcK;
   const int64_t block = (int64_t)NT * kTcK;
-  group_stride = (int64_t)limbs.size() * ntiles * ksteps * WB * block;
+  const int PL = sx ? 2 * WB : WB;  // SX: the planes of w, then those of w' = 2^32 w mod q
+  group_stride = (int64_t)limbs.size() * ntiles * ksteps * PL * block;
   out.assign(static_cast<size_t>(wgroups * group_stride), 0);
   for (int64_t g = 0; g < wgroups; ++g)
     for (size_t lp = 0; lp < limbs.size(); ++lp) {
@@ -424,9 +443,10 @@ void pack_weights_tc(const std::vector<uint64_t>& wres, int64_t wgroups, int mg,
           const int ks = t / kTcK, kk = t % kTcK;
           // core-matrix offset inside the NT x 32 block: n groups of 8 at 128 B, k chunks of 16 at NT/8*128 B
           const int64_t off = ((int64_t)(kk >> 4) * (NT / 8) + (nn >> 3)) * 128 + (nn & 7) * 16 + (kk & 15);
-          for (int a = 0; a < WB; ++a) {
-            const int64_t base = g * group_stride + ((((int64_t)lp * ntiles + ntile) * ksteps + ks) * WB + a) * block;
-            out[static_cast<size_t>(base + off)] = static_cast<uint8_t>(v >> (8 * a));
+          const uint64_t v2 = sx ? static_cast<uint64_t>((static_cast<unsigned __int128>(v) << 32) % primes[j]) : 0;
+          for (int a = 0; a < PL; ++a) {
+            const int64_t base = g * group_stride + ((((int64_t)lp * ntiles + ntile) * ksteps + ks) * PL + a) * block;
+            out[static_cast<size_t>(base + off)] = static_cast<uint8_t>((a < WB ? v : v2) >> (8 * (a % WB)));
           }
         }
       }
@@ -434,14 +454,14 @@ void pack_weights_tc(const std::vector<uint64_t>& wres, int64_t wgroups, int mg,
 }
 
 // byte planes of the input items, then one persistent GEMM launch per residue width
-template <int XB, int NT>
+template <int XB, int NT, bool SX = false>
 static void launch_tc(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* idx, const uint8_t* wpk,
                       int64_t w_group_stride, const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt,
                       int nl, const std::vector<int>& limbs, cudaStream_t s, double alg_bytes, double alg_macs) {
-  using Cf = TcCfg<XB, XB, NT>;
+  using Cf = TcCfg<XB, XB, NT, SX>;
   static bool attr = false;
   if (!attr) {
-    HG_CUDA(cudaFuncSetAttribute((const void*)k_gemm_tc<XB, XB, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    HG_CUDA(cudaFuncSetAttribute((const void*)k_gemm_tc<XB, XB, NT, SX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  Cf::smem));
     attr = true;
   }
@@ -465,8 +485,8 @@ static void launch_tc(const Context& c, const uint64_t* x, int64_t x_items, cons
   const int64_t tiles = (int64_t)ntiles * (n / kTcM) * 2 * groups * LL.count;
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
   c.kt_begin("k_gemm_tc", s, alg_bytes, alg_macs);
-  k_gemm_tc<XB, XB, NT><<<grid, kTcThreadsWS, Cf::smem, s>>>(planes, idx, wpk, oidx, out, mg, kt, nl, LL, groups,
-                                                         w_group_stride, c.kp());
+  k_gemm_tc<XB, XB, NT, SX><<<grid, kTcThreadsWS, Cf::smem, s>>>(planes, idx, wpk, oidx, out, mg, kt, nl, LL, groups,
+                                                             w_group_stride, c.kp());
   c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
@@ -485,8 +505,23 @@ bool gemm_tc_supported(const Context& c, int mg, int kt, int nl) {
 }
 
 int tc_bytes(const Context& c, int limb) { return limb_bytes(c.primes()[limb]); }
-// output tile: the smallest MMA N covering the outputs (fewer TMEM columns -> more CTAs per SM)
-int tc_ntile(int bytes, int mg) { return mg <= 16 ? 16 : (mg <= 32 || bytes > 4) ? 32 : 64; }
+// HG_TC_SPLITX=0: 5..7-byte residues without the split-x form (XB + WB - 1 shift groups)
+bool tc_splitx(int bytes) {
+  static const bool on = [] {
+    const char* e = std::getenv("HG_TC_SPLITX");
+    return !(e && e[0] == '0');
+  }();
+  return on && bytes >= 5;
+}
+// output tile: the smallest MMA N covering the outputs, capped by the TMEM columns S x N <= 512
+// (S = 7 for 4-byte residues; split-x: 8 / 9 / 10 for 5 / 6 / 7 bytes; else 2 bytes - 1)
+int tc_ntile(int bytes, int mg) {
+  if (mg <= 16) return 16;
+  if (mg <= 32) return 32;
+  if (bytes == 4) return 64;
+  if (tc_splitx(bytes)) return bytes == 5 ? 64 : 48;
+  return 32;
+}
 
 void gemm_tc(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* idx, const uint8_t* wpk,
              int64_t w_group_stride, const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt, int nl,
@@ -505,8 +540,20 @@ void gemm_tc(const Context& c, const uint64_t* x, int64_t x_items, const int32_t
     return;                                                                                           \
   }
   HG_TC(4, 16) HG_TC(4, 32) HG_TC(4, 64)
-  HG_TC(5, 16) HG_TC(5, 32) HG_TC(6, 16) HG_TC(6, 32) HG_TC(7, 16) HG_TC(7, 32)
+  if (!tc_splitx(bytes)) {
+    HG_TC(5, 16) HG_TC(5, 32) HG_TC(6, 16) HG_TC(6, 32) HG_TC(7, 16) HG_TC(7, 32)
+  }
 #undef HG_TC
+#define HG_TCX(B, NT)                                                                                       \
+  if (bytes == B && nt == NT) {                                                                             \
+    launch_tc<B, NT, true>(c, x, x_items, idx, wpk, w_group_stride, oidx, out, groups, mg, kt, nl, limbs, s, \
+                           frac * (in_items + (double)groups * mg) * item_bytes,                           \
+                           frac * (double)groups * mg * kt * 2.0 * nl * c.n() * B * B);                    \
+    return;                                                                                                 \
+  }
+  HG_TCX(5, 16) HG_TCX(5, 32) HG_TCX(5, 64) HG_TCX(6, 16) HG_TCX(6, 32) HG_TCX(6, 48)
+  HG_TCX(7, 16) HG_TCX(7, 32) HG_TCX(7, 48)
+#undef HG_TCX
   fail(HG_EINTERNAL, "tensor-core GEMM: unsupported residue width");
 }
 

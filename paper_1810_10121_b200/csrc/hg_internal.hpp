@@ -420,7 +420,9 @@ bool gemm_tc_supported(const Context& c, int mg, int kt, int nl);
 int tc_bytes(const Context& c, int limb);
 int tc_ntile(int bytes, int mg);
 void pack_weights_tc(const std::vector<uint64_t>& wres, int64_t wgroups, int mg, int kt, int nl,
-                     const std::vector<int>& limbs, int WB, int NT, std::vector<uint8_t>& out, int64_t& group_stride);
+                     const std::vector<int>& limbs, int WB, int NT, std::vector<uint8_t>& out, int64_t& group_stride,
+                     bool sx, const std::vector<uint64_t>& primes);
+bool tc_splitx(int bytes);
 void gemm_tc(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* idx, const uint8_t* wpk,
              int64_t w_group_stride, const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt, int nl,
              const std::vector<int>& limbs, int bytes, cudaStream_t s);

@@ -1852,6 +1852,14 @@ bool relin_digits_ok(const Context& c, int nl) {
          classify(c, 0, nl, fp64_lane()).wide.count == 0;
 }
 
+static int lane_slots() {
+  static const int v = [] {
+    const char* e = std::getenv("HG_LANE_SLOTS");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 // target limbs [lb, le) of the key switch; rs: fused rescale of those limbs (digit rows only)
 static void relin_impl(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, int64_t a_stride,
                        int64_t b_stride, bool given_d, const uint64_t* c2, uint64_t* out, int64_t items, int nl,
@@ -1876,7 +1884,11 @@ static void relin_impl(const Context& c, const Keys& keys, const uint64_t* a, co
         using Cf = RelinCfg<W_, LT, SPLIT, DIG>;
         const int threads = Cf::threads;
         const int halves = SPLIT ? 2 : 1;
-        const int G = pick_group(items, (int64_t)LL.count * halves, 148LL * Cf::min_blocks, 16);
+        // with two lanes in flight, HG_LANE_SLOTS=k sizes each lane's grid for k CTAs per SM, so
+        // the IMAD-bound 32-bit and DFMA-bound fp64 key switches can share every SM (A/B)
+        const int lanes_busy = (cl.small.count > 0) + (cl.fp.count > 0) + (cl.wide.count > 0);
+        const int slots_per_sm = (lanes_busy > 1 && lane_slots() > 0) ? lane_slots() : Cf::min_blocks;
+        const int G = pick_group(items, (int64_t)LL.count * halves, 148LL * slots_per_sm, 64);
         const unsigned grid = (unsigned)(LL.count * ((items + G - 1) / G) * halves);
         // d_in_out: relin_c2 already wrote d0, d1 into `out` for this lane; add to them in place
         const bool in_out = !given_d && d_in_out && relin_d_in_out<W_, LOGN>();
