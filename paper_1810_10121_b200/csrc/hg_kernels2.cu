@@ -1590,7 +1590,7 @@ template <typename W, int LOGN>
 static void grid_for(const LimbList& LL, int64_t rows, unsigned& grid, int& G) {
   using Cf = Cfg<W, LOGN>;
   const int per_sm = std::max<int>(1, (int)(kSmemCap / Cf::smem));
-  G = group_size(rows, LL.count, std::min(per_sm, 2));
+  G = pick_group(rows, LL.count, 148LL * std::min(per_sm, 2), 16);
   grid = (unsigned)(LL.count * ((rows + G - 1) / G));
 }
 
@@ -1888,7 +1888,7 @@ static void relin_impl(const Context& c, const Keys& keys, const uint64_t* a, co
         // the IMAD-bound 32-bit and DFMA-bound fp64 key switches can share every SM (A/B)
         const int lanes_busy = (cl.small.count > 0) + (cl.fp.count > 0) + (cl.wide.count > 0);
         const int slots_per_sm = (lanes_busy > 1 && lane_slots() > 0) ? lane_slots() : Cf::min_blocks;
-        const int G = pick_group(items, (int64_t)LL.count * halves, 148LL * slots_per_sm, 64);
+        const int G = pick_group(items, (int64_t)LL.count * halves, 148LL * slots_per_sm, 16);
         const unsigned grid = (unsigned)(LL.count * ((items + G - 1) / G) * halves);
         // d_in_out: relin_c2 already wrote d0, d1 into `out` for this lane; add to them in place
         const bool in_out = !given_d && d_in_out && relin_d_in_out<W_, LOGN>();
