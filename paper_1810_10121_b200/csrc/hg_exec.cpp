@@ -566,6 +566,13 @@ struct Val {
   // consumer): `ct` holds the padded tensor with the fill positions still unwritten
   std::string prepad;
   int64_t prepad_count = 0;  // the input's own element count (ExecProfile handles)
+  // byte planes of `ct` for a consuming tcgen05 GEMM, written by the producer (fused x^2):
+  // residue width -> (plane buffer, limbs of that width); valid while `ct` is this tensor
+  struct Planes {
+    const void* of = nullptr;
+    std::map<int, std::pair<std::shared_ptr<DevArr>, std::vector<int>>> cls;
+  };
+  std::shared_ptr<Planes> planes;
   bool is_raw() const { return raw != nullptr; }
   bool is_cipher() const { return ct != nullptr; }
   int64_t handles() const { return ct ? (prepad.empty() ? ct->count : prepad_count) : 0; }
@@ -629,6 +636,15 @@ struct NodeCache {
   };
   std::vector<TcClass> tc;
 };
+
+// HG_PLANES_FUSION=0: the Dot after a fused x^2 splits its input into byte planes itself
+bool planes_fusion_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("HG_PLANES_FUSION");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 // HG_PREPAD=0: bound inputs feeding a Pad are encrypted compactly and copied into place by the Pad
 bool prepad_enabled() {
@@ -1396,9 +1412,16 @@ Val contraction(hg_plan* P, const GNode& node, const std::vector<int64_t>& out_s
   auto run_gemm = [&](uint64_t* accp) {
     if (C.local_count == 0) return;  // nothing assigned to this rank
     if (!C.tc.empty()) {
-      for (const auto& tcc : C.tc)
+      for (const auto& tcc : C.tc) {
+        // byte planes written by x's producer (fused x^2) when they describe exactly this class
+        const uint8_t* given = nullptr;
+        if (x.planes && x.planes->of == xt.get()) {
+          auto it = x.planes->cls.find(tcc.bytes);
+          if (it != x.planes->cls.end() && it->second.second == tcc.limbs) given = it->second.first->as<uint8_t>();
+        }
         k2::gemm_tc(c, xt->p, xt->count, C.idx->as<int32_t>(), tcc.w->as<uint8_t>(), tcc.group_stride,
-                    C.oidx->as<int32_t>(), accp, lg, lmg, kt, level + 1, tcc.limbs, tcc.bytes, S(P));
+                    C.oidx->as<int32_t>(), accp, lg, lmg, kt, level + 1, tcc.limbs, tcc.bytes, S(P), given);
+      }
       P->launches += static_cast<int64_t>(C.tc.size());
     } else {
       k::gemm_groups(c, xt->p, xt->count, C.idx->as<int32_t>(), C.w->as<uint64_t>(), C.w_group_stride,
@@ -1615,6 +1638,7 @@ Val kernel_poly_act(hg_plan* P, const GNode& node, const std::vector<int64_t>& o
     return o;
   };
   std::shared_ptr<CtT> acc;
+  std::shared_ptr<Val::Planes> planes_out;
   if (x.shard && P->world > 1) {
     // sharded x^2 (keeps_shard): multiply_rescale on this rank's element ranges only
     check(a == 1.0 && b == 0.0 && cc == 0.0, HG_EINTERNAL, "sharded polynomial activation must be x^2");
@@ -1646,6 +1670,46 @@ Val kernel_poly_act(hg_plan* P, const GNode& node, const std::vector<int64_t>& o
     const double dropped = static_cast<double>(c.primes()[level]);
     auto o = new_ct(P, m, level - 1, xe->scale * xe->scale / dropped);
     const int64_t item_bytes = static_cast<int64_t>(2) * nl * c.n() * 8;
+    // x^2 feeding (through Reshapes) a tensor-core Dot: the fused kernel writes the GEMM's byte
+    // planes of its output as well, so the Dot skips k_split_planes
+    std::shared_ptr<Val::Planes> planes;
+    if (a == 1.0 && b == 0.0 && cc == 0.0 && P->world == 1 && k2::relin_rescale_fusable(c, nl) &&
+        tc_enabled() && planes_fusion_enabled()) {
+      const GNode* cur = &node;
+      const GNode* dot = nullptr;
+      for (int hop = 0; hop < 4 && !dot; ++hop) {
+        const GNode* only = nullptr;
+        int users = 0;
+        for (const auto& [nid, nd] : P->g.nodes)
+          for (const auto& in : nd.inputs)
+            if (in == cur->id) {
+              ++users;
+              only = &nd;
+            }
+        const bool is_out = std::find(P->g.outputs.begin(), P->g.outputs.end(), cur->id) != P->g.outputs.end();
+        if (users != 1 || is_out) break;
+        if (only->op == Op::Reshape) cur = only;
+        else if (only->op == Op::Dot && only->inputs.size() == 2 && only->inputs[0] == cur->id) dot = only;
+        else break;
+      }
+      if (dot) {
+        const GNode& wn = P->g.nodes.at(dot->inputs[1]);
+        if (wn.op == Op::Constant && wn.data && wn.data->shape.size() == 2) {
+          const int kt = static_cast<int>(wn.data->shape[0]), mg = static_cast<int>(wn.data->shape[1]);
+          const int onl = level;  // the output's limbs (level - 1 + 1)
+          if (mg >= tc_min_outputs() && kt >= tc_min_terms() && k2::gemm_tc_supported(c, mg, kt, onl)) {
+            planes = std::make_shared<Val::Planes>();
+            std::map<int, std::vector<int>> by_bytes;
+            for (int j = 0; j < onl; ++j) by_bytes[k2::tc_bytes(c, j)].push_back(j);
+            for (auto& [bytes, limbs] : by_bytes)
+              planes->cls[bytes] = {std::make_shared<DevArr>(static_cast<size_t>(m) * 2 * limbs.size() * c.n() * bytes,
+                                                             S(P)),
+                                    limbs};
+            planes->of = o.get();
+          }
+        }
+      }
+    }
     const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(m, (int64_t(4) << 30) / item_bytes));
     for (int64_t b0 = 0; b0 < m; b0 += chunk) {
       const int64_t cnt = std::min(chunk, m - b0);
@@ -1655,8 +1719,19 @@ Val kernel_poly_act(hg_plan* P, const GNode& node, const std::vector<int64_t>& o
       if (k2::relin_rescale_fusable(c, nl)) {
         // the rest-limb rescale inside the key switch (top limb first)
         DevArr d32(static_cast<size_t>(cnt * item_bytes) / 2, S(P));
+        k2::RsPlanes rp;
+        if (planes)
+          for (const auto& [bytes, pr] : planes->cls)
+            for (size_t lp = 0; lp < pr.second.size(); ++lp) {
+              const int j = pr.second[lp];
+              const int64_t nlc = static_cast<int64_t>(pr.second.size());
+              rp.base[j] = pr.first->as<uint8_t>() + b0 * 2 * nlc * c.n() * bytes;  // this chunk's items
+              rp.lp[j] = static_cast<int>(lp);
+              rp.nlc[j] = static_cast<int>(nlc);
+              rp.xb[j] = bytes;
+            }
         k2::mul_relin_rescale(c, *P->keys, xe->item(b0), xe->item(b0), o->item(b0), cnt, nl, prod.as<uint64_t>(),
-                              c2.as<uint64_t>(), d32.as<uint32_t>(), sc.as<int32_t>(), S(P));
+                              c2.as<uint64_t>(), d32.as<uint32_t>(), sc.as<int32_t>(), S(P), planes ? &rp : nullptr);
       } else {
         k::square_relin(c, *P->keys, xe->item(b0), prod.as<uint64_t>(), cnt, nl, c2.as<uint64_t>(), S(P));
         k::rescale(c, prod.as<uint64_t>(), o->item(b0), cnt * 2, nl, sc.as<int64_t>(), S(P));
@@ -1664,6 +1739,7 @@ Val kernel_poly_act(hg_plan* P, const GNode& node, const std::vector<int64_t>& o
       P->launches += 4;
     }
     acc = o;
+    if (planes && a == 1.0 && b == 0.0 && cc == 0.0) planes_out = planes;
     if (a == -1.0) acc = negate_t(acc);
     else if (a != 1.0) acc = mul_const_rescale(acc, a, static_cast<double>(c.primes()[acc->level]));
     if (b != 0.0) {
@@ -1723,6 +1799,7 @@ Val kernel_poly_act(hg_plan* P, const GNode& node, const std::vector<int64_t>& o
   out.shape = out_shape;
   out.batched = x.batched;
   out.ct = acc;
+  out.planes = planes_out;
   return out;
 }
 
@@ -2326,6 +2403,7 @@ Val kernel_rearrange(hg_plan* P, const GNode& node, const std::vector<int64_t>& 
     out.batched = out_batched;
     out.ct = x.ct;  // handle copy: zero-copy view
     out.shard = x.shard;  // same element order: ownership carries over
+    out.planes = x.planes;
     return out;
   }
   const auto es = element_space(out_shape, out_batched);

@@ -457,7 +457,8 @@ void pack_weights_tc(const std::vector<uint64_t>& wres, int64_t wgroups, int mg,
 template <int XB, int NT, bool SX = false>
 static void launch_tc(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* idx, const uint8_t* wpk,
                       int64_t w_group_stride, const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt,
-                      int nl, const std::vector<int>& limbs, cudaStream_t s, double alg_bytes, double alg_macs) {
+                      int nl, const std::vector<int>& limbs, cudaStream_t s, double alg_bytes, double alg_macs,
+                      const uint8_t* planes_given) {
   using Cf = TcCfg<XB, XB, NT, SX>;
   static bool attr = false;
   if (!attr) {
@@ -470,10 +471,12 @@ static void launch_tc(const Context& c, const uint64_t* x, int64_t x_items, cons
   for (size_t i = 0; i < limbs.size(); ++i) LL.limb[i] = limbs[i];
   const int64_t n = c.n();
   const size_t plane_bytes = (size_t)x_items * 2 * LL.count * n * XB;
-  uint8_t* planes = static_cast<uint8_t*>(const_cast<Context&>(c).scratch(plane_bytes, 11));
+  // planes_given: the producer of x (the fused key switch + rescale) already wrote them
+  uint8_t* planes = planes_given ? const_cast<uint8_t*>(planes_given)
+                                 : static_cast<uint8_t*>(const_cast<Context&>(c).scratch(plane_bytes, 11));
   int sms = 148;
   HG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device()));
-  {
+  if (!planes_given) {
     const int64_t work = x_items * 2 * LL.count * (n / 4);
     const unsigned blocks = (unsigned)std::min<int64_t>((work + 255) / 256, (int64_t)sms * 16);
     c.kt_begin("k_split_planes", s, (double)x_items * 2 * LL.count * n * (8 + XB), 0.0);
@@ -525,7 +528,7 @@ int tc_ntile(int bytes, int mg) {
 
 void gemm_tc(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* idx, const uint8_t* wpk,
              int64_t w_group_stride, const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt, int nl,
-             const std::vector<int>& limbs, int bytes, cudaStream_t s) {
+             const std::vector<int>& limbs, int bytes, cudaStream_t s, const uint8_t* planes_given) {
   // algorithmic work of the tensor-core launch: u8 x u8 MACs (residue MACs x bytes^2), the
   // unit the i8 tensor peak is quoted in
   const double item_bytes = 2.0 * nl * c.n() * 8;
@@ -536,7 +539,7 @@ void gemm_tc(const Context& c, const uint64_t* x, int64_t x_items, const int32_t
   if (bytes == B && nt == NT) {                                                                       \
     launch_tc<B, NT>(c, x, x_items, idx, wpk, w_group_stride, oidx, out, groups, mg, kt, nl, limbs, s, \
                      frac * (in_items + (double)groups * mg) * item_bytes,                            \
-                     frac * (double)groups * mg * kt * 2.0 * nl * c.n() * B * B);                     \
+                     frac * (double)groups * mg * kt * 2.0 * nl * c.n() * B * B, planes_given);       \
     return;                                                                                           \
   }
   HG_TC(4, 16) HG_TC(4, 32) HG_TC(4, 64)
@@ -548,7 +551,7 @@ void gemm_tc(const Context& c, const uint64_t* x, int64_t x_items, const int32_t
   if (bytes == B && nt == NT) {                                                                             \
     launch_tc<B, NT, true>(c, x, x_items, idx, wpk, w_group_stride, oidx, out, groups, mg, kt, nl, limbs, s, \
                            frac * (in_items + (double)groups * mg) * item_bytes,                           \
-                           frac * (double)groups * mg * kt * 2.0 * nl * c.n() * B * B);                    \
+                           frac * (double)groups * mg * kt * 2.0 * nl * c.n() * B * B, planes_given);      \
     return;                                                                                                 \
   }
   HG_TCX(5, 16) HG_TCX(5, 32) HG_TCX(5, 64) HG_TCX(6, 16) HG_TCX(6, 32) HG_TCX(6, 48)

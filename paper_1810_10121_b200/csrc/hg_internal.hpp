@@ -409,9 +409,15 @@ void relin(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t
 // top prime < 2^31).  Scratch: prod [items][2][nl][N], c2 (digit rows), d32 [items][2][nl][N] u32,
 // cen [items][2][N] int32.  out: [items][2][nl-1][N]
 bool relin_rescale_fusable(const Context& c, int nl);
+// byte planes of the rescaled output written by the fused kernel for a consuming tcgen05 GEMM:
+// per output limb j the (chunk-offset) class buffer, position in the class, class size, width
+struct RsPlanes {
+  uint8_t* base[HG_MAX_LIMBS] = {};
+  int lp[HG_MAX_LIMBS] = {}, nlc[HG_MAX_LIMBS] = {}, xb[HG_MAX_LIMBS] = {};
+};
 void mul_relin_rescale(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, uint64_t* out,
                        int64_t items, int nl, uint64_t* prod, uint64_t* c2, uint32_t* d32, int32_t* cen,
-                       cudaStream_t s);
+                       cudaStream_t s, const RsPlanes* planes = nullptr);
 
 // tcgen05 byte-split GEMM (hg_gemm_tc.cu).  Limbs are processed per residue
 // width (bytes = ceil(bits(q)/8)); weights pre-packed by pack_weights_tc for
@@ -425,7 +431,8 @@ void pack_weights_tc(const std::vector<uint64_t>& wres, int64_t wgroups, int mg,
 bool tc_splitx(int bytes);
 void gemm_tc(const Context& c, const uint64_t* x, int64_t x_items, const int32_t* idx, const uint8_t* wpk,
              int64_t w_group_stride, const int32_t* oidx, uint64_t* out, int64_t groups, int mg, int kt, int nl,
-             const std::vector<int>& limbs, int bytes, cudaStream_t s);
+             const std::vector<int>& limbs, int bytes, cudaStream_t s,
+             const uint8_t* planes_given = nullptr);
 }  // namespace k2
 
 }  // namespace hg

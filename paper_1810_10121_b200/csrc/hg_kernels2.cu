@@ -744,6 +744,11 @@ struct RsArgs {
   const int32_t* cen;  // [item][2][N] centred top-limb lift (q_t < 2^31)
   uint64_t* out;       // [item][2][nl - 1][N] rescaled output
   RescaleC R;
+  // optional byte planes of the rescaled output for the tensor-core GEMM that consumes it
+  // (k_split_planes layout, hg_gemm_tc.cu): per output limb j the plane buffer of its residue
+  // width class (null: none), its position in the class and the class's limb count and width
+  uint8_t* pl_base[HG_MAX_LIMBS];
+  int pl_lp[HG_MAX_LIMBS], pl_nlc[HG_MAX_LIMBS], pl_xb[HG_MAX_LIMBS];
 };
 
 template <typename W, int LOGN, bool GIVEN_D, bool SPLIT, bool DIG, bool RS = false>
@@ -1097,15 +1102,31 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
         W y[16];
         lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, y);
         ulonglong2* o2 = reinterpret_cast<ulonglong2*>(rs.out + (((int64_t)item * 2 + p) * t + j) * nfull + hoff + k0);
+        uint64_t v[16];
 #pragma unroll
         for (int h = 0; h < 8; ++h) {
-          uint64_t v[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const W f = p ? acc1[0][2 * h + e] : acc0[0][2 * h + e];
-            v[e] = rescale_word<W>((uint64_t)f, (uint64_t)canon4<W>(y[2 * h + e], q, q2), Q, inv, inv_s, inv_s32);
+            v[2 * h + e] =
+                rescale_word<W>((uint64_t)f, (uint64_t)canon4<W>(y[2 * h + e], q, q2), Q, inv, inv_s, inv_s32);
           }
-          o2[h] = make_ulonglong2(v[0], v[1]);
+          o2[h] = make_ulonglong2(v[2 * h], v[2 * h + 1]);
+        }
+        if (rs.pl_base[j] != nullptr) {  // the consumer GEMM's byte planes, 16 bytes per plane
+          const int xb = rs.pl_xb[j];
+          const int64_t col = hoff + k0;
+          uint8_t* pb = rs.pl_base[j] + (((int64_t)item * 2 + p) * rs.pl_nlc[j] + rs.pl_lp[j]) * nfull * xb +
+                        (col >> 7) * xb * 128 + (col & 127);
+          for (int b = 0; b < xb; ++b) {
+            uint32_t wv[4];
+#pragma unroll
+            for (int w4 = 0; w4 < 4; ++w4)
+              wv[w4] = (uint32_t)((v[4 * w4] >> (8 * b)) & 0xFF) | ((uint32_t)((v[4 * w4 + 1] >> (8 * b)) & 0xFF) << 8) |
+                       ((uint32_t)((v[4 * w4 + 2] >> (8 * b)) & 0xFF) << 16) |
+                       ((uint32_t)((v[4 * w4 + 3] >> (8 * b)) & 0xFF) << 24);
+            *reinterpret_cast<uint4*>(pb + b * 128) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+          }
         }
       }
       __syncthreads();  // shared memory reused by the next item
@@ -1973,7 +1994,7 @@ bool relin_rescale_fusable(const Context& c, int nl) {
 // The un-rescaled limbs j < t are never written.  Bit-identical to multiply + relinearize + rescale.
 void mul_relin_rescale(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, uint64_t* out,
                        int64_t items, int nl, uint64_t* prod, uint64_t* c2, uint32_t* d32, int32_t* cen,
-                       cudaStream_t s) {
+                       cudaStream_t s, const RsPlanes* planes) {
   check(relin_rescale_fusable(c, nl), HG_EINTERNAL, "fused key switch + rescale not available for this chain");
   if (items <= 0) return;
   const int64_t pw = (int64_t)nl * c.n();
@@ -2006,6 +2027,13 @@ void mul_relin_rescale(const Context& c, const Keys& keys, const uint64_t* a, co
   RsArgs rs{};
   rs.cen = cen;
   rs.out = out;
+  if (planes)
+    for (int j = 0; j < t; ++j) {
+      rs.pl_base[j] = planes->base[j];
+      rs.pl_lp[j] = planes->lp[j];
+      rs.pl_nlc[j] = planes->nlc[j];
+      rs.pl_xb[j] = planes->xb[j];
+    }
   for (int j = 0; j < t; ++j) {
     rs.R.inv[j] = c.inv_q(t, j);
     rs.R.inv_s[j] = c.inv_q_shoup(t, j);

@@ -29,7 +29,7 @@ cap() {  # name kernel-regex launches-to-skip traffic-key workload-command...
 }
 B="python bench.py --steps 1 --warmup 1 --no-cpu"
 cap ${R}_ncu_relin_u32 k_relin_t 1 k_relin_rs_t/u32 $B
-cap ${R}_ncu_relin_f64 k_relin_t 1 k_relin_t/f64 $B
+cap ${R}_ncu_relin_f64 k_relin_t 2 k_relin_rs_t/f64 $B
 cap ${R}_ncu_rescale_u32 k_rescale_rest 0 k_rescale_rest_t/u32 $B
 cap ${R}_ncu_gemm_tc k_gemm_tc 0 k_gemm_tc $B
 cap ${R}_ncu_gemm_lz k_gemm_lz 0 k_gemm_lz $B
