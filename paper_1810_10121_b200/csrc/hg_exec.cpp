@@ -953,9 +953,10 @@ void encrypt_items(hg_plan* P, const std::vector<uint64_t>& seeds, const uint64_
   int* deferred = nullptr;
   if (P->in_run && !P->sync_sampling && P->sample_flag_used < P->sample_flag_cap)
     deferred = &P->sample_flags[P->sample_flag_used++];
-  k::sample_encryption_gpu(c, seeds.data(), m, d.as<int64_t>(), S(P), deferred, seeds_dev);
-  // mcoef: plaintexts as signed coefficients, folded into the e0 transform (one NTT fewer)
-  k2::encrypt(c, *P->keys, d.as<int64_t>(), mcoef, pt, out, m, level + 1, S(P), omap);
+  // mcoef: plaintexts as signed coefficients, folded into e0 by the sampler (NTT(e0 + m) =
+  // NTT(e0) + NTT(m) word for word: one transform and one row read fewer per limb)
+  k::sample_encryption_gpu(c, seeds.data(), m, d.as<int64_t>(), S(P), deferred, seeds_dev, mcoef);
+  k2::encrypt(c, *P->keys, d.as<int64_t>(), nullptr, pt, out, m, level + 1, S(P), omap);
 }
 
 std::shared_ptr<CtT> new_ct(hg_plan* P, int64_t count, int level, double scale) {

@@ -362,7 +362,8 @@ void gather_items(const Context& c, const uint64_t* in, const int32_t* idx, uint
 // values needing the host fix-up lands there once the stream reaches it (0 = output final)
 // seeds_dev: the same seeds already on the device (skips the host->device copy)
 void sample_encryption_gpu(const Context& c, const uint64_t* seeds_host, int64_t items, int64_t* out, cudaStream_t s,
-                           int* deferred_flag_count = nullptr, const uint64_t* seeds_dev = nullptr);
+                           int* deferred_flag_count = nullptr, const uint64_t* seeds_dev = nullptr,
+                           const int64_t* mfold = nullptr);
 // out[dst[i]] = in[src ? src[i] : i] for whole items
 void scatter_items(const Context& c, const uint64_t* in, const int32_t* src, const int32_t* dst, uint64_t* out,
                    int64_t items, int64_t item_words, cudaStream_t s);

@@ -1259,7 +1259,8 @@ struct SampleFlag {
 
 __global__ void k_sample_encryption(const uint64_t* __restrict__ seeds, int64_t items, int n, uint64_t h_mask,
                                     uint64_t h_error, int64_t* __restrict__ out, int* __restrict__ nflags,
-                                    SampleFlag* __restrict__ flags, int cap, double guard) {
+                                    SampleFlag* __restrict__ flags, int cap, double guard,
+                                    const int64_t* __restrict__ mfold) {
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (gid >= items * n) return;
   const int64_t item = gid / n;
@@ -1290,7 +1291,9 @@ __global__ void k_sample_encryption(const uint64_t* __restrict__ seeds, int64_t 
       if (fabs(frac - 0.5) < guard) flag = true;
       r = llround(v);
     }
-    o[(1 + which) * n + k] = r;
+    // mfold: the plaintext's signed coefficients folded into e0 (e0 + m is exact in int64: |e0| <= 28,
+    // |m| < 9e18), so the encryption lifts one row where it lifted two
+    o[(1 + which) * n + k] = (which == 0 && mfold) ? r + mfold[item * n + k] : r;
     if (flag) {
       const int slot = atomicAdd(nflags, 1);
       if (slot < cap) flags[slot] = SampleFlag{(int32_t)item, which, k, u1 <= 1e-300 ? 1 : 0};
@@ -1301,7 +1304,7 @@ __global__ void k_sample_encryption(const uint64_t* __restrict__ seeds, int64_t 
 
 namespace k {
 void sample_encryption_gpu(const Context& c, const uint64_t* seeds_host, int64_t items, int64_t* out,
-                           cudaStream_t s, int* deferred_flag_count, const uint64_t* seeds_dev) {
+                           cudaStream_t s, int* deferred_flag_count, const uint64_t* seeds_dev, const int64_t* mfold) {
   if (items <= 0) return;
   const int n = (int)c.n();
   const int cap = 1024;
@@ -1327,7 +1330,7 @@ void sample_encryption_gpu(const Context& c, const uint64_t* seeds_host, int64_t
   const int64_t total = items * n;
   c.kt_begin("k_sample_encryption", s, (double)items * 3 * n * 8, 0.0);
   k_sample_encryption<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(d_seeds, items, n, fnv("mask"), fnv("error"),
-                                                                       out, d_n, d_flags, cap, guard);
+                                                                       out, d_n, d_flags, cap, guard, mfold);
   c.kt_end(s);
   HG_CUDA(cudaGetLastError());
   if (deferred_flag_count) {
@@ -1346,6 +1349,11 @@ void sample_encryption_gpu(const Context& c, const uint64_t* seeds_host, int64_t
   auto resample_item = [&](int64_t it) {
     whole.resize(3 * (size_t)n);
     sample_encryption(seeds_host[it], n, whole.data(), whole.data() + n, whole.data() + 2 * n);
+    if (mfold) {  // e0 + m, as the kernel writes it
+      std::vector<int64_t> m((size_t)n);
+      HG_CUDA(cudaMemcpy(m.data(), mfold + it * n, (size_t)n * 8, cudaMemcpyDeviceToHost));
+      for (int k = 0; k < n; ++k) whole[(size_t)n + k] += m[(size_t)k];
+    }
     HG_CUDA(cudaMemcpy(out + it * 3 * n, whole.data(), whole.size() * 8, cudaMemcpyHostToDevice));
   };
   if (nflags > cap) {
@@ -1363,7 +1371,12 @@ void sample_encryption_gpu(const Context& c, const uint64_t* seeds_host, int64_t
     // advance to draw index base (two draws per Gaussian): state += base * golden
     const uint64_t base = (uint64_t)f.which * 2 * n + 2 * (uint64_t)f.k;
     for (uint64_t i = 0; i < base; ++i) e.next();
-    const int64_t v = static_cast<int64_t>(std::llround(e.gaussian() * 3.2));
+    int64_t v = static_cast<int64_t>(std::llround(e.gaussian() * 3.2));
+    if (mfold && f.which == 0) {
+      int64_t m = 0;
+      HG_CUDA(cudaMemcpy(&m, mfold + (int64_t)f.item * n + f.k, 8, cudaMemcpyDeviceToHost));
+      v += m;
+    }
     HG_CUDA(cudaMemcpy(out + (int64_t)f.item * 3 * n + (1 + f.which) * n + f.k, &v, 8, cudaMemcpyHostToDevice));
   }
 }

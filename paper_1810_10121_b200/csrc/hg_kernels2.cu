@@ -576,6 +576,90 @@ HG_KERNEL k_encrypt_t(const int64_t* __restrict__ samples, const int64_t* __rest
   }
 }
 
+// Fused encryption, half rows, software-pipelined (N >= 2^13): two CTAs per (limb, item group),
+// one per half of the evaluations; the first forward stage is applied while lifting the sample
+// row, and the NEXT sample row (u, e0, e1 of an item in turn) streams into shared memory with
+// cp.async behind the current transform -- the unpipelined kernel waited on these loads
+// (long_scoreboard ~12 warps per issue).  The plaintext coefficients of an input binding are
+// folded into e0 by the sampler (e0 + m, exact in int64), so each transform reads one row.
+template <typename W, int LOGN>
+struct EncPCfg {
+  static constexpr int n = 1 << LOGN, nfull = 2 * n;
+  static constexpr size_t s_off = Cfg<W, LOGN>::smem;
+  static constexpr size_t smem = s_off + (size_t)nfull * 8;
+  static constexpr bool fits = Cfg<W, LOGN>::TWS && smem <= kSmemCap;
+  static constexpr int min_blocks = 2 * smem <= kSmemCap ? 2 : 1;
+};
+template <typename W, int LOGN>
+__global__ void __launch_bounds__(Cfg<W, LOGN>::threads, (EncPCfg<W, LOGN>::min_blocks))
+    k_encrypt_p(const int64_t* __restrict__ samples, const uint64_t* __restrict__ pt, const uint64_t* __restrict__ pk,
+                int64_t key_poly_words, uint64_t* __restrict__ out, int nl, int64_t items, int G, const LimbList LL,
+                const CtxParams P, const int32_t* __restrict__ omap) {
+  extern __shared__ __align__(16) uint64_t smem[];
+  using EC = EncPCfg<W, LOGN>;
+  constexpr int n = EC::n, nfull = EC::nfull, T = lz::lz_threads<LOGN>();
+  static_assert((n >> 4) == T * 1 || (n >> 4) <= T, "one evaluation group per thread");
+  const int half = (int)(blockIdx.x & 1);
+  Cta<W, LOGN> c(smem, LL, items, G, P, false, (int)(blockIdx.x >> 1), half);
+  const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
+  const uint32_t mu32 = (uint32_t)((1ULL << 32) / c.L->q);
+  const ProdMod<W> pm(*c.L);
+  const uint64_t Q = c.L->q;
+  const int j = c.limb;
+  const int64_t pw = (int64_t)nl * nfull, hoff = (int64_t)half * n;
+  const lz::TWT<W> psi1 = half_twiddle<W>(first_twiddle<W>(*c.L), q, half);
+  int64_t* sbuf = reinterpret_cast<int64_t*>(reinterpret_cast<uint8_t*>(smem) + EC::s_off);
+  auto stage = [&](int r, int t) {  // sample row t (u, e0 + m, e1) of item r -> sbuf
+    const uint4* g = reinterpret_cast<const uint4*>(samples + ((int64_t)r * 3 + t) * nfull);
+    for (int ch = threadIdx.x; ch < nfull / 2; ch += T) cp_async16(reinterpret_cast<uint4*>(sbuf) + ch, g + ch);
+    cp_async_commit();
+  };
+  if (c.r0 < c.r1) stage(c.r0, 0);
+  const int vt = threadIdx.x, k0 = vt << 4;
+  const bool live = vt < (n >> 4);
+  for (int r = c.r0; r < c.r1; ++r) {
+    W u[16];
+#pragma unroll 1
+    for (int t = 0; t < 3; ++t) {
+      cp_async_wait_all();
+      __syncthreads();  // sbuf holds row (r, t); the previous transform's last pass is done
+      lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
+        return ct_one<W>(lift_any<W>(sbuf[k], *c.L, mu32), lift_any<W>(sbuf[k + n], *c.L, mu32), psi1, q, q2);
+      }, c.tw, q, q2);
+      if (t < 2) stage(r, t + 1);  // sbuf consumed (fwd_first_from ends with a barrier)
+      else if (r + 1 < c.r1) stage(r + 1, 0);
+      lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2);
+      W y[16];
+      if (live) lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, y);
+      if (t == 0) {
+#pragma unroll
+        for (int h = 0; h < 16; ++h) u[h] = canon4<W>(y[h], q, q2);
+        continue;
+      }
+      if (!live) continue;
+      const int p = t - 1;
+      const uint64_t* kp = pk + (int64_t)p * key_poly_words + (int64_t)j * nfull + hoff + k0;
+      const uint64_t* pp = (p == 0 && pt) ? pt + (int64_t)r * pw + (int64_t)j * nfull + hoff + k0 : nullptr;
+      const int64_t ro = omap ? (int64_t)omap[r] : (int64_t)r;
+      ulonglong2* o2 = reinterpret_cast<ulonglong2*>(out + (ro * 2 + p) * pw + (int64_t)j * nfull + hoff + k0);
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        const ulonglong2 kv = __ldg(reinterpret_cast<const ulonglong2*>(kp) + h);
+        ulonglong2 pv = make_ulonglong2(0, 0);
+        if (pp) pv = __ldg(reinterpret_cast<const ulonglong2*>(pp) + h);
+        uint64_t v[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const uint64_t a = pm(e ? kv.y : kv.x, (uint64_t)u[2 * h + e]);
+          v[e] = add_mod(a, (uint64_t)canon4<W>(y[2 * h + e], q, q2), Q);
+          if (pp) v[e] = add_mod(v[e], e ? pv.y : pv.x, Q);
+        }
+        o2[h] = make_ulonglong2(v[0], v[1]);
+      }
+    }
+  }
+}
+
 // relinearisation prologue: c2 = INTT(a1 * b1) per (item, limb i)  (ckks_backend.hpp:509).
 // With d != nullptr it also writes the tensor terms d0 = a0 b0, d1 = a0 b1 + a1 b0
 // (ckks_backend.hpp:306-318) as out[item][2][nl][N], so the key switch only adds its
@@ -1668,6 +1752,17 @@ void lift_ntt(const Context& c, const int64_t* src, uint64_t* out, int64_t items
   run(cl.wide, uint64_t{}, lf.wide());
 }
 
+// HG_ENCRYPT_PIPE=1: the half-row pipelined encryption kernel (measured neutral against the
+// whole-row kernel on c3's input binding, 0.91 vs 0.90 ms, and slightly slower on small batches,
+// so it is off by default)
+static bool encrypt_pipelined() {
+  static const bool on = [] {
+    const char* e = std::getenv("HG_ENCRYPT_PIPE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const int64_t* mcoef, const uint64_t* pt,
              uint64_t* out, int64_t items, int nl, cudaStream_t s, const int32_t* omap) {
   if (items <= 0) return;
@@ -1678,6 +1773,24 @@ void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const i
     using W = decltype(wtag);
     if (LL.count == 0) return;
     by_logn<W>(c, [&]<typename W_, int LOGN>() {
+      if constexpr (LOGN >= 13 && !std::is_same_v<W_, uint64_t>) {
+        using EC = EncPCfg<W_, LOGN - 1>;
+        if constexpr (EC::fits) {
+          if (mcoef == nullptr && encrypt_pipelined()) {
+            const int G = pick_group(items, (int64_t)LL.count * 2, 148LL * EC::min_blocks, 16);
+            const unsigned grid = (unsigned)(LL.count * ((items + G - 1) / G) * 2);
+            set_smem_attr((const void*)k_encrypt_p<W_, LOGN - 1>, EC::smem);
+            c.kt_begin(std::is_floating_point_v<W_> ? "k_encrypt_t/f64" : "k_encrypt_t/u32", s,
+                       (double)items * LL.count * (2 + (pt ? 1 : 0)) * nw + (double)items * 3 * nw * LL.count,
+                       (double)items * LL.count * (3 * bfly(c) + 2.0 * c.n()));
+            k_encrypt_p<W_, LOGN - 1><<<grid, Cfg<W_, LOGN - 1>::threads, EC::smem, s>>>(
+                samples, pt, keys.pk.as<uint64_t>(), kpw, out, nl, items, G, LL, c.kp(), omap);
+            c.kt_end(s);
+            HG_CUDA(cudaGetLastError());
+            return;
+          }
+        }
+      }
       using Cf = Cfg<W_, LOGN>;
       unsigned grid;
       int G;
