@@ -147,6 +147,9 @@ int hg_sample_encryption_host(hg_context* ctx, const uint64_t* seeds, int64_t it
 /* coefficient-domain m = c0 + c1 s (+ ...) -> host [items][nl][N] */
 int hg_decrypt_coeffs(hg_context* ctx, const hg_keys* keys, const uint64_t* ct, int64_t items, int size, int level,
                       uint64_t* m_host);
+/* CRT reconstruction and slot decode of decrypted outputs (ring.hpp:438-480, encoder.hpp:80-89)
+ * on the GPU (1, default) or on the host (0); the values are bit-identical either way */
+int hg_set_gpu_decode(int on);
 /* decrypt + CRT + decode to `count` slot values per item (host [items][count]) */
 int hg_decrypt(hg_context* ctx, const hg_keys* keys, const uint64_t* ct, int64_t items, int size, int level,
                double scale, int64_t count, double* values_host);

@@ -367,6 +367,16 @@ int hg_decrypt(hg_context* ctx, const hg_keys* keys, const uint64_t* ct, int64_t
     hg::Context& c = *ctx->c;
     level_ok(c, level);
     const int64_t n = c.n();
+    if (hg::gpu_decode_enabled()) {  // decrypt, CRT and slot decode on the GPU; only the values cross PCIe
+      const size_t words = static_cast<size_t>(items) * (level + 1) * n;
+      auto* md = static_cast<uint64_t*>(c.scratch(words * 8, 6));
+      auto* vd = static_cast<double*>(c.scratch(static_cast<size_t>(items * count) * 8 + 8, 11));
+      hg::k::decrypt(c, *keys->k, ct, md, items, size, level + 1, ctx->stream());
+      hg::k::decode_gpu(c, md, items, level + 1, scale, count, vd, count, 1, ctx->stream());
+      HG_CUDA(cudaMemcpyAsync(values, vd, static_cast<size_t>(items * count) * 8, cudaMemcpyDeviceToHost, ctx->stream()));
+      HG_CUDA(cudaStreamSynchronize(ctx->stream()));
+      return;
+    }
     std::vector<uint64_t> m(static_cast<size_t>(items * (level + 1) * n));
     int rc = hg_decrypt_coeffs(ctx, keys, ct, items, size, level, m.data());
     if (rc) hg::fail(rc, g_err);
@@ -424,6 +434,12 @@ int hg_bench_modmul(hg_context* ctx, int wide, double* modmul_per_s) {
 
 int64_t hg_kernel_launches(const hg_context* ctx) { return ctx ? ctx->c->kt_launches() : 0; }
 
+// 1 (default): CRT + slot decode of decrypted outputs on the GPU; 0: on the host.  Same values.
+int hg_set_gpu_decode(int on) {
+  hg::set_gpu_decode(on != 0);
+  return 0;
+}
+
 }  // extern "C"
 
 extern "C" {
@@ -457,6 +473,13 @@ int hg_decode(hg_context* ctx, const uint64_t* pt_dev, int level, double scale, 
     auto* m = static_cast<uint64_t*>(c.scratch(static_cast<size_t>(words * 8), 6));
     HG_CUDA(cudaMemcpyAsync(m, pt_dev, words * 8, cudaMemcpyDeviceToDevice, ctx->stream()));
     hg::k::ntt(c, m, level + 1, level + 1, true, ctx->stream());
+    if (hg::gpu_decode_enabled()) {
+      auto* vd = static_cast<double*>(c.scratch(static_cast<size_t>(count) * 8 + 8, 11));
+      hg::k::decode_gpu(c, m, 1, level + 1, scale, count, vd, count, 1, ctx->stream());
+      HG_CUDA(cudaMemcpyAsync(values, vd, static_cast<size_t>(count) * 8, cudaMemcpyDeviceToHost, ctx->stream()));
+      HG_CUDA(cudaStreamSynchronize(ctx->stream()));
+      return;
+    }
     std::vector<uint64_t> mh(static_cast<size_t>(words));
     HG_CUDA(cudaMemcpyAsync(mh.data(), m, words * 8, cudaMemcpyDeviceToHost, ctx->stream()));
     HG_CUDA(cudaStreamSynchronize(ctx->stream()));

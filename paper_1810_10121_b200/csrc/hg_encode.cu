@@ -53,7 +53,7 @@ __device__ __forceinline__ int64_t finish_coeff(double2 a, int64_t k, const doub
 __global__ void __launch_bounds__(kEncThreads) k_encode_fft_block(
     const double* __restrict__ values, int64_t count, int64_t col_stride, int64_t elem_stride,
     const double* __restrict__ roots, const double* __restrict__ half, int logn, int logb, double norm, double scale,
-    int64_t* __restrict__ out, double2* __restrict__ scratch, int* flag) {
+    int64_t* __restrict__ out, double2* __restrict__ scratch, int* flag, int64_t ostride, bool accumulate) {
   extern __shared__ double2 a[];
   const int64_t n = int64_t(1) << logn;
   const int bsz = 1 << logb;
@@ -80,7 +80,13 @@ __global__ void __launch_bounds__(kEncThreads) k_encode_fft_block(
     __syncthreads();
   }
   if (logb == logn) {
-    for (int k = threadIdx.x; k < bsz; k += blockDim.x) out[e * n + k] = finish_coeff(a[k], k, half, norm, scale, flag);
+    // accumulate: the coefficients are added to what `out` holds (input binding folds the plaintext
+    // into the e0 sample row of the fresh encryption, exact in int64)
+    for (int k = threadIdx.x; k < bsz; k += blockDim.x) {
+      const int64_t v = finish_coeff(a[k], k, half, norm, scale, flag);
+      int64_t* o = out + e * ostride + k;
+      *o = accumulate ? *o + v : v;
+    }
   } else {
     for (int j = threadIdx.x; j < bsz; j += blockDim.x) scratch[e * n + base + j] = a[j];
   }
@@ -88,7 +94,7 @@ __global__ void __launch_bounds__(kEncThreads) k_encode_fft_block(
 
 // one radix-2 stage of length 2^lg over the whole transform, in global memory
 __global__ void k_encode_fft_stage(double2* __restrict__ a, int64_t cols, int logn, int lg,
-                                   const double* __restrict__ roots) {
+                                   const double* __restrict__ roots, bool conj = false) {
   const int64_t n = int64_t(1) << logn;
   const int64_t h = int64_t(1) << (lg - 1);
   const int64_t step = n >> lg;
@@ -99,7 +105,7 @@ __global__ void k_encode_fft_stage(double2* __restrict__ a, int64_t cols, int lo
     const int64_t u = ((t >> (lg - 1)) << lg) + j;
     double2* c = a + e * n;
     const double2 w = __ldg(reinterpret_cast<const double2*>(roots) + j * step);
-    const double2 v = cmul_rn(c[u + h], w.x, w.y);
+    const double2 v = cmul_rn(c[u + h], w.x, conj ? -w.y : w.y);
     const double2 x = c[u];
     c[u] = make_double2(__dadd_rn(x.x, v.x), __dadd_rn(x.y, v.y));
     c[u + h] = make_double2(__dsub_rn(x.x, v.x), __dsub_rn(x.y, v.y));
@@ -107,19 +113,181 @@ __global__ void k_encode_fft_stage(double2* __restrict__ a, int64_t cols, int lo
 }
 
 __global__ void k_encode_finish(const double2* __restrict__ a, int64_t cols, int logn, const double* __restrict__ half,
-                                double norm, double scale, int64_t* __restrict__ out, int* flag) {
+                                double norm, double scale, int64_t* __restrict__ out, int* flag, int64_t ostride,
+                                bool accumulate) {
   const int64_t n = int64_t(1) << logn;
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < cols * n; g += (int64_t)gridDim.x * blockDim.x)
-    out[g] = finish_coeff(a[g], g % n, half, norm, scale, flag);
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < cols * n; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = finish_coeff(a[g], g % n, half, norm, scale, flag);
+    int64_t* o = out + (g / n) * ostride + g % n;
+    *o = accumulate ? *o + v : v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Decode on the GPU (ckks_backend.hpp:493-505 coeffs_to_values; ring.hpp:438-480
+// CrtReconstructor; encoder.hpp:80-89 + 92-109): per coefficient the CRT sum
+// sum_i punct_i * (m_i punct_inv_i mod q_i) in (nl + 1)-word integers, reduced below Q,
+// centred, converted to a double word by word from the top (r = r 2^64 + a_i), divided by
+// the scale; then b_k = c_k conj(half_k) and the conjugate radix-2 FFT.  Multiword order,
+// the conversion and every fp64 operation follow the reference, so the decoded doubles are
+// bit-identical to its host decode.
+//   tab: [total (W) | half (W) | punct_inv (nl) | punct (nl x W)], W = nl + 1 (Context::crt_dev)
+// ---------------------------------------------------------------------------
+constexpr int kCrtMaxW = HG_MAX_LIMBS + 1;
+
+__device__ __forceinline__ int w_cmp_dev(const uint64_t* a, const uint64_t* b, int W) {
+  for (int i = W - 1; i >= 0; --i)
+    if (a[i] != b[i]) return a[i] < b[i] ? -1 : 1;
+  return 0;
+}
+// a -= b (a >= b)
+__device__ __forceinline__ void w_sub_dev(uint64_t* a, const uint64_t* b, int W) {
+  uint64_t borrow = 0;
+  for (int i = 0; i < W; ++i) {
+    const uint64_t o = b[i], before = a[i];
+    a[i] = before - o - borrow;
+    borrow = (before < o || (borrow && before == o)) ? 1 : 0;
+  }
+}
+__device__ __forceinline__ double w_double_dev(const uint64_t* a, int W) {
+  double r = 0.0;
+  for (int i = W - 1; i >= 0; --i) r = __dadd_rn(__dmul_rn(r, 18446744073709551616.0), __ull2double_rn(a[i]));
+  return r;
+}
+
+__global__ void k_decode_crt(const uint64_t* __restrict__ m, int64_t items, int nl, int n,
+                             const uint64_t* __restrict__ tab, double scale, const double* __restrict__ half,
+                             double2* __restrict__ b, const CtxParams P) {
+  const int W = nl + 1;
+  const uint64_t* total = tab;
+  const uint64_t* halfq = tab + W;
+  const uint64_t* pinv = tab + 2 * W;
+  const uint64_t* punct = tab + 2 * W + nl;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < items * n; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t item = g / n;
+    const int k = (int)(g % n);
+    uint64_t acc[kCrtMaxW];
+    for (int w = 0; w < W; ++w) acc[w] = 0;
+    for (int i = 0; i < nl; ++i) {
+      const uint64_t sv = mul_mod(m[(item * nl + i) * n + k], pinv[i], P.limb[i]);
+      uint64_t carry = 0;
+      for (int w = 0; w < W; ++w) {
+        const uint64_t pw = punct[i * W + w];
+        const uint64_t lo = pw * sv, hi = __umul64hi(pw, sv);
+        const uint64_t s1 = lo + acc[w];
+        const uint64_t s2 = s1 + carry;
+        carry = hi + (s1 < lo ? 1 : 0) + (s2 < s1 ? 1 : 0);
+        acc[w] = s2;
+      }
+    }
+    while (w_cmp_dev(acc, total, W) >= 0) w_sub_dev(acc, total, W);
+    double v;
+    if (w_cmp_dev(acc, halfq, W) > 0) {
+      uint64_t neg[kCrtMaxW];
+      for (int w = 0; w < W; ++w) neg[w] = total[w];
+      w_sub_dev(neg, acc, W);
+      v = -w_double_dev(neg, W);
+    } else {
+      v = w_double_dev(acc, W);
+    }
+    const double coeff = __ddiv_rn(v, scale);
+    b[g] = make_double2(__dmul_rn(coeff, __ldg(half + 2 * k)), __dmul_rn(coeff, -__ldg(half + 2 * k + 1)));
+  }
+}
+
+// conjugate FFT block of the decode: like k_encode_fft_block, input b (natural order, read
+// bit-reversed), twiddles conjugated; with B == N the first `count` real parts are the values,
+// written to out[e * out_es + m * out_ms]
+__global__ void __launch_bounds__(kEncThreads) k_decode_fft_block(
+    const double2* __restrict__ b, const double* __restrict__ roots, int logn, int logb, int64_t count,
+    double* __restrict__ out, int64_t out_es, int64_t out_ms, double2* __restrict__ scratch) {
+  extern __shared__ double2 a[];
+  const int64_t n = int64_t(1) << logn;
+  const int bsz = 1 << logb;
+  const int64_t e = blockIdx.x;
+  const int64_t base = (int64_t)blockIdx.y * bsz;
+  for (int j = threadIdx.x; j < bsz; j += blockDim.x) {
+    const int64_t i = (int64_t)(__brev((unsigned)(base + j)) >> (32 - logn));
+    a[j] = b[e * n + i];
+  }
+  __syncthreads();
+  for (int lg = 1; lg <= logb; ++lg) {
+    const int h = 1 << (lg - 1);
+    const int64_t step = n >> lg;
+    for (int t = threadIdx.x; t < bsz / 2; t += blockDim.x) {
+      const int j = t & (h - 1);
+      const int u = ((t >> (lg - 1)) << lg) + j;
+      const double2 w = __ldg(reinterpret_cast<const double2*>(roots) + j * step);
+      const double2 v = cmul_rn(a[u + h], w.x, -w.y);
+      const double2 x = a[u];
+      a[u] = make_double2(__dadd_rn(x.x, v.x), __dadd_rn(x.y, v.y));
+      a[u + h] = make_double2(__dsub_rn(x.x, v.x), __dsub_rn(x.y, v.y));
+    }
+    __syncthreads();
+  }
+  if (logb == logn) {
+    for (int64_t k = threadIdx.x; k < count; k += blockDim.x) out[e * out_es + k * out_ms] = a[k].x;
+  } else {
+    for (int j = threadIdx.x; j < bsz; j += blockDim.x) scratch[e * n + base + j] = a[j];
+  }
+}
+
+__global__ void k_decode_finish(const double2* __restrict__ a, int64_t cols, int logn, int64_t count,
+                                double* __restrict__ out, int64_t out_es, int64_t out_ms) {
+  const int64_t n = int64_t(1) << logn;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < cols * count; g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = g / count, k = g % count;
+    out[e * out_es + k * out_ms] = a[e * n + k].x;
+  }
 }
 
 }  // namespace
 
 namespace k {
 
+void decode_gpu(const Context& c, const uint64_t* m, int64_t items, int nl, double scale, int64_t count, double* out,
+                int64_t out_es, int64_t out_ms, cudaStream_t s) {
+  if (items == 0) return;
+  check(count >= 0 && count <= c.slot_count(), HG_ECAPACITY, "requested more slots than the ring provides");
+  check(nl >= 1 && nl + 1 <= kCrtMaxW, HG_EINTERNAL, "decode: limb count");
+  const int logn = c.logn();
+  const int logb = std::min(logn, kEncBlockLog);
+  const int64_t n = c.n();
+  const size_t smem = sizeof(double2) << logb;
+  static bool attr = false;
+  if (!attr) {
+    HG_CUDA(cudaFuncSetAttribute((const void*)k_decode_fft_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(double2) << kEncBlockLog)));
+    attr = true;
+  }
+  const size_t bw = static_cast<size_t>(items * n) * sizeof(double2);
+  double2* b = static_cast<double2*>(const_cast<Context&>(c).scratch(bw * (logb < logn ? 2 : 1), 10));
+  double2* scratch = logb < logn ? b + items * n : nullptr;
+  c.kt_begin("k_decode", s, (double)items * nl * n * 8 + (double)items * count * 8, (double)items * (n / 2) * logn * 4);
+  const int64_t total = items * n;
+  k_decode_crt<<<(unsigned)std::min<int64_t>((total + 127) / 128, 148 * 16), 128, 0, s>>>(
+      m, items, nl, (int)n, c.crt_dev(nl), scale, c.enc_half_dev(), b, c.kp());
+  HG_CUDA(cudaGetLastError());
+  dim3 grid((unsigned)items, (unsigned)(n >> logb));
+  k_decode_fft_block<<<grid, kEncThreads, smem, s>>>(b, c.enc_roots_dev(), logn, logb, count, out, out_es, out_ms, scratch);
+  HG_CUDA(cudaGetLastError());
+  if (logb < logn) {
+    const int blocks = 148 * 8;
+    for (int lg = logb + 1; lg <= logn; ++lg) {
+      k_encode_fft_stage<<<blocks, 256, 0, s>>>(scratch, items, logn, lg, c.enc_roots_dev(), true);
+      HG_CUDA(cudaGetLastError());
+    }
+    k_decode_finish<<<blocks, 256, 0, s>>>(scratch, items, logn, count, out, out_es, out_ms);
+    HG_CUDA(cudaGetLastError());
+  }
+  c.kt_end(s);
+}
+
 void encode_fft(const Context& c, const double* values, int64_t cols, int64_t count, int64_t col_stride,
-                int64_t elem_stride, double scale, int64_t* out, int* flag, cudaStream_t s) {
+                int64_t elem_stride, double scale, int64_t* out, int* flag, cudaStream_t s, int64_t out_stride,
+                bool accumulate) {
   if (cols == 0) return;
+  if (out_stride == 0) out_stride = c.n();
   check(count >= 0 && count <= c.slot_count(), HG_ECAPACITY, "payload exceeds the available slot capacity");
   const int logn = c.logn();
   const int logb = std::min(logn, kEncBlockLog);
@@ -138,7 +306,8 @@ void encode_fft(const Context& c, const double* values, int64_t cols, int64_t co
              (double)cols * (n / 2) * logn * 4);
   dim3 grid((unsigned)cols, (unsigned)(n >> logb));
   k_encode_fft_block<<<grid, kEncThreads, smem, s>>>(values, count, col_stride, elem_stride, c.enc_roots_dev(),
-                                                    c.enc_half_dev(), logn, logb, norm, scale, out, scratch, flag);
+                                                    c.enc_half_dev(), logn, logb, norm, scale, out, scratch, flag,
+                                                    out_stride, accumulate);
   HG_CUDA(cudaGetLastError());
   if (logb < logn) {
     const int blocks = 148 * 8;
@@ -146,7 +315,8 @@ void encode_fft(const Context& c, const double* values, int64_t cols, int64_t co
       k_encode_fft_stage<<<blocks, 256, 0, s>>>(scratch, cols, logn, lg, c.enc_roots_dev());
       HG_CUDA(cudaGetLastError());
     }
-    k_encode_finish<<<blocks, 256, 0, s>>>(scratch, cols, logn, c.enc_half_dev(), norm, scale, out, flag);
+    k_encode_finish<<<blocks, 256, 0, s>>>(scratch, cols, logn, c.enc_half_dev(), norm, scale, out, flag, out_stride,
+                                           accumulate);
     HG_CUDA(cudaGetLastError());
   }
   c.kt_end(s);

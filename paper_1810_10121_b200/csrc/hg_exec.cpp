@@ -690,6 +690,7 @@ struct hg_plan {
   // crosses PCIe while the previous run still computes (created on first use)
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t copy_done = nullptr;
+  int* bind_flags = nullptr;  // pinned: [0] sampler values needing the host fix-up, [1] encoder overflow
   hg_context* hctx = nullptr;
   hg::Context* ctx = nullptr;
   const hg::Keys* keys = nullptr;
@@ -703,8 +704,8 @@ struct hg_plan {
   // values, plaintexts, ciphertexts): re-binding reuses them instead of growing the
   // stream-ordered pool while the previous binding is still alive
   struct BindBufs {
-    std::shared_ptr<hg::DevArr> staged, pt;
-    size_t staged_bytes = 0, pt_bytes = 0;
+    std::shared_ptr<hg::DevArr> staged, samples;
+    size_t staged_bytes = 0, samples_bytes = 0;
     std::shared_ptr<hg::CtT> ct;
     std::shared_ptr<hg::DevArr> omap;  // input element -> position in the padded layout
     int64_t padded = 0;                // padded element count (0: not pre-padded)
@@ -2927,6 +2928,7 @@ int hg_plan_set_options(hg_plan* P, const char* options_json) {
 void hg_plan_destroy(hg_plan* plan) {
   if (!plan) return;
   cudaStreamSynchronize(plan->ctx->stream());
+  if (plan->bind_flags) cudaFreeHost(plan->bind_flags);
   if (plan->copy_stream) {
     cudaStreamSynchronize(plan->copy_stream);
     cudaStreamDestroy(plan->copy_stream);
@@ -2975,37 +2977,6 @@ int hg_plan_bind_input(hg_plan* P, const char* param_id, const double* values, i
       return;
     }
     auto& bb = P->bind_bufs[param_id];
-    const double* dvals = values;
-    if (!on_device) {
-      const size_t sb = static_cast<size_t>(count) * 8;
-      bool fresh = false;
-      if (!bb.staged || bb.staged_bytes != sb) {
-        bb.staged = std::make_shared<hg::DevArr>(sb, hg::S(P));
-        bb.staged_bytes = sb;
-        fresh = true;
-      }
-      // the staging buffer is free: the previous bind of this input synchronised after its
-      // encode read it.  The copy runs on the plan's copy stream; the encode waits for it.
-      if (!P->copy_stream) {
-        HG_CUDA(cudaStreamCreateWithFlags(&P->copy_stream, cudaStreamNonBlocking));
-        HG_CUDA(cudaEventCreateWithFlags(&P->copy_done, cudaEventDisableTiming));
-      }
-      if (fresh) {  // a stream-ordered allocation on S(P): the copy stream waits for it
-        HG_CUDA(cudaEventRecord(P->copy_done, hg::S(P)));
-        HG_CUDA(cudaStreamWaitEvent(P->copy_stream, P->copy_done, 0));
-      }
-      HG_CUDA(cudaMemcpyAsync(bb.staged->p, values, sb, cudaMemcpyHostToDevice, P->copy_stream));
-      HG_CUDA(cudaEventRecord(P->copy_done, P->copy_stream));
-      HG_CUDA(cudaStreamWaitEvent(hg::S(P), P->copy_done, 0));
-      dvals = bb.staged->as<double>();
-    }
-    // the encoder's coefficients [nb][N] (encrypt folds them into its e0 transform)
-    const size_t pb = static_cast<size_t>(nb) * c.n() * 8;
-    if (!bb.pt || bb.pt_bytes != pb) {
-      bb.pt = std::make_shared<hg::DevArr>(pb, hg::S(P));
-      bb.pt_bytes = pb;
-    }
-    hg::encode_coeffs(P, dvals, nb, P->batch, 1, nb, c.default_scale(), bb.pt->as<int64_t>());
     // a Parameter whose only consumer is a Pad (and which is no graph output) is encrypted
     // straight into the padded layout: the Pad then only encrypts its fills (no copy pass)
     std::string pad_id;
@@ -3053,8 +3024,86 @@ int hg_plan_bind_input(hg_plan* P, const char* param_id, const double* values, i
       ct = bb.ct;
     else
       ct = bb.ct = hg::new_ct(P, count_ct, L, c.default_scale());
-    hg::encrypt_items(P, seeds, nullptr, L, ct->p, nullptr, bb.pt->as<int64_t>(),
-                      pad_id.empty() ? nullptr : bb.omap->as<int32_t>());
+    const int64_t n = c.n();
+    const size_t smb = static_cast<size_t>(nb) * 3 * n * 8;
+    if (!bb.samples || bb.samples_bytes != smb) {
+      bb.samples = std::make_shared<hg::DevArr>(smb, hg::S(P));
+      bb.samples_bytes = smb;
+    }
+    int64_t* samples = bb.samples->as<int64_t>();
+    const size_t sb = static_cast<size_t>(count) * 8;
+    if (!on_device) {
+      bool fresh = false;
+      if (!bb.staged || bb.staged_bytes != sb) {
+        bb.staged = std::make_shared<hg::DevArr>(sb, hg::S(P));
+        bb.staged_bytes = sb;
+        fresh = true;
+      }
+      // the staging buffer is free: the previous bind of this input synchronised after its
+      // encode read it.  The copies run on the plan's copy stream; each chunk's encode waits for it.
+      if (!P->copy_stream) {
+        HG_CUDA(cudaStreamCreateWithFlags(&P->copy_stream, cudaStreamNonBlocking));
+        HG_CUDA(cudaEventCreateWithFlags(&P->copy_done, cudaEventDisableTiming));
+      }
+      if (fresh) {  // a stream-ordered allocation on S(P): the copy stream waits for it
+        HG_CUDA(cudaEventRecord(P->copy_done, hg::S(P)));
+        HG_CUDA(cudaStreamWaitEvent(P->copy_stream, P->copy_done, 0));
+      }
+    }
+    if (!P->bind_flags) HG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&P->bind_flags), 2 * sizeof(int)));
+    hg::check(c.default_scale() > 0.0, HG_E_VALIDATION, "encoding scale must be positive");
+    // Pipeline (pack_cipher = encode + encrypt per column, packing.hpp:85-102): the fresh-encryption
+    // samples of every column are drawn first (no dependence on the data, so they overlap the first
+    // copy); then, per chunk of columns, the H2D copy (copy stream), the slot encode, whose
+    // coefficients are added into the chunk's e0 sample rows (NTT(e0 + m) = NTT(e0) + NTT(m) word
+    // for word: one transform and one row read fewer per limb), and the fused encryption.  A later
+    // chunk's copy overlaps the previous chunk's encode and encryption.  One synchronisation at the
+    // end checks the encoder's overflow flag and the sampler's host-fix-up count (rare: the binding
+    // is redone with the synchronous sampler).
+    // chunks of 296 columns: whole waves of the encoder (one CTA per column and SM) and of the
+    // encryption (two CTAs per SM), so chunking costs no wave quantisation
+    const int64_t chunk_cols = 296;
+    const int chunks = (!on_device && nb > chunk_cols) ? static_cast<int>((nb + chunk_cols - 1) / chunk_cols) : 1;
+    auto attempt = [&](bool sync_sampling) {
+      hg::DevArr flag(sizeof(int), hg::S(P));
+      HG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), hg::S(P)));
+      P->bind_flags[0] = 0;
+      P->bind_flags[1] = 0;
+      hg::k::sample_encryption_gpu(c, seeds.data(), nb, samples, hg::S(P), sync_sampling ? nullptr : &P->bind_flags[0]);
+      for (int ch = 0; ch < chunks; ++ch) {
+        const int64_t e0 = chunks == 1 ? 0 : ch * chunk_cols, e1 = chunks == 1 ? nb : std::min<int64_t>(nb, e0 + chunk_cols);
+        if (e1 <= e0) continue;
+        const double* dvals = values;
+        if (!on_device) {
+          double* st = bb.staged->as<double>();
+          if (chunks == 1) {
+            HG_CUDA(cudaMemcpyAsync(st, values, sb, cudaMemcpyHostToDevice, P->copy_stream));
+          } else {  // columns e0..e1 of every batch row
+            HG_CUDA(cudaMemcpy2DAsync(st + e0, static_cast<size_t>(nb) * 8, values + e0, static_cast<size_t>(nb) * 8,
+                                      static_cast<size_t>(e1 - e0) * 8, static_cast<size_t>(P->batch),
+                                      cudaMemcpyHostToDevice, P->copy_stream));
+          }
+          HG_CUDA(cudaEventRecord(P->copy_done, P->copy_stream));
+          HG_CUDA(cudaStreamWaitEvent(hg::S(P), P->copy_done, 0));
+          dvals = st;
+        }
+        // column e: slot b at values[b * nb + e] (packing.hpp:57-63)
+        hg::k::encode_fft(c, dvals + e0, e1 - e0, P->batch, 1, nb, c.default_scale(), samples + (e0 * 3 + 1) * n,
+                          flag.as<int>(), hg::S(P), 3 * n, true);
+        hg::k2::encrypt(c, *P->keys, samples + e0 * 3 * n, nullptr, nullptr,
+                        pad_id.empty() ? ct->p + e0 * ct->item_words() : ct->p, e1 - e0, L + 1, hg::S(P),
+                        pad_id.empty() ? nullptr : bb.omap->as<int32_t>() + e0);
+        P->launches += 2;
+      }
+      HG_CUDA(cudaMemcpyAsync(&P->bind_flags[1], flag.p, sizeof(int), cudaMemcpyDeviceToHost, hg::S(P)));
+      HG_CUDA(cudaStreamSynchronize(hg::S(P)));
+      hg::check(P->bind_flags[1] == 0, HG_E_VALIDATION, "encoded coefficient overflows the integer range");
+      return sync_sampling || P->bind_flags[0] == 0;
+    };
+    if (!attempt(false)) {
+      P->sampler_reruns += 1;
+      attempt(true);
+    }
     hg::Val v;
     v.shape = shape;
     v.batched = true;
@@ -3245,6 +3294,13 @@ int hg_plan_output(hg_plan* P, const char* id, double* values, int64_t capacity,
     const int64_t n = c.n();
     hg::DevArr md(static_cast<size_t>(m) * nl * n * 8, hg::S(P));
     hg::k::decrypt(c, *P->keys, v.ct->p, md.as<uint64_t>(), m, 2, nl, hg::S(P));
+    if (hg::gpu_decode_enabled()) {  // CRT + slot decode on the GPU, written row-major batch x elements
+      hg::DevArr vd(static_cast<size_t>(m * batch) * 8 + 8, hg::S(P));
+      hg::k::decode_gpu(c, md.as<uint64_t>(), m, nl, v.ct->scale, batch, vd.as<double>(), 1, m, hg::S(P));
+      HG_CUDA(cudaMemcpyAsync(values, vd.p, static_cast<size_t>(m * batch) * 8, cudaMemcpyDeviceToHost, hg::S(P)));
+      HG_CUDA(cudaStreamSynchronize(hg::S(P)));
+      return;
+    }
     std::vector<uint64_t> mh(static_cast<size_t>(m) * nl * n);
     HG_CUDA(cudaMemcpyAsync(mh.data(), md.p, mh.size() * 8, cudaMemcpyDeviceToHost, hg::S(P)));
     HG_CUDA(cudaStreamSynchronize(hg::S(P)));
@@ -3298,6 +3354,7 @@ struct hg_output {
   size_t pinned_bytes = 0;
   cudaEvent_t done = nullptr;
   std::vector<double> values;
+  bool values_pinned = false;  // GPU decode: the values are in `pinned` once `done` has fired
   int64_t count = 0;
   std::string err;
   int err_code = 0;
@@ -3331,6 +3388,26 @@ int hg_plan_output_async(hg_plan* P, const char* id, hg_output** out) {
     const double scale = v.ct->scale;
     const size_t words = static_cast<size_t>(m) * nl * n;
     t->pool = pinned_pool();
+    if (hg::gpu_decode_enabled()) {
+      // decrypt, CRT and decode on the GPU; the values land in pinned memory and hg_output_wait
+      // only waits for the copy
+      const size_t vb = static_cast<size_t>(m * batch) * 8 + 8;
+      t->pinned = static_cast<uint64_t*>(t->pool->get(vb));
+      t->pinned_bytes = vb;
+      HG_CUDA(cudaEventCreateWithFlags(&t->done, cudaEventDisableTiming));
+      {
+        hg::DevArr md(words * 8, hg::S(P));
+        hg::DevArr vd(vb, hg::S(P));
+        hg::k::decrypt(c, *P->keys, v.ct->p, md.as<uint64_t>(), m, 2, nl, hg::S(P));
+        hg::k::decode_gpu(c, md.as<uint64_t>(), m, nl, scale, batch, vd.as<double>(), 1, m, hg::S(P));
+        HG_CUDA(cudaMemcpyAsync(t->pinned, vd.p, static_cast<size_t>(m * batch) * 8, cudaMemcpyDeviceToHost, hg::S(P)));
+      }
+      HG_CUDA(cudaEventRecord(t->done, hg::S(P)));
+      t->count = m * batch;
+      t->values_pinned = true;
+      *out = t.release();
+      return;
+    }
     t->pinned = static_cast<uint64_t*>(t->pool->get(words * 8));
     t->pinned_bytes = words * 8;
     HG_CUDA(cudaEventCreateWithFlags(&t->done, cudaEventDisableTiming));
@@ -3378,9 +3455,15 @@ int hg_output_wait(hg_output* t, double* values, int64_t capacity, int64_t* coun
     if (own->th.joinable()) own->th.join();
     if (own->err_code) hg::fail(own->err_code, own->err);
     if (count) *count = own->count;
+    if (own->values_pinned) HG_CUDA(cudaEventSynchronize(own->done));
     if (values) {
       hg::check(capacity >= own->count, HG_E_VALIDATION, "output buffer too small");
-      std::copy(own->values.begin(), own->values.end(), values);
+      if (own->values_pinned) {
+        const double* pv = reinterpret_cast<const double*>(own->pinned);
+        std::copy(pv, pv + own->count, values);
+      } else {
+        std::copy(own->values.begin(), own->values.end(), values);
+      }
     }
   });
 }

@@ -6,6 +6,7 @@
 // because ciphertext parity with the CPU reference depends on it.  Compiled
 // with -ffp-contract=off and no -march flags: the reference's x86-64 build has
 // no FMA, so neither may we.
+#include <atomic>
 #include <cmath>
 #include <complex>
 #include <cstring>
@@ -676,6 +677,37 @@ std::shared_ptr<const CrtTables> Context::crt(int nl) const {
   auto it = m_crt.find(nl);
   if (it == m_crt.end()) it = m_crt.emplace(nl, std::make_shared<const CrtTables>(make_crt(m_q, nl))).first;
   return it->second;
+}
+
+static std::atomic<int> g_gpu_decode{-1};
+bool gpu_decode_enabled() {
+  int v = g_gpu_decode.load();
+  if (v < 0) {
+    const char* e = std::getenv("HG_GPU_DECODE");
+    v = (e && e[0] == '0') ? 0 : 1;
+    g_gpu_decode.store(v);
+  }
+  return v != 0;
+}
+void set_gpu_decode(bool on) { g_gpu_decode.store(on ? 1 : 0); }
+
+const uint64_t* Context::crt_dev(int nl) const {
+  const std::shared_ptr<const CrtTables> t = crt(nl);
+  std::lock_guard<std::mutex> lock(m_crt_mu);
+  auto it = m_crt_dev.find(nl);
+  if (it == m_crt_dev.end()) {
+    const int W = t->width;
+    std::vector<uint64_t> h;
+    h.insert(h.end(), t->total.begin(), t->total.end());
+    h.insert(h.end(), t->half.begin(), t->half.end());
+    h.insert(h.end(), t->punct_inv.begin(), t->punct_inv.end());
+    for (int i = 0; i < nl; ++i) h.insert(h.end(), t->punct[static_cast<size_t>(i)].begin(), t->punct[static_cast<size_t>(i)].end());
+    check(static_cast<int>(h.size()) == 2 * W + nl + nl * W, HG_EINTERNAL, "crt table size");
+    DevBuf d(h.size() * 8);
+    HG_CUDA(cudaMemcpy(d.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice));
+    it = m_crt_dev.emplace(nl, std::move(d)).first;
+  }
+  return it->second.as<uint64_t>();
 }
 
 void decode_coeffs_host(const Context& ctx, const uint64_t* m, int nl, double scale, int64_t count, double* out) {

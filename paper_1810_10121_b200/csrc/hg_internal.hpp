@@ -209,6 +209,8 @@ class Context {
   void* scratch(size_t bytes, int slot = 0);
   // CRT tables per active-limb count (built lazily by decode_coeffs_host)
   std::shared_ptr<const struct CrtTables> crt(int nl) const;
+  // the same tables on the device for the GPU decode: [total | half | punct_inv | punct], W = nl + 1
+  const uint64_t* crt_dev(int nl) const;
   // per-kernel CUDA-event timing (off by default; bench.py turns it on over the timed region)
   void kt_enable(bool on) const { m_kt_on = on; }
   bool kt_enabled() const { return m_kt_on; }
@@ -243,6 +245,7 @@ class Context {
   mutable int64_t m_kt_launches = 0;
   mutable std::mutex m_crt_mu;
   mutable std::map<int, std::shared_ptr<const struct CrtTables>> m_crt;
+  mutable std::map<int, DevBuf> m_crt_dev;
   ContextParamsH m_p;
   int m_logn = 0;
   int m_device = 0;
@@ -287,6 +290,15 @@ void sample_gaussian(Rng& r, int64_t n, double sigma, int64_t* out);
 // fresh-encryption samples for one seed: u, e0, e1 (ckks_backend.hpp:470-490)
 void sample_encryption(uint64_t seed, int64_t n, int64_t* u, int64_t* e0, int64_t* e1);
 
+// CRT reconstruction + /scale + slot decode of coefficient-domain m [items][nl][N] on the GPU,
+// bit-identical to decode_coeffs_host: value k of item e goes to out[e * out_es + k * out_ms] (device)
+namespace k {
+void decode_gpu(const Context& c, const uint64_t* m, int64_t items, int nl, double scale, int64_t count, double* out,
+                int64_t out_es, int64_t out_ms, cudaStream_t s);
+}
+// GPU decode on (default; HG_GPU_DECODE=0 or hg_set_gpu_decode(0): the host decode, same results)
+bool gpu_decode_enabled();
+void set_gpu_decode(bool on);
 // CRT reconstruction + /scale + slot decode of coefficient-domain m (host)
 void decode_coeffs_host(const Context& c, const uint64_t* m, int nl, double scale, int64_t count, double* out);
 
@@ -370,8 +382,10 @@ void scatter_items(const Context& c, const uint64_t* in, const int32_t* src, con
 // bit-exact slot encode on the GPU (encoder.hpp:58-77 + ckks_backend.hpp:186-192):
 // column e holds values[e*col_stride + m*elem_stride], m < count; out int64 [cols][N]
 // = llround(coeff * scale).  Sets *flag (device int) when a coefficient overflows.
+// out_stride: words between consecutive columns' outputs (0: N); accumulate: out += coefficients
 void encode_fft(const Context& c, const double* values, int64_t cols, int64_t count, int64_t col_stride,
-                int64_t elem_stride, double scale, int64_t* out, int* flag, cudaStream_t s);
+                int64_t elem_stride, double scale, int64_t* out, int* flag, cudaStream_t s, int64_t out_stride = 0,
+                bool accumulate = false);
 // register-only Shoup modmul throughput on every SM (modmul/s); wide = 64-bit words
 double modmul_peak(const Context& c, int mode, cudaStream_t s);  // 0: u32 Shoup, 1: u64 Shoup, 2: fp64
 void keygen_b(const Context& c, const uint64_t* a, const uint64_t* sk, const uint64_t* e, uint64_t* out, int nl,

@@ -48,8 +48,9 @@ struct Cta {
   W* s;
   const lz::TWT<W>* tw;
   // half >= 0: a half transform of a 2^(LOGN+1)-point forward NTT (its own twiddle table)
+  // stage = false: the twiddles stay in global memory (L1/L2-resident), shared memory holds the row only
   __device__ __forceinline__ Cta(uint64_t* smem, const LimbList& LL, int64_t rows, int G, const CtxParams& P,
-                                 bool inverse, int bid = -1, int half = -1) {
+                                 bool inverse, int bid = -1, int half = -1, bool stage = true) {
     if (bid < 0) bid = blockIdx.x;
     limb = LL.limb[bid % LL.count];
     const int g = bid / LL.count;
@@ -64,10 +65,14 @@ struct Cta {
       else src = L->fwh + half * Cfg<W, LOGN>::N;
     }
     if constexpr (Cfg<W, LOGN>::TWS) {
-      auto* t = reinterpret_cast<lz::TWT<W>*>(reinterpret_cast<uint8_t*>(smem) + Cfg<W, LOGN>::data_bytes);
-      stage_tw(t, src, Cfg<W, LOGN>::N);
-      tw = t;
-      __syncthreads();  // kernels may start with a fused first pass that reads twiddles at once
+      if (stage) {
+        auto* t = reinterpret_cast<lz::TWT<W>*>(reinterpret_cast<uint8_t*>(smem) + Cfg<W, LOGN>::data_bytes);
+        stage_tw(t, src, Cfg<W, LOGN>::N);
+        tw = t;
+        __syncthreads();  // kernels may start with a fused first pass that reads twiddles at once
+      } else {
+        tw = src;
+      }
     } else {
       tw = src;
     }
@@ -123,11 +128,13 @@ __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t 
 // ---------------------------------------------------------------------------
 // batched NTT of rows: row k of limb j at base + (k*nl + j) N
 // ---------------------------------------------------------------------------
-template <typename W, int LOGN, bool INV>
-__global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_blocks)
+// TWG: twiddles read from global memory, so a 2^14-point 32-bit row CTA needs 66 KB instead of
+// 194 KB of shared memory and two CTAs (32 warps) fit per SM
+template <typename W, int LOGN, bool INV, bool TWG = false>
+__global__ void __launch_bounds__(Cfg<W, LOGN>::threads, (TWG ? 2 : Cfg<W, LOGN>::min_blocks))
     k_ntt_t(uint64_t* __restrict__ base, int nl, int64_t rows, int G, const LimbList LL, const CtxParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
-  Cta<W, LOGN> c(smem, LL, rows, G, P, INV);
+  Cta<W, LOGN> c(smem, LL, rows, G, P, INV, -1, -1, !TWG);
   constexpr int n = 1 << LOGN;
   const W q = (W)c.L->q, q2 = lz::q2_of<W>(*c.L);
   for (int r = c.r0; r < c.r1; ++r) {
@@ -835,7 +842,10 @@ struct RsArgs {
   int pl_lp[HG_MAX_LIMBS], pl_nlc[HG_MAX_LIMBS], pl_xb[HG_MAX_LIMBS];
 };
 
-template <typename W, int LOGN, bool GIVEN_D, bool SPLIT, bool DIG, bool RS = false>
+// NR (32-bit lanes with q < 2^27, nr_forward_ok): the digit and lift transforms run without
+// conditional subtractions and the Montgomery MAC accumulates without reduction; the accumulators
+// (< (2 rows + 1) q < 2^32) are reduced once per item.  Same canonical outputs.
+template <typename W, int LOGN, bool GIVEN_D, bool SPLIT, bool DIG, bool RS = false, bool NR = false>
 __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, const uint64_t* __restrict__ b,
                                            int64_t a_stride, int64_t b_stride, const uint64_t* __restrict__ c2,
                                            const uint64_t* __restrict__ kval, const uint64_t* __restrict__ kpack,
@@ -852,6 +862,8 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
   constexpr bool C2S = RC::C2S && !DIG;
   constexpr bool KS = RC::KS;
   static_assert(!DIG || SPLIT, "digit rows are staged for half-row CTAs");
+  static_assert(!NR || (DIG && ((KS && sizeof(W) == 4) || std::is_floating_point_v<W>)),
+                "no-reduce key switch: staged 32-bit lanes and the fp64 lane");
   // DIG: c2 holds u16 digit rows [item][sd][nfull] (relin_c2 with digits); ds stages one row
   const uint16_t* const dig = reinterpret_cast<const uint16_t*>(c2);
   uint16_t* const ds = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(smem) + RC::ds_off);
@@ -1008,8 +1020,8 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
             else if (item + 1 < c.r1) { stage_c2(c2 + (int64_t)(item + 1) * pw); c2_staged = true; }
           }
         } else if constexpr (DIG) {
-          lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
-            return ct_one<W>((W)(uint32_t)ds[k], (W)(uint32_t)ds[k + n], psi1, q, q2);  // x0 +/- psi x1
+          lz::fwd_first_from<W, LOGN, NR>(c.s, [&](int k) {
+            return ct_one<W, NR>((W)(uint32_t)ds[k], (W)(uint32_t)ds[k + n], psi1, q, q2);  // x0 +/- psi x1
           }, c.tw, q, q2);
           // row consumed (fwd_first_from ends with a barrier): stage the next one behind this NTT
           if (row + 1 < sd) { stage_dig(item, row + 1); c2_staged = true; }
@@ -1023,7 +1035,7 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
           lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return (W)(uint32_t)((__ldg(src + k) >> sh) & 0x7FFF); }, c.tw, q, q2);
         }
         if constexpr (KS && DIG) {
-          lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2, [&] { mb_wait(&mb[1], ks_ph); });  // key rows landed
+          lz::fwd_middle<W, LOGN, NR>(c.s, c.tw, q, q2, [&] { mb_wait(&mb[1], ks_ph); });  // key rows landed
           ks_ph ^= 1;
         } else if constexpr (KS) {
           // key row landed (the c2 prefetch committed after it may still be in flight)
@@ -1043,7 +1055,7 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
           (void)o0;
           (void)o1;
           W x[16];
-          lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, x);
+          lz::fwd_last<W, LOGN, NR>(c.s, vt, c.tw, q, q2, x);
           const int64_t koff = (int64_t)row * 2 * K.key_poly_words + (int64_t)j * nfull + hoff + k0;
           if constexpr (KS) {
             // Montgomery MAC: U = (x km + m q) / 2^32 with m = -(x km) q^{-1} mod 2^32; x < 4q < 2^32,
@@ -1060,8 +1072,13 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
                 const uint32_t ub = (uint32_t)((tb + (uint64_t)((uint32_t)tb * qneg) * q32) >> 32);
                 const uint32_t ua = (uint32_t)((ta + (uint64_t)((uint32_t)ta * qneg) * q32) >> 32);
                 const uint32_t s0 = (uint32_t)acc0[gi][4 * h + e] + ub, s1 = (uint32_t)acc1[gi][4 * h + e] + ua;
-                acc0[gi][4 * h + e] = (W)min(s0, s0 - q232);
-                acc1[gi][4 * h + e] = (W)min(s1, s1 - q232);
+                if constexpr (NR) {
+                  acc0[gi][4 * h + e] = (W)s0;
+                  acc1[gi][4 * h + e] = (W)s1;
+                } else {
+                  acc0[gi][4 * h + e] = (W)min(s0, s0 - q232);
+                  acc1[gi][4 * h + e] = (W)min(s1, s1 - q232);
+                }
               }
             }
           } else if constexpr (std::is_floating_point_v<W>) {
@@ -1080,6 +1097,9 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
                 if constexpr (AG) {
                   od0[2 * h + e] = reduce_f64(__dadd_rn(od0[2 * h + e], t0), q, q2);
                   od1[2 * h + e] = reduce_f64(__dadd_rn(od1[2 * h + e], t1), q, q2);
+                } else if constexpr (NR) {  // |acc| < 2 rows q < 2^51
+                  acc0[gi][2 * h + e] = __dadd_rn(acc0[gi][2 * h + e], t0);
+                  acc1[gi][2 * h + e] = __dadd_rn(acc1[gi][2 * h + e], t1);
                 } else {
                   acc0[gi][2 * h + e] = reduce_f64(__dadd_rn(acc0[gi][2 * h + e], t0), q, q2);
                   acc1[gi][2 * h + e] = reduce_f64(__dadd_rn(acc1[gi][2 * h + e], t1), q, q2);
@@ -1137,6 +1157,16 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
         __syncthreads();  // smem reused by the next digit
       }
     }
+    if constexpr (NR && sizeof(W) == 4) {  // accumulators < (2 rows + 1) q -> [0, 2q), as the epilogues expect
+      const uint32_t q32 = (uint32_t)Q, mu = (uint32_t)((1ULL << 32) / Q);
+#pragma unroll
+      for (int gi = 0; gi < GPT; ++gi)
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+          acc0[gi][r] = (W)((uint32_t)acc0[gi][r] - __umulhi((uint32_t)acc0[gi][r], mu) * q32);
+          acc1[gi][r] = (W)((uint32_t)acc1[gi][r] - __umulhi((uint32_t)acc1[gi][r], mu) * q32);
+        }
+    }
     // epilogue: + d0, d1; canonical store
     if constexpr (RS) {
       static_assert(DIG && GIVEN_D && GPT == 1, "fused rescale: digit-row key switch with given d0, d1");
@@ -1178,13 +1208,13 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
       for (int p = 0; p < 2; ++p) {
         const int32_t* cv = rs.cen + ((int64_t)item * 2 + p) * nfull;
         if (p == 1) __syncthreads();  // the previous transform's last pass has read shared memory
-        lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
-          return ct_one<W>(lift_cen<W, int32_t>(__ldg(cv + k), *c.L, mu32),
-                           lift_cen<W, int32_t>(__ldg(cv + k + n), *c.L, mu32), psi1, q, q2);
+        lz::fwd_first_from<W, LOGN, NR>(c.s, [&](int k) {
+          return ct_one<W, NR>(lift_cen<W, int32_t>(__ldg(cv + k), *c.L, mu32),
+                               lift_cen<W, int32_t>(__ldg(cv + k + n), *c.L, mu32), psi1, q, q2);
         }, c.tw, q, q2);
-        lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2);
+        lz::fwd_middle<W, LOGN, NR>(c.s, c.tw, q, q2);
         W y[16];
-        lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, y);
+        lz::fwd_last<W, LOGN, NR>(c.s, vt, c.tw, q, q2, y);
         ulonglong2* o2 = reinterpret_cast<ulonglong2*>(rs.out + (((int64_t)item * 2 + p) * t + j) * nfull + hoff + k0);
         uint64_t v[16];
 #pragma unroll
@@ -1192,8 +1222,10 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const W f = p ? acc1[0][2 * h + e] : acc0[0][2 * h + e];
-            v[2 * h + e] =
-                rescale_word<W>((uint64_t)f, (uint64_t)canon4<W>(y[2 * h + e], q, q2), Q, inv, inv_s, inv_s32);
+            W yc;
+            if constexpr (NR && sizeof(W) == 4) yc = (W)reduce_any32((uint32_t)y[2 * h + e], (uint32_t)Q, mu32);
+            else yc = canon4<W>(y[2 * h + e], q, q2);
+            v[2 * h + e] = rescale_word<W>((uint64_t)f, (uint64_t)yc, Q, inv, inv_s, inv_s32);
           }
           o2[h] = make_ulonglong2(v[2 * h], v[2 * h + 1]);
         }
@@ -1300,14 +1332,14 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
   }
 }
 
-template <typename W, int LOGN, bool GIVEN_D, bool SPLIT = false, bool DIG = false, bool RS = false>
+template <typename W, int LOGN, bool GIVEN_D, bool SPLIT = false, bool DIG = false, bool RS = false, bool NR = false>
 __global__ void __launch_bounds__(RelinCfg<W, LOGN, SPLIT, DIG>::threads, RelinCfg<W, LOGN, SPLIT, DIG>::min_blocks)
     k_relin_t(const uint64_t* a, const uint64_t* __restrict__ b, int64_t a_stride, int64_t b_stride,
               const uint64_t* __restrict__ c2, const uint64_t* __restrict__ kval,
               const uint64_t* __restrict__ kpack, const uint32_t* __restrict__ kmont, uint64_t* out,
               int nl, int64_t items, int G, const RelinC K, const LimbList LL, const CtxParams P,
               const uint32_t* __restrict__ d32, const RsArgs rs) {
-  relin_body<W, LOGN, GIVEN_D, SPLIT, DIG, RS>((int)blockIdx.x, a, b, a_stride, b_stride, c2, kval, kpack, kmont, out,
+  relin_body<W, LOGN, GIVEN_D, SPLIT, DIG, RS, NR>((int)blockIdx.x, a, b, a_stride, b_stride, c2, kval, kpack, kmont, out,
                                           nl, items, G, K, LL, P, d32, rs);
 }
 
@@ -1699,6 +1731,16 @@ static void grid_for(const LimbList& LL, int64_t rows, unsigned& grid, int& G) {
   grid = (unsigned)(LL.count * ((rows + G - 1) / G));
 }
 
+// HG_NTT_TWG=1: the standalone 2^14-point 32-bit transform reads its twiddles from global memory
+// (two CTAs per SM instead of one)
+static bool ntt_twg() {
+  static const bool on = [] {
+    const char* e = std::getenv("HG_NTT_TWG");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 void ntt(const Context& c, uint64_t* base, int64_t rows_per_limb, int nl, int limb_begin, int limb_end, bool inverse,
          cudaStream_t s) {
   if (rows_per_limb <= 0) return;
@@ -1712,9 +1754,22 @@ void ntt(const Context& c, uint64_t* base, int64_t rows_per_limb, int nl, int li
       unsigned grid;
       int G;
       grid_for<W_, LOGN>(LL, rows_per_limb, grid, G);
+      c.kt_begin(std::is_floating_point_v<W_> ? "k_ntt_t/f64" : sizeof(W_) == 4 ? "k_ntt_t/u32" : "k_ntt_t/u64", s, 2.0 * rows_per_limb * LL.count * nw, (double)rows_per_limb * LL.count * bfly(c));
+      if constexpr (LOGN == 14 && sizeof(W_) == 4) {
+        if (ntt_twg()) {  // two CTAs per SM, twiddles from L1/L2
+          G = pick_group(rows_per_limb, LL.count, 148LL * 2, 16);
+          grid = (unsigned)(LL.count * ((rows_per_limb + G - 1) / G));
+          const void* fn = inverse ? (const void*)k_ntt_t<W_, LOGN, true, true> : (const void*)k_ntt_t<W_, LOGN, false, true>;
+          set_smem_attr(fn, Cf::data_bytes);
+          if (inverse) k_ntt_t<W_, LOGN, true, true><<<grid, Cf::threads, Cf::data_bytes, s>>>(base, nl, rows_per_limb, G, LL, c.kp());
+          else k_ntt_t<W_, LOGN, false, true><<<grid, Cf::threads, Cf::data_bytes, s>>>(base, nl, rows_per_limb, G, LL, c.kp());
+          c.kt_end(s);
+          HG_CUDA(cudaGetLastError());
+          return;
+        }
+      }
       const void* fn = inverse ? (const void*)k_ntt_t<W_, LOGN, true> : (const void*)k_ntt_t<W_, LOGN, false>;
       set_smem_attr(fn, Cf::smem);
-      c.kt_begin(std::is_floating_point_v<W_> ? "k_ntt_t/f64" : sizeof(W_) == 4 ? "k_ntt_t/u32" : "k_ntt_t/u64", s, 2.0 * rows_per_limb * LL.count * nw, (double)rows_per_limb * LL.count * bfly(c));
       if (inverse) k_ntt_t<W_, LOGN, true><<<grid, Cf::threads, Cf::smem, s>>>(base, nl, rows_per_limb, G, LL, c.kp());
       else k_ntt_t<W_, LOGN, false><<<grid, Cf::threads, Cf::smem, s>>>(base, nl, rows_per_limb, G, LL, c.kp());
       c.kt_end(s);
@@ -1994,6 +2049,23 @@ static int lane_slots() {
   return v;
 }
 
+// No-reduce 32-bit transforms and key MAC (HG_RELIN_NR=0 turns them off): every limb of the lane
+// must keep (4 + 2 log N) q (a forward transform on inputs < 4q) and (2 rows + 2) q (the MAC
+// accumulators, started at d < q) below 2^32
+static bool relin_nr_ok(const Context& c, const LimbList& LL, int rows, bool fp) {
+  static const bool on = [] {
+    const char* e = std::getenv("HG_RELIN_NR");
+    return !(e && e[0] == '0');
+  }();
+  if (!on) return false;
+  const uint64_t m = (uint64_t)std::max(4 + 2 * c.logn(), 2 * rows + 2);
+  for (int k = 0; k < LL.count; ++k) {
+    // fp64 lane: |t| < 2q per butterfly / MAC term, everything below 2^51 (m < 128)
+    if (fp ? c.primes()[LL.limb[k]] >= (1ULL << 44) || m > 128 : c.primes()[LL.limb[k]] * m >= (1ULL << 32)) return false;
+  }
+  return true;
+}
+
 // target limbs [lb, le) of the key switch; rs: fused rescale of those limbs (digit rows only)
 static void relin_impl(const Context& c, const Keys& keys, const uint64_t* a, const uint64_t* b, int64_t a_stride,
                        int64_t b_stride, bool given_d, const uint64_t* c2, uint64_t* out, int64_t items, int nl,
@@ -2013,7 +2085,7 @@ static void relin_impl(const Context& c, const Keys& keys, const uint64_t* a, co
     using W = decltype(wtag);
     if (LL.count == 0) return;
     by_logn<W>(c, [&]<typename W_, int LOGN>() {
-      auto go = [&]<bool SPLIT, bool DIG = false, bool RS = false>() {
+      auto go = [&]<bool SPLIT, bool DIG = false, bool RS = false, bool NR = false>() {
         constexpr int LT = SPLIT ? LOGN - 1 : LOGN;
         using Cf = RelinCfg<W_, LT, SPLIT, DIG>;
         const int threads = Cf::threads;
@@ -2031,8 +2103,9 @@ static void relin_impl(const Context& c, const Keys& keys, const uint64_t* a, co
         const uint32_t* dd32 = (in_out && sizeof(W_) == 4) ? d32 : nullptr;
         const uint64_t* aa = in_out ? out : a;
         const int64_t as = in_out ? 2LL * nl * c.n() : a_stride;
-        const void* fn = gd ? (const void*)k_relin_t<W_, LT, true, SPLIT, DIG, RS>
+        const void* fn = gd ? (const void*)k_relin_t<W_, LT, true, SPLIT, DIG, RS, NR>
                             : (const void*)k_relin_t<W_, LT, false, SPLIT, DIG>;
+        check(!NR || (gd && (dd32 != nullptr || sizeof(W_) == 8)), HG_EINTERNAL, "no-reduce key switch needs the u32 tensor terms");
         set_smem_attr(fn, Cf::smem);
         const double frac = (double)LL.count / nl;
         // bytes: c2 + (a, b | d0, d1) + out once, key rows once; modmuls: digit NTTs + key MACs (+ tensor)
@@ -2044,7 +2117,7 @@ static void relin_impl(const Context& c, const Keys& keys, const uint64_t* a, co
                    (double)items * LL.count * (sd * (bfly(c) + 2.0 * c.n()) + (gd ? 0.0 : 3.0 * c.n()) +
                                                (RS ? 2.0 * (bfly(c) + c.n()) : 0.0)));
         if (gd)
-          k_relin_t<W_, LT, true, SPLIT, DIG, RS><<<grid, threads, Cf::smem, s>>>(
+          k_relin_t<W_, LT, true, SPLIT, DIG, RS, NR><<<grid, threads, Cf::smem, s>>>(
               aa, b, as, b_stride, c2, keys.relin.as<uint64_t>(), keys.relin_pack.as<uint64_t>(),
               keys.relin_mont.as<uint32_t>(), out, nl, items, G, K, LL, c.kp(), dd32, rsa);
         else if constexpr (!RS)
@@ -2064,6 +2137,12 @@ static void relin_impl(const Context& c, const Keys& keys, const uint64_t* a, co
         else go.template operator()<true>();
       }
       else if constexpr (LOGN == 13 && !std::is_same_v<W_, uint64_t>) {
+        // 32-bit lanes with q < 2^27 (c3's 26-bit primes): transforms and MAC without reductions
+        // fp64 lanes with q < 2^44 (c3's 36-bit primes): no reduction of the additive inputs
+        const bool nr = digits && !given_d && d_in_out && (sizeof(W_) == 8 || d32 != nullptr) &&
+                        relin_nr_ok(c, LL, sd, std::is_floating_point_v<W_>);
+        if (nr && rs) return go.template operator()<true, true, true, true>();
+        if (nr) return go.template operator()<true, true, false, true>();
         if (digits && rs) go.template operator()<true, true, true>();
         else if (digits) go.template operator()<true, true>();
         else if (relin_split13()) go.template operator()<true>();

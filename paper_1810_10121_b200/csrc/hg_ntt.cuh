@@ -252,9 +252,25 @@ __device__ __forceinline__ W csub(W a, W m) {
   else return a >= m ? a - m : a;
 }
 
-template <typename W>
+// NR (32-bit lane, small primes): no conditional subtraction.  The Shoup product accepts any
+// 32-bit x and returns t < 2q, so both outputs grow by at most 2q per stage; a transform of S
+// stages on inputs < 4q stays below (4 + 2S) q, which the caller guarantees is < 2^32
+// (nr_forward_ok: q < 2^27 at N <= 2^14).  Outputs are congruent to ct_lz's; the consumer
+// reduces them (reduce_any32) or feeds a MAC that accepts any 32-bit word.
+template <typename W, bool NR = false>
 __device__ __forceinline__ void ct_lz(W& a, W& b, typename Lz<W>::TW w, W q, W q2) {
-  if constexpr (std::is_floating_point_v<W>) {  // fp64 lane: q2 = 1/q
+  if constexpr (NR && std::is_floating_point_v<W>) {
+    // fp64 lane, q < 2^44: |t| < 2q, so S stages on inputs below 2q stay below (2 + 2S) q < 2^51,
+    // the range mulmod_f64 and canon_f64 accept; the additive input is not reduced
+    const double t = mulmod_f64(b, w, q, q2);
+    b = __dsub_rn(a, t);
+    a = __dadd_rn(a, t);
+  } else if constexpr (NR) {
+    static_assert(std::is_integral_v<W> && sizeof(W) == 4, "no-reduce butterflies: 32-bit and fp64 lanes");
+    const W t = Lz<W>::mulw(b, w, q);
+    b = a - t + q2;
+    a = a + t;
+  } else if constexpr (std::is_floating_point_v<W>) {  // fp64 lane: q2 = 1/q
     const double x = reduce_f64(a, q, q2);
     const double t = mulmod_f64(b, w, q, q2);
     a = __dadd_rn(x, t);
@@ -276,9 +292,11 @@ __device__ __forceinline__ typename Lz<W>::TW half_twiddle(typename Lz<W>::TW w,
   else if constexpr (sizeof(W) == 4) return half ? make_uint2((uint32_t)q - w.x, ~w.y) : w;
   else return half ? make_ulonglong2((uint64_t)q - w.x, ~w.y) : w;
 }
-template <typename W>
+template <typename W, bool NR = false>
 __device__ __forceinline__ W ct_one(W a, W b, typename Lz<W>::TW w, W q, W q2) {
-  if constexpr (std::is_floating_point_v<W>) return __dadd_rn(reduce_f64(a, q, q2), mulmod_f64(b, w, q, q2));
+  if constexpr (NR && std::is_floating_point_v<W>) return __dadd_rn(a, mulmod_f64(b, w, q, q2));
+  else if constexpr (NR) return a + Lz<W>::mulw(b, w, q);
+  else if constexpr (std::is_floating_point_v<W>) return __dadd_rn(reduce_f64(a, q, q2), mulmod_f64(b, w, q, q2));
   else return csub(a, q2) + Lz<W>::mulw(b, w, q);
 }
 template <typename W>
@@ -293,6 +311,11 @@ __device__ __forceinline__ void gs_lz(W& a, W& b, typename Lz<W>::TW w, W q, W q
     a = s;
     b = Lz<W>::mulw(d, w, q);
   }
+}
+// any 32-bit x -> [0, q): one Barrett step with mu = floor(2^32 / q) leaves [0, 2q)
+__device__ __forceinline__ uint32_t reduce_any32(uint32_t x, uint32_t q, uint32_t mu) {
+  const uint32_t r = x - __umulhi(x, mu) * q;
+  return min(r, r - q);
 }
 // [0, 4q) -> [0, q)   (fp64 lane: any |x| < 2^51 -> [0, q))
 template <typename W>

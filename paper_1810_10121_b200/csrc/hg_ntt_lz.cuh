@@ -48,7 +48,7 @@ __device__ __forceinline__ W q2_of(const LimbInfo& L) {
 
 // ---- forward (Cooley-Tukey), remainder-first passes ------------------------
 // stages S0 .. S0+K-1 of block g; pass-ordered twiddle at 2^S + (r >> (K-st)) 2^S0 + g
-template <typename W, int K, int S0>
+template <typename W, int K, int S0, bool NR = false>
 __device__ __forceinline__ void fwd_group(W (&x)[1 << K], int g, const TWT<W>* tw, W q, W q2) {
   constexpr int R = 1 << K;
 #pragma unroll
@@ -57,12 +57,12 @@ __device__ __forceinline__ void fwd_group(W (&x)[1 << K], int g, const TWT<W>* t
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       if (r & hd) continue;
-      ct_lz(x[r], x[r + hd], tw[(1 << (S0 + st)) + ((r >> (K - st)) << S0) + g], q, q2);
+      ct_lz<W, NR>(x[r], x[r + hd], tw[(1 << (S0 + st)) + ((r >> (K - st)) << S0) + g], q, q2);
     }
   }
 }
 
-template <typename W, int LOGN, int K, int S0>
+template <typename W, int LOGN, int K, int S0, bool NR = false>
 __device__ __forceinline__ void fwd_pass(W* s, const TWT<W>* tw, W q, W q2) {
   constexpr int R = 1 << K, TL = LOGN - S0 - K;
 #pragma unroll
@@ -72,7 +72,7 @@ __device__ __forceinline__ void fwd_pass(W* s, const TWT<W>* tw, W q, W q2) {
     W x[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) x[r] = s[pb + pow_<W>(r,TL)];
-    fwd_group<W, K, S0>(x, g, tw, q, q2);
+    fwd_group<W, K, S0, NR>(x, g, tw, q, q2);
 #pragma unroll
     for (int r = 0; r < R; ++r) s[pb + pow_<W>(r,TL)] = x[r];
   }
@@ -104,7 +104,7 @@ __device__ __forceinline__ void fwd_but_last(W* s, const TWT<W>* tw, W q, W q2) 
 // First pass with its input produced on the fly: element k (natural order) = get(k).
 // Fuses the staging of a freshly computed row (e.g. a relinearisation digit) into
 // the pass, saving one shared-memory store + load per element.  Ends with a barrier.
-template <typename W, int LOGN, typename Get>
+template <typename W, int LOGN, bool NR = false, typename Get>
 __device__ __forceinline__ void fwd_first_from(W* s, Get get, const TWT<W>* tw, W q, W q2) {
   constexpr int K = (LOGN & 3) ? (LOGN & 3) : 4, R = 1 << K, TL = LOGN - K;
 #pragma unroll
@@ -113,7 +113,7 @@ __device__ __forceinline__ void fwd_first_from(W* s, Get get, const TWT<W>* tw, 
     W x[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) x[r] = get(vt + (r << TL));
-    fwd_group<W, K, 0>(x, 0, tw, q, q2);
+    fwd_group<W, K, 0, NR>(x, 0, tw, q, q2);
 #pragma unroll
     for (int r = 0; r < R; ++r) s[pb + pow_<W>(r, TL)] = x[r];
   }
@@ -124,11 +124,11 @@ struct NoHook {
 };
 // the passes between fwd_first_from and fwd_last; ends with a barrier, and runs
 // `pre()` (e.g. a cp.async wait) right before that last barrier
-template <typename W, int LOGN, typename Pre = NoHook>
+template <typename W, int LOGN, bool NR = false, typename Pre = NoHook>
 __device__ __forceinline__ void fwd_middle(W* s, const TWT<W>* tw, W q, W q2, Pre pre = Pre{}) {
   constexpr int K0 = (LOGN & 3) ? (LOGN & 3) : 4;
   if constexpr (K0 + 4 < LOGN) {
-    fwd_pass<W, LOGN, 4, K0>(s, tw, q, q2);
+    fwd_pass<W, LOGN, 4, K0, NR>(s, tw, q, q2);
     if constexpr (!(K0 + 8 < LOGN)) pre();
     __syncthreads();
   } else {
@@ -136,19 +136,19 @@ __device__ __forceinline__ void fwd_middle(W* s, const TWT<W>* tw, W q, W q2, Pr
     __syncthreads();
   }
   if constexpr (K0 + 8 < LOGN) {
-    fwd_pass<W, LOGN, 4, K0 + 4>(s, tw, q, q2);
+    fwd_pass<W, LOGN, 4, K0 + 4, NR>(s, tw, q, q2);
     pre();
     __syncthreads();
   }
 }
 
 // the last pass of group vt: x[r] = evaluation 16 vt + r, in [0, 4q)
-template <typename W, int LOGN>
+template <typename W, int LOGN, bool NR = false>
 __device__ __forceinline__ void fwd_last(const W* s, int vt, const TWT<W>* tw, W q, W q2, W (&x)[16]) {
   const int pb = padw<W>(vt << 4);
 #pragma unroll
   for (int r = 0; r < 16; ++r) x[r] = s[pb + r];
-  fwd_group<W, 4, LOGN - 4>(x, vt, tw, q, q2);
+  fwd_group<W, 4, LOGN - 4, NR>(x, vt, tw, q, q2);
 }
 
 template <typename W, int LOGN>
