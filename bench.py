@@ -10,7 +10,8 @@ per slot; Pad -> Conv 5x5/2 (5 maps) -> x^2 -> Dense 845->100 -> x^2 -> Dense
 (input ciphertexts resident in HBM -> output ciphertexts in HBM); `value` is
 images/s over all ranks.  `e2e` is the same metric through the public C-ABI with
 host buffers: host pixels -> encode + encrypt -> graph -> decrypt + decode ->
-host logits, i.e. what heg::execute does for the reference arm.
+host logits, i.e. what heg::execute does for the reference arm (all of it on the
+GPU: only the pixels and the decoded logits cross PCIe).
 
 The reference arm (`--impl reference`) runs the UNMODIFIED reference executor
 (oracle/_ref/ref_harness: heg::execute + CkksBackend compiled from
@@ -52,7 +53,7 @@ def dist_env():
 class ClockSampler:
     """nvidia-smi clocks/throttle sampling during the timed region (B200_PROFILING.md)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -61,6 +62,15 @@ class ClockSampler:
         self.rows = []
         self._p = None
         self._f = None
+        self._t0 = None
+        self._t1 = None
+
+    def mark_begin(self):
+        self._t0 = time.time()
+
+    def mark_end(self):
+        time.sleep(0.25)  # make sure at least one sample lands inside short regions
+        self._t1 = time.time()
 
     def __enter__(self):
         # one long-running sampler process (-lms 200); no per-sample fork inside the timed region
@@ -76,16 +86,27 @@ class ClockSampler:
     def __exit__(self, *exc):
         if self._p is None:
             return
-        time.sleep(0.25)  # make sure at least one sample lands inside short regions
         self._p.terminate()
         try:
             self._p.wait(timeout=5)
         except Exception:
             self._p.kill()
         self._f.seek(0)
+        import datetime
+
+        allrows, inside = [], []
         for line in self._f.read().splitlines():
-            if line.strip():
-                self.rows.append([c.strip() for c in line.split(",")])
+            if not line.strip():
+                continue
+            r = [c.strip() for c in line.split(",")]
+            allrows.append(r)
+            try:  # "2026/10/21 16:34:02.123": keep the samples taken inside the marked region
+                ts = datetime.datetime.strptime(r[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                if self._t0 is not None and self._t1 is not None and self._t0 - 0.05 <= ts <= self._t1 + 0.05:
+                    inside.append(r)
+            except ValueError:
+                pass
+        self.rows = inside if inside else allrows
         self._f.close()
 
     def summary(self) -> dict:
@@ -292,20 +313,28 @@ def ours_arm(args):
     stream = torch.cuda.current_stream(dev)
 
     # ---- value: server-side graph, inputs resident in HBM ----
-    for _ in range(args.warmup):
-        plan.run()
-    launches0 = ctx.kernel_launches()
-    barrier()
-    torch.cuda.synchronize()
+    # the clock sampler (one nvidia-smi -lms process) starts before the warm-up, so its start-up
+    # (NVML initialisation) never falls inside the timed region; only samples taken between the
+    # region's first and last step are reported
     with ClockSampler(dev) as clocks:
+        for _ in range(args.warmup):
+            plan.run()
+        launches0 = ctx.kernel_launches()
+        barrier()
+        torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        clocks.mark_begin()
+        value_marks = [time.perf_counter()]
         e0.record(stream)
         for _ in range(args.steps):
             plan.run()
+            value_marks.append(time.perf_counter())
         e1.record(stream)
         torch.cuda.synchronize()
+        clocks.mark_end()
     barrier()
+    value_step_ms = [round(1e3 * (b - a), 3) for a, b in zip(value_marks[:-1], value_marks[1:])]
     launches = ctx.kernel_launches() - launches0
     ms_total = e0.elapsed_time(e1)
     # the same K steps again with a CUDA event pair around every launch (on the launching
@@ -334,16 +363,23 @@ def ours_arm(args):
     images = spec["batch"] * (1 if shard else ws)  # shard: one batch split over the ranks; replicas: one per rank
     value = images / (ms_step / 1e3)
 
-    # ---- e2e: pinned host pixels -> H2D -> GPU encode+encrypt -> graph -> decrypt -> D2H -> host decode ----
+    # ---- e2e: pinned host pixels -> H2D -> GPU encode+encrypt -> graph -> GPU decrypt+decode -> D2H logits ----
     x_host = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).pin_memory()
-    for _ in range(max(1, args.warmup)):  # warms the pinned output pool and the stream-ordered pool
+    # warm-up in the timed loop's own pattern (two output tickets in flight), so the pinned output
+    # buffers and the stream-ordered pool reach their steady state before the timed region
+    pending = None
+    for _ in range(max(2, args.warmup)):
         plan.bind_input("x", x_host)
         plan.run()
-        logits = plan.output(out_id)
+        ticket = plan.output_async(out_id)
+        if pending is not None:
+            logits = pending.wait()
+        pending = ticket
+    logits = pending.wait()
     barrier()
     torch.cuda.synchronize()
-    # pipelined: the host decode of step i (hg_plan_output_async) overlaps step i+1's GPU work;
-    # every step still does its own H2D, encode, encrypt, graph, decrypt, D2H and decode
+    # pipelined: the D2H of step i's logits (hg_plan_output_async) overlaps step i+1's GPU work;
+    # every step still does its own H2D, encode, encrypt, graph, decrypt, decode and D2H
     t1 = time.perf_counter()
     e2e_marks = []
     pending = None
@@ -368,7 +404,10 @@ def ours_arm(args):
     elems = int(np.prod(x.shape[1:]))
     h2d = x_host.numel() * 8 + elems * 8  # pixels + one encryption seed per input ciphertext
     o_elems, o_level, _ = plan.output_info(out_id)
-    d2h = o_elems * (o_level + 1) * n * 8  # decrypted coefficient-domain outputs (c3: 10 logits, 2 limbs)
+    if os.environ.get("HG_GPU_DECODE", "1") != "0":
+        d2h = o_elems * spec["batch"] * 8  # the decoded logits (decrypt, CRT and slot decode run on the GPU)
+    else:
+        d2h = o_elems * (o_level + 1) * n * 8  # decrypted coefficient-domain outputs (c3: 10 logits, 2 limbs)
 
     # ---- roofline + CPU baseline (rank 0, N=1 only for the CPU leg) ----
     int_peaks = {"modmul32_per_s": ctx.modmul_peak(0), "modmul64_per_s": ctx.modmul_peak(1),
@@ -413,6 +452,7 @@ def ours_arm(args):
             "kernels": stats,
             "kernels_region_ms_per_step": ms_kernel_region,
             "clocks": clocks.summary(),
+            "value_step_ms": value_step_ms,
             "profile_ms": plan.profile()["wall_ms"],
         }
         print(json.dumps(line), flush=True)

@@ -18,7 +18,7 @@
 namespace hg {
 namespace {
 
-constexpr int kEncThreads = 512;
+constexpr int kEncThreads = 1024;
 constexpr int kEncBlockLog = 13;  // FFT blocks of up to 8192 complex doubles (128 KB) in shared memory
 
 __device__ __forceinline__ double2 cmul_rn(double2 x, double wr, double wi) {
