@@ -65,6 +65,22 @@ class ClockSampler:
         self._t0 = None
         self._t1 = None
 
+    def wait_ready(self, timeout_s: float = 8.0):
+        """Block until the sampler has written its first line: nvidia-smi's start-up (NVML
+        initialisation) stalls CUDA calls of other processes for milliseconds and must not fall
+        inside a timed region."""
+        if self._p is None:
+            return
+        t_end = time.time() + timeout_s
+        while time.time() < t_end and self._p.poll() is None:
+            try:
+                if os.fstat(self._f.fileno()).st_size > 0:
+                    time.sleep(0.05)
+                    return
+            except OSError:
+                return
+            time.sleep(0.02)
+
     def mark_begin(self):
         self._t0 = time.time()
 
@@ -313,10 +329,11 @@ def ours_arm(args):
     stream = torch.cuda.current_stream(dev)
 
     # ---- value: server-side graph, inputs resident in HBM ----
-    # the clock sampler (one nvidia-smi -lms process) starts before the warm-up, so its start-up
-    # (NVML initialisation) never falls inside the timed region; only samples taken between the
-    # region's first and last step are reported
+    # the clock sampler (one nvidia-smi -lms process) starts, and writes its first sample, before
+    # the warm-up, so its start-up (NVML initialisation) never falls inside the timed region; only
+    # samples taken between the region's first and last step are reported
     with ClockSampler(dev) as clocks:
+        clocks.wait_ready()
         for _ in range(args.warmup):
             plan.run()
         launches0 = ctx.kernel_launches()

@@ -3097,7 +3097,12 @@ int hg_plan_bind_input(hg_plan* P, const char* param_id, const double* values, i
       }
       HG_CUDA(cudaMemcpyAsync(&P->bind_flags[1], flag.p, sizeof(int), cudaMemcpyDeviceToHost, hg::S(P)));
       HG_CUDA(cudaStreamSynchronize(hg::S(P)));
-      hg::check(P->bind_flags[1] == 0, HG_E_VALIDATION, "encoded coefficient overflows the integer range");
+      if (P->bind_flags[1] != 0) {
+        // the encryption already ran on the rejected coefficients: an earlier binding that shared
+        // these ciphertext buffers is gone too, so the parameter is unbound until the next bind
+        P->bound.erase(param_id);
+        hg::fail(HG_E_VALIDATION, "encoded coefficient overflows the integer range");
+      }
       return sync_sampling || P->bind_flags[0] == 0;
     };
     if (!attempt(false)) {

@@ -130,8 +130,10 @@ __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t 
 // ---------------------------------------------------------------------------
 // TWG: twiddles read from global memory, so a 2^14-point 32-bit row CTA needs 66 KB instead of
 // 194 KB of shared memory and two CTAs (32 warps) fit per SM
-template <typename W, int LOGN, bool INV, bool TWG = false>
-__global__ void __launch_bounds__(Cfg<W, LOGN>::threads, (TWG ? 2 : Cfg<W, LOGN>::min_blocks))
+// T: threads per CTA.  A 2^15-point 32-bit row fills one SM's shared memory with one CTA, so
+// that CTA runs 1024 threads (32 warps, 64 registers) instead of 512.
+template <typename W, int LOGN, bool INV, bool TWG = false, int T = Cfg<W, LOGN>::threads>
+__global__ void __launch_bounds__(T, (TWG ? 2 : T > 512 ? 1 : Cfg<W, LOGN>::min_blocks))
     k_ntt_t(uint64_t* __restrict__ base, int nl, int64_t rows, int G, const LimbList LL, const CtxParams P) {
   extern __shared__ __align__(16) uint64_t smem[];
   Cta<W, LOGN> c(smem, LL, rows, G, P, INV, -1, -1, !TWG);
@@ -140,11 +142,11 @@ __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, (TWG ? 2 : Cfg<W, LOGN>
   for (int r = c.r0; r < c.r1; ++r) {
     uint64_t* g = base + ((int64_t)r * nl + c.limb) * n;
     l2_next(r + 1 < c.r1, g + (int64_t)nl * n, n * 8);
-    lz::load<W, LOGN>(c.s, g);
+    lz::load<W, LOGN, T>(c.s, g);
     __syncthreads();
-    if (INV) lz::inv<W, LOGN>(c.s, c.tw, Lz<W>::ninv(*c.L), q, q2);
-    else lz::fwd<W, LOGN>(c.s, c.tw, q, q2);
-    lz::store<W, LOGN>(g, c.s);
+    if (INV) lz::inv<W, LOGN, T>(c.s, c.tw, Lz<W>::ninv(*c.L), q, q2);
+    else lz::fwd<W, LOGN, T>(c.s, c.tw, q, q2);
+    lz::store<W, LOGN, T>(g, c.s);
     __syncthreads();
   }
 }
@@ -1054,9 +1056,9 @@ __device__ __forceinline__ void relin_body(const int vb, const uint64_t* a, cons
           uint64_t* o1 = o0 + pw;
           (void)o0;
           (void)o1;
+          const int64_t koff = (int64_t)row * 2 * K.key_poly_words + (int64_t)j * nfull + hoff + k0;
           W x[16];
           lz::fwd_last<W, LOGN, NR>(c.s, vt, c.tw, q, q2, x);
-          const int64_t koff = (int64_t)row * 2 * K.key_poly_words + (int64_t)j * nfull + hoff + k0;
           if constexpr (KS) {
             // Montgomery MAC: U = (x km + m q) / 2^32 with m = -(x km) q^{-1} mod 2^32; x < 4q < 2^32,
             // km < q, so U < 2q and U = x w mod q
@@ -1764,6 +1766,18 @@ void ntt(const Context& c, uint64_t* base, int64_t rows_per_limb, int nl, int li
           set_smem_attr(fn, Cf::data_bytes);
           if (inverse) k_ntt_t<W_, LOGN, true, true><<<grid, Cf::threads, Cf::data_bytes, s>>>(base, nl, rows_per_limb, G, LL, c.kp());
           else k_ntt_t<W_, LOGN, false, true><<<grid, Cf::threads, Cf::data_bytes, s>>>(base, nl, rows_per_limb, G, LL, c.kp());
+          c.kt_end(s);
+          HG_CUDA(cudaGetLastError());
+          return;
+        }
+      }
+      if constexpr (LOGN == 15 && sizeof(W_) == 4) {
+        if (ntt_twg()) {  // one CTA per SM by shared memory: 1024 threads (twiddles are global at 2^15 anyway)
+          static_assert(!Cf::TWS, "2^15-point 32-bit rows read their twiddles from global memory");
+          const void* fn = inverse ? (const void*)k_ntt_t<W_, LOGN, true, false, 1024> : (const void*)k_ntt_t<W_, LOGN, false, false, 1024>;
+          set_smem_attr(fn, Cf::smem);
+          if (inverse) k_ntt_t<W_, LOGN, true, false, 1024><<<grid, 1024, Cf::smem, s>>>(base, nl, rows_per_limb, G, LL, c.kp());
+          else k_ntt_t<W_, LOGN, false, false, 1024><<<grid, 1024, Cf::smem, s>>>(base, nl, rows_per_limb, G, LL, c.kp());
           c.kt_end(s);
           HG_CUDA(cudaGetLastError());
           return;

@@ -62,11 +62,12 @@ __device__ __forceinline__ void fwd_group(W (&x)[1 << K], int g, const TWT<W>* t
   }
 }
 
-template <typename W, int LOGN, int K, int S0, bool NR = false>
+// T: threads per CTA (the default everywhere; the standalone 2^15-point transform runs 1024)
+template <typename W, int LOGN, int K, int S0, bool NR = false, int T = lz_threads<LOGN>()>
 __device__ __forceinline__ void fwd_pass(W* s, const TWT<W>* tw, W q, W q2) {
   constexpr int R = 1 << K, TL = LOGN - S0 - K;
 #pragma unroll
-  for (int vt = threadIdx.x; vt < (1 << (LOGN - K)); vt += lz_threads<LOGN>()) {
+  for (int vt = threadIdx.x; vt < (1 << (LOGN - K)); vt += T) {
     const int g = vt >> TL;
     const int pb = padw<W>((g << (LOGN - S0)) + (vt & ((1 << TL) - 1)));
     W x[R];
@@ -79,23 +80,23 @@ __device__ __forceinline__ void fwd_pass(W* s, const TWT<W>* tw, W q, W q2) {
 }
 
 // all passes but the last radix-16 one; ends with a barrier
-template <typename W, int LOGN>
+template <typename W, int LOGN, int T = lz_threads<LOGN>()>
 __device__ __forceinline__ void fwd_but_last(W* s, const TWT<W>* tw, W q, W q2) {
   constexpr int REM = LOGN & 3;
   if constexpr (REM != 0) {
-    fwd_pass<W, LOGN, REM, 0>(s, tw, q, q2);
+    fwd_pass<W, LOGN, REM, 0, false, T>(s, tw, q, q2);
     __syncthreads();
   }
   if constexpr (REM + 4 < LOGN) {
-    fwd_pass<W, LOGN, 4, REM>(s, tw, q, q2);
+    fwd_pass<W, LOGN, 4, REM, false, T>(s, tw, q, q2);
     __syncthreads();
   }
   if constexpr (REM + 8 < LOGN) {
-    fwd_pass<W, LOGN, 4, REM + 4>(s, tw, q, q2);
+    fwd_pass<W, LOGN, 4, REM + 4, false, T>(s, tw, q, q2);
     __syncthreads();
   }
   if constexpr (REM + 12 < LOGN) {
-    fwd_pass<W, LOGN, 4, REM + 8>(s, tw, q, q2);
+    fwd_pass<W, LOGN, 4, REM + 8, false, T>(s, tw, q, q2);
     __syncthreads();
   }
   static_assert(LOGN <= 16, "transform size");
@@ -151,10 +152,10 @@ __device__ __forceinline__ void fwd_last(const W* s, int vt, const TWT<W>* tw, W
   fwd_group<W, 4, LOGN - 4, NR>(x, vt, tw, q, q2);
 }
 
-template <typename W, int LOGN>
+template <typename W, int LOGN, int T = lz_threads<LOGN>()>
 __device__ __forceinline__ void fwd(W* s, const TWT<W>* tw, W q, W q2) {
-  fwd_but_last<W, LOGN>(s, tw, q, q2);
-  for (int vt = threadIdx.x; vt < (1 << (LOGN - 4)); vt += lz_threads<LOGN>()) {
+  fwd_but_last<W, LOGN, T>(s, tw, q, q2);
+  for (int vt = threadIdx.x; vt < (1 << (LOGN - 4)); vt += T) {
     W x[16];
     fwd_last<W, LOGN>(s, vt, tw, q, q2, x);
     const int pb = padw<W>(vt << 4);
@@ -180,11 +181,11 @@ __device__ __forceinline__ void inv_group(W (&x)[1 << K], int gi, const TWT<W>* 
   }
 }
 
-template <typename W, int LOGN, int K, int S0, bool LAST>
+template <typename W, int LOGN, int K, int S0, bool LAST, int T = lz_threads<LOGN>()>
 __device__ __forceinline__ void inv_pass(W* s, const TWT<W>* tw, TWT<W> ninv, W q, W q2) {
   constexpr int R = 1 << K;
 #pragma unroll
-  for (int vt = threadIdx.x; vt < (1 << (LOGN - K)); vt += lz_threads<LOGN>()) {
+  for (int vt = threadIdx.x; vt < (1 << (LOGN - K)); vt += T) {
     const int gi = vt >> S0;
     const int pb = padw<W>((gi << (S0 + K)) + (vt & ((1 << S0) - 1)));
     W x[R];
@@ -206,44 +207,44 @@ __device__ __forceinline__ void inv_pass(W* s, const TWT<W>* tw, TWT<W> ninv, W 
 }
 
 // full inverse, input canonical, output canonical and scaled by N^{-1}; ends with a barrier
-template <typename W, int LOGN>
+template <typename W, int LOGN, int T = lz_threads<LOGN>()>
 __device__ __forceinline__ void inv(W* s, const TWT<W>* tw, TWT<W> ninv, W q, W q2) {
   constexpr int REM = LOGN & 3;
   if constexpr (REM != 0) {
-    inv_pass<W, LOGN, REM, 0, false>(s, tw, ninv, q, q2);
+    inv_pass<W, LOGN, REM, 0, false, T>(s, tw, ninv, q, q2);
     __syncthreads();
   }
   if constexpr (REM + 4 < LOGN) {
-    inv_pass<W, LOGN, 4, REM, false>(s, tw, ninv, q, q2);
+    inv_pass<W, LOGN, 4, REM, false, T>(s, tw, ninv, q, q2);
     __syncthreads();
   }
   if constexpr (REM + 8 < LOGN) {
-    inv_pass<W, LOGN, 4, REM + 4, false>(s, tw, ninv, q, q2);
+    inv_pass<W, LOGN, 4, REM + 4, false, T>(s, tw, ninv, q, q2);
     __syncthreads();
   }
   if constexpr (REM + 12 < LOGN) {
-    inv_pass<W, LOGN, 4, REM + 8, false>(s, tw, ninv, q, q2);
+    inv_pass<W, LOGN, 4, REM + 8, false, T>(s, tw, ninv, q, q2);
     __syncthreads();
   }
-  inv_pass<W, LOGN, 4, LOGN - 4, true>(s, tw, ninv, q, q2);
+  inv_pass<W, LOGN, 4, LOGN - 4, true, T>(s, tw, ninv, q, q2);
   __syncthreads();
 }
 
 // ---- global <-> padded shared staging ---------------------------------------
-template <typename W, int LOGN>
+template <typename W, int LOGN, int T = lz_threads<LOGN>()>
 __device__ __forceinline__ void load(W* s, const uint64_t* __restrict__ g) {
   const ulonglong2* g2 = reinterpret_cast<const ulonglong2*>(g);
-  for (int i = threadIdx.x; i < (1 << (LOGN - 1)); i += lz_threads<LOGN>()) {
+  for (int i = threadIdx.x; i < (1 << (LOGN - 1)); i += T) {
     const ulonglong2 v = g2[i];
     const int p = padw<W>(2 * i);
     s[p] = (W)v.x;
     s[p + 1] = (W)v.y;
   }
 }
-template <typename W, int LOGN>
+template <typename W, int LOGN, int T = lz_threads<LOGN>()>
 __device__ __forceinline__ void store(uint64_t* __restrict__ g, const W* s) {
   ulonglong2* g2 = reinterpret_cast<ulonglong2*>(g);
-  for (int i = threadIdx.x; i < (1 << (LOGN - 1)); i += lz_threads<LOGN>()) {
+  for (int i = threadIdx.x; i < (1 << (LOGN - 1)); i += T) {
     const int p = padw<W>(2 * i);
     g2[i] = make_ulonglong2((uint64_t)s[p], (uint64_t)s[p + 1]);
   }

@@ -39,3 +39,8 @@ cap ${R}_ncu_scatter k_scatter_items 0 k_scatter_items $B
 cap ${R}_ncu_encode k_encode_fft 0 k_encode_fft_block python bench.py --steps 1 --warmup 1 --no-cpu
 cap ${R}_ncu_ntt k_ntt_t 12 k_ntt_t python tools/prim_sweep.py --ns 16384 --ls 7
 cap ${R}_ncu_gemm_tc_c5 k_gemm_tc 0 k_gemm_tc_c5 python tools/diag_step.py c5 1
+# BASELINE config 2: the primitive sweep, and where an end-to-end step goes (bind / run / output)
+if [ -z "$SKIP_SWEEP" ]; then
+  timeout 1500 python tools/prim_sweep.py --out gpurun_out/${R}_sweep_c2.jsonl > gpurun_out/${R}_sweep_c2.log 2>&1
+  ITERS=4 timeout 600 python tools/e2e_breakdown.py c3 > gpurun_out/${R}_e2e_breakdown.log 2>&1
+fi
