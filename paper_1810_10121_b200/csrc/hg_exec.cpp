@@ -3365,6 +3365,7 @@ struct hg_output {
   int err_code = 0;
   ~hg_output() {
     if (th.joinable()) th.join();
+    if (done && values_pinned) cudaEventSynchronize(done);  // the D2H copy still targets `pinned`
     if (done) cudaEventDestroy(done);
     if (pinned) pool->put(pinned, pinned_bytes);
   }

@@ -508,7 +508,26 @@ __device__ __forceinline__ W lift_any(int64_t v, const LimbInfo& L, uint32_t mu3
   else return (W)lift_signed(v, L);
 }
 
-HG_KERNEL k_encrypt_t(const int64_t* __restrict__ samples, const int64_t* __restrict__ mcoef,
+// the ternary mask u and the error e1 are tiny by construction (|u| <= 1, |e| <= 28 from the
+// clipped Box-Muller draw): their lift is one conditional add.  Only the e0 row can carry a
+// folded plaintext and takes the general lift.
+template <typename W>
+__device__ __forceinline__ W lift_tiny(int64_t v, W q) {
+  if constexpr (std::is_floating_point_v<W>) return (double)v;
+  else if constexpr (sizeof(W) == 4) return (W)((int32_t)v + (v < 0 ? (int32_t)q : 0));
+  else return (W)(v < 0 ? (uint64_t)q + (uint64_t)v : (uint64_t)v);
+}
+// canonical value of a forward-transform output (NR: any 32-bit word, see ct_lz)
+template <typename W, bool NR>
+__device__ __forceinline__ W canon_fwd(W y, W q, W q2, uint32_t mu32) {
+  if constexpr (NR && std::is_integral_v<W> && sizeof(W) == 4) return (W)reduce_any32((uint32_t)y, (uint32_t)q, mu32);
+  else return canon4<W>(y, q, q2);
+}
+
+// NR: no-reduce butterflies (q < 2^27 on the 32-bit lane, q < 2^44 on the fp64 lane; inputs < q)
+template <typename W, int LOGN, bool NR = false>
+__global__ void __launch_bounds__(Cfg<W, LOGN>::threads, Cfg<W, LOGN>::min_blocks)
+k_encrypt_t(const int64_t* __restrict__ samples, const int64_t* __restrict__ mcoef,
                       const uint64_t* __restrict__ pt, const uint64_t* __restrict__ pk, int64_t key_poly_words,
                       uint64_t* __restrict__ out, int nl, int64_t items, int G, const LimbList LL,
                       const CtxParams P, const int32_t* __restrict__ omap) {
@@ -528,37 +547,41 @@ HG_KERNEL k_encrypt_t(const int64_t* __restrict__ samples, const int64_t* __rest
     if (pt) l2_next(r + 1 < c.r1, pt + (int64_t)(r + 1) * pw + (int64_t)j * n, n * 8);
     // ---- NTT(u) -> registers (canonical) ----
     W u[GPT][16];
-    lz::fwd_first_from<W, LOGN>(c.s, [&](int k) { return lift_any<W>(__ldg(su + k), *c.L, mu32); }, c.tw, q, q2);
-    lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2);
+    lz::fwd_first_from<W, LOGN, NR>(c.s, [&](int k) { return lift_tiny<W>(__ldg(su + k), q); }, c.tw, q, q2);
+    lz::fwd_middle<W, LOGN, NR>(c.s, c.tw, q, q2);
 #pragma unroll
     for (int gi = 0; gi < GPT; ++gi) {
       W y[16];
-      lz::fwd_last<W, LOGN>(c.s, threadIdx.x + gi * T, c.tw, q, q2, y);
+      lz::fwd_last<W, LOGN, NR>(c.s, threadIdx.x + gi * T, c.tw, q, q2, y);
 #pragma unroll
-      for (int h = 0; h < 16; ++h) u[gi][h] = canon4<W>(y[h], q, q2);
+      for (int h = 0; h < 16; ++h) u[gi][h] = canon_fwd<W, NR>(y[h], q, q2, mu32);
     }
 #pragma unroll 1
     for (int p = 0; p < 2; ++p) {
       __syncthreads();  // the previous transform's last pass has read shared memory
       const int64_t* se = su + (int64_t)(1 + p) * n;
       const int64_t* mc = (p == 0 && mcoef) ? mcoef + (int64_t)r * n : nullptr;
-      lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
-        W v = lift_any<W>(__ldg(se + k), *c.L, mu32);
-        if (mc) {
-          const W m = lift_any<W>(__ldg(mc + k), *c.L, mu32);
-          if constexpr (std::is_floating_point_v<W>) v = reduce_f64(__dadd_rn(v, m), q, q2);
-          else v = csub<W>((W)(v + m), q);
-        }
-        return v;
-      }, c.tw, q, q2);
-      lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2);
+      if (p == 0) {  // e0 (+ a folded or separate plaintext): the general lift
+        lz::fwd_first_from<W, LOGN, NR>(c.s, [&](int k) {
+          W v = lift_any<W>(__ldg(se + k), *c.L, mu32);
+          if (mc) {
+            const W m = lift_any<W>(__ldg(mc + k), *c.L, mu32);
+            if constexpr (std::is_floating_point_v<W>) v = reduce_f64(__dadd_rn(v, m), q, q2);
+            else v = csub<W>((W)(v + m), q);
+          }
+          return v;
+        }, c.tw, q, q2);
+      } else {
+        lz::fwd_first_from<W, LOGN, NR>(c.s, [&](int k) { return lift_tiny<W>(__ldg(se + k), q); }, c.tw, q, q2);
+      }
+      lz::fwd_middle<W, LOGN, NR>(c.s, c.tw, q, q2);
       const uint64_t* kp = pk + (int64_t)p * key_poly_words + (int64_t)j * n;
       const uint64_t* pp = (p == 0 && pt) ? pt + (int64_t)r * pw + (int64_t)j * n : nullptr;
 #pragma unroll
       for (int gi = 0; gi < GPT; ++gi) {
         const int vt = threadIdx.x + gi * T, k0 = vt << 4;
         W y[16];
-        lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, y);
+        lz::fwd_last<W, LOGN, NR>(c.s, vt, c.tw, q, q2, y);
         const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(kp + k0);
         const ulonglong2* p2 = pp ? reinterpret_cast<const ulonglong2*>(pp + k0) : nullptr;
         const int pb = lz::padw<W>(k0);
@@ -570,7 +593,7 @@ HG_KERNEL k_encrypt_t(const int64_t* __restrict__ samples, const int64_t* __rest
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const uint64_t a = pm(e ? kv.y : kv.x, (uint64_t)u[gi][2 * h + e]);
-            uint64_t v = add_mod(a, (uint64_t)canon4<W>(y[2 * h + e], q, q2), Q);
+            uint64_t v = add_mod(a, (uint64_t)canon_fwd<W, NR>(y[2 * h + e], q, q2, mu32), Q);
             if (p2) v = add_mod(v, e ? pv.y : pv.x, Q);
             c.s[pb + 2 * h + e] = (W)v;  // the last pass read its own 16 slots only
           }
@@ -599,7 +622,7 @@ struct EncPCfg {
   static constexpr bool fits = Cfg<W, LOGN>::TWS && smem <= kSmemCap;
   static constexpr int min_blocks = 2 * smem <= kSmemCap ? 2 : 1;
 };
-template <typename W, int LOGN>
+template <typename W, int LOGN, bool NR = false>
 __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, (EncPCfg<W, LOGN>::min_blocks))
     k_encrypt_p(const int64_t* __restrict__ samples, const uint64_t* __restrict__ pt, const uint64_t* __restrict__ pk,
                 int64_t key_poly_words, uint64_t* __restrict__ out, int nl, int64_t items, int G, const LimbList LL,
@@ -632,17 +655,23 @@ __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, (EncPCfg<W, LOGN>::min_
     for (int t = 0; t < 3; ++t) {
       cp_async_wait_all();
       __syncthreads();  // sbuf holds row (r, t); the previous transform's last pass is done
-      lz::fwd_first_from<W, LOGN>(c.s, [&](int k) {
-        return ct_one<W>(lift_any<W>(sbuf[k], *c.L, mu32), lift_any<W>(sbuf[k + n], *c.L, mu32), psi1, q, q2);
-      }, c.tw, q, q2);
+      if (t == 1) {  // e0 (+ a folded plaintext): the general lift
+        lz::fwd_first_from<W, LOGN, NR>(c.s, [&](int k) {
+          return ct_one<W, NR>(lift_any<W>(sbuf[k], *c.L, mu32), lift_any<W>(sbuf[k + n], *c.L, mu32), psi1, q, q2);
+        }, c.tw, q, q2);
+      } else {  // u, e1: tiny by construction
+        lz::fwd_first_from<W, LOGN, NR>(c.s, [&](int k) {
+          return ct_one<W, NR>(lift_tiny<W>(sbuf[k], q), lift_tiny<W>(sbuf[k + n], q), psi1, q, q2);
+        }, c.tw, q, q2);
+      }
       if (t < 2) stage(r, t + 1);  // sbuf consumed (fwd_first_from ends with a barrier)
       else if (r + 1 < c.r1) stage(r + 1, 0);
-      lz::fwd_middle<W, LOGN>(c.s, c.tw, q, q2);
+      lz::fwd_middle<W, LOGN, NR>(c.s, c.tw, q, q2);
       W y[16];
-      if (live) lz::fwd_last<W, LOGN>(c.s, vt, c.tw, q, q2, y);
+      if (live) lz::fwd_last<W, LOGN, NR>(c.s, vt, c.tw, q, q2, y);
       if (t == 0) {
 #pragma unroll
-        for (int h = 0; h < 16; ++h) u[h] = canon4<W>(y[h], q, q2);
+        for (int h = 0; h < 16; ++h) u[h] = canon_fwd<W, NR>(y[h], q, q2, mu32);
         continue;
       }
       if (!live) continue;
@@ -660,7 +689,7 @@ __global__ void __launch_bounds__(Cfg<W, LOGN>::threads, (EncPCfg<W, LOGN>::min_
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const uint64_t a = pm(e ? kv.y : kv.x, (uint64_t)u[2 * h + e]);
-          v[e] = add_mod(a, (uint64_t)canon4<W>(y[2 * h + e], q, q2), Q);
+          v[e] = add_mod(a, (uint64_t)canon_fwd<W, NR>(y[2 * h + e], q, q2, mu32), Q);
           if (pp) v[e] = add_mod(v[e], e ? pv.y : pv.x, Q);
         }
         o2[h] = make_ulonglong2(v[0], v[1]);
@@ -1822,6 +1851,20 @@ void lift_ntt(const Context& c, const int64_t* src, uint64_t* out, int64_t items
   run(cl.wide, uint64_t{}, lf.wide());
 }
 
+// No-reduce forward transforms on canonical inputs (HG_RELIN_NR=0 turns them off with the key
+// switch's): (4 + 2 log N) q < 2^32 on the 32-bit lane, q < 2^44 on the fp64 lane
+static bool forward_nr_ok(const Context& c, const LimbList& LL, bool fp) {
+  static const bool on = [] {
+    const char* e = std::getenv("HG_RELIN_NR");
+    return !(e && e[0] == '0');
+  }();
+  if (!on) return false;
+  const uint64_t m = (uint64_t)(4 + 2 * c.logn());
+  for (int k = 0; k < LL.count; ++k)
+    if (fp ? c.primes()[LL.limb[k]] >= (1ULL << 44) : c.primes()[LL.limb[k]] * m >= (1ULL << 32)) return false;
+  return true;
+}
+
 // HG_ENCRYPT_PIPE=1: the half-row pipelined encryption kernel (measured neutral against the
 // whole-row kernel on c3's input binding, 0.91 vs 0.90 ms, and slightly slower on small batches,
 // so it is off by default)
@@ -1849,12 +1892,23 @@ void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const i
           if (mcoef == nullptr && encrypt_pipelined()) {
             const int G = pick_group(items, (int64_t)LL.count * 2, 148LL * EC::min_blocks, 16);
             const unsigned grid = (unsigned)(LL.count * ((items + G - 1) / G) * 2);
-            set_smem_attr((const void*)k_encrypt_p<W_, LOGN - 1>, EC::smem);
             c.kt_begin(std::is_floating_point_v<W_> ? "k_encrypt_t/f64" : "k_encrypt_t/u32", s,
                        (double)items * LL.count * (2 + (pt ? 1 : 0)) * nw + (double)items * 3 * nw * LL.count,
                        (double)items * LL.count * (3 * bfly(c) + 2.0 * c.n()));
-            k_encrypt_p<W_, LOGN - 1><<<grid, Cfg<W_, LOGN - 1>::threads, EC::smem, s>>>(
-                samples, pt, keys.pk.as<uint64_t>(), kpw, out, nl, items, G, LL, c.kp(), omap);
+            bool nr = false;
+            if constexpr (LOGN == 13) nr = forward_nr_ok(c, LL, std::is_floating_point_v<W_>);
+            if constexpr (LOGN == 13) {
+              if (nr) {
+                set_smem_attr((const void*)k_encrypt_p<W_, LOGN - 1, true>, EC::smem);
+                k_encrypt_p<W_, LOGN - 1, true><<<grid, Cfg<W_, LOGN - 1>::threads, EC::smem, s>>>(
+                    samples, pt, keys.pk.as<uint64_t>(), kpw, out, nl, items, G, LL, c.kp(), omap);
+              }
+            }
+            if (!nr) {
+              set_smem_attr((const void*)k_encrypt_p<W_, LOGN - 1>, EC::smem);
+              k_encrypt_p<W_, LOGN - 1><<<grid, Cfg<W_, LOGN - 1>::threads, EC::smem, s>>>(
+                  samples, pt, keys.pk.as<uint64_t>(), kpw, out, nl, items, G, LL, c.kp(), omap);
+            }
             c.kt_end(s);
             HG_CUDA(cudaGetLastError());
             return;
@@ -1865,13 +1919,24 @@ void encrypt(const Context& c, const Keys& keys, const int64_t* samples, const i
       unsigned grid;
       int G;
       grid_for<W_, LOGN>(LL, items, grid, G);
-      set_smem_attr((const void*)k_encrypt_t<W_, LOGN>, Cf::smem);
       // bytes: samples (3 N, + m N) read, 2 polys written (+ pt read); modmuls: 3 transforms + 2 N key products
       c.kt_begin(std::is_floating_point_v<W_> ? "k_encrypt_t/f64" : sizeof(W_) == 4 ? "k_encrypt_t/u32" : "k_encrypt_t/u64", s,
                  (double)items * LL.count * (2 + (pt ? 1 : 0)) * nw + (double)items * (3 + (mcoef ? 1 : 0)) * nw,
                  (double)items * LL.count * (3 * bfly(c) + 2.0 * c.n()));
-      k_encrypt_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(samples, mcoef, pt, keys.pk.as<uint64_t>(), kpw, out,
-                                                                nl, items, G, LL, c.kp(), omap);
+      bool nr = false;
+      if constexpr (LOGN == 13 && !std::is_same_v<W_, uint64_t>) nr = forward_nr_ok(c, LL, std::is_floating_point_v<W_>);
+      if constexpr (LOGN == 13 && !std::is_same_v<W_, uint64_t>) {
+        if (nr) {  // c3's 26- and 36-bit primes: no-reduce butterflies
+          set_smem_attr((const void*)k_encrypt_t<W_, LOGN, true>, Cf::smem);
+          k_encrypt_t<W_, LOGN, true><<<grid, Cf::threads, Cf::smem, s>>>(samples, mcoef, pt, keys.pk.as<uint64_t>(), kpw,
+                                                                          out, nl, items, G, LL, c.kp(), omap);
+        }
+      }
+      if (!nr) {
+        set_smem_attr((const void*)k_encrypt_t<W_, LOGN>, Cf::smem);
+        k_encrypt_t<W_, LOGN><<<grid, Cf::threads, Cf::smem, s>>>(samples, mcoef, pt, keys.pk.as<uint64_t>(), kpw, out,
+                                                                  nl, items, G, LL, c.kp(), omap);
+      }
       c.kt_end(s);
       HG_CUDA(cudaGetLastError());
     });

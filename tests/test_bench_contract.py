@@ -46,3 +46,33 @@ def test_workload_config_names_the_workload():
     args = argparse.Namespace(config="c5", batch=8192, gpus=2, mode="replicas")
     cfg = bench.workload_config(args, {"n": 16384, "bits": [50] + [30] * 5 + [50], "scale_bits": 30})
     assert cfg["workload"].startswith("BASELINE configs[4]") and cfg["global_batch"] == 16384
+
+
+def test_clock_sampler_keeps_the_samples_inside_the_marked_region(tmp_path):
+    """The sampler process runs from before the warm-up; only rows stamped inside the timed
+    region are summarised (all rows when none fell inside)."""
+    import datetime
+    import time
+
+    def row(t, mhz, cap="Not Active"):
+        ts = datetime.datetime.fromtimestamp(t).strftime("%Y/%m/%d %H:%M:%S.%f")[:-3]
+        return f"{ts}, {mhz}, 1965, 700.00, 0x0, Not Active, Not Active, Not Active, {cap}\n"
+
+    now = time.time()
+    cs = bench.ClockSampler(0)
+    cs._p = type("P", (), {"terminate": lambda s: None, "wait": lambda s, timeout=None: 0, "kill": lambda s: None})()
+    cs._f = open(tmp_path / "smi.csv", "w+")
+    cs._f.write(row(now - 5.0, 300) + row(now - 0.5, 1965, "Active") + row(now - 0.2, 1950) + row(now + 5.0, 345))
+    cs._t0, cs._t1 = now - 1.0, now
+    cs.__exit__(None, None, None)
+    s = cs.summary()
+    assert s["samples"] == 2 and s["sm_mhz"] == 1957.5 and s["sm_max_mhz"] == 1965.0
+    assert s["reasons"] == ["sw_power_cap"]
+    # no row inside the region: fall back to every row
+    cs2 = bench.ClockSampler(0)
+    cs2._p = cs._p
+    cs2._f = open(tmp_path / "smi2.csv", "w+")
+    cs2._f.write(row(now - 50.0, 300))
+    cs2._t0, cs2._t1 = now - 1.0, now
+    cs2.__exit__(None, None, None)
+    assert cs2.summary()["samples"] == 1
