@@ -3064,6 +3064,10 @@ int hg_plan_bind_input(hg_plan* P, const char* param_id, const double* values, i
     // encryption (two CTAs per SM), so chunking costs no wave quantisation
     const int64_t chunk_cols = 296;
     const int chunks = (!on_device && nb > chunk_cols) ? static_cast<int>((nb + chunk_cols - 1) / chunk_cols) : 1;
+    static const bool enc_chunked = [] {
+      const char* e = std::getenv("HG_BIND_ENCRYPT_CHUNKED");
+      return !(e && e[0] == '0');
+    }();
     auto attempt = [&](bool sync_sampling) {
       hg::DevArr flag(sizeof(int), hg::S(P));
       HG_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), hg::S(P)));
@@ -3090,10 +3094,18 @@ int hg_plan_bind_input(hg_plan* P, const char* param_id, const double* values, i
         // column e: slot b at values[b * nb + e] (packing.hpp:57-63)
         hg::k::encode_fft(c, dvals + e0, e1 - e0, P->batch, 1, nb, c.default_scale(), samples + (e0 * 3 + 1) * n,
                           flag.as<int>(), hg::S(P), 3 * n, true);
-        hg::k2::encrypt(c, *P->keys, samples + e0 * 3 * n, nullptr, nullptr,
-                        pad_id.empty() ? ct->p + e0 * ct->item_words() : ct->p, e1 - e0, L + 1, hg::S(P),
-                        pad_id.empty() ? nullptr : bb.omap->as<int32_t>() + e0);
-        P->launches += 2;
+        P->launches += 1;
+        if (enc_chunked) {
+          hg::k2::encrypt(c, *P->keys, samples + e0 * 3 * n, nullptr, nullptr,
+                          pad_id.empty() ? ct->p + e0 * ct->item_words() : ct->p, e1 - e0, L + 1, hg::S(P),
+                          pad_id.empty() ? nullptr : bb.omap->as<int32_t>() + e0);
+          P->launches += 1;
+        }
+      }
+      if (!enc_chunked) {  // HG_BIND_ENCRYPT_CHUNKED=0: one encryption over every column after the encodes
+        hg::k2::encrypt(c, *P->keys, samples, nullptr, nullptr, ct->p, nb, L + 1, hg::S(P),
+                        pad_id.empty() ? nullptr : bb.omap->as<int32_t>());
+        P->launches += 1;
       }
       HG_CUDA(cudaMemcpyAsync(&P->bind_flags[1], flag.p, sizeof(int), cudaMemcpyDeviceToHost, hg::S(P)));
       HG_CUDA(cudaStreamSynchronize(hg::S(P)));
