@@ -37,6 +37,8 @@ cap ${R}_ncu_gemm_f64 k_gemm_f64 0 k_gemm_f64 $B
 cap ${R}_ncu_relin_c2_u32 k_relin_c2_t 0 k_relin_c2_t/u32 $B
 cap ${R}_ncu_scatter k_scatter_items 0 k_scatter_items $B
 cap ${R}_ncu_encode k_encode_fft 0 k_encode_fft_block python bench.py --steps 1 --warmup 1 --no-cpu
+ITERS=1 cap ${R}_ncu_encrypt_u32 k_encrypt_t 0 k_encrypt_t/u32 python tools/e2e_breakdown.py c3
+ITERS=1 cap ${R}_ncu_encrypt_f64 k_encrypt_t 1 k_encrypt_t/f64 python tools/e2e_breakdown.py c3
 cap ${R}_ncu_ntt k_ntt_t 12 k_ntt_t python tools/prim_sweep.py --ns 16384 --ls 7
 cap ${R}_ncu_gemm_tc_c5 k_gemm_tc 0 k_gemm_tc_c5 python tools/diag_step.py c5 1
 # BASELINE config 2: the primitive sweep, and where an end-to-end step goes (bind / run / output)
