@@ -197,6 +197,10 @@ int64_t hg_plan_launches(const hg_plan* plan);
  * to the unsharded run on every rank. */
 /* 128-byte NCCL unique id (rank 0 creates it; the caller broadcasts it, e.g. via torch.distributed) */
 int hg_comm_unique_id(void* id_out);
+/* one-rank self-test of the NCCL transport on the context's GPU: loads libnccl, creates a 1-rank
+ * communicator and runs the transport's all-gather-v (grouped in-place broadcasts) over `ranges`
+ * item ranges of `item_words` words; 0 on success */
+int hg_comm_selftest(hg_context* ctx, int ranges, int64_t item_words);
 /* join a `world`-rank group as `rank` on the plan's device; world == 1 turns sharding off */
 int hg_plan_set_comm(hg_plan* plan, int rank, int world, const void* id);
 /* host-mediated transport instead of NCCL (tests, or a deployment with its own collective): at

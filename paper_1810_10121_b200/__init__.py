@@ -125,6 +125,7 @@ def lib():
         "hg_bench_modmul": (C.c_int, [vp, C.c_int, C.POINTER(C.c_double)]),
         "hg_decode": (C.c_int, [vp, vp, C.c_int, C.c_double, C.c_int64, f64p]),
         "hg_set_gpu_decode": (C.c_int, [C.c_int]),
+        "hg_comm_selftest": (C.c_int, [vp, C.c_int, C.c_int64]),
         "hg_fill_constant": (C.c_int, [vp, u64p, C.c_int, vp]),
         "hg_sample_encryption": (C.c_int, [vp, u64p, C.c_int64, vp]),
         "hg_sample_encryption_host": (C.c_int, [vp, u64p, C.c_int64, vp]),

@@ -2784,20 +2784,23 @@ void nccl_ok(ncclResult_t r, const char* what) {
   if (r != ncclSuccess) fail(HG_ECUDA, std::string(what) + ": " + nccl().errstr(r));
 }
 
+// the all-gather-v itself: every rank broadcasts its own item ranges in place, one NCCL group
+void nccl_allgatherv(ncclComm_t comm, uint64_t* base, int64_t ew, const ShardMap& m, cudaStream_t s) {
+  nccl_ok(nccl().gstart(), "ncclGroupStart");
+  for (int r = 0; r < static_cast<int>(m.ranges.size()); ++r)
+    for (const auto& [b, e] : m.ranges[static_cast<size_t>(r)])
+      nccl_ok(nccl().bcast(base + b * ew, base + b * ew, static_cast<size_t>((e - b) * ew), ncclUint64, r, comm, s),
+              "ncclBroadcast");
+  nccl_ok(nccl().gend(), "ncclGroupEnd");
+}
+
 struct NcclTransport final : Transport {
   ncclComm_t comm = nullptr;
   ~NcclTransport() override {
     if (comm) nccl().destroy(comm);
   }
   void allgatherv(hg_plan* P, const std::string&, CtT& ct, const ShardMap& m) override {
-    const int64_t ew = ct.item_words();
-    nccl_ok(nccl().gstart(), "ncclGroupStart");
-    for (int r = 0; r < static_cast<int>(m.ranges.size()); ++r)
-      for (const auto& [b, e] : m.ranges[static_cast<size_t>(r)])
-        nccl_ok(nccl().bcast(ct.p + b * ew, ct.p + b * ew, static_cast<size_t>((e - b) * ew), ncclUint64, r, comm,
-                             S(P)),
-                "ncclBroadcast");
-    nccl_ok(nccl().gend(), "ncclGroupEnd");
+    nccl_allgatherv(comm, ct.p, ct.item_words(), m, S(P));
   }
 };
 
@@ -3176,6 +3179,39 @@ int hg_comm_unique_id(void* id_out) {
     ncclUniqueId id;
     hg::nccl_ok(hg::nccl().get_id(&id), "ncclGetUniqueId");
     std::memcpy(id_out, &id, sizeof(id));
+  });
+}
+
+// One-rank self-test of the NCCL transport on this context's GPU (a one-GPU box cannot run two
+// ranks): loads libnccl, creates a 1-rank communicator, runs the transport's all-gather-v (grouped
+// in-place broadcasts of `ranges` item ranges of `item_words` words) and checks the buffer.
+int hg_comm_selftest(hg_context* hctx, int ranges, int64_t item_words) {
+  return guard_x([&] {
+    hg::check(hctx && ranges >= 1 && item_words >= 1, HG_E_VALIDATION, "invalid argument");
+    hg::Context& cx = hg::ctx_ref(hctx);
+    hg::DeviceGuard dg_(cx.device());
+    cudaStream_t s = cx.stream();
+    ncclUniqueId uid;
+    hg::nccl_ok(hg::nccl().get_id(&uid), "ncclGetUniqueId");
+    ncclComm_t comm = nullptr;
+    hg::nccl_ok(hg::nccl().init(&comm, 1, uid, 0), "ncclCommInitRank");
+    struct Guard {
+      ncclComm_t c;
+      ~Guard() { hg::nccl().destroy(c); }
+    } g{comm};
+    const int64_t items = 3LL * ranges;  // every third item run belongs to the (only) rank
+    std::vector<uint64_t> h(static_cast<size_t>(items * item_words));
+    for (size_t i = 0; i < h.size(); ++i) h[i] = 0x9E3779B97F4A7C15ULL * (i + 1);
+    hg::DevArr d(h.size() * 8, s);
+    HG_CUDA(cudaMemcpyAsync(d.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice, s));
+    hg::ShardMap m;
+    m.ranges.resize(1);
+    for (int r = 0; r < ranges; ++r) m.ranges[0].push_back({3LL * r, 3LL * r + 2});
+    hg::nccl_allgatherv(comm, d.as<uint64_t>(), item_words, m, s);
+    std::vector<uint64_t> back(h.size());
+    HG_CUDA(cudaMemcpyAsync(back.data(), d.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
+    HG_CUDA(cudaStreamSynchronize(s));
+    hg::check(back == h, HG_E_INTERNAL, "NCCL self-test: the gathered buffer changed");
   });
 }
 
