@@ -224,7 +224,7 @@ template <int XB, int WB, int NT, bool SX = false>
 __global__ void __launch_bounds__(kTcThreadsWS, 1)
     k_gemm_tc(const uint8_t* __restrict__ planes, const int32_t* __restrict__ idx, const uint8_t* __restrict__ wpk,
               const int32_t* __restrict__ oidx, uint64_t* __restrict__ out, int mg, int kt, int nl,
-              const LimbListTc LL, int64_t groups, int64_t w_group_stride, const CtxParams P) {
+              const LimbListTc LL, int64_t groups, int64_t w_group_stride, const CtxParams P, const int wbulk) {
   using Cf = TcCfg<XB, WB, NT, SX>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cf::off_bar);
@@ -335,7 +335,22 @@ __global__ void __launch_bounds__(kTcThreadsWS, 1)
         for (int i = 0; i < MAXC; ++i) cur[i] = nxt[i];
         const uint32_t wdst = sbase + Cf::off_w + slot * Cf::w_bytes;
         const uint8_t* wsrc = wt + (int64_t)s * Cf::w_bytes;
-        for (int c = pt; c < Cf::w_bytes / 16; c += kTcProducers) cp_async16(wdst + c * 16, wsrc + c * 16);
+        if (wbulk) {
+          // the packed W tile is contiguous: one thread adds its bytes to the slot's `full` barrier
+          // (expect_tx) and issues one bulk copy (TMA, no tensor map) that completes on it; the
+          // producers' own arrivals (after their gathered rows land) close the phase
+          if (pt == 0) {
+            asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[slot])),
+                         "r"((uint32_t)Cf::w_bytes)
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(wdst),
+                "l"(wsrc), "r"((uint32_t)Cf::w_bytes), "r"(smem_u32(&full[slot]))
+                : "memory");
+          }
+        } else {
+          for (int c = pt; c < Cf::w_bytes / 16; c += kTcProducers) cp_async16(wdst + c * 16, wsrc + c * 16);
+        }
         cp_async_commit();
         if (k >= Cf::LOOK) {
           cp_async_wait<Cf::LOOK>();
@@ -488,8 +503,12 @@ static void launch_tc(const Context& c, const uint64_t* x, int64_t x_items, cons
   const int64_t tiles = (int64_t)ntiles * (n / kTcM) * 2 * groups * LL.count;
   const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
   c.kt_begin("k_gemm_tc", s, alg_bytes, alg_macs);
+  static const int wbulk = [] {  // HG_TC_WBULK=0: the W tile by the producers' cp.async
+    const char* e = std::getenv("HG_TC_WBULK");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
   k_gemm_tc<XB, XB, NT, SX><<<grid, kTcThreadsWS, Cf::smem, s>>>(planes, idx, wpk, oidx, out, mg, kt, nl, LL, groups,
-                                                             w_group_stride, c.kp());
+                                                             w_group_stride, c.kp(), wbulk);
   c.kt_end(s);
   HG_CUDA(cudaGetLastError());
 }
