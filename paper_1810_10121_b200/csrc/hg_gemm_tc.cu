@@ -83,15 +83,18 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
                : "r"(taddr));
 }
 
-// instruction descriptor: D s32, A/B u8, A MN-major, B K-major, M = 128, N = NT
-template <int NT>
-__host__ __device__ constexpr uint32_t idesc_i8() {
+// instruction descriptor: D s32, A/B u8, A MN-major, B K-major, M = 128, N = nn (a multiple of 16, <= 256)
+__host__ __device__ constexpr uint32_t idesc_i8_n(int nn) {
   return (2u << 4)                      // c_format = S32
          | (0u << 7) | (0u << 10)       // a/b format = UINT8
          | (1u << 15)                   // a_major = MN
          | (0u << 16)                   // b_major = K
-         | ((uint32_t)(NT >> 3) << 17)  // n_dim
+         | ((uint32_t)(nn >> 3) << 17)  // n_dim
          | ((uint32_t)(kTcM >> 4) << 24);
+}
+template <int NT>
+__host__ __device__ constexpr uint32_t idesc_i8() {
+  return idesc_i8_n(NT);
 }
 
 // A tile (X bytes, MN-major): core matrix = 8 k-rows x 16 coefficient bytes (128 B);
@@ -99,10 +102,18 @@ __host__ __device__ constexpr uint32_t idesc_i8() {
 __device__ __forceinline__ int a_off(int m, int k) { return ((k >> 3) * (kTcM / 16) + (m >> 4)) * 128 + (k & 7) * 16 + (m & 15); }
 constexpr int kATileBytes = kTcM * kTcK;  // 4 KB per byte plane
 
-// B tile (W bytes, K-major): core matrix = 8 n-rows x 16 k bytes; n groups at 128 B (SBO),
-// the two 16-byte k chunks at NT/8 * 128 B (LBO).  Packed on the host in this exact order.
+// B tile (W bytes, K-major): core matrix = 8 n-rows x 16 k bytes; n groups at 128 B (SBO).  The
+// PL byte planes of a K step are packed plane after plane inside each of the two 16-byte k
+// chunks, [k chunk][plane][n group][128 B], so consecutive planes form ONE B operand of
+// N = planes x NT rows with the k chunks PL * NT/8 * 128 B apart (LBO): a K step after the first
+// multiplies an x plane by all the w planes in one wide MMA (N <= 256) whose output columns are
+// the consecutive shift groups b .. b + WB - 1.  tcgen05.mma costs the same issue time for every
+// N <= 64 (tools/umma_bench.cu: N = 256 gives 1.8x the MAC rate of N = 64), so 4 wide MMAs per
+// K step replace 16 narrow ones.  Packed on the host in this exact order.
 template <int NT>
 constexpr int kBTileBytes = NT * kTcK;
+template <int NT>
+constexpr int kBPlaneStride = (NT / 8) * 128;  // bytes between consecutive planes inside a k chunk
 
 // SX (split x, residues of 5..7 bytes): x = x_lo + 2^32 x_hi with x_lo the planes 0..3 and x_hi the
 // planes 4..XB-1; the hi planes multiply the weight planes of w' = 2^32 w mod q, so
@@ -125,7 +136,8 @@ struct TcCfg {
   static constexpr int S = SX ? WB + 3 : XB + WB - 1;  // shift groups
   static constexpr int COLS = S * NT <= 32 ? 32 : S * NT <= 64 ? 64 : S * NT <= 128 ? 128 : S * NT <= 256 ? 256 : 512;
   static constexpr int a_bytes = XB * kATileBytes;
-  static constexpr int w_bytes = (SX ? 2 : 1) * WB * kBTileBytes<NT>;  // SX: w then w' planes
+  static constexpr int PL = (SX ? 2 : 1) * WB;             // weight planes per K step (SX: w then w')
+  static constexpr int w_bytes = PL * kBTileBytes<NT>;
   // A/W ring as deep as shared memory allows; loads run LOOK K steps ahead of the MMA
   // (L2 latency ~1-2 us vs ~0.3 us of MMA per step), a slot is refilled 2 steps after its MMA
   static constexpr int RING = (220 * 1024) / (a_bytes + w_bytes) < 12 ? (220 * 1024) / (a_bytes + w_bytes) : 12;
@@ -226,6 +238,7 @@ __global__ void __launch_bounds__(kTcThreadsWS, 1)
               const int32_t* __restrict__ oidx, uint64_t* __restrict__ out, int mg, int kt, int nl,
               const LimbListTc LL, int64_t groups, int64_t w_group_stride, const CtxParams P, const int wbulk) {
   using Cf = TcCfg<XB, WB, NT, SX>;
+  const bool wide = (wbulk & 4) != 0;  // HG_TC_WIDE (default on): wide MMAs after a tile's first K step
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cf::off_bar);
   uint64_t* empty = full + Cf::RING;
@@ -274,15 +287,34 @@ __global__ void __launch_bounds__(kTcThreadsWS, 1)
           asm volatile("tcgen05.fence::after_thread_sync;");
           const uint32_t sa = sbase + slot * Cf::a_bytes;
           const uint32_t sb = sbase + Cf::off_w + slot * Cf::w_bytes;
+          constexpr uint32_t lbo = (uint32_t)(Cf::PL * kBPlaneStride<NT>);
+          if (s == 0 || !wide) {
+            // first K step of a tile: one MMA per (w plane, x plane); the first MMA of each shift
+            // group overwrites the accumulator (a wide MMA has one accumulate flag for all its groups)
 #pragma unroll
-          for (int a = 0; a < WB; ++a) {
+            for (int a = 0; a < WB; ++a) {
+#pragma unroll
+              for (int b = 0; b < XB; ++b) {
+                const int sg = tc_group<XB, WB, SX>(a, b);
+                const int wpl = (SX && b >= 4) ? WB + a : a;  // SX: hi x planes meet the w' planes
+                const uint32_t acc = (s > 0 || !tc_first<XB, WB, SX>(a, b)) ? 1u : 0u;
+                umma_i8(tmem + (uint32_t)(sg * NT), umma_desc(sa + b * kATileBytes, 1024, 128),
+                        umma_desc(sb + wpl * kBPlaneStride<NT>, lbo, 128), idesc, acc);
+              }
+            }
+          } else {
+            // later K steps: x plane b against its WB weight planes at once, in chunks of <= 256 rows
+            constexpr int cmax = 256 / NT, nch = (WB + cmax - 1) / cmax, cnt = (WB + nch - 1) / nch;
 #pragma unroll
             for (int b = 0; b < XB; ++b) {
-              const int sg = tc_group<XB, WB, SX>(a, b);
-              const int wpl = (SX && b >= 4) ? WB + a : a;  // SX: hi x planes meet the w' planes
-              const uint32_t acc = (s > 0 || !tc_first<XB, WB, SX>(a, b)) ? 1u : 0u;
-              umma_i8(tmem + (uint32_t)(sg * NT), umma_desc(sa + b * kATileBytes, 1024, 128),
-                      umma_desc(sb + wpl * kBTileBytes<NT>, (NT / 8) * 128, 128), idesc, acc);
+              const int g0 = (SX && b >= 4) ? b - 4 : b;   // first shift group of this x plane
+              const int p0 = (SX && b >= 4) ? WB : 0;      // SX: hi x planes meet the w' planes
+#pragma unroll
+              for (int a0 = 0; a0 < WB; a0 += cnt) {
+                const int na = (WB - a0) < cnt ? (WB - a0) : cnt;
+                umma_i8(tmem + (uint32_t)((g0 + a0) * NT), umma_desc(sa + b * kATileBytes, 1024, 128),
+                        umma_desc(sb + (p0 + a0) * kBPlaneStride<NT>, lbo, 128), idesc_i8_n(na * NT), 1u);
+              }
             }
           }
           umma_commit(&empty[slot]);
@@ -335,7 +367,7 @@ __global__ void __launch_bounds__(kTcThreadsWS, 1)
         for (int i = 0; i < MAXC; ++i) cur[i] = nxt[i];
         const uint32_t wdst = sbase + Cf::off_w + slot * Cf::w_bytes;
         const uint8_t* wsrc = wt + (int64_t)s * Cf::w_bytes;
-        if (wbulk) {
+        if (wbulk & 1) {
           // the packed W tile is contiguous: one thread adds its bytes to the slot's `full` barrier
           // (expect_tx) and issues one bulk copy (TMA, no tensor map) that completes on it; the
           // producers' own arrivals (after their gathered rows land) close the phase
@@ -438,8 +470,9 @@ int limb_bytes(uint64_t q) { return (64 - __builtin_clzll(q) + 7) / 8; }
 namespace k2 {
 
 // Host packing of the byte-split weights, per limb (in `limbs` order), for the
-// tensor-core GEMM: [group][limb_pos][n-tile][k-step][byte plane][NT x 32 bytes],
-// each NT x 32 block in the K-major core-matrix order the B descriptor expects.
+// tensor-core GEMM: [group][limb_pos][n-tile][k-step][k chunk (2)][byte plane][n group][128 B]:
+// the K-major core-matrix order the B descriptors expect, the planes consecutive inside each
+// 16-byte k chunk so that several planes form one wide B operand (kBPlaneStride).
 void pack_weights_tc(const std::vector<uint64_t>& wres, int64_t wgroups, int mg, int kt, int nl,
                      const std::vector<int>& limbs, int WB, int NT, std::vector<uint8_t>& out, int64_t& group_stride,
                      bool sx, const std::vector<uint64_t>& primes) {
@@ -456,11 +489,11 @@ void pack_weights_tc(const std::vector<uint64_t>& wres, int64_t wgroups, int mg,
         for (int t = 0; t < kt; ++t) {
           const uint64_t v = wres[static_cast<size_t>(((g * mg + m) * kt + t) * nl + j)];
           const int ks = t / kTcK, kk = t % kTcK;
-          // core-matrix offset inside the NT x 32 block: n groups of 8 at 128 B, k chunks of 16 at NT/8*128 B
-          const int64_t off = ((int64_t)(kk >> 4) * (NT / 8) + (nn >> 3)) * 128 + (nn & 7) * 16 + (kk & 15);
           const uint64_t v2 = sx ? static_cast<uint64_t>((static_cast<unsigned __int128>(v) << 32) % primes[j]) : 0;
+          const int64_t base = g * group_stride + (((int64_t)lp * ntiles + ntile) * ksteps + ks) * PL * block;
           for (int a = 0; a < PL; ++a) {
-            const int64_t base = g * group_stride + ((((int64_t)lp * ntiles + ntile) * ksteps + ks) * PL + a) * block;
+            // k chunk of 16 terms, then plane a, then the group of 8 outputs, then (output, term) inside the core matrix
+            const int64_t off = (((int64_t)(kk >> 4) * PL + a) * (NT / 8) + (nn >> 3)) * 128 + (nn & 7) * 16 + (kk & 15);
             out[static_cast<size_t>(base + off)] = static_cast<uint8_t>((a < WB ? v : v2) >> (8 * (a % WB)));
           }
         }
@@ -505,7 +538,8 @@ static void launch_tc(const Context& c, const uint64_t* x, int64_t x_items, cons
   c.kt_begin("k_gemm_tc", s, alg_bytes, alg_macs);
   static const int wbulk = [] {  // HG_TC_WBULK=0: the W tile by the producers' cp.async
     const char* e = std::getenv("HG_TC_WBULK");
-    return (e && e[0] == '0') ? 0 : 1;
+    const char* w = std::getenv("HG_TC_WIDE");  // HG_TC_WIDE=0: one MMA per (w plane, x plane) in every K step
+    return ((e && e[0] == '0') ? 0 : 1) | ((w && w[0] == '0') ? 0 : 4);
   }();
   k_gemm_tc<XB, XB, NT, SX><<<grid, kTcThreadsWS, Cf::smem, s>>>(planes, idx, wpk, oidx, out, mg, kt, nl, LL, groups,
                                                              w_group_stride, c.kp(), wbulk);
