@@ -18,7 +18,7 @@
 namespace hg {
 namespace {
 
-constexpr int kEncThreads = 1024;
+constexpr int kEncThreads = 512;
 constexpr int kEncBlockLog = 13;  // FFT blocks of up to 8192 complex doubles (128 KB) in shared memory
 
 __device__ __forceinline__ double2 cmul_rn(double2 x, double wr, double wi) {
@@ -50,45 +50,96 @@ __device__ __forceinline__ int64_t finish_coeff(double2 a, int64_t k, const doub
 // One CTA per (column, block of B consecutive bit-reversed positions): load with
 // the full-length bit reversal, run every stage with len <= B in shared memory.
 // When B == N the post-processing (half-root twist, 2/N, scale, llround) is fused.
+// K radix-2 stages lg0 .. lg0 + K - 1 of the transform in registers: a work item owns the 2^K
+// elements base + r 2^(lg0-1), r < 2^K, which those stages only combine with one another.  Every
+// butterfly is the reference's (same pair, same root, the same explicitly rounded operations), so
+// the values are bit-identical to the stage-by-stage loop; only shared-memory round trips and
+// barriers are saved (13 -> 4 for N = 8192).  conj: the decode's conjugate roots.
+template <int K>
+__device__ __forceinline__ void fft_pass(double2* a, const double2* tw, int64_t n, int lg0, int items, bool conj) {
+  constexpr int R = 1 << K;
+  const int lsh = lg0 - 1;
+  for (int w = threadIdx.x; w < items; w += blockDim.x) {
+    const int lo = w & ((1 << lsh) - 1), hi = w >> lsh;
+    const int base = (hi << (lsh + K)) + lo;
+    double2 x[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) x[r] = a[base + (r << lsh)];
+#pragma unroll
+    for (int st = 0; st < K; ++st) {
+      const int64_t step = n >> (lg0 + st);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (r & (1 << st)) continue;
+        const int j = ((r & ((1 << st) - 1)) << lsh) + lo;
+        const double2 wv = tw[j * step];
+        const double2 v = cmul_rn(x[r + (1 << st)], wv.x, conj ? -wv.y : wv.y);
+        const double2 xv = x[r];
+        x[r] = make_double2(__dadd_rn(xv.x, v.x), __dadd_rn(xv.y, v.y));
+        x[r + (1 << st)] = make_double2(__dsub_rn(xv.x, v.x), __dsub_rn(xv.y, v.y));
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) a[base + (r << lsh)] = x[r];
+  }
+  __syncthreads();
+}
+// all logb stages of a block held in shared memory: a first pass of ((logb - 1) mod 4) + 1 stages, then passes of 4
+__device__ __forceinline__ void fft_stages(double2* a, const double2* tw, int64_t n, int logb, bool conj) {
+  const int k0 = ((logb - 1) & 3) + 1;
+  const int bsz = 1 << logb;
+  switch (k0) {
+    case 1: fft_pass<1>(a, tw, n, 1, bsz >> 1, conj); break;
+    case 2: fft_pass<2>(a, tw, n, 1, bsz >> 2, conj); break;
+    case 3: fft_pass<3>(a, tw, n, 1, bsz >> 3, conj); break;
+    default: fft_pass<4>(a, tw, n, 1, bsz >> 4, conj); break;
+  }
+  for (int lg0 = k0 + 1; lg0 <= logb; lg0 += 4) fft_pass<4>(a, tw, n, lg0, bsz >> 4, conj);
+}
+
+// tws: the roots e^{-2 pi i j / N}, j < N/2 (every twiddle a stage uses), are staged in shared
+// memory behind the block (the stages were bound by the latency of their strided global loads); a
+// CTA then loops over columns blockIdx.x, blockIdx.x + gridDim.x, ... with the table staged once.
 __global__ void __launch_bounds__(kEncThreads) k_encode_fft_block(
     const double* __restrict__ values, int64_t count, int64_t col_stride, int64_t elem_stride,
     const double* __restrict__ roots, const double* __restrict__ half, int logn, int logb, double norm, double scale,
-    int64_t* __restrict__ out, double2* __restrict__ scratch, int* flag, int64_t ostride, bool accumulate) {
+    int64_t* __restrict__ out, double2* __restrict__ scratch, int* flag, int64_t ostride, bool accumulate,
+    int64_t cols, bool tws) {
   extern __shared__ double2 a[];
   const int64_t n = int64_t(1) << logn;
   const int bsz = 1 << logb;
-  const int64_t e = blockIdx.x;
   const int64_t base = (int64_t)blockIdx.y * bsz;
-  const double* col = values + e * col_stride;
-  for (int j = threadIdx.x; j < bsz; j += blockDim.x) {
-    const int64_t i = (int64_t)(__brev((unsigned)(base + j)) >> (32 - logn));
-    a[j] = make_double2(i < count ? col[i * elem_stride] : 0.0, 0.0);
+  const double2* tw = reinterpret_cast<const double2*>(roots);
+  if (tws) {
+    double2* ts = a + bsz;
+    for (int j = threadIdx.x; j < (int)(n / 2); j += blockDim.x) ts[j] = __ldg(reinterpret_cast<const double2*>(roots) + j);
+    tw = ts;  // (the first barrier below orders the staging)
   }
-  __syncthreads();
-  for (int lg = 1; lg <= logb; ++lg) {
-    const int h = 1 << (lg - 1);
-    const int64_t step = n >> lg;
-    for (int t = threadIdx.x; t < bsz / 2; t += blockDim.x) {
-      const int j = t & (h - 1);
-      const int u = ((t >> (lg - 1)) << lg) + j;
-      const double2 w = __ldg(reinterpret_cast<const double2*>(roots) + j * step);
-      const double2 v = cmul_rn(a[u + h], w.x, w.y);
-      const double2 x = a[u];
-      a[u] = make_double2(__dadd_rn(x.x, v.x), __dadd_rn(x.y, v.y));
-      a[u + h] = make_double2(__dsub_rn(x.x, v.x), __dsub_rn(x.y, v.y));
+  for (int64_t e = blockIdx.x; e < cols; e += gridDim.x) {
+    const double* col = values + e * col_stride;
+    // the bit-reversed gather: scattered 8-byte loads, 8 in flight per thread
+#pragma unroll 8
+    for (int j = threadIdx.x; j < bsz; j += blockDim.x) {
+      const int64_t i = (int64_t)(__brev((unsigned)(base + j)) >> (32 - logn));
+      a[j] = make_double2(i < count ? __ldg(col + i * elem_stride) : 0.0, 0.0);
     }
     __syncthreads();
-  }
-  if (logb == logn) {
-    // accumulate: the coefficients are added to what `out` holds (input binding folds the plaintext
-    // into the e0 sample row of the fresh encryption, exact in int64)
-    for (int k = threadIdx.x; k < bsz; k += blockDim.x) {
-      const int64_t v = finish_coeff(a[k], k, half, norm, scale, flag);
-      int64_t* o = out + e * ostride + k;
-      *o = accumulate ? *o + v : v;
+    fft_stages(a, tw, n, logb, false);
+    if (logb == logn) {
+      // accumulate: the coefficients are added to what `out` holds (input binding folds the plaintext
+      // into the e0 sample row of the fresh encryption, exact in int64)
+      // (the previous values and the half roots of 4 coefficients load together)
+#pragma unroll 4
+      for (int k = threadIdx.x; k < bsz; k += blockDim.x) {
+        int64_t* o = out + e * ostride + k;
+        const int64_t prev = accumulate ? *o : 0;
+        const int64_t v = finish_coeff(a[k], k, half, norm, scale, flag);
+        *o = prev + v;
+      }
+    } else {
+      for (int j = threadIdx.x; j < bsz; j += blockDim.x) scratch[e * n + base + j] = a[j];
     }
-  } else {
-    for (int j = threadIdx.x; j < bsz; j += blockDim.x) scratch[e * n + base + j] = a[j];
+    __syncthreads();  // the block is reused by the next column
   }
 }
 
@@ -292,22 +343,24 @@ void encode_fft(const Context& c, const double* values, int64_t cols, int64_t co
   const int logn = c.logn();
   const int logb = std::min(logn, kEncBlockLog);
   const int64_t n = c.n();
-  const size_t smem = sizeof(double2) << logb;
+  // whole transforms in shared memory (N <= 8192) also stage the N/2 roots there: 128 + 64 KB
+  const bool tws = logb == logn;
+  const size_t smem = (sizeof(double2) << logb) + (tws ? (sizeof(double2) << (logn - 1)) : 0);
   const double norm = 2.0 / static_cast<double>(n);  // encoder.hpp:72, on the host like the reference
   static bool attr = false;
   if (!attr) {
     HG_CUDA(cudaFuncSetAttribute((const void*)k_encode_fft_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(sizeof(double2) << kEncBlockLog)));
+                                 (int)((sizeof(double2) << kEncBlockLog) + (sizeof(double2) << (kEncBlockLog - 1)))));
     attr = true;
   }
   double2* scratch = nullptr;
   if (logb < logn) scratch = static_cast<double2*>(const_cast<Context&>(c).scratch(static_cast<size_t>(cols * n) * sizeof(double2), 9));
   c.kt_begin("k_encode_fft", s, (double)cols * count * 8 + (double)cols * n * 8,
              (double)cols * (n / 2) * logn * 4);
-  dim3 grid((unsigned)cols, (unsigned)(n >> logb));
+  dim3 grid((unsigned)(tws ? std::min<int64_t>(cols, 148) : cols), (unsigned)(n >> logb));
   k_encode_fft_block<<<grid, kEncThreads, smem, s>>>(values, count, col_stride, elem_stride, c.enc_roots_dev(),
                                                     c.enc_half_dev(), logn, logb, norm, scale, out, scratch, flag,
-                                                    out_stride, accumulate);
+                                                    out_stride, accumulate, cols, tws);
   HG_CUDA(cudaGetLastError());
   if (logb < logn) {
     const int blocks = 148 * 8;
