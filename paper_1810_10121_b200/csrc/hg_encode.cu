@@ -262,20 +262,7 @@ __global__ void __launch_bounds__(kEncThreads) k_decode_fft_block(
     a[j] = b[e * n + i];
   }
   __syncthreads();
-  for (int lg = 1; lg <= logb; ++lg) {
-    const int h = 1 << (lg - 1);
-    const int64_t step = n >> lg;
-    for (int t = threadIdx.x; t < bsz / 2; t += blockDim.x) {
-      const int j = t & (h - 1);
-      const int u = ((t >> (lg - 1)) << lg) + j;
-      const double2 w = __ldg(reinterpret_cast<const double2*>(roots) + j * step);
-      const double2 v = cmul_rn(a[u + h], w.x, -w.y);
-      const double2 x = a[u];
-      a[u] = make_double2(__dadd_rn(x.x, v.x), __dadd_rn(x.y, v.y));
-      a[u + h] = make_double2(__dsub_rn(x.x, v.x), __dsub_rn(x.y, v.y));
-    }
-    __syncthreads();
-  }
+  fft_stages(a, reinterpret_cast<const double2*>(roots), n, logb, true);  // the conjugate roots
   if (logb == logn) {
     for (int64_t k = threadIdx.x; k < count; k += blockDim.x) out[e * out_es + k * out_ms] = a[k].x;
   } else {
