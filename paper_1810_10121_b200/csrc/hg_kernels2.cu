@@ -164,10 +164,12 @@ __device__ __forceinline__ W lift_cen(CT v, const LimbInfo& L, uint32_t mu32) {
     return (double)v;  // |v| < 2^30 <= q_j: a signed fp64-lane residue
   } else if constexpr (sizeof(CT) == 4 && sizeof(W) == 4) {
     // |v| < 2^30, q_j < 2^30: |v| mod q_j by a Shoup product with 1 (mu32 = floor(2^32 / q_j))
-    const uint32_t q = (uint32_t)L.q, av = (uint32_t)(v < 0 ? -v : v);
+    // branch-free: |v|, one Barrett step, one conditional subtraction, one select
+    const uint32_t q = (uint32_t)L.q, av = (uint32_t)abs(v);
     uint32_t r = av - __umulhi(av, mu32) * q;
-    r = r >= q ? r - q : r;
-    return (v < 0 && r != 0) ? q - r : r;
+    r = min(r, r - q);
+    const uint32_t nr = q - r;
+    return ((v < 0) & (r != 0)) ? nr : r;
   } else if constexpr (sizeof(CT) == 8 && sizeof(W) == 4) {
     // |v| < 2^63, q_j < 2^30 (a wide top limb lifted into a small one): |v| = hi 2^32 + lo with
     // hi (2^32 mod q) and lo reduced by 32-bit Shoup products into [0, 2q) each; the sum is
